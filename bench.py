@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""bench.py -- Faugere-Lachartre reduction (GBLA, arXiv 1602.06097) on B200.
+
+One STEP = one gbla_reduce over the bench workload (BASELINE.json configs[1]
+= c1, 45,000 x 55,000, p = 65521): splice -> sparse phase (Alg 2, fused
+reduce_C + update_D) -> fully reduced echelon of D, device-resident CSR in,
+device-resident R + rank out.
+
+metric  nnz-AXPY Gop/s mod p: exact sparse-phase modMAC count (Alg 2 count,
+        equal to the oracle's) / whole-step time.  ms_per_step is the F4
+        matrix reduction time.
+e2e     the same metric through the C ABI with HOST buffers: pinned-host CSR
+        copied in by the library (GBLA_HOST_INPUT) and R + pivcol copied back
+        to host, inside the timed region.
+--impl reference   the CPU oracle (oracle/, plain C) on the box's host cores,
+        each step a bounded sample of c1's targets (same metric, unit).
+
+Multi-GPU (torchrun, N > 1): see DESIGN.md §"Multi-GPU"; one process per GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def _peaks():
+    try:
+        return json.load(open(MEASURED)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, bounded samples."""
+    world, rank, _ = _dist()
+    if world > 1 and rank != 0:
+        return
+    import gbla_gen
+    import oracle
+    cfg = gbla_gen.CONFIGS[args.config]
+    M = gbla_gen.f4_matrix(cfg)
+    S = oracle.splice(M)
+    threads = oracle.default_threads()
+    rng = np.random.default_rng(123)
+    per_step = args.ref_targets
+    for _ in range(args.warmup):
+        oracle.dnew_rows(M, S, targets=np.sort(rng.choice(S.mN, max(8, per_step // 8), replace=False)),
+                         threads=threads)
+    times, ops = [], 0
+    for _ in range(args.steps):
+        t = np.sort(rng.choice(S.mN, per_step, replace=False))
+        t0 = time.perf_counter()
+        _, _, o = oracle.dnew_rows(M, S, targets=t, threads=threads)
+        times.append(time.perf_counter() - t0)
+        ops += int(o.sum())
+    tot = sum(times)
+    gops = ops / tot / 1e9
+    sample = (f"oracle Alg 2 (sparse phase) on {per_step} random targets of {args.config} per step "
+              f"(of mN={S.mN}); splice not timed; RREF not included")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gops, 4), "unit": "Gop/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64 accumulate, u16 residues", "data": "synthetic",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "p": cfg.p},
+        "cpu_baseline": {"value": round(gops, 4), "unit": "Gop/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(gops, 4), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "nnz-AXPY Gop/s mod p (F4 matrix reduction, gbla_reduce)"
+
+
+def cpu_baseline(cfg_name: str, M, targets: int):
+    import oracle
+    S = oracle.splice(M)
+    threads = oracle.default_threads()
+    rng = np.random.default_rng(7)
+    t = np.sort(rng.choice(S.mN, min(targets, S.mN), replace=False))
+    t0 = time.perf_counter()
+    _, _, o = oracle.dnew_rows(M, S, targets=t, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": round(int(o.sum()) / dt / 1e9, 4), "unit": "Gop/s", "cores": threads, "kind": "oracle",
+            "sample": f"oracle Alg 2 (sparse phase only) on {t.size} random targets of {cfg_name} "
+                      f"(of mN={S.mN}), {dt:.1f} s wall on {threads} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--flags", type=int, default=0, help="gbla_reduce flags")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-targets", type=int, default=384)
+    ap.add_argument("--ref-targets", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import gbla_gen
+    import paper_1602_06097_b200 as gb
+
+    world, rank, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    cfg = gbla_gen.CONFIGS[args.config]
+    M = gbla_gen.f4_matrix(cfg)              # host, seeded (same matrix on every rank: weak scaling replicas)
+    rp = torch.from_numpy(M.row_ptr).cuda()
+    col = torch.from_numpy(M.col).cuda()
+    val = torch.from_numpy(M.val).cuda()
+    ctx = gb.Context(dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step():
+        h = gb.gbla_reduce(ctx, M.m, M.n, rp, col, val, M.p, flags=args.flags, stream=stream)
+        return h
+
+    for _ in range(max(args.warmup, 0)):
+        step().free()
+    torch.cuda.synchronize()
+    launches0 = gb.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phases = []
+    ops = dense_ops = 0
+    rank_d = None
+    clocks = ClockSampler(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.zero_()                                 # L2 flush between timed steps
+        ev[i][0].record(stream)
+        h = step()
+        ev[i][1].record(stream)
+        phases.append(h.phase_ms())
+        ops, dense_ops = h.opcount()
+        rank_d = h.dims(), h.rref()[0]
+        h.free()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = gb.kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if rank == 0:
+        hp = [torch.from_numpy(a).pin_memory() for a in (M.row_ptr, M.col, M.val)]
+        hn = [t.numpy() for t in hp]
+        (npiv, mN, nN), rk = rank_d
+        h2d = M.row_ptr.nbytes + M.col.nbytes + M.val.nbytes
+        d2h = rk * nN * 2 + rk * 4
+        e_ms = []
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h = gb.gbla_reduce(ctx, M.m, M.n, hn[0], hn[1], hn[2], M.p, flags=args.flags, stream=stream)
+            r, pc_h, R_h = h.rref_to_host(stream=stream)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            h.free()
+            if i > 0:
+                e_ms.append(dt)
+        em = statistics.mean(e_ms)
+        e2e = {"value": round(ops / (em / 1e3) / 1e9 * world, 4), "unit": "Gop/s", "ms_per_step": round(em, 3),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "note": "host wall clock around gbla_reduce(GBLA_HOST_INPUT, pinned) + gbla_copy_rref_to_host"}
+
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        ph = {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]}
+        # dominant kernel and its roofline (DESIGN.md §"Roofline")
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        dom = max(("reduce_C", "echelon"), key=lambda k: ph[k])
+        if dom == "reduce_C":
+            # k_reduce_targets: INT-pipe modMACs; peak = 1 IMAD (32-bit) per modMAC per lane at 64 lanes/clk/SM
+            peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
+            ach = ops / (ph["reduce_C"] / 1e3) / 1e12
+            roof = {"kernel": "k_reduce_targets<MODE_FUSED>", "bound": "alu", "achieved": round(ach, 4),
+                    "peak": round(peak, 3), "unit": "Tmodmac/s", "frac": round(ach / peak, 4), "traffic": None,
+                    "peak_source": f"{sm_count} SMs x 64 IMAD/clk x {sm_mhz:.0f} MHz (B200_PROFILING.md clocks; "
+                                   f"{peak_src} sm_max_mhz)"}
+        else:
+            peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
+            ach = dense_ops / (ph["echelon"] / 1e3) / 1e12
+            roof = {"kernel": "echelon (k_trailing_int)", "bound": "alu", "achieved": round(ach, 4),
+                    "peak": round(peak, 3), "unit": "Tmodmac/s", "frac": round(ach / peak, 4), "traffic": None,
+                    "peak_source": f"{sm_count} SMs x 64 IMAD/clk x {sm_mhz:.0f} MHz"}
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(cfg.name, M, args.cpu_targets)
+        line = {
+            "metric": METRIC, "value": round(ops / (ms / 1e3) / 1e9 * world, 4), "unit": "Gop/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u16 residues, u64 delayed-reduction accumulators (exact mod p)", "data": "synthetic",
+            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "npiv": cfg.npiv, "p": cfg.p,
+                       "density": cfg.density, "band": cfg.band, "rank_planted": cfg.rank_planted,
+                       "flags": args.flags, "l2": "flushed (256 MiB write) between timed steps; inputs > L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "sparse_modmac_per_step": ops, "dense_modmac_per_step": dense_ops,
+            "rank_D": rank_d[1], "npiv": rank_d[0][0],
+            "phase_ms": ph, "step_ms": [round(x, 3) for x in step_ms],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "gpu_launches_per_step": round(launches / max(args.steps, 1), 1),
+            "clocks": clk, "peaks_source": peak_src,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

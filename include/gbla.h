@@ -1,0 +1,179 @@
+/*
+ * gbla.h -- C ABI of libgbla: Faugere-Lachartre reduction of F4/F5
+ * Macaulay matrices over GF(p), p < 2^16, on NVIDIA B200 (sm_100a).
+ *
+ * Paper: Boyer, Eder, Faugere, Lachartre, Martani, "GBLA -- Groebner Basis
+ * Linear Algebra Package", arXiv 1602.06097.  Citations "P:n" are lines of
+ * its LaTeX source; DESIGN.md lists the readings R1..R22 of
+ * passages the paper leaves silent or garbled.
+ *
+ * Conventions for every call
+ *   - All matrix pointers are DEVICE pointers unless the GBLA_HOST_INPUT flag
+ *     says otherwise.  Work is enqueued on `stream` (a cudaStream_t passed as
+ *     void*, NULL = legacy default stream); calls that must learn sizes
+ *     (gbla_splice, gbla_echelon_D) synchronize that stream.
+ *   - Inputs are caller-owned and never written; they must stay valid until
+ *     the stream work that reads them completes.  Every buffer the library
+ *     creates is owned by the handle that created it and is released by
+ *     gbla_mat_free / gbla_ctx_destroy.  Device memory comes from the
+ *     context's allocator (gbla_ctx_set_allocator; default cudaMallocAsync).
+ *   - All outputs are canonical residues in [0, p).
+ *   - Errors: host-checkable problems (NULL pointers, sizes, p not a prime in
+ *     (2, 2^16), unknown flags, call order) return a status synchronously
+ *     and change nothing.  Input errors found on the device (unsorted or
+ *     duplicate columns, col >= n, val == 0 or val >= p) are latched and
+ *     returned as GBLA_E_INVAL by gbla_splice (which synchronizes); the
+ *     handle is then not created.  gbla_last_error() gives a thread-local
+ *     message for the last non-OK status.  There is no CPU fallback: without
+ *     a usable sm_100 device every compute call returns GBLA_E_CUDA.
+ *   - A gbla_mat handle is single-stream and single-thread.
+ */
+#ifndef GBLA_H
+#define GBLA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GBLA_OK = 0,
+    GBLA_E_INVAL = 1,    /* malformed input (pointers, sizes, CSR content)       */
+    GBLA_E_DOMAIN = 2,   /* p not prime or not in (2, 2^16)                      */
+    GBLA_E_ORDER = 3,    /* call sequence violates the contract below            */
+    GBLA_E_NOMEM = 4,    /* device allocation failed                             */
+    GBLA_E_CUDA = 5,     /* CUDA runtime error / no sm_100 device                */
+    GBLA_E_NCCL = 6,     /* NCCL error (multi-GPU)                               */
+    GBLA_E_INTERNAL = 7
+} gbla_status;
+
+/* ---- flags ------------------------------------------------------------ */
+#define GBLA_ORDER_NEW       0x00u  /* gbla_reduce: new order, Alg 2 [default] */
+#define GBLA_ORDER_STANDARD  0x01u  /* gbla_reduce: Steps 2-3 with TRSM        */
+#define GBLA_FUSE_D          0x02u  /* gbla_reduce_C: also update D (Alg 2)  */
+#define GBLA_HOST_INPUT      0x04u  /* gbla_splice/gbla_reduce: M's arrays are host memory */
+#define GBLA_KEEP_CPRIME     0x08u  /* fused gbla_reduce_C also stores C' = C A^-1         */
+#define GBLA_SPARSE_INT      0x10u  /* sparse phase: per-target multiline AXPY (INT pipe)  */
+#define GBLA_DENSE_INT       0x20u  /* echelon trailing update on the INT pipe             */
+#define GBLA_DENSE_TC        0x40u  /* echelon trailing update on tcgen05 (u8-limb IMMA)   */
+#define GBLA_FLAGS_ALL       0x7Fu
+
+/* ---- input ------------------------------------------------------------ */
+/* Sparse matrix M (m x n) over GF(p) in CSR: row i holds the entries
+ * (col[q], val[q]) for q in [row_ptr[i], row_ptr[i+1]); columns strictly
+ * increasing within a row, 1 <= val < p.  Rows are polynomials, columns
+ * monomials in decreasing monomial order.  Rows need not be
+ * monic: Step 1 normalizes them (reading R6).  Zero rows are
+ * allowed (reading R7).  m, n < 2^31. */
+typedef struct {
+    int64_t m, n, nnz;
+    const uint64_t *row_ptr;   /* m+1 */
+    const uint32_t *col;       /* nnz */
+    const uint16_t *val;       /* nnz */
+} gbla_csr;
+
+typedef struct gbla_ctx_s *gbla_ctx;   /* device, allocator, optional NCCL comm */
+typedef struct gbla_mat_s *gbla_mat;   /* one spliced matrix and its results    */
+
+typedef void *(*gbla_alloc_fn)(size_t bytes, void *stream, void *user);
+typedef void (*gbla_free_fn)(void *ptr, void *stream, void *user);
+
+/* ---- context ---------------------------------------------------------- */
+/* Bind to CUDA device `device` (must be sm_100).  GBLA_E_CUDA otherwise. */
+gbla_status gbla_ctx_create(int device, gbla_ctx *out);
+/* Route every device allocation through (alloc, free); NULL restores the
+ * default (cudaMallocAsync / cudaFreeAsync on the call's stream). */
+gbla_status gbla_ctx_set_allocator(gbla_ctx ctx, gbla_alloc_fn alloc, gbla_free_fn free_fn, void *user);
+/* Multi-GPU: join an NCCL communicator built from a 128-byte ncclUniqueId
+ * shared by the caller (e.g. through torch.distributed), as `rank` of
+ * `world`.  Collective: every rank must call it.  world == 1 detaches. */
+gbla_status gbla_ctx_set_comm(gbla_ctx ctx, const void *nccl_unique_id, int rank, int world);
+/* Fill out128 with a fresh ncclUniqueId (call on one rank, broadcast it). */
+gbla_status gbla_nccl_get_unique_id(void *out128);
+void gbla_ctx_destroy(gbla_ctx ctx);
+
+/* ---- the six calls (north star) ------------------------ */
+
+/* Step 1: normalize rows; lead(r) = first column;
+ * pivot columns P = { lead(r) } (R2); for each c in P the pivot row is the
+ * candidate of minimum (weight, row id) (R1: "keep A as sparse as
+ * possible"); sigma orders P ascending then the other columns
+ * ascending (R3, R4); pivot rows in sigma(lead) order form A|B, all other
+ * rows in original order form C|D (R5, R7).  Builds the device formats
+ * (sigma-ordered rows, two-row multilines of A|B) and the dense
+ * D quadrant.  Synchronizes `stream`.  flags: GBLA_HOST_INPUT only. */
+gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags,
+                        void *stream, gbla_mat *out);
+
+/* Step 2, TRSM: B <- A^-1 B (A unit upper triangular; "one only
+ * reads A and writes to B").  Result kept as dense B' (n_piv x nN). */
+gbla_status gbla_reduce_B(gbla_mat h, void *stream);
+
+/* C <- C A^-1 (new order): per non-pivot row, forward
+ * substitution over the pivots in ascending order, lambda = current entry,
+ * row -= lambda * A_j (Alg 2, readings R8, R9).  Without
+ * GBLA_FUSE_D the coefficients are stored as C' (mN x n_piv, the 4-step
+ * variant P:689-698).  With GBLA_FUSE_D the B rows are applied in the same
+ * pass (Alg 2) and D holds D - C A^-1 B on return. */
+gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream);
+
+/* Step 3 / 4-step variant step 4:
+ * D <- D - C' B after an unfused gbla_reduce_C, or D <- D - C B' after
+ * gbla_reduce_B.  Requires exactly one of them since gbla_splice
+ * (GBLA_E_ORDER otherwise: both would give D - C A^-1 A^-1 B). */
+gbla_status gbla_update_D(gbla_mat h, void *stream);
+
+/* Step 4, fully reduced (reading R13): R = RREF(D) over GF(p):
+ * rows sorted by pivot column, leading 1, zero in every other pivot column,
+ * zero rows dropped.  *rank = rows(R); rank(M) = n_piv + rank.
+ * Echelons the CURRENT D (callable after any of the above).  flags select
+ * the trailing-update engine (GBLA_DENSE_TC default, GBLA_DENSE_INT).
+ * Synchronizes `stream`. */
+gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *rank);
+
+/* The whole pipeline: splice -> (new order: fused reduce_C | standard:
+ * reduce_B + update_D) -> echelon_D.  Returns the handle holding every
+ * result.  Synchronizes `stream`. */
+gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags,
+                        void *stream, gbla_mat *out);
+
+/* ---- results (views valid until gbla_mat_free) ------------------------- */
+gbla_status gbla_get_dims(gbla_mat h, int64_t *npiv, int64_t *mN, int64_t *nN);
+/* sigma[n]: column c -> sigma index; pivot_row[npiv]; nonpivot_row[mN]
+ * (original row ids).  Device pointers. */
+gbla_status gbla_get_maps(gbla_mat h, const uint32_t **sigma, const uint32_t **pivot_row,
+                          const uint32_t **nonpivot_row);
+/* Current dense D (mN x nN, row stride *ld elements), device. */
+gbla_status gbla_get_D(gbla_mat h, const uint16_t **D, int64_t *ld);
+/* C' (mN x npiv, stride *ld) after unfused reduce_C; NULL otherwise. */
+gbla_status gbla_get_Cprime(gbla_mat h, const uint16_t **X, int64_t *ld);
+/* B' (npiv x nN, stride *ld) after reduce_B; NULL otherwise. */
+gbla_status gbla_get_Bprime(gbla_mat h, const uint16_t **Bp, int64_t *ld);
+/* Densify an original quadrant ('A','B','C','D', normalized, sigma order)
+ * into caller-provided device memory `out` (rows x cols, stride ld). */
+gbla_status gbla_densify_quadrant(gbla_mat h, char which, uint16_t *out, int64_t ld, void *stream);
+/* R (rank x nN, stride *ld) and pivcol[rank] after gbla_echelon_D. */
+gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol,
+                          const uint16_t **R, int64_t *ld);
+/* Copy R (row-major, rank x nN, no padding) and pivcol to HOST memory. */
+gbla_status gbla_copy_rref_to_host(gbla_mat h, uint32_t *pivcol, uint16_t *R, void *stream);
+/* modMAC counts: sparse phase (Alg 2 count: for every nonzero lambda_j,
+ * nnz(row_j) - 1) and the echelon's dense modMACs (algorithmic). */
+gbla_status gbla_get_opcount(gbla_mat h, uint64_t *sparse_modmac, uint64_t *dense_modmac);
+/* Per-phase device times in ms of the last calls on this handle
+ * (splice, reduce_C, reduce_B, update_D, echelon). */
+gbla_status gbla_get_phase_ms(gbla_mat h, float *ms5);
+gbla_status gbla_sync(gbla_mat h);
+void gbla_mat_free(gbla_mat h);
+const char *gbla_last_error(void);
+/* Number of libgbla kernels launched by this process so far (diagnostics). */
+uint64_t gbla_kernel_launches(void);
+/* Library build/version string. */
+const char *gbla_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBLA_H */

@@ -1,0 +1,351 @@
+"""Thin Python binding of libgbla (include/gbla.h) -- argument marshalling only.
+
+Every step of the reduction runs in the CUDA kernels of ``csrc/``.  PyTorch
+is used for device memory (the library allocates through torch's caching
+allocator via ``gbla_ctx_set_allocator``), streams and process groups.
+There is no CPU fallback: importing this package without the built
+``libgbla.so`` raises, and every call raises on a non-OK status.
+
+Names follow the C ABI: gbla_splice, gbla_reduce_B, gbla_reduce_C,
+gbla_update_D, gbla_echelon_D, gbla_reduce.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgbla.so")
+
+# flags (include/gbla.h)
+GBLA_ORDER_NEW = 0x00
+GBLA_ORDER_STANDARD = 0x01
+GBLA_FUSE_D = 0x02
+GBLA_HOST_INPUT = 0x04
+GBLA_KEEP_CPRIME = 0x08
+GBLA_SPARSE_INT = 0x10
+GBLA_DENSE_INT = 0x20
+GBLA_DENSE_TC = 0x40
+
+_STATUS = {0: "GBLA_OK", 1: "GBLA_E_INVAL", 2: "GBLA_E_DOMAIN", 3: "GBLA_E_ORDER", 4: "GBLA_E_NOMEM",
+           5: "GBLA_E_CUDA", 6: "GBLA_E_NCCL", 7: "GBLA_E_INTERNAL"}
+
+
+class GblaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _CSR(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libgbla.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libgbla.so not found at {path}: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp, i64, u32, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int
+    P = ctypes.POINTER
+    sig = {
+        "gbla_ctx_create": ([ctypes.c_int, P(vp)], st),
+        "gbla_ctx_set_allocator": ([vp, _ALLOC_FN, _FREE_FN, vp], st),
+        "gbla_ctx_set_comm": ([vp, vp, ctypes.c_int, ctypes.c_int], st),
+        "gbla_ctx_destroy": ([vp], None),
+        "gbla_splice": ([vp, P(_CSR), u32, u32, vp, P(vp)], st),
+        "gbla_reduce_B": ([vp, vp], st),
+        "gbla_reduce_C": ([vp, u32, vp], st),
+        "gbla_update_D": ([vp, vp], st),
+        "gbla_echelon_D": ([vp, u32, vp, P(i64)], st),
+        "gbla_reduce": ([vp, P(_CSR), u32, u32, vp, P(vp)], st),
+        "gbla_get_dims": ([vp, P(i64), P(i64), P(i64)], st),
+        "gbla_get_maps": ([vp, P(vp), P(vp), P(vp)], st),
+        "gbla_get_D": ([vp, P(vp), P(i64)], st),
+        "gbla_get_Cprime": ([vp, P(vp), P(i64)], st),
+        "gbla_get_Bprime": ([vp, P(vp), P(i64)], st),
+        "gbla_densify_quadrant": ([vp, ctypes.c_char, vp, i64, vp], st),
+        "gbla_get_rref": ([vp, P(i64), P(vp), P(vp), P(i64)], st),
+        "gbla_copy_rref_to_host": ([vp, vp, vp, vp], st),
+        "gbla_get_opcount": ([vp, P(ctypes.c_uint64), P(ctypes.c_uint64)], st),
+        "gbla_get_phase_ms": ([vp, P(ctypes.c_float)], st),
+        "gbla_sync": ([vp], st),
+        "gbla_mat_free": ([vp], None),
+        "gbla_last_error": ([], ctypes.c_char_p),
+        "gbla_version": ([], ctypes.c_char_p),
+        "gbla_nccl_get_unique_id": ([vp], st),
+        "gbla_kernel_launches": ([], ctypes.c_uint64),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names the binding expects the library to export (tests check them)."""
+    return ["gbla_ctx_create", "gbla_ctx_set_allocator", "gbla_ctx_set_comm", "gbla_ctx_destroy",
+            "gbla_splice", "gbla_reduce_B", "gbla_reduce_C", "gbla_update_D", "gbla_echelon_D", "gbla_reduce",
+            "gbla_get_dims", "gbla_get_maps", "gbla_get_D", "gbla_get_Cprime", "gbla_get_Bprime",
+            "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
+            "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
+            "gbla_kernel_launches", "gbla_nccl_get_unique_id"]
+
+
+def _check(status: int):
+    if status != 0:
+        msg = _lib.gbla_last_error()
+        raise GblaError(status, msg.decode() if msg else "")
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class _DevView:
+    """__cuda_array_interface__ wrapper so torch can view library memory."""
+
+    def __init__(self, ptr, shape, typestr, strides=None):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3,
+                                         "strides": strides}
+
+
+def _view(ptr, shape, dtype_str, ld=None, itemsize=None):
+    import torch
+    strides = None
+    if ld is not None and len(shape) == 2:
+        strides = (ld * itemsize, itemsize)
+    if ptr is None or ptr == 0 or any(s == 0 for s in shape):
+        tdt = {"<u2": torch.uint16, "<u4": torch.uint32, "<u8": torch.uint64}[dtype_str]
+        return torch.zeros(shape, dtype=tdt, device="cuda")
+    return torch.as_tensor(_DevView(ptr, shape, dtype_str, strides), device="cuda")
+
+
+class Context:
+    """A libgbla context on one CUDA device; device memory comes from torch."""
+
+    def __init__(self, device: int = 0, torch_allocator: bool = True):
+        import torch
+        L = load_library()
+        self._h = ctypes.c_void_p()
+        _check(L.gbla_ctx_create(device, ctypes.byref(self._h)))
+        self.device = device
+        self._live = {}
+        if torch_allocator:
+            dev = torch.device("cuda", device)
+
+            def _alloc(nbytes, stream, user):
+                t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                ptr = t.data_ptr()
+                self._live[ptr] = t
+                return ptr
+
+            def _free(ptr, stream, user):
+                self._live.pop(int(ptr) if ptr else 0, None)
+
+            self._alloc_cb = _ALLOC_FN(_alloc)
+            self._free_cb = _FREE_FN(_free)
+            _check(L.gbla_ctx_set_allocator(self._h, self._alloc_cb, self._free_cb, None))
+
+    def set_comm(self, unique_id: bytes, rank: int, world: int):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(_lib.gbla_ctx_set_comm(self._h, buf, rank, world))
+
+    def close(self):
+        if self._h:
+            _lib.gbla_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(L.gbla_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class Mat:
+    """A spliced matrix (gbla_mat) and its results."""
+
+    def __init__(self, ctx: Context, handle, p: int, keep=()):
+        self.ctx = ctx
+        self._h = handle
+        self.p = p
+        self._keep = keep
+
+    # ---- results
+    def dims(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.gbla_get_dims(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def maps(self):
+        """(sigma[n], pivot_row[npiv], nonpivot_row[mN]) as new torch tensors (int64)."""
+        npiv, mN, nN = self.dims()
+        s, pr, nr = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.gbla_get_maps(self._h, ctypes.byref(s), ctypes.byref(pr), ctypes.byref(nr)))
+        return (_view(s.value, (npiv + nN,), "<u4").clone(), _view(pr.value, (npiv,), "<u4").clone(),
+                _view(nr.value, (mN,), "<u4").clone())
+
+    def D(self):
+        npiv, mN, nN = self.dims()
+        d, ld = ctypes.c_void_p(), ctypes.c_int64()
+        _check(_lib.gbla_get_D(self._h, ctypes.byref(d), ctypes.byref(ld)))
+        return _view(d.value, (mN, nN), "<u2", ld.value, 2).clone()
+
+    def cprime(self):
+        npiv, mN, nN = self.dims()
+        d, ld = ctypes.c_void_p(), ctypes.c_int64()
+        _check(_lib.gbla_get_Cprime(self._h, ctypes.byref(d), ctypes.byref(ld)))
+        return None if not d.value else _view(d.value, (mN, npiv), "<u2", ld.value, 2).clone()
+
+    def bprime(self):
+        npiv, mN, nN = self.dims()
+        d, ld = ctypes.c_void_p(), ctypes.c_int64()
+        _check(_lib.gbla_get_Bprime(self._h, ctypes.byref(d), ctypes.byref(ld)))
+        return None if not d.value else _view(d.value, (npiv, nN), "<u2", ld.value, 2).clone()
+
+    def quadrant(self, which: str, stream=None):
+        import torch
+        npiv, mN, nN = self.dims()
+        shape = {"A": (npiv, npiv), "B": (npiv, nN), "C": (mN, npiv), "D": (mN, nN)}[which]
+        ld = max(shape[1], 1)
+        out = torch.zeros((max(shape[0], 1), ld), dtype=torch.uint16, device="cuda")
+        _check(_lib.gbla_densify_quadrant(self._h, which.encode(), ctypes.c_void_p(out.data_ptr()), ld,
+                                          _stream_ptr(stream)))
+        torch.cuda.current_stream().synchronize()
+        return out[:shape[0], :shape[1]]
+
+    def rref(self):
+        """(rank, pivcol[rank], R[rank x nN]) as new torch tensors."""
+        npiv, mN, nN = self.dims()
+        rk, pc, R, ld = ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+        _check(_lib.gbla_get_rref(self._h, ctypes.byref(rk), ctypes.byref(pc), ctypes.byref(R), ctypes.byref(ld)))
+        r = rk.value
+        return r, _view(pc.value, (r,), "<u4").clone(), _view(R.value, (r, nN), "<u2", ld.value, 2).clone()
+
+    def rref_to_host(self, stream=None):
+        """(rank, pivcol, R) copied to host numpy arrays by the library."""
+        npiv, mN, nN = self.dims()
+        rk = ctypes.c_int64()
+        _check(_lib.gbla_get_rref(self._h, ctypes.byref(rk), None, None, None))
+        r = rk.value
+        pc = np.zeros(max(r, 1), np.uint32)
+        R = np.zeros((max(r, 1), max(nN, 1)), np.uint16)
+        _check(_lib.gbla_copy_rref_to_host(self._h, pc.ctypes.data_as(ctypes.c_void_p),
+                                           R.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
+        return r, pc[:r], R[:r, :nN]
+
+    def opcount(self):
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.gbla_get_opcount(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def phase_ms(self):
+        arr = (ctypes.c_float * 5)()
+        _check(_lib.gbla_get_phase_ms(self._h, arr))
+        return dict(zip(["splice", "reduce_C", "reduce_B", "update_D", "echelon"], list(arr)))
+
+    def free(self):
+        if self._h:
+            _lib.gbla_mat_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _csr_struct(m, n, row_ptr, col, val):
+    """Marshal a CSR given as torch CUDA tensors (device) or numpy arrays (host)."""
+    host = isinstance(row_ptr, np.ndarray)
+    if host:
+        row_ptr = np.ascontiguousarray(row_ptr, np.uint64)
+        col = np.ascontiguousarray(col, np.uint32)
+        val = np.ascontiguousarray(val, np.uint16)
+        ptrs = [a.ctypes.data for a in (row_ptr, col, val)]
+        nnz = int(row_ptr[-1]) if row_ptr.size else 0
+        keep = (row_ptr, col, val)
+    else:
+        import torch
+        for t, dt in ((row_ptr, torch.uint64), (col, torch.uint32), (val, torch.uint16)):
+            if not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+                raise TypeError("device CSR must be contiguous CUDA tensors of dtypes uint64/uint32/uint16")
+        ptrs = [t.data_ptr() for t in (row_ptr, col, val)]
+        nnz = int(col.numel())
+        keep = (row_ptr, col, val)
+    return _CSR(m, n, nnz, ptrs[0], ptrs[1], ptrs[2]), host, keep
+
+
+# ---- the six calls ------------------------------------------------------
+def gbla_splice(ctx: Context, m, n, row_ptr, col, val, p, stream=None) -> Mat:
+    """Step 1.  CSR arrays: torch CUDA tensors or numpy (host)."""
+    csr, host, keep = _csr_struct(m, n, row_ptr, col, val)
+    h = ctypes.c_void_p()
+    _check(_lib.gbla_splice(ctx._h, ctypes.byref(csr), p, GBLA_HOST_INPUT if host else 0, _stream_ptr(stream),
+                            ctypes.byref(h)))
+    return Mat(ctx, h, p, keep)
+
+
+def gbla_reduce_B(mat: Mat, stream=None):
+    _check(_lib.gbla_reduce_B(mat._h, _stream_ptr(stream)))
+
+
+def gbla_reduce_C(mat: Mat, fused: bool = True, keep_cprime: bool = False, stream=None):
+    flags = (GBLA_FUSE_D if fused else 0) | (GBLA_KEEP_CPRIME if keep_cprime else 0)
+    _check(_lib.gbla_reduce_C(mat._h, flags, _stream_ptr(stream)))
+
+
+def gbla_update_D(mat: Mat, stream=None):
+    _check(_lib.gbla_update_D(mat._h, _stream_ptr(stream)))
+
+
+def gbla_echelon_D(mat: Mat, flags: int = 0, stream=None) -> int:
+    r = ctypes.c_int64()
+    _check(_lib.gbla_echelon_D(mat._h, flags, _stream_ptr(stream), ctypes.byref(r)))
+    return r.value
+
+
+def gbla_reduce(ctx: Context, m, n, row_ptr, col, val, p, flags: int = 0, stream=None) -> Mat:
+    """Whole pipeline (new order by default).  Host numpy input => the library
+    copies it to the device (GBLA_HOST_INPUT)."""
+    csr, host, keep = _csr_struct(m, n, row_ptr, col, val)
+    h = ctypes.c_void_p()
+    _check(_lib.gbla_reduce(ctx._h, ctypes.byref(csr), p, flags | (GBLA_HOST_INPUT if host else 0),
+                            _stream_ptr(stream), ctypes.byref(h)))
+    return Mat(ctx, h, p, keep)
+
+
+def kernel_launches() -> int:
+    return int(load_library().gbla_kernel_launches())
+
+
+def version() -> str:
+    return load_library().gbla_version().decode()

@@ -1,0 +1,398 @@
+// api.cu -- the C ABI of include/gbla.h: argument checks, call-order state
+// machine, allocation through the context allocator, phase timing.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "internal.cuh"
+
+#include <atomic>
+
+static thread_local char g_err[1024];
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+extern "C" uint64_t gbla_kernel_launches(void) { return g_launches.load(); }
+
+void set_error(const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+extern "C" const char *gbla_last_error(void) { return g_err; }
+
+extern "C" const char *gbla_version(void)
+{
+    return "libgbla 0.1 (sm_100a; Faugere-Lachartre over GF(p), p < 2^16; arXiv 1602.06097)";
+}
+
+void *ctx_alloc(gbla_ctx c, size_t bytes, cudaStream_t s)
+{
+    if (bytes == 0) bytes = 16;
+    if (c->alloc) return c->alloc(bytes, (void *)s, c->user);
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void ctx_free(gbla_ctx c, void *p, cudaStream_t s)
+{
+    if (!p) return;
+    if (c->free_fn) c->free_fn(p, (void *)s, c->user);
+    else cudaFreeAsync(p, s);
+}
+
+gbla_status dalloc(gbla_mat h, size_t bytes, void **out)
+{
+    void *p = ctx_alloc(h->ctx, bytes, h->stream);
+    if (!p) {
+        cudaGetLastError();
+        set_error("device allocation of %zu bytes failed", bytes);
+        return GBLA_E_NOMEM;
+    }
+    h->allocs.push_back({p, bytes});
+    *out = p;
+    return GBLA_OK;
+}
+
+void dfree_all(gbla_mat h)
+{
+    for (auto &a : h->allocs) ctx_free(h->ctx, a.ptr, h->stream);
+    h->allocs.clear();
+}
+
+// ------------------------------------------------------------------ context
+extern "C" gbla_status gbla_ctx_create(int device, gbla_ctx *out)
+{
+    if (!out) { set_error("gbla_ctx_create: out is NULL"); return GBLA_E_INVAL; }
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_error("gbla_ctx_create: no CUDA device (libgbla has no CPU fallback)");
+        return GBLA_E_CUDA;
+    }
+    if (device < 0 || device >= ndev) { set_error("gbla_ctx_create: bad device %d", device); return GBLA_E_INVAL; }
+    cudaDeviceProp prop;
+    GBLA_CUDA_TRY(cudaSetDevice(device));
+    GBLA_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error("gbla_ctx_create: device %d is sm_%d%d; libgbla is built for sm_100a only", device, prop.major,
+                  prop.minor);
+        return GBLA_E_CUDA;
+    }
+    gbla_ctx c = new gbla_ctx_s();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    c->cc_major = prop.major;
+    c->cc_minor = prop.minor;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    *out = c;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_ctx_set_allocator(gbla_ctx ctx, gbla_alloc_fn alloc, gbla_free_fn free_fn, void *user)
+{
+    if (!ctx) { set_error("NULL context"); return GBLA_E_INVAL; }
+    if ((alloc == nullptr) != (free_fn == nullptr)) { set_error("allocator needs both alloc and free"); return GBLA_E_INVAL; }
+    ctx->alloc = alloc;
+    ctx->free_fn = free_fn;
+    ctx->user = user;
+    return GBLA_OK;
+}
+
+gbla_status dist_set_comm(gbla_ctx ctx, const void *id, int rank, int world);
+void dist_destroy(gbla_ctx ctx);
+
+extern "C" gbla_status gbla_ctx_set_comm(gbla_ctx ctx, const void *nccl_unique_id, int rank, int world)
+{
+    if (!ctx) { set_error("NULL context"); return GBLA_E_INVAL; }
+    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) {
+        set_error("gbla_ctx_set_comm: bad rank %d / world %d", rank, world);
+        return GBLA_E_INVAL;
+    }
+    return dist_set_comm(ctx, nccl_unique_id, rank, world);
+}
+
+extern "C" void gbla_ctx_destroy(gbla_ctx ctx)
+{
+    if (!ctx) return;
+    dist_destroy(ctx);
+    delete ctx;
+}
+
+// ------------------------------------------------------------------ helpers
+static bool is_prime_u32(uint32_t p)
+{
+    if (p < 2) return false;
+    for (uint32_t d = 2; (uint64_t)d * d <= p; d++)
+        if (p % d == 0) return false;
+    return true;
+}
+
+struct PhaseTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit PhaseTimer(cudaStream_t st) : s(st) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+    float stop() {
+        float ms = 0;
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        return ms;
+    }
+    ~PhaseTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+static gbla_status check_mat(gbla_mat h, void *stream)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    h->stream = (cudaStream_t)stream;
+    GBLA_CUDA_TRY(cudaSetDevice(h->ctx->device));
+    return GBLA_OK;
+}
+
+// ------------------------------------------------------------------ calls
+extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags, void *stream,
+                                   gbla_mat *out)
+{
+    if (!out) { set_error("gbla_splice: out is NULL"); return GBLA_E_INVAL; }
+    *out = nullptr;
+    if (!ctx || !M) { set_error("gbla_splice: NULL argument"); return GBLA_E_INVAL; }
+    if (flags & ~(uint32_t)GBLA_HOST_INPUT) { set_error("gbla_splice: unsupported flags 0x%x", flags); return GBLA_E_INVAL; }
+    if (p <= 2 || p >= 65536 || !is_prime_u32(p)) {
+        set_error("gbla_splice: p = %u is not a prime in (2, 2^16)", p);
+        return GBLA_E_DOMAIN;
+    }
+    if (M->m < 0 || M->n < 0 || M->nnz < 0 || M->m >= (1ll << 31) || M->n >= (1ll << 31)) {
+        set_error("gbla_splice: bad dimensions m=%lld n=%lld nnz=%lld", (long long)M->m, (long long)M->n,
+                  (long long)M->nnz);
+        return GBLA_E_INVAL;
+    }
+    if (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))) { set_error("gbla_splice: NULL CSR array"); return GBLA_E_INVAL; }
+    GBLA_CUDA_TRY(cudaSetDevice(ctx->device));
+    gbla_mat h = new gbla_mat_s();
+    h->ctx = ctx;
+    h->stream = (cudaStream_t)stream;
+    h->m = M->m; h->n = M->n; h->nnz = M->nnz;
+    h->p = p;
+    h->F = make_field(p);
+    PhaseTimer tm(h->stream);
+    gbla_status s = splice_impl(h, M, flags);
+    if (s != GBLA_OK) {
+        cudaStreamSynchronize(h->stream);
+        cudaGetLastError();
+        dfree_all(h);
+        delete h;
+        return s;
+    }
+    h->phase_ms[0] = tm.stop();
+    *out = h;
+    return GBLA_OK;
+}
+
+gbla_status reduce_c_dispatch(gbla_mat h, bool fused, bool keep_x);
+
+extern "C" gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (flags & ~(uint32_t)(GBLA_FUSE_D | GBLA_KEEP_CPRIME | GBLA_SPARSE_INT)) {
+        set_error("gbla_reduce_C: unsupported flags 0x%x", flags);
+        return GBLA_E_INVAL;
+    }
+    if (h->did_cprime || h->did_fused) { set_error("gbla_reduce_C: already reduced"); return GBLA_E_ORDER; }
+    const bool fused = flags & GBLA_FUSE_D;
+    if (fused && (h->did_reduce_B || h->did_update)) {
+        set_error("gbla_reduce_C(FUSE_D) after reduce_B/update_D would reduce D twice");
+        return GBLA_E_ORDER;
+    }
+    PhaseTimer tm(h->stream);
+    GBLA_TRY(reduce_c_int(h, fused, (flags & GBLA_KEEP_CPRIME) != 0));
+    h->phase_ms[1] = tm.stop();
+    if (fused) { h->did_fused = true; h->did_update = true; if (flags & GBLA_KEEP_CPRIME) h->did_cprime = true; }
+    else h->did_cprime = true;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_reduce_B(gbla_mat h, void *stream)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (h->did_reduce_B) { set_error("gbla_reduce_B: already done"); return GBLA_E_ORDER; }
+    PhaseTimer tm(h->stream);
+    GBLA_TRY(reduce_b_int(h));
+    h->phase_ms[2] = tm.stop();
+    h->did_reduce_B = true;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_update_D(gbla_mat h, void *stream)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (h->did_update) { set_error("gbla_update_D: D already updated"); return GBLA_E_ORDER; }
+    const bool have_x = h->did_cprime, have_b = h->did_reduce_B;
+    if (have_x == have_b) {
+        set_error(have_x ? "gbla_update_D: both reduce_B and reduce_C were run (would give D - C A^-1 A^-1 B)"
+                         : "gbla_update_D: needs reduce_B or an unfused reduce_C first");
+        return GBLA_E_ORDER;
+    }
+    PhaseTimer tm(h->stream);
+    if (have_x) GBLA_TRY(update_d_from_x_int(h));
+    else GBLA_TRY(update_d_from_bp_int(h));
+    h->phase_ms[3] = tm.stop();
+    h->did_update = true;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *rank)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (flags & ~(uint32_t)(GBLA_DENSE_INT | GBLA_DENSE_TC)) {
+        set_error("gbla_echelon_D: unsupported flags 0x%x", flags);
+        return GBLA_E_INVAL;
+    }
+    if (h->rank >= 0) { set_error("gbla_echelon_D: already echelonized"); return GBLA_E_ORDER; }
+    PhaseTimer tm(h->stream);
+    GBLA_TRY(echelon_impl(h, flags));
+    h->phase_ms[4] = tm.stop();
+    if (rank) *rank = h->rank;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags, void *stream,
+                                   gbla_mat *out)
+{
+    if (!out) { set_error("gbla_reduce: out is NULL"); return GBLA_E_INVAL; }
+    *out = nullptr;
+    if (flags & ~(uint32_t)GBLA_FLAGS_ALL) { set_error("gbla_reduce: unsupported flags 0x%x", flags); return GBLA_E_INVAL; }
+    gbla_mat h = nullptr;
+    GBLA_TRY(gbla_splice(ctx, M, p, flags & GBLA_HOST_INPUT, stream, &h));
+    gbla_status s;
+    if (flags & GBLA_ORDER_STANDARD) {
+        s = gbla_reduce_B(h, stream);
+        if (s == GBLA_OK) s = gbla_update_D(h, stream);
+    } else {
+        s = gbla_reduce_C(h, GBLA_FUSE_D | (flags & (GBLA_KEEP_CPRIME | GBLA_SPARSE_INT)), stream);
+    }
+    if (s == GBLA_OK) s = gbla_echelon_D(h, flags & (GBLA_DENSE_INT | GBLA_DENSE_TC), stream, nullptr);
+    if (s != GBLA_OK) { gbla_mat_free(h); return s; }
+    *out = h;
+    return GBLA_OK;
+}
+
+// ------------------------------------------------------------------ results
+extern "C" gbla_status gbla_get_dims(gbla_mat h, int64_t *npiv, int64_t *mN, int64_t *nN)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (npiv) *npiv = h->npiv;
+    if (mN) *mN = h->mN;
+    if (nN) *nN = h->nN;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_maps(gbla_mat h, const uint32_t **sigma, const uint32_t **pivot_row,
+                                     const uint32_t **nonpivot_row)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (sigma) *sigma = h->sigma;
+    if (pivot_row) *pivot_row = h->pivot_row;
+    if (nonpivot_row) *nonpivot_row = h->nonpivot_row;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_D(gbla_mat h, const uint16_t **D, int64_t *ld)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (D) *D = h->D;
+    if (ld) *ld = h->ldD;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_Cprime(gbla_mat h, const uint16_t **X, int64_t *ld)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (X) *X = h->did_cprime ? h->X : nullptr;
+    if (ld) *ld = h->ldX;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_Bprime(gbla_mat h, const uint16_t **Bp, int64_t *ld)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (Bp) *Bp = h->did_reduce_B ? h->Bp : nullptr;
+    if (ld) *ld = h->ldB;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_densify_quadrant(gbla_mat h, char which, uint16_t *out, int64_t ld, void *stream)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (!out) { set_error("densify: out is NULL"); return GBLA_E_INVAL; }
+    return densify_impl(h, which, out, ld);
+}
+
+extern "C" gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol, const uint16_t **R,
+                                     int64_t *ld)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (h->rank < 0) { set_error("gbla_get_rref: echelon_D not run"); return GBLA_E_ORDER; }
+    if (rank) *rank = h->rank;
+    if (pivcol) *pivcol = h->pivcol;
+    if (R) *R = h->R;
+    if (ld) *ld = h->ldR;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_copy_rref_to_host(gbla_mat h, uint32_t *pivcol, uint16_t *R, void *stream)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (h->rank < 0) { set_error("gbla_copy_rref_to_host: echelon_D not run"); return GBLA_E_ORDER; }
+    if (h->rank == 0) return GBLA_OK;
+    if (pivcol) GBLA_CUDA_TRY(cudaMemcpyAsync(pivcol, h->pivcol, h->rank * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (R && h->nN)
+        GBLA_CUDA_TRY(cudaMemcpy2DAsync(R, h->nN * 2, h->R, h->ldR * 2, h->nN * 2, h->rank, cudaMemcpyDeviceToHost,
+                                        h->stream));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_opcount(gbla_mat h, uint64_t *sparse_modmac, uint64_t *dense_modmac)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (sparse_modmac) *sparse_modmac = h->sparse_ops;
+    if (dense_modmac) *dense_modmac = h->dense_ops;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_phase_ms(gbla_mat h, float *ms5)
+{
+    if (!h || !ms5) { set_error("NULL argument"); return GBLA_E_INVAL; }
+    memcpy(ms5, h->phase_ms, sizeof h->phase_ms);
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_sync(gbla_mat h)
+{
+    if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return GBLA_OK;
+}
+
+extern "C" void gbla_mat_free(gbla_mat h)
+{
+    if (!h) return;
+    cudaSetDevice(h->ctx->device);
+    dfree_all(h);
+    cudaStreamSynchronize(h->stream);
+    delete h;
+}

@@ -1,0 +1,173 @@
+// internal.cuh -- shared internals of libgbla (CUDA path only; the oracle
+// shares nothing with this file).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "gbla.h"
+
+#define GBLA_NONE 0xFFFFFFFFu
+
+// ------------------------------------------------------------------ field
+// GF(p), p < 2^16 prime.  Residues are kept in [0, p); products of two
+// residues are < 2^32, so u64 accumulators hold >= 2^32 products before
+// overflow (delayed reduction).  Reduction of a u64 uses Barrett
+// with m64 = floor(2^64 / p): q = mulhi(x, m64) >= floor(x/p) - 1, so one
+// conditional subtraction gives the canonical residue.
+struct Field {
+    uint32_t p;
+    uint32_t pad;
+    uint64_t m64;
+};
+
+static inline Field make_field(uint32_t p) {
+    Field F;
+    F.p = p;
+    F.pad = 0;
+    F.m64 = ~0ull / p;
+    return F;
+}
+
+__device__ __forceinline__ uint32_t fmod64(uint64_t x, const Field &F) {
+    uint64_t q = __umul64hi(x, F.m64);
+    uint64_t r = x - q * (uint64_t)F.p;
+    return (uint32_t)(r >= F.p ? r - F.p : r);
+}
+__device__ __forceinline__ uint32_t fmul(uint32_t a, uint32_t b, const Field &F) {
+    return fmod64((uint64_t)a * b, F);
+}
+// a^(p-2) = a^-1 (Fermat; p prime).  a != 0.
+__device__ __forceinline__ uint32_t finv(uint32_t a, const Field &F) {
+    uint32_t e = F.p - 2, r = 1, b = a;
+    while (e) {
+        if (e & 1) r = fmul(r, b, F);
+        b = fmul(b, b, F);
+        e >>= 1;
+    }
+    return r;
+}
+__device__ __forceinline__ uint32_t fneg(uint32_t a, const Field &F) { return a ? F.p - a : 0; }
+
+// ------------------------------------------------------------------ launches
+// Host-side count of libgbla kernel launches (bench.py reports it).
+void note_launch(int n = 1);
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+#define GBLA_CUDA_TRY(expr)                                                              \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            set_error("%s:%d: %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+            return GBLA_E_CUDA;                                                          \
+        }                                                                                \
+    } while (0)
+#define GBLA_TRY(expr)                      \
+    do {                                    \
+        gbla_status s_ = (expr);            \
+        if (s_ != GBLA_OK) return s_;       \
+    } while (0)
+
+// ------------------------------------------------------------------ handles
+struct gbla_ctx_s {
+    int device = 0;
+    int sm_count = 0;
+    int cc_major = 0, cc_minor = 0;
+    size_t smem_optin = 0;
+    gbla_alloc_fn alloc = nullptr;
+    gbla_free_fn free_fn = nullptr;
+    void *user = nullptr;
+    void *nccl_comm = nullptr;   // ncclComm_t
+    int rank = 0, world = 1;
+};
+
+struct Alloc {
+    void *ptr;
+    size_t bytes;
+};
+
+struct gbla_mat_s {
+    gbla_ctx ctx = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t m = 0, n = 0, nnz = 0, npiv = 0, mN = 0, nN = 0, npairs = 0;
+    uint32_t p = 0;
+    Field F{};
+
+    // input (device); owned copy when the caller gave host memory
+    const uint64_t *row_ptr = nullptr;
+    const uint32_t *col = nullptr;
+    const uint16_t *val = nullptr;
+
+    // Step 1 maps
+    uint32_t *lead = nullptr;          // [m]  first column or NONE
+    uint16_t *inv_lead = nullptr;      // [m]  inverse of the leading value
+    uint32_t *sigma = nullptr;         // [n]
+    uint32_t *pivot_row = nullptr;     // [npiv]
+    uint32_t *pcol = nullptr;          // [npiv] original column of pivot i
+    uint32_t *nonpivot_row = nullptr;  // [mN]
+    uint32_t *tlead = nullptr;         // [mN] sigma(lead) of each target (n for zero rows)
+    uint32_t *order = nullptr;         // [mN] targets sorted by tlead (longest first)
+
+    // sigma-ordered rows: A|B (pivot order) and C|D (original order)
+    uint64_t *ab_ptr = nullptr; uint32_t *ab_col = nullptr; uint16_t *ab_val = nullptr;
+    uint32_t *ab_np = nullptr;         // [npiv] entries with sigma col < npiv (A part)
+    uint64_t *cd_ptr = nullptr; uint32_t *cd_col = nullptr; uint16_t *cd_val = nullptr;
+    uint32_t *cd_np = nullptr;         // [mN]
+    int64_t nnz_ab = 0, nnz_cd = 0;
+
+    // two-row multilines of A|B: pair k = pivot rows (2k, 2k+1)
+    uint64_t *ml_ptr = nullptr;        // [npairs+1] slot offsets
+    uint32_t *ml_col = nullptr;        // [slots] union columns (sigma order)
+    uint32_t *ml_val = nullptr;        // [slots] lo16 = row 2k value, hi16 = row 2k+1 value
+    uint32_t *ml_np = nullptr;         // [npairs] slots with col < npiv
+    uint32_t *ml_skip = nullptr;       // [npairs] leading slots with col <= 2k+1
+    uint16_t *ml_a01 = nullptr;        // [npairs] A[2k][2k+1]
+    uint32_t *ab_w = nullptr;          // [npiv] nnz of pivot row
+    int64_t nslots = 0;
+
+    // dense matrices
+    uint16_t *D = nullptr; int64_t ldD = 0;     // mN x nN (current D)
+    uint16_t *X = nullptr; int64_t ldX = 0;     // C' (mN x npiv)
+    uint16_t *Bp = nullptr; int64_t ldB = 0;    // B' (npiv x nN)
+    uint16_t *R = nullptr; int64_t ldR = 0;     // rank x nN
+    uint32_t *pivcol = nullptr;
+    int64_t rank = -1;
+
+    uint64_t *opcount = nullptr;       // [mN] per-target sparse modMACs
+    uint64_t sparse_ops = 0, dense_ops = 0;
+
+    // call-order state
+    bool did_reduce_B = false, did_cprime = false, did_update = false, did_fused = false;
+    float phase_ms[5] = {0, 0, 0, 0, 0};
+
+    std::vector<Alloc> allocs;
+};
+
+// device memory through the context allocator, recorded on the handle
+gbla_status dalloc(gbla_mat h, size_t bytes, void **out);
+template <class T>
+static inline gbla_status dalloc_t(gbla_mat h, size_t count, T **out) {
+    return dalloc(h, count * sizeof(T) + 16, reinterpret_cast<void **>(out));
+}
+void dfree_all(gbla_mat h);
+void *ctx_alloc(gbla_ctx c, size_t bytes, cudaStream_t s);
+void ctx_free(gbla_ctx c, void *p, cudaStream_t s);
+
+// phases
+gbla_status splice_impl(gbla_mat h, const gbla_csr *M, uint32_t flags);
+gbla_status reduce_c_int(gbla_mat h, bool fused, bool keep_x);
+gbla_status update_d_from_x_int(gbla_mat h);
+gbla_status reduce_b_int(gbla_mat h);
+gbla_status update_d_from_bp_int(gbla_mat h);
+gbla_status echelon_impl(gbla_mat h, uint32_t flags);
+gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
+
+static inline unsigned grid_for(int64_t work, int per_block) {
+    int64_t g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > 0x7fffffff) g = 0x7fffffff;
+    return (unsigned)g;
+}

@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bar: bit-exact for everything (integer arithmetic mod p): maps, quadrants,
+C', B', D_new, modMAC counts, rank, R and pivot columns.
+Run on a B200 via gpurun: python -m pytest tests -m gpu -x -q
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gbla_gen
+import oracle
+from conftest import csr_from_dense
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def gb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a GPU")
+    import paper_1602_06097_b200 as gb
+    return gb
+
+
+@pytest.fixture(scope="module")
+def ctx(gb):
+    return gb.Context(0)
+
+
+def to_dev(M):
+    import torch
+    return (torch.from_numpy(M.row_ptr.astype(np.uint64)).cuda(), torch.from_numpy(M.col.astype(np.uint32)).cuda(),
+            torch.from_numpy(M.val.astype(np.uint16)).cuda())
+
+
+def np_(t):
+    return t.cpu().numpy()
+
+
+def gpu_reduce(gb, ctx, M, flags=0):
+    rp, c, v = to_dev(M)
+    h = gb.gbla_reduce(ctx, M.m, M.n, rp, c, v, M.p, flags=flags)
+    return h
+
+
+def check_full(gb, ctx, M, res=None, flags=0, check_dnew=True):
+    if res is None:
+        res = oracle.reduce(M, want_x=True)
+    S = res.splice
+    rp, c, v = to_dev(M)
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+    npiv, mN, nN = h.dims()
+    assert (npiv, mN, nN) == (S.npiv, S.mN, S.nN)
+    sig, prow, nprow = h.maps()
+    assert np.array_equal(np_(sig), S.sigma) and np.array_equal(np_(prow), S.pivot_row)
+    assert np.array_equal(np_(nprow), S.nonpivot_row)
+    if flags & gb.GBLA_ORDER_STANDARD:
+        gb.gbla_reduce_B(h)
+        gb.gbla_update_D(h)
+    else:
+        gb.gbla_reduce_C(h, fused=True)
+    if check_dnew:
+        assert np.array_equal(np_(h.D()), res.dnew), "D_new differs"
+    if not (flags & gb.GBLA_ORDER_STANDARD):
+        assert h.opcount()[0] == res.modmac
+    r = gb.gbla_echelon_D(h, flags & (gb.GBLA_DENSE_INT | gb.GBLA_DENSE_TC))
+    rank, pc, R = h.rref()
+    assert r == rank == res.rank
+    assert np.array_equal(np_(pc), res.pivcol)
+    assert np.array_equal(np_(R), res.R)
+    h.free()
+
+
+def test_splice_quadrants_random_suite(gb, ctx):
+    for M in gbla_gen.random_suite(80, seed0=21):
+        S = oracle.splice(M)
+        A, B, C, D = oracle.quadrants(M, S)
+        rp, c, v = to_dev(M)
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        sig, prow, nprow = h.maps()
+        assert np.array_equal(np_(sig), S.sigma)
+        assert np.array_equal(np_(prow), S.pivot_row)
+        assert np.array_equal(np_(nprow), S.nonpivot_row)
+        for name, ref in (("A", A), ("B", B), ("C", C), ("D", D)):
+            assert np.array_equal(np_(h.quadrant(name)).astype(np.uint32), ref), name
+        h.free()
+
+
+def test_pipeline_random_suite_new_order(gb, ctx):
+    for M in gbla_gen.random_suite(150, seed0=23):
+        check_full(gb, ctx, M)
+
+
+def test_pipeline_random_suite_standard_order(gb, ctx):
+    for M in gbla_gen.random_suite(60, seed0=25):
+        check_full(gb, ctx, M, flags=gb.GBLA_ORDER_STANDARD)
+
+
+def test_unfused_cprime_bprime(gb, ctx):
+    for M in list(gbla_gen.random_suite(40, seed0=27)) + [gbla_gen.f4_matrix("c0")]:
+        S = oracle.splice(M)
+        A, B, C, D = oracle.quadrants(M, S)
+        dn, x, ops = oracle.dnew_rows(M, S, want_x=True)
+        rp, c, v = to_dev(M)
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        gb.gbla_reduce_C(h, fused=False)
+        assert np.array_equal(np_(h.cprime()), x)
+        gb.gbla_update_D(h)
+        assert np.array_equal(np_(h.D()), dn)
+        assert h.opcount()[0] == int(ops.sum())
+        h.free()
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        gb.gbla_reduce_B(h)
+        if M.m <= 200:
+            assert np.array_equal(np_(h.bprime()).astype(np.uint32), oracle.trsm(A, B, M.p))
+        gb.gbla_update_D(h)
+        assert np.array_equal(np_(h.D()), dn)
+        h.free()
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        gb.gbla_reduce_C(h, fused=True, keep_cprime=True)
+        assert np.array_equal(np_(h.cprime()), x)
+        assert np.array_equal(np_(h.D()), dn)
+        h.free()
+
+
+def test_c0_full(gb, ctx, c0_matrix, c0_oracle):
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_ORDER_STANDARD)
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_DENSE_INT)
+
+
+def test_host_input_and_host_copy(gb, ctx, c0_matrix, c0_oracle):
+    M = c0_matrix
+    h = gb.gbla_reduce(ctx, M.m, M.n, M.row_ptr, M.col, M.val, M.p)     # numpy => GBLA_HOST_INPUT
+    r, pc, R = h.rref_to_host()
+    assert r == c0_oracle.rank and np.array_equal(pc, c0_oracle.pivcol) and np.array_equal(R, c0_oracle.R)
+    h.free()
+
+
+def test_c1_full_size_against_golden(gb, ctx):
+    """c1 (bench workload) at full size: counts and digests written by the
+    oracle (tests/golden/make_golden.py), plus sampled D_new rows computed by
+    the oracle one by one."""
+    g = json.load(open(os.path.join(GOLD, "c1_oracle.json")))
+    M = gbla_gen.f4_matrix("c1")
+    h = gpu_reduce(gb, ctx, M)
+    npiv, mN, nN = h.dims()
+    assert (npiv, mN, nN) == (g["npiv"], g["mN"], g["nN"])
+    assert h.opcount()[0] == g["modmac_sparse"]
+    r, pc, R = h.rref()
+    assert r == g["rank_D"]
+    assert oracle.rref_digest(r, nN, np_(pc), np_(R)) == g["rref_sha256"]
+    h.free()
+    # D_new: digest + sampled rows by the oracle
+    rp, c, v = to_dev(M)
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+    gb.gbla_reduce_C(h, fused=True)
+    D = np_(h.D())
+    assert oracle.array_digest(D) == g["dnew_sha256"]
+    S = oracle.splice(M)
+    rng = np.random.default_rng(5)
+    t = np.sort(rng.choice(S.mN, 24, replace=False))
+    dn, _, ops = oracle.dnew_rows(M, S, targets=t)
+    assert np.array_equal(D[t], dn)
+    h.free()
+
+
+def test_edge_cases(gb, ctx):
+    cases = [
+        np.eye(6, dtype=np.int64),                        # A = I, no C|D
+        np.zeros((4, 5), dtype=np.int64),                 # all zero rows, npiv = 0
+        np.array([[0, 0, 3, 1], [0, 0, 0, 0], [0, 0, 6, 2]]),   # zero row + dependent
+        np.array([[1, 2], [1, 3]]),                       # SPEC tie example
+        np.array([[5]]),                                  # 1x1
+        np.ones((7, 3), dtype=np.int64),                  # wide dependence
+        np.triu(np.ones((9, 9), dtype=np.int64)),         # dense upper triangular
+    ]
+    for a in cases:
+        for p in (3, 7, 65521):
+            M = csr_from_dense(a, p)
+            check_full(gb, ctx, M)
+    # odd / even pivot counts with the multiline pairing, dense D
+    rng = np.random.default_rng(3)
+    for npiv in (1, 2, 3, 63, 64, 65, 129):
+        n, m = npiv + 70, npiv + 90
+        a = np.zeros((m, n), dtype=np.int64)
+        a[:npiv, :npiv] = np.triu(rng.integers(0, 65521, (npiv, npiv)))
+        np.fill_diagonal(a[:npiv, :npiv], 1)
+        a[:npiv, npiv:] = rng.integers(0, 65521, (npiv, 70))
+        a[npiv:, :] = rng.integers(0, 65521, (90, n))
+        check_full(gb, ctx, csr_from_dense(a, 65521))
+
+
+def test_errors(gb, ctx):
+    M = csr_from_dense([[1, 2], [0, 3]], 7)
+    rp, c, v = to_dev(M)
+    with pytest.raises(gb.GblaError) as e:
+        gb.gbla_splice(ctx, M.m, M.n, rp, c, v, 8)
+    assert e.value.status == 2
+    import torch
+    bad_c = torch.flip(c, [0]).contiguous()
+    with pytest.raises(gb.GblaError) as e:
+        gb.gbla_splice(ctx, M.m, M.n, rp, bad_c, v, 7)
+    assert e.value.status == 1
+    bad_v = v.clone(); bad_v[0] = 7
+    with pytest.raises(gb.GblaError) as e:
+        gb.gbla_splice(ctx, M.m, M.n, rp, c, bad_v, 7)
+    assert e.value.status == 1
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, 7)
+    with pytest.raises(gb.GblaError) as e:
+        gb.gbla_update_D(h)                        # nothing to update with
+    assert e.value.status == 3
+    gb.gbla_reduce_B(h)
+    gb.gbla_reduce_C(h, fused=False)
+    with pytest.raises(gb.GblaError) as e:
+        gb.gbla_update_D(h)                        # both: would apply A^-1 twice
+    assert e.value.status == 3
+    h.free()
