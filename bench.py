@@ -232,7 +232,7 @@ def main():
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
-    if rank == 0:
+    if rank == 0 and args.e2e_steps > 0:
         hp = [torch.from_numpy(a).pin_memory() for a in (M.row_ptr, M.col, M.val)]
         hn = [t.numpy() for t in hp]
         (npiv, mN, nN), rk = rank_d

@@ -139,6 +139,16 @@ gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *ra
 gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags,
                         void *stream, gbla_mat *out);
 
+/* K11 as a standalone op (used by the echelon; exposed for tests/benches):
+ *   C[r_i, x] <- (C[r_i, x] - sum_{k<K} A[i, k] * B[k, x]) mod p,
+ *   i < rows, x < cols, r_i = rowidx ? rowidx[i] : i.
+ * A: rows x K (row stride lda), B: K x cols (stride ldb), C: stride ldc; all
+ * device u16 residues < p; K <= 128.  engine 0 = tcgen05 (u8 limbs, exact:
+ * 128 * 255^2 * 2 < 2^31 per s32 accumulator), 1 = INT pipe.  Synchronizes. */
+gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K,
+                         const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
+                         const uint32_t *rowidx, uint16_t *C, int64_t ldc, int engine, void *stream);
+
 /* ---- results (views valid until gbla_mat_free) ------------------------- */
 gbla_status gbla_get_dims(gbla_mat h, int64_t *npiv, int64_t *mN, int64_t *nN);
 /* sigma[n]: column c -> sigma index; pivot_row[npiv]; nonpivot_row[mN]

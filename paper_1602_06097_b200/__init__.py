@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH):
         "gbla_version": ([], ctypes.c_char_p),
         "gbla_nccl_get_unique_id": ([vp], st),
         "gbla_kernel_launches": ([], ctypes.c_uint64),
+        "gbla_modgemm": ([vp, u32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -104,7 +105,7 @@ def exported_symbols():
             "gbla_get_dims", "gbla_get_maps", "gbla_get_D", "gbla_get_Cprime", "gbla_get_Bprime",
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
-            "gbla_kernel_launches", "gbla_nccl_get_unique_id"]
+            "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm"]
 
 
 def _check(status: int):
@@ -318,8 +319,12 @@ def gbla_reduce_B(mat: Mat, stream=None):
     _check(_lib.gbla_reduce_B(mat._h, _stream_ptr(stream)))
 
 
-def gbla_reduce_C(mat: Mat, fused: bool = True, keep_cprime: bool = False, stream=None):
+def gbla_reduce_C(mat: Mat, fused: bool = True, keep_cprime: bool = False, int_pipe: bool = False, stream=None):
+    """C <- C A^-1 (new order); fused: also D <- D - C A^-1 B.  int_pipe selects
+    the per-target multiline AXPY kernel (GBLA_SPARSE_INT) instead of the
+    tensor-core block path."""
     flags = (GBLA_FUSE_D if fused else 0) | (GBLA_KEEP_CPRIME if keep_cprime else 0)
+    flags |= GBLA_SPARSE_INT if int_pipe else 0
     _check(_lib.gbla_reduce_C(mat._h, flags, _stream_ptr(stream)))
 
 
@@ -341,6 +346,18 @@ def gbla_reduce(ctx: Context, m, n, row_ptr, col, val, p, flags: int = 0, stream
     _check(_lib.gbla_reduce(ctx._h, ctypes.byref(csr), p, flags | (GBLA_HOST_INPUT if host else 0),
                             _stream_ptr(stream), ctypes.byref(h)))
     return Mat(ctx, h, p, keep)
+
+
+def gbla_modgemm(ctx: Context, p: int, A, B, C, rowidx=None, engine: int = 0, stream=None):
+    """K11: C[rowidx[i]] -= A[i] @ B  (mod p), in place.  A: rows x K, B: K x cols,
+    C: torch uint16 CUDA tensors (2-D, unit column stride); K <= 128."""
+    rows, K = A.shape
+    K2, cols = B.shape
+    assert K == K2 and C.shape[1] >= cols
+    ri = ctypes.c_void_p(rowidx.data_ptr()) if rowidx is not None else None
+    _check(_lib.gbla_modgemm(ctx._h, p, rows, cols, K, ctypes.c_void_p(A.data_ptr()), A.stride(0),
+                             ctypes.c_void_p(B.data_ptr()), B.stride(0), ri, ctypes.c_void_p(C.data_ptr()),
+                             C.stride(0), engine, _stream_ptr(stream)))
 
 
 def kernel_launches() -> int:

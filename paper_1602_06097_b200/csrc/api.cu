@@ -194,6 +194,7 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
         cudaStreamSynchronize(h->stream);
         cudaGetLastError();
         dfree_all(h);
+        band_free(h);
         delete h;
         return s;
     }
@@ -218,7 +219,14 @@ extern "C" gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream)
         return GBLA_E_ORDER;
     }
     PhaseTimer tm(h->stream);
-    GBLA_TRY(reduce_c_int(h, fused, (flags & GBLA_KEEP_CPRIME) != 0));
+    const bool keep_x = (flags & GBLA_KEEP_CPRIME) != 0;
+    if (flags & GBLA_SPARSE_INT) {
+        GBLA_TRY(reduce_c_int(h, fused, keep_x));
+    } else {
+        // tensor-core block path (sparse_tc.cu): C' tiles, then D -= C' B
+        GBLA_TRY(reduce_c_tc(h, keep_x || !fused));
+        if (fused) GBLA_TRY(update_d_tc(h));
+    }
     h->phase_ms[1] = tm.stop();
     if (fused) { h->did_fused = true; h->did_update = true; if (flags & GBLA_KEEP_CPRIME) h->did_cprime = true; }
     else h->did_cprime = true;
@@ -247,7 +255,8 @@ extern "C" gbla_status gbla_update_D(gbla_mat h, void *stream)
         return GBLA_E_ORDER;
     }
     PhaseTimer tm(h->stream);
-    if (have_x) GBLA_TRY(update_d_from_x_int(h));
+    if (have_x && h->have_xt) GBLA_TRY(update_d_tc(h));
+    else if (have_x) GBLA_TRY(update_d_from_x_int(h));
     else GBLA_TRY(update_d_from_bp_int(h));
     h->phase_ms[3] = tm.stop();
     h->did_update = true;
@@ -394,5 +403,6 @@ extern "C" void gbla_mat_free(gbla_mat h)
     cudaSetDevice(h->ctx->device);
     dfree_all(h);
     cudaStreamSynchronize(h->stream);
+    band_free(h);
     delete h;
 }

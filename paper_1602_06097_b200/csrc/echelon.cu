@@ -1,36 +1,49 @@
 // echelon.cu -- Step 4, fully reduced (reading R13): R = RREF(D)
-// by blocked Gauss-Jordan over column panels of width K.
+// by blocked Gauss-Jordan over column panels of width PK.
 //
-// Invariant before panel [c0, c0+K): every row is either a pivot row (its
+// Invariant before panel [c0, c0+PK): every row is either a pivot row (its
 // pivot column < c0) or ACTIVE, and active rows are zero on all columns < c0
 // (a column < c0 is either a pivot column, eliminated from every other row,
 // or a column in which no active row was nonzero).  Per panel:
-//   K10 k_panel     one CTA scans the active rows in order and builds, in
-//                   shared memory, the reduced echelon basis of their panel
-//                   slices (incremental: reduce a candidate by the basis; if
-//                   nonzero, normalize at its first nonzero column and
-//                   eliminate that column from the basis).  It records the
-//                   selected rows S, their pivot columns and the transform T
-//                   with basis = T * D[S, panel].  It stops early when the
-//                   basis has K rows (full rank panel).  The resulting pivot
-//                   columns are the canonical ones (the basis is an RREF).
+//   K10 k_panel     one CTA (1024 threads) builds, in shared memory, the
+//                   reduced echelon basis of the active rows' panel slices:
+//                   candidates (active rows with a nonzero slice, in row
+//                   order) come in chunks; a chunk is first reduced by the
+//                   current basis in parallel (delayed u64 reduction), then
+//                   integrated one row at a time: a nonzero row is normalized
+//                   at its first nonzero column (inverse table) and that
+//                   column is eliminated from the basis and from the rest of
+//                   the chunk by the whole CTA.  Each row carries its
+//                   transform, so the basis is T * D[S, panel] for the
+//                   selected rows S.  The scan stops when the basis has PK
+//                   rows.  The basis is an RREF of the panel's row space, so
+//                   its pivot columns are the canonical ones.
 //       k_gather    F[i] = D[i, pivot columns] for every non-selected row
 //                   (active AND earlier pivot rows: back elimination), plus
 //                   the list of rows with F[i] != 0
-//       k_rnew      Rn = T * D[S, c0:]    (new pivot rows, full width)
-//   K11 trailing    D[i, c0:] -= F[i] * Rn    (modular GEMM; this file: the
-//                   INT-pipe engine; tc_gemm.cu: the tcgen05 engine)
+//       Rn          Rn = T * D[S, c0:]    (new pivot rows, full width)
+//   K11 trailing    D[i, c0:] -= F[i] * Rn    (modular GEMM)
 //       k_commit    D[S, c0:] = Rn; rowpiv[S] = pivot columns
+// Engines: GBLA_DENSE_TC (default): PK = 128, Rn and the trailing update on
+// tcgen05 (tc_gemm.cu); GBLA_DENSE_INT: PK = 64, both on the INT pipe.
 // At the end K13 compacts R (rows sorted by pivot column) and pivcol.
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
 
+gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                           const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc);
+gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
+                             const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
+                             uint8_t *Thi);
+
 namespace {
 
-constexpr int PK = 64;            // panel width of the INT engine
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int KPT = 128;          // K width of the tensor-core operand planes
 
+template <int PK>
 struct PanelState {
     uint32_t kp;                  // pivots found in this panel
     uint32_t nrows;               // rows with a nonzero coefficient
@@ -39,100 +52,180 @@ struct PanelState {
     uint16_t T[PK * PK];          // basis = T * D[S, panel]
 };
 
-// One CTA, 1024 threads.  Lane l of warp 0 holds panel columns 2l, 2l+1.
+// inverse table: inv[a] = a^-1 mod p (inv[0] = 0)
+__global__ void k_invtab(Field F, uint16_t *__restrict__ inv)
+{
+    const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < F.p) inv[a] = a ? (uint16_t)finv(a, F) : 0;
+}
+
+template <int PK>
+constexpr int panel_smem() { return (2 * (2 * PK) * PK + PK * PK) * (int)sizeof(uint16_t); }
+
+template <int PK>
 __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t c0, Field F,
                                                 const uint16_t *__restrict__ D, int64_t ldD,
-                                                uint32_t *__restrict__ rowpiv, PanelState *__restrict__ ps)
+                                                uint32_t *__restrict__ rowpiv, PanelState<PK> *__restrict__ ps,
+                                                uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,
+                                                const uint16_t *__restrict__ invtab)
 {
-    __shared__ uint32_t basis[PK][PK];
-    __shared__ uint32_t Tm[PK][PK];
-    __shared__ uint32_t bpc[PK];
-    __shared__ uint32_t bsel[PK];
-    __shared__ uint32_t cand[1024];
+    constexpr int CH = PK;             // candidates per chunk
+    constexpr int G = PK / 16;         // 16-column groups per row
+    constexpr int CPL = PK / 32;       // columns per lane
+    extern __shared__ uint16_t dsm[];
+    // rows [0, PK): basis; rows [PK, PK + CH): candidates.  X = panel values, A = transform.
+    uint16_t(*X)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm);
+    uint16_t(*A)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm + (PK + CH) * PK);
+    uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm + 2 * (PK + CH) * PK);   // [CH][PK] factors
+    __shared__ uint32_t bpc[PK], bsel[PK], crow[CH], selfc[CH], gbuf[PK + CH];
+    __shared__ uint32_t prx[PK], pra[PK];
     __shared__ uint32_t wcount[32];
-    __shared__ uint32_t s_ncand, s_nb;
+    __shared__ int s_ncand;
+    __shared__ long long s_next;
+    __shared__ uint32_t s_pself;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t p = F.p;
     const int64_t width = (nN - c0) < PK ? (nN - c0) : PK;
-    if (tid == 0) s_nb = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < mN; base += 1024) {
-        // 1. candidates of this chunk, in row order
-        int64_t r = base + tid;
-        bool cand_ok = false;
+    uint32_t nb = 0;
+    int64_t pos = 0;
+    while (nb < (uint32_t)PK && pos < mN) {
+        // (1) next chunk of candidates, in row order
+        const int64_t r = pos + tid;
+        bool ok = false;
         if (r < mN && rowpiv[r] == GBLA_NONE) {
             const uint16_t *row = D + (size_t)r * ldD + c0;
-            for (int64_t c = 0; c < width; c++)
-                if (row[c]) { cand_ok = true; break; }
+            if (width == PK) {
+                for (int c = 0; c < PK; c += 8) {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(row + c);
+                    if (v.x | v.y | v.z | v.w) { ok = true; break; }
+                }
+            } else {
+                for (int64_t c = 0; c < width; c++)
+                    if (row[c]) { ok = true; break; }
+            }
         }
-        unsigned msk = __ballot_sync(FULL, cand_ok);
+        const unsigned msk = __ballot_sync(FULL, ok);
         if (lane == 0) wcount[warp] = __popc(msk);
         __syncthreads();
         if (tid == 0) {
             uint32_t s = 0;
-            for (int w = 0; w < 32; w++) { uint32_t c = wcount[w]; wcount[w] = s; s += c; }
-            s_ncand = s;
+            for (int w = 0; w < 32; w++) { const uint32_t c = wcount[w]; wcount[w] = s; s += c; }
+            s_ncand = s < (uint32_t)CH ? (int)s : CH;
+            s_next = pos + 1024;
         }
         __syncthreads();
-        if (cand_ok) cand[wcount[warp] + __popc(msk & ((1u << lane) - 1u))] = (uint32_t)r;
+        const uint32_t rank = wcount[warp] + __popc(msk & ((1u << lane) - 1u));
+        if (ok && rank < (uint32_t)CH) crow[rank] = (uint32_t)r;
+        if (ok && rank == (uint32_t)CH) s_next = r;          // first candidate not taken
         __syncthreads();
-        // 2. warp 0 integrates the candidates
-        if (warp == 0) {
-            uint32_t nb = s_nb;
-            for (uint32_t ci = 0; ci < s_ncand && nb < PK; ci++) {
-                const uint32_t rr = cand[ci];
-                const uint16_t *row = D + (size_t)rr * ldD + c0;
-                uint32_t x0 = (2 * lane < width) ? row[2 * lane] : 0;
-                uint32_t x1 = (2 * lane + 1 < width) ? row[2 * lane + 1] : 0;
-                uint32_t a0 = (2 * lane == (int)nb) ? 1u : 0u, a1 = (2 * lane + 1 == (int)nb) ? 1u : 0u;
-                for (uint32_t b = 0; b < nb; b++) {
-                    const uint32_t pcb = bpc[b];
-                    uint32_t xv = (pcb & 1) ? x1 : x0;
-                    uint32_t f = __shfl_sync(FULL, xv, pcb >> 1);
-                    if (f) {
-                        const uint32_t nf = F.p - f;
-                        x0 = fmod64(x0 + (uint64_t)nf * basis[b][2 * lane], F);
-                        x1 = fmod64(x1 + (uint64_t)nf * basis[b][2 * lane + 1], F);
-                        a0 = fmod64(a0 + (uint64_t)nf * Tm[b][2 * lane], F);
-                        a1 = fmod64(a1 + (uint64_t)nf * Tm[b][2 * lane + 1], F);
-                    }
-                }
-                unsigned nzm = __ballot_sync(FULL, (x0 | x1) != 0);
-                if (!nzm) continue;                                   // in the span: dependent
-                const int src = __ffs(nzm) - 1;
-                uint32_t first0 = __shfl_sync(FULL, x0, src);
-                uint32_t first1 = __shfl_sync(FULL, x1, src);
-                const uint32_t c = first0 ? 2 * src : 2 * src + 1;
-                const uint32_t inv = finv(first0 ? first0 : first1, F);
-                x0 = fmul(x0, inv, F); x1 = fmul(x1, inv, F);
-                a0 = fmul(a0, inv, F); a1 = fmul(a1, inv, F);
-                for (uint32_t b = 0; b < nb; b++) {
-                    const uint32_t g = basis[b][c];
-                    __syncwarp();
-                    if (g) {
-                        const uint32_t ng = F.p - g;
-                        basis[b][2 * lane] = fmod64(basis[b][2 * lane] + (uint64_t)ng * x0, F);
-                        basis[b][2 * lane + 1] = fmod64(basis[b][2 * lane + 1] + (uint64_t)ng * x1, F);
-                        Tm[b][2 * lane] = fmod64(Tm[b][2 * lane] + (uint64_t)ng * a0, F);
-                        Tm[b][2 * lane + 1] = fmod64(Tm[b][2 * lane + 1] + (uint64_t)ng * a1, F);
-                    }
-                    __syncwarp();
-                }
-                basis[nb][2 * lane] = x0; basis[nb][2 * lane + 1] = x1;
-                Tm[nb][2 * lane] = a0; Tm[nb][2 * lane + 1] = a1;
-                if (lane == 0) { bpc[nb] = c; bsel[nb] = rr; }
-                nb++;
-                __syncwarp();
+        const int ncand = s_ncand;
+        pos = s_next;
+        if (ncand == 0) continue;
+        // (2) load the candidates' panel slices
+        for (int idx = tid; idx < ncand * PK; idx += 1024) {
+            const int ci = idx / PK, k = idx % PK;
+            X[PK + ci][k] = k < width ? D[(size_t)crow[ci] * ldD + c0 + k] : 0;
+            A[PK + ci][k] = 0;
+        }
+        if (tid < ncand) selfc[tid] = 1;
+        __syncthreads();
+        // (3) reduce the chunk by the current basis (RREF, so each factor is the
+        //     candidate's original entry at the basis pivot column)
+        if (nb > 0) {
+            // snapshot of the factors, then 8-column items (u64 delayed reduction)
+            for (int idx = tid; idx < ncand * (int)nb; idx += 1024) {
+                const int ci = idx / (int)nb, b = idx % (int)nb;
+                FS[ci][b] = X[PK + ci][bpc[b]];
             }
-            if (lane == 0) s_nb = nb;
+            __syncthreads();
+            for (int item = tid; item < ncand * (PK / 8); item += 1024) {
+                const int ci = item / (PK / 8), g8 = item % (PK / 8);
+                uint64_t ax[8], aa[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) { ax[u] = X[PK + ci][g8 * 8 + u]; aa[u] = 0; }
+                for (uint32_t b = 0; b < nb; b++) {
+                    const uint32_t f = FS[ci][b];
+                    if (!f) continue;
+                    const uint64_t nf = p - f;
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        ax[u] += nf * X[b][g8 * 8 + u];
+                        aa[u] += nf * A[b][g8 * 8 + u];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    X[PK + ci][g8 * 8 + u] = (uint16_t)fmod64(ax[u], F);
+                    A[PK + ci][g8 * 8 + u] = (uint16_t)fmod64(aa[u], F);
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        if (s_nb >= PK) break;
+        // (4) integrate the chunk row by row
+        for (int ci = 0; ci < ncand && nb < (uint32_t)PK; ci++) {
+            const uint16_t *cx = X[PK + ci];
+            bool nz = false;
+#pragma unroll
+            for (int u = 0; u < CPL; u++) nz |= cx[lane * CPL + u] != 0;
+            const unsigned nzm = __ballot_sync(FULL, nz);
+            if (!nzm) continue;                                  // dependent on the basis
+            const int src = __ffs(nzm) - 1;
+            uint32_t c = src * CPL;
+            while (cx[c] == 0) c++;
+            const int nrows = (int)nb + (ncand - ci - 1);
+            if (warp == 0) {
+                const uint32_t inv = invtab[cx[c]];
+#pragma unroll
+                for (int u = 0; u < CPL; u++) {
+                    const int k = lane * CPL + u;
+                    prx[k] = fmul(cx[k], inv, F);
+                    pra[k] = fmul(A[PK + ci][k], inv, F);
+                }
+                if (lane == 0) s_pself = fmul(selfc[ci], inv, F);
+                for (int rr = lane; rr < nrows; rr += 32) {
+                    const int row = rr < (int)nb ? rr : PK + ci + 1 + (rr - (int)nb);
+                    gbuf[rr] = X[row][c];
+                }
+            }
+            __syncthreads();
+            const uint32_t pself = s_pself;
+            for (int item = tid; item < nrows * G; item += 1024) {
+                const int rr = item / G, g = item % G;
+                const uint32_t gv = gbuf[rr];
+                if (!gv) continue;
+                const int row = rr < (int)nb ? rr : PK + ci + 1 + (rr - (int)nb);
+                const uint64_t ng = p - gv;
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const int k = g * 16 + u;
+                    X[row][k] = (uint16_t)fmod64(X[row][k] + ng * prx[k], F);
+                    uint64_t av = A[row][k] + ng * pra[k];
+                    if (k == (int)nb) av += ng * pself;
+                    A[row][k] = (uint16_t)fmod64(av, F);
+                }
+            }
+            if (tid < PK) {
+                X[nb][tid] = (uint16_t)prx[tid];
+                A[nb][tid] = (uint16_t)(tid < (int)nb ? pra[tid] : (tid == (int)nb ? pself : 0));
+            }
+            if (tid == 0) { bpc[nb] = c; bsel[nb] = crow[ci]; }
+            __syncthreads();
+            nb++;
+        }
     }
-    const uint32_t nb = s_nb;
+    __syncthreads();
     if (tid == 0) { ps->kp = nb; ps->nrows = 0; }
     for (int i = tid; i < PK * PK; i += blockDim.x) {
-        int b = i / PK, s = i % PK;
-        ps->T[i] = (b < (int)nb && s < (int)nb) ? (uint16_t)Tm[b][s] : 0;
+        const int b = i / PK, s = i % PK;
+        ps->T[i] = (b < (int)nb && s < (int)nb) ? A[b][s] : 0;
+    }
+    if (Tlo) {   // T as limb planes [KPT rows][KPT], zero padded (A operand of the Rn GEMM)
+        for (int i = tid; i < KPT * KPT; i += blockDim.x) {
+            const int b = i / KPT, s = i % KPT;
+            const uint16_t v = (b < (int)nb && s < (int)nb && b < PK && s < PK) ? A[b][s] : 0;
+            Tlo[i] = (uint8_t)(v & 0xff);
+            Thi[i] = (uint8_t)(v >> 8);
+        }
     }
     if (tid < (int)nb) {
         ps->sel[tid] = bsel[tid];
@@ -141,32 +234,68 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
     }
 }
 
-// F[i][b] = D[i][pc_b] for rows not selected in this panel; row list of the
-// rows with a nonzero coefficient.  One thread per row.
+// F[i][b] = D[i][pc_b] for rows not selected in this panel, compacted to the
+// list of rows with a nonzero coefficient.  INT engine: Fc[i][PK] u16 by row;
+// TC engine: limb planes by slot, zero padded to KPT.
+template <int PK, bool TC>
 __global__ void k_gather(int64_t mN, int64_t c0, const uint16_t *__restrict__ D, int64_t ldD,
-                         const uint32_t *__restrict__ rowpiv, PanelState *__restrict__ ps,
-                         uint16_t *__restrict__ Fc, uint32_t *__restrict__ rows)
+                         const uint32_t *__restrict__ rowpiv, PanelState<PK> *__restrict__ ps,
+                         uint16_t *__restrict__ Fc, uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi,
+                         uint32_t *__restrict__ rows)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t kp = ps->kp;
     if (i >= mN || kp == 0) return;
     const uint32_t rp = rowpiv[i];
     if (rp != GBLA_NONE && rp >= (uint64_t)c0) return;   // selected now: becomes Rn
+    const uint16_t *drow = D + (size_t)i * ldD;
     bool nz = false;
-    for (uint32_t b = 0; b < kp; b++) {
-        uint16_t v = D[(size_t)i * ldD + ps->pc[b]];
-        Fc[(size_t)i * PK + b] = v;
-        nz |= v != 0;
-    }
-    if (nz) {
-        uint32_t slot = atomicAdd(&ps->nrows, 1u);
-        rows[slot] = (uint32_t)i;
+    for (uint32_t b = 0; b < kp; b++) nz |= drow[ps->pc[b]] != 0;
+    if (!nz) return;
+    const uint32_t slot = atomicAdd(&ps->nrows, 1u);
+    rows[slot] = (uint32_t)i;
+    if (TC) {
+        for (uint32_t b = 0; b < KPT; b += 16) {
+            uint8_t lo[16], hi[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint16_t v = b + u < kp ? drow[ps->pc[b + u]] : 0;
+                lo[u] = (uint8_t)(v & 0xff);
+                hi[u] = (uint8_t)(v >> 8);
+            }
+            *reinterpret_cast<uint4 *>(Flo + (size_t)slot * KPT + b) = *reinterpret_cast<uint4 *>(lo);
+            *reinterpret_cast<uint4 *>(Fhi + (size_t)slot * KPT + b) = *reinterpret_cast<uint4 *>(hi);
+        }
+    } else {
+        for (uint32_t b = 0; b < kp; b++) Fc[(size_t)i * PK + b] = drow[ps->pc[b]];
     }
 }
 
-// Rn[b][x] = sum_s T[b][s] * D[S_s][c0 + x]
+// TC engine: transposed limb planes of D[S, c0:]: Bt[x][s] = D[sel_s][c0 + x]
+__global__ void k_gather_st(int64_t nN, int64_t c0, const uint16_t *__restrict__ D, int64_t ldD,
+                            const PanelState<KPT> *__restrict__ ps, uint8_t *__restrict__ Blo,
+                            uint8_t *__restrict__ Bhi)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c0 + x >= nN) return;
+    const uint32_t kp = ps->kp;
+    for (uint32_t s = 0; s < KPT; s += 16) {
+        uint8_t lo[16], hi[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const uint16_t v = (s + u < kp) ? D[(size_t)ps->sel[s + u] * ldD + c0 + x] : 0;
+            lo[u] = (uint8_t)(v & 0xff);
+            hi[u] = (uint8_t)(v >> 8);
+        }
+        *reinterpret_cast<uint4 *>(Blo + (size_t)x * KPT + s) = *reinterpret_cast<uint4 *>(lo);
+        *reinterpret_cast<uint4 *>(Bhi + (size_t)x * KPT + s) = *reinterpret_cast<uint4 *>(hi);
+    }
+}
+
+// INT engine: Rn[b][x] = sum_s T[b][s] * D[S_s][c0 + x]
+template <int PK>
 __global__ void k_rnew(int64_t nN, int64_t c0, Field F, const uint16_t *__restrict__ D, int64_t ldD,
-                       const PanelState *__restrict__ ps, uint16_t *__restrict__ Rn, int64_t ldR)
+                       const PanelState<PK> *__restrict__ ps, uint16_t *__restrict__ Rn, int64_t ldR)
 {
     const uint32_t kp = ps->kp;
     const uint32_t b = blockIdx.y;
@@ -174,20 +303,20 @@ __global__ void k_rnew(int64_t nN, int64_t c0, Field F, const uint16_t *__restri
     if (b >= kp || c0 + x >= nN) return;
     uint64_t acc = 0;
     for (uint32_t s = 0; s < kp; s++) {
-        uint32_t t = ps->T[b * PK + s];
+        const uint32_t t = ps->T[b * PK + s];
         if (t) acc += (uint64_t)t * D[(size_t)ps->sel[s] * ldD + c0 + x];
     }
     Rn[(size_t)b * ldR + x] = (uint16_t)fmod64(acc, F);
 }
 
-// INT-pipe trailing update: 32 listed rows x 256 columns per CTA.
+// INT-pipe trailing update: 32 listed rows x 256 columns per CTA (PK = 64).
 __global__ void __launch_bounds__(256) k_trailing_int(int64_t nN, int64_t c0, Field F, uint16_t *__restrict__ D,
-                                                      int64_t ldD, const PanelState *__restrict__ ps,
+                                                      int64_t ldD, const PanelState<64> *__restrict__ ps,
                                                       const uint16_t *__restrict__ Fc,
                                                       const uint32_t *__restrict__ rows,
-                                                      const uint16_t *__restrict__ Rn, int64_t ldR,
-                                                      unsigned long long *__restrict__ dense_ops)
+                                                      const uint16_t *__restrict__ Rn, int64_t ldR)
 {
+    constexpr int PK = 64;
     __shared__ uint32_t sF[32][PK + 1];
     __shared__ uint16_t sR[PK][256];
     const uint32_t kp = ps->kp, nr = ps->nrows;
@@ -196,14 +325,12 @@ __global__ void __launch_bounds__(256) k_trailing_int(int64_t nN, int64_t c0, Fi
     const int64_t x0 = (int64_t)blockIdx.x * 256;
     if (kp == 0 || row0 >= nr || x0 >= width) return;
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0)
-        atomicAdd(dense_ops, (unsigned long long)nr * kp * width + (unsigned long long)kp * kp * width);
     for (int i = tid; i < 32 * PK; i += 256) {
-        int rr = i / PK, b = i % PK;
+        const int rr = i / PK, b = i % PK;
         sF[rr][b] = (row0 + rr < nr && b < (int)kp) ? Fc[(size_t)rows[row0 + rr] * PK + b] : 0;
     }
     for (int i = tid; i < PK * 256; i += 256) {
-        int b = i / 256, x = i % 256;
+        const int b = i / 256, x = i % 256;
         sR[b][x] = (b < (int)kp && x0 + x < width) ? Rn[(size_t)b * ldR + x0 + x] : 0;
     }
     __syncthreads();
@@ -232,17 +359,17 @@ __global__ void __launch_bounds__(256) k_trailing_int(int64_t nN, int64_t c0, Fi
         for (int u = 0; u < 8; u++) {
             const int64_t x = lane + 32 * u;
             if (x0 + x < width) {
-                uint32_t s = fmod64(acc[a][u], F);
-                uint32_t d = drow[x];
-                uint32_t v = d >= s ? d - s : d + F.p - s;
-                drow[x] = (uint16_t)v;
+                const uint32_t s = fmod64(acc[a][u], F);
+                const uint32_t d = drow[x];
+                drow[x] = (uint16_t)(d >= s ? d - s : d + F.p - s);
             }
         }
     }
 }
 
+template <int PK>
 __global__ void k_commit(int64_t nN, int64_t c0, uint16_t *__restrict__ D, int64_t ldD,
-                         const PanelState *__restrict__ ps, const uint16_t *__restrict__ Rn, int64_t ldR)
+                         const PanelState<PK> *__restrict__ ps, const uint16_t *__restrict__ Rn, int64_t ldR)
 {
     const uint32_t b = blockIdx.y;
     const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -250,17 +377,23 @@ __global__ void k_commit(int64_t nN, int64_t c0, uint16_t *__restrict__ D, int64
     D[(size_t)ps->sel[b] * ldD + c0 + x] = Rn[(size_t)b * ldR + x];
 }
 
-__global__ void k_reset_rows(PanelState *ps) { ps->nrows = 0; }
+// algorithmic dense modMACs of the panel: nrows*kp*width + kp*kp*width
+template <int PK>
+__global__ void k_count(int64_t width, const PanelState<PK> *__restrict__ ps, unsigned long long *__restrict__ ops)
+{
+    const unsigned long long kp = ps->kp, nr = ps->nrows;
+    *ops += nr * kp * (unsigned long long)width + kp * kp * (unsigned long long)width;
+}
 
 // K13: R rows sorted by pivot column.
 __global__ void k_mark(int64_t mN, const uint32_t *__restrict__ rowpiv, uint32_t *__restrict__ colrow)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < mN && rowpiv[i] != GBLA_NONE) colrow[rowpiv[i]] = (uint32_t)i;
 }
 __global__ void k_colflag(int64_t nN, const uint32_t *__restrict__ colrow, uint32_t *__restrict__ flag)
 {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c < nN) flag[c] = colrow[c] != GBLA_NONE;
     else if (c == nN) flag[c] = 0;
 }
@@ -278,45 +411,116 @@ __global__ void k_compact(int64_t nN, int64_t cbase, const uint32_t *__restrict_
         R[(size_t)k * ldR + x] = D[(size_t)r * ldD + x];
 }
 
+template <int PK>
+gbla_status set_panel_smem()
+{
+    static bool done = false;
+    if (!done) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<PK>()));
+        done = true;
+    }
+    return GBLA_OK;
+}
+
+gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab)
+{
+    constexpr int PK = 64;
+    cudaStream_t st = h->stream;
+    const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
+    uint32_t *rows;
+    uint16_t *Fc, *Rn;
+    PanelState<PK> *ps;
+    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 1) * PK, &Fc));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
+    GBLA_TRY(dalloc(h, sizeof(PanelState<PK>), (void **)&ps));
+    GBLA_TRY(set_panel_smem<PK>());
+    for (int64_t c0 = 0; c0 < nN; c0 += PK) {
+        const int64_t width = nN - c0;
+        k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, nullptr, nullptr,
+                                                        invtab);
+        k_gather<PK, false><<<grid_for(mN, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, Fc, nullptr, nullptr,
+                                                              rows);
+        k_rnew<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps, Rn, ldR);
+        k_trailing_int<<<dim3(grid_for(width, 256), grid_for(mN, 32)), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps,
+                                                                                      Fc, rows, Rn, ldR);
+        k_commit<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->D, ldD, ps, Rn, ldR);
+        k_count<PK><<<1, 1, 0, st>>>(width, ps, dops);
+        note_launch(6);
+        GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    return GBLA_OK;
+}
+
+gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab)
+{
+    constexpr int PK = KPT;
+    cudaStream_t st = h->stream;
+    const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
+    const int64_t npad = (nN + 63) / 64 * 64 + 64;
+    uint32_t *rows;
+    uint16_t *Rn;
+    uint8_t *Flo, *Fhi, *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
+    PanelState<PK> *ps;
+    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * KPT, &Flo));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * KPT, &Fhi));
+    GBLA_TRY(dalloc_t(h, (size_t)KPT * KPT, &Tlo));
+    GBLA_TRY(dalloc_t(h, (size_t)KPT * KPT, &Thi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Blo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Bhi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Rtlo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Rthi));
+    GBLA_TRY(dalloc_t(h, (size_t)KPT * ldR, &Rn));
+    GBLA_TRY(dalloc(h, sizeof(PanelState<PK>), (void **)&ps));
+    GBLA_TRY(set_panel_smem<PK>());
+    for (int64_t c0 = 0; c0 < nN; c0 += PK) {
+        const int64_t width = nN - c0;
+        k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, Tlo, Thi, invtab);
+        k_gather<PK, true><<<grid_for(mN, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, nullptr, Flo, Fhi,
+                                                             rows);
+        k_gather_st<<<grid_for(width, 128), 128, 0, st>>>(nN, c0, h->D, ldD, ps, Blo, Bhi);
+        note_launch(3);
+        // Rn = T * D[S, c0:]  (plus its transposed limb planes)
+        GBLA_TRY(modgemm_tc_store(st, width, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi));
+        // D[rows, c0:] -= F * Rn
+        GBLA_TRY(modgemm_tc_sub(st, mN, &ps->nrows, width, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D + c0, ldD));
+        k_commit<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->D, ldD, ps, Rn, ldR);
+        k_count<PK><<<1, 1, 0, st>>>(width, ps, dops);
+        note_launch(2);
+        GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    return GBLA_OK;
+}
+
 }  // namespace
 
 gbla_status echelon_impl(gbla_mat h, uint32_t flags)
 {
     cudaStream_t st = h->stream;
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD;
-    (void)flags;
-    uint32_t *rowpiv, *rows, *colrow, *cflag, *cidx;
-    uint16_t *Fc, *Rn;
-    PanelState *ps;
+    uint32_t *rowpiv, *colrow, *cflag, *cidx;
+    uint16_t *invtab;
     unsigned long long *dops;
-    const int64_t ldR = ldD;
     GBLA_TRY(dalloc_t(h, mN + 1, &rowpiv));
-    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
-    GBLA_TRY(dalloc_t(h, (size_t)(mN + 1) * PK, &Fc));
-    GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
-    GBLA_TRY(dalloc(h, sizeof(PanelState), (void **)&ps));
     GBLA_TRY(dalloc_t(h, 1, &dops));
+    GBLA_TRY(dalloc_t(h, 65536, &invtab));
     GBLA_CUDA_TRY(cudaMemsetAsync(rowpiv, 0xff, (mN + 1) * 4, st));
     GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 8, st));
+    k_invtab<<<grid_for(h->p, 256), 256, 0, st>>>(h->F, invtab);
+    note_launch();
     if (mN > 0 && nN > 0) {
-        for (int64_t c0 = 0; c0 < nN; c0 += PK) {
-            const int64_t width = nN - c0;
-            k_panel<<<1, 1024, 0, st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps); note_launch();
-            k_gather<<<grid_for(mN, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, Fc, rows); note_launch();
-            k_rnew<<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps, Rn, ldR); note_launch();
-            dim3 tg(grid_for(width, 256), grid_for(mN, 32));
-            k_trailing_int<<<tg, 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps, Fc, rows, Rn, ldR, dops); note_launch();
-            k_commit<<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->D, ldD, ps, Rn, ldR); note_launch();
-            GBLA_CUDA_TRY(cudaGetLastError());
-        }
+        if (flags & GBLA_DENSE_INT) GBLA_TRY(panels_int(h, rowpiv, dops, invtab));
+        else GBLA_TRY(panels_tc(h, rowpiv, dops, invtab));
     }
     // K13: compaction
     GBLA_TRY(dalloc_t(h, nN + 1, &colrow));
     GBLA_TRY(dalloc_t(h, nN + 1, &cflag));
     GBLA_TRY(dalloc_t(h, nN + 1, &cidx));
     GBLA_CUDA_TRY(cudaMemsetAsync(colrow, 0xff, (nN + 1) * 4, st));
-    k_mark<<<grid_for(mN, 256), 256, 0, st>>>(mN, rowpiv, colrow); note_launch();
-    k_colflag<<<grid_for(nN + 1, 256), 256, 0, st>>>(nN, colrow, cflag); note_launch();
+    k_mark<<<grid_for(mN, 256), 256, 0, st>>>(mN, rowpiv, colrow);
+    k_colflag<<<grid_for(nN + 1, 256), 256, 0, st>>>(nN, colrow, cflag);
+    note_launch(2);
     {
         size_t tb = 0;
         GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, cflag, cidx, (int)(nN + 1), st));
@@ -337,9 +541,10 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     if (rk > 0 && nN > 0) {
         const unsigned gx = grid_for(nN, 256) < 8 ? grid_for(nN, 256) : 8;
         for (int64_t cb = 0; cb < nN; cb += 65535) {   // gridDim.y <= 65535
-            int64_t cnt = nN - cb < 65535 ? nN - cb : 65535;
+            const int64_t cnt = nN - cb < 65535 ? nN - cb : 65535;
             k_compact<<<dim3(gx, (unsigned)cnt), 256, 0, st>>>(nN, cb, colrow, cidx, h->D, ldD, h->R, h->ldR,
-                                                               h->pivcol); note_launch();
+                                                               h->pivcol);
+            note_launch();
         }
         GBLA_CUDA_TRY(cudaGetLastError());
     }

@@ -141,7 +141,11 @@ struct gbla_mat_s {
 
     // call-order state
     bool did_reduce_B = false, did_cprime = false, did_update = false, did_fused = false;
+    bool have_xt = false;              // C' held as tensor-core tiles (sparse_tc.cu)
     float phase_ms[5] = {0, 0, 0, 0, 0};
+
+    // tensor-core sparse path: dense band tiles of A|B, X tiles (sparse_tc.cu)
+    struct BandTiles *bt = nullptr;
 
     std::vector<Alloc> allocs;
 };
@@ -163,6 +167,10 @@ gbla_status update_d_from_x_int(gbla_mat h);
 gbla_status reduce_b_int(gbla_mat h);
 gbla_status update_d_from_bp_int(gbla_mat h);
 gbla_status echelon_impl(gbla_mat h, uint32_t flags);
+gbla_status reduce_c_tc(gbla_mat h, bool want_x16);
+gbla_status update_d_tc(gbla_mat h);
+void band_free(gbla_mat h);
+gbla_status ensure_x(gbla_mat h);
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
 
 static inline unsigned grid_for(int64_t work, int per_block) {

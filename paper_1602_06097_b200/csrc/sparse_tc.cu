@@ -1,0 +1,604 @@
+// sparse_tc.cu -- the sparse triangular phase on the tensor cores.
+//
+// C' = C A^-1 and D_new = D - C' B, the 4-step variant of the new order
+// ("carry out the reduction of C by A, but store the
+// corresponding coefficients", then "reduce D by B using the coefficients
+// stored in C'"), blocked by 128 x 128 tiles in sigma order:
+//
+//   band tiles   [A|B] rows in blocks I of 128 pivots; every 128 x 128 tile
+//                of the band (A tiles J in [I, amax(I)], B tiles K in
+//                [bmin(I), bmax(I)]) is stored DENSE as two u8 limb planes in
+//                the tcgen05 K-major core-matrix layout, transposed (K = the
+//                pivot index i, MN = the column): the B operand of X_I * A_IJ
+//                and X_I * B_IK.  Padded pivots npiv..NB*128-1 are identity.
+//   diag inverse inv(A_JJ) (unit upper triangular) per block, same layout.
+//   K5' sweep    one CTA per tile T of 128 targets (sorted by lead), J
+//                ascending from the tile's first lead block:
+//                  Y   = C_J[T] - sum_{I<J, A_IJ != 0} X_I[T] A_IJ   (GEMM)
+//                  X_J = Y inv(A_JJ)                                 (GEMM)
+//                which is forward substitution x_t A = c_t (Alg 2) done a
+//                block of 128 pivots at a time.  X_J[T] is stored as limb
+//                planes (A operand of later steps and of the update).
+//   K7' update   D[T, K] -= sum_I X_I[T] B_IK   (output-stationary GEMM)
+// Every GEMM: tcgen05.mma kind::i8, M = N = 128, K = 128 per tile pair,
+// three s32 TMEM accumulators HH | X | LL (exactness: tc_gemm.cu header),
+// operands staged by cp.async.bulk (TMA bulk copies) in a 2-stage mbarrier
+// pipeline, one elected thread issuing.  The results are the same exact
+// residues as Alg 2 (X = C A^-1 is unique), bit for bit.
+#include <vector>
+
+#include "internal.cuh"
+#include "tc.cuh"
+
+struct BandTiles {
+    int64_t NB = 0, NNB = 0, ntiles = 0;
+    int64_t nA = 0, nB = 0;
+    uint8_t *tilesA = nullptr, *tilesB = nullptr, *invT = nullptr, *Xt = nullptr;
+    uint64_t *offA = nullptr, *offB = nullptr;
+    uint32_t *amax = nullptr, *bmin = nullptr, *bmax = nullptr;
+    uint32_t *jl_ptr = nullptr, *jl_idx = nullptr, *kl_ptr = nullptr, *kl_idx = nullptr;
+    unsigned long long *ops = nullptr;   // [2] A-part, B-part modMACs (Alg 2 count)
+    bool swept = false;
+};
+
+namespace {
+
+constexpr uint32_t TB = 32768, PB = 16384;
+
+__global__ void k_band_ranges(int64_t npiv, const uint64_t *__restrict__ ab_ptr, const uint32_t *__restrict__ ab_col,
+                              const uint32_t *__restrict__ ab_np, uint32_t *__restrict__ amax,
+                              uint32_t *__restrict__ bmin, uint32_t *__restrict__ bmax)
+{
+    __shared__ uint32_t s_am, s_bl, s_bh;
+    const uint32_t I = blockIdx.x;
+    if (threadIdx.x == 0) { s_am = I; s_bl = 0xffffffffu; s_bh = 0; }
+    __syncthreads();
+    const int64_t i = (int64_t)I * 128 + threadIdx.x;
+    if (i < npiv) {
+        const uint64_t s = ab_ptr[i], e = ab_ptr[i + 1];
+        const uint32_t np = ab_np[i];
+        atomicMax(&s_am, ab_col[s + np - 1] / 128u);
+        if (e > s + np) {
+            atomicMin(&s_bl, (uint32_t)((ab_col[s + np] - npiv) / 128));
+            atomicMax(&s_bh, (uint32_t)((ab_col[e - 1] - npiv) / 128));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { amax[I] = s_am; bmin[I] = s_bl; bmax[I] = s_bh; }
+}
+
+// scatter the normalized pivot rows into the band tiles (warp per row)
+__global__ void k_band_fill(int64_t npiv, const uint64_t *__restrict__ ab_ptr, const uint32_t *__restrict__ ab_col,
+                            const uint16_t *__restrict__ ab_val, const uint64_t *__restrict__ offA,
+                            const uint64_t *__restrict__ offB, const uint32_t *__restrict__ bmin,
+                            uint8_t *__restrict__ tilesA, uint8_t *__restrict__ tilesB)
+{
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= npiv) return;
+    const uint32_t I = (uint32_t)(i / 128), k = (uint32_t)(i % 128);
+    for (uint64_t q = ab_ptr[i] + lane; q < ab_ptr[i + 1]; q += 32) {
+        const uint32_t c = ab_col[q];
+        const uint16_t v = ab_val[q];
+        uint8_t *tile;
+        uint32_t r;
+        if (c < (uint64_t)npiv) {
+            tile = tilesA + (offA[I] + (c / 128u - I)) * (uint64_t)TB;
+            r = c % 128u;
+        } else {
+            const uint32_t nc = c - (uint32_t)npiv;
+            tile = tilesB + (offB[I] + (nc / 128u - bmin[I])) * (uint64_t)TB;
+            r = nc % 128u;
+        }
+        const uint32_t o = tc::toff(r, k);
+        tile[o] = (uint8_t)(v & 0xff);
+        tile[PB + o] = (uint8_t)(v >> 8);
+    }
+}
+
+// padded pivots are identity rows
+__global__ void k_band_pad(int64_t npiv, int64_t NB, const uint64_t *__restrict__ offA, uint8_t *__restrict__ tilesA)
+{
+    const int64_t i = npiv + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= NB * 128) return;
+    const uint32_t I = (uint32_t)(i / 128), k = (uint32_t)(i % 128);
+    tilesA[offA[I] * (uint64_t)TB + tc::toff(k, k)] = 1;
+}
+
+constexpr int DIAG_SMEM = 2 * 128 * 129 * 2;
+
+// inv(A_JJ), unit upper triangular, as a B operand tile (K = i, MN = j)
+__global__ void __launch_bounds__(128) k_diag_inv(Field F, const uint64_t *__restrict__ offA,
+                                                  const uint8_t *__restrict__ tilesA, uint8_t *__restrict__ invT)
+{
+    extern __shared__ uint16_t dyn_inv[];
+    uint16_t(*U)[129] = reinterpret_cast<uint16_t(*)[129]>(dyn_inv);
+    uint16_t(*Y)[129] = reinterpret_cast<uint16_t(*)[129]>(dyn_inv + 128 * 129);
+    const uint32_t J = blockIdx.x, j = threadIdx.x;
+    const uint8_t *t = tilesA + offA[J] * (uint64_t)TB;     // tile (J, J) is first in row block J
+    for (uint32_t idx = j; idx < 128 * 128; idx += 128) {
+        const uint32_t r = idx / 128, kk = idx % 128;       // element A[kk][r]
+        const uint32_t o = tc::toff(r, kk);
+        U[kk][r] = (uint16_t)(t[o] | (t[PB + o] << 8));
+    }
+    __syncthreads();
+    for (uint32_t i = 0; i < 128; i++) Y[i][j] = (i == j) ? 1 : 0;
+    for (int i = (int)j - 1; i >= 0; i--) {
+        uint64_t acc = 0;
+        for (uint32_t k = i + 1; k <= j; k++) acc += (uint64_t)U[i][k] * Y[k][j];
+        Y[i][j] = (uint16_t)fneg(fmod64(acc, F), F);
+    }
+    uint8_t *o = invT + (uint64_t)J * TB;
+    for (uint32_t i = 0; i < 128; i++) {
+        const uint16_t v = Y[i][j];
+        const uint32_t off = tc::toff(j, i);
+        o[off] = (uint8_t)(v & 0xff);
+        o[PB + off] = (uint8_t)(v >> 8);
+    }
+}
+
+// 16 MMAs: D(HH|X|LL) (+)= A(lo,hi) x B(lo,hi), K = 128, M = N = 128
+__device__ __forceinline__ void issue_mmas(uint32_t tbase, uint32_t sA, uint32_t sB, bool acc_in)
+{
+    const uint32_t idesc = tc::idesc_u8(128, 128);
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        const uint32_t off = s * 4096;
+        const uint64_t dAl = tc::desc_kmajor(sA + off, 2048, 128), dAh = tc::desc_kmajor(sA + PB + off, 2048, 128);
+        const uint64_t dBl = tc::desc_kmajor(sB + off, 2048, 128), dBh = tc::desc_kmajor(sB + PB + off, 2048, 128);
+        const uint32_t acc = (acc_in || s > 0) ? 1u : 0u;
+        tc::mma_i8(tbase + 0, dAh, dBh, idesc, acc);
+        tc::mma_i8(tbase + 128, dAh, dBl, idesc, acc);
+        tc::mma_i8(tbase + 128, dAl, dBh, idesc, 1u);
+        tc::mma_i8(tbase + 256, dAl, dBl, idesc, acc);
+    }
+}
+
+__device__ __forceinline__ void read_S(uint32_t lane_addr, int c, uint64_t (&S)[16])
+{
+    uint32_t hh[16], xx[16], ll[16];
+    __syncwarp();
+    tc::tmem_ld16(lane_addr + c, hh);
+    tc::tmem_ld16(lane_addr + 128 + c, xx);
+    tc::tmem_ld16(lane_addr + 256 + c, ll);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; j++) S[j] = ((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j];
+}
+
+struct SweepArgs {
+    int64_t mN, npiv, NB;
+    Field F;
+    const uint32_t *order, *tlead;
+    const uint64_t *cd_ptr;
+    const uint32_t *cd_col;
+    const uint16_t *cd_val;
+    const uint32_t *cd_np;
+    const uint8_t *tilesA, *invT;
+    const uint64_t *offA;
+    const uint32_t *jl_ptr, *jl_idx;
+    uint8_t *Xt;
+    uint16_t *X16;
+    int64_t ldX;
+    const uint32_t *ab_w, *ab_np;
+    unsigned long long *ops;
+};
+
+constexpr int SWEEP_SMEM = 2 * 65536 + 2 * TB;
+
+__global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *stg = smem;
+    uint8_t *Ys = smem + 2 * 65536;
+    uint8_t *INV = Ys + TB;
+    __shared__ uint64_t full[2], mdone[2], accbar, invbar;
+    __shared__ uint32_t tmem_s;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t T = blockIdx.x, first = T * 128;
+    const uint32_t lead0 = a.tlead[a.order[first]];
+    if (lead0 >= (uint64_t)a.npiv) return;                     // tile of zero rows: X = 0
+    const int64_t Jmin = lead0 / 128;
+    const int64_t slot = first + tid;
+    const bool live = slot < a.mN;
+    const uint32_t t = live ? a.order[slot] : 0;
+    uint64_t q = live ? a.cd_ptr[t] : 0;
+    const uint64_t qe = live ? a.cd_ptr[t] + a.cd_np[t] : 0;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
+    if (tid == 0) {
+        tc::mbar_init(&full[0], 1); tc::mbar_init(&full[1], 1);
+        tc::mbar_init(&mdone[0], 1); tc::mbar_init(&mdone[1], 1);
+        tc::mbar_init(&accbar, 1); tc::mbar_init(&invbar, 1);
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tmem_s;
+    const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
+    uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0}, ph_acc = 0, ph_inv = 0;
+    unsigned long long opsA = 0, opsB = 0;
+    const uint32_t sStg = tc::smem_u32(stg), sY = tc::smem_u32(Ys), sINV = tc::smem_u32(INV);
+    uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
+    const uint32_t p = a.F.p;
+
+    for (int64_t J = Jmin; J < a.NB; J++) {
+        const uint32_t l1 = a.jl_ptr[J + 1];
+        uint32_t lb = a.jl_ptr[J];
+        while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
+        const uint32_t nI = l1 - lb;
+        if (tid == 0) {
+            tc::mbar_expect_tx(&invbar, TB);
+            tc::bulk_g2s(INV, a.invT + (size_t)J * TB, TB, &invbar);
+            auto load = [&](uint32_t it) {
+                const uint32_t I = a.jl_idx[lb + it];
+                const int s = it & 1;
+                tc::mbar_expect_tx(&full[s], 2 * TB);
+                tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
+                tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
+            };
+            if (nI > 0) load(0);
+            if (nI > 1) load(1);
+            for (uint32_t it = 0; it < nI; it++) {
+                const int s = it & 1;
+                tc::mbar_wait(&full[s], ph_full[s]);
+                ph_full[s] ^= 1;
+                tc::fence_after();
+                issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > 0);
+                if (it + 2 < nI) {
+                    tc::commit(&mdone[s]);
+                    tc::mbar_wait(&mdone[s], ph_md[s]);
+                    ph_md[s] ^= 1;
+                    load(it + 2);
+                }
+            }
+            if (nI > 0) tc::commit(&accbar);
+        }
+        if (nI > 0) {
+            tc::mbar_wait(&accbar, ph_acc);
+            ph_acc ^= 1;
+            tc::fence_after();
+        }
+        // epilogue 1: Y = C_J - S  -> shared memory (A operand of stage 2)
+        const uint32_t jbase = (uint32_t)J * 128;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 16) {
+            uint64_t S[16];
+            if (nI > 0) {
+                read_S(lane_addr, c, S);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; j++) S[j] = 0;
+            }
+            uint8_t lo[16], hi[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t y = fneg(fmod64(S[j], a.F), a.F);
+                lo[j] = (uint8_t)(y & 0xff);
+                hi[j] = (uint8_t)(y >> 8);
+            }
+            const uint32_t o = tc::toff(tid, c);
+            *reinterpret_cast<uint4 *>(Ys + o) = *reinterpret_cast<uint4 *>(lo);
+            *reinterpret_cast<uint4 *>(Ys + PB + o) = *reinterpret_cast<uint4 *>(hi);
+            while (q < qe) {
+                const uint32_t col = a.cd_col[q];
+                if (col >= jbase + c + 16) break;
+                const uint32_t oo = tc::toff(tid, col - jbase);
+                uint32_t y = Ys[oo] | (Ys[PB + oo] << 8);
+                y += a.cd_val[q];
+                if (y >= p) y -= p;
+                Ys[oo] = (uint8_t)(y & 0xff);
+                Ys[PB + oo] = (uint8_t)(y >> 8);
+                q++;
+            }
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        // stage 2: X_J = Y inv(A_JJ)
+        if (tid == 0) {
+            tc::mbar_wait(&invbar, ph_inv);
+            tc::fence_after();
+            issue_mmas(tbase, sY, sINV, false);
+            tc::commit(&accbar);
+        }
+        ph_inv ^= 1;
+        tc::mbar_wait(&accbar, ph_acc);
+        ph_acc ^= 1;
+        tc::fence_after();
+        // epilogue 2: X_J -> limb-plane tile (global) [+ C' u16], op counts
+        uint8_t *xt = Xrow + (size_t)J * TB;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 16) {
+            uint64_t S[16];
+            read_S(lane_addr, c, S);
+            uint8_t lo[16], hi[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t x = fmod64(S[j], a.F);
+                lo[j] = (uint8_t)(x & 0xff);
+                hi[j] = (uint8_t)(x >> 8);
+                const uint32_t jg = jbase + c + j;
+                if (live && jg < (uint64_t)a.npiv) {
+                    if (x) {
+                        opsA += a.ab_np[jg] - 1;
+                        opsB += a.ab_w[jg] - a.ab_np[jg];
+                    }
+                    if (a.X16) a.X16[(size_t)t * a.ldX + jg] = (uint16_t)x;
+                }
+            }
+            const uint32_t o = tc::toff(tid, c);
+            *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo);
+            *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi);
+        }
+        tc::fence_async_all();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    for (int o = 16; o; o >>= 1) {
+        opsA += __shfl_xor_sync(0xffffffffu, opsA, o);
+        opsB += __shfl_xor_sync(0xffffffffu, opsB, o);
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&a.ops[0], opsA);
+        atomicAdd(&a.ops[1], opsB);
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+struct UpdArgs {
+    int64_t mN, npiv, nN, NB;
+    Field F;
+    const uint32_t *order, *tlead;
+    const uint8_t *Xt, *tilesB;
+    const uint64_t *offB;
+    const uint32_t *bmin, *kl_ptr, *kl_idx;
+    uint16_t *D;
+    int64_t ldD;
+};
+
+constexpr int UPD_SMEM = 2 * 65536;
+
+__global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t full[2], mdone[2], accbar;
+    __shared__ uint32_t tmem_s;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t K = blockIdx.x, T = blockIdx.y, first = T * 128;
+    const uint32_t lead0 = a.tlead[a.order[first]];
+    if (lead0 >= (uint64_t)a.npiv) return;
+    const int64_t Jmin = lead0 / 128;
+    const uint32_t l1 = a.kl_ptr[K + 1];
+    uint32_t lb = a.kl_ptr[K];
+    while (lb < l1 && a.kl_idx[lb] < Jmin) lb++;
+    const uint32_t nI = l1 - lb;
+    if (nI == 0) return;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
+    if (tid == 0) {
+        tc::mbar_init(&full[0], 1); tc::mbar_init(&full[1], 1);
+        tc::mbar_init(&mdone[0], 1); tc::mbar_init(&mdone[1], 1);
+        tc::mbar_init(&accbar, 1);
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tmem_s;
+    const uint32_t sStg = tc::smem_u32(smem);
+    const uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
+    if (tid == 0) {
+        uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0};
+        auto load = [&](uint32_t it) {
+            const uint32_t I = a.kl_idx[lb + it];
+            const int s = it & 1;
+            tc::mbar_expect_tx(&full[s], 2 * TB);
+            tc::bulk_g2s(smem + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
+            tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + (a.offB[I] + (uint64_t)(K - a.bmin[I])) * TB, TB,
+                         &full[s]);
+        };
+        load(0);
+        if (nI > 1) load(1);
+        for (uint32_t it = 0; it < nI; it++) {
+            const int s = it & 1;
+            tc::mbar_wait(&full[s], ph_full[s]);
+            ph_full[s] ^= 1;
+            tc::fence_after();
+            issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > 0);
+            if (it + 2 < nI) {
+                tc::commit(&mdone[s]);
+                tc::mbar_wait(&mdone[s], ph_md[s]);
+                ph_md[s] ^= 1;
+                load(it + 2);
+            }
+        }
+        tc::commit(&accbar);
+    }
+    tc::mbar_wait(&accbar, 0);
+    tc::fence_after();
+    const int64_t slot = first + tid;
+    const bool live = slot < a.mN;
+    uint16_t *drow = live ? a.D + (size_t)a.order[slot] * a.ldD + K * 128 : nullptr;
+    const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
+    const uint32_t p = a.F.p;
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 16) {
+        uint64_t S[16];
+        read_S(lane_addr, c, S);
+        if (!live) continue;
+        uint4 v[2];
+        v[0] = *reinterpret_cast<const uint4 *>(drow + c);
+        v[1] = *reinterpret_cast<const uint4 *>(drow + c + 8);
+        uint16_t *d = reinterpret_cast<uint16_t *>(v);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const uint32_t s = fmod64(S[j], a.F);
+            const uint32_t x = d[j];
+            d[j] = (uint16_t)(x >= s ? x - s : x + p - s);
+        }
+        *reinterpret_cast<uint4 *>(drow + c) = v[0];
+        *reinterpret_cast<uint4 *>(drow + c + 8) = v[1];
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace
+
+void band_free(gbla_mat h)
+{
+    delete h->bt;
+    h->bt = nullptr;
+}
+
+static gbla_status band_build(gbla_mat h)
+{
+    if (h->bt) return GBLA_OK;
+    cudaStream_t st = h->stream;
+    BandTiles *bt = new BandTiles();
+    h->bt = bt;
+    const int64_t npiv = h->npiv, nN = h->nN;
+    bt->NB = (npiv + 127) / 128;
+    bt->NNB = (nN + 127) / 128;
+    bt->ntiles = (h->mN + 127) / 128;
+    const int64_t NB = bt->NB, NNB = bt->NNB;
+    GBLA_TRY(dalloc_t(h, 2, &bt->ops));
+    GBLA_CUDA_TRY(cudaMemsetAsync(bt->ops, 0, 16, st));
+    if (NB == 0) return GBLA_OK;
+    GBLA_TRY(dalloc_t(h, NB, &bt->amax));
+    GBLA_TRY(dalloc_t(h, NB, &bt->bmin));
+    GBLA_TRY(dalloc_t(h, NB, &bt->bmax));
+    k_band_ranges<<<(unsigned)NB, 128, 0, st>>>(npiv, h->ab_ptr, h->ab_col, h->ab_np, bt->amax, bt->bmin, bt->bmax);
+    note_launch();
+    std::vector<uint32_t> amax(NB), bmin(NB), bmax(NB);
+    GBLA_CUDA_TRY(cudaMemcpyAsync(amax.data(), bt->amax, NB * 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bmin.data(), bt->bmin, NB * 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bmax.data(), bt->bmax, NB * 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint64_t> offA(NB), offB(NB);
+    std::vector<std::vector<uint32_t>> jl(NB), kl(NNB > 0 ? NNB : 1);
+    uint64_t nA = 0, nB = 0;
+    for (int64_t I = 0; I < NB; I++) {
+        if (amax[I] >= NB) amax[I] = NB - 1;
+        offA[I] = nA;
+        nA += amax[I] - I + 1;
+        for (uint32_t J = I + 1; J <= amax[I]; J++) jl[J].push_back((uint32_t)I);
+        offB[I] = nB;
+        if (bmin[I] <= bmax[I] && bmin[I] != 0xffffffffu) {
+            nB += bmax[I] - bmin[I] + 1;
+            for (uint32_t K = bmin[I]; K <= bmax[I]; K++) kl[K].push_back((uint32_t)I);
+        }
+    }
+    bt->nA = nA;
+    bt->nB = nB;
+    std::vector<uint32_t> jptr(NB + 1), kptr(NNB + 1), jidx, kidx;
+    for (int64_t J = 0; J < NB; J++) { jptr[J] = (uint32_t)jidx.size(); jidx.insert(jidx.end(), jl[J].begin(), jl[J].end()); }
+    jptr[NB] = (uint32_t)jidx.size();
+    for (int64_t K = 0; K < NNB; K++) { kptr[K] = (uint32_t)kidx.size(); kidx.insert(kidx.end(), kl[K].begin(), kl[K].end()); }
+    kptr[NNB] = (uint32_t)kidx.size();
+    GBLA_TRY(dalloc_t(h, NB, &bt->offA));
+    GBLA_TRY(dalloc_t(h, NB, &bt->offB));
+    GBLA_TRY(dalloc_t(h, NB + 1, &bt->jl_ptr));
+    GBLA_TRY(dalloc_t(h, jidx.size() + 1, &bt->jl_idx));
+    GBLA_TRY(dalloc_t(h, NNB + 1, &bt->kl_ptr));
+    GBLA_TRY(dalloc_t(h, kidx.size() + 1, &bt->kl_idx));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bt->amax, amax.data(), NB * 4, cudaMemcpyHostToDevice, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bt->offA, offA.data(), NB * 8, cudaMemcpyHostToDevice, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bt->offB, offB.data(), NB * 8, cudaMemcpyHostToDevice, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bt->jl_ptr, jptr.data(), (NB + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (!jidx.empty())
+        GBLA_CUDA_TRY(cudaMemcpyAsync(bt->jl_idx, jidx.data(), jidx.size() * 4, cudaMemcpyHostToDevice, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(bt->kl_ptr, kptr.data(), (NNB + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (!kidx.empty())
+        GBLA_CUDA_TRY(cudaMemcpyAsync(bt->kl_idx, kidx.data(), kidx.size() * 4, cudaMemcpyHostToDevice, st));
+    GBLA_TRY(dalloc(h, nA * TB + 16, (void **)&bt->tilesA));
+    GBLA_TRY(dalloc(h, (nB > 0 ? nB : 1) * TB + 16, (void **)&bt->tilesB));
+    GBLA_TRY(dalloc(h, NB * TB + 16, (void **)&bt->invT));
+    GBLA_CUDA_TRY(cudaMemsetAsync(bt->tilesA, 0, nA * TB, st));
+    if (nB) GBLA_CUDA_TRY(cudaMemsetAsync(bt->tilesB, 0, nB * TB, st));
+    k_band_fill<<<grid_for(npiv * 32, 256), 256, 0, st>>>(npiv, h->ab_ptr, h->ab_col, h->ab_val, bt->offA, bt->offB,
+                                                          bt->bmin, bt->tilesA, bt->tilesB);
+    if (NB * 128 > npiv) k_band_pad<<<1, 128, 0, st>>>(npiv, NB, bt->offA, bt->tilesA);
+    {
+        static bool attr = false;
+        if (!attr) {
+            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, DIAG_SMEM));
+            attr = true;
+        }
+    }
+    k_diag_inv<<<(unsigned)NB, 128, DIAG_SMEM, st>>>(h->F, bt->offA, bt->tilesA, bt->invT);
+    note_launch(3);
+    GBLA_CUDA_TRY(cudaGetLastError());
+    // the X (C') tiles of every target tile
+    GBLA_TRY(dalloc(h, (size_t)(bt->ntiles > 0 ? bt->ntiles : 1) * NB * TB + 16, (void **)&bt->Xt));
+    return GBLA_OK;
+}
+
+gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
+{
+    cudaStream_t st = h->stream;
+    if (want_x16) GBLA_TRY(ensure_x(h));
+    if (h->mN == 0 || h->npiv == 0) {     // C is empty: C' = 0, D_new = D
+        h->have_xt = true;
+        return GBLA_OK;
+    }
+    GBLA_TRY(band_build(h));
+    BandTiles *bt = h->bt;
+    if (bt->NB > 0) {
+        static bool attr = false;
+        if (!attr) {
+            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
+            attr = true;
+        }
+        SweepArgs a;
+        a.mN = h->mN; a.npiv = h->npiv; a.NB = bt->NB; a.F = h->F;
+        a.order = h->order; a.tlead = h->tlead;
+        a.cd_ptr = h->cd_ptr; a.cd_col = h->cd_col; a.cd_val = h->cd_val; a.cd_np = h->cd_np;
+        a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
+        a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
+        a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
+        a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
+        k_sweep<<<(unsigned)bt->ntiles, 128, SWEEP_SMEM, st>>>(a);
+        note_launch();
+        GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    bt->swept = true;
+    unsigned long long ops[2] = {0, 0};
+    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, bt->ops, 16, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    h->sparse_ops += ops[0];
+    h->have_xt = true;
+    return GBLA_OK;
+}
+
+gbla_status update_d_tc(gbla_mat h)
+{
+    cudaStream_t st = h->stream;
+    if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
+    BandTiles *bt = h->bt;
+    if (!bt || !bt->swept) { set_error("update_d_tc: no C' tiles"); return GBLA_E_INTERNAL; }
+    if (h->mN > 0 && bt->NB > 0 && bt->NNB > 0) {
+        static bool attr = false;
+        if (!attr) {
+            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM));
+            attr = true;
+        }
+        UpdArgs a;
+        a.mN = h->mN; a.npiv = h->npiv; a.nN = h->nN; a.NB = bt->NB; a.F = h->F;
+        a.order = h->order; a.tlead = h->tlead;
+        a.Xt = bt->Xt; a.tilesB = bt->tilesB; a.offB = bt->offB; a.bmin = bt->bmin;
+        a.kl_ptr = bt->kl_ptr; a.kl_idx = bt->kl_idx; a.D = h->D; a.ldD = h->ldD;
+        dim3 grid((unsigned)bt->NNB, (unsigned)bt->ntiles);
+        k_update_tc<<<grid, 128, UPD_SMEM, st>>>(a);
+        note_launch();
+        GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    unsigned long long ops[2] = {0, 0};
+    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, bt->ops, 16, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    h->sparse_ops += ops[1];
+    return GBLA_OK;
+}

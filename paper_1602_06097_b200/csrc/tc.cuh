@@ -101,3 +101,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 }
 
 }  // namespace tc
+
+namespace tc {
+
+// mbarrier: arrive and set the expected transaction bytes
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// Bulk (non-tensor) TMA copy global -> shared, completion on an mbarrier
+// (SASS UBLKCP).  bytes: multiple of 16; addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// order generic-proxy writes before later async-proxy (bulk copy / tensor core) reads
+__device__ __forceinline__ void fence_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// byte offset of element (r, k) of a 128 x 128 u8 operand plane in the
+// K-major SWIZZLE_NONE core-matrix layout (8 rows x 16 bytes per core
+// matrix; K chunks 2048 bytes apart, 8-row groups 128 bytes apart)
+__host__ __device__ __forceinline__ uint32_t toff(uint32_t r, uint32_t k)
+{
+    return (k >> 4) * 2048u + (r >> 3) * 128u + (r & 7u) * 16u + (k & 15u);
+}
+
+}  // namespace tc

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(128) k_modgemm_tc(
     const uint8_t *__restrict__ Alo, const uint8_t *__restrict__ Ahi,     // [rows_pad][KP]
     const uint8_t *__restrict__ Blo, const uint8_t *__restrict__ Bhi,     // [cols_pad][KP]
     const uint32_t *__restrict__ rowidx, uint16_t *__restrict__ C, int64_t ldc,
-    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi)                 // MODE_STORE: [cols_pad][KP]
+    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,                 // MODE_STORE: [cols_pad][KP]
+    bool vec)                                                             // C rows 32-byte aligned
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sAh = smem, *sAl = smem + SMEM_A, *sBh = smem + 2 * SMEM_A, *sBl = smem + 2 * SMEM_A + SMEM_B;
@@ -115,6 +116,32 @@ __global__ void __launch_bounds__(128) k_modgemm_tc(
         tc::tmem_ld16(lane_addr + 2 * BN + c, ll);
         tc::tmem_wait_ld();
         if (!live) continue;
+        if (vec && x0 + c + 16 <= cols) {
+            // 32-byte row segments: two 16-byte vector accesses per chunk
+            uint4 v[2];
+            uint16_t *d = reinterpret_cast<uint16_t *>(v);
+            if (MODE == MODE_SUB) {
+                v[0] = *reinterpret_cast<const uint4 *>(crow + c);
+                v[1] = *reinterpret_cast<const uint4 *>(crow + c + 8);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint64_t S = ((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j];
+                const uint32_t s = fmod64(S, F);
+                if (MODE == MODE_SUB) {
+                    const uint32_t dv = d[j];
+                    d[j] = (uint16_t)(dv >= s ? dv - s : dv + F.p - s);
+                } else {
+                    d[j] = (uint16_t)s;
+                    const int64_t x = x0 + c + j;
+                    Tlo[(size_t)x * KP + slot] = (uint8_t)(s & 0xff);
+                    Thi[(size_t)x * KP + slot] = (uint8_t)(s >> 8);
+                }
+            }
+            *reinterpret_cast<uint4 *>(crow + c) = v[0];
+            *reinterpret_cast<uint4 *>(crow + c + 8) = v[1];
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int64_t x = x0 + c + j;
@@ -191,8 +218,9 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
     }
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
     dim3 grid(grid_for(cols, BN), grid_for(max_rows, BM));
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 31) == 0) && (ldc % 16 == 0);
     k_modgemm_tc<MODE_SUB><<<grid, 128, SMEM_TOTAL, st>>>(max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx,
-                                                          C, ldc, nullptr, nullptr);
+                                                          C, ldc, nullptr, nullptr, vec);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -210,8 +238,9 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
     }
     if (cols <= 0) return GBLA_OK;
     dim3 grid(grid_for(cols, BN), 1);
+    const bool vec = ((reinterpret_cast<uintptr_t>(O) & 31) == 0) && (ldo % 16 == 0);
     k_modgemm_tc<MODE_STORE><<<grid, 128, SMEM_TOTAL, st>>>(BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo,
-                                                            Tlo, Thi);
+                                                            Tlo, Thi, vec);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;

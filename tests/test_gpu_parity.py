@@ -63,7 +63,7 @@ def check_full(gb, ctx, M, res=None, flags=0, check_dnew=True):
         gb.gbla_reduce_B(h)
         gb.gbla_update_D(h)
     else:
-        gb.gbla_reduce_C(h, fused=True)
+        gb.gbla_reduce_C(h, fused=True, int_pipe=bool(flags & gb.GBLA_SPARSE_INT))
     if check_dnew:
         assert np.array_equal(np_(h.D()), res.dnew), "D_new differs"
     if not (flags & gb.GBLA_ORDER_STANDARD):
@@ -96,6 +96,11 @@ def test_pipeline_random_suite_new_order(gb, ctx):
         check_full(gb, ctx, M)
 
 
+def test_pipeline_random_suite_int_pipe(gb, ctx):
+    for M in gbla_gen.random_suite(80, seed0=29):
+        check_full(gb, ctx, M, flags=gb.GBLA_SPARSE_INT | gb.GBLA_DENSE_INT)
+
+
 def test_pipeline_random_suite_standard_order(gb, ctx):
     for M in gbla_gen.random_suite(60, seed0=25):
         check_full(gb, ctx, M, flags=gb.GBLA_ORDER_STANDARD)
@@ -121,17 +126,38 @@ def test_unfused_cprime_bprime(gb, ctx):
         gb.gbla_update_D(h)
         assert np.array_equal(np_(h.D()), dn)
         h.free()
-        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
-        gb.gbla_reduce_C(h, fused=True, keep_cprime=True)
-        assert np.array_equal(np_(h.cprime()), x)
-        assert np.array_equal(np_(h.D()), dn)
-        h.free()
+        for ip in (False, True):
+            h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+            gb.gbla_reduce_C(h, fused=True, keep_cprime=True, int_pipe=ip)
+            assert np.array_equal(np_(h.cprime()), x)
+            assert np.array_equal(np_(h.D()), dn)
+            assert h.opcount()[0] == int(ops.sum())
+            h.free()
+            h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+            gb.gbla_reduce_C(h, fused=False, int_pipe=ip)
+            assert np.array_equal(np_(h.cprime()), x)
+            gb.gbla_update_D(h)
+            assert np.array_equal(np_(h.D()), dn)
+            h.free()
 
 
 def test_c0_full(gb, ctx, c0_matrix, c0_oracle):
     check_full(gb, ctx, c0_matrix, c0_oracle)
     check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_ORDER_STANDARD)
     check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_DENSE_INT)
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_SPARSE_INT)
+
+
+def test_scaled_configs_tc_vs_int(gb, ctx):
+    """The tensor-core block path and the INT-pipe AXPY path on every config
+    shape at reduced scale (several 128-blocks, ragged tails): D_new, counts,
+    R against the oracle."""
+    for name, sc in (("c1", 0.05), ("c2", 0.02), ("c3", 0.03), ("c4", 0.004)):
+        cfg = gbla_gen.scaled(gbla_gen.CONFIGS[name], sc)
+        M = gbla_gen.f4_matrix(cfg)
+        res = oracle.reduce(M)
+        check_full(gb, ctx, M, res)
+        check_full(gb, ctx, M, res, flags=gb.GBLA_SPARSE_INT | gb.GBLA_DENSE_INT)
 
 
 def test_host_input_and_host_copy(gb, ctx, c0_matrix, c0_oracle):
@@ -221,3 +247,50 @@ def test_errors(gb, ctx):
         gb.gbla_update_D(h)                        # both: would apply A^-1 twice
     assert e.value.status == 3
     h.free()
+
+
+def test_modgemm_tc_and_int_against_numpy(gb, ctx):
+    """K11 alone: exact C - A*B mod p for ragged shapes (several tiles and a
+    ragged tail), both engines, with and without a row-index gather."""
+    import torch
+    from pins import matmul_mod
+    rng = np.random.default_rng(8)
+    shapes = [(1, 1, 1), (5, 7, 3), (128, 64, 128), (129, 65, 127), (300, 200, 128), (1000, 333, 77), (77, 1030, 128)]
+    for p in (3, 251, 32003, 65521):
+        for rows, cols, K in shapes:
+            A = rng.integers(0, p, (rows, K)); B = rng.integers(0, p, (K, cols))
+            C0 = rng.integers(0, p, (rows + 3, cols))
+            perm = rng.permutation(rows + 3)[:rows].astype(np.uint32)
+            exp = C0.copy()
+            exp[perm] = (C0[perm] - matmul_mod(A, B, p)) % p
+            for engine in (0, 1):
+                tA = torch.from_numpy(A.astype(np.uint16)).cuda()
+                tB = torch.from_numpy(B.astype(np.uint16)).cuda()
+                tC = torch.from_numpy(C0.astype(np.uint16)).cuda()
+                gb.gbla_modgemm(ctx, p, tA, tB, tC, rowidx=torch.from_numpy(perm).cuda(), engine=engine)
+                assert np.array_equal(tC.cpu().numpy().astype(np.int64), exp), (p, rows, cols, K, engine)
+    # worst case for the s32 limb accumulators: all entries p - 1, K = 128
+    p = 65521
+    A = np.full((128, 128), p - 1); B = np.full((128, 64), p - 1); C0 = np.zeros((128, 64), np.int64)
+    tC = torch.from_numpy(C0.astype(np.uint16)).cuda()
+    gb.gbla_modgemm(ctx, p, torch.from_numpy(A.astype(np.uint16)).cuda(),
+                    torch.from_numpy(B.astype(np.uint16)).cuda(), tC)
+    assert np.array_equal(tC.cpu().numpy().astype(np.int64), (C0 - matmul_mod(A, B, p)) % p)
+
+
+def test_echelon_engines_agree_c0_and_dense(gb, ctx, c0_matrix, c0_oracle):
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_DENSE_TC)
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_DENSE_INT)
+    # dense random D with rank deficiency (dense-D-heavy shape, like c3)
+    rng = np.random.default_rng(4)
+    for p in (32003, 65521):
+        base = rng.integers(0, p, (150, 400))
+        comb = rng.integers(0, p, (100, 150))
+        from pins import matmul_mod
+        dep = matmul_mod(comb, base, p)
+        a = np.vstack([base, dep])[rng.permutation(250)]
+        M = csr_from_dense(np.hstack([np.zeros((250, 0), np.int64), a]), p)
+        res = oracle.reduce(M)
+        assert res.rank_M == 150
+        for f in (gb.GBLA_DENSE_TC, gb.GBLA_DENSE_INT):
+            check_full(gb, ctx, M, res, flags=f)
