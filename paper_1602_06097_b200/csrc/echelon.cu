@@ -27,10 +27,16 @@
 // Engines: GBLA_DENSE_TC (default): PK = 128, Rn and the trailing update on
 // tcgen05 (tc_gemm.cu); GBLA_DENSE_INT: PK = 64, both on the INT pipe.
 // At the end K13 compacts R (rows sorted by pivot column) and pivcol.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "internal.cuh"
+#include "tc.cuh"
 
+void modgemm_set_sms(int sms);
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc);
@@ -60,171 +66,196 @@ __global__ void k_invtab(Field F, uint16_t *__restrict__ inv)
 }
 
 template <int PK>
-constexpr int panel_smem() { return (2 * (2 * PK) * PK + PK * PK) * (int)sizeof(uint16_t); }
+constexpr int panel_smem() { return (2 * PK) * PK * (int)sizeof(uint32_t) + PK * PK * (int)sizeof(uint16_t); }
 
 template <int PK>
 __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t c0, Field F,
                                                 const uint16_t *__restrict__ D, int64_t ldD,
                                                 uint32_t *__restrict__ rowpiv, PanelState<PK> *__restrict__ ps,
                                                 uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,
-                                                const uint16_t *__restrict__ invtab)
+                                                const uint16_t *__restrict__ invtab,
+                                                const uint8_t *__restrict__ cflag,
+                                                unsigned long long *__restrict__ trace)
 {
+    // optional per-panel trace (GBLA_PANEL_TRACE): cycles in scan / load / reduce / integrate,
+    // candidates, pivots, chunks
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tmark = clock64();
+#define PANEL_LAP(k_)                                                  \
+    do {                                                               \
+        if (trace) { const long long t_ = clock64(); tr[k_] += t_ - tmark; tmark = t_; } \
+    } while (0)
     constexpr int CH = PK;             // candidates per chunk
-    constexpr int G = PK / 16;         // 16-column groups per row
     constexpr int CPL = PK / 32;       // columns per lane
-    extern __shared__ uint16_t dsm[];
-    // rows [0, PK): basis; rows [PK, PK + CH): candidates.  X = panel values, A = transform.
-    uint16_t(*X)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm);
-    uint16_t(*A)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm + (PK + CH) * PK);
-    uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm + 2 * (PK + CH) * PK);   // [CH][PK] factors
-    __shared__ uint32_t bpc[PK], bsel[PK], crow[CH], selfc[CH], gbuf[PK + CH];
-    __shared__ uint32_t prx[PK], pra[PK];
+    extern __shared__ uint32_t dsm32[];
+    // rows [0, PK): basis; rows [PK, PK + CH): candidates.  Each entry packs the
+    // panel value (low 16 bits) and the transform coefficient (high 16 bits).
+    uint32_t(*XA)[PK] = reinterpret_cast<uint32_t(*)[PK]>(dsm32);
+    uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm32 + (PK + CH) * PK);   // [CH][PK] factors
+    __shared__ uint32_t bpc[PK], bsel[PK], crow[CH], selfc[CH];
+    __shared__ uint32_t brow[PK];      // physical XA row of basis slot b during a chunk
+    __shared__ uint32_t sinv[PK];
+    const uint32_t m32 = 0xffffffffu / F.p;   // 32-bit Barrett: v < 2^32 -> v mod p
+    auto mod32 = [&](uint32_t v) -> uint32_t {
+        const uint32_t r = v - __umulhi(v, m32) * F.p;
+        return r >= F.p ? r - F.p : r;
+    };
     __shared__ uint32_t wcount[32];
     __shared__ int s_ncand;
     __shared__ long long s_next;
-    __shared__ uint32_t s_pself;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t p = F.p;
     const int64_t width = (nN - c0) < PK ? (nN - c0) : PK;
+    if (tid < PK) brow[tid] = tid;
     uint32_t nb = 0;
     int64_t pos = 0;
     while (nb < (uint32_t)PK && pos < mN) {
-        // (1) next chunk of candidates, in row order
-        const int64_t r = pos + tid;
-        bool ok = false;
-        if (r < mN && rowpiv[r] == GBLA_NONE) {
-            const uint16_t *row = D + (size_t)r * ldD + c0;
-            if (width == PK) {
-                for (int c = 0; c < PK; c += 8) {
-                    const uint4 v = *reinterpret_cast<const uint4 *>(row + c);
-                    if (v.x | v.y | v.z | v.w) { ok = true; break; }
-                }
-            } else {
-                for (int64_t c = 0; c < width; c++)
-                    if (row[c]) { ok = true; break; }
+        // (1) next chunk of up to CH candidates (k_cand flags), in row order:
+        //     scan 1024 rows per round until the chunk is full or the rows run out
+        int ncand = 0;
+        while (ncand < CH && pos < mN) {
+            const int64_t r = pos + tid;
+            const bool ok = r < mN && cflag[r] != 0;
+            const unsigned msk = __ballot_sync(FULL, ok);
+            if (lane == 0) wcount[warp] = __popc(msk);
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t s = 0;
+                for (int w = 0; w < 32; w++) { const uint32_t c = wcount[w]; wcount[w] = s; s += c; }
+                s_ncand = (ncand + (int)s) < CH ? ncand + (int)s : CH;
+                s_next = pos + 1024;
             }
+            __syncthreads();
+            const uint32_t rank = ncand + wcount[warp] + __popc(msk & ((1u << lane) - 1u));
+            if (ok && rank < (uint32_t)CH) crow[rank] = (uint32_t)r;
+            if (ok && rank == (uint32_t)CH) s_next = r;      // first candidate not taken
+            __syncthreads();
+            ncand = s_ncand;
+            pos = s_next;
         }
-        const unsigned msk = __ballot_sync(FULL, ok);
-        if (lane == 0) wcount[warp] = __popc(msk);
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t s = 0;
-            for (int w = 0; w < 32; w++) { const uint32_t c = wcount[w]; wcount[w] = s; s += c; }
-            s_ncand = s < (uint32_t)CH ? (int)s : CH;
-            s_next = pos + 1024;
-        }
-        __syncthreads();
-        const uint32_t rank = wcount[warp] + __popc(msk & ((1u << lane) - 1u));
-        if (ok && rank < (uint32_t)CH) crow[rank] = (uint32_t)r;
-        if (ok && rank == (uint32_t)CH) s_next = r;          // first candidate not taken
-        __syncthreads();
-        const int ncand = s_ncand;
-        pos = s_next;
+        PANEL_LAP(0);
         if (ncand == 0) continue;
+        tr[4] += ncand;
+        tr[6] += 1;
         // (2) load the candidates' panel slices
         for (int idx = tid; idx < ncand * PK; idx += 1024) {
             const int ci = idx / PK, k = idx % PK;
-            X[PK + ci][k] = k < width ? D[(size_t)crow[ci] * ldD + c0 + k] : 0;
-            A[PK + ci][k] = 0;
+            XA[PK + ci][k] = k < width ? D[(size_t)crow[ci] * ldD + c0 + k] : 0;
         }
         if (tid < ncand) selfc[tid] = 1;
         __syncthreads();
+        PANEL_LAP(1);
         // (3) reduce the chunk by the current basis (RREF, so each factor is the
         //     candidate's original entry at the basis pivot column)
         if (nb > 0) {
             // snapshot of the factors, then 8-column items (u64 delayed reduction)
             for (int idx = tid; idx < ncand * (int)nb; idx += 1024) {
                 const int ci = idx / (int)nb, b = idx % (int)nb;
-                FS[ci][b] = X[PK + ci][bpc[b]];
+                FS[ci][b] = (uint16_t)(XA[PK + ci][bpc[b]] & 0xffffu);
             }
             __syncthreads();
             for (int item = tid; item < ncand * (PK / 8); item += 1024) {
                 const int ci = item / (PK / 8), g8 = item % (PK / 8);
                 uint64_t ax[8], aa[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) { ax[u] = X[PK + ci][g8 * 8 + u]; aa[u] = 0; }
+                for (int u = 0; u < 8; u++) { ax[u] = XA[PK + ci][g8 * 8 + u] & 0xffffu; aa[u] = 0; }
                 for (uint32_t b = 0; b < nb; b++) {
                     const uint32_t f = FS[ci][b];
                     if (!f) continue;
                     const uint64_t nf = p - f;
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
-                        ax[u] += nf * X[b][g8 * 8 + u];
-                        aa[u] += nf * A[b][g8 * 8 + u];
+                        const uint32_t v = XA[b][g8 * 8 + u];
+                        ax[u] += nf * (v & 0xffffu);
+                        aa[u] += nf * (v >> 16);
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    X[PK + ci][g8 * 8 + u] = (uint16_t)fmod64(ax[u], F);
-                    A[PK + ci][g8 * 8 + u] = (uint16_t)fmod64(aa[u], F);
-                }
+                for (int u = 0; u < 8; u++)
+                    XA[PK + ci][g8 * 8 + u] = fmod64(ax[u], F) | (fmod64(aa[u], F) << 16);
             }
             __syncthreads();
         }
+        PANEL_LAP(2);
         // (4) integrate the chunk row by row
         for (int ci = 0; ci < ncand && nb < (uint32_t)PK; ci++) {
-            const uint16_t *cx = X[PK + ci];
+            const uint32_t *cx = XA[PK + ci];
             bool nz = false;
 #pragma unroll
-            for (int u = 0; u < CPL; u++) nz |= cx[lane * CPL + u] != 0;
+            for (int u = 0; u < CPL; u++) nz |= (cx[lane * CPL + u] & 0xffffu) != 0;
             const unsigned nzm = __ballot_sync(FULL, nz);
             if (!nzm) continue;                                  // dependent on the basis
             const int src = __ffs(nzm) - 1;
             uint32_t c = src * CPL;
-            while (cx[c] == 0) c++;
+            while ((cx[c] & 0xffffu) == 0) c++;
+            // Fraction-free step (no inverse on the critical path): with the
+            // pivot row P = candidate ci (pivot value v at column c; its own
+            // transform coefficient sc at index nb), every other row R of the
+            // basis and of the rest of the chunk becomes  v*R - g*P,  g = R[c].
+            // Basis rows are renormalized once per chunk (below).
+            const uint32_t v = cx[c] & 0xffffu;
+            const uint32_t sc = selfc[ci];
             const int nrows = (int)nb + (ncand - ci - 1);
-            if (warp == 0) {
-                const uint32_t inv = invtab[cx[c]];
+            if (tid == 0) {
+                // P joins the basis as slot nb (in place; its transform gets sc at index nb)
+                XA[PK + ci][nb] = (XA[PK + ci][nb] & 0xffffu) | (sc << 16);
+                brow[nb] = PK + ci;
+                bpc[nb] = c;
+                bsel[nb] = crow[ci];
+            }
+            for (int rr = warp; rr < nrows; rr += 32) {     // one warp per row
+                const int cand = rr - (int)nb;
+                const uint32_t row = rr < (int)nb ? brow[rr] : (uint32_t)(PK + ci + 1 + cand);
+                const uint32_t gl = (lane == (int)(c / CPL)) ? (XA[row][c] & 0xffffu) : 0u;
+                const uint32_t g = __shfl_sync(FULL, gl, c / CPL);
+                if (!g) continue;
+                const uint32_t ng = p - g;
 #pragma unroll
                 for (int u = 0; u < CPL; u++) {
                     const int k = lane * CPL + u;
-                    prx[k] = fmul(cx[k], inv, F);
-                    pra[k] = fmul(A[PK + ci][k], inv, F);
+                    const uint32_t val = XA[row][k], P = cx[k];
+                    const uint32_t pa = (k == (int)nb) ? sc : (P >> 16);
+                    const uint32_t x = mod32(mod32(v * (val & 0xffffu)) + ng * (P & 0xffffu));
+                    const uint32_t a = mod32(mod32(v * (val >> 16)) + ng * pa);
+                    XA[row][k] = x | (a << 16);
                 }
-                if (lane == 0) s_pself = fmul(selfc[ci], inv, F);
-                for (int rr = lane; rr < nrows; rr += 32) {
-                    const int row = rr < (int)nb ? rr : PK + ci + 1 + (rr - (int)nb);
-                    gbuf[rr] = X[row][c];
-                }
+                if (cand >= 0 && lane == 0) selfc[ci + 1 + cand] = mod32(v * selfc[ci + 1 + cand]);
             }
-            __syncthreads();
-            const uint32_t pself = s_pself;
-            for (int item = tid; item < nrows * G; item += 1024) {
-                const int rr = item / G, g = item % G;
-                const uint32_t gv = gbuf[rr];
-                if (!gv) continue;
-                const int row = rr < (int)nb ? rr : PK + ci + 1 + (rr - (int)nb);
-                const uint64_t ng = p - gv;
-#pragma unroll
-                for (int u = 0; u < 16; u++) {
-                    const int k = g * 16 + u;
-                    X[row][k] = (uint16_t)fmod64(X[row][k] + ng * prx[k], F);
-                    uint64_t av = A[row][k] + ng * pra[k];
-                    if (k == (int)nb) av += ng * pself;
-                    A[row][k] = (uint16_t)fmod64(av, F);
-                }
-            }
-            if (tid < PK) {
-                X[nb][tid] = (uint16_t)prx[tid];
-                A[nb][tid] = (uint16_t)(tid < (int)nb ? pra[tid] : (tid == (int)nb ? pself : 0));
-            }
-            if (tid == 0) { bpc[nb] = c; bsel[nb] = crow[ci]; }
             __syncthreads();
             nb++;
         }
+        // normalize the basis (leading 1 at each pivot column) and compact it into slots [0, nb)
+        if (tid < (int)nb) sinv[tid] = invtab[XA[brow[tid]][bpc[tid]] & 0xffffu];
+        __syncthreads();
+        for (int idx = tid; idx < (int)nb * PK; idx += 1024) {
+            const int b = idx / PK, k = idx % PK;
+            const uint32_t val = XA[brow[b]][k], s = sinv[b];
+            XA[b][k] = mod32((val & 0xffffu) * s) | (mod32((val >> 16) * s) << 16);
+        }
+        __syncthreads();
+        if (tid < (int)nb) brow[tid] = tid;
+        __syncthreads();
+        PANEL_LAP(3);
     }
     __syncthreads();
+    if (trace && tid == 0) {
+        tr[5] = nb;
+        unsigned long long *o = trace + (c0 / PK) * 8;
+        for (int k = 0; k < 8; k++) o[k] = tr[k];
+    }
+#undef PANEL_LAP
     if (tid == 0) { ps->kp = nb; ps->nrows = 0; }
     for (int i = tid; i < PK * PK; i += blockDim.x) {
         const int b = i / PK, s = i % PK;
-        ps->T[i] = (b < (int)nb && s < (int)nb) ? A[b][s] : 0;
+        ps->T[i] = (b < (int)nb && s < (int)nb) ? (uint16_t)(XA[b][s] >> 16) : 0;
     }
-    if (Tlo) {   // T as limb planes [KPT rows][KPT], zero padded (A operand of the Rn GEMM)
+    if (Tlo) {   // T as one A tile (limb planes, core-matrix layout), zero padded: A operand of the Rn GEMM
         for (int i = tid; i < KPT * KPT; i += blockDim.x) {
             const int b = i / KPT, s = i % KPT;
-            const uint16_t v = (b < (int)nb && s < (int)nb && b < PK && s < PK) ? A[b][s] : 0;
-            Tlo[i] = (uint8_t)(v & 0xff);
-            Thi[i] = (uint8_t)(v >> 8);
+            const uint16_t v = (b < (int)nb && s < (int)nb && b < PK && s < PK) ? (uint16_t)(XA[b][s] >> 16) : 0;
+            const uint32_t o = tc::toff((uint32_t)b, (uint32_t)s);
+            Tlo[o] = (uint8_t)(v & 0xff);
+            Thi[o] = (uint8_t)(v >> 8);
         }
     }
     if (tid < (int)nb) {
@@ -232,6 +263,32 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
         ps->pc[tid] = (uint32_t)c0 + bpc[tid];
         rowpiv[bsel[tid]] = (uint32_t)c0 + bpc[tid];    // marks S (pivot col >= c0)
     }
+}
+
+// candidate flags of panel [c0, c0+PK): active row with a nonzero slice.
+// One thread per row, all slice loads issued together.
+template <int PK>
+__global__ void k_cand(int64_t mN, int64_t nN, int64_t c0, const uint16_t *__restrict__ D, int64_t ldD,
+                       const uint32_t *__restrict__ rowpiv, uint8_t *__restrict__ cflag)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= mN) return;
+    bool ok = false;
+    if (rowpiv[r] == GBLA_NONE) {
+        const uint16_t *row = D + (size_t)r * ldD + c0;
+        if (nN - c0 >= PK) {
+            uint4 v[PK / 8];
+#pragma unroll
+            for (int c = 0; c < PK / 8; c++) v[c] = *reinterpret_cast<const uint4 *>(row + 8 * c);
+            uint32_t o = 0;
+#pragma unroll
+            for (int c = 0; c < PK / 8; c++) o |= v[c].x | v[c].y | v[c].z | v[c].w;
+            ok = o != 0;
+        } else {
+            for (int64_t c = 0; c < nN - c0; c++) ok |= row[c] != 0;
+        }
+    }
+    cflag[r] = ok;
 }
 
 // F[i][b] = D[i][pc_b] for rows not selected in this panel, compacted to the
@@ -243,31 +300,43 @@ __global__ void k_gather(int64_t mN, int64_t c0, const uint16_t *__restrict__ D,
                          uint16_t *__restrict__ Fc, uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi,
                          uint32_t *__restrict__ rows)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per row; lane l holds coefficients b = l*CPL .. l*CPL+CPL-1
+    constexpr int CPL = PK / 32;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
     if (i >= mN || kp == 0) return;
     const uint32_t rp = rowpiv[i];
     if (rp != GBLA_NONE && rp >= (uint64_t)c0) return;   // selected now: becomes Rn
     const uint16_t *drow = D + (size_t)i * ldD;
+    uint16_t v[CPL];
     bool nz = false;
-    for (uint32_t b = 0; b < kp; b++) nz |= drow[ps->pc[b]] != 0;
-    if (!nz) return;
-    const uint32_t slot = atomicAdd(&ps->nrows, 1u);
-    rows[slot] = (uint32_t)i;
-    if (TC) {
-        for (uint32_t b = 0; b < KPT; b += 16) {
-            uint8_t lo[16], hi[16];
 #pragma unroll
-            for (int u = 0; u < 16; u++) {
-                const uint16_t v = b + u < kp ? drow[ps->pc[b + u]] : 0;
-                lo[u] = (uint8_t)(v & 0xff);
-                hi[u] = (uint8_t)(v >> 8);
-            }
-            *reinterpret_cast<uint4 *>(Flo + (size_t)slot * KPT + b) = *reinterpret_cast<uint4 *>(lo);
-            *reinterpret_cast<uint4 *>(Fhi + (size_t)slot * KPT + b) = *reinterpret_cast<uint4 *>(hi);
+    for (int u = 0; u < CPL; u++) {
+        const uint32_t b = lane * CPL + u;
+        v[u] = b < kp ? drow[ps->pc[b]] : 0;
+        nz |= v[u] != 0;
+    }
+    if (!__any_sync(FULL, nz)) return;
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(&ps->nrows, 1u);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (lane == 0) rows[slot] = (uint32_t)i;
+    if (TC) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int u = 0; u < CPL; u++) {
+            lo |= (uint32_t)(v[u] & 0xff) << (8 * u);
+            hi |= (uint32_t)(v[u] >> 8) << (8 * u);
         }
+        static_assert(!TC || CPL == 4, "TC engine: 4 coefficients per lane");
+        // A tiles of the trailing GEMM: 128 slots per tile, core-matrix layout
+        const size_t o = (size_t)(slot / 128) * (KPT * 128) + tc::toff(slot % 128, lane * CPL);
+        *reinterpret_cast<uint32_t *>(Flo + o) = lo;
+        *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
     } else {
-        for (uint32_t b = 0; b < kp; b++) Fc[(size_t)i * PK + b] = drow[ps->pc[b]];
+#pragma unroll
+        for (int u = 0; u < CPL; u++) Fc[(size_t)i * PK + lane * CPL + u] = v[u];
     }
 }
 
@@ -279,7 +348,8 @@ __global__ void k_gather_st(int64_t nN, int64_t c0, const uint16_t *__restrict__
     const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c0 + x >= nN) return;
     const uint32_t kp = ps->kp;
-    for (uint32_t s = 0; s < KPT; s += 16) {
+    {
+        const uint32_t s = blockIdx.y * 16;      // one 16-row group of S per grid row
         uint8_t lo[16], hi[16];
 #pragma unroll
         for (int u = 0; u < 16; u++) {
@@ -287,8 +357,10 @@ __global__ void k_gather_st(int64_t nN, int64_t c0, const uint16_t *__restrict__
             lo[u] = (uint8_t)(v & 0xff);
             hi[u] = (uint8_t)(v >> 8);
         }
-        *reinterpret_cast<uint4 *>(Blo + (size_t)x * KPT + s) = *reinterpret_cast<uint4 *>(lo);
-        *reinterpret_cast<uint4 *>(Bhi + (size_t)x * KPT + s) = *reinterpret_cast<uint4 *>(hi);
+        // B tiles of the Rn GEMM: 64 columns per tile, core-matrix layout (K = s)
+        const size_t o = (size_t)(x / 64) * (64 * KPT) + tc::toff64((uint32_t)(x % 64), s);
+        *reinterpret_cast<uint4 *>(Blo + o) = *reinterpret_cast<uint4 *>(lo);
+        *reinterpret_cast<uint4 *>(Bhi + o) = *reinterpret_cast<uint4 *>(hi);
     }
 }
 
@@ -435,11 +507,15 @@ gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
     GBLA_TRY(dalloc(h, sizeof(PanelState<PK>), (void **)&ps));
     GBLA_TRY(set_panel_smem<PK>());
+    uint8_t *cflag;
+    GBLA_TRY(dalloc_t(h, mN + 1, &cflag));
     for (int64_t c0 = 0; c0 < nN; c0 += PK) {
         const int64_t width = nN - c0;
+        k_cand<PK><<<grid_for(mN, 256), 256, 0, st>>>(mN, nN, c0, h->D, ldD, rowpiv, cflag);
         k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, nullptr, nullptr,
-                                                        invtab);
-        k_gather<PK, false><<<grid_for(mN, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, Fc, nullptr, nullptr,
+                                                        invtab, cflag, nullptr);
+        note_launch();
+        k_gather<PK, false><<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, Fc, nullptr, nullptr,
                                                               rows);
         k_rnew<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps, Rn, ldR);
         k_trailing_int<<<dim3(grid_for(width, 256), grid_for(mN, 32)), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps,
@@ -456,6 +532,7 @@ gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, co
 {
     constexpr int PK = KPT;
     cudaStream_t st = h->stream;
+    modgemm_set_sms(h->ctx->sm_count);
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
     const int64_t npad = (nN + 63) / 64 * 64 + 64;
     uint32_t *rows;
@@ -474,12 +551,23 @@ gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, co
     GBLA_TRY(dalloc_t(h, (size_t)KPT * ldR, &Rn));
     GBLA_TRY(dalloc(h, sizeof(PanelState<PK>), (void **)&ps));
     GBLA_TRY(set_panel_smem<PK>());
+    uint8_t *cflag;
+    GBLA_TRY(dalloc_t(h, mN + 1, &cflag));
+    const int64_t npanels = (nN + PK - 1) / PK;
+    unsigned long long *trace = nullptr;
+    if (getenv("GBLA_PANEL_TRACE")) {
+        GBLA_TRY(dalloc_t(h, (size_t)npanels * 8, &trace));
+        GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, (size_t)npanels * 64, st));
+    }
     for (int64_t c0 = 0; c0 < nN; c0 += PK) {
         const int64_t width = nN - c0;
-        k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, Tlo, Thi, invtab);
-        k_gather<PK, true><<<grid_for(mN, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, nullptr, Flo, Fhi,
+        k_cand<PK><<<grid_for(mN, 256), 256, 0, st>>>(mN, nN, c0, h->D, ldD, rowpiv, cflag);
+        k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, Tlo, Thi, invtab,
+                                                        cflag, trace);
+        note_launch();
+        k_gather<PK, true><<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, nullptr, Flo, Fhi,
                                                              rows);
-        k_gather_st<<<grid_for(width, 128), 128, 0, st>>>(nN, c0, h->D, ldD, ps, Blo, Bhi);
+        k_gather_st<<<dim3(grid_for(width, 128), KPT / 16), 128, 0, st>>>(nN, c0, h->D, ldD, ps, Blo, Bhi);
         note_launch(3);
         // Rn = T * D[S, c0:]  (plus its transposed limb planes)
         GBLA_TRY(modgemm_tc_store(st, width, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi));
@@ -489,6 +577,19 @@ gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, co
         k_count<PK><<<1, 1, 0, st>>>(width, ps, dops);
         note_launch(2);
         GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    if (trace) {   // diagnostics: per-panel phase cycles
+        std::vector<unsigned long long> tr((size_t)npanels * 8);
+        GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t q = 0; q < npanels; q++)
+            for (int k = 0; k < 8; k++) s[k] += (double)tr[q * 8 + k];
+        fprintf(stderr,
+                "[gbla panel trace] %lld panels, mean per panel: scan %.0f load %.0f reduce %.0f integrate %.0f cycles;"
+                " candidates %.1f pivots %.1f chunks %.1f\n",
+                (long long)npanels, s[0] / npanels, s[1] / npanels, s[2] / npanels, s[3] / npanels, s[4] / npanels,
+                s[5] / npanels, s[6] / npanels);
     }
     return GBLA_OK;
 }

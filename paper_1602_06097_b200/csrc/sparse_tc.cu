@@ -25,6 +25,9 @@
 // operands staged by cp.async.bulk (TMA bulk copies) in a 2-stage mbarrier
 // pipeline, one elected thread issuing.  The results are the same exact
 // residues as Alg 2 (X = C A^-1 is unique), bit for bit.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <vector>
 
 #include "internal.cuh"
@@ -170,30 +173,64 @@ struct SweepArgs {
     int64_t mN, npiv, NB;
     Field F;
     const uint32_t *order, *tlead;
-    const uint64_t *cd_ptr;
-    const uint32_t *cd_col;
-    const uint16_t *cd_val;
-    const uint32_t *cd_np;
     const uint8_t *tilesA, *invT;
     const uint64_t *offA;
     const uint32_t *jl_ptr, *jl_idx;
-    uint8_t *Xt;
+    uint8_t *Xt;                   // X tiles; tile (T, J) holds C_J[T] until step J overwrites it with X_J[T]
     uint16_t *X16;
     int64_t ldX;
     const uint32_t *ab_w, *ab_np;
     unsigned long long *ops;
+    unsigned long long *trace;     // optional: per (J, CTA) phase timestamps (GBLA_SWEEP_TRACE)
 };
 
-constexpr int SWEEP_SMEM = 2 * 65536 + 2 * TB;
+#define SWEEP_MARK(slot_)                                                                  \
+    do {                                                                                   \
+        if (a.trace && tid == 0)                                                           \
+            a.trace[((size_t)J * 256 + blockIdx.x) * 8 + (slot_)] = clock64();             \
+    } while (0)
 
+// pos[order[i]] = i (rank of every target in lead order)
+__global__ void k_pos(int64_t mN, const uint32_t *__restrict__ order, uint32_t *__restrict__ pos)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < mN) pos[order[i]] = (uint32_t)i;
+}
+
+// C_J[T] into the X tiles (dense limb planes, A-operand layout): warp per target row
+__global__ void k_cfill(int64_t mN, int64_t NB, const uint32_t *__restrict__ pos, const uint64_t *__restrict__ cd_ptr,
+                        const uint32_t *__restrict__ cd_col, const uint16_t *__restrict__ cd_val,
+                        const uint32_t *__restrict__ cd_np, uint8_t *__restrict__ Xt)
+{
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= mN) return;
+    const uint32_t ps = pos[t];
+    const uint64_t T = ps / 128, r = ps % 128;
+    const uint64_t s = cd_ptr[t], e = s + cd_np[t];
+    for (uint64_t q = s + lane; q < e; q += 32) {
+        const uint32_t c = cd_col[q];
+        const uint16_t v = cd_val[q];
+        uint8_t *tile = Xt + (T * NB + c / 128) * (uint64_t)TB;
+        const uint32_t o = tc::toff((uint32_t)r, c % 128);
+        tile[o] = (uint8_t)(v & 0xff);
+        tile[PB + o] = (uint8_t)(v >> 8);
+    }
+}
+
+constexpr int NSTAGE = 3;
+constexpr int SWEEP_SMEM = NSTAGE * 65536 + TB;   // 3 operand stages + inv(A_JJ); Y reuses stage 0
+
+// Persistent: CTA T = target tile T sweeps J from its first lead block.
 __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stg = smem;
-    uint8_t *Ys = smem + 2 * 65536;
-    uint8_t *INV = Ys + TB;
-    __shared__ uint64_t full[2], mdone[2], accbar, invbar;
+    uint8_t *Ys = smem;                        // stage 0's A half, free after stage 1
+    uint8_t *INV = smem + NSTAGE * 65536;
+    __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar, invbar;
     __shared__ uint32_t tmem_s;
+    __shared__ uint32_t s_np[128], s_w[128];
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t T = blockIdx.x, first = T * 128;
     const uint32_t lead0 = a.tlead[a.order[first]];
@@ -202,64 +239,74 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     const int64_t slot = first + tid;
     const bool live = slot < a.mN;
     const uint32_t t = live ? a.order[slot] : 0;
-    uint64_t q = live ? a.cd_ptr[t] : 0;
-    const uint64_t qe = live ? a.cd_ptr[t] + a.cd_np[t] : 0;
     if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
     if (tid == 0) {
-        tc::mbar_init(&full[0], 1); tc::mbar_init(&full[1], 1);
-        tc::mbar_init(&mdone[0], 1); tc::mbar_init(&mdone[1], 1);
-        tc::mbar_init(&accbar, 1); tc::mbar_init(&invbar, 1);
+        for (int s = 0; s < NSTAGE; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&mdone[s], 1); }
+        tc::mbar_init(&accbar, 1);
+        tc::mbar_init(&invbar, 1);
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_s;
     const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-    uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0}, ph_acc = 0, ph_inv = 0;
+    uint32_t ph_acc = 0, ph_inv = 0;
+    uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
     unsigned long long opsA = 0, opsB = 0;
     const uint32_t sStg = tc::smem_u32(stg), sY = tc::smem_u32(Ys), sINV = tc::smem_u32(INV);
     uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
     const uint32_t p = a.F.p;
 
     for (int64_t J = Jmin; J < a.NB; J++) {
+        SWEEP_MARK(0);
+        const uint32_t jbase = (uint32_t)J * 128;
+        {
+            const uint32_t jg = jbase + tid;
+            s_np[tid] = jg < (uint64_t)a.npiv ? a.ab_np[jg] : 1;
+            s_w[tid] = jg < (uint64_t)a.npiv ? a.ab_w[jg] : 1;
+        }
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
         const uint32_t nI = l1 - lb;
+        SWEEP_MARK(1);
         if (tid == 0) {
             tc::mbar_expect_tx(&invbar, TB);
             tc::bulk_g2s(INV, a.invT + (size_t)J * TB, TB, &invbar);
             auto load = [&](uint32_t it) {
                 const uint32_t I = a.jl_idx[lb + it];
-                const int s = it & 1;
+                const int s = it % NSTAGE;
                 tc::mbar_expect_tx(&full[s], 2 * TB);
                 tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
                 tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
             };
-            if (nI > 0) load(0);
-            if (nI > 1) load(1);
+            for (uint32_t it = 0; it < nI && it < (uint32_t)NSTAGE; it++) load(it);
             for (uint32_t it = 0; it < nI; it++) {
-                const int s = it & 1;
+                const int s = it % NSTAGE;
                 tc::mbar_wait(&full[s], ph_full[s]);
                 ph_full[s] ^= 1;
                 tc::fence_after();
                 issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > 0);
-                if (it + 2 < nI) {
-                    tc::commit(&mdone[s]);
-                    tc::mbar_wait(&mdone[s], ph_md[s]);
-                    ph_md[s] ^= 1;
-                    load(it + 2);
+                if (it + NSTAGE < nI) tc::commit(&mdone[s]);     // stage s is reloaded for it + NSTAGE
+                // refill the stage of the previous iteration once its MMAs are done
+                if (it >= 1 && it - 1 + NSTAGE < nI) {
+                    const int sp = (it - 1) % NSTAGE;
+                    tc::mbar_wait(&mdone[sp], ph_md[sp]);
+                    ph_md[sp] ^= 1;
+                    load(it - 1 + NSTAGE);
                 }
             }
             if (nI > 0) tc::commit(&accbar);
+            SWEEP_MARK(2);
         }
         if (nI > 0) {
             tc::mbar_wait(&accbar, ph_acc);
             ph_acc ^= 1;
             tc::fence_after();
         }
-        // epilogue 1: Y = C_J - S  -> shared memory (A operand of stage 2)
-        const uint32_t jbase = (uint32_t)J * 128;
+        SWEEP_MARK(3);
+        // epilogue 1: Y = C_J - S -> shared memory (A operand of stage 2); C_J row from the tile itself
+        const uint8_t *ct = Xrow + (size_t)J * TB;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 16) {
             uint64_t S[16];
@@ -269,32 +316,27 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
 #pragma unroll
                 for (int j = 0; j < 16; j++) S[j] = 0;
             }
+            const uint32_t o = tc::toff(tid, c);
+            uint4 clo = *reinterpret_cast<const uint4 *>(ct + o);
+            uint4 chi = *reinterpret_cast<const uint4 *>(ct + PB + o);
+            const uint8_t *cl = reinterpret_cast<const uint8_t *>(&clo), *ch = reinterpret_cast<const uint8_t *>(&chi);
             uint8_t lo[16], hi[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                const uint32_t y = fneg(fmod64(S[j], a.F), a.F);
+                const uint32_t cv = cl[j] | (ch[j] << 8);
+                const uint32_t s = fmod64(S[j], a.F);
+                const uint32_t y = cv >= s ? cv - s : cv + p - s;
                 lo[j] = (uint8_t)(y & 0xff);
                 hi[j] = (uint8_t)(y >> 8);
             }
-            const uint32_t o = tc::toff(tid, c);
             *reinterpret_cast<uint4 *>(Ys + o) = *reinterpret_cast<uint4 *>(lo);
             *reinterpret_cast<uint4 *>(Ys + PB + o) = *reinterpret_cast<uint4 *>(hi);
-            while (q < qe) {
-                const uint32_t col = a.cd_col[q];
-                if (col >= jbase + c + 16) break;
-                const uint32_t oo = tc::toff(tid, col - jbase);
-                uint32_t y = Ys[oo] | (Ys[PB + oo] << 8);
-                y += a.cd_val[q];
-                if (y >= p) y -= p;
-                Ys[oo] = (uint8_t)(y & 0xff);
-                Ys[PB + oo] = (uint8_t)(y >> 8);
-                q++;
-            }
         }
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
+        SWEEP_MARK(4);
         // stage 2: X_J = Y inv(A_JJ)
         if (tid == 0) {
             tc::mbar_wait(&invbar, ph_inv);
@@ -306,35 +348,40 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         tc::mbar_wait(&accbar, ph_acc);
         ph_acc ^= 1;
         tc::fence_after();
-        // epilogue 2: X_J -> limb-plane tile (global) [+ C' u16], op counts
+        SWEEP_MARK(5);
+        // epilogue 2: X_J -> limb-plane tile (global) [+ C' u16], op counts (Alg 2 count)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 16) {
             uint64_t S[16];
             read_S(lane_addr, c, S);
             uint8_t lo[16], hi[16];
+            uint16_t xs[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
                 const uint32_t x = fmod64(S[j], a.F);
                 lo[j] = (uint8_t)(x & 0xff);
                 hi[j] = (uint8_t)(x >> 8);
-                const uint32_t jg = jbase + c + j;
-                if (live && jg < (uint64_t)a.npiv) {
-                    if (x) {
-                        opsA += a.ab_np[jg] - 1;
-                        opsB += a.ab_w[jg] - a.ab_np[jg];
-                    }
-                    if (a.X16) a.X16[(size_t)t * a.ldX + jg] = (uint16_t)x;
+                xs[j] = (uint16_t)x;
+                if (x && live) {
+                    opsA += s_np[c + j] - 1;
+                    opsB += s_w[c + j] - s_np[c + j];
                 }
             }
             const uint32_t o = tc::toff(tid, c);
             *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo);
             *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi);
+            if (a.X16 && live) {
+#pragma unroll
+                for (int j = 0; j < 16; j++)
+                    if (jbase + c + j < (uint64_t)a.npiv) a.X16[(size_t)t * a.ldX + jbase + c + j] = xs[j];
+            }
         }
-        tc::fence_async_all();
+        tc::fence_async_all();     // X_J is read by later steps through the async proxy
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
+        SWEEP_MARK(6);
     }
     for (int o = 16; o; o >>= 1) {
         opsA += __shfl_xor_sync(0xffffffffu, opsA, o);
@@ -553,17 +600,48 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
             GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
             attr = true;
         }
+        // C tiles into the X tile storage
+        uint32_t *pos;
+        GBLA_TRY(dalloc_t(h, h->mN, &pos));
+        GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)bt->ntiles * bt->NB * TB, st));
+        k_pos<<<grid_for(h->mN, 256), 256, 0, st>>>(h->mN, h->order, pos);
+        k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, bt->NB, pos, h->cd_ptr, h->cd_col, h->cd_val,
+                                                           h->cd_np, bt->Xt);
+        note_launch(2);
         SweepArgs a;
         a.mN = h->mN; a.npiv = h->npiv; a.NB = bt->NB; a.F = h->F;
         a.order = h->order; a.tlead = h->tlead;
-        a.cd_ptr = h->cd_ptr; a.cd_col = h->cd_col; a.cd_val = h->cd_val; a.cd_np = h->cd_np;
         a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
         a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
         a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
         a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
+        const bool trace = getenv("GBLA_SWEEP_TRACE") != nullptr && bt->ntiles <= 256;
+        a.trace = nullptr;
+        if (trace) {
+            GBLA_TRY(dalloc_t(h, (size_t)bt->NB * 256 * 8, &a.trace));
+            GBLA_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)bt->NB * 256 * 8 * 8, st));
+        }
         k_sweep<<<(unsigned)bt->ntiles, 128, SWEEP_SMEM, st>>>(a);
         note_launch();
         GBLA_CUDA_TRY(cudaGetLastError());
+        if (trace) {   // diagnostics: mean cycles per phase over (J, CTA)
+            std::vector<unsigned long long> tr((size_t)bt->NB * 256 * 8);
+            GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
+            GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+            double sum[6] = {0, 0, 0, 0, 0, 0};
+            long cnt = 0;
+            for (size_t e = 0; e < (size_t)bt->NB * 256; e++) {
+                const unsigned long long *tt = &tr[e * 8];
+                if (!tt[0] || !tt[6]) continue;
+                for (int k = 0; k < 6; k++) sum[k] += (double)(tt[k + 1] - tt[k]);
+                cnt++;
+            }
+            if (cnt)
+                fprintf(stderr,
+                        "[gbla sweep trace] %ld CTA-steps, mean cycles: setup %.0f  stage1-issue %.0f  stage1-wait %.0f"
+                        "  epi1 %.0f  stage2 %.0f  epi2 %.0f\n",
+                        cnt, sum[0] / cnt, sum[1] / cnt, sum[2] / cnt, sum[3] / cnt, sum[4] / cnt, sum[5] / cnt);
+        }
     }
     bt->swept = true;
     unsigned long long ops[2] = {0, 0};

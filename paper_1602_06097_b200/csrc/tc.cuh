@@ -133,4 +133,10 @@ __host__ __device__ __forceinline__ uint32_t toff(uint32_t r, uint32_t k)
     return (k >> 4) * 2048u + (r >> 3) * 128u + (r & 7u) * 16u + (k & 15u);
 }
 
+// same for a 64-row plane (B tiles of the 128 x 64 modular GEMM)
+__host__ __device__ __forceinline__ uint32_t toff64(uint32_t r, uint32_t k)
+{
+    return (k >> 4) * 1024u + (r >> 3) * 128u + (r & 7u) * 16u + (k & 15u);
+}
+
 }  // namespace tc

@@ -9,13 +9,24 @@
 //   S = 65536*HH + 256*X + LL  <  2^40
 // in u64 and reduces it once mod p (Barrett).  4 u8 MACs per modMAC.
 //
-// Tile: BM = 128 rows (TMEM lanes) x BN = 64 columns, K = 128.  TMEM holds
-// three accumulators HH | X | LL (3 x 64 columns of a 256-column
-// allocation).  One thread issues 16 MMAs (4 K-steps of 32 x 4 limb
-// products), commits to an mbarrier; 4 warps run the epilogue
-// (tcgen05.ld 32x32b: warp w owns lanes 32w..32w+31).
+// Operands live in HBM as PRE-TILED limb planes: an A tile is 128 rows x
+// 128 K (16 KB per plane), a B tile 64 columns x 128 K (8 KB per plane), each
+// already in the tcgen05 K-major SWIZZLE_NONE core-matrix layout, so one
+// cp.async.bulk (TMA bulk copy, SASS UBLKCP) per plane stages it.
+//
+// Persistent kernel: CTA b (128 threads) owns a contiguous range of output
+// tiles (BM = 128 rows x BN = 64 columns) in row-tile-major order, so the A
+// tile of a row tile is fetched once and reused for all of its column tiles
+// (a stage re-copies A only when its row tile changes); the next tile's
+// operands are double-buffered behind the current MMAs.  TMEM holds
+// HH | X | LL (3 x 64 columns of a 256-column allocation); one thread issues
+// 16 MMAs (4 K-steps x 4 limb products) and commits to an mbarrier; 4 warps
+// run the epilogue: tcgen05.ld (warp w owns lanes 32w..32w+31), reduce mod
+// p, stage the 128 x 64 result in shared memory (XOR-swizzled 16-byte
+// chunks), then read-modify-write C one full 128-byte row segment per warp
+// instruction.
 //   MODE_SUB    C[rowidx[i], x] = C - S   mod p     (trailing update)
-//   MODE_STORE  O[i, x] = S mod p, plus the transposed limb planes of O
+//   MODE_STORE  O[i, x] = S mod p, plus O's limb planes as B tiles
 //               (the B operand of a following MODE_SUB GEMM)
 #include "internal.cuh"
 #include "tc.cuh"
@@ -23,143 +34,154 @@
 namespace {
 
 constexpr int BM = 128, BN = 64, KP = 128;
-constexpr int SMEM_A = BM * KP;     // bytes per limb plane
-constexpr int SMEM_B = BN * KP;
-constexpr int SMEM_TOTAL = 2 * SMEM_A + 2 * SMEM_B;
+constexpr uint32_t A_PLANE = BM * KP;      // 16 KB
+constexpr uint32_t B_PLANE = BN * KP;      // 8 KB
+constexpr uint32_t A_BYTES = 2 * A_PLANE, B_BYTES = 2 * B_PLANE;
+constexpr uint32_t STAGE = A_BYTES + B_BYTES;   // 48 KB
+constexpr int SMEM_TOTAL = 2 * STAGE;
 enum { MODE_SUB = 0, MODE_STORE = 1 };
+
+using tc::toff64;
+
 
 template <int MODE>
 __global__ void __launch_bounds__(128) k_modgemm_tc(
     int64_t nrows, const uint32_t *__restrict__ nrows_dev, int64_t cols, Field F,
-    const uint8_t *__restrict__ Alo, const uint8_t *__restrict__ Ahi,     // [rows_pad][KP]
-    const uint8_t *__restrict__ Blo, const uint8_t *__restrict__ Bhi,     // [cols_pad][KP]
+    const uint8_t *__restrict__ Alo, const uint8_t *__restrict__ Ahi,     // A tiles (row tile rt at rt*A_PLANE)
+    const uint8_t *__restrict__ Blo, const uint8_t *__restrict__ Bhi,     // B tiles (col tile ct at ct*B_PLANE)
     const uint32_t *__restrict__ rowidx, uint16_t *__restrict__ C, int64_t ldc,
-    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,                 // MODE_STORE: [cols_pad][KP]
-    bool vec)                                                             // C rows 32-byte aligned
+    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi)                 // MODE_STORE: output B tiles
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sAh = smem, *sAl = smem + SMEM_A, *sBh = smem + 2 * SMEM_A, *sBl = smem + 2 * SMEM_A + SMEM_B;
-    __shared__ uint64_t bar;
+    __shared__ uint64_t full[2], accbar;
     __shared__ uint32_t tmem_base;
     const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : nrows;
-    const int64_t row0 = (int64_t)blockIdx.y * BM;
-    const int64_t x0 = (int64_t)blockIdx.x * BN;
-    if (row0 >= nr || x0 >= cols) return;
+    const int64_t ntr = (nr + BM - 1) / BM, ntc = (cols + BN - 1) / BN, ntiles = ntr * ntc;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t_begin = (int64_t)blockIdx.x * per;
+    const int64_t t_end = t_begin + per < ntiles ? t_begin + per : ntiles;
+    if (t_begin >= t_end) return;
     const int tid = threadIdx.x, warp = tid >> 5;
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc % 8 == 0);   // 16-byte row segments
 
     if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
-    if (tid == 0) tc::mbar_init(&bar, 1);
-
-    // A tile -> core-matrix layout: chunk (row r, k16 q) at q*BM*16 + (r/8)*128 + (r%8)*16
-    for (int i = tid; i < BM * (KP / 16); i += 128) {
-        const int r = i >> 3, q = i & 7;
-        uint4 vh = make_uint4(0, 0, 0, 0), vl = vh;
-        if (row0 + r < nr) {
-            const size_t g = (size_t)(row0 + r) * KP + q * 16;
-            vh = *reinterpret_cast<const uint4 *>(Ahi + g);
-            vl = *reinterpret_cast<const uint4 *>(Alo + g);
-        }
-        const int o = q * (BM * 16) + (r >> 3) * 128 + (r & 7) * 16;
-        *reinterpret_cast<uint4 *>(sAh + o) = vh;
-        *reinterpret_cast<uint4 *>(sAl + o) = vl;
+    if (tid == 0) {
+        tc::mbar_init(&full[0], 1);
+        tc::mbar_init(&full[1], 1);
+        tc::mbar_init(&accbar, 1);
     }
-    for (int i = tid; i < BN * (KP / 16); i += 128) {
-        const int x = i >> 3, q = i & 7;
-        uint4 vh = make_uint4(0, 0, 0, 0), vl = vh;
-        if (x0 + x < cols) {
-            const size_t g = (size_t)(x0 + x) * KP + q * 16;
-            vh = *reinterpret_cast<const uint4 *>(Bhi + g);
-            vl = *reinterpret_cast<const uint4 *>(Blo + g);
-        }
-        const int o = q * (BN * 16) + (x >> 3) * 128 + (x & 7) * 16;
-        *reinterpret_cast<uint4 *>(sBh + o) = vh;
-        *reinterpret_cast<uint4 *>(sBl + o) = vl;
-    }
-    tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_base;
-
-    if (tid == 0) {
-        const uint32_t idesc = tc::idesc_u8(BM, BN);
-        const uint32_t aH = tc::smem_u32(sAh), aL = tc::smem_u32(sAl);
-        const uint32_t bH = tc::smem_u32(sBh), bL = tc::smem_u32(sBl);
-#pragma unroll
-        for (int s = 0; s < KP / 32; s++) {
-            const uint32_t ao = s * 2 * (BM * 16), bo = s * 2 * (BN * 16);
-            const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
-            const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
-            const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
-            const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
-            tc::mma_i8(tbase + 0, dAh, dBh, idesc, s > 0);          // HH
-            tc::mma_i8(tbase + BN, dAh, dBl, idesc, s > 0);         // X
-            tc::mma_i8(tbase + BN, dAl, dBh, idesc, 1);             // X
-            tc::mma_i8(tbase + 2 * BN, dAl, dBl, idesc, s > 0);     // LL
-        }
-        tc::commit(&bar);
-    }
-    tc::mbar_wait(&bar, 0);
-    tc::fence_after();
-
-    // epilogue: thread tid <-> tile row tid <-> TMEM lane tid
-    const int64_t slot = row0 + tid;
-    const bool live = slot < nr;
     const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-    uint16_t *crow = nullptr;
-    if (live) crow = C + (size_t)(MODE == MODE_SUB && rowidx ? rowidx[slot] : slot) * ldc + x0;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-        uint32_t hh[16], xx[16], ll[16];
-        tc::tmem_ld16(lane_addr + c, hh);
-        tc::tmem_ld16(lane_addr + BN + c, xx);
-        tc::tmem_ld16(lane_addr + 2 * BN + c, ll);
-        tc::tmem_wait_ld();
-        if (!live) continue;
-        if (vec && x0 + c + 16 <= cols) {
-            // 32-byte row segments: two 16-byte vector accesses per chunk
-            uint4 v[2];
-            uint16_t *d = reinterpret_cast<uint16_t *>(v);
-            if (MODE == MODE_SUB) {
-                v[0] = *reinterpret_cast<const uint4 *>(crow + c);
-                v[1] = *reinterpret_cast<const uint4 *>(crow + c + 8);
-            }
+    const uint32_t s0 = tc::smem_u32(smem);
+    int64_t stage_rt[2] = {-1, -1};                     // row tile whose A is in each stage (thread 0)
+
+    auto load = [&](int64_t tile, int s) {
+        const int64_t rt = tile / ntc, ct = tile % ntc;
+        uint8_t *st = smem + s * STAGE;
+        const bool needA = stage_rt[s] != rt;
+        tc::mbar_expect_tx(&full[s], needA ? STAGE : B_BYTES);
+        if (needA) {
+            tc::bulk_g2s(st, Ahi + rt * A_PLANE, A_PLANE, &full[s]);
+            tc::bulk_g2s(st + A_PLANE, Alo + rt * A_PLANE, A_PLANE, &full[s]);
+            stage_rt[s] = rt;
+        }
+        tc::bulk_g2s(st + A_BYTES, Bhi + ct * B_PLANE, B_PLANE, &full[s]);
+        tc::bulk_g2s(st + A_BYTES + B_PLANE, Blo + ct * B_PLANE, B_PLANE, &full[s]);
+    };
+    if (tid == 0) load(t_begin, 0);
+    uint32_t ph_full[2] = {0, 0}, ph_acc = 0;
+    int s = 0;
+    for (int64_t tile = t_begin; tile < t_end; tile++, s ^= 1) {
+        const int64_t rt = tile / ntc, ct = tile % ntc;
+        const int64_t row0 = rt * BM, x0 = ct * BN;
+        if (tid == 0) {
+            if (tile + 1 < t_end) load(tile + 1, s ^ 1);   // stage s^1 is free: its MMAs completed last iteration
+            tc::mbar_wait(&full[s], ph_full[s]);
+            tc::fence_after();
+            const uint32_t idesc = tc::idesc_u8(BM, BN);
+            const uint32_t aH = s0 + s * STAGE, aL = aH + A_PLANE, bH = aH + A_BYTES, bL = bH + B_PLANE;
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint64_t S = ((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j];
-                const uint32_t s = fmod64(S, F);
-                if (MODE == MODE_SUB) {
-                    const uint32_t dv = d[j];
-                    d[j] = (uint16_t)(dv >= s ? dv - s : dv + F.p - s);
-                } else {
-                    d[j] = (uint16_t)s;
-                    const int64_t x = x0 + c + j;
-                    Tlo[(size_t)x * KP + slot] = (uint8_t)(s & 0xff);
-                    Thi[(size_t)x * KP + slot] = (uint8_t)(s >> 8);
+            for (int k = 0; k < KP / 32; k++) {
+                const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
+                const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
+                const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
+                const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
+                const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
+                tc::mma_i8(tbase + 0, dAh, dBh, idesc, k > 0);          // HH
+                tc::mma_i8(tbase + BN, dAh, dBl, idesc, k > 0);         // X
+                tc::mma_i8(tbase + BN, dAl, dBh, idesc, 1);             // X
+                tc::mma_i8(tbase + 2 * BN, dAl, dBl, idesc, k > 0);     // LL
+            }
+            tc::commit(&accbar);
+        }
+        ph_full[s] ^= 1;
+        tc::mbar_wait(&accbar, ph_acc);
+        ph_acc ^= 1;
+        tc::fence_after();
+
+        // epilogue part 1: TMEM -> S mod p (thread tid = tile row tid; its 64 results in registers)
+        const int64_t slot = row0 + tid;
+        uint16_t subs[BN];
+#pragma unroll
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t hh[16], xx[16], ll[16];
+            __syncwarp();
+            tc::tmem_ld16(lane_addr + c, hh);
+            tc::tmem_ld16(lane_addr + BN + c, xx);
+            tc::tmem_ld16(lane_addr + 2 * BN + c, ll);
+            tc::tmem_wait_ld();
+            uint16_t *sv = subs + c;
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                sv[j] = (uint16_t)fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], F);
+            if (MODE == MODE_STORE) {
+                // B tile planes of the result: row (= K index) slot, columns x (= MN index)
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t x = (uint32_t)(x0 + c + j);
+                    const size_t o = (size_t)(x / BN) * B_PLANE + toff64(x % BN, (uint32_t)slot);
+                    Tlo[o] = (uint8_t)(sv[j] & 0xff);
+                    Thi[o] = (uint8_t)(sv[j] >> 8);
                 }
             }
-            *reinterpret_cast<uint4 *>(crow + c) = v[0];
-            *reinterpret_cast<uint4 *>(crow + c + 8) = v[1];
-            continue;
         }
+        tc::fence_before();
+        __syncthreads();                  // TMEM free for the next tile's MMAs
+        tc::fence_after();
+        // epilogue part 2: the thread's 128-byte row segment, 8 vector loads in flight
+        if (slot < nr) {
+            uint16_t *crow = C + (size_t)(MODE == MODE_SUB && rowidx ? rowidx[slot] : slot) * ldc + x0;
+            if (vec && x0 + BN <= cols) {
+                uint4 d[BN / 8];
+                if (MODE == MODE_SUB) {
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const int64_t x = x0 + c + j;
-            if (x >= cols) break;
-            const uint64_t S = ((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j];
-            const uint32_t s = fmod64(S, F);
-            if (MODE == MODE_SUB) {
-                const uint32_t d = crow[c + j];
-                crow[c + j] = (uint16_t)(d >= s ? d - s : d + F.p - s);
+                    for (int u = 0; u < BN / 8; u++) d[u] = reinterpret_cast<const uint4 *>(crow)[u];
+                }
+                uint16_t *dv = reinterpret_cast<uint16_t *>(d);
+#pragma unroll
+                for (int j = 0; j < BN; j++) {
+                    const uint32_t sv = subs[j];
+                    if (MODE == MODE_SUB) {
+                        const uint32_t x = dv[j];
+                        dv[j] = (uint16_t)(x >= sv ? x - sv : x + F.p - sv);
+                    } else {
+                        dv[j] = (uint16_t)sv;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < BN / 8; u++) reinterpret_cast<uint4 *>(crow)[u] = d[u];
             } else {
-                crow[c + j] = (uint16_t)s;
-                Tlo[(size_t)x * KP + slot] = (uint8_t)(s & 0xff);
-                Thi[(size_t)x * KP + slot] = (uint8_t)(s >> 8);
+                for (int j = 0; j < BN && x0 + j < cols; j++) {
+                    const uint32_t sv = subs[j];
+                    const uint32_t x = crow[j];
+                    crow[j] = (uint16_t)(MODE == MODE_SUB ? (x >= sv ? x - sv : x + F.p - sv) : sv);
+                }
             }
         }
     }
-    tc::fence_before();
-    __syncthreads();
     if (warp == 0) tc::tmem_dealloc<256>(tbase);
 }
 
@@ -179,7 +201,7 @@ __global__ void k_modgemm_int(int64_t rows, int64_t cols, int64_t K, Field F, co
     *c = (uint16_t)(d >= s ? d - s : d + F.p - s);
 }
 
-// rows x K (lda) u16 -> limb planes [rows_pad][KP], zero padded
+// rows x K (lda) u16 -> A tiles (limb planes), zero padded
 __global__ void k_split_rows(int64_t rows, int64_t rows_pad, int64_t K, const uint16_t *__restrict__ A, int64_t lda,
                              uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
 {
@@ -187,40 +209,53 @@ __global__ void k_split_rows(int64_t rows, int64_t rows_pad, int64_t K, const ui
     if (idx >= rows_pad * KP) return;
     const int64_t i = idx / KP, k = idx % KP;
     const uint16_t v = (i < rows && k < K) ? A[i * lda + k] : 0;
-    lo[idx] = (uint8_t)(v & 0xff);
-    hi[idx] = (uint8_t)(v >> 8);
+    const size_t o = (size_t)(i / BM) * A_PLANE + tc::toff((uint32_t)(i % BM), (uint32_t)k);
+    lo[o] = (uint8_t)(v & 0xff);
+    hi[o] = (uint8_t)(v >> 8);
 }
 
-// K x cols (ldb) u16 -> transposed limb planes [cols_pad][KP], zero padded
+// K x cols (ldb) u16 -> B tiles (limb planes, K-major), zero padded
 __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, const uint16_t *__restrict__ B, int64_t ldb,
                              uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= cols_pad * KP) return;
-    const int64_t x = idx / KP, k = idx % KP;
+    const int64_t x = idx % cols_pad, k = idx / cols_pad;
     const uint16_t v = (x < cols && k < K) ? B[k * ldb + x] : 0;
-    lo[idx] = (uint8_t)(v & 0xff);
-    hi[idx] = (uint8_t)(v >> 8);
+    const size_t o = (size_t)(x / BN) * B_PLANE + toff64((uint32_t)(x % BN), (uint32_t)k);
+    lo[o] = (uint8_t)(v & 0xff);
+    hi[o] = (uint8_t)(v >> 8);
 }
+
+template <int MODE>
+gbla_status set_attr()
+{
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           SMEM_TOTAL));
+        attr = true;
+    }
+    return GBLA_OK;
+}
+
+int g_sms = 148;
 
 }  // namespace
 
-// host launchers used by echelon.cu
+// ---- host launchers used by echelon.cu -------------------------------------
+// A tiles: rows grouped by 128 (A_PLANE bytes per plane per tile); B tiles:
+// columns grouped by 64 (B_PLANE bytes per plane per tile).
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc)
 {
-    static bool attr = false;
-    if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_tc<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           SMEM_TOTAL));
-        attr = true;
-    }
+    GBLA_TRY(set_attr<MODE_SUB>());
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
-    dim3 grid(grid_for(cols, BN), grid_for(max_rows, BM));
-    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 31) == 0) && (ldc % 16 == 0);
-    k_modgemm_tc<MODE_SUB><<<grid, 128, SMEM_TOTAL, st>>>(max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx,
-                                                          C, ldc, nullptr, nullptr, vec);
+    const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
+    const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
+    k_modgemm_tc<MODE_SUB><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi,
+                                                                    rowidx, C, ldc, nullptr, nullptr);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -230,21 +265,18 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi)
 {
-    static bool attr = false;
-    if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_tc<MODE_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           SMEM_TOTAL));
-        attr = true;
-    }
+    GBLA_TRY(set_attr<MODE_STORE>());
     if (cols <= 0) return GBLA_OK;
-    dim3 grid(grid_for(cols, BN), 1);
-    const bool vec = ((reinterpret_cast<uintptr_t>(O) & 31) == 0) && (ldo % 16 == 0);
-    k_modgemm_tc<MODE_STORE><<<grid, 128, SMEM_TOTAL, st>>>(BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo,
-                                                            Tlo, Thi, vec);
+    const int64_t tiles = (cols + BN - 1) / BN;
+    const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
+    k_modgemm_tc<MODE_STORE><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi,
+                                                                      nullptr, O, ldo, Tlo, Thi);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }
+
+void modgemm_set_sms(int sms) { g_sms = sms > 0 ? sms : 148; }
 
 // ---- C ABI: K11 as a standalone op -------------------------------------
 extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K,
@@ -260,6 +292,7 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
     if (rows == 0 || cols == 0) return GBLA_OK;
     cudaStream_t st = (cudaStream_t)stream;
     GBLA_CUDA_TRY(cudaSetDevice(ctx->device));
+    modgemm_set_sms(ctx->sm_count);
     const Field F = make_field(p);
     if (engine == 1) {
         dim3 g(grid_for(cols, 128), (unsigned)rows);
