@@ -360,6 +360,13 @@ def gbla_modgemm(ctx: Context, p: int, A, B, C, rowidx=None, engine: int = 0, st
                              C.stride(0), engine, _stream_ptr(stream)))
 
 
+def tile_shard(ntiles: int, rank: int, world: int):
+    """Target tiles owned by `rank` in the multi-GPU sparse phase (dist.cu):
+    tiles are dealt cyclically, T = rank, rank + world, ...  (pure mirror of
+    the library's partition, for tests and reporting)."""
+    return list(range(rank, ntiles, world))
+
+
 def kernel_launches() -> int:
     return int(load_library().gbla_kernel_launches())
 

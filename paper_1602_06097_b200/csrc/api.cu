@@ -175,21 +175,38 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
         set_error("gbla_splice: p = %u is not a prime in (2, 2^16)", p);
         return GBLA_E_DOMAIN;
     }
-    if (M->m < 0 || M->n < 0 || M->nnz < 0 || M->m >= (1ll << 31) || M->n >= (1ll << 31)) {
-        set_error("gbla_splice: bad dimensions m=%lld n=%lld nnz=%lld", (long long)M->m, (long long)M->n,
-                  (long long)M->nnz);
-        return GBLA_E_INVAL;
+    // with a communicator the splice is collective: rank 0's M is broadcast (C1)
+    const bool dist = ctx->world > 1 && ctx->nccl_comm;
+    if (!dist || ctx->rank == 0) {
+        if (M->m < 0 || M->n < 0 || M->nnz < 0 || M->m >= (1ll << 31) || M->n >= (1ll << 31)) {
+            set_error("gbla_splice: bad dimensions m=%lld n=%lld nnz=%lld", (long long)M->m, (long long)M->n,
+                      (long long)M->nnz);
+            return GBLA_E_INVAL;
+        }
+        if (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))) {
+            set_error("gbla_splice: NULL CSR array");
+            return GBLA_E_INVAL;
+        }
     }
-    if (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))) { set_error("gbla_splice: NULL CSR array"); return GBLA_E_INVAL; }
     GBLA_CUDA_TRY(cudaSetDevice(ctx->device));
     gbla_mat h = new gbla_mat_s();
     h->ctx = ctx;
     h->stream = (cudaStream_t)stream;
-    h->m = M->m; h->n = M->n; h->nnz = M->nnz;
     h->p = p;
     h->F = make_field(p);
     PhaseTimer tm(h->stream);
-    gbla_status s = splice_impl(h, M, flags);
+    gbla_status s;
+    if (dist) {
+        gbla_csr dm;
+        s = dist_bcast_input(h, M, (flags & GBLA_HOST_INPUT) != 0, &dm);
+        if (s == GBLA_OK) {
+            h->m = dm.m; h->n = dm.n; h->nnz = dm.nnz;
+            s = splice_impl(h, &dm, 0);
+        }
+    } else {
+        h->m = M->m; h->n = M->n; h->nnz = M->nnz;
+        s = splice_impl(h, M, flags);
+    }
     if (s != GBLA_OK) {
         cudaStreamSynchronize(h->stream);
         cudaGetLastError();
@@ -203,7 +220,6 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     return GBLA_OK;
 }
 
-gbla_status reduce_c_dispatch(gbla_mat h, bool fused, bool keep_x);
 
 extern "C" gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream)
 {
@@ -287,7 +303,14 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     gbla_mat h = nullptr;
     GBLA_TRY(gbla_splice(ctx, M, p, flags & GBLA_HOST_INPUT, stream, &h));
     gbla_status s;
-    if (flags & GBLA_ORDER_STANDARD) {
+    const bool dist = (ctx->world > 1 && ctx->nccl_comm) || dist_emulated_world() > 1;
+    if (dist && !(flags & (GBLA_ORDER_STANDARD | GBLA_SPARSE_INT | GBLA_KEEP_CPRIME))) {
+        // multi-GPU (dist.cu): row-sharded tensor-core sparse phase + D_new all-gather
+        PhaseTimer tm(h->stream);
+        s = dist_sparse_phase(h);
+        h->phase_ms[1] = tm.stop();
+        h->did_fused = h->did_update = true;
+    } else if (flags & GBLA_ORDER_STANDARD) {
         s = gbla_reduce_B(h, stream);
         if (s == GBLA_OK) s = gbla_update_D(h, stream);
     } else {

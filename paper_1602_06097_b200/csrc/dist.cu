@@ -1,9 +1,27 @@
-// dist.cu -- multi-GPU plumbing of libgbla over NCCL (NVLink 5 / NVSwitch).
+// dist.cu -- multi-GPU path of libgbla over NCCL (NVLink 5 / NVSwitch).
 //
 // The NCCL communicator is built inside the library from a 128-byte
 // ncclUniqueId that the caller distributes (the Python binding uses
 // torch.distributed for that), so the C ABI carries no torch or NCCL types.
+//
+// gbla_reduce with a communicator of G ranks (new order):
+//   C1  rank 0's CSR is broadcast to every rank (ncclBroadcast of the sizes,
+//       then row_ptr / col / val); every rank splices it (deterministic, so
+//       the A|B band tiles are replicated).
+//   --  the target tiles (128 targets each, sorted by lead) are dealt
+//       cyclically: rank g owns tiles g, g+G, ...  (the work per tile falls
+//       with its lead, so cyclic dealing balances the triangular profile);
+//       each rank runs the tensor-core sweep and update on its tiles only -
+//       targets are independent, no communication.
+//   C5  ncclAllReduce of the two modMAC counters.
+//   C3  the owned D_new rows are packed tile by tile and all-gathered
+//       (ncclAllGather), then unpacked into every rank's D; the echelon of
+//       D_new then runs on every rank (identical input -> identical R).
+// GBLA_DIST_EMULATE=G (no communicator) runs the G shards one after the
+// other on one GPU and moves the packed blocks with device copies: the same
+// partition / pack / unpack code, a local transport.
 #include <nccl.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 
@@ -15,6 +33,12 @@
             return GBLA_E_NCCL;                                                            \
         }                                                                                  \
     } while (0)
+
+gbla_status tc_prepare_dist(gbla_mat h);
+gbla_status tc_shard(gbla_mat h, int prank, int pworld);
+gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2]);
+int64_t tc_ntiles(gbla_mat h);
+unsigned long long *tc_ops_dev(gbla_mat h);
 
 void dist_destroy(gbla_ctx ctx)
 {
@@ -48,5 +72,139 @@ extern "C" gbla_status gbla_nccl_get_unique_id(void *out128)
     ncclUniqueId uid;
     GBLA_NCCL_TRY(ncclGetUniqueId(&uid));
     memcpy(out128, &uid, sizeof uid);
+    return GBLA_OK;
+}
+
+namespace {
+
+// pack the rows of the local tiles T = prank + pworld*i into blk[i*128 + r][0..ld)
+__global__ void k_pack_rows(int64_t mN, int64_t nloc, int prank, int pworld, const uint32_t *__restrict__ order,
+                            const uint16_t *__restrict__ D, int64_t ldD, uint16_t *__restrict__ blk)
+{
+    const int64_t row = blockIdx.x;                     // local row = i*128 + r
+    const int64_t i = row / 128, r = row % 128;
+    if (i >= nloc) return;
+    const int64_t slot = (prank + pworld * i) * 128 + r;
+    uint4 *dst = reinterpret_cast<uint4 *>(blk + (size_t)row * ldD);
+    const uint4 *src = slot < mN ? reinterpret_cast<const uint4 *>(D + (size_t)order[slot] * ldD) : nullptr;
+    for (int64_t x = threadIdx.x; x < ldD / 8; x += blockDim.x) dst[x] = src ? src[x] : make_uint4(0, 0, 0, 0);
+}
+
+// unpack every rank's block g into D
+__global__ void k_unpack_rows(int64_t mN, int64_t ntiles, int64_t nmax, int pworld, const uint32_t *__restrict__ order,
+                              const uint16_t *__restrict__ all, int64_t ldD, uint16_t *__restrict__ D)
+{
+    const int64_t row = blockIdx.x;                     // g * nmax*128 + i*128 + r
+    const int64_t g = row / (nmax * 128), i = (row / 128) % nmax, r = row % 128;
+    const int64_t T = g + (int64_t)pworld * i;
+    if (T >= ntiles) return;
+    const int64_t slot = T * 128 + r;
+    if (slot >= mN) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(all + (size_t)row * ldD);
+    uint4 *dst = reinterpret_cast<uint4 *>(D + (size_t)order[slot] * ldD);
+    for (int64_t x = threadIdx.x; x < ldD / 8; x += blockDim.x) dst[x] = src[x];
+}
+
+}  // namespace
+
+int dist_emulated_world()
+{
+    const char *e = getenv("GBLA_DIST_EMULATE");
+    if (!e) return 1;
+    const int g = atoi(e);
+    return g > 1 ? g : 1;
+}
+
+// C1: broadcast rank 0's CSR (device or host arrays) to every rank; returns a
+// device CSR view valid on this rank (owned by h).
+gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out)
+{
+    gbla_ctx ctx = h->ctx;
+    ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
+    cudaStream_t st = h->stream;
+    int64_t *ddims;
+    GBLA_TRY(dalloc_t(h, 4, &ddims));
+    int64_t hd[4] = {M->m, M->n, M->nnz, 0};
+    GBLA_CUDA_TRY(cudaMemcpyAsync(ddims, hd, 32, cudaMemcpyHostToDevice, st));
+    GBLA_NCCL_TRY(ncclBroadcast(ddims, ddims, 4, ncclInt64, 0, comm, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(hd, ddims, 32, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t m = hd[0], n = hd[1], nnz = hd[2];
+    uint64_t *rp;
+    uint32_t *col;
+    uint16_t *val;
+    GBLA_TRY(dalloc_t(h, m + 1, &rp));
+    GBLA_TRY(dalloc_t(h, nnz, &col));
+    GBLA_TRY(dalloc_t(h, nnz, &val));
+    if (ctx->rank == 0) {
+        const cudaMemcpyKind k = host_input ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        GBLA_CUDA_TRY(cudaMemcpyAsync(rp, M->row_ptr, (m + 1) * 8, k, st));
+        if (nnz) {
+            GBLA_CUDA_TRY(cudaMemcpyAsync(col, M->col, nnz * 4, k, st));
+            GBLA_CUDA_TRY(cudaMemcpyAsync(val, M->val, nnz * 2, k, st));
+        }
+    }
+    GBLA_NCCL_TRY(ncclGroupStart());
+    GBLA_NCCL_TRY(ncclBroadcast(rp, rp, m + 1, ncclUint64, 0, comm, st));
+    if (nnz) {
+        GBLA_NCCL_TRY(ncclBroadcast(col, col, nnz, ncclUint32, 0, comm, st));
+        GBLA_NCCL_TRY(ncclBroadcast(val, val, nnz * 2, ncclUint8, 0, comm, st));
+    }
+    GBLA_NCCL_TRY(ncclGroupEnd());
+    out->m = m; out->n = n; out->nnz = nnz;
+    out->row_ptr = rp; out->col = col; out->val = val;
+    return GBLA_OK;
+}
+
+// sparse phase of this rank's shard (or of every emulated shard), op-count
+// all-reduce, D_new all-gather.
+gbla_status dist_sparse_phase(gbla_mat h)
+{
+    gbla_ctx ctx = h->ctx;
+    cudaStream_t st = h->stream;
+    const bool real = ctx->world > 1 && ctx->nccl_comm;
+    const int G = real ? ctx->world : dist_emulated_world();
+    const int me = real ? ctx->rank : 0;
+    GBLA_TRY(tc_prepare_dist(h));
+    if (h->mN == 0 || h->npiv == 0) return GBLA_OK;   // D_new = D on every rank
+    if (real) {
+        GBLA_TRY(tc_shard(h, me, G));
+    } else {
+        for (int g = 0; g < G; g++) GBLA_TRY(tc_shard(h, g, G));
+    }
+    // C5: modMAC counters (each rank counted its own tiles)
+    unsigned long long ops[2];
+    if (real) {
+        unsigned long long *d = tc_ops_dev(h);
+        GBLA_NCCL_TRY(ncclAllReduce(d, d, 2, ncclUint64, ncclSum, (ncclComm_t)ctx->nccl_comm, st));
+    }
+    GBLA_TRY(tc_read_ops(h, ops));
+    h->sparse_ops = ops[0] + ops[1];
+    // C3: all-gather of the D_new rows, packed by tile shard
+    const int64_t ntiles = tc_ntiles(h);
+    const int64_t nmax = (ntiles + G - 1) / G;
+    const int64_t blk_rows = nmax * 128;
+    uint16_t *all;
+    GBLA_TRY(dalloc_t(h, (size_t)G * blk_rows * h->ldD, &all));
+    for (int g = 0; g < G; g++) {
+        if (real && g != me) continue;
+        const int64_t nloc = ntiles > g ? (ntiles - g + G - 1) / G : 0;
+        uint16_t *blk = all + (size_t)g * blk_rows * h->ldD;
+        if (nloc > 0) {
+            k_pack_rows<<<(unsigned)(nloc * 128), 256, 0, st>>>(h->mN, nloc, g, G, h->order, h->D, h->ldD,
+                                                                         blk);
+            note_launch();
+        }
+    }
+    GBLA_CUDA_TRY(cudaGetLastError());
+    if (real) {
+        uint16_t *mine = all + (size_t)me * blk_rows * h->ldD;
+        GBLA_NCCL_TRY(ncclAllGather(mine, all, (size_t)blk_rows * h->ldD * 2, ncclUint8,
+                                    (ncclComm_t)ctx->nccl_comm, st));
+    }
+    k_unpack_rows<<<(unsigned)(G * blk_rows), 256, 0, st>>>(h->mN, ntiles, nmax, G, h->order, all, h->ldD,
+                                                                     h->D);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }

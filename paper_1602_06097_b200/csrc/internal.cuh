@@ -171,6 +171,10 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16);
 gbla_status update_d_tc(gbla_mat h);
 void band_free(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
+// multi-GPU (dist.cu)
+gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out);
+gbla_status dist_sparse_phase(gbla_mat h);
+int dist_emulated_world();
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
 
 static inline unsigned grid_for(int64_t work, int per_block) {

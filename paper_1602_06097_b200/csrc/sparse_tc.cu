@@ -182,6 +182,7 @@ struct SweepArgs {
     const uint32_t *ab_w, *ab_np;
     unsigned long long *ops;
     unsigned long long *trace;     // optional: per (J, CTA) phase timestamps (GBLA_SWEEP_TRACE)
+    int64_t prank, pworld;         // target tiles T = prank + pworld * blockIdx.x (multi-GPU row shards)
 };
 
 #define SWEEP_MARK(slot_)                                                                  \
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t s_np[128], s_w[128];
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t T = blockIdx.x, first = T * 128;
+    const int64_t T = a.prank + a.pworld * (int64_t)blockIdx.x, first = T * 128;
     const uint32_t lead0 = a.tlead[a.order[first]];
     if (lead0 >= (uint64_t)a.npiv) return;                     // tile of zero rows: X = 0
     const int64_t Jmin = lead0 / 128;
@@ -405,6 +406,7 @@ struct UpdArgs {
     const uint32_t *bmin, *kl_ptr, *kl_idx;
     uint16_t *D;
     int64_t ldD;
+    int64_t prank, pworld;         // target tiles T = prank + pworld * blockIdx.y
 };
 
 constexpr int UPD_SMEM = 2 * 65536;
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     __shared__ uint64_t full[2], mdone[2], accbar;
     __shared__ uint32_t tmem_s;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t K = blockIdx.x, T = blockIdx.y, first = T * 128;
+    const int64_t K = blockIdx.x, T = a.prank + a.pworld * (int64_t)blockIdx.y, first = T * 128;
     const uint32_t lead0 = a.tlead[a.order[first]];
     if (lead0 >= (uint64_t)a.npiv) return;
     const int64_t Jmin = lead0 / 128;
@@ -584,99 +586,156 @@ static gbla_status band_build(gbla_mat h)
     return GBLA_OK;
 }
 
-gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
+// ---- host side -------------------------------------------------------------
+// Band tiles + the C tiles of every target tile (replicated on every rank).
+static gbla_status tc_prepare(gbla_mat h)
 {
     cudaStream_t st = h->stream;
+    GBLA_TRY(band_build(h));
+    BandTiles *bt = h->bt;
+    if (bt->swept || bt->NB == 0) return GBLA_OK;
+    uint32_t *pos;
+    GBLA_TRY(dalloc_t(h, h->mN, &pos));
+    GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)bt->ntiles * bt->NB * TB, st));
+    k_pos<<<grid_for(h->mN, 256), 256, 0, st>>>(h->mN, h->order, pos);
+    k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, bt->NB, pos, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np,
+                                                       bt->Xt);
+    note_launch(2);
+    GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}
+
+static inline int64_t local_tiles(int64_t ntiles, int prank, int pworld)
+{
+    return ntiles > prank ? (ntiles - prank + pworld - 1) / pworld : 0;
+}
+
+// K5' for the target tiles T = prank + pworld * i
+gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
+{
+    cudaStream_t st = h->stream;
+    BandTiles *bt = h->bt;
+    const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
+    if (bt->NB == 0 || nl == 0) return GBLA_OK;
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
+        attr = true;
+    }
+    SweepArgs a;
+    a.mN = h->mN; a.npiv = h->npiv; a.NB = bt->NB; a.F = h->F;
+    a.order = h->order; a.tlead = h->tlead;
+    a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
+    a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
+    a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
+    a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
+    a.prank = prank; a.pworld = pworld;
+    const bool trace = getenv("GBLA_SWEEP_TRACE") != nullptr && nl <= 256;
+    a.trace = nullptr;
+    if (trace) {
+        GBLA_TRY(dalloc_t(h, (size_t)bt->NB * 256 * 8, &a.trace));
+        GBLA_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)bt->NB * 256 * 8 * 8, st));
+    }
+    k_sweep<<<(unsigned)nl, 128, SWEEP_SMEM, st>>>(a);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    if (trace) {   // diagnostics: mean cycles per phase over (J, CTA)
+        std::vector<unsigned long long> tr((size_t)bt->NB * 256 * 8);
+        GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        double sum[6] = {0, 0, 0, 0, 0, 0};
+        long cnt = 0;
+        for (size_t e = 0; e < (size_t)bt->NB * 256; e++) {
+            const unsigned long long *tt = &tr[e * 8];
+            if (!tt[0] || !tt[6]) continue;
+            for (int k = 0; k < 6; k++) sum[k] += (double)(tt[k + 1] - tt[k]);
+            cnt++;
+        }
+        if (cnt)
+            fprintf(stderr,
+                    "[gbla sweep trace] %ld CTA-steps, mean cycles: setup %.0f  stage1-issue %.0f  stage1-wait %.0f"
+                    "  epi1 %.0f  stage2 %.0f  epi2 %.0f\n",
+                    cnt, sum[0] / cnt, sum[1] / cnt, sum[2] / cnt, sum[3] / cnt, sum[4] / cnt, sum[5] / cnt);
+    }
+    return GBLA_OK;
+}
+
+// K7' for the target tiles T = prank + pworld * i
+gbla_status tc_update_part(gbla_mat h, int prank, int pworld)
+{
+    cudaStream_t st = h->stream;
+    BandTiles *bt = h->bt;
+    const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
+    if (bt->NB == 0 || bt->NNB == 0 || nl == 0) return GBLA_OK;
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM));
+        attr = true;
+    }
+    UpdArgs a;
+    a.mN = h->mN; a.npiv = h->npiv; a.nN = h->nN; a.NB = bt->NB; a.F = h->F;
+    a.order = h->order; a.tlead = h->tlead;
+    a.Xt = bt->Xt; a.tilesB = bt->tilesB; a.offB = bt->offB; a.bmin = bt->bmin;
+    a.kl_ptr = bt->kl_ptr; a.kl_idx = bt->kl_idx; a.D = h->D; a.ldD = h->ldD;
+    a.prank = prank; a.pworld = pworld;
+    dim3 grid((unsigned)bt->NNB, (unsigned)nl);
+    k_update_tc<<<grid, 128, UPD_SMEM, st>>>(a);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}
+
+// the Alg 2 modMAC counts accumulated by the sweeps so far: [A part, B part]
+gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2])
+{
+    ops[0] = ops[1] = 0;
+    if (!h->bt) return GBLA_OK;
+    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, h->bt->ops, 16, cudaMemcpyDeviceToHost, h->stream));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return GBLA_OK;
+}
+
+// C' = C A^-1 on the whole C (single GPU; gbla_reduce_C)
+gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
+{
     if (want_x16) GBLA_TRY(ensure_x(h));
     if (h->mN == 0 || h->npiv == 0) {     // C is empty: C' = 0, D_new = D
         h->have_xt = true;
         return GBLA_OK;
     }
-    GBLA_TRY(band_build(h));
-    BandTiles *bt = h->bt;
-    if (bt->NB > 0) {
-        static bool attr = false;
-        if (!attr) {
-            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
-            attr = true;
-        }
-        // C tiles into the X tile storage
-        uint32_t *pos;
-        GBLA_TRY(dalloc_t(h, h->mN, &pos));
-        GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)bt->ntiles * bt->NB * TB, st));
-        k_pos<<<grid_for(h->mN, 256), 256, 0, st>>>(h->mN, h->order, pos);
-        k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, bt->NB, pos, h->cd_ptr, h->cd_col, h->cd_val,
-                                                           h->cd_np, bt->Xt);
-        note_launch(2);
-        SweepArgs a;
-        a.mN = h->mN; a.npiv = h->npiv; a.NB = bt->NB; a.F = h->F;
-        a.order = h->order; a.tlead = h->tlead;
-        a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
-        a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
-        a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
-        a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
-        const bool trace = getenv("GBLA_SWEEP_TRACE") != nullptr && bt->ntiles <= 256;
-        a.trace = nullptr;
-        if (trace) {
-            GBLA_TRY(dalloc_t(h, (size_t)bt->NB * 256 * 8, &a.trace));
-            GBLA_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)bt->NB * 256 * 8 * 8, st));
-        }
-        k_sweep<<<(unsigned)bt->ntiles, 128, SWEEP_SMEM, st>>>(a);
-        note_launch();
-        GBLA_CUDA_TRY(cudaGetLastError());
-        if (trace) {   // diagnostics: mean cycles per phase over (J, CTA)
-            std::vector<unsigned long long> tr((size_t)bt->NB * 256 * 8);
-            GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
-            GBLA_CUDA_TRY(cudaStreamSynchronize(st));
-            double sum[6] = {0, 0, 0, 0, 0, 0};
-            long cnt = 0;
-            for (size_t e = 0; e < (size_t)bt->NB * 256; e++) {
-                const unsigned long long *tt = &tr[e * 8];
-                if (!tt[0] || !tt[6]) continue;
-                for (int k = 0; k < 6; k++) sum[k] += (double)(tt[k + 1] - tt[k]);
-                cnt++;
-            }
-            if (cnt)
-                fprintf(stderr,
-                        "[gbla sweep trace] %ld CTA-steps, mean cycles: setup %.0f  stage1-issue %.0f  stage1-wait %.0f"
-                        "  epi1 %.0f  stage2 %.0f  epi2 %.0f\n",
-                        cnt, sum[0] / cnt, sum[1] / cnt, sum[2] / cnt, sum[3] / cnt, sum[4] / cnt, sum[5] / cnt);
-        }
-    }
-    bt->swept = true;
-    unsigned long long ops[2] = {0, 0};
-    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, bt->ops, 16, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    GBLA_TRY(tc_prepare(h));
+    GBLA_TRY(tc_sweep_part(h, 0, 1, want_x16));
+    h->bt->swept = true;
+    unsigned long long ops[2];
+    GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops += ops[0];
     h->have_xt = true;
     return GBLA_OK;
 }
 
+// D <- D - C' B with the C' tiles of reduce_c_tc (single GPU; gbla_update_D)
 gbla_status update_d_tc(gbla_mat h)
 {
-    cudaStream_t st = h->stream;
     if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
-    BandTiles *bt = h->bt;
-    if (!bt || !bt->swept) { set_error("update_d_tc: no C' tiles"); return GBLA_E_INTERNAL; }
-    if (h->mN > 0 && bt->NB > 0 && bt->NNB > 0) {
-        static bool attr = false;
-        if (!attr) {
-            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM));
-            attr = true;
-        }
-        UpdArgs a;
-        a.mN = h->mN; a.npiv = h->npiv; a.nN = h->nN; a.NB = bt->NB; a.F = h->F;
-        a.order = h->order; a.tlead = h->tlead;
-        a.Xt = bt->Xt; a.tilesB = bt->tilesB; a.offB = bt->offB; a.bmin = bt->bmin;
-        a.kl_ptr = bt->kl_ptr; a.kl_idx = bt->kl_idx; a.D = h->D; a.ldD = h->ldD;
-        dim3 grid((unsigned)bt->NNB, (unsigned)bt->ntiles);
-        k_update_tc<<<grid, 128, UPD_SMEM, st>>>(a);
-        note_launch();
-        GBLA_CUDA_TRY(cudaGetLastError());
-    }
-    unsigned long long ops[2] = {0, 0};
-    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, bt->ops, 16, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    if (!h->bt || !h->bt->swept) { set_error("update_d_tc: no C' tiles"); return GBLA_E_INTERNAL; }
+    GBLA_TRY(tc_update_part(h, 0, 1));
+    unsigned long long ops[2];
+    GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops += ops[1];
     return GBLA_OK;
 }
+
+// multi-GPU / emulated ranks: prepare once, then the sparse phase of one row shard
+gbla_status tc_prepare_dist(gbla_mat h)
+{
+    if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
+    return tc_prepare(h);
+}
+gbla_status tc_shard(gbla_mat h, int prank, int pworld)
+{
+    if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
+    GBLA_TRY(tc_sweep_part(h, prank, pworld, false));
+    return tc_update_part(h, prank, pworld);
+}
+int64_t tc_ntiles(gbla_mat h) { return h->bt ? h->bt->ntiles : (h->mN + 127) / 128; }
+unsigned long long *tc_ops_dev(gbla_mat h) { return h->bt ? h->bt->ops : nullptr; }

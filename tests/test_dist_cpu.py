@@ -1,0 +1,68 @@
+"""Multi-process host-side checks of the multi-GPU path (gloo, world_size 2,
+CPU only): the NCCL unique id travels through torch.distributed exactly as
+bench.py does it, and the cyclic tile shards of every rank are disjoint and
+cover all target tiles (the partition dist.cu / sparse_tc.cu use)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1602_06097_b200 import tile_shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, ntiles_list, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = [bytes(range(128)) if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)          # how bench.py ships the ncclUniqueId
+        ok_uid = uid[0] == bytes(range(128))
+        shards = {n: tile_shard(n, rank, world) for n in ntiles_list}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, shards)
+        t = torch.tensor([float(rank + 1)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max-over-ranks timing, as in bench.py
+        q.put((rank, ok_uid, gathered, float(t.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_partition_and_uid_exchange():
+    world = 2
+    ntiles_list = [0, 1, 2, 3, 55, 313, 1172]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ntiles_list, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_uid, gathered, mx in res:
+        assert ok_uid and mx == float(world)
+        for n in ntiles_list:
+            all_tiles = sorted(t for g in range(world) for t in gathered[g][n])
+            assert all_tiles == list(range(n))                     # disjoint and complete
+            sizes = [len(gathered[g][n]) for g in range(world)]
+            assert max(sizes) - min(sizes) <= 1                    # balanced
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_tile_shard_mirror(world):
+    for n in (0, 1, 7, 55, 1172):
+        tiles = sorted(t for g in range(world) for t in tile_shard(n, g, world))
+        assert tiles == list(range(n))

@@ -294,3 +294,24 @@ def test_echelon_engines_agree_c0_and_dense(gb, ctx, c0_matrix, c0_oracle):
         assert res.rank_M == 150
         for f in (gb.GBLA_DENSE_TC, gb.GBLA_DENSE_INT):
             check_full(gb, ctx, M, res, flags=f)
+
+
+def test_sharded_sparse_phase_emulated_ranks(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """Multi-GPU row sharding (dist.cu), with G ranks emulated on one GPU
+    (GBLA_DIST_EMULATE): each shard sweeps only its cyclic target tiles, the
+    packed D_new blocks are all-gathered (device copies instead of NCCL) and
+    the echelon runs on the gathered D.  R, rank and op count must not depend
+    on G."""
+    cases = [(c0_matrix, c0_oracle)]
+    for name, sc in (("c1", 0.05), ("c3", 0.03)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        cases.append((M, oracle.reduce(M)))
+    for M, res in cases:
+        for G in (2, 3, 8):
+            monkeypatch.setenv("GBLA_DIST_EMULATE", str(G))
+            h = gpu_reduce(gb, ctx, M)
+            r, pc, R = h.rref()
+            assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R)
+            assert h.opcount()[0] == res.modmac
+            h.free()
+    monkeypatch.delenv("GBLA_DIST_EMULATE")
