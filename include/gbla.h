@@ -178,6 +178,14 @@ gbla_status gbla_get_phase_ms(gbla_mat h, float *ms5);
 gbla_status gbla_sync(gbla_mat h);
 void gbla_mat_free(gbla_mat h);
 const char *gbla_last_error(void);
+/* Device time of one kernel family, summed over its launches on this handle
+ * (CUDA events on the handle's stream; recorded only when the environment
+ * variable GBLA_KERNEL_TIMERS is set when the handle is created).  which:
+ * 0 = K5' sweep (C' = C A^-1 block forward substitution, tcgen05),
+ * 1 = K7' update (D -= C' B, tcgen05), 2 = K10 panel factorization,
+ * 3 = K11 trailing update of the echelon (tcgen05), 4 = K11 new pivot rows.
+ * Synchronizes the handle's stream. */
+gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int64_t *launches);
 /* Number of libgbla kernels launched by this process so far (diagnostics). */
 uint64_t gbla_kernel_launches(void);
 /* Library build/version string. */

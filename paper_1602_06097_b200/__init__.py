@@ -89,6 +89,7 @@ def load_library(path: str = LIB_PATH):
         "gbla_nccl_get_unique_id": ([vp], st),
         "gbla_kernel_launches": ([], ctypes.c_uint64),
         "gbla_modgemm": ([vp, u32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp], st),
+        "gbla_get_kernel_ms": ([vp, ctypes.c_int, P(ctypes.c_float), P(i64)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -105,7 +106,7 @@ def exported_symbols():
             "gbla_get_dims", "gbla_get_maps", "gbla_get_D", "gbla_get_Cprime", "gbla_get_Bprime",
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
-            "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm"]
+            "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms"]
 
 
 def _check(status: int):
@@ -266,6 +267,18 @@ class Mat:
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         _check(_lib.gbla_get_opcount(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    KERNELS = ("sweep", "update", "panel", "trailing", "rnew")
+
+    def kernel_ms(self):
+        """{family: (ms, launches)} from the library's CUDA-event timers
+        (non-empty only if GBLA_KERNEL_TIMERS was set at handle creation)."""
+        out = {}
+        for i, name in enumerate(self.KERNELS):
+            ms, n = ctypes.c_float(), ctypes.c_int64()
+            _check(_lib.gbla_get_kernel_ms(self._h, i, ctypes.byref(ms), ctypes.byref(n)))
+            out[name] = (ms.value, n.value)
+        return out
 
     def phase_ms(self):
         arr = (ctypes.c_float * 5)()

@@ -194,6 +194,7 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     h->stream = (cudaStream_t)stream;
     h->p = p;
     h->F = make_field(p);
+    h->kt.on = getenv("GBLA_KERNEL_TIMERS") != nullptr;
     PhaseTimer tm(h->stream);
     gbla_status s;
     if (dist) {
@@ -413,6 +414,22 @@ extern "C" gbla_status gbla_get_phase_ms(gbla_mat h, float *ms5)
     return GBLA_OK;
 }
 
+extern "C" gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int64_t *launches)
+{
+    if (!h || which < 0 || which >= KT_N) { set_error("gbla_get_kernel_ms: bad argument"); return GBLA_E_INVAL; }
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const auto &v = h->kt.ev[which];
+    float tot = 0;
+    for (size_t i = 0; i + 1 < v.size(); i += 2) {
+        float t = 0;
+        GBLA_CUDA_TRY(cudaEventElapsedTime(&t, v[i], v[i + 1]));
+        tot += t;
+    }
+    if (ms) *ms = tot;
+    if (launches) *launches = (int64_t)(v.size() / 2);
+    return GBLA_OK;
+}
+
 extern "C" gbla_status gbla_sync(gbla_mat h)
 {
     if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
@@ -427,5 +444,7 @@ extern "C" void gbla_mat_free(gbla_mat h)
     dfree_all(h);
     cudaStreamSynchronize(h->stream);
     band_free(h);
+    for (auto &v : h->kt.ev)
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
     delete h;
 }

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
     uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(dsm32 + (PK + CH) * PK);   // [CH][PK] factors
     __shared__ uint32_t bpc[PK], bsel[PK], crow[CH], selfc[CH];
     __shared__ uint32_t brow[PK];      // physical XA row of basis slot b during a chunk
+    __shared__ uint32_t skey[CH], perm[CH];
     __shared__ uint32_t sinv[PK];
     const uint32_t m32 = 0xffffffffu / F.p;   // 32-bit Barrett: v < 2^32 -> v mod p
     auto mod32 = [&](uint32_t v) -> uint32_t {
@@ -177,8 +178,34 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
             __syncthreads();
         }
         PANEL_LAP(2);
-        // (4) integrate the chunk row by row
-        for (int ci = 0; ci < ncand && nb < (uint32_t)PK; ci++) {
+        // (4a) order the chunk by leading column: in a staircase the rest of the
+        //      chunk is then zero at each new pivot column (no forward work)
+        for (int ci = warp; ci < ncand; ci += 32) {
+            bool nz = false;
+#pragma unroll
+            for (int u = 0; u < CPL; u++) nz |= (XA[PK + ci][lane * CPL + u] & 0xffffu) != 0;
+            const unsigned m = __ballot_sync(FULL, nz);
+            if (lane == 0) {
+                uint32_t key = 0xffffu;
+                if (m) {
+                    const int src = __ffs(m) - 1;
+                    key = src * CPL;
+                    while ((XA[PK + ci][key] & 0xffffu) == 0) key++;
+                }
+                skey[ci] = key;
+            }
+        }
+        __syncthreads();
+        if (tid < ncand) {
+            const uint32_t kc = skey[tid];
+            int rk = 0;
+            for (int j = 0; j < ncand; j++) rk += (skey[j] < kc) || (skey[j] == kc && j < tid);
+            perm[rk] = tid;
+        }
+        __syncthreads();
+        // (4b) integrate the chunk row by row, in that order
+        for (int q = 0; q < ncand && nb < (uint32_t)PK; q++) {
+            const int ci = perm[q];
             const uint32_t *cx = XA[PK + ci];
             bool nz = false;
 #pragma unroll
@@ -195,7 +222,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
             // Basis rows are renormalized once per chunk (below).
             const uint32_t v = cx[c] & 0xffffu;
             const uint32_t sc = selfc[ci];
-            const int nrows = (int)nb + (ncand - ci - 1);
+            const int nrows = (int)nb + (ncand - q - 1);
             if (tid == 0) {
                 // P joins the basis as slot nb (in place; its transform gets sc at index nb)
                 XA[PK + ci][nb] = (XA[PK + ci][nb] & 0xffffu) | (sc << 16);
@@ -204,8 +231,8 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
                 bsel[nb] = crow[ci];
             }
             for (int rr = warp; rr < nrows; rr += 32) {     // one warp per row
-                const int cand = rr - (int)nb;
-                const uint32_t row = rr < (int)nb ? brow[rr] : (uint32_t)(PK + ci + 1 + cand);
+                const int cand = rr < (int)nb ? -1 : perm[q + 1 + (rr - (int)nb)];
+                const uint32_t row = rr < (int)nb ? brow[rr] : (uint32_t)(PK + cand);
                 const uint32_t gl = (lane == (int)(c / CPL)) ? (XA[row][c] & 0xffffu) : 0u;
                 const uint32_t g = __shfl_sync(FULL, gl, c / CPL);
                 if (!g) continue;
@@ -219,7 +246,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
                     const uint32_t a = mod32(mod32(v * (val >> 16)) + ng * pa);
                     XA[row][k] = x | (a << 16);
                 }
-                if (cand >= 0 && lane == 0) selfc[ci + 1 + cand] = mod32(v * selfc[ci + 1 + cand]);
+                if (cand >= 0 && lane == 0) selfc[cand] = mod32(v * selfc[cand]);
             }
             __syncthreads();
             nb++;
@@ -562,17 +589,23 @@ gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, co
     for (int64_t c0 = 0; c0 < nN; c0 += PK) {
         const int64_t width = nN - c0;
         k_cand<PK><<<grid_for(mN, 256), 256, 0, st>>>(mN, nN, c0, h->D, ldD, rowpiv, cflag);
+        kt_mark(h, KT_PANEL);
         k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, Tlo, Thi, invtab,
                                                         cflag, trace);
+        kt_mark(h, KT_PANEL);
         note_launch();
         k_gather<PK, true><<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, nullptr, Flo, Fhi,
                                                              rows);
         k_gather_st<<<dim3(grid_for(width, 128), KPT / 16), 128, 0, st>>>(nN, c0, h->D, ldD, ps, Blo, Bhi);
         note_launch(3);
         // Rn = T * D[S, c0:]  (plus its transposed limb planes)
+        kt_mark(h, KT_RN);
         GBLA_TRY(modgemm_tc_store(st, width, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi));
+        kt_mark(h, KT_RN);
         // D[rows, c0:] -= F * Rn
+        kt_mark(h, KT_TRAIL);
         GBLA_TRY(modgemm_tc_sub(st, mN, &ps->nrows, width, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D + c0, ldD));
+        kt_mark(h, KT_TRAIL);
         k_commit<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->D, ldD, ps, Rn, ldR);
         k_count<PK><<<1, 1, 0, st>>>(width, ps, dops);
         note_launch(2);

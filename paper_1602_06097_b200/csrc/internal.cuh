@@ -89,6 +89,13 @@ struct Alloc {
     size_t bytes;
 };
 
+// per-kernel-family CUDA-event timers (GBLA_KERNEL_TIMERS=1; gbla_get_kernel_ms)
+enum { KT_SWEEP = 0, KT_UPDATE = 1, KT_PANEL = 2, KT_TRAIL = 3, KT_RN = 4, KT_N = 5 };
+struct KTimers {
+    bool on = false;
+    std::vector<cudaEvent_t> ev[KT_N];
+};
+
 struct gbla_mat_s {
     gbla_ctx ctx = nullptr;
     cudaStream_t stream = nullptr;
@@ -147,6 +154,8 @@ struct gbla_mat_s {
     // tensor-core sparse path: dense band tiles of A|B, X tiles (sparse_tc.cu)
     struct BandTiles *bt = nullptr;
 
+    KTimers kt;
+
     std::vector<Alloc> allocs;
 };
 
@@ -171,6 +180,14 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16);
 gbla_status update_d_tc(gbla_mat h);
 void band_free(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
+static inline void kt_mark(gbla_mat h, int which)
+{
+    if (!h->kt.on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, h->stream);
+    h->kt.ev[which].push_back(e);
+}
 // multi-GPU (dist.cu)
 gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out);
 gbla_status dist_sparse_phase(gbla_mat h);

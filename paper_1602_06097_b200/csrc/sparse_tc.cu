@@ -636,7 +636,9 @@ gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
         GBLA_TRY(dalloc_t(h, (size_t)bt->NB * 256 * 8, &a.trace));
         GBLA_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)bt->NB * 256 * 8 * 8, st));
     }
+    kt_mark(h, KT_SWEEP);
     k_sweep<<<(unsigned)nl, 128, SWEEP_SMEM, st>>>(a);
+    kt_mark(h, KT_SWEEP);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     if (trace) {   // diagnostics: mean cycles per phase over (J, CTA)
@@ -679,7 +681,9 @@ gbla_status tc_update_part(gbla_mat h, int prank, int pworld)
     a.kl_ptr = bt->kl_ptr; a.kl_idx = bt->kl_idx; a.D = h->D; a.ldD = h->ldD;
     a.prank = prank; a.pworld = pworld;
     dim3 grid((unsigned)bt->NNB, (unsigned)nl);
+    kt_mark(h, KT_UPDATE);
     k_update_tc<<<grid, 128, UPD_SMEM, st>>>(a);
+    kt_mark(h, KT_UPDATE);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;

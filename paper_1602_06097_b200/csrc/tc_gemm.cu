@@ -122,9 +122,29 @@ __global__ void __launch_bounds__(128) k_modgemm_tc(
         ph_acc ^= 1;
         tc::fence_after();
 
-        // epilogue part 1: TMEM -> S mod p (thread tid = tile row tid; its 64 results in registers)
+        // epilogue: thread tid = tile row tid; its 128-byte row segment of C is
+        // loaded first (8 vector loads in flight), the 4 TMEM chunks are folded in
+        // (constant register indices: no local memory), then stored back
         const int64_t slot = row0 + tid;
-        uint16_t subs[BN];
+        const bool live = slot < nr;
+        uint16_t *crow = live ? C + (size_t)(MODE == MODE_SUB && rowidx ? rowidx[slot] : slot) * ldc + x0 : nullptr;
+        const bool fast = live && vec && x0 + BN <= cols;
+        uint32_t d[BN / 2];                                   // u16 pairs
+#pragma unroll
+        for (int w = 0; w < BN / 2; w++) d[w] = 0;
+        if (MODE == MODE_SUB && live) {
+            if (fast) {
+#pragma unroll
+                for (int u = 0; u < BN / 8; u++) {
+                    const uint4 q = reinterpret_cast<const uint4 *>(crow)[u];
+                    d[4 * u] = q.x; d[4 * u + 1] = q.y; d[4 * u + 2] = q.z; d[4 * u + 3] = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < BN; j++)
+                    if (x0 + j < cols) d[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
+            }
+        }
 #pragma unroll
         for (int c = 0; c < BN; c += 16) {
             uint32_t hh[16], xx[16], ll[16];
@@ -133,53 +153,39 @@ __global__ void __launch_bounds__(128) k_modgemm_tc(
             tc::tmem_ld16(lane_addr + BN + c, xx);
             tc::tmem_ld16(lane_addr + 2 * BN + c, ll);
             tc::tmem_wait_ld();
-            uint16_t *sv = subs + c;
 #pragma unroll
-            for (int j = 0; j < 16; j++)
-                sv[j] = (uint16_t)fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], F);
-            if (MODE == MODE_STORE) {
-                // B tile planes of the result: row (= K index) slot, columns x (= MN index)
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < 16; j += 2) {
+                const uint32_t s0 = fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], F);
+                const uint32_t s1 = fmod64(((uint64_t)hh[j + 1] << 16) + ((uint64_t)xx[j + 1] << 8) + ll[j + 1], F);
+                const int w = (c + j) / 2;
+                if (MODE == MODE_SUB) {
+                    uint32_t lo = d[w] & 0xffffu, hi = d[w] >> 16;
+                    lo = lo >= s0 ? lo - s0 : lo + F.p - s0;
+                    hi = hi >= s1 ? hi - s1 : hi + F.p - s1;
+                    d[w] = lo | (hi << 16);
+                } else {
+                    d[w] = s0 | (s1 << 16);
+                    // B tile planes of the result: row (= K index) slot, columns x (= MN index)
                     const uint32_t x = (uint32_t)(x0 + c + j);
                     const size_t o = (size_t)(x / BN) * B_PLANE + toff64(x % BN, (uint32_t)slot);
-                    Tlo[o] = (uint8_t)(sv[j] & 0xff);
-                    Thi[o] = (uint8_t)(sv[j] >> 8);
+                    Tlo[o] = (uint8_t)(s0 & 0xff);
+                    Thi[o] = (uint8_t)(s0 >> 8);
+                    Tlo[o + 16] = (uint8_t)(s1 & 0xff);         // x+1 -> next core-matrix row (16 bytes on)
+                    Thi[o + 16] = (uint8_t)(s1 >> 8);
                 }
             }
         }
         tc::fence_before();
         __syncthreads();                  // TMEM free for the next tile's MMAs
         tc::fence_after();
-        // epilogue part 2: the thread's 128-byte row segment, 8 vector loads in flight
-        if (slot < nr) {
-            uint16_t *crow = C + (size_t)(MODE == MODE_SUB && rowidx ? rowidx[slot] : slot) * ldc + x0;
-            if (vec && x0 + BN <= cols) {
-                uint4 d[BN / 8];
-                if (MODE == MODE_SUB) {
+        if (fast) {
 #pragma unroll
-                    for (int u = 0; u < BN / 8; u++) d[u] = reinterpret_cast<const uint4 *>(crow)[u];
-                }
-                uint16_t *dv = reinterpret_cast<uint16_t *>(d);
+            for (int u = 0; u < BN / 8; u++)
+                reinterpret_cast<uint4 *>(crow)[u] = make_uint4(d[4 * u], d[4 * u + 1], d[4 * u + 2], d[4 * u + 3]);
+        } else if (live) {
 #pragma unroll
-                for (int j = 0; j < BN; j++) {
-                    const uint32_t sv = subs[j];
-                    if (MODE == MODE_SUB) {
-                        const uint32_t x = dv[j];
-                        dv[j] = (uint16_t)(x >= sv ? x - sv : x + F.p - sv);
-                    } else {
-                        dv[j] = (uint16_t)sv;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < BN / 8; u++) reinterpret_cast<uint4 *>(crow)[u] = d[u];
-            } else {
-                for (int j = 0; j < BN && x0 + j < cols; j++) {
-                    const uint32_t sv = subs[j];
-                    const uint32_t x = crow[j];
-                    crow[j] = (uint16_t)(MODE == MODE_SUB ? (x >= sv ? x - sv : x + F.p - sv) : sv);
-                }
-            }
+            for (int j = 0; j < BN; j++)
+                if (x0 + j < cols) crow[j] = (uint16_t)(d[j / 2] >> (16 * (j & 1)));
         }
     }
     if (warp == 0) tc::tmem_dealloc<256>(tbase);
