@@ -79,11 +79,16 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
 {
     // optional per-panel trace (GBLA_PANEL_TRACE): cycles in scan / load / reduce / integrate,
     // candidates, pivots, chunks
-    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long tmark = clock64();
+    // (kept in shared memory, updated by thread 0 only: no registers held across the loop)
+    __shared__ unsigned long long tr[8];
+    __shared__ long long tmark;
+    if (trace && threadIdx.x == 0) {
+        for (int k = 0; k < 8; k++) tr[k] = 0;
+        tmark = clock64();
+    }
 #define PANEL_LAP(k_)                                                  \
     do {                                                               \
-        if (trace) { const long long t_ = clock64(); tr[k_] += t_ - tmark; tmark = t_; } \
+        if (trace && threadIdx.x == 0) { const long long t_ = clock64(); tr[k_] += t_ - tmark; tmark = t_; } \
     } while (0)
     constexpr int CH = PK;             // candidates per chunk
     constexpr int CPL = PK / 32;       // columns per lane
@@ -95,6 +100,8 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
     __shared__ uint32_t bpc[PK], bsel[PK], crow[CH], selfc[CH];
     __shared__ uint32_t brow[PK];      // physical XA row of basis slot b during a chunk
     __shared__ uint32_t skey[CH], perm[CH];
+    __shared__ uint32_t Ub[32][33], Wb[32][33];   // block of U and its inverse (back substitution)
+    __shared__ uint16_t Gs[PK][32];               // factors of the rows above a block
     __shared__ uint32_t sinv[PK];
     const uint32_t m32 = 0xffffffffu / F.p;   // 32-bit Barrett: v < 2^32 -> v mod p
     auto mod32 = [&](uint32_t v) -> uint32_t {
@@ -136,8 +143,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
         }
         PANEL_LAP(0);
         if (ncand == 0) continue;
-        tr[4] += ncand;
-        tr[6] += 1;
+        if (trace && tid == 0) { tr[4] += ncand; tr[6] += 1; }
         // (2) load the candidates' panel slices
         for (int idx = tid; idx < ncand * PK; idx += 1024) {
             const int ci = idx / PK, k = idx % PK;
@@ -215,14 +221,14 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
             const int src = __ffs(nzm) - 1;
             uint32_t c = src * CPL;
             while ((cx[c] & 0xffffu) == 0) c++;
-            // Fraction-free step (no inverse on the critical path): with the
+            // Forward, fraction-free step (no inverse on the critical path): the
             // pivot row P = candidate ci (pivot value v at column c; its own
-            // transform coefficient sc at index nb), every other row R of the
-            // basis and of the rest of the chunk becomes  v*R - g*P,  g = R[c].
-            // Basis rows are renormalized once per chunk (below).
+            // transform coefficient sc at index nb) joins the basis unreduced,
+            // and every remaining candidate R becomes  v*R - g*P,  g = R[c].
+            // The basis is reduced and normalized afterwards in blocks (4c).
             const uint32_t v = cx[c] & 0xffffu;
             const uint32_t sc = selfc[ci];
-            const int nrows = (int)nb + (ncand - q - 1);
+            const int nrows = ncand - q - 1;
             if (tid == 0) {
                 // P joins the basis as slot nb (in place; its transform gets sc at index nb)
                 XA[PK + ci][nb] = (XA[PK + ci][nb] & 0xffffu) | (sc << 16);
@@ -230,9 +236,9 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
                 bpc[nb] = c;
                 bsel[nb] = crow[ci];
             }
-            for (int rr = warp; rr < nrows; rr += 32) {     // one warp per row
-                const int cand = rr < (int)nb ? -1 : perm[q + 1 + (rr - (int)nb)];
-                const uint32_t row = rr < (int)nb ? brow[rr] : (uint32_t)(PK + cand);
+            for (int rr = warp; rr < nrows; rr += 32) {     // one warp per remaining candidate
+                const int cand = perm[q + 1 + rr];
+                const uint32_t row = (uint32_t)(PK + cand);
                 const uint32_t gl = (lane == (int)(c / CPL)) ? (XA[row][c] & 0xffffu) : 0u;
                 const uint32_t g = __shfl_sync(FULL, gl, c / CPL);
                 if (!g) continue;
@@ -246,23 +252,108 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
                     const uint32_t a = mod32(mod32(v * (val >> 16)) + ng * pa);
                     XA[row][k] = x | (a << 16);
                 }
-                if (cand >= 0 && lane == 0) selfc[cand] = mod32(v * selfc[cand]);
+                if (lane == 0) selfc[cand] = mod32(v * selfc[cand]);
             }
             __syncthreads();
             nb++;
         }
-        // normalize the basis (leading 1 at each pivot column) and compact it into slots [0, nb)
-        if (tid < (int)nb) sinv[tid] = invtab[XA[brow[tid]][bpc[tid]] & 0xffffu];
-        __syncthreads();
+        PANEL_LAP(3);
+        // (4c) compact the basis into slots [0, nb): slot b < nb0 already there
         for (int idx = tid; idx < (int)nb * PK; idx += 1024) {
             const int b = idx / PK, k = idx % PK;
-            const uint32_t val = XA[brow[b]][k], s = sinv[b];
-            XA[b][k] = mod32((val & 0xffffu) * s) | (mod32((val >> 16) * s) << 16);
+            if (brow[b] != (uint32_t)b) XA[b][k] = XA[brow[b]][k];
         }
         __syncthreads();
         if (tid < (int)nb) brow[tid] = tid;
+        // (4d) reduce + normalize the basis, 32-row blocks from the bottom.  U[i][j] =
+        //      row_i at pivot column j is upper triangular (old rows: identity on old
+        //      pivots; new rows: zero at every earlier pivot).  Per block: W = U_bb^-1
+        //      (one warp), block <- W * block, then the block's pivot columns are
+        //      eliminated from every row above (u64 delayed reduction, one mod).
+        for (int r1 = (int)nb; r1 > 0; r1 -= 32) {
+            const int r0 = r1 - 32 > 0 ? r1 - 32 : 0, bs = r1 - r0;
+            __syncthreads();
+            for (int idx = tid; idx < bs * bs; idx += 1024) {
+                const int i = idx / bs, j = idx % bs;
+                Ub[i][j] = XA[r0 + i][bpc[r0 + j]] & 0xffffu;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const int j = lane;
+                if (j < bs) sinv[j] = invtab[Ub[j][j]];
+                __syncwarp();
+                if (j < bs) {
+                    Wb[j][j] = sinv[j];
+                    for (int i = j - 1; i >= 0; i--) {
+                        uint64_t acc = 0;
+                        for (int k = i + 1; k <= j; k++) acc += (uint64_t)Ub[i][k] * Wb[k][j];
+                        Wb[i][j] = fmul(fneg(fmod64(acc, F), F), sinv[i], F);
+                    }
+                    for (int i = j + 1; i < bs; i++) Wb[i][j] = 0;
+                }
+            }
+            // factors of the rows above at the block's pivot columns (before they change)
+            for (int idx = tid; idx < r0 * bs; idx += 1024) {
+                const int r = idx / bs, k = idx % bs;
+                Gs[r][k] = (uint16_t)(XA[r][bpc[r0 + k]] & 0xffffu);
+            }
+            __syncthreads();
+            // block <- W * block  (items: 4 consecutive columns of one block row)
+            static_assert(32 * (PK / 4) <= 1024, "one block-multiply item per thread");
+            uint32_t outv[4];
+            {
+                const int item = tid;
+                if (item < bs * (PK / 4)) {
+                const int i = item / (PK / 4), k0 = (item % (PK / 4)) * 4;
+                uint64_t ax[4] = {0, 0, 0, 0}, aa[4] = {0, 0, 0, 0};
+                for (int k = i; k < bs; k++) {
+                    const uint64_t w = Wb[i][k];
+                    if (!w) continue;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t val = XA[r0 + k][k0 + u];
+                        ax[u] += w * (val & 0xffffu);
+                        aa[u] += w * (val >> 16);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) outv[u] = fmod64(ax[u], F) | (fmod64(aa[u], F) << 16);
+                }
+            }
+            __syncthreads();
+            if (tid < bs * (PK / 4)) {
+                const int i = tid / (PK / 4), k0 = (tid % (PK / 4)) * 4;
+#pragma unroll
+                for (int u = 0; u < 4; u++) XA[r0 + i][k0 + u] = outv[u];
+            }
+            __syncthreads();
+            // rows above: R <- R - sum_k g_k * block_k
+            for (int item = tid; item < r0 * (PK / 4); item += 1024) {
+                const int r = item / (PK / 4), k0 = (item % (PK / 4)) * 4;
+                uint64_t ax[4], aa[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t val = XA[r][k0 + u];
+                    ax[u] = val & 0xffffu;
+                    aa[u] = val >> 16;
+                }
+                for (int k = 0; k < bs; k++) {
+                    const uint32_t g = Gs[r][k];
+                    if (!g) continue;
+                    const uint64_t ng = p - g;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t val = XA[r0 + k][k0 + u];
+                        ax[u] += ng * (val & 0xffffu);
+                        aa[u] += ng * (val >> 16);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) XA[r][k0 + u] = fmod64(ax[u], F) | (fmod64(aa[u], F) << 16);
+            }
+        }
         __syncthreads();
-        PANEL_LAP(3);
+        PANEL_LAP(7);
     }
     __syncthreads();
     if (trace && tid == 0) {
@@ -619,10 +710,10 @@ gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, co
         for (int64_t q = 0; q < npanels; q++)
             for (int k = 0; k < 8; k++) s[k] += (double)tr[q * 8 + k];
         fprintf(stderr,
-                "[gbla panel trace] %lld panels, mean per panel: scan %.0f load %.0f reduce %.0f integrate %.0f cycles;"
-                " candidates %.1f pivots %.1f chunks %.1f\n",
-                (long long)npanels, s[0] / npanels, s[1] / npanels, s[2] / npanels, s[3] / npanels, s[4] / npanels,
-                s[5] / npanels, s[6] / npanels);
+                "[gbla panel trace] %lld panels, mean per panel: scan %.0f load %.0f reduce %.0f integrate %.0f"
+                " backsub %.0f cycles; candidates %.1f pivots %.1f chunks %.1f\n",
+                (long long)npanels, s[0] / npanels, s[1] / npanels, s[2] / npanels, s[3] / npanels, s[7] / npanels,
+                s[4] / npanels, s[5] / npanels, s[6] / npanels);
     }
     return GBLA_OK;
 }
