@@ -141,6 +141,47 @@ def run_reference(args):
 
 METRIC = "nnz-AXPY Gop/s mod p (F4 matrix reduction, gbla_reduce)"
 
+# kernel families timed by the library (gbla_get_kernel_ms) and how each is bounded
+KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1, tcgen05)", "update": "k_update_tc (K7', D -= C' B, tcgen05)",
+                "panel": "k_panel (K10, panel RREF, one CTA)", "trailing": "k_modgemm_tc<SUB> (K11 trailing update)",
+                "rnew": "k_modgemm_tc<STORE> (K11 new pivot rows)"}
+TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def roofline(kms, kwork, peaks, peak_src, sm_count):
+    """Roofline of the dominant kernel family (largest CUDA-event time over
+    the timed steps).  Tensor-core kernels: achieved = algorithmic modMACs x
+    4 u8 MACs (limb split) x 2 ops / kernel time, against the int8 dense peak
+    = 2 x the measured bf16 burst peak (B200 nominal int8:bf16 = 4.5:2.25).
+    The panel (one CTA, INT pipe): achieved = its modMACs / time against the
+    whole GPU's IMAD rate (148 SMs x 64 lanes x max clock)."""
+    dom = max(kms, key=lambda k: kms[k][0])
+    ms, n = kms[dom]
+    work = kwork[dom]
+    try:
+        traffic_db = json.load(open(TRAFFIC))
+    except Exception:
+        traffic_db = {}
+    tr = traffic_db.get(dom)
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    if dom == "panel":
+        peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
+        ach = work / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        out = {"bound": "alu", "achieved": round(ach, 5), "peak": round(peak, 3), "unit": "Tmodmac/s",
+               "peak_source": f"{sm_count} SMs x 64 IMAD/clk x {sm_mhz:.0f} MHz (derived; one modMAC = one IMAD)"}
+    else:
+        peak = 2.0 * float(peaks["bf16_tflops"])
+        ach = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        out = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 1), "unit": "TOPS",
+               "peak_source": f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TF/s "
+                              f"(MEASURED_PEAKS.json; nominal int8:bf16 = 2)",
+               "modmac_per_s_T": round(work / (ms / 1e3) / 1e12, 3) if ms > 0 else 0.0}
+    out.update({"kernel": KERNEL_NAMES[dom], "frac": round(out["achieved"] / out["peak"], 5) if out["peak"] else 0.0,
+                "kernel_ms_total": round(ms, 3), "launches": n, "algorithmic_modmac": int(work),
+                "traffic": (tr["dram_bytes_per_launch"] if tr else None),
+                "traffic_source": (f"profiles/{tr['source']} (ncu dram__bytes_read+write per launch)" if tr else None)})
+    return out
+
 
 def cpu_baseline(cfg_name: str, M, targets: int):
     import oracle
@@ -172,6 +213,7 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    os.environ.setdefault("GBLA_KERNEL_TIMERS", "1")    # per-kernel CUDA events on the library's stream
     import torch
     import gbla_gen
     import paper_1602_06097_b200 as gb
@@ -209,6 +251,8 @@ def main():
     launches0 = gb.kernel_launches()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phases = []
+    kms = {k: [0.0, 0] for k in gb.Mat.KERNELS}
+    kwork = {k: 0 for k in gb.Mat.KERNELS}
     ops = dense_ops = 0
     rank_d = None
     clocks = ClockSampler(dev)
@@ -222,6 +266,11 @@ def main():
         h = step()
         ev[i][1].record(stream)
         phases.append(h.phase_ms())
+        for k, (ms_k, n_k) in h.kernel_ms().items():
+            kms[k][0] += ms_k
+            kms[k][1] += n_k
+        for k, w in h.kernel_work().items():
+            kwork[k] += w
         ops, dense_ops = h.opcount()
         rank_d = h.dims(), h.rref()[0]
         h.free()
@@ -267,24 +316,7 @@ def main():
     if rank == 0:
         peaks, peak_src = _peaks()
         ph = {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]}
-        # dominant kernel and its roofline (DESIGN.md §"Roofline")
-        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        dom = max(("reduce_C", "echelon"), key=lambda k: ph[k])
-        if dom == "reduce_C":
-            # k_reduce_targets: INT-pipe modMACs; peak = 1 IMAD (32-bit) per modMAC per lane at 64 lanes/clk/SM
-            peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
-            ach = ops / (ph["reduce_C"] / 1e3) / 1e12
-            roof = {"kernel": "k_reduce_targets<MODE_FUSED>", "bound": "alu", "achieved": round(ach, 4),
-                    "peak": round(peak, 3), "unit": "Tmodmac/s", "frac": round(ach / peak, 4), "traffic": None,
-                    "peak_source": f"{sm_count} SMs x 64 IMAD/clk x {sm_mhz:.0f} MHz (B200_PROFILING.md clocks; "
-                                   f"{peak_src} sm_max_mhz)"}
-        else:
-            peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
-            ach = dense_ops / (ph["echelon"] / 1e3) / 1e12
-            roof = {"kernel": "echelon (k_trailing_int)", "bound": "alu", "achieved": round(ach, 4),
-                    "peak": round(peak, 3), "unit": "Tmodmac/s", "frac": round(ach / peak, 4), "traffic": None,
-                    "peak_source": f"{sm_count} SMs x 64 IMAD/clk x {sm_mhz:.0f} MHz"}
+        roof = roofline(kms, kwork, peaks, peak_src, sm_count=torch.cuda.get_device_properties(dev).multi_processor_count)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(cfg.name, M, args.cpu_targets)
@@ -303,6 +335,7 @@ def main():
             "sparse_modmac_per_step": ops, "dense_modmac_per_step": dense_ops,
             "rank_D": rank_d[1], "npiv": rank_d[0][0],
             "phase_ms": ph, "step_ms": [round(x, 3) for x in step_ms],
+            "kernel_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kms.items()},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "gpu_launches_per_step": round(launches / max(args.steps, 1), 1),
             "clocks": clk, "peaks_source": peak_src,

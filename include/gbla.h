@@ -102,8 +102,9 @@ void gbla_ctx_destroy(gbla_ctx ctx);
  * possible"); sigma orders P ascending then the other columns
  * ascending (R3, R4); pivot rows in sigma(lead) order form A|B, all other
  * rows in original order form C|D (R5, R7).  Builds the device formats
- * (sigma-ordered rows, two-row multilines of A|B) and the dense
- * D quadrant.  Synchronizes `stream`.  flags: GBLA_HOST_INPUT only. */
+ * (sigma-ordered rows and the dense D quadrant; the two-row multilines of
+ * A|B, are built on first use: gbla_get_multilines or the
+ * GBLA_SPARSE_INT path).  Synchronizes `stream`.  flags: GBLA_HOST_INPUT only. */
 gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags,
                         void *stream, gbla_mat *out);
 
@@ -164,6 +165,16 @@ gbla_status gbla_get_Bprime(gbla_mat h, const uint16_t **Bp, int64_t *ld);
 /* Densify an original quadrant ('A','B','C','D', normalized, sigma order)
  * into caller-provided device memory `out` (rows x cols, stride ld). */
 gbla_status gbla_densify_quadrant(gbla_mat h, char which, uint16_t *out, int64_t ld, void *stream);
+/* Two-row multilines of A|B (Definition, example P:524-556):
+ * pair k = sigma-ordered pivot rows (2k, 2k+1) (the last pair of an odd
+ * n_piv has a zero second row); its slots are q in [ptr[k], ptr[k+1]): col[q]
+ * = a sigma column of the union of both supports (ascending, no column where
+ * both rows are zero), val[q] = row 2k value (low 16 bits) | row 2k+1 value
+ * (high 16 bits), explicit zeros allowed (the paper's `val`, interleaved per
+ * column; `pos` = col).  Built on first call (enqueued on `stream`, which is
+ * synchronized).  Device pointers, owned by h; *npairs = ceil(n_piv / 2). */
+gbla_status gbla_get_multilines(gbla_mat h, void *stream, int64_t *npairs, const uint64_t **ptr,
+                                const uint32_t **col, const uint32_t **val);
 /* R (rank x nN, stride *ld) and pivcol[rank] after gbla_echelon_D. */
 gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol,
                           const uint16_t **R, int64_t *ld);
@@ -186,6 +197,11 @@ const char *gbla_last_error(void);
  * 3 = K11 trailing update of the echelon (tcgen05), 4 = K11 new pivot rows.
  * Synchronizes the handle's stream. */
 gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int64_t *launches);
+/* Algorithmic modMACs of the same kernel family on this handle (this rank):
+ * 0 = Alg 2 A-part count (sum over nonzero lambda_j of nnz(A_j) - 1),
+ * 1 = Alg 2 B-part count, 2 = sum over panels of candidates * kp * 128,
+ * 3 = sum over panels of nrows * kp * width, 4 = sum of kp * kp * width. */
+gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *modmac);
 /* Number of libgbla kernels launched by this process so far (diagnostics). */
 uint64_t gbla_kernel_launches(void);
 /* Library build/version string. */

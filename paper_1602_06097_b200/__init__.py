@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH):
         "gbla_kernel_launches": ([], ctypes.c_uint64),
         "gbla_modgemm": ([vp, u32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp], st),
         "gbla_get_kernel_ms": ([vp, ctypes.c_int, P(ctypes.c_float), P(i64)], st),
+        "gbla_get_multilines": ([vp, vp, P(i64), P(vp), P(vp), P(vp)], st),
+        "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -106,7 +108,8 @@ def exported_symbols():
             "gbla_get_dims", "gbla_get_maps", "gbla_get_D", "gbla_get_Cprime", "gbla_get_Bprime",
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
-            "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms"]
+            "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
+            "gbla_get_multilines", "gbla_get_kernel_work"]
 
 
 def _check(status: int):
@@ -243,6 +246,17 @@ class Mat:
         torch.cuda.current_stream().synchronize()
         return out[:shape[0], :shape[1]]
 
+    def multilines(self, stream=None):
+        """Two-row multilines of A|B: (ptr[npairs+1], col[slots],
+        val[slots]) as new torch tensors; val packs row 2k (low 16 bits) and
+        row 2k+1 (high 16 bits)."""
+        npr, ptr, col, val = ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.gbla_get_multilines(self._h, _stream_ptr(stream), ctypes.byref(npr), ctypes.byref(ptr),
+                                        ctypes.byref(col), ctypes.byref(val)))
+        P = _view(ptr.value, (npr.value + 1,), "<u8").clone()
+        ns = int(P[-1].item()) if npr.value >= 0 else 0
+        return P, _view(col.value, (ns,), "<u4").clone(), _view(val.value, (ns,), "<u4").clone()
+
     def rref(self):
         """(rank, pivcol[rank], R[rank x nN]) as new torch tensors."""
         npiv, mN, nN = self.dims()
@@ -278,6 +292,15 @@ class Mat:
             ms, n = ctypes.c_float(), ctypes.c_int64()
             _check(_lib.gbla_get_kernel_ms(self._h, i, ctypes.byref(ms), ctypes.byref(n)))
             out[name] = (ms.value, n.value)
+        return out
+
+    def kernel_work(self):
+        """{family: algorithmic modMACs} (gbla_get_kernel_work)."""
+        out = {}
+        for i, name in enumerate(self.KERNELS):
+            w = ctypes.c_uint64()
+            _check(_lib.gbla_get_kernel_work(self._h, i, ctypes.byref(w)))
+            out[name] = w.value
         return out
 
     def phase_ms(self):

@@ -374,6 +374,19 @@ extern "C" gbla_status gbla_densify_quadrant(gbla_mat h, char which, uint16_t *o
     return densify_impl(h, which, out, ld);
 }
 
+extern "C" gbla_status gbla_get_multilines(gbla_mat h, void *stream, int64_t *npairs, const uint64_t **ptr,
+                                           const uint32_t **col, const uint32_t **val)
+{
+    GBLA_TRY(check_mat(h, stream));
+    GBLA_TRY(ensure_multilines(h));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (npairs) *npairs = h->npairs;
+    if (ptr) *ptr = h->ml_ptr;
+    if (col) *col = h->ml_col;
+    if (val) *val = h->ml_val;
+    return GBLA_OK;
+}
+
 extern "C" gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol, const uint16_t **R,
                                      int64_t *ld)
 {
@@ -427,6 +440,13 @@ extern "C" gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int6
     }
     if (ms) *ms = tot;
     if (launches) *launches = (int64_t)(v.size() / 2);
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *modmac)
+{
+    if (!h || which < 0 || which >= KT_N || !modmac) { set_error("gbla_get_kernel_work: bad argument"); return GBLA_E_INVAL; }
+    *modmac = h->kwork[which];
     return GBLA_OK;
 }
 

@@ -174,6 +174,9 @@ gbla_status dist_sparse_phase(gbla_mat h)
     }
     // C5: modMAC counters (each rank counted its own tiles)
     unsigned long long ops[2];
+    GBLA_TRY(tc_read_ops(h, ops));            // this rank's tiles (kernel work for the roofline)
+    h->kwork[KT_SWEEP] = ops[0];
+    h->kwork[KT_UPDATE] = ops[1];
     if (real) {
         unsigned long long *d = tc_ops_dev(h);
         GBLA_NCCL_TRY(ncclAllReduce(d, d, 2, ncclUint64, ncclSum, (ncclComm_t)ctx->nccl_comm, st));

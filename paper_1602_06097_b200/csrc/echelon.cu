@@ -53,6 +53,7 @@ template <int PK>
 struct PanelState {
     uint32_t kp;                  // pivots found in this panel
     uint32_t nrows;               // rows with a nonzero coefficient
+    uint32_t ncand;               // candidate rows scanned by the panel
     uint32_t sel[PK];             // selected rows
     uint32_t pc[PK];              // absolute pivot columns
     uint16_t T[PK * PK];          // basis = T * D[S, panel]
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
     const uint32_t p = F.p;
     const int64_t width = (nN - c0) < PK ? (nN - c0) : PK;
     if (tid < PK) brow[tid] = tid;
-    uint32_t nb = 0;
+    uint32_t nb = 0, ncand_tot = 0;
     int64_t pos = 0;
     while (nb < (uint32_t)PK && pos < mN) {
         // (1) next chunk of up to CH candidates (k_cand flags), in row order:
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
         }
         PANEL_LAP(0);
         if (ncand == 0) continue;
+        ncand_tot += ncand;
         if (trace && tid == 0) { tr[4] += ncand; tr[6] += 1; }
         // (2) load the candidates' panel slices
         for (int idx = tid; idx < ncand * PK; idx += 1024) {
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(1024) k_panel(int64_t mN, int64_t nN, int64_t 
         for (int k = 0; k < 8; k++) o[k] = tr[k];
     }
 #undef PANEL_LAP
-    if (tid == 0) { ps->kp = nb; ps->nrows = 0; }
+    if (tid == 0) { ps->kp = nb; ps->nrows = 0; ps->ncand = ncand_tot; }
     for (int i = tid; i < PK * PK; i += blockDim.x) {
         const int b = i / PK, s = i % PK;
         ps->T[i] = (b < (int)nb && s < (int)nb) ? (uint16_t)(XA[b][s] >> 16) : 0;
@@ -567,12 +569,15 @@ __global__ void k_commit(int64_t nN, int64_t c0, uint16_t *__restrict__ D, int64
     D[(size_t)ps->sel[b] * ldD + c0 + x] = Rn[(size_t)b * ldR + x];
 }
 
-// algorithmic dense modMACs of the panel: nrows*kp*width + kp*kp*width
+// algorithmic dense modMACs of the panel: ops[0] += nrows*kp*width (trailing
+// update), ops[1] += kp*kp*width (new pivot rows)
 template <int PK>
 __global__ void k_count(int64_t width, const PanelState<PK> *__restrict__ ps, unsigned long long *__restrict__ ops)
 {
     const unsigned long long kp = ps->kp, nr = ps->nrows;
-    *ops += nr * kp * (unsigned long long)width + kp * kp * (unsigned long long)width;
+    ops[0] += nr * kp * (unsigned long long)width;
+    ops[1] += kp * kp * (unsigned long long)width;
+    ops[2] += (unsigned long long)ps->ncand * kp * PK;   // panel RREF: each pivot eliminated from every candidate
 }
 
 // K13: R rows sorted by pivot column.
@@ -728,10 +733,10 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     uint16_t *invtab;
     unsigned long long *dops;
     GBLA_TRY(dalloc_t(h, mN + 1, &rowpiv));
-    GBLA_TRY(dalloc_t(h, 1, &dops));
+    GBLA_TRY(dalloc_t(h, 3, &dops));
     GBLA_TRY(dalloc_t(h, 65536, &invtab));
     GBLA_CUDA_TRY(cudaMemsetAsync(rowpiv, 0xff, (mN + 1) * 4, st));
-    GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 8, st));
+    GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 24, st));
     k_invtab<<<grid_for(h->p, 256), 256, 0, st>>>(h->F, invtab);
     note_launch();
     if (mN > 0 && nN > 0) {
@@ -754,12 +759,15 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
         GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t, tb, cflag, cidx, (int)(nN + 1), st));
     }
     uint32_t rk = 0;
-    unsigned long long dv = 0;
+    unsigned long long dv[3] = {0, 0, 0};
     GBLA_CUDA_TRY(cudaMemcpyAsync(&rk, cidx + nN, 4, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaMemcpyAsync(&dv, dops, 8, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 24, cudaMemcpyDeviceToHost, st));
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
     h->rank = rk;
-    h->dense_ops = dv;
+    h->dense_ops = dv[0] + dv[1];
+    h->kwork[KT_TRAIL] = dv[0];
+    h->kwork[KT_RN] = dv[1];
+    h->kwork[KT_PANEL] = dv[2];
     h->ldR = ldD;
     GBLA_TRY(dalloc_t(h, (size_t)(rk > 0 ? rk : 1) * h->ldR, &h->R));
     GBLA_TRY(dalloc_t(h, rk + 1, &h->pivcol));

@@ -145,6 +145,7 @@ struct gbla_mat_s {
 
     uint64_t *opcount = nullptr;       // [mN] per-target sparse modMACs
     uint64_t sparse_ops = 0, dense_ops = 0;
+    uint64_t kwork[KT_N] = {0, 0, 0, 0, 0};   // algorithmic modMACs per kernel family (this rank)
 
     // call-order state
     bool did_reduce_B = false, did_cprime = false, did_update = false, did_fused = false;
@@ -180,6 +181,7 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16);
 gbla_status update_d_tc(gbla_mat h);
 void band_free(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
+gbla_status ensure_multilines(gbla_mat h);
 static inline void kt_mark(gbla_mat h, int which)
 {
     if (!h->kt.on) return;

@@ -184,6 +184,7 @@ gbla_status launch_targets(gbla_mat h)
 {
     cudaStream_t st = h->stream;
     if (h->mN == 0) return GBLA_OK;
+    GBLA_TRY(ensure_multilines(h));
     int per_sm = 0;
     GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce_targets<MODE>, 256, 0));
     if (per_sm < 1) per_sm = 1;

@@ -176,20 +176,45 @@ struct SweepArgs {
     const uint8_t *tilesA, *invT;
     const uint64_t *offA;
     const uint32_t *jl_ptr, *jl_idx;
-    uint8_t *Xt;                   // X tiles; tile (T, J) holds C_J[T] until step J overwrites it with X_J[T]
+    uint8_t *Xt;                   // X tiles; tile (T, J) holds C_J[T] until task (T, J) overwrites it with X_J[T]
     uint16_t *X16;
     int64_t ldX;
     const uint32_t *ab_w, *ab_np;
     unsigned long long *ops;
-    unsigned long long *trace;     // optional: per (J, CTA) phase timestamps (GBLA_SWEEP_TRACE)
-    int64_t prank, pworld;         // target tiles T = prank + pworld * blockIdx.x (multi-GPU row shards)
+    int64_t prank, pworld;         // target tiles T = prank + pworld * i (multi-GPU row shards), i = local tile
+    // dependency-driven schedule: task (i, J) computes X_J of local tile i.  Tasks are
+    // numbered J-major: those of column block J are [toff[J], toff[J+1]) = local tiles
+    // 0 .. toff[J+1]-toff[J]-1 (tiles are sorted by lead, so the active ones are a prefix).
+    const uint32_t *toff;          // [NB+1]
+    const uint32_t *jmin;          // [nl] first block of local tile i
+    uint32_t *flags;               // [nl*NB] 1 once X_J of local tile i is stored
+    unsigned int *next;            // task counter
+    uint32_t ntasks;
 };
 
-#define SWEEP_MARK(slot_)                                                                  \
-    do {                                                                                   \
-        if (a.trace && tid == 0)                                                           \
-            a.trace[((size_t)J * 256 + blockIdx.x) * 8 + (slot_)] = clock64();             \
-    } while (0)
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// first block of every local target tile (NB for a tile of zero rows)
+__global__ void k_tile_jmin(int64_t nl, int64_t mN, int64_t npiv, int64_t NB, int64_t prank, int64_t pworld,
+                            const uint32_t *__restrict__ order, const uint32_t *__restrict__ tlead,
+                            uint32_t *__restrict__ jmin)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nl) return;
+    const int64_t first = (prank + pworld * i) * 128;
+    const uint32_t l = first < mN ? tlead[order[first]] : (uint32_t)npiv;
+    jmin[i] = l >= (uint64_t)npiv ? (uint32_t)NB : l / 128u;
+}
 
 // pos[order[i]] = i (rank of every target in lead order)
 __global__ void k_pos(int64_t mN, const uint32_t *__restrict__ order, uint32_t *__restrict__ pos)
@@ -222,24 +247,27 @@ __global__ void k_cfill(int64_t mN, int64_t NB, const uint32_t *__restrict__ pos
 constexpr int NSTAGE = 3;
 constexpr int SWEEP_SMEM = NSTAGE * 65536 + TB;   // 3 operand stages + inv(A_JJ); Y reuses stage 0
 
-// Persistent: CTA T = target tile T sweeps J from its first lead block.
+// K5': persistent, dependency-driven block forward substitution.  Every CTA
+// claims tasks (i, J) in J-major order from a global counter; a task
+// accumulates S = sum_I X_I[T] A_IJ over the band list of block J, waiting
+// for each X_I[T] to be published (flag) just before its operands are
+// staged, then X_J = (C_J - S) inv(A_JJ) is stored and published.  A task
+// only waits on tasks with smaller numbers, which were claimed earlier by
+// co-resident CTAs (cooperative launch), so the schedule cannot deadlock;
+// the chain of one tile costs one tile-pair GEMM + two epilogues per block
+// while the rest of each task's GEMMs run off the critical path, and the
+// A_IJ tiles of one J are shared in L2 by all tiles working on J.
 __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stg = smem;
-    uint8_t *Ys = smem;                        // stage 0's A half, free after stage 1
+    uint8_t *Ys = smem;                        // stage 0's X half, free once the accumulation is done
     uint8_t *INV = smem + NSTAGE * 65536;
     __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar, invbar;
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t s_np[128], s_w[128];
+    __shared__ uint32_t s_task;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t T = a.prank + a.pworld * (int64_t)blockIdx.x, first = T * 128;
-    const uint32_t lead0 = a.tlead[a.order[first]];
-    if (lead0 >= (uint64_t)a.npiv) return;                     // tile of zero rows: X = 0
-    const int64_t Jmin = lead0 / 128;
-    const int64_t slot = first + tid;
-    const bool live = slot < a.mN;
-    const uint32_t t = live ? a.order[slot] : 0;
     if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&mdone[s], 1); }
@@ -255,11 +283,27 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
     unsigned long long opsA = 0, opsB = 0;
     const uint32_t sStg = tc::smem_u32(stg), sY = tc::smem_u32(Ys), sINV = tc::smem_u32(INV);
-    uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
     const uint32_t p = a.F.p;
 
-    for (int64_t J = Jmin; J < a.NB; J++) {
-        SWEEP_MARK(0);
+    for (;;) {
+        if (tid == 0) s_task = atomicAdd(a.next, 1u);
+        __syncthreads();
+        const uint32_t task = s_task;
+        if (task >= a.ntasks) break;
+        // decode: J = last block with toff[J] <= task
+        uint32_t lo = 0, hi = (uint32_t)a.NB;          // toff[lo] <= task < toff[hi]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (a.toff[mid] <= task) lo = mid; else hi = mid;
+        }
+        const int64_t J = lo, li = task - a.toff[lo];
+        const int64_t T = a.prank + a.pworld * li, first = T * 128;
+        const int64_t Jmin = a.jmin[li];
+        const int64_t slot = first + tid;
+        const bool live = slot < a.mN;
+        const uint32_t t = live ? a.order[slot] : 0;
+        uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
+        const uint32_t *fl = a.flags + (size_t)li * a.NB;
         const uint32_t jbase = (uint32_t)J * 128;
         {
             const uint32_t jg = jbase + tid;
@@ -270,7 +314,6 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
         const uint32_t nI = l1 - lb;
-        SWEEP_MARK(1);
         if (tid == 0) {
             tc::mbar_expect_tx(&invbar, TB);
             tc::bulk_g2s(INV, a.invT + (size_t)J * TB, TB, &invbar);
@@ -278,8 +321,13 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
                 const uint32_t I = a.jl_idx[lb + it];
                 const int s = it % NSTAGE;
                 tc::mbar_expect_tx(&full[s], 2 * TB);
-                tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
                 tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
+                // X_I[T] is produced by task (li, I): wait until it is published
+                if (ld_acquire(fl + I) == 0) {
+                    while (ld_acquire(fl + I) == 0) __nanosleep(64);
+                }
+                fence_proxy_async_global();
+                tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
             };
             for (uint32_t it = 0; it < nI && it < (uint32_t)NSTAGE; it++) load(it);
             for (uint32_t it = 0; it < nI; it++) {
@@ -298,14 +346,12 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
                 }
             }
             if (nI > 0) tc::commit(&accbar);
-            SWEEP_MARK(2);
         }
         if (nI > 0) {
             tc::mbar_wait(&accbar, ph_acc);
             ph_acc ^= 1;
             tc::fence_after();
         }
-        SWEEP_MARK(3);
         // epilogue 1: Y = C_J - S -> shared memory (A operand of stage 2); C_J row from the tile itself
         const uint8_t *ct = Xrow + (size_t)J * TB;
 #pragma unroll 1
@@ -321,23 +367,22 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
             uint4 clo = *reinterpret_cast<const uint4 *>(ct + o);
             uint4 chi = *reinterpret_cast<const uint4 *>(ct + PB + o);
             const uint8_t *cl = reinterpret_cast<const uint8_t *>(&clo), *ch = reinterpret_cast<const uint8_t *>(&chi);
-            uint8_t lo[16], hi[16];
+            uint8_t lo8[16], hi8[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
                 const uint32_t cv = cl[j] | (ch[j] << 8);
-                const uint32_t s = fmod64(S[j], a.F);
-                const uint32_t y = cv >= s ? cv - s : cv + p - s;
-                lo[j] = (uint8_t)(y & 0xff);
-                hi[j] = (uint8_t)(y >> 8);
+                const uint32_t sv = fmod64(S[j], a.F);
+                const uint32_t y = cv >= sv ? cv - sv : cv + p - sv;
+                lo8[j] = (uint8_t)(y & 0xff);
+                hi8[j] = (uint8_t)(y >> 8);
             }
-            *reinterpret_cast<uint4 *>(Ys + o) = *reinterpret_cast<uint4 *>(lo);
-            *reinterpret_cast<uint4 *>(Ys + PB + o) = *reinterpret_cast<uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(Ys + o) = *reinterpret_cast<uint4 *>(lo8);
+            *reinterpret_cast<uint4 *>(Ys + PB + o) = *reinterpret_cast<uint4 *>(hi8);
         }
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
-        SWEEP_MARK(4);
         // stage 2: X_J = Y inv(A_JJ)
         if (tid == 0) {
             tc::mbar_wait(&invbar, ph_inv);
@@ -349,20 +394,19 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         tc::mbar_wait(&accbar, ph_acc);
         ph_acc ^= 1;
         tc::fence_after();
-        SWEEP_MARK(5);
         // epilogue 2: X_J -> limb-plane tile (global) [+ C' u16], op counts (Alg 2 count)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 16) {
             uint64_t S[16];
             read_S(lane_addr, c, S);
-            uint8_t lo[16], hi[16];
+            uint8_t lo8[16], hi8[16];
             uint16_t xs[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
                 const uint32_t x = fmod64(S[j], a.F);
-                lo[j] = (uint8_t)(x & 0xff);
-                hi[j] = (uint8_t)(x >> 8);
+                lo8[j] = (uint8_t)(x & 0xff);
+                hi8[j] = (uint8_t)(x >> 8);
                 xs[j] = (uint16_t)x;
                 if (x && live) {
                     opsA += s_np[c + j] - 1;
@@ -370,19 +414,22 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
                 }
             }
             const uint32_t o = tc::toff(tid, c);
-            *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo);
-            *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo8);
+            *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi8);
             if (a.X16 && live) {
 #pragma unroll
                 for (int j = 0; j < 16; j++)
                     if (jbase + c + j < (uint64_t)a.npiv) a.X16[(size_t)t * a.ldX + jbase + c + j] = xs[j];
             }
         }
-        tc::fence_async_all();     // X_J is read by later steps through the async proxy
+        fence_proxy_async_global();     // X_J is read by later tasks through the async proxy
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
-        SWEEP_MARK(6);
+        if (tid == 0) {
+            __threadfence();
+            st_release(a.flags + (size_t)li * a.NB + J, 1u);
+        }
     }
     for (int o = 16; o; o >>= 1) {
         opsA += __shfl_xor_sync(0xffffffffu, opsA, o);
@@ -616,49 +663,65 @@ gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
     cudaStream_t st = h->stream;
     BandTiles *bt = h->bt;
     const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
-    if (bt->NB == 0 || nl == 0) return GBLA_OK;
-    static bool attr = false;
-    if (!attr) {
+    const int64_t NB = bt->NB;
+    if (NB == 0 || nl == 0) return GBLA_OK;
+    static int occ = -1;
+    if (occ < 0) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
-        attr = true;
+        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, 128, SWEEP_SMEM));
+        if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     }
+    // task schedule: first block of every local tile -> J-major task offsets
+    uint32_t *jmin, *toff, *flags;
+    unsigned int *next;
+    GBLA_TRY(dalloc_t(h, nl, &jmin));
+    GBLA_TRY(dalloc_t(h, NB + 1, &toff));
+    GBLA_TRY(dalloc_t(h, (size_t)nl * NB, &flags));
+    GBLA_TRY(dalloc_t(h, 1, &next));
+    k_tile_jmin<<<grid_for(nl, 256), 256, 0, st>>>(nl, h->mN, h->npiv, NB, prank, pworld, h->order, h->tlead, jmin);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    std::vector<uint32_t> hj(nl), ho(NB + 1);
+    GBLA_CUDA_TRY(cudaMemcpyAsync(hj.data(), jmin, nl * 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)nl * NB * 4, st));
+    GBLA_CUDA_TRY(cudaMemsetAsync(next, 0, 4, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        // tiles are sorted by lead, so jmin is nondecreasing in i: active tiles of J are a prefix
+        int64_t i = 0;
+        uint64_t tot = 0;
+        for (int64_t J = 0; J < NB; J++) {
+            while (i < nl && hj[i] <= (uint64_t)J) i++;
+            ho[J] = (uint32_t)tot;
+            tot += (uint64_t)i;
+        }
+        ho[NB] = (uint32_t)tot;
+        if (tot >= 0xffffffffull) { set_error("k_sweep: too many tasks"); return GBLA_E_INTERNAL; }
+        for (int64_t q = 1; q < nl; q++)
+            if (hj[q] < hj[q - 1]) { set_error("k_sweep: target tiles not sorted by lead"); return GBLA_E_INTERNAL; }
+    }
+    GBLA_CUDA_TRY(cudaMemcpyAsync(toff, ho.data(), (NB + 1) * 4, cudaMemcpyHostToDevice, st));
+    const uint32_t ntasks = ho[NB];
+    if (ntasks == 0) return GBLA_OK;
     SweepArgs a;
-    a.mN = h->mN; a.npiv = h->npiv; a.NB = bt->NB; a.F = h->F;
+    a.mN = h->mN; a.npiv = h->npiv; a.NB = NB; a.F = h->F;
     a.order = h->order; a.tlead = h->tlead;
     a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
     a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
     a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
     a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
     a.prank = prank; a.pworld = pworld;
-    const bool trace = getenv("GBLA_SWEEP_TRACE") != nullptr && nl <= 256;
-    a.trace = nullptr;
-    if (trace) {
-        GBLA_TRY(dalloc_t(h, (size_t)bt->NB * 256 * 8, &a.trace));
-        GBLA_CUDA_TRY(cudaMemsetAsync(a.trace, 0, (size_t)bt->NB * 256 * 8 * 8, st));
-    }
+    a.toff = toff; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
+    int64_t grid = (int64_t)h->ctx->sm_count * occ;
+    if (grid > (int64_t)ntasks) grid = ntasks;
+    // co-residency of every CTA is what makes the flag waits safe: cooperative launch
+    void *kargs[] = {&a};
     kt_mark(h, KT_SWEEP);
-    k_sweep<<<(unsigned)nl, 128, SWEEP_SMEM, st>>>(a);
+    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(128), kargs,
+                                              (size_t)SWEEP_SMEM, st));
     kt_mark(h, KT_SWEEP);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
-    if (trace) {   // diagnostics: mean cycles per phase over (J, CTA)
-        std::vector<unsigned long long> tr((size_t)bt->NB * 256 * 8);
-        GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
-        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
-        double sum[6] = {0, 0, 0, 0, 0, 0};
-        long cnt = 0;
-        for (size_t e = 0; e < (size_t)bt->NB * 256; e++) {
-            const unsigned long long *tt = &tr[e * 8];
-            if (!tt[0] || !tt[6]) continue;
-            for (int k = 0; k < 6; k++) sum[k] += (double)(tt[k + 1] - tt[k]);
-            cnt++;
-        }
-        if (cnt)
-            fprintf(stderr,
-                    "[gbla sweep trace] %ld CTA-steps, mean cycles: setup %.0f  stage1-issue %.0f  stage1-wait %.0f"
-                    "  epi1 %.0f  stage2 %.0f  epi2 %.0f\n",
-                    cnt, sum[0] / cnt, sum[1] / cnt, sum[2] / cnt, sum[3] / cnt, sum[4] / cnt, sum[5] / cnt);
-    }
     return GBLA_OK;
 }
 
@@ -713,6 +776,7 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops += ops[0];
+    h->kwork[KT_SWEEP] = ops[0];
     h->have_xt = true;
     return GBLA_OK;
 }
@@ -726,6 +790,7 @@ gbla_status update_d_tc(gbla_mat h)
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops += ops[1];
+    h->kwork[KT_UPDATE] = ops[1];
     return GBLA_OK;
 }
 

@@ -187,15 +187,13 @@ __global__ void k_ml_count(int64_t npairs, int64_t npiv, const uint64_t *__restr
 __global__ void k_ml_fill(int64_t npairs, int64_t npiv, const uint64_t *__restrict__ ab_ptr,
                           const uint32_t *__restrict__ ab_col, const uint16_t *__restrict__ ab_val,
                           const uint64_t *__restrict__ ml_ptr, uint32_t *__restrict__ ml_col,
-                          uint32_t *__restrict__ ml_val, uint16_t *__restrict__ a01, uint32_t *__restrict__ w)
+                          uint32_t *__restrict__ ml_val, uint16_t *__restrict__ a01)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= npairs) return;
     int64_t r0 = 2 * k, r1 = 2 * k + 1;
     uint64_t a = ab_ptr[r0], ae = ab_ptr[r0 + 1];
     uint64_t b = r1 < npiv ? ab_ptr[r1] : 0, be = r1 < npiv ? ab_ptr[r1 + 1] : 0;
-    w[r0] = (uint32_t)(ae - a);
-    if (r1 < npiv) w[r1] = (uint32_t)(be - b);
     uint64_t o = ml_ptr[k];
     uint16_t v01 = 0;
     while (a < ae || b < be) {
@@ -211,6 +209,13 @@ __global__ void k_ml_fill(int64_t npairs, int64_t npiv, const uint64_t *__restri
         o++;
     }
     a01[k] = v01;
+}
+
+// w[i] = nnz of sigma-ordered pivot row i
+__global__ void k_row_w(int64_t npiv, const uint64_t *__restrict__ ab_ptr, uint32_t *__restrict__ w)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npiv) w[i] = (uint32_t)(ab_ptr[i + 1] - ab_ptr[i]);
 }
 
 // Densify part of the sigma-ordered rows: entries with sigma col in
@@ -364,26 +369,10 @@ gbla_status splice_impl(gbla_mat h, const gbla_csr *M, uint32_t flags)
                                                             h->cd_val, h->cd_np); note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
 
-    // two-row multilines of A|B
-    const int64_t np2 = h->npairs;
-    uint64_t *cnt;
-    GBLA_TRY(dalloc_t(h, np2 + 1, &cnt));
-    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_ptr));
-    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_np));
-    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_skip));
-    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_a01));
+    // pivot row weights (nnz), used for the Alg 2 op count; the two-row
+    // multilines are built on first use (ensure_multilines: INT-pipe path only)
     GBLA_TRY(dalloc_t(h, npiv + 1, &h->ab_w));
-    k_ml_count<<<grid_for(np2 + 1, 128), 128, 0, st>>>(np2, npiv, h->ab_ptr, h->ab_col, cnt, h->ml_np, h->ml_skip); note_launch();
-    GBLA_TRY(exclusive_scan<uint64_t>(h, cnt, h->ml_ptr, np2 + 1));
-    GBLA_CUDA_TRY(cudaMemcpyAsync(&tmp64[0], h->ml_ptr + np2, 8, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
-    h->nslots = (int64_t)tmp64[0];
-    GBLA_TRY(dalloc_t(h, h->nslots, &h->ml_col));
-    GBLA_TRY(dalloc_t(h, h->nslots, &h->ml_val));
-    if (np2)
-        k_ml_fill<<<grid_for(np2, 128), 128, 0, st>>>(np2, npiv, h->ab_ptr, h->ab_col, h->ab_val, h->ml_ptr,
-                                                      h->ml_col, h->ml_val, h->ml_a01, h->ab_w); note_launch();
-    GBLA_CUDA_TRY(cudaGetLastError());
+    if (npiv) k_row_w<<<grid_for(npiv, 256), 256, 0, st>>>(npiv, h->ab_ptr, h->ab_w); note_launch();
 
     // targets sorted by sigma(lead): longest first
     GBLA_TRY(dalloc_t(h, mN + 1, &h->order));
@@ -411,6 +400,35 @@ gbla_status splice_impl(gbla_mat h, const gbla_csr *M, uint32_t flags)
         k_densify<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, h->cd_ptr, h->cd_col, h->cd_val, npiv, n, h->D, h->ldD); note_launch();
     GBLA_TRY(dalloc_t(h, mN + 1, &h->opcount));
     GBLA_CUDA_TRY(cudaMemsetAsync(h->opcount, 0, (mN + 1) * 8, st));
+    GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}
+
+// Two-row multilines of A|B, built on first use by the INT-pipe
+// kernels (the tensor-core path reads the sigma-ordered rows directly).
+gbla_status ensure_multilines(gbla_mat h)
+{
+    if (h->ml_ptr) return GBLA_OK;
+    cudaStream_t st = h->stream;
+    const int64_t npiv = h->npiv;
+    const int64_t np2 = h->npairs;
+    uint64_t tmp64 = 0;
+    uint64_t *cnt;
+    GBLA_TRY(dalloc_t(h, np2 + 1, &cnt));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_ptr));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_np));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_skip));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->ml_a01));
+    k_ml_count<<<grid_for(np2 + 1, 128), 128, 0, st>>>(np2, npiv, h->ab_ptr, h->ab_col, cnt, h->ml_np, h->ml_skip); note_launch();
+    GBLA_TRY(exclusive_scan<uint64_t>(h, cnt, h->ml_ptr, np2 + 1));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(&tmp64, h->ml_ptr + np2, 8, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    h->nslots = (int64_t)tmp64;
+    GBLA_TRY(dalloc_t(h, h->nslots, &h->ml_col));
+    GBLA_TRY(dalloc_t(h, h->nslots, &h->ml_val));
+    if (np2)
+        k_ml_fill<<<grid_for(np2, 128), 128, 0, st>>>(np2, npiv, h->ab_ptr, h->ab_col, h->ab_val, h->ml_ptr,
+                                                      h->ml_col, h->ml_val, h->ml_a01); note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }

@@ -1,0 +1,61 @@
+#!/usr/bin/env python
+"""Per-kernel DRAM traffic from one `ncu --set full` capture, for bench.py's
+roofline "traffic" field.  Usage (here, no GPU needed):
+    python scripts/ncu_traffic.py gpurun_out/prof.ncu-rep profiles/ncu_traffic.json
+Writes {family: {kernel, dram_bytes_per_launch, duration_ms, tensor_pct,
+launches, source}} averaged over the captured launches of each family."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+FAMILIES = [("k_sweep", "sweep"), ("k_update_tc", "update"), ("k_panel", "panel"),
+            ("k_modgemm_tc<0>", "trailing"), ("k_modgemm_tc<1>", "rnew"), ("k_trail", "trailing"),
+            ("k_rnew_tc", "rnew")]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+TSCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
+
+
+def family(name):
+    for key, fam in FAMILIES:
+        if key in name:
+            return fam
+    return None
+
+
+def main():
+    rep, out = sys.argv[1], sys.argv[2]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    col = {h: i for i, h in enumerate(hdr)}
+    acc = {}
+    for r in rows[2:]:
+        fam = family(r[col["Kernel Name"]])
+        if fam is None:
+            continue
+        rd = float(r[col["dram__bytes_read.sum"]]) * SCALE[units[col["dram__bytes_read.sum"]]]
+        wr = float(r[col["dram__bytes_write.sum"]]) * SCALE[units[col["dram__bytes_write.sum"]]]
+        t = float(r[col["gpu__time_duration.sum"]]) * TSCALE[units[col["gpu__time_duration.sum"]]]
+        k = "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"
+        tp = float(r[col[k]]) if k in col and r[col[k]] else None
+        a = acc.setdefault(fam, {"kernel": r[col["Kernel Name"]].split("(")[0], "bytes": 0.0, "ms": 0.0, "n": 0,
+                                 "tensor": []})
+        a["bytes"] += rd + wr
+        a["ms"] += t
+        a["n"] += 1
+        if tp is not None:
+            a["tensor"].append(tp)
+    res = {}
+    for fam, a in acc.items():
+        res[fam] = {"kernel": a["kernel"], "dram_bytes_per_launch": round(a["bytes"] / a["n"]),
+                    "duration_ms_per_launch": round(a["ms"] / a["n"], 4),
+                    "tensor_pipe_pct_of_active": round(sum(a["tensor"]) / len(a["tensor"]), 2) if a["tensor"] else None,
+                    "launches_captured": a["n"], "source": rep.split("/")[-1]}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

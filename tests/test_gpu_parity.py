@@ -91,6 +91,30 @@ def test_splice_quadrants_random_suite(gb, ctx):
         h.free()
 
 
+def test_multilines_match_oracle_definition(gb, ctx):
+    """a2: the device two-row multilines of A|B equal the oracle's multiline
+    (Definition, pinned by the paper's example P:524-556) of every
+    pair of sigma-ordered pivot rows."""
+    cases = list(gbla_gen.random_suite(30, seed0=31)) + [gbla_gen.f4_matrix("c0")]
+    for M in cases:
+        S = oracle.splice(M)
+        A, B, C, D = oracle.quadrants(M, S)
+        AB = np.hstack([A, B]).astype(np.uint32)
+        rp, c, v = to_dev(M)
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        ptr, col, val = (np_(t) for t in h.multilines())
+        assert ptr.size == (S.npiv + 1) // 2 + 1
+        for k in range((S.npiv + 1) // 2):
+            r1 = AB[2 * k]
+            r2 = AB[2 * k + 1] if 2 * k + 1 < S.npiv else np.zeros_like(r1)
+            pos, mv = oracle.multiline(r1, r2)
+            q0, q1 = int(ptr[k]), int(ptr[k + 1])
+            assert np.array_equal(col[q0:q1], pos), (k, col[q0:q1], pos)
+            packed = mv[0::2].astype(np.uint64) | (mv[1::2].astype(np.uint64) << 16)
+            assert np.array_equal(val[q0:q1].astype(np.uint64), packed), k
+        h.free()
+
+
 def test_pipeline_random_suite_new_order(gb, ctx):
     for M in gbla_gen.random_suite(150, seed0=23):
         check_full(gb, ctx, M)
