@@ -37,12 +37,13 @@
 #include "tc.cuh"
 
 void modgemm_set_sms(int sms);
+gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab);
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                           const uint32_t *rowidx, uint16_t *C, int64_t ldc);
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev);
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi);
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev);
 
 namespace {
 
@@ -651,78 +652,6 @@ gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     return GBLA_OK;
 }
 
-gbla_status panels_tc(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab)
-{
-    constexpr int PK = KPT;
-    cudaStream_t st = h->stream;
-    modgemm_set_sms(h->ctx->sm_count);
-    const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
-    const int64_t npad = (nN + 63) / 64 * 64 + 64;
-    uint32_t *rows;
-    uint16_t *Rn;
-    uint8_t *Flo, *Fhi, *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
-    PanelState<PK> *ps;
-    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
-    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * KPT, &Flo));
-    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * KPT, &Fhi));
-    GBLA_TRY(dalloc_t(h, (size_t)KPT * KPT, &Tlo));
-    GBLA_TRY(dalloc_t(h, (size_t)KPT * KPT, &Thi));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Blo));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Bhi));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Rtlo));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * KPT, &Rthi));
-    GBLA_TRY(dalloc_t(h, (size_t)KPT * ldR, &Rn));
-    GBLA_TRY(dalloc(h, sizeof(PanelState<PK>), (void **)&ps));
-    GBLA_TRY(set_panel_smem<PK>());
-    uint8_t *cflag;
-    GBLA_TRY(dalloc_t(h, mN + 1, &cflag));
-    const int64_t npanels = (nN + PK - 1) / PK;
-    unsigned long long *trace = nullptr;
-    if (getenv("GBLA_PANEL_TRACE")) {
-        GBLA_TRY(dalloc_t(h, (size_t)npanels * 8, &trace));
-        GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, (size_t)npanels * 64, st));
-    }
-    for (int64_t c0 = 0; c0 < nN; c0 += PK) {
-        const int64_t width = nN - c0;
-        k_cand<PK><<<grid_for(mN, 256), 256, 0, st>>>(mN, nN, c0, h->D, ldD, rowpiv, cflag);
-        kt_mark(h, KT_PANEL);
-        k_panel<PK><<<1, 1024, panel_smem<PK>(), st>>>(mN, nN, c0, h->F, h->D, ldD, rowpiv, ps, Tlo, Thi, invtab,
-                                                        cflag, trace);
-        kt_mark(h, KT_PANEL);
-        note_launch();
-        k_gather<PK, true><<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, nullptr, Flo, Fhi,
-                                                             rows);
-        k_gather_st<<<dim3(grid_for(width, 128), KPT / 16), 128, 0, st>>>(nN, c0, h->D, ldD, ps, Blo, Bhi);
-        note_launch(3);
-        // Rn = T * D[S, c0:]  (plus its transposed limb planes)
-        kt_mark(h, KT_RN);
-        GBLA_TRY(modgemm_tc_store(st, width, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi));
-        kt_mark(h, KT_RN);
-        // D[rows, c0:] -= F * Rn
-        kt_mark(h, KT_TRAIL);
-        GBLA_TRY(modgemm_tc_sub(st, mN, &ps->nrows, width, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D + c0, ldD));
-        kt_mark(h, KT_TRAIL);
-        k_commit<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->D, ldD, ps, Rn, ldR);
-        k_count<PK><<<1, 1, 0, st>>>(width, ps, dops);
-        note_launch(2);
-        GBLA_CUDA_TRY(cudaGetLastError());
-    }
-    if (trace) {   // diagnostics: per-panel phase cycles
-        std::vector<unsigned long long> tr((size_t)npanels * 8);
-        GBLA_CUDA_TRY(cudaMemcpyAsync(tr.data(), trace, tr.size() * 8, cudaMemcpyDeviceToHost, st));
-        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
-        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int64_t q = 0; q < npanels; q++)
-            for (int k = 0; k < 8; k++) s[k] += (double)tr[q * 8 + k];
-        fprintf(stderr,
-                "[gbla panel trace] %lld panels, mean per panel: scan %.0f load %.0f reduce %.0f integrate %.0f"
-                " backsub %.0f cycles; candidates %.1f pivots %.1f chunks %.1f\n",
-                (long long)npanels, s[0] / npanels, s[1] / npanels, s[2] / npanels, s[3] / npanels, s[7] / npanels,
-                s[4] / npanels, s[5] / npanels, s[6] / npanels);
-    }
-    return GBLA_OK;
-}
-
 }  // namespace
 
 gbla_status echelon_impl(gbla_mat h, uint32_t flags)
@@ -741,7 +670,7 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     note_launch();
     if (mN > 0 && nN > 0) {
         if (flags & GBLA_DENSE_INT) GBLA_TRY(panels_int(h, rowpiv, dops, invtab));
-        else GBLA_TRY(panels_tc(h, rowpiv, dops, invtab));
+        else GBLA_TRY(panels_tc2(h, rowpiv, dops, invtab));
     }
     // K13: compaction
     GBLA_TRY(dalloc_t(h, nN + 1, &colrow));

@@ -1,0 +1,887 @@
+// panel.cu -- Step 4 (reading R13) on the tensor cores, v2:
+// blocked Gauss-Jordan over WIDTH-ADAPTIVE column panels holding up to
+// PK = 128 pivots each, so that every trailing update is a K = 128 modular
+// GEMM whatever the rank profile of D (a staircase D_new has ~0.4 pivots
+// per column, a dense one ~1).
+//
+// Invariant before the panel starting at column c0 (as in echelon.cu): every
+// row is a pivot row (pivot column < c0) or ACTIVE, and active rows are zero
+// on all columns < c0.  Per panel (all state on the device; c0 of panel k is
+// c1 of panel k-1, so the host never waits between panels):
+//   k_lead2    lead[r] = first nonzero column of active row r in [c0, c0+PW)
+//   k_panel2   one CTA: the panel width w is the largest w <= PW such that at
+//              most PK active rows lead in [c0, c0+w) ("wide" mode: those
+//              rows are the candidates, so at most PK pivots); if more than
+//              PK rows lead in [c0, c0+128) the panel is [c0, c0+128) and
+//              candidates come in chunks ("dense" mode, stop at w pivots).
+//              The candidates' panel slices are reduced by the basis, then
+//              put in echelon form by parallel ROUNDS: every row finds its
+//              leading column, one row per column becomes a head (normalized,
+//              established heads first) and eliminates that column from the
+//              rows that share it; rounds repeat until all leading columns
+//              differ.  A blocked back substitution (32-row blocks, the
+//              unit-triangular block inverse by repeated squaring) makes the
+//              basis reduced.  Every row carries its coefficients over the
+//              candidates (E), so basis = T * D[S, panel] for the selected
+//              rows S.
+//   k_gather2  F[i] = D[i, pivot columns] for every other row (active rows
+//              and earlier pivot rows: back elimination), rows with F != 0
+//   K11        Rn = T * D[S, c0:] and D[rows, c0:] -= F * Rn (tc_gemm.cu)
+//   k_commit2  D[S, c0:] = Rn, op counts
+// The basis of a panel is the RREF of the active rows restricted to
+// [c0, c0+w), so its pivot columns are the canonical ones and R is unique.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "internal.cuh"
+#include "tc.cuh"
+
+gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                           const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev);
+gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
+                             const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev);
+void modgemm_set_sms(int sms);
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int PK = 128;                 // pivots per panel = K of the trailing GEMM
+constexpr int PW = 512;                 // widest panel (columns)
+constexpr int LDX = PW + PK;            // row of the store: values [0, PW) | coefficients [PW, PW+PK)
+constexpr int NT = 1024;                // threads of k_panel2
+constexpr uint32_t NONE16 = 0xffffffffu;
+
+struct P2State {
+    int64_t c0, c1;                     // panel columns [c0, c1)
+    uint32_t kp;                        // pivots
+    uint32_t nrows;                     // rows listed for the trailing update
+    uint32_t ncand;                     // candidates integrated
+    uint32_t pad;
+    uint32_t sel[PK];                   // selected rows (D row ids), pivot order of T
+    uint32_t pc[PK];                    // absolute pivot columns
+};
+
+constexpr int P2_SMEM = PK * LDX * 2 + PK * PK * 2;   // row store + factor snapshot (192 KB)
+
+__device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
+{
+    const uint32_t r = v - __umulhi(v, m32) * p;
+    return r >= p ? r - p : r;
+}
+
+__device__ __forceinline__ void ld8(const uint16_t *s, uint32_t (&v)[8])
+{
+    const uint4 q = *reinterpret_cast<const uint4 *>(s);
+    v[0] = q.x & 0xffffu; v[1] = q.x >> 16; v[2] = q.y & 0xffffu; v[3] = q.y >> 16;
+    v[4] = q.z & 0xffffu; v[5] = q.z >> 16; v[6] = q.w & 0xffffu; v[7] = q.w >> 16;
+}
+__device__ __forceinline__ void st8(uint16_t *s, const uint32_t (&v)[8])
+{
+    *reinterpret_cast<uint4 *>(s) = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                                               v[6] | (v[7] << 16));
+}
+
+// lead[r] = first nonzero column of active row r in [c0, c0 + PW) relative to c0, else NONE.
+// One warp per row, 8 columns (16 bytes) per lane per step.
+__global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
+                        const uint32_t *__restrict__ rowpiv, const P2State *__restrict__ prev,
+                        uint32_t *__restrict__ lead)
+{
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= mN) return;
+    const int64_t c0 = prev->c1;
+    uint32_t res = NONE16;
+    if (rowpiv[r] == GBLA_NONE && c0 < nN) {
+        const int64_t wmax = nN - c0 < PW ? nN - c0 : PW;
+        const uint16_t *row = D + (size_t)r * ldD + c0;     // c0 is a multiple of 8? not in general
+        for (int64_t base = 0; base < wmax && res == NONE16; base += 256) {
+            const int64_t k0 = base + lane * 8;
+            uint32_t first = NONE16;
+            for (int u = 0; u < 8; u++) {
+                const int64_t k = k0 + u;
+                if (k < wmax && row[k] != 0) { first = (uint32_t)k; break; }
+            }
+            const unsigned m = __ballot_sync(FULL, first != NONE16);
+            if (m) res = __shfl_sync(FULL, first, __ffs(m) - 1);
+        }
+    }
+    if (lane == 0) lead[r] = res;
+}
+
+// Inverse W of a unit upper triangular 32 x 32 matrix U (entries beyond bs: identity),
+// by doubling block sizes: with the diagonal blocks of size s already inverted,
+// each aligned 2s-block [[A, B], [0, C]] gets its off-diagonal block -A^-1 B C^-1.
+// Five levels, two products each, all threads; U is left unchanged.
+__device__ void unit_upper_inverse(const uint32_t (*U)[33], uint32_t (*W)[33], uint32_t (*Q)[33], const Field &F)
+{
+    const int tid = threadIdx.x, i = tid >> 5, j = tid & 31;
+    W[i][j] = (i == j) ? 1u : 0u;
+    __syncthreads();
+    for (int s = 1; s < 32; s <<= 1) {
+        const int ne = 16 * s;                  // (32 / 2s) pairs x s^2 entries
+        int q = 0, r = 0, c = 0, base = 0;
+        if (tid < ne) {
+            q = tid / (s * s);
+            r = (tid / s) % s;
+            c = tid % s;
+            base = q * 2 * s;
+            uint64_t acc = 0;                   // (B C^-1)[r][c]
+            for (int k = 0; k <= c; k++) acc += (uint64_t)U[base + r][base + s + k] * W[base + s + k][base + s + c];
+            Q[base + r][base + s + c] = fmod64(acc, F);
+        }
+        __syncthreads();
+        if (tid < ne) {
+            uint64_t acc = 0;                   // (A^-1 (B C^-1))[r][c]
+            for (int k = r; k < s; k++) acc += (uint64_t)W[base + r][base + k] * Q[base + k][base + s + c];
+            const uint32_t z = fmod64(acc, F);
+            W[base + r][base + s + c] = z ? F.p - z : 0;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field F, const uint16_t *__restrict__ D,
+                                                   int64_t ldD, uint32_t *__restrict__ rowpiv,
+                                                   const uint32_t *__restrict__ lead,
+                                                   const P2State *__restrict__ prev, P2State *__restrict__ cur,
+                                                   uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,
+                                                   const uint16_t *__restrict__ invtab,
+                                                   unsigned long long *__restrict__ trace)
+{
+    extern __shared__ __align__(16) uint16_t X[];          // [PK][LDX] row store
+    uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(X + PK * LDX);   // factor snapshot
+    __shared__ uint32_t hist[PW + 1];       // lead histogram -> prefix; reused as column -> head key
+    __shared__ uint32_t crow[PK];           // D row of each physical row of the store
+    __shared__ uint32_t clead[PK];          // leading column of each physical row (chunk rounds)
+    __shared__ uint32_t cstat[PK];          // 0 free, 1 candidate, 2 head (this chunk), 3 basis
+    __shared__ uint32_t bphys[PK];          // physical row of basis slot b (slots sorted by pivot per chunk)
+    __shared__ uint32_t bpc[PK];            // pivot column (window-relative) of basis slot b
+    __shared__ uint32_t freel[PK];
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t Ub[32][33], Rb[32][33], Qb[32][33];
+    constexpr int CLMAX = 1024;
+    __shared__ uint32_t clist[CLMAX];        // rows leading inside the window (wide-mode candidates)
+    __shared__ uint32_t hmap[PW];            // column -> established head of this chunk
+    __shared__ uint32_t hinv[PK];            // inverse of each head's leading value (wide mode)
+    __shared__ uint32_t s_u[8];
+    __shared__ long long s_pos;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t p = F.p;
+    const uint32_t m32 = 0xffffffffu / p;
+    const int64_t c0 = prev->c1;
+    // optional trace (GBLA_PANEL_TRACE): cycles per phase, accumulated over panels by thread 0
+    long long t_mark = trace ? clock64() : 0;
+#define P2_LAP(k_)                                                                        \
+    do {                                                                                  \
+        if (trace && tid == 0) { const long long t_ = clock64(); trace[k_] += t_ - t_mark; t_mark = t_; } \
+    } while (0)
+    int64_t wmax = nN - c0;
+    if (wmax > PW) wmax = PW;
+    if (wmax <= 0) {
+        if (tid == 0) { cur->c0 = c0; cur->c1 = c0; cur->kp = 0; cur->nrows = 0; cur->ncand = 0; }
+        return;
+    }
+    // ---- 1. width from the lead histogram
+    for (int k = tid; k <= PW; k += NT) hist[k] = 0;
+    if (tid == 0) s_u[5] = 0;
+    __syncthreads();
+    for (int64_t r = tid; r < mN; r += NT) {
+        const uint32_t l = lead[r];
+        if (l < (uint64_t)wmax) {
+            atomicAdd(&hist[l], 1u);
+            const uint32_t q = atomicAdd(&s_u[5], 1u);
+            if (q < (uint32_t)CLMAX) clist[q] = (uint32_t)r;
+        }
+    }
+    __syncthreads();
+    {   // exclusive prefix over hist[0..PW] (threads 0..PW-1 own one entry each; PW <= NT)
+        const uint32_t v = tid < PW ? hist[tid] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = wsum[lane], z = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, z, o);
+                if (lane >= o) z += y;
+            }
+            wsum[lane] = z - w;
+        }
+        __syncthreads();
+        const uint32_t excl = x - v + wsum[warp];
+        __syncthreads();
+        if (tid < PW) hist[tid] = excl;
+        if (tid == PW - 1) hist[PW] = excl + v;
+        __syncthreads();
+    }
+    // hist[c] = number of active rows leading in [c0, c0 + c)
+    const int64_t w128 = wmax < 128 ? wmax : 128;
+    if (tid == 0) { s_u[0] = (uint32_t)w128; s_u[1] = 0; }
+    __syncthreads();
+    const bool dense = hist[w128] > (uint32_t)PK;
+    if (!dense) {
+        // widest w with <= PK candidates; a multiple of 32 (c0 stays 64-byte aligned for the
+        // GEMM epilogue's vector path) unless the panel reaches the last column
+        for (int64_t c = w128 + tid; c <= wmax; c += NT)
+            if (hist[c] <= (uint32_t)PK && (c == wmax || (c & 31) == 0)) atomicMax(&s_u[0], (uint32_t)c);
+    }
+    __syncthreads();
+    const int width = (int)s_u[0];
+    P2_LAP(0);
+    const int ldv = (width + 31) & ~31;          // value columns kept (multiple of 32)
+    static_assert(32 * (128 / 8 + PK / 8) <= NT, "dense-mode block multiply: one item per thread");
+    const int cpl = ldv / 32;                    // value columns per lane
+    const uint32_t target = dense ? (uint32_t)width : (uint32_t)PK;   // stop when nb reaches it
+    for (int k = tid; k < PK; k += NT) cstat[k] = 0;
+    __syncthreads();
+
+    // ---- 2. chunks of candidates (rows with lead < width), in row order
+    uint32_t nb = 0, ncand_tot = 0;
+    int64_t pos = 0;
+    while (nb < target && pos < mN) {
+        // free physical rows
+        if (warp == 0) {
+            uint32_t base = 0;
+            for (int q0 = 0; q0 < PK; q0 += 32) {
+                const bool fr = cstat[q0 + lane] == 0;
+                const unsigned m = __ballot_sync(FULL, fr);
+                if (fr) freel[base + __popc(m & ((1u << lane) - 1u))] = q0 + lane;
+                base += __popc(m);
+            }
+            if (lane == 0) s_u[2] = base;
+        }
+        __syncthreads();
+        const uint32_t nfree = s_u[2];
+        // collect up to nfree candidates from pos on
+        int ncand = 0;
+        if (!dense && s_u[5] <= (uint32_t)CLMAX) {
+            // wide mode: the candidates (<= PK) are in the window list; take them in row order
+            const int ncl = (int)s_u[5];
+            const int t = tid;
+            const bool ok = t < ncl && lead[clist[t]] < (uint32_t)width;
+            const unsigned msk = __ballot_sync(FULL, ok);
+            if (lane == 0) wsum[warp] = __popc(msk);
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t s = 0;
+                for (int w = 0; w < 32; w++) { const uint32_t c = wsum[w]; wsum[w] = s; s += c; }
+                s_u[3] = s;
+            }
+            __syncthreads();
+            if (ok) clead[wsum[warp] + __popc(msk & ((1u << lane) - 1u))] = clist[t];   // clead: scratch
+            __syncthreads();
+            ncand = (int)s_u[3];
+            if (tid < ncand) {                       // order by (lead, row): physical ~ pivot order
+                const uint32_t r = clead[tid];
+                const uint64_t kr = ((uint64_t)lead[r] << 32) | r;
+                int rk = 0;
+                for (int j = 0; j < ncand; j++) {
+                    const uint32_t r2 = clead[j];
+                    rk += (((uint64_t)lead[r2] << 32) | r2) < kr;
+                }
+                crow[freel[rk]] = r;
+                cstat[freel[rk]] = 1;
+            }
+            pos = mN;
+            __syncthreads();
+        }
+        while (ncand < (int)nfree && pos < mN) {
+            const int64_t r = pos + tid;
+            const bool ok = r < mN && lead[r] < (uint32_t)width;
+            const unsigned msk = __ballot_sync(FULL, ok);
+            if (lane == 0) wsum[warp] = __popc(msk);
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t s = 0;
+                for (int w = 0; w < 32; w++) { const uint32_t c = wsum[w]; wsum[w] = s; s += c; }
+                s_u[3] = (ncand + (int)s) < (int)nfree ? ncand + s : nfree;
+                s_pos = pos + NT;
+            }
+            __syncthreads();
+            const uint32_t rk = ncand + wsum[warp] + __popc(msk & ((1u << lane) - 1u));
+            if (ok && rk < nfree) { crow[freel[rk]] = (uint32_t)r; cstat[freel[rk]] = 1; }
+            if (ok && rk == nfree) s_pos = r;            // first candidate not taken
+            __syncthreads();
+            ncand = (int)s_u[3];
+            pos = s_pos;
+        }
+        if (ncand == 0) break;
+        ncand_tot += ncand;
+        P2_LAP(1);
+        // (a) load the chunk: values D[r, c0 + k], coefficients = unit vector at the physical row
+        {
+            const bool vec = ((c0 & 7) == 0) && ((ldD & 7) == 0);
+            const int gv = ldv / 8;                   // 8-column groups of values
+            for (int idx = tid; idx < ncand * gv; idx += NT) {
+                const int ci = idx / gv, g = idx % gv;
+                const uint32_t q = freel[ci];
+                const uint16_t *src = D + (size_t)crow[q] * ldD + c0 + 8 * g;
+                uint4 v;
+                if (vec && 8 * g + 8 <= width) {
+                    v = *reinterpret_cast<const uint4 *>(src);
+                } else {
+                    uint16_t t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) t[u] = (8 * g + u < width) ? src[u] : 0;
+                    v = *reinterpret_cast<uint4 *>(t);
+                }
+                *reinterpret_cast<uint4 *>(X + q * LDX + 8 * g) = v;
+            }
+            for (int idx = tid; idx < ncand * PK; idx += NT) {
+                const int ci = idx / PK, k = idx % PK;
+                const uint32_t q = freel[ci];
+                X[q * LDX + PW + k] = (k == (int)q) ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        P2_LAP(2);
+        // (b) reduce the chunk by the basis (RREF: the factor is the entry at the basis pivot)
+        if (nb > 0) {
+            for (int idx = tid; idx < ncand * (int)nb; idx += NT) {
+                const int ci = idx / nb, b = idx % nb;
+                FS[ci][b] = X[freel[ci] * LDX + bpc[b]];
+            }
+            __syncthreads();
+            const int ng = (ldv + PK) / 8;                 // 8-column groups of values and coefficients
+            for (int item = tid; item < ncand * ng; item += NT) {
+                const int ci = item / ng, g = item % ng;
+                const int k0 = g * 8 < ldv ? g * 8 : PW + (g * 8 - ldv);
+                uint16_t *xr = X + freel[ci] * LDX + k0;
+                uint32_t v8[8];
+                ld8(xr, v8);
+                uint64_t acc[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) acc[u] = v8[u];
+                for (uint32_t b = 0; b < nb; b++) {
+                    const uint32_t f = FS[ci][b];
+                    if (!f) continue;
+                    const uint64_t nf = p - f;
+                    ld8(X + bphys[b] * LDX + k0, v8);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) acc[u] += nf * v8[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) v8[u] = fmod64(acc[u], F);
+                st8(xr, v8);
+            }
+            __syncthreads();
+        }
+        P2_LAP(3);
+        // (c) rounds: leading columns, one head per column, eliminate collisions
+        for (int k = tid; k < width; k += NT) hmap[k] = NONE16;
+        __syncthreads();
+        for (;;) {
+            if (trace && tid == 0) trace[8] += 1;
+            // (c1) every remaining candidate (warp per row): leading column; while an established
+            //      head owns it, eliminate it (heads are fixed, so this chain needs no block sync)
+            for (int ci = warp; ci < ncand; ci += 32) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] != 1) continue;
+                uint16_t *xr = X + q * LDX;
+                int base = 0;
+                for (;;) {
+                    uint32_t ld = NONE16;
+                    for (; base < ldv; base += 32) {
+                        const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
+                        if (m) { ld = base + __ffs(m) - 1; break; }
+                    }
+                    if (ld == NONE16) {                       // dependent: zero on the panel
+                        if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
+                        break;
+                    }
+                    const uint32_t hq = hmap[ld];
+                    if (hq == NONE16) {
+                        if (lane == 0) clead[q] = ld;
+                        break;
+                    }
+                    const uint16_t *hr = X + hq * LDX;
+                    // dense mode: heads are normalized; wide mode: scale by the head's inverse
+                    const uint32_t gl = dense ? xr[ld] : mod32(xr[ld] * hinv[hq], p, m32);
+                    const uint32_t ng = gl ? p - gl : 0;
+                    __syncwarp();
+                    for (int k = base + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(xr[k] + ng * hr[k], p, m32);
+                    for (int k = lane; k < PK; k += 32)
+                        xr[PW + k] = (uint16_t)mod32(xr[PW + k] + ng * hr[PW + k], p, m32);
+                    __syncwarp();
+                }
+            }
+            for (int k = tid; k < width; k += NT) hist[k] = NONE16;
+            __syncthreads();
+            P2_LAP(3);
+            // (c2) one new head per leading column among the remaining candidates
+            for (int ci = tid; ci < ncand; ci += NT) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] == 1) atomicMin(&hist[clead[q]], q);
+            }
+            __syncthreads();
+            int coll = 0;
+            for (int ci = tid; ci < ncand; ci += NT) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] == 1) {
+                    if (hist[clead[q]] == q) cstat[q] = 4;     // new head: normalize below
+                    else coll = 1;                              // eliminated next round
+                }
+            }
+            coll = __syncthreads_or(coll);
+            for (int ci = warp; ci < ncand; ci += 32) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] != 4) continue;
+                uint16_t *xr = X + q * LDX;
+                const uint32_t iv = invtab[xr[clead[q]]];
+                if (!dense) {                       // wide mode: keep the row, remember 1 / lead value
+                    if (lane == 0) hinv[q] = iv;
+                    continue;
+                }
+                __syncwarp();
+                for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
+                for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
+            }
+            __syncthreads();
+            for (int ci = tid; ci < ncand; ci += NT) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] == 4) { cstat[q] = 2; hmap[clead[q]] = q; }
+            }
+            __syncthreads();
+            P2_LAP(4);
+            if (!coll) break;
+        }
+        // (d) the chunk's heads, sorted by leading column, become basis slots nb .. nb+h-1
+        if (tid < ncand) {
+            const uint32_t q = freel[tid];
+            if (cstat[q] == 2) {
+                uint32_t rk = 0;
+                for (int cj = 0; cj < ncand; cj++) {
+                    const uint32_t q2 = freel[cj];
+                    rk += cstat[q2] == 2 && clead[q2] < clead[q];
+                }
+                bphys[nb + rk] = q;
+                bpc[nb + rk] = clead[q];
+            }
+        }
+        if (tid == 0) {
+            uint32_t h = 0;
+            for (int cj = 0; cj < ncand; cj++) h += cstat[freel[cj]] == 2;
+            s_u[4] = h;
+        }
+        __syncthreads();
+        const uint32_t nb0 = nb, h = s_u[4];
+        // dead rows are free again (their coefficient columns are zero in every head)
+        for (int ci = tid; ci < ncand; ci += NT) {
+            const uint32_t q = freel[ci];
+            if (cstat[q] == 1 || cstat[q] == 0) cstat[q] = 0;
+            else if (cstat[q] == 2) cstat[q] = 3;
+        }
+        nb = nb0 + h;
+        __syncthreads();
+        // (e) back substitution over the new slots, 32-slot blocks from the bottom.  With U = the
+        //     basis at its pivot columns (unit upper triangular among the new slots, whose rows
+        //     are zero left of their pivots): block <- W block (W = inverse of the block's diagonal
+        //     part of U), then every slot above (older slots and new slots above the block) -=
+        //     its entries at the block's pivots * block.  A slot's entries at the pivots of other
+        //     blocks never change (block rows are zero there), so G is read from the rows as they
+        //     are.  Dense mode reduces values and coefficients (later chunks are reduced by the
+        //     basis); wide mode (one chunk) only needs the coefficients: T = U^-1 E.
+        P2_LAP(4);
+        if (!dense) {
+            // Wide mode (one chunk, nb0 = 0): heads h_b (pivot order, not normalized) with
+            // coefficients E_b.  U[b][b'] = h_b[pc_b'] / h_b[pc_b] is unit upper triangular and the
+            // RREF basis is W (h_b / h_b[pc_b]) with W = U^-1, so T = W E', E'_b = E_b / h_b[pc_b].
+            // W by doubling block sizes (128 x 128, entries beyond nb: identity), then T with the
+            // zero entries of E' skipped (E' is nearly diagonal on a staircase).  The value rows
+            // are dead now: W and Q live in their first 512 bytes.
+            uint16_t(*U)[PK] = FS;
+            for (int idx = tid; idx < PK * PK; idx += NT) {
+                const int b = idx / PK, b2 = idx % PK;
+                uint32_t v = (b == b2) ? 1u : 0u;
+                if (b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
+                U[b][b2] = (uint16_t)v;
+            }
+            __syncthreads();
+            // bphys is a permutation of the physical rows 0..nb-1 only if the chunk filled them;
+            // W / Q rows are indexed by logical slot b in 0..127 (all rows of the store exist)
+#define WM(i_, j_) X[(i_) * LDX + (j_)]
+#define QM(i_, j_) X[(i_) * LDX + PK + (j_)]
+            // the E rows (coefficients at offset PW) of every physical row stay untouched
+            for (int idx = tid; idx < PK * PK; idx += NT) WM(idx / PK, idx % PK) = (idx / PK == idx % PK) ? 1 : 0;
+            __syncthreads();
+            for (int s = 1; s < PK; s <<= 1) {
+                const int ne = (PK / 2) * s;       // (PK / 2s) pairs x s^2 entries
+                for (int e = tid; e < ne; e += NT) {
+                    const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
+                    uint64_t acc = 0;               // (B C^-1)[r][c]
+                    for (int k = 0; k <= c; k++) acc += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
+                    QM(base + r, base + s + c) = (uint16_t)fmod64(acc, F);
+                }
+                __syncthreads();
+                for (int e = tid; e < ne; e += NT) {
+                    const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
+                    uint64_t acc = 0;               // (A^-1 (B C^-1))[r][c]
+                    for (int k = r; k < s; k++) acc += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
+                    const uint32_t z = fmod64(acc, F);
+                    WM(base + r, base + s + c) = (uint16_t)(z ? p - z : 0);
+                }
+                __syncthreads();
+            }
+            P2_LAP(14);
+            // T = W E' -> the T tile (K index = logical slot of the coefficient's physical row)
+            for (int b = tid; b < PK; b += NT) hist[b] = NONE16;
+            __syncthreads();
+            if (tid < (int)nb) hist[bphys[tid]] = tid;           // physical -> logical
+            __syncthreads();
+            for (int pass = 0; pass < PK / 64; pass++) {
+                const int s = tid & (PK - 1), g = tid >> 7;      // physical column, 8-row group
+                const int b0 = pass * 64 + g * 8;
+                uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                if (b0 < (int)nb) {
+                    for (int b2 = b0; b2 < (int)nb; b2++) {
+                        const uint32_t q2 = bphys[b2];
+                        const uint32_t e = X[q2 * LDX + PW + s];
+                        if (!e) continue;
+                        const uint32_t ep = mod32(e * hinv[q2], p, m32);
+#pragma unroll
+                        for (int j = 0; j < 8; j++)
+                            if (b0 + j <= b2) acc[j] += (uint64_t)WM(b0 + j, b2) * ep;
+                    }
+                }
+                const uint32_t ls = hist[s];
+                if (ls != NONE16) {
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const int b = b0 + j;
+                        const uint32_t v = b < (int)nb ? fmod64(acc[j], F) : 0;
+                        const uint32_t o = tc::toff((uint32_t)b, ls);
+                        Tlo[o] = (uint8_t)(v & 0xff);
+                        Thi[o] = (uint8_t)(v >> 8);
+                    }
+                }
+            }
+            // K columns of the T tile beyond nb are zero
+            for (int idx = tid; idx < PK * PK; idx += NT) {
+                const int b = idx / PK, k = idx % PK;
+                if (k >= (int)nb) {
+                    const uint32_t o = tc::toff((uint32_t)b, (uint32_t)k);
+                    Tlo[o] = 0;
+                    Thi[o] = 0;
+                }
+            }
+#undef WM
+#undef QM
+            P2_LAP(15);
+            break;
+        }
+        const int gv = dense ? ldv / 8 : 0;      // value groups updated
+        const int ng = gv + PK / 8;              // + coefficient groups
+        for (int r1 = (int)nb; r1 > (int)nb0; r1 -= 32) {
+            const int r0 = r1 - 32 > (int)nb0 ? r1 - 32 : (int)nb0, bs = r1 - r0;
+            {
+                const int i = tid >> 5, j = tid & 31;
+                Ub[i][j] = (i < bs && j < bs) ? X[bphys[r0 + i] * LDX + bpc[r0 + j]] : (i == j ? 1u : 0u);
+            }
+            for (int idx = tid; idx < r0 * bs; idx += NT) {
+                const int r = idx / bs, k = idx % bs;
+                FS[r][k] = X[bphys[r] * LDX + bpc[r0 + k]];
+            }
+            __syncthreads();
+            P2_LAP(13);
+            unit_upper_inverse(Ub, Rb, Qb, F);     // Rb = block inverse
+            P2_LAP(14);
+            // block <- W * block (read everything, then write); bs * ng <= 32 * 32 = NT items
+            if (tid == 0) s_u[6] = 0;
+            uint32_t outv[8];
+            const int item = tid;
+            if (item < bs * ng) {
+                const int i = item / ng, g = item % ng;
+                const int k0 = g < gv ? g * 8 : PW + (g - gv) * 8;
+                uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int k = i; k < bs; k++) {
+                    const uint64_t w = Rb[i][k];
+                    if (!w) continue;
+                    uint32_t v8[8];
+                    ld8(X + bphys[r0 + k] * LDX + k0, v8);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) acc[u] += w * v8[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) outv[u] = fmod64(acc[u], F);
+            }
+            __syncthreads();
+            if (item < bs * ng) {
+                const int i = item / ng, g = item % ng;
+                const int k0 = g < gv ? g * 8 : PW + (g - gv) * 8;
+                st8(X + bphys[r0 + i] * LDX + k0, outv);
+                if (outv[0] | outv[1] | outv[2] | outv[3] | outv[4] | outv[5] | outv[6] | outv[7])
+                    atomicOr(&s_u[6], 1u << g);                  // 8-column groups where the block is nonzero
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t m = s_u[6], j = 0;
+                while (m) { wsum[j++] = __ffs(m) - 1; m &= m - 1; }
+                s_u[7] = j;
+            }
+            __syncthreads();
+            P2_LAP(15);
+            if (trace && tid == 0) trace[7] += s_u[7];
+            // rows above: R <- R - sum_k g_k * block_k, two rows per item, nonzero groups only
+            const int ngm = (int)s_u[7], nrp = (r0 + 1) / 2;
+            for (int it = tid; it < nrp * ngm; it += NT) {
+                const int rp = it / ngm, g = (int)wsum[it % ngm];
+                const int k0 = g < gv ? g * 8 : PW + (g - gv) * 8;
+                const int ra = 2 * rp, rb = 2 * rp + 1;
+                const bool hb = rb < r0;
+                uint16_t *xa = X + bphys[ra] * LDX + k0;
+                uint16_t *xb = hb ? X + bphys[rb] * LDX + k0 : xa;
+                uint32_t v8[8];
+                uint64_t aa[8], ab[8];
+                ld8(xa, v8);
+#pragma unroll
+                for (int u = 0; u < 8; u++) aa[u] = v8[u];
+                ld8(xb, v8);
+#pragma unroll
+                for (int u = 0; u < 8; u++) ab[u] = v8[u];
+                for (int k = 0; k < bs; k++) {
+                    const uint32_t ga = FS[ra][k], gb = hb ? FS[rb][k] : 0;
+                    if (!(ga | gb)) continue;
+                    const uint64_t na = ga ? p - ga : 0, nb2 = gb ? p - gb : 0;
+                    ld8(X + bphys[r0 + k] * LDX + k0, v8);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        aa[u] += na * v8[u];
+                        ab[u] += nb2 * v8[u];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) v8[u] = fmod64(aa[u], F);
+                st8(xa, v8);
+                if (hb) {
+#pragma unroll
+                    for (int u = 0; u < 8; u++) v8[u] = fmod64(ab[u], F);
+                    st8(xb, v8);
+                }
+            }
+            __syncthreads();
+            P2_LAP(5);
+        }
+        P2_LAP(5);
+        if (!dense) break;                       // wide mode: every candidate was in the one chunk
+    }
+    // ---- 3. outputs: T (A operand tile of the Rn GEMM; wide mode wrote it), S, pivot columns, rowpiv
+    for (int i = tid; dense && i < PK * PK; i += NT) {
+        const int b = i / PK, s = i % PK;
+        const uint16_t v = (b < (int)nb && s < (int)nb) ? X[bphys[b] * LDX + PW + bphys[s]] : 0;
+        const uint32_t o = tc::toff((uint32_t)b, (uint32_t)s);
+        Tlo[o] = (uint8_t)(v & 0xff);
+        Thi[o] = (uint8_t)(v >> 8);
+    }
+    if (tid < (int)nb) {
+        const uint32_t r = crow[bphys[tid]];
+        cur->sel[tid] = r;
+        cur->pc[tid] = (uint32_t)(c0 + bpc[tid]);
+        rowpiv[r] = (uint32_t)(c0 + bpc[tid]);          // marks S (pivot column >= c0)
+    }
+    P2_LAP(6);
+    if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; }
+#undef P2_LAP
+    if (tid == 0) {
+        cur->c0 = c0;
+        cur->c1 = c0 + width;
+        cur->kp = nb;
+        cur->nrows = 0;
+        cur->ncand = ncand_tot;
+    }
+}
+
+// F[slot] = D[i, pivot columns] for every row i not selected in this panel with
+// a nonzero coefficient (limb planes of the trailing GEMM's A tiles), rows[slot] = i.
+__global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ldD,
+                          const uint32_t *__restrict__ rowpiv, P2State *__restrict__ ps,
+                          uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows)
+{
+    constexpr int CPL = PK / 32;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t kp = ps->kp;
+    if (i >= mN || kp == 0) return;
+    const uint32_t rp = rowpiv[i];
+    if (rp != GBLA_NONE && rp >= (uint64_t)ps->c0) return;   // selected now: becomes Rn
+    const uint16_t *drow = D + (size_t)i * ldD;
+    uint16_t v[CPL];
+    bool nz = false;
+#pragma unroll
+    for (int u = 0; u < CPL; u++) {
+        const uint32_t b = lane * CPL + u;
+        v[u] = b < kp ? drow[ps->pc[b]] : 0;
+        nz |= v[u] != 0;
+    }
+    if (!__any_sync(FULL, nz)) return;
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(&ps->nrows, 1u);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (lane == 0) rows[slot] = (uint32_t)i;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int u = 0; u < CPL; u++) {
+        lo |= (uint32_t)(v[u] & 0xff) << (8 * u);
+        hi |= (uint32_t)(v[u] >> 8) << (8 * u);
+    }
+    const size_t o = (size_t)(slot / 128) * (PK * 128) + tc::toff(slot % 128, lane * CPL);
+    *reinterpret_cast<uint32_t *>(Flo + o) = lo;
+    *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
+}
+
+// transposed limb planes of D[S, c0:]: B operand tiles (64 columns x K = 128) of the Rn GEMM
+__global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
+                             const P2State *__restrict__ ps, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi)
+{
+    const uint32_t kp = ps->kp;
+    if (kp == 0) return;
+    const int64_t c0 = ps->c0;
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c0 + x >= nN) return;
+    const uint32_t s = blockIdx.y * 16;
+    if (s >= kp) {      // zero K rows beyond kp (the tile is reused panel to panel)
+        const size_t o = (size_t)(x / 64) * (64 * PK) + tc::toff64((uint32_t)(x % 64), s);
+        *reinterpret_cast<uint4 *>(Blo + o) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4 *>(Bhi + o) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    uint8_t lo[16], hi[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+        const uint16_t v = (s + u < kp) ? D[(size_t)ps->sel[s + u] * ldD + c0 + x] : 0;
+        lo[u] = (uint8_t)(v & 0xff);
+        hi[u] = (uint8_t)(v >> 8);
+    }
+    const size_t o = (size_t)(x / 64) * (64 * PK) + tc::toff64((uint32_t)(x % 64), s);
+    *reinterpret_cast<uint4 *>(Blo + o) = *reinterpret_cast<uint4 *>(lo);
+    *reinterpret_cast<uint4 *>(Bhi + o) = *reinterpret_cast<uint4 *>(hi);
+}
+
+// D[S_b, c0 + x] = Rn[b][x]; op counts (block 0, thread 0)
+__global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, const P2State *__restrict__ ps,
+                          const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops)
+{
+    const uint32_t b = blockIdx.y;
+    const uint32_t kp = ps->kp;
+    const int64_t c0 = ps->c0;
+    if (b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
+        const unsigned long long w = (unsigned long long)(nN - c0);
+        ops[0] += (unsigned long long)ps->nrows * kp * w;                     // trailing update
+        ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
+        ops[2] += (unsigned long long)ps->ncand * kp * (unsigned long long)(ps->c1 - c0);   // panel RREF
+    }
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kp || c0 + x >= nN) return;
+    D[(size_t)ps->sel[b] * ldD + c0 + x] = Rn[(size_t)b * ldR + x];
+}
+
+__global__ void k_p2_init(P2State *ps)
+{
+    ps[0].c0 = ps[0].c1 = 0;
+    ps[1].c0 = ps[1].c1 = 0;
+    ps[0].kp = ps[1].kp = 0;
+    ps[0].nrows = ps[1].nrows = 0;
+}
+
+}  // namespace
+
+// Echelon of D with width-adaptive panels (GBLA_DENSE_TC, default).
+gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab)
+{
+    cudaStream_t st = h->stream;
+    modgemm_set_sms(h->ctx->sm_count);
+    const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
+    const int64_t npad = (nN + 63) / 64 * 64 + 64;
+    uint32_t *rows, *lead;
+    uint16_t *Rn;
+    uint8_t *Flo, *Fhi, *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
+    P2State *ps;
+    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
+    GBLA_TRY(dalloc_t(h, mN + 1, &lead));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Flo));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Fhi));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rtlo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rthi));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
+    GBLA_TRY(dalloc(h, 2 * sizeof(P2State), (void **)&ps));
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+        attr = true;
+    }
+    k_p2_init<<<1, 1, 0, st>>>(ps);
+    note_launch();
+    unsigned long long *trace = nullptr;
+    if (getenv("GBLA_PANEL_TRACE")) {
+        GBLA_TRY(dalloc_t(h, 16, &trace));
+        GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 16 * 8, st));
+    }
+    // panels are launched in batches; c0 lives on the device, so the host only checks for
+    // completion between batches (a panel past the end does nothing)
+    int64_t *c1_host = nullptr;
+    GBLA_CUDA_TRY(cudaMallocHost(&c1_host, sizeof(int64_t)));
+    int batch = 8;
+    int64_t k = 0;
+    gbla_status status = GBLA_OK;
+    for (;;) {
+        for (int q = 0; q < batch; q++, k++) {
+            P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
+            k_lead2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
+            kt_mark(h, KT_PANEL);
+            k_panel2<<<1, NT, P2_SMEM, st>>>(mN, nN, h->F, h->D, ldD, rowpiv, lead, prev, cur, Tlo, Thi, invtab,
+                                             trace);
+            kt_mark(h, KT_PANEL);
+            k_gather2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows);
+            k_gather_st2<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, h->D, ldD, cur, Blo, Bhi);
+            note_launch(4);
+            kt_mark(h, KT_RN);
+            status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp);
+            kt_mark(h, KT_RN);
+            if (status != GBLA_OK) break;
+            kt_mark(h, KT_TRAIL);
+            status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D, ldD, &cur->c0);
+            kt_mark(h, KT_TRAIL);
+            if (status != GBLA_OK) break;
+            k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops);
+            note_launch();
+            if (cudaGetLastError() != cudaSuccess) { set_error("echelon: launch failed"); status = GBLA_E_CUDA; break; }
+        }
+        if (status != GBLA_OK) break;
+        P2State *last = ps + ((k - 1) & 1);
+        if (cudaMemcpyAsync(c1_host, &last->c1, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            set_error("echelon: %s", cudaGetErrorString(cudaGetLastError()));
+            status = GBLA_E_CUDA;
+            break;
+        }
+        if (*c1_host >= nN) break;
+        // the remaining columns bound the panels still needed (>= 1 column each, usually far more)
+        batch = 16;
+    }
+    cudaFreeHost(c1_host);
+    if (trace && status == GBLA_OK) {   // diagnostics: mean cycles per phase over the panels that ran
+        unsigned long long tr[16];
+        GBLA_CUDA_TRY(cudaMemcpy(tr, trace, sizeof tr, cudaMemcpyDeviceToHost));
+        const double n = tr[9] ? (double)tr[9] : 1.0;
+        fprintf(stderr,
+                "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f reduce %.0f "
+                "rounds(c2) %.0f rows-above %.0f output %.0f; rounds(c1) %.0f, backsub: snapshot %.0f inverse %.0f "
+                "W-mult %.0f; rounds/panel %.2f candidates %.1f pivots %.1f width %.1f groups/block %.1f\n",
+                tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n,
+                tr[3] / n, tr[13] / n, tr[14] / n, tr[15] / n, tr[8] / n,
+                tr[10] / n, tr[11] / n, tr[12] / n, tr[7] / (n * 4));
+    }
+    return status;
+}

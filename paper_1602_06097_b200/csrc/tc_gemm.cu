@@ -50,11 +50,19 @@ __global__ void __launch_bounds__(128) k_modgemm_tc(
     const uint8_t *__restrict__ Alo, const uint8_t *__restrict__ Ahi,     // A tiles (row tile rt at rt*A_PLANE)
     const uint8_t *__restrict__ Blo, const uint8_t *__restrict__ Bhi,     // B tiles (col tile ct at ct*B_PLANE)
     const uint32_t *__restrict__ rowidx, uint16_t *__restrict__ C, int64_t ldc,
-    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi)                 // MODE_STORE: output B tiles
+    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,                 // MODE_STORE: output B tiles
+    const int64_t *__restrict__ c0_dev,      // optional: columns [*c0_dev, cols) (MODE_SUB: of C)
+    const uint32_t *__restrict__ skip_dev)   // optional: nothing to do when *skip_dev == 0
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t full[2], accbar;
     __shared__ uint32_t tmem_base;
+    if (skip_dev && *skip_dev == 0) return;
+    if (c0_dev) {
+        const int64_t c0 = *c0_dev;
+        cols -= c0;
+        if (MODE == MODE_SUB) C += c0;
+    }
     const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : nrows;
     const int64_t ntr = (nr + BM - 1) / BM, ntc = (cols + BN - 1) / BN, ntiles = ntr * ntc;
     const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
@@ -254,14 +262,14 @@ int g_sms = 148;
 // columns grouped by 64 (B_PLANE bytes per plane per tile).
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                           const uint32_t *rowidx, uint16_t *C, int64_t ldc)
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev)
 {
     GBLA_TRY(set_attr<MODE_SUB>());
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
     const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
     const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
     k_modgemm_tc<MODE_SUB><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi,
-                                                                    rowidx, C, ldc, nullptr, nullptr);
+                                                                    rowidx, C, ldc, nullptr, nullptr, c0_dev, nullptr);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -269,14 +277,14 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
 
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi)
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev)
 {
     GBLA_TRY(set_attr<MODE_STORE>());
     if (cols <= 0) return GBLA_OK;
     const int64_t tiles = (cols + BN - 1) / BN;
     const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
     k_modgemm_tc<MODE_STORE><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi,
-                                                                      nullptr, O, ldo, Tlo, Thi);
+                                                                      nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -315,7 +323,7 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
     k_split_rows<<<grid_for(rp * KP, 256), 256, 0, st>>>(rows, rp, K, A, lda, Alo, Ahi);
     k_split_cols<<<grid_for(cp * KP, 256), 256, 0, st>>>(cols, cp, K, B, ldb, Blo, Bhi);
     note_launch(2);
-    gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc);
+    gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
