@@ -182,14 +182,15 @@ gbla_status update_d_tc(gbla_mat h);
 void band_free(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
 gbla_status ensure_multilines(gbla_mat h);
-static inline void kt_mark(gbla_mat h, int which)
+static inline void kt_mark_on(gbla_mat h, int which, cudaStream_t s)
 {
     if (!h->kt.on) return;
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
-    cudaEventRecord(e, h->stream);
+    cudaEventRecord(e, s);
     h->kt.ev[which].push_back(e);
 }
+static inline void kt_mark(gbla_mat h, int which) { kt_mark_on(h, which, h->stream); }
 // multi-GPU (dist.cu)
 gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out);
 gbla_status dist_sparse_phase(gbla_mat h);

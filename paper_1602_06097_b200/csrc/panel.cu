@@ -33,12 +33,15 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <vector>
+
 #include "internal.cuh"
 #include "tc.cuh"
 
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev);
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap);
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev);
@@ -515,63 +518,85 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
             __syncthreads();
             for (int s = 1; s < PK; s <<= 1) {
                 const int ne = (PK / 2) * s;       // (PK / 2s) pairs x s^2 entries
+                // entries in rows or columns >= nb stay identity / zero (U is the identity there)
+                if (s >= (int)nb) break;
                 for (int e = tid; e < ne; e += NT) {
                     const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
-                    uint64_t acc = 0;               // (B C^-1)[r][c]
-                    for (int k = 0; k <= c; k++) acc += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
-                    QM(base + r, base + s + c) = (uint16_t)fmod64(acc, F);
+                    if (base + r >= (int)nb || base + s + c >= (int)nb) continue;
+                    uint64_t a0 = 0, a1 = 0;        // (B C^-1)[r][c]
+                    int k = 0;
+                    for (; k + 1 <= c; k += 2) {
+                        a0 += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
+                        a1 += (uint64_t)U[base + r][base + s + k + 1] * WM(base + s + k + 1, base + s + c);
+                    }
+                    if (k <= c) a0 += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
+                    QM(base + r, base + s + c) = (uint16_t)fmod64(a0 + a1, F);
                 }
                 __syncthreads();
                 for (int e = tid; e < ne; e += NT) {
                     const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
-                    uint64_t acc = 0;               // (A^-1 (B C^-1))[r][c]
-                    for (int k = r; k < s; k++) acc += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
-                    const uint32_t z = fmod64(acc, F);
+                    if (base + r >= (int)nb || base + s + c >= (int)nb) continue;
+                    uint64_t a0 = 0, a1 = 0;        // (A^-1 (B C^-1))[r][c]
+                    const int kmax = (base + s <= (int)nb) ? s : (int)nb - base;
+                    int k = r;
+                    for (; k + 1 < kmax; k += 2) {
+                        a0 += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
+                        a1 += (uint64_t)WM(base + r, base + k + 1) * QM(base + k + 1, base + s + c);
+                    }
+                    if (k < kmax) a0 += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
+                    const uint32_t z = fmod64(a0 + a1, F);
                     WM(base + r, base + s + c) = (uint16_t)(z ? p - z : 0);
                 }
                 __syncthreads();
             }
             P2_LAP(14);
-            // T = W E' -> the T tile (K index = logical slot of the coefficient's physical row)
-            for (int b = tid; b < PK; b += NT) hist[b] = NONE16;
+            // T = W E' -> the T tile (K index = logical slot).  Column s of E' (s = physical row of
+            // a head) has few nonzeros (1 on a staircase: the head itself): list them per column,
+            // (row, value) pairs in the dead value area of store row s, then T[b][ls] =
+            // sum over the list of W[b][row] * value.
+            constexpr int LMAX = 8;
+            uint32_t *lcnt = clead;                               // per physical column (clead is dead)
+            for (int k = tid; k < PK; k += NT) lcnt[k] = 0;
             __syncthreads();
-            if (tid < (int)nb) hist[bphys[tid]] = tid;           // physical -> logical
-            __syncthreads();
-            for (int pass = 0; pass < PK / 64; pass++) {
-                const int s = tid & (PK - 1), g = tid >> 7;      // physical column, 8-row group
-                const int b0 = pass * 64 + g * 8;
-                uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                if (b0 < (int)nb) {
-                    for (int b2 = b0; b2 < (int)nb; b2++) {
-                        const uint32_t q2 = bphys[b2];
-                        const uint32_t e = X[q2 * LDX + PW + s];
-                        if (!e) continue;
-                        const uint32_t ep = mod32(e * hinv[q2], p, m32);
-#pragma unroll
-                        for (int j = 0; j < 8; j++)
-                            if (b0 + j <= b2) acc[j] += (uint64_t)WM(b0 + j, b2) * ep;
-                    }
-                }
-                const uint32_t ls = hist[s];
-                if (ls != NONE16) {
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const int b = b0 + j;
-                        const uint32_t v = b < (int)nb ? fmod64(acc[j], F) : 0;
-                        const uint32_t o = tc::toff((uint32_t)b, ls);
-                        Tlo[o] = (uint8_t)(v & 0xff);
-                        Thi[o] = (uint8_t)(v >> 8);
+            for (int b2 = warp; b2 < (int)nb; b2 += 32) {        // warp per head row: contiguous E row
+                const uint32_t q2 = bphys[b2];
+                const uint32_t hv = hinv[q2];
+                for (int sc = lane; sc < PK; sc += 32) {
+                    const uint32_t e = X[q2 * LDX + PW + sc];
+                    if (!e) continue;
+                    const uint32_t j = atomicAdd(&lcnt[sc], 1u);
+                    if (j < (uint32_t)LMAX) {
+                        uint16_t *lst = X + sc * LDX + 2 * PK;   // [0, LMAX) rows, [LMAX, 2 LMAX) values
+                        lst[j] = (uint16_t)b2;
+                        lst[LMAX + j] = (uint16_t)mod32(e * hv, p, m32);
                     }
                 }
             }
-            // K columns of the T tile beyond nb are zero
+            __syncthreads();
             for (int idx = tid; idx < PK * PK; idx += NT) {
-                const int b = idx / PK, k = idx % PK;
-                if (k >= (int)nb) {
-                    const uint32_t o = tc::toff((uint32_t)b, (uint32_t)k);
-                    Tlo[o] = 0;
-                    Thi[o] = 0;
+                const int b = idx >> 7, ls = idx & (PK - 1);
+                uint32_t v = 0;
+                if (b < (int)nb && ls < (int)nb) {
+                    const uint32_t sc = bphys[ls];
+                    const uint16_t *lst = X + sc * LDX + 2 * PK;
+                    const uint32_t cnt = lcnt[sc];
+                    uint64_t acc = 0;
+                    if (cnt <= (uint32_t)LMAX) {
+                        for (uint32_t j = 0; j < cnt; j++) {
+                            const uint32_t b2 = lst[j];
+                            if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lst[LMAX + j];
+                        }
+                    } else {                                      // dense column: every head row
+                        for (int b2 = b; b2 < (int)nb; b2++) {
+                            const uint32_t e = X[bphys[b2] * LDX + PW + sc];
+                            if (e) acc += (uint64_t)WM(b, b2) * mod32(e * hinv[bphys[b2]], p, m32);
+                        }
+                    }
+                    v = fmod64(acc, F);
                 }
+                const uint32_t o = tc::toff((uint32_t)b, (uint32_t)ls);
+                Tlo[o] = (uint8_t)(v & 0xff);
+                Thi[o] = (uint8_t)(v >> 8);
             }
 #undef WM
 #undef QM
@@ -766,20 +791,24 @@ __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t
 }
 
 // D[S_b, c0 + x] = Rn[b][x]; op counts (block 0, thread 0)
+// part 0: all columns; 1: the next panel's window [c1, c1 + PW); 2: the other columns (+ op counts)
 __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, const P2State *__restrict__ ps,
-                          const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops)
+                          const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops, int part)
 {
     const uint32_t b = blockIdx.y;
     const uint32_t kp = ps->kp;
     const int64_t c0 = ps->c0;
-    if (b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
+    if (part != 1 && b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
         const unsigned long long w = (unsigned long long)(nN - c0);
         ops[0] += (unsigned long long)ps->nrows * kp * w;                     // trailing update
         ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * kp * (unsigned long long)(ps->c1 - c0);   // panel RREF
     }
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t w = ps->c1 - c0;
+    const int64_t x = (part == 1 ? w : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= kp || c0 + x >= nN) return;
+    const bool in_win = x >= w && x < w + PW;
+    if ((part == 1 && !in_win) || (part == 2 && in_win)) return;
     D[(size_t)ps->sel[b] * ldD + c0 + x] = Rn[(size_t)b * ldR + x];
 }
 
@@ -794,20 +823,30 @@ __global__ void k_p2_init(P2State *ps)
 }  // namespace
 
 // Echelon of D with width-adaptive panels (GBLA_DENSE_TC, default).
+// Echelon of D with width-adaptive panels (GBLA_DENSE_TC, default), with a
+// look-ahead of one panel: the trailing update of panel k is split into the
+// next panel's window (done first) and the rest; the next panel (lead, panel
+// factorization, gather of F) runs on a side stream on the one SM the
+// trailing GEMM leaves free while the rest of the update runs.  Hazards: the
+// side stream reads D only inside the window (updated and committed before
+// it starts) and writes the other parity of F / rows / the panel state; the
+// main stream waits for it before the next panel's GEMMs.
 gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab)
 {
     cudaStream_t st = h->stream;
     modgemm_set_sms(h->ctx->sm_count);
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
     const int64_t npad = (nN + 63) / 64 * 64 + 64;
-    uint32_t *rows, *lead;
+    uint32_t *rows[2], *lead;
     uint16_t *Rn;
-    uint8_t *Flo, *Fhi, *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
+    uint8_t *Flo[2], *Fhi[2], *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
     P2State *ps;
-    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
+    for (int q = 0; q < 2; q++) {
+        GBLA_TRY(dalloc_t(h, mN + 1, &rows[q]));
+        GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Flo[q]));
+        GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Fhi[q]));
+    }
     GBLA_TRY(dalloc_t(h, mN + 1, &lead));
-    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Flo));
-    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Fhi));
     GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo));
     GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi));
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
@@ -821,67 +860,145 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
         attr = true;
     }
-    k_p2_init<<<1, 1, 0, st>>>(ps);
-    note_launch();
     unsigned long long *trace = nullptr;
     if (getenv("GBLA_PANEL_TRACE")) {
         GBLA_TRY(dalloc_t(h, 16, &trace));
         GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 16 * 8, st));
     }
-    // panels are launched in batches; c0 lives on the device, so the host only checks for
-    // completion between batches (a panel past the end does nothing)
+    const bool lookahead = getenv("GBLA_NO_LOOKAHEAD") == nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t evA = nullptr, evB = nullptr;
     int64_t *c1_host = nullptr;
-    GBLA_CUDA_TRY(cudaMallocHost(&c1_host, sizeof(int64_t)));
+    gbla_status status = GBLA_OK;
+    auto fail = [&](const char *what) {
+        set_error("echelon: %s: %s", what, cudaGetErrorString(cudaGetLastError()));
+        status = GBLA_E_CUDA;
+    };
+    const int gemm_grid = lookahead ? h->ctx->sm_count - 1 : h->ctx->sm_count;   // one SM for the next panel
+    // the panel factorization of panel k on stream s (prev = panel k-1's state)
+    auto factor = [&](cudaStream_t s, int64_t k) {
+        P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
+        k_lead2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
+        kt_mark_on(h, KT_PANEL, s);
+        k_panel2<<<1, NT, P2_SMEM, s>>>(mN, nN, h->F, h->D, ldD, rowpiv, lead, prev, cur, Tlo, Thi, invtab, trace);
+        kt_mark_on(h, KT_PANEL, s);
+        k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
+                                                          rows[k & 1]);
+        note_launch(3);
+    };
+    if (lookahead) {
+        int lo_pri = 0, hi_pri = 0;        // the next panel is the critical path: schedule it first
+        cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+        if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_pri) != cudaSuccess ||
+            cudaEventCreateWithFlags(&evA, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&evB, cudaEventDisableTiming) != cudaSuccess)
+            fail("stream/event creation");
+    }
+    if (status == GBLA_OK && cudaMallocHost(&c1_host, sizeof(int64_t)) != cudaSuccess) fail("cudaMallocHost");
+    if (status == GBLA_OK) {
+        k_p2_init<<<1, 1, 0, st>>>(ps);
+        note_launch();
+        factor(st, 0);                                  // panel 0 on the main stream
+    }
+    // optional timeline (GBLA_ECH_TIMELINE=n): device times of the first n look-ahead iterations
+    const int ntl = getenv("GBLA_ECH_TIMELINE") ? atoi(getenv("GBLA_ECH_TIMELINE")) : 0;
+    std::vector<cudaEvent_t> tl;
+    auto tmark = [&](int64_t it, cudaStream_t s) {
+        if (it >= ntl) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        tl.push_back(e);
+    };
     int batch = 8;
     int64_t k = 0;
-    gbla_status status = GBLA_OK;
-    for (;;) {
-        for (int q = 0; q < batch; q++, k++) {
-            P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
-            k_lead2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
-            kt_mark(h, KT_PANEL);
-            k_panel2<<<1, NT, P2_SMEM, st>>>(mN, nN, h->F, h->D, ldD, rowpiv, lead, prev, cur, Tlo, Thi, invtab,
-                                             trace);
-            kt_mark(h, KT_PANEL);
-            k_gather2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows);
+    while (status == GBLA_OK) {
+        for (int q = 0; q < batch && status == GBLA_OK; q++, k++) {
+            P2State *cur = ps + (k & 1);
+            const int f = (int)(k & 1);
+            tmark(k, st);
             k_gather_st2<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, h->D, ldD, cur, Blo, Bhi);
-            note_launch(4);
+            note_launch();
             kt_mark(h, KT_RN);
             status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp);
             kt_mark(h, KT_RN);
             if (status != GBLA_OK) break;
-            kt_mark(h, KT_TRAIL);
-            status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D, ldD, &cur->c0);
-            kt_mark(h, KT_TRAIL);
-            if (status != GBLA_OK) break;
-            k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops);
-            note_launch();
-            if (cudaGetLastError() != cudaSuccess) { set_error("echelon: launch failed"); status = GBLA_E_CUDA; break; }
+            if (!lookahead) {
+                kt_mark(h, KT_TRAIL);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
+                                        ldD, &cur->c0, nullptr, 0, 0, gemm_grid);
+                kt_mark(h, KT_TRAIL);
+                if (status != GBLA_OK) break;
+                k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 0);
+                note_launch();
+                factor(st, k + 1);
+            } else {
+                // the next panel's window first, then the next panel beside the rest of the update
+                kt_mark(h, KT_TRAIL);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid);
+                if (status != GBLA_OK) break;
+                k_commit2<<<dim3(PW / 256, PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 1);
+                note_launch();
+                if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
+                    fail("event");
+                    break;
+                }
+                tmark(k, side);
+                factor(side, k + 1);
+                tmark(k, side);
+                if (cudaEventRecord(evB, side) != cudaSuccess) { fail("event"); break; }
+                tmark(k, st);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid);
+                kt_mark(h, KT_TRAIL);
+                if (status != GBLA_OK) break;
+                k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 2);
+                note_launch();
+                tmark(k, st);
+                if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
+            }
+            if (cudaGetLastError() != cudaSuccess) { fail("launch"); break; }
         }
         if (status != GBLA_OK) break;
         P2State *last = ps + ((k - 1) & 1);
         if (cudaMemcpyAsync(c1_host, &last->c1, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess) {
-            set_error("echelon: %s", cudaGetErrorString(cudaGetLastError()));
-            status = GBLA_E_CUDA;
+            fail("sync");
             break;
         }
         if (*c1_host >= nN) break;
-        // the remaining columns bound the panels still needed (>= 1 column each, usually far more)
         batch = 16;
     }
-    cudaFreeHost(c1_host);
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+    }
+    if (!tl.empty()) {
+        cudaDeviceSynchronize();
+        // per iteration: [start(main), side start, side end, rest start(main), rest end(main)]
+        for (size_t i = 0; i + 5 <= tl.size(); i += 5) {
+            float a[5];
+            for (int j = 0; j < 5; j++) cudaEventElapsedTime(&a[j], tl[0], tl[i + j]);
+            fprintf(stderr, "[gbla timeline] it %zu: start %.1f  side %.1f..%.1f (%.1f us)  rest %.1f..%.1f (%.1f us)\n",
+                    i / 5, a[0] * 1e3, a[1] * 1e3, a[2] * 1e3, (a[2] - a[1]) * 1e3, a[3] * 1e3, a[4] * 1e3,
+                    (a[4] - a[3]) * 1e3);
+        }
+        for (cudaEvent_t e : tl) cudaEventDestroy(e);
+    }
+    if (evA) cudaEventDestroy(evA);
+    if (evB) cudaEventDestroy(evB);
+    if (c1_host) cudaFreeHost(c1_host);
     if (trace && status == GBLA_OK) {   // diagnostics: mean cycles per phase over the panels that ran
         unsigned long long tr[16];
         GBLA_CUDA_TRY(cudaMemcpy(tr, trace, sizeof tr, cudaMemcpyDeviceToHost));
         const double n = tr[9] ? (double)tr[9] : 1.0;
         fprintf(stderr,
-                "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f reduce %.0f "
-                "rounds(c2) %.0f rows-above %.0f output %.0f; rounds(c1) %.0f, backsub: snapshot %.0f inverse %.0f "
-                "W-mult %.0f; rounds/panel %.2f candidates %.1f pivots %.1f width %.1f groups/block %.1f\n",
-                tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n,
-                tr[3] / n, tr[13] / n, tr[14] / n, tr[15] / n, tr[8] / n,
-                tr[10] / n, tr[11] / n, tr[12] / n, tr[7] / (n * 4));
+                "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f rounds(c1) %.0f "
+                "rounds(c2) %.0f dense-backsub %.0f output %.0f; wide: inverse %.0f T %.0f; rounds/panel %.2f "
+                "candidates %.1f pivots %.1f width %.1f\n",
+                tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[14] / n,
+                tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
     }
     return status;
 }

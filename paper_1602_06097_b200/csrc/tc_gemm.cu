@@ -14,17 +14,18 @@
 // already in the tcgen05 K-major SWIZZLE_NONE core-matrix layout, so one
 // cp.async.bulk (TMA bulk copy, SASS UBLKCP) per plane stages it.
 //
-// Persistent kernel: CTA b (128 threads) owns a contiguous range of output
-// tiles (BM = 128 rows x BN = 64 columns) in row-tile-major order, so the A
-// tile of a row tile is fetched once and reused for all of its column tiles
-// (a stage re-copies A only when its row tile changes); the next tile's
-// operands are double-buffered behind the current MMAs.  TMEM holds
-// HH | X | LL (3 x 64 columns of a 256-column allocation); one thread issues
-// 16 MMAs (4 K-steps x 4 limb products) and commits to an mbarrier; 4 warps
-// run the epilogue: tcgen05.ld (warp w owns lanes 32w..32w+31), reduce mod
-// p, stage the 128 x 64 result in shared memory (XOR-swizzled 16-byte
-// chunks), then read-modify-write C one full 128-byte row segment per warp
-// instruction.
+// k_modgemm_ws: persistent, one CTA per SM (128 KB of operand stages), warp
+// specialized: warp 0 stages the A tile of a row tile once (double-buffered)
+// and the B tiles through a 4-stage ring, warp 1 issues the 16 MMAs of a
+// 128 x 64 output tile (4 K-steps x 4 limb products) into one of two TMEM
+// accumulators (HH | X | LL, 3 x 64 columns each), and 8 epilogue warps
+// drain the other accumulator (tcgen05.ld: warp w reads TMEM lanes
+// 32*(w%4)..+31, half of the columns each), reduce mod p and
+// read-modify-write C (16-byte vectors per thread, the C row segment
+// prefetched before the accumulator is ready).  Loads, MMAs and epilogue of
+// consecutive tiles overlap.  Each CTA owns a contiguous range of output
+// tiles in row-tile-major order (A reuse).  Column-tile subsets (CT_WINDOW /
+// CT_REST) split one update into the echelon look-ahead's two parts.
 //   MODE_SUB    C[rowidx[i], x] = C - S   mod p     (trailing update)
 //   MODE_STORE  O[i, x] = S mod p, plus O's limb planes as B tiles
 //               (the B operand of a following MODE_SUB GEMM)
@@ -38,165 +39,254 @@ constexpr uint32_t A_PLANE = BM * KP;      // 16 KB
 constexpr uint32_t B_PLANE = BN * KP;      // 8 KB
 constexpr uint32_t A_BYTES = 2 * A_PLANE, B_BYTES = 2 * B_PLANE;
 constexpr uint32_t STAGE = A_BYTES + B_BYTES;   // 48 KB
-constexpr int SMEM_TOTAL = 2 * STAGE;
 enum { MODE_SUB = 0, MODE_STORE = 1 };
 
 using tc::toff64;
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
 
+
+// Column-tile subsets (look-ahead of the echelon): with W0 = (*win_dev - c0) / BN and
+// W1 = ceil((*win_dev - c0 + win_w) / BN): CT_WINDOW = tiles [W0, W1), CT_REST = the others.
+enum { CT_ALL = 0, CT_WINDOW = 1, CT_REST = 2 };
+
+struct MMArgs {
+    int64_t nrows;                    // rows (if nrows_dev is NULL)
+    const uint32_t *nrows_dev;
+    int64_t cols;                     // columns (total; minus *c0_dev if given)
+    Field F;
+    const uint8_t *Alo, *Ahi, *Blo, *Bhi;
+    const uint32_t *rowidx;
+    uint16_t *C;
+    int64_t ldc;
+    uint8_t *Tlo, *Thi;               // MODE_STORE: limb planes of the result as B tiles
+    const int64_t *c0_dev;
+    const uint32_t *skip_dev;
+    const int64_t *win_dev;
+    int64_t win_w;
+    int ctsel;
+};
+
+constexpr int NSB = 4;                               // B stages
+constexpr int WS_THREADS = 320;                      // producer, MMA, 8 epilogue warps
+constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB: one CTA per SM)
+
+// Warp-specialized persistent K11: warp 0 stages operands (A tile once per row
+// tile, double-buffered; B tiles through a 4-stage ring), warp 1 issues the
+// MMAs into one of two TMEM accumulators (HH | X | LL, 192 columns each), warps
+// 2..9 drain the other accumulator (warp w reads TMEM lanes 32*(w%4).., half of
+// the 64 columns each), so loads, MMAs and the epilogue of consecutive tiles
+// overlap.  Each CTA owns a contiguous range of output tiles in row-tile-major
+// order (A reuse).
 template <int MODE>
-__global__ void __launch_bounds__(128) k_modgemm_tc(
-    int64_t nrows, const uint32_t *__restrict__ nrows_dev, int64_t cols, Field F,
-    const uint8_t *__restrict__ Alo, const uint8_t *__restrict__ Ahi,     // A tiles (row tile rt at rt*A_PLANE)
-    const uint8_t *__restrict__ Blo, const uint8_t *__restrict__ Bhi,     // B tiles (col tile ct at ct*B_PLANE)
-    const uint32_t *__restrict__ rowidx, uint16_t *__restrict__ C, int64_t ldc,
-    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,                 // MODE_STORE: output B tiles
-    const int64_t *__restrict__ c0_dev,      // optional: columns [*c0_dev, cols) (MODE_SUB: of C)
-    const uint32_t *__restrict__ skip_dev)   // optional: nothing to do when *skip_dev == 0
+__global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t full[2], accbar;
+    __shared__ uint64_t afull[2], aempty[2], bfull[NSB], bempty[NSB], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
-    if (skip_dev && *skip_dev == 0) return;
-    if (c0_dev) {
-        const int64_t c0 = *c0_dev;
+    if (g.skip_dev && *g.skip_dev == 0) return;
+    int64_t cols = g.cols, c0 = 0;
+    uint16_t *C = g.C;
+    if (g.c0_dev) {
+        c0 = *g.c0_dev;
         cols -= c0;
         if (MODE == MODE_SUB) C += c0;
     }
-    const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : nrows;
-    const int64_t ntr = (nr + BM - 1) / BM, ntc = (cols + BN - 1) / BN, ntiles = ntr * ntc;
+    if (cols <= 0) return;
+    const int64_t nr = g.nrows_dev ? (int64_t)*g.nrows_dev : g.nrows;
+    const int64_t ntr = (nr + BM - 1) / BM, ntc_all = (cols + BN - 1) / BN;
+    int64_t w0 = 0, w1 = 0;
+    if (g.ctsel != CT_ALL) {
+        const int64_t rel = *g.win_dev - c0;
+        w0 = rel / BN;
+        w1 = (rel + g.win_w + BN - 1) / BN;
+        if (w0 > ntc_all) w0 = ntc_all;
+        if (w1 > ntc_all) w1 = ntc_all;
+    }
+    const int64_t ntc = g.ctsel == CT_ALL ? ntc_all : g.ctsel == CT_WINDOW ? w1 - w0 : ntc_all - (w1 - w0);
+    const int64_t ntiles = ntr * ntc;
     const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const int64_t t_begin = (int64_t)blockIdx.x * per;
     const int64_t t_end = t_begin + per < ntiles ? t_begin + per : ntiles;
     if (t_begin >= t_end) return;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (ldc % 8 == 0);   // 16-byte row segments
-
-    if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
+    auto ct_of = [&](int64_t j) -> int64_t {
+        if (g.ctsel == CT_WINDOW) return w0 + j;
+        if (g.ctsel == CT_REST) return j < w0 ? j : j + (w1 - w0);
+        return j;
+    };
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
-        tc::mbar_init(&full[0], 1);
-        tc::mbar_init(&full[1], 1);
-        tc::mbar_init(&accbar, 1);
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&afull[i], 1);
+            tc::mbar_init(&aempty[i], 1);
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], 8);
+        }
+        for (int i = 0; i < NSB; i++) {
+            tc::mbar_init(&bfull[i], 1);
+            tc::mbar_init(&bempty[i], 1);
+        }
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_base;
-    const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-    const uint32_t s0 = tc::smem_u32(smem);
-    int64_t stage_rt[2] = {-1, -1};                     // row tile whose A is in each stage (thread 0)
+    uint8_t *Abuf = smem, *Bbuf = smem + 2 * A_BYTES;
 
-    auto load = [&](int64_t tile, int s) {
-        const int64_t rt = tile / ntc, ct = tile % ntc;
-        uint8_t *st = smem + s * STAGE;
-        const bool needA = stage_rt[s] != rt;
-        tc::mbar_expect_tx(&full[s], needA ? STAGE : B_BYTES);
-        if (needA) {
-            tc::bulk_g2s(st, Ahi + rt * A_PLANE, A_PLANE, &full[s]);
-            tc::bulk_g2s(st + A_PLANE, Alo + rt * A_PLANE, A_PLANE, &full[s]);
-            stage_rt[s] = rt;
-        }
-        tc::bulk_g2s(st + A_BYTES, Bhi + ct * B_PLANE, B_PLANE, &full[s]);
-        tc::bulk_g2s(st + A_BYTES + B_PLANE, Blo + ct * B_PLANE, B_PLANE, &full[s]);
-    };
-    if (tid == 0) load(t_begin, 0);
-    uint32_t ph_full[2] = {0, 0}, ph_acc = 0;
-    int s = 0;
-    for (int64_t tile = t_begin; tile < t_end; tile++, s ^= 1) {
-        const int64_t rt = tile / ntc, ct = tile % ntc;
-        const int64_t row0 = rt * BM, x0 = ct * BN;
-        if (tid == 0) {
-            if (tile + 1 < t_end) load(tile + 1, s ^ 1);   // stage s^1 is free: its MMAs completed last iteration
-            tc::mbar_wait(&full[s], ph_full[s]);
-            tc::fence_after();
-            const uint32_t idesc = tc::idesc_u8(BM, BN);
-            const uint32_t aH = s0 + s * STAGE, aL = aH + A_PLANE, bH = aH + A_BYTES, bL = bH + B_PLANE;
-#pragma unroll
-            for (int k = 0; k < KP / 32; k++) {
-                const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
-                const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
-                const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
-                const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
-                const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
-                tc::mma_i8(tbase + 0, dAh, dBh, idesc, k > 0);          // HH
-                tc::mma_i8(tbase + BN, dAh, dBl, idesc, k > 0);         // X
-                tc::mma_i8(tbase + BN, dAl, dBh, idesc, 1);             // X
-                tc::mma_i8(tbase + 2 * BN, dAl, dBl, idesc, k > 0);     // LL
+    if (warp == 0) {
+        if (lane == 0) {                       // ---- producer
+            int64_t cur_rt = -1;
+            int aslot = 1;
+            uint32_t aph[2] = {1, 1}, bph[NSB] = {1, 1, 1, 1};
+            int s = 0;
+            for (int64_t tile = t_begin; tile < t_end; tile++) {
+                const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
+                if (rt != cur_rt) {
+                    aslot ^= 1;
+                    tc::mbar_wait(&aempty[aslot], aph[aslot]);
+                    aph[aslot] ^= 1;
+                    uint8_t *ab = Abuf + aslot * A_BYTES;
+                    tc::mbar_expect_tx(&afull[aslot], A_BYTES);
+                    tc::bulk_g2s(ab, g.Ahi + rt * A_PLANE, A_PLANE, &afull[aslot]);
+                    tc::bulk_g2s(ab + A_PLANE, g.Alo + rt * A_PLANE, A_PLANE, &afull[aslot]);
+                    cur_rt = rt;
+                }
+                tc::mbar_wait(&bempty[s], bph[s]);
+                bph[s] ^= 1;
+                uint8_t *bb = Bbuf + s * B_BYTES;
+                tc::mbar_expect_tx(&bfull[s], B_BYTES);
+                tc::bulk_g2s(bb, g.Bhi + ct * B_PLANE, B_PLANE, &bfull[s]);
+                tc::bulk_g2s(bb + B_PLANE, g.Blo + ct * B_PLANE, B_PLANE, &bfull[s]);
+                s = (s + 1) % NSB;
             }
-            tc::commit(&accbar);
         }
-        ph_full[s] ^= 1;
-        tc::mbar_wait(&accbar, ph_acc);
-        ph_acc ^= 1;
-        tc::fence_after();
-
-        // epilogue: thread tid = tile row tid; its 128-byte row segment of C is
-        // loaded first (8 vector loads in flight), the 4 TMEM chunks are folded in
-        // (constant register indices: no local memory), then stored back
-        const int64_t slot = row0 + tid;
-        const bool live = slot < nr;
-        uint16_t *crow = live ? C + (size_t)(MODE == MODE_SUB && rowidx ? rowidx[slot] : slot) * ldc + x0 : nullptr;
-        const bool fast = live && vec && x0 + BN <= cols;
-        uint32_t d[BN / 2];                                   // u16 pairs
+    } else if (warp == 1) {
+        if (lane == 0) {                       // ---- MMA issuer
+            int64_t cur_rt = -1;
+            int aslot = 1;
+            uint32_t aph[2] = {0, 0}, bph[NSB] = {0, 0, 0, 0}, tph[2] = {1, 1};
+            int s = 0, ab = 0;
+            const uint32_t idesc = tc::idesc_u8(BM, BN);
+            for (int64_t tile = t_begin; tile < t_end; tile++) {
+                const int64_t rt = tile / ntc;
+                if (rt != cur_rt) {
+                    if (cur_rt >= 0) tc::commit(&aempty[aslot]);   // old A free once its MMAs finish
+                    aslot ^= 1;
+                    tc::mbar_wait(&afull[aslot], aph[aslot]);
+                    aph[aslot] ^= 1;
+                    cur_rt = rt;
+                }
+                tc::mbar_wait(&bfull[s], bph[s]);
+                bph[s] ^= 1;
+                tc::mbar_wait(&tempty[ab], tph[ab]);              // accumulator drained
+                tph[ab] ^= 1;
+                tc::fence_after();
+                const uint32_t aH = tc::smem_u32(Abuf + aslot * A_BYTES), aL = aH + A_PLANE;
+                const uint32_t bH = tc::smem_u32(Bbuf + s * B_BYTES), bL = bH + B_PLANE;
+                const uint32_t d = tbase + ab * 3 * BN;
 #pragma unroll
-        for (int w = 0; w < BN / 2; w++) d[w] = 0;
-        if (MODE == MODE_SUB && live) {
+                for (int k = 0; k < KP / 32; k++) {
+                    const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
+                    const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
+                    const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
+                    const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
+                    const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
+                    tc::mma_i8(d + 0, dAh, dBh, idesc, k > 0);          // HH
+                    tc::mma_i8(d + BN, dAh, dBl, idesc, k > 0);         // X
+                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);             // X
+                    tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, k > 0);     // LL
+                }
+                tc::commit(&bempty[s]);                                 // B stage free
+                tc::commit(&tfull[ab]);                                 // accumulator ready
+                s = (s + 1) % NSB;
+                ab ^= 1;
+            }
+        }
+    } else {                                   // ---- epilogue warps 2..9
+        const int e = warp - 2, quarter = warp & 3, half = e >> 2;
+        const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (g.ldc % 8 == 0);
+        uint32_t tph[2] = {0, 0};
+        int ab = 0;
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
+            const int64_t row0 = rt * BM, x0 = ct * BN + half * 32;
+            const int64_t slot = row0 + quarter * 32 + lane;
+            const bool live = slot < nr;
+            uint16_t *crow = nullptr;
+            if (live) crow = C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot] : slot) * g.ldc + x0;
+            const bool fast = live && vec && x0 + 32 <= cols;
+            uint32_t dv[16];
+#pragma unroll
+            for (int w = 0; w < 16; w++) dv[w] = 0;
+            if (MODE == MODE_SUB && live) {          // prefetch the C row segment before waiting
+                if (fast) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint4 q = reinterpret_cast<const uint4 *>(crow)[u];
+                        dv[4 * u] = q.x; dv[4 * u + 1] = q.y; dv[4 * u + 2] = q.z; dv[4 * u + 3] = q.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; j++)
+                        if (x0 + j < cols) dv[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
+                }
+            }
+            tc::mbar_wait(&tfull[ab], tph[ab]);
+            tph[ab] ^= 1;
+            tc::fence_after();
+            const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 3 * BN + half * 32;
+#pragma unroll
+            for (int c = 0; c < 32; c += 16) {
+                uint32_t hh[16], xx[16], ll[16];
+                tc::tmem_ld16(la + c, hh);
+                tc::tmem_ld16(la + BN + c, xx);
+                tc::tmem_ld16(la + 2 * BN + c, ll);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const uint32_t s0 = fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], g.F);
+                    const uint32_t s1 = fmod64(((uint64_t)hh[j + 1] << 16) + ((uint64_t)xx[j + 1] << 8) + ll[j + 1], g.F);
+                    const int w = (c + j) / 2;
+                    if (MODE == MODE_SUB) {
+                        uint32_t lo = dv[w] & 0xffffu, hi = dv[w] >> 16;
+                        lo = lo >= s0 ? lo - s0 : lo + g.F.p - s0;
+                        hi = hi >= s1 ? hi - s1 : hi + g.F.p - s1;
+                        dv[w] = lo | (hi << 16);
+                    } else {
+                        dv[w] = s0 | (s1 << 16);
+                        if (live) {
+                            const uint32_t x = (uint32_t)(x0 + c + j);
+                            const size_t o = (size_t)(x / BN) * B_PLANE + toff64(x % BN, (uint32_t)slot);
+                            g.Tlo[o] = (uint8_t)(s0 & 0xff);
+                            g.Thi[o] = (uint8_t)(s0 >> 8);
+                            g.Tlo[o + 16] = (uint8_t)(s1 & 0xff);
+                            g.Thi[o + 16] = (uint8_t)(s1 >> 8);
+                        }
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);          // accumulator may be overwritten
+            ab ^= 1;
             if (fast) {
 #pragma unroll
-                for (int u = 0; u < BN / 8; u++) {
-                    const uint4 q = reinterpret_cast<const uint4 *>(crow)[u];
-                    d[4 * u] = q.x; d[4 * u + 1] = q.y; d[4 * u + 2] = q.z; d[4 * u + 3] = q.w;
-                }
-            } else {
+                for (int u = 0; u < 4; u++)
+                    reinterpret_cast<uint4 *>(crow)[u] = make_uint4(dv[4 * u], dv[4 * u + 1], dv[4 * u + 2], dv[4 * u + 3]);
+            } else if (live) {
 #pragma unroll
-                for (int j = 0; j < BN; j++)
-                    if (x0 + j < cols) d[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
+                for (int j = 0; j < 32; j++)
+                    if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
             }
-        }
-#pragma unroll
-        for (int c = 0; c < BN; c += 16) {
-            uint32_t hh[16], xx[16], ll[16];
-            __syncwarp();
-            tc::tmem_ld16(lane_addr + c, hh);
-            tc::tmem_ld16(lane_addr + BN + c, xx);
-            tc::tmem_ld16(lane_addr + 2 * BN + c, ll);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-                const uint32_t s0 = fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], F);
-                const uint32_t s1 = fmod64(((uint64_t)hh[j + 1] << 16) + ((uint64_t)xx[j + 1] << 8) + ll[j + 1], F);
-                const int w = (c + j) / 2;
-                if (MODE == MODE_SUB) {
-                    uint32_t lo = d[w] & 0xffffu, hi = d[w] >> 16;
-                    lo = lo >= s0 ? lo - s0 : lo + F.p - s0;
-                    hi = hi >= s1 ? hi - s1 : hi + F.p - s1;
-                    d[w] = lo | (hi << 16);
-                } else {
-                    d[w] = s0 | (s1 << 16);
-                    // B tile planes of the result: row (= K index) slot, columns x (= MN index)
-                    const uint32_t x = (uint32_t)(x0 + c + j);
-                    const size_t o = (size_t)(x / BN) * B_PLANE + toff64(x % BN, (uint32_t)slot);
-                    Tlo[o] = (uint8_t)(s0 & 0xff);
-                    Thi[o] = (uint8_t)(s0 >> 8);
-                    Tlo[o + 16] = (uint8_t)(s1 & 0xff);         // x+1 -> next core-matrix row (16 bytes on)
-                    Thi[o + 16] = (uint8_t)(s1 >> 8);
-                }
-            }
-        }
-        tc::fence_before();
-        __syncthreads();                  // TMEM free for the next tile's MMAs
-        tc::fence_after();
-        if (fast) {
-#pragma unroll
-            for (int u = 0; u < BN / 8; u++)
-                reinterpret_cast<uint4 *>(crow)[u] = make_uint4(d[4 * u], d[4 * u + 1], d[4 * u + 2], d[4 * u + 3]);
-        } else if (live) {
-#pragma unroll
-            for (int j = 0; j < BN; j++)
-                if (x0 + j < cols) crow[j] = (uint16_t)(d[j / 2] >> (16 * (j & 1)));
         }
     }
-    if (warp == 0) tc::tmem_dealloc<256>(tbase);
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
 // INT-pipe reference engine for the same op (tests / GBLA_DENSE_INT).
@@ -246,8 +336,7 @@ gbla_status set_attr()
 {
     static bool attr = false;
     if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           SMEM_TOTAL));
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
         attr = true;
     }
     return GBLA_OK;
@@ -262,14 +351,17 @@ int g_sms = 148;
 // columns grouped by 64 (B_PLANE bytes per plane per tile).
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev)
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap)
 {
     GBLA_TRY(set_attr<MODE_SUB>());
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
     const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
-    const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
-    k_modgemm_tc<MODE_SUB><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi,
-                                                                    rowidx, C, ldc, nullptr, nullptr, c0_dev, nullptr);
+    int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
+    if (grid > tiles) grid = tiles;
+    MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
+             c0_dev, nullptr, win_dev, win_w, ctsel};
+    k_modgemm_ws<MODE_SUB><<<(unsigned)grid, WS_THREADS, WS_SMEM, st>>>(a);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -282,9 +374,10 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
     GBLA_TRY(set_attr<MODE_STORE>());
     if (cols <= 0) return GBLA_OK;
     const int64_t tiles = (cols + BN - 1) / BN;
-    const int64_t grid = tiles < 2 * g_sms ? tiles : 2 * g_sms;
-    k_modgemm_tc<MODE_STORE><<<(unsigned)grid, 128, SMEM_TOTAL, st>>>(BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi,
-                                                                      nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev);
+    int64_t grid = (tiles + 1) / 2;                       // two column tiles per CTA (TMEM double buffer)
+    if (grid > g_sms) grid = g_sms;
+    MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev, nullptr, 0, CT_ALL};
+    k_modgemm_ws<MODE_STORE><<<(unsigned)grid, WS_THREADS, WS_SMEM, st>>>(a);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -323,7 +416,8 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
     k_split_rows<<<grid_for(rp * KP, 256), 256, 0, st>>>(rows, rp, K, A, lda, Alo, Ahi);
     k_split_cols<<<grid_for(cp * KP, 256), 256, 0, st>>>(cols, cp, K, B, ldb, Blo, Bhi);
     note_launch(2);
-    gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr);
+    gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
+                                   CT_ALL, 0);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));

@@ -184,6 +184,15 @@ def test_scaled_configs_tc_vs_int(gb, ctx):
         check_full(gb, ctx, M, res, flags=gb.GBLA_SPARSE_INT | gb.GBLA_DENSE_INT)
 
 
+def test_echelon_without_lookahead(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """The echelon's look-ahead (next panel on a side stream beside the rest of
+    the trailing update) and the serial schedule give the same R."""
+    monkeypatch.setenv("GBLA_NO_LOOKAHEAD", "1")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c3"], 0.03))
+    check_full(gb, ctx, M, oracle.reduce(M))
+
+
 def test_host_input_and_host_copy(gb, ctx, c0_matrix, c0_oracle):
     M = c0_matrix
     h = gb.gbla_reduce(ctx, M.m, M.n, M.row_ptr, M.col, M.val, M.p)     # numpy => GBLA_HOST_INPUT
