@@ -217,11 +217,14 @@ class Mat:
         return (_view(s.value, (npiv + nN,), "<u4").clone(), _view(pr.value, (npiv,), "<u4").clone(),
                 _view(nr.value, (mN,), "<u4").clone())
 
-    def D(self):
+    def D(self, clone: bool = True):
+        """Current D (mN x nN).  clone=False returns a view of the library's
+        buffer (valid until the next call on this handle changes it)."""
         npiv, mN, nN = self.dims()
         d, ld = ctypes.c_void_p(), ctypes.c_int64()
         _check(_lib.gbla_get_D(self._h, ctypes.byref(d), ctypes.byref(ld)))
-        return _view(d.value, (mN, nN), "<u2", ld.value, 2).clone()
+        v = _view(d.value, (mN, nN), "<u2", ld.value, 2)
+        return v.clone() if clone else v
 
     def cprime(self):
         npiv, mN, nN = self.dims()

@@ -59,6 +59,17 @@ gbla_status dalloc(gbla_mat h, size_t bytes, void **out)
     return GBLA_OK;
 }
 
+void dfree(gbla_mat h, void *p)
+{
+    if (!p) return;
+    for (size_t i = 0; i < h->allocs.size(); i++)
+        if (h->allocs[i].ptr == p) {
+            ctx_free(h->ctx, p, h->stream);
+            h->allocs.erase(h->allocs.begin() + i);
+            return;
+        }
+}
+
 void dfree_all(gbla_mat h)
 {
     for (auto &a : h->allocs) ctx_free(h->ctx, a.ptr, h->stream);
@@ -241,8 +252,7 @@ extern "C" gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream)
         GBLA_TRY(reduce_c_int(h, fused, keep_x));
     } else {
         // tensor-core block path (sparse_tc.cu): C' tiles, then D -= C' B
-        GBLA_TRY(reduce_c_tc(h, keep_x || !fused));
-        if (fused) GBLA_TRY(update_d_tc(h));
+        GBLA_TRY(reduce_c_tc(h, keep_x || !fused, fused));
     }
     h->phase_ms[1] = tm.stop();
     if (fused) { h->did_fused = true; h->did_update = true; if (flags & GBLA_KEEP_CPRIME) h->did_cprime = true; }

@@ -34,7 +34,7 @@
         }                                                                                  \
     } while (0)
 
-gbla_status tc_prepare_dist(gbla_mat h);
+void band_release(gbla_mat h);
 gbla_status tc_shard(gbla_mat h, int prank, int pworld);
 gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2]);
 int64_t tc_ntiles(gbla_mat h);
@@ -165,13 +165,13 @@ gbla_status dist_sparse_phase(gbla_mat h)
     const bool real = ctx->world > 1 && ctx->nccl_comm;
     const int G = real ? ctx->world : dist_emulated_world();
     const int me = real ? ctx->rank : 0;
-    GBLA_TRY(tc_prepare_dist(h));
     if (h->mN == 0 || h->npiv == 0) return GBLA_OK;   // D_new = D on every rank
     if (real) {
         GBLA_TRY(tc_shard(h, me, G));
     } else {
         for (int g = 0; g < G; g++) GBLA_TRY(tc_shard(h, g, G));
     }
+    band_release(h);
     // C5: modMAC counters (each rank counted its own tiles)
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));            // this rank's tiles (kernel work for the roofline)

@@ -167,6 +167,7 @@ static inline gbla_status dalloc_t(gbla_mat h, size_t count, T **out) {
     return dalloc(h, count * sizeof(T) + 16, reinterpret_cast<void **>(out));
 }
 void dfree_all(gbla_mat h);
+void dfree(gbla_mat h, void *p);      // release one allocation early
 void *ctx_alloc(gbla_ctx c, size_t bytes, cudaStream_t s);
 void ctx_free(gbla_ctx c, void *p, cudaStream_t s);
 
@@ -177,9 +178,10 @@ gbla_status update_d_from_x_int(gbla_mat h);
 gbla_status reduce_b_int(gbla_mat h);
 gbla_status update_d_from_bp_int(gbla_mat h);
 gbla_status echelon_impl(gbla_mat h, uint32_t flags);
-gbla_status reduce_c_tc(gbla_mat h, bool want_x16);
+gbla_status reduce_c_tc(gbla_mat h, bool want_x16, bool fused);
 gbla_status update_d_tc(gbla_mat h);
 void band_free(gbla_mat h);
+void band_release(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
 gbla_status ensure_multilines(gbla_mat h);
 static inline void kt_mark_on(gbla_mat h, int which, cudaStream_t s)

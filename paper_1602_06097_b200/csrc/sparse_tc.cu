@@ -41,6 +41,7 @@ struct BandTiles {
     uint32_t *amax = nullptr, *bmin = nullptr, *bmax = nullptr;
     uint32_t *jl_ptr = nullptr, *jl_idx = nullptr, *kl_ptr = nullptr, *kl_idx = nullptr;
     unsigned long long *ops = nullptr;   // [2] A-part, B-part modMACs (Alg 2 count)
+    int64_t xt_cap = 0;                  // target tiles the X-tile buffer holds
     bool swept = false;
 };
 
@@ -181,7 +182,8 @@ struct SweepArgs {
     int64_t ldX;
     const uint32_t *ab_w, *ab_np;
     unsigned long long *ops;
-    int64_t prank, pworld;         // target tiles T = prank + pworld * i (multi-GPU row shards), i = local tile
+    int64_t prank, pworld;         // target tiles T = prank + pworld * (i0 + li) (multi-GPU row shards)
+    int64_t i0;                    // first local tile of this batch; Xt / jmin / flags are batch-relative (li)
     // dependency-driven schedule: task (i, J) computes X_J of local tile i.  Tasks are
     // numbered J-major: those of column block J are [toff[J], toff[J+1]) = local tiles
     // 0 .. toff[J+1]-toff[J]-1 (tiles are sorted by lead, so the active ones are a prefix).
@@ -206,12 +208,12 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 
 // first block of every local target tile (NB for a tile of zero rows)
 __global__ void k_tile_jmin(int64_t nl, int64_t mN, int64_t npiv, int64_t NB, int64_t prank, int64_t pworld,
-                            const uint32_t *__restrict__ order, const uint32_t *__restrict__ tlead,
+                            int64_t i0, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tlead,
                             uint32_t *__restrict__ jmin)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nl) return;
-    const int64_t first = (prank + pworld * i) * 128;
+    const int64_t first = (prank + pworld * (i0 + i)) * 128;
     const uint32_t l = first < mN ? tlead[order[first]] : (uint32_t)npiv;
     jmin[i] = l >= (uint64_t)npiv ? (uint32_t)NB : l / 128u;
 }
@@ -223,8 +225,10 @@ __global__ void k_pos(int64_t mN, const uint32_t *__restrict__ order, uint32_t *
     if (i < mN) pos[order[i]] = (uint32_t)i;
 }
 
-// C_J[T] into the X tiles (dense limb planes, A-operand layout): warp per target row
-__global__ void k_cfill(int64_t mN, int64_t NB, const uint32_t *__restrict__ pos, const uint64_t *__restrict__ cd_ptr,
+// C_J[T] into the X tiles of the batch's local tiles [i0, i1) (dense limb planes, A-operand
+// layout): warp per target row
+__global__ void k_cfill(int64_t mN, int64_t NB, int64_t prank, int64_t pworld, int64_t i0, int64_t i1,
+                        const uint32_t *__restrict__ pos, const uint64_t *__restrict__ cd_ptr,
                         const uint32_t *__restrict__ cd_col, const uint16_t *__restrict__ cd_val,
                         const uint32_t *__restrict__ cd_np, uint8_t *__restrict__ Xt)
 {
@@ -232,7 +236,11 @@ __global__ void k_cfill(int64_t mN, int64_t NB, const uint32_t *__restrict__ pos
     const int lane = threadIdx.x & 31;
     if (t >= mN) return;
     const uint32_t ps = pos[t];
-    const uint64_t T = ps / 128, r = ps % 128;
+    const int64_t Tg = ps / 128;
+    if (Tg < prank || (Tg - prank) % pworld != 0) return;
+    const int64_t li = (Tg - prank) / pworld;
+    if (li < i0 || li >= i1) return;
+    const uint64_t T = (uint64_t)(li - i0), r = ps % 128;
     const uint64_t s = cd_ptr[t], e = s + cd_np[t];
     for (uint64_t q = s + lane; q < e; q += 32) {
         const uint32_t c = cd_col[q];
@@ -297,12 +305,12 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
             if (a.toff[mid] <= task) lo = mid; else hi = mid;
         }
         const int64_t J = lo, li = task - a.toff[lo];
-        const int64_t T = a.prank + a.pworld * li, first = T * 128;
+        const int64_t T = a.prank + a.pworld * (a.i0 + li), first = T * 128;
         const int64_t Jmin = a.jmin[li];
         const int64_t slot = first + tid;
         const bool live = slot < a.mN;
         const uint32_t t = live ? a.order[slot] : 0;
-        uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
+        uint8_t *Xrow = a.Xt + (size_t)li * a.NB * TB;
         const uint32_t *fl = a.flags + (size_t)li * a.NB;
         const uint32_t jbase = (uint32_t)J * 128;
         {
@@ -453,7 +461,8 @@ struct UpdArgs {
     const uint32_t *bmin, *kl_ptr, *kl_idx;
     uint16_t *D;
     int64_t ldD;
-    int64_t prank, pworld;         // target tiles T = prank + pworld * blockIdx.y
+    int64_t prank, pworld;         // target tiles T = prank + pworld * (i0 + blockIdx.y)
+    int64_t i0;                    // first local tile of the batch (Xt is batch-relative)
 };
 
 constexpr int UPD_SMEM = 2 * 65536;
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     __shared__ uint64_t full[2], mdone[2], accbar;
     __shared__ uint32_t tmem_s;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t K = blockIdx.x, T = a.prank + a.pworld * (int64_t)blockIdx.y, first = T * 128;
+    const int64_t K = blockIdx.x, T = a.prank + a.pworld * (a.i0 + (int64_t)blockIdx.y), first = T * 128;
     const uint32_t lead0 = a.tlead[a.order[first]];
     if (lead0 >= (uint64_t)a.npiv) return;
     const int64_t Jmin = lead0 / 128;
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     tc::fence_after();
     const uint32_t tbase = tmem_s;
     const uint32_t sStg = tc::smem_u32(smem);
-    const uint8_t *Xrow = a.Xt + (size_t)T * a.NB * TB;
+    const uint8_t *Xrow = a.Xt + (size_t)blockIdx.y * a.NB * TB;
     if (tid == 0) {
         uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0};
         auto load = [&](uint32_t it) {
@@ -628,43 +637,40 @@ static gbla_status band_build(gbla_mat h)
     k_diag_inv<<<(unsigned)NB, 128, DIAG_SMEM, st>>>(h->F, bt->offA, bt->tilesA, bt->invT);
     note_launch(3);
     GBLA_CUDA_TRY(cudaGetLastError());
-    // the X (C') tiles of every target tile
-    GBLA_TRY(dalloc(h, (size_t)(bt->ntiles > 0 ? bt->ntiles : 1) * NB * TB + 16, (void **)&bt->Xt));
     return GBLA_OK;
 }
 
 // ---- host side -------------------------------------------------------------
-// Band tiles + the C tiles of every target tile (replicated on every rank).
-static gbla_status tc_prepare(gbla_mat h)
-{
-    cudaStream_t st = h->stream;
-    GBLA_TRY(band_build(h));
-    BandTiles *bt = h->bt;
-    if (bt->swept || bt->NB == 0) return GBLA_OK;
-    uint32_t *pos;
-    GBLA_TRY(dalloc_t(h, h->mN, &pos));
-    GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)bt->ntiles * bt->NB * TB, st));
-    k_pos<<<grid_for(h->mN, 256), 256, 0, st>>>(h->mN, h->order, pos);
-    k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, bt->NB, pos, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np,
-                                                       bt->Xt);
-    note_launch(2);
-    GBLA_CUDA_TRY(cudaGetLastError());
-    return GBLA_OK;
-}
-
 static inline int64_t local_tiles(int64_t ntiles, int prank, int pworld)
 {
     return ntiles > prank ? (ntiles - prank + pworld - 1) / pworld : 0;
 }
 
-// K5' for the target tiles T = prank + pworld * i
-gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
+// X tiles per batch of target tiles: all of them if they fit beside what is
+// already allocated (keeping a reserve for the echelon), else as many as fit
+// (1172 tiles x 6641 blocks x 32 KB would be 255 GB).
+static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
+{
+    const int64_t per_tile = h->bt->NB * (int64_t)TB;
+    const char *e = getenv("GBLA_XT_BATCH");          // tests: force small batches
+    if (e && atoll(e) > 0) return atoll(e) < nl ? atoll(e) : nl;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
+    const int64_t reserve = (int64_t)4 << 30;
+    int64_t budget = (int64_t)fr - reserve;
+    if (budget < per_tile) budget = per_tile;
+    const int64_t b = budget / per_tile;
+    return b < nl ? (b > 0 ? b : 1) : nl;
+}
+
+// K5' for the local target tiles [i0, i1) (T = prank + pworld * i)
+static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0, int64_t i1, bool want_x16)
 {
     cudaStream_t st = h->stream;
     BandTiles *bt = h->bt;
-    const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
+    const int64_t nl = i1 - i0;
     const int64_t NB = bt->NB;
-    if (NB == 0 || nl == 0) return GBLA_OK;
+    if (NB == 0 || nl <= 0) return GBLA_OK;
     static int occ = -1;
     if (occ < 0) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
@@ -678,7 +684,8 @@ gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
     GBLA_TRY(dalloc_t(h, NB + 1, &toff));
     GBLA_TRY(dalloc_t(h, (size_t)nl * NB, &flags));
     GBLA_TRY(dalloc_t(h, 1, &next));
-    k_tile_jmin<<<grid_for(nl, 256), 256, 0, st>>>(nl, h->mN, h->npiv, NB, prank, pworld, h->order, h->tlead, jmin);
+    k_tile_jmin<<<grid_for(nl, 256), 256, 0, st>>>(nl, h->mN, h->npiv, NB, prank, pworld, i0, h->order, h->tlead,
+                                                     jmin);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     std::vector<uint32_t> hj(nl), ho(NB + 1);
@@ -710,7 +717,7 @@ gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
     a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
     a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
     a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
-    a.prank = prank; a.pworld = pworld;
+    a.prank = prank; a.pworld = pworld; a.i0 = i0;
     a.toff = toff; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
     int64_t grid = (int64_t)h->ctx->sm_count * occ;
     if (grid > (int64_t)ntasks) grid = ntasks;
@@ -725,13 +732,13 @@ gbla_status tc_sweep_part(gbla_mat h, int prank, int pworld, bool want_x16)
     return GBLA_OK;
 }
 
-// K7' for the target tiles T = prank + pworld * i
-gbla_status tc_update_part(gbla_mat h, int prank, int pworld)
+// K7' for the local target tiles [i0, i1)
+static gbla_status tc_update_batch(gbla_mat h, int prank, int pworld, int64_t i0, int64_t i1)
 {
     cudaStream_t st = h->stream;
     BandTiles *bt = h->bt;
-    const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
-    if (bt->NB == 0 || bt->NNB == 0 || nl == 0) return GBLA_OK;
+    const int64_t nl = i1 - i0;
+    if (bt->NB == 0 || bt->NNB == 0 || nl <= 0) return GBLA_OK;
     static bool attr = false;
     if (!attr) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM));
@@ -742,12 +749,17 @@ gbla_status tc_update_part(gbla_mat h, int prank, int pworld)
     a.order = h->order; a.tlead = h->tlead;
     a.Xt = bt->Xt; a.tilesB = bt->tilesB; a.offB = bt->offB; a.bmin = bt->bmin;
     a.kl_ptr = bt->kl_ptr; a.kl_idx = bt->kl_idx; a.D = h->D; a.ldD = h->ldD;
-    a.prank = prank; a.pworld = pworld;
-    dim3 grid((unsigned)bt->NNB, (unsigned)nl);
-    kt_mark(h, KT_UPDATE);
-    k_update_tc<<<grid, 128, UPD_SMEM, st>>>(a);
-    kt_mark(h, KT_UPDATE);
-    note_launch();
+    a.prank = prank; a.pworld = pworld; a.i0 = i0;
+    for (int64_t y0 = 0; y0 < nl; y0 += 65535) {       // gridDim.y <= 65535
+        const int64_t ny = nl - y0 < 65535 ? nl - y0 : 65535;
+        a.i0 = i0 + y0;
+        UpdArgs b = a;
+        b.Xt = bt->Xt + (size_t)y0 * bt->NB * TB;
+        kt_mark(h, KT_UPDATE);
+        k_update_tc<<<dim3((unsigned)bt->NNB, (unsigned)ny), 128, UPD_SMEM, st>>>(b);
+        kt_mark(h, KT_UPDATE);
+        note_launch();
+    }
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }
@@ -762,49 +774,94 @@ gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2])
     return GBLA_OK;
 }
 
-// C' = C A^-1 on the whole C (single GPU; gbla_reduce_C)
-gbla_status reduce_c_tc(gbla_mat h, bool want_x16)
+// The sparse phase of the local target tiles of rank prank of pworld: in batches of
+// target tiles (X tiles = C_J, then X_J), sweep (C' = C A^-1) and, if `update`,
+// D -= C' B.  Without `update` every X tile must stay resident for a later
+// gbla_update_D (one batch).  After a fused pass the band and X tiles are released.
+static gbla_status tc_sparse(gbla_mat h, int prank, int pworld, bool want_x16, bool update)
+{
+    cudaStream_t st = h->stream;
+    GBLA_TRY(band_build(h));
+    BandTiles *bt = h->bt;
+    const int64_t NB = bt->NB;
+    const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
+    if (NB == 0 || nl == 0) return GBLA_OK;
+    if (!bt->tilesA) { set_error("sparse phase: band tiles already released"); return GBLA_E_ORDER; }
+    if (!bt->Xt) {
+        bt->xt_cap = update ? xt_batch_tiles(h, nl) : nl;
+        GBLA_TRY(dalloc(h, (size_t)bt->xt_cap * NB * TB + 16, (void **)&bt->Xt));
+    }
+    const int64_t per = bt->xt_cap < nl ? bt->xt_cap : nl;
+    if (!update && per < nl) { set_error("unfused reduce_C needs every C' tile resident"); return GBLA_E_NOMEM; }
+    uint32_t *pos;
+    GBLA_TRY(dalloc_t(h, h->mN, &pos));
+    k_pos<<<grid_for(h->mN, 256), 256, 0, st>>>(h->mN, h->order, pos);
+    note_launch();
+    for (int64_t i0 = 0; i0 < nl; i0 += per) {
+        const int64_t i1 = i0 + per < nl ? i0 + per : nl;
+        GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)(i1 - i0) * NB * TB, st));
+        k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, NB, prank, pworld, i0, i1, pos, h->cd_ptr,
+                                                           h->cd_col, h->cd_val, h->cd_np, bt->Xt);
+        note_launch();
+        GBLA_CUDA_TRY(cudaGetLastError());
+        GBLA_TRY(tc_sweep_batch(h, prank, pworld, i0, i1, want_x16));
+        if (update) GBLA_TRY(tc_update_batch(h, prank, pworld, i0, i1));
+    }
+    return GBLA_OK;
+}
+
+// device buffers of the band / X tiles are dead after the update: give them back
+// before the echelon (c4 needs the memory)
+void band_release(gbla_mat h)
+{
+    BandTiles *bt = h->bt;
+    if (!bt) return;
+    dfree(h, bt->tilesA); bt->tilesA = nullptr;
+    dfree(h, bt->tilesB); bt->tilesB = nullptr;
+    dfree(h, bt->invT); bt->invT = nullptr;
+    dfree(h, bt->Xt); bt->Xt = nullptr;
+    bt->xt_cap = 0;
+}
+
+// C' = C A^-1 on the whole C (single GPU; gbla_reduce_C); fused: also D -= C' B
+gbla_status reduce_c_tc(gbla_mat h, bool want_x16, bool fused)
 {
     if (want_x16) GBLA_TRY(ensure_x(h));
     if (h->mN == 0 || h->npiv == 0) {     // C is empty: C' = 0, D_new = D
         h->have_xt = true;
         return GBLA_OK;
     }
-    GBLA_TRY(tc_prepare(h));
-    GBLA_TRY(tc_sweep_part(h, 0, 1, want_x16));
-    h->bt->swept = true;
+    GBLA_TRY(tc_sparse(h, 0, 1, want_x16, fused));
+    if (h->bt) h->bt->swept = true;
+    if (fused) band_release(h);
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));
-    h->sparse_ops += ops[0];
+    h->sparse_ops += ops[0] + (fused ? ops[1] : 0);
     h->kwork[KT_SWEEP] = ops[0];
-    h->have_xt = true;
+    if (fused) h->kwork[KT_UPDATE] = ops[1];
+    h->have_xt = !fused;
     return GBLA_OK;
 }
 
-// D <- D - C' B with the C' tiles of reduce_c_tc (single GPU; gbla_update_D)
+// D <- D - C' B with the C' tiles of an unfused reduce_c_tc (single GPU; gbla_update_D)
 gbla_status update_d_tc(gbla_mat h)
 {
     if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
-    if (!h->bt || !h->bt->swept) { set_error("update_d_tc: no C' tiles"); return GBLA_E_INTERNAL; }
-    GBLA_TRY(tc_update_part(h, 0, 1));
+    if (!h->bt || !h->bt->swept || !h->bt->Xt) { set_error("update_d_tc: no C' tiles"); return GBLA_E_INTERNAL; }
+    GBLA_TRY(tc_update_batch(h, 0, 1, 0, local_tiles(h->bt->ntiles, 0, 1)));
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops += ops[1];
     h->kwork[KT_UPDATE] = ops[1];
+    band_release(h);
     return GBLA_OK;
 }
 
-// multi-GPU / emulated ranks: prepare once, then the sparse phase of one row shard
-gbla_status tc_prepare_dist(gbla_mat h)
-{
-    if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
-    return tc_prepare(h);
-}
+// multi-GPU / emulated ranks: the sparse phase of one row shard (fused)
 gbla_status tc_shard(gbla_mat h, int prank, int pworld)
 {
     if (h->mN == 0 || h->npiv == 0) return GBLA_OK;
-    GBLA_TRY(tc_sweep_part(h, prank, pworld, false));
-    return tc_update_part(h, prank, pworld);
+    return tc_sparse(h, prank, pworld, false, true);
 }
 int64_t tc_ntiles(gbla_mat h) { return h->bt ? h->bt->ntiles : (h->mN + 127) / 128; }
 unsigned long long *tc_ops_dev(gbla_mat h) { return h->bt ? h->bt->ops : nullptr; }

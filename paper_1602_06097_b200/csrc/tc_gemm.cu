@@ -18,9 +18,9 @@
 // specialized: warp 0 stages the A tile of a row tile once (double-buffered)
 // and the B tiles through a 4-stage ring, warp 1 issues the 16 MMAs of a
 // 128 x 64 output tile (4 K-steps x 4 limb products) into one of two TMEM
-// accumulators (HH | X | LL, 3 x 64 columns each), and 8 epilogue warps
+// accumulators (HH | X | LL, 3 x 64 columns each), and 16 epilogue warps
 // drain the other accumulator (tcgen05.ld: warp w reads TMEM lanes
-// 32*(w%4)..+31, half of the columns each), reduce mod p and
+// 32*(w%4)..+31, a quarter of the columns each), reduce mod p and
 // read-modify-write C (16-byte vectors per thread, the C row segment
 // prefetched before the accumulator is ready).  Loads, MMAs and epilogue of
 // consecutive tiles overlap.  Each CTA owns a contiguous range of output
@@ -71,13 +71,15 @@ struct MMArgs {
 };
 
 constexpr int NSB = 4;                               // B stages
-constexpr int WS_THREADS = 320;                      // producer, MMA, 8 epilogue warps
+constexpr int EPI_WARPS = 16;                        // 4 per TMEM lane quarter, 16 columns each
+constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
+constexpr int WS_THREADS = 64 + 32 * EPI_WARPS;      // producer, MMA, epilogue warps
 constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB: one CTA per SM)
 
 // Warp-specialized persistent K11: warp 0 stages operands (A tile once per row
 // tile, double-buffered; B tiles through a 4-stage ring), warp 1 issues the
 // MMAs into one of two TMEM accumulators (HH | X | LL, 192 columns each), warps
-// 2..9 drain the other accumulator (warp w reads TMEM lanes 32*(w%4).., half of
+// 2.. drain the other accumulator (warp w reads TMEM lanes 32*(w%4).., a part of
 // the 64 columns each), so loads, MMAs and the epilogue of consecutive tiles
 // overlap.  Each CTA owns a contiguous range of output tiles in row-tile-major
 // order (A reuse).
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
             tc::mbar_init(&afull[i], 1);
             tc::mbar_init(&aempty[i], 1);
             tc::mbar_init(&tfull[i], 1);
-            tc::mbar_init(&tempty[i], 8);
+            tc::mbar_init(&tempty[i], EPI_WARPS);
         }
         for (int i = 0; i < NSB; i++) {
             tc::mbar_init(&bfull[i], 1);
@@ -207,40 +209,40 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
             }
         }
     } else {                                   // ---- epilogue warps 2..9
-        const int e = warp - 2, quarter = warp & 3, half = e >> 2;
+        const int e = warp - 2, quarter = warp & 3, part = e >> 2;
         const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (g.ldc % 8 == 0);
         uint32_t tph[2] = {0, 0};
         int ab = 0;
         for (int64_t tile = t_begin; tile < t_end; tile++) {
             const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
-            const int64_t row0 = rt * BM, x0 = ct * BN + half * 32;
+            const int64_t row0 = rt * BM, x0 = ct * BN + part * EPI_COLS;
             const int64_t slot = row0 + quarter * 32 + lane;
             const bool live = slot < nr;
             uint16_t *crow = nullptr;
             if (live) crow = C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot] : slot) * g.ldc + x0;
-            const bool fast = live && vec && x0 + 32 <= cols;
-            uint32_t dv[16];
+            const bool fast = live && vec && x0 + EPI_COLS <= cols;
+            uint32_t dv[EPI_COLS / 2];
 #pragma unroll
-            for (int w = 0; w < 16; w++) dv[w] = 0;
+            for (int w = 0; w < EPI_COLS / 2; w++) dv[w] = 0;
             if (MODE == MODE_SUB && live) {          // prefetch the C row segment before waiting
                 if (fast) {
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < EPI_COLS / 8; u++) {
                         const uint4 q = reinterpret_cast<const uint4 *>(crow)[u];
                         dv[4 * u] = q.x; dv[4 * u + 1] = q.y; dv[4 * u + 2] = q.z; dv[4 * u + 3] = q.w;
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 32; j++)
+                    for (int j = 0; j < EPI_COLS; j++)
                         if (x0 + j < cols) dv[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
                 }
             }
             tc::mbar_wait(&tfull[ab], tph[ab]);
             tph[ab] ^= 1;
             tc::fence_after();
-            const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 3 * BN + half * 32;
+            const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 3 * BN + part * EPI_COLS;
 #pragma unroll
-            for (int c = 0; c < 32; c += 16) {
+            for (int c = 0; c < EPI_COLS; c += 16) {
                 uint32_t hh[16], xx[16], ll[16];
                 tc::tmem_ld16(la + c, hh);
                 tc::tmem_ld16(la + BN + c, xx);
@@ -275,11 +277,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
             ab ^= 1;
             if (fast) {
 #pragma unroll
-                for (int u = 0; u < 4; u++)
+                for (int u = 0; u < EPI_COLS / 8; u++)
                     reinterpret_cast<uint4 *>(crow)[u] = make_uint4(dv[4 * u], dv[4 * u + 1], dv[4 * u + 2], dv[4 * u + 3]);
             } else if (live) {
 #pragma unroll
-                for (int j = 0; j < 32; j++)
+                for (int j = 0; j < EPI_COLS; j++)
                     if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
             }
         }

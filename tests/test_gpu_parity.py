@@ -184,6 +184,23 @@ def test_scaled_configs_tc_vs_int(gb, ctx):
         check_full(gb, ctx, M, res, flags=gb.GBLA_SPARSE_INT | gb.GBLA_DENSE_INT)
 
 
+def test_xt_batches(gb, ctx, monkeypatch):
+    """The sparse phase in batches of target tiles (how c4 fits in HBM): forcing
+    2-tile batches must not change D_new, the op count or R."""
+    monkeypatch.setenv("GBLA_XT_BATCH", "2")
+    for name, sc in (("c1", 0.05), ("c3", 0.03), ("c4", 0.004)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        check_full(gb, ctx, M, oracle.reduce(M))
+    monkeypatch.setenv("GBLA_DIST_EMULATE", "3")
+    M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.05))
+    res = oracle.reduce(M)
+    h = gpu_reduce(gb, ctx, M)
+    r, pc, R = h.rref()
+    assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R)
+    assert h.opcount()[0] == res.modmac
+    h.free()
+
+
 def test_echelon_without_lookahead(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     """The echelon's look-ahead (next panel on a side stream beside the rest of
     the trailing update) and the serial schedule give the same R."""
