@@ -7,11 +7,36 @@
 #include "internal.cuh"
 
 #include <atomic>
+#include <mutex>
 
 static thread_local char g_err[1024];
 static std::atomic<unsigned long long> g_launches{0};
 
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+static std::mutex g_ev_mu;
+static std::vector<cudaEvent_t> g_ev_pool;
+
+cudaEvent_t kt_event_get()
+{
+    {
+        std::lock_guard<std::mutex> lk(g_ev_mu);
+        if (!g_ev_pool.empty()) {
+            cudaEvent_t e = g_ev_pool.back();
+            g_ev_pool.pop_back();
+            return e;
+        }
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return e;
+}
+
+void kt_event_put(cudaEvent_t e)
+{
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    g_ev_pool.push_back(e);
+}
 
 extern "C" uint64_t gbla_kernel_launches(void) { return g_launches.load(); }
 
@@ -475,6 +500,6 @@ extern "C" void gbla_mat_free(gbla_mat h)
     cudaStreamSynchronize(h->stream);
     band_free(h);
     for (auto &v : h->kt.ev)
-        for (cudaEvent_t e : v) cudaEventDestroy(e);
+        for (cudaEvent_t e : v) kt_event_put(e);
     delete h;
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
 #include <string>
 #include <vector>
 
@@ -184,11 +185,16 @@ void band_free(gbla_mat h);
 void band_release(gbla_mat h);
 gbla_status ensure_x(gbla_mat h);
 gbla_status ensure_multilines(gbla_mat h);
+// process-wide pool of timing events (creating events per mark costs host time
+// that the panel loop cannot spare); events go back to the pool at gbla_mat_free
+cudaEvent_t kt_event_get();
+void kt_event_put(cudaEvent_t e);
 static inline void kt_mark_on(gbla_mat h, int which, cudaStream_t s)
 {
     if (!h->kt.on) return;
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return;
+    if (s != h->stream && getenv("GBLA_KT_MAIN_ONLY")) return;
+    cudaEvent_t e = kt_event_get();
+    if (!e) return;
     cudaEventRecord(e, s);
     h->kt.ev[which].push_back(e);
 }

@@ -92,10 +92,10 @@ __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, 
                         const uint32_t *__restrict__ rowpiv, const P2State *__restrict__ prev,
                         uint32_t *__restrict__ lead)
 {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (r >= mN) return;
     const int64_t c0 = prev->c1;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     uint32_t res = NONE16;
     if (rowpiv[r] == GBLA_NONE && c0 < nN) {
         const int64_t wmax = nN - c0 < PW ? nN - c0 : PW;
@@ -112,6 +112,7 @@ __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, 
         }
     }
     if (lane == 0) lead[r] = res;
+    }
 }
 
 // Inverse W of a unit upper triangular 32 x 32 matrix U (entries beyond bs: identity),
@@ -731,12 +732,13 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows)
 {
     constexpr int CPL = PK / 32;
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
-    if (i >= mN || kp == 0) return;
+    if (kp == 0) return;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mN;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const uint32_t rp = rowpiv[i];
-    if (rp != GBLA_NONE && rp >= (uint64_t)ps->c0) return;   // selected now: becomes Rn
+    if (rp != GBLA_NONE && rp >= (uint64_t)ps->c0) continue;   // selected now: becomes Rn
     const uint16_t *drow = D + (size_t)i * ldD;
     uint16_t v[CPL];
     bool nz = false;
@@ -746,7 +748,7 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
         v[u] = b < kp ? drow[ps->pc[b]] : 0;
         nz |= v[u] != 0;
     }
-    if (!__any_sync(FULL, nz)) return;
+    if (!__any_sync(FULL, nz)) continue;
     uint32_t slot = 0;
     if (lane == 0) slot = atomicAdd(&ps->nrows, 1u);
     slot = __shfl_sync(FULL, slot, 0);
@@ -760,6 +762,7 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     const size_t o = (size_t)(slot / 128) * (PK * 128) + tc::toff(slot % 128, lane * CPL);
     *reinterpret_cast<uint32_t *>(Flo + o) = lo;
     *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
+    }
 }
 
 // transposed limb planes of D[S, c0:]: B operand tiles (64 columns x K = 128) of the Rn GEMM
@@ -804,12 +807,34 @@ __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, con
         ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * kp * (unsigned long long)(ps->c1 - c0);   // panel RREF
     }
+    // grid-stride over (row b, 8-column group); a few hundred blocks, so the next panel's
+    // CTA is not queued behind thousands of tiny ones
     const int64_t w = ps->c1 - c0;
-    const int64_t x = (part == 1 ? w : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= kp || c0 + x >= nN) return;
-    const bool in_win = x >= w && x < w + PW;
-    if ((part == 1 && !in_win) || (part == 2 && in_win)) return;
-    D[(size_t)ps->sel[b] * ldD + c0 + x] = Rn[(size_t)b * ldR + x];
+    const int64_t width = nN - c0;
+    if (width <= 0) return;
+    const int64_t xlo = part == 1 ? w : 0;
+    const int64_t xhi = part == 1 ? (w + PW < width ? w + PW : width) : width;
+    const int64_t ng = (xhi - xlo + 7) / 8;
+    const bool vec = (c0 % 8 == 0) && (ldD % 8 == 0) && (ldR % 8 == 0) && (w % 8 == 0);
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < (int64_t)kp * ng;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t bb = (uint32_t)(it / ng);
+        const int64_t x0 = xlo + (it % ng) * 8;
+        uint16_t *dst = D + (size_t)ps->sel[bb] * ldD + c0;
+        const uint16_t *src = Rn + (size_t)bb * ldR;
+        if (vec && x0 + 8 <= xhi && (part != 2 || x0 + 8 <= w || x0 >= w + PW)) {
+            *reinterpret_cast<uint4 *>(dst + x0) = *reinterpret_cast<const uint4 *>(src + x0);
+        } else {
+            for (int u = 0; u < 8; u++) {
+                const int64_t x = x0 + u;
+                if (x >= xhi) break;
+                const bool in_win = x >= w && x < w + PW;
+                if (part == 2 && in_win) continue;
+                dst[x] = src[x];
+            }
+        }
+    }
+    (void)b;
 }
 
 __global__ void k_p2_init(P2State *ps)
@@ -878,11 +903,13 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // the panel factorization of panel k on stream s (prev = panel k-1's state)
     auto factor = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
-        k_lead2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
+        const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                                : 4u * h->ctx->sm_count;
+        k_lead2<<<rgrid, 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
         kt_mark_on(h, KT_PANEL, s);
         k_panel2<<<1, NT, P2_SMEM, s>>>(mN, nN, h->F, h->D, ldD, rowpiv, lead, prev, cur, Tlo, Thi, invtab, trace);
         kt_mark_on(h, KT_PANEL, s);
-        k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
+        k_gather2<<<rgrid, 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
                                                           rows[k & 1]);
         note_launch(3);
     };
@@ -894,7 +921,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             cudaEventCreateWithFlags(&evB, cudaEventDisableTiming) != cudaSuccess)
             fail("stream/event creation");
     }
-    if (status == GBLA_OK && cudaMallocHost(&c1_host, sizeof(int64_t)) != cudaSuccess) fail("cudaMallocHost");
+    if (status == GBLA_OK && cudaMallocHost(&c1_host, 2 * sizeof(int64_t)) != cudaSuccess) fail("cudaMallocHost");
     if (status == GBLA_OK) {
         k_p2_init<<<1, 1, 0, st>>>(ps);
         note_launch();
@@ -910,8 +937,16 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         cudaEventRecord(e, s);
         tl.push_back(e);
     };
+    // batches of panels; the host checks the previous batch's end column (pinned
+    // copy + event) while the current one runs, so the GPU never waits for the host
     int batch = 8;
     int64_t k = 0;
+    cudaEvent_t bev[2] = {nullptr, nullptr};
+    int64_t bk[2] = {0, 0};
+    int nb_done = 0;
+    if (status == GBLA_OK && (cudaEventCreateWithFlags(&bev[0], cudaEventDisableTiming) != cudaSuccess ||
+                              cudaEventCreateWithFlags(&bev[1], cudaEventDisableTiming) != cudaSuccess))
+        fail("event");
     while (status == GBLA_OK) {
         for (int q = 0; q < batch && status == GBLA_OK; q++, k++) {
             P2State *cur = ps + (k & 1);
@@ -929,7 +964,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                         ldD, &cur->c0, nullptr, 0, 0, gemm_grid);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
-                k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 0);
+                k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 0);
                 note_launch();
                 factor(st, k + 1);
             } else {
@@ -938,7 +973,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid);
                 if (status != GBLA_OK) break;
-                k_commit2<<<dim3(PW / 256, PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 1);
+                k_commit2<<<h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 1);
                 note_launch();
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
@@ -953,7 +988,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
-                k_commit2<<<dim3(grid_for(nN, 256), PK), 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 2);
+                k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 2);
                 note_launch();
                 tmark(k, st);
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
@@ -962,14 +997,30 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         }
         if (status != GBLA_OK) break;
         P2State *last = ps + ((k - 1) & 1);
-        if (cudaMemcpyAsync(c1_host, &last->c1, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess) {
-            fail("sync");
+        const int slot = nb_done & 1;
+        if (cudaMemcpyAsync(c1_host + slot, &last->c1, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaEventRecord(bev[slot], st) != cudaSuccess) {
+            fail("event");
             break;
         }
-        if (*c1_host >= nN) break;
-        batch = 16;
+        bk[slot] = k;                              // panels enqueued through this batch
+        nb_done++;
+        if (nb_done >= 2) {                        // the batch before this one: done soon if not yet
+            const int ps2 = (nb_done - 2) & 1;
+            if (cudaEventSynchronize(bev[ps2]) != cudaSuccess) { fail("sync"); break; }
+            const int64_t c1d = c1_host[ps2];
+            if (c1d >= nN) break;
+            // size the next batch from the mean panel width so far (few no-op panels at the end)
+            const double w = (double)c1d / (double)(bk[ps2] > 0 ? bk[ps2] : 1);
+            const double need = (double)(nN - c1d) / (w > 1.0 ? w : 1.0) - (double)(k - bk[ps2]);
+            batch = need < 1.0 ? 1 : (need > 16.0 ? 16 : (int)need + 1);
+        } else {
+            batch = 8;
+        }
     }
+    if (status == GBLA_OK && cudaStreamSynchronize(st) != cudaSuccess) fail("sync");
+    for (int q = 0; q < 2; q++)
+        if (bev[q]) cudaEventDestroy(bev[q]);
     if (side) {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
