@@ -330,8 +330,9 @@ def main():
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "npiv": cfg.npiv, "p": cfg.p,
                        "density": cfg.density, "band": cfg.band, "rank_planted": cfg.rank_planted,
                        "flags": args.flags, "l2": "flushed (256 MiB write) between timed steps; inputs > L2",
-                       "parallelism": (f"{world} GPUs: C1 broadcast of M, target tiles sharded, D_new all-gather, "
-                                       f"echelon replicated") if world > 1 else "1 GPU"},
+                       "parallelism": (f"{world} GPUs: C1 broadcast of M, target tiles sharded (sparse phase), "
+                                       f"row-sharded distributed echelon (NCCL all-reduce / all-gather per "
+                                       f"panel, R assembled by broadcasts)") if world > 1 else "1 GPU"},
             "sparse_modmac_per_step": ops, "dense_modmac_per_step": dense_ops,
             "rank_D": rank_d[1], "npiv": rank_d[0][0],
             "phase_ms": ph, "step_ms": [round(x, 3) for x in step_ms],

@@ -346,6 +346,7 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
         s = dist_sparse_phase(h);
         h->phase_ms[1] = tm.stop();
         h->did_fused = h->did_update = true;
+        h->dist_rows = true;
     } else if (flags & GBLA_ORDER_STANDARD) {
         s = gbla_reduce_B(h, stream);
         if (s == GBLA_OK) s = gbla_update_D(h, stream);

@@ -14,12 +14,16 @@
 //       each rank runs the tensor-core sweep and update on its tiles only -
 //       targets are independent, no communication.
 //   C5  ncclAllReduce of the two modMAC counters.
-//   C3  the owned D_new rows are packed tile by tile and all-gathered
-//       (ncclAllGather), then unpacked into every rank's D; the echelon of
-//       D_new then runs on every rank (identical input -> identical R).
+//   --  D_new stays row-sharded (each rank holds the rows of its tiles); the
+//       echelon is distributed (panel.cu: panels_dist): per
+//       panel an all-reduce of lead counts, an all-gather of the candidates'
+//       slices, the same panel factorization on every rank, an all-reduce of
+//       the selected rows and a local trailing update; R is assembled by
+//       broadcasts of every rank's pivot rows.
 // GBLA_DIST_EMULATE=G (no communicator) runs the G shards one after the
-// other on one GPU and moves the packed blocks with device copies: the same
-// partition / pack / unpack code, a local transport.
+// other on one GPU (one shared D whose rows the ranks split) and replaces the
+// collectives by device copies / sums: the same partition, kernels and data
+// movement, a local transport.
 #include <nccl.h>
 #include <stdlib.h>
 
@@ -75,37 +79,6 @@ extern "C" gbla_status gbla_nccl_get_unique_id(void *out128)
     return GBLA_OK;
 }
 
-namespace {
-
-// pack the rows of the local tiles T = prank + pworld*i into blk[i*128 + r][0..ld)
-__global__ void k_pack_rows(int64_t mN, int64_t nloc, int prank, int pworld, const uint32_t *__restrict__ order,
-                            const uint16_t *__restrict__ D, int64_t ldD, uint16_t *__restrict__ blk)
-{
-    const int64_t row = blockIdx.x;                     // local row = i*128 + r
-    const int64_t i = row / 128, r = row % 128;
-    if (i >= nloc) return;
-    const int64_t slot = (prank + pworld * i) * 128 + r;
-    uint4 *dst = reinterpret_cast<uint4 *>(blk + (size_t)row * ldD);
-    const uint4 *src = slot < mN ? reinterpret_cast<const uint4 *>(D + (size_t)order[slot] * ldD) : nullptr;
-    for (int64_t x = threadIdx.x; x < ldD / 8; x += blockDim.x) dst[x] = src ? src[x] : make_uint4(0, 0, 0, 0);
-}
-
-// unpack every rank's block g into D
-__global__ void k_unpack_rows(int64_t mN, int64_t ntiles, int64_t nmax, int pworld, const uint32_t *__restrict__ order,
-                              const uint16_t *__restrict__ all, int64_t ldD, uint16_t *__restrict__ D)
-{
-    const int64_t row = blockIdx.x;                     // g * nmax*128 + i*128 + r
-    const int64_t g = row / (nmax * 128), i = (row / 128) % nmax, r = row % 128;
-    const int64_t T = g + (int64_t)pworld * i;
-    if (T >= ntiles) return;
-    const int64_t slot = T * 128 + r;
-    if (slot >= mN) return;
-    const uint4 *src = reinterpret_cast<const uint4 *>(all + (size_t)row * ldD);
-    uint4 *dst = reinterpret_cast<uint4 *>(D + (size_t)order[slot] * ldD);
-    for (int64_t x = threadIdx.x; x < ldD / 8; x += blockDim.x) dst[x] = src[x];
-}
-
-}  // namespace
 
 int dist_emulated_world()
 {
@@ -183,31 +156,28 @@ gbla_status dist_sparse_phase(gbla_mat h)
     }
     GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops = ops[0] + ops[1];
-    // C3: all-gather of the D_new rows, packed by tile shard
-    const int64_t ntiles = tc_ntiles(h);
-    const int64_t nmax = (ntiles + G - 1) / G;
-    const int64_t blk_rows = nmax * 128;
-    uint16_t *all;
-    GBLA_TRY(dalloc_t(h, (size_t)G * blk_rows * h->ldD, &all));
-    for (int g = 0; g < G; g++) {
-        if (real && g != me) continue;
-        const int64_t nloc = ntiles > g ? (ntiles - g + G - 1) / G : 0;
-        uint16_t *blk = all + (size_t)g * blk_rows * h->ldD;
-        if (nloc > 0) {
-            k_pack_rows<<<(unsigned)(nloc * 128), 256, 0, st>>>(h->mN, nloc, g, G, h->order, h->D, h->ldD,
-                                                                         blk);
-            note_launch();
-        }
-    }
-    GBLA_CUDA_TRY(cudaGetLastError());
-    if (real) {
-        uint16_t *mine = all + (size_t)me * blk_rows * h->ldD;
-        GBLA_NCCL_TRY(ncclAllGather(mine, all, (size_t)blk_rows * h->ldD * 2, ncclUint8,
-                                    (ncclComm_t)ctx->nccl_comm, st));
-    }
-    k_unpack_rows<<<(unsigned)(G * blk_rows), 256, 0, st>>>(h->mN, ntiles, nmax, G, h->order, all, h->ldD,
-                                                                     h->D);
-    note_launch();
-    GBLA_CUDA_TRY(cudaGetLastError());
+    // D_new stays row-sharded: the echelon is distributed (panel.cu: panels_dist)
+    return GBLA_OK;
+}
+
+// ---- transport of the distributed echelon (NCCL, on the handle's stream) ---------
+gbla_status dist_allreduce_u32(gbla_mat h, uint32_t *buf, size_t n)
+{
+    GBLA_NCCL_TRY(ncclAllReduce(buf, buf, n, ncclUint32, ncclSum, (ncclComm_t)h->ctx->nccl_comm, h->stream));
+    return GBLA_OK;
+}
+gbla_status dist_allreduce_u64(gbla_mat h, unsigned long long *buf, size_t n)
+{
+    GBLA_NCCL_TRY(ncclAllReduce(buf, buf, n, ncclUint64, ncclSum, (ncclComm_t)h->ctx->nccl_comm, h->stream));
+    return GBLA_OK;
+}
+gbla_status dist_allgather(gbla_mat h, const void *send, void *recv, size_t bytes)
+{
+    GBLA_NCCL_TRY(ncclAllGather(send, recv, bytes, ncclUint8, (ncclComm_t)h->ctx->nccl_comm, h->stream));
+    return GBLA_OK;
+}
+gbla_status dist_bcast(gbla_mat h, void *buf, size_t bytes, int root)
+{
+    GBLA_NCCL_TRY(ncclBroadcast(buf, buf, bytes, ncclUint8, root, (ncclComm_t)h->ctx->nccl_comm, h->stream));
     return GBLA_OK;
 }

@@ -38,6 +38,8 @@
 
 void modgemm_set_sms(int sms);
 gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab);
+gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab, int G,
+                        int me, bool real);
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev);
@@ -668,6 +670,12 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 24, st));
     k_invtab<<<grid_for(h->p, 256), 256, 0, st>>>(h->F, invtab);
     note_launch();
+    // row-sharded D (multi-GPU, or emulated ranks): the distributed echelon assembles R itself
+    const bool real = h->ctx->world > 1 && h->ctx->nccl_comm;
+    const int G = real ? h->ctx->world : dist_emulated_world();
+    if (h->dist_rows && G > 1 && !(flags & GBLA_DENSE_INT)) {
+        if (mN > 0 && nN > 0) return panels_dist(h, rowpiv, dops, invtab, G, real ? h->ctx->rank : 0, real);
+    }
     if (mN > 0 && nN > 0) {
         if (flags & GBLA_DENSE_INT) GBLA_TRY(panels_int(h, rowpiv, dops, invtab));
         else GBLA_TRY(panels_tc2(h, rowpiv, dops, invtab));

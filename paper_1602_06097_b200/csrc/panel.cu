@@ -35,6 +35,8 @@
 
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "internal.cuh"
 #include "tc.cuh"
 
@@ -68,6 +70,22 @@ struct P2State {
 
 constexpr int P2_SMEM = PK * LDX * 2 + PK * PK * 2;   // row store + factor snapshot (192 KB)
 
+// Where the panel reads its rows.  Single GPU: all rows of D, window at column c0.
+// Distributed echelon: the candidates gathered from every rank (their window slices,
+// leads and D row ids), the global lead histogram, and the owner map (rowpiv is only
+// marked for this rank's rows).
+struct PanelSrc {
+    const uint16_t *D;          // row r, window column k at D[r * ldD + (gathered ? 0 : c0) + k]
+    int64_t ldD;
+    int64_t nrows;
+    const uint32_t *lead;       // [nrows] window-relative leading column, NONE if not active
+    const uint32_t *rid;        // [nrows] D row id (NULL: identity)
+    const uint32_t *ghist;      // [PW] global lead counts (NULL: counted here)
+    const uint8_t *owner;       // [mN] rank of each D row (NULL: every row is local)
+    int me;
+    int gathered;
+};
+
 __device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
 {
     const uint32_t r = v - __umulhi(v, m32) * p;
@@ -90,12 +108,13 @@ __device__ __forceinline__ void st8(uint16_t *s, const uint32_t (&v)[8])
 // One warp per row, 8 columns (16 bytes) per lane per step.
 __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
                         const uint32_t *__restrict__ rowpiv, const P2State *__restrict__ prev,
-                        uint32_t *__restrict__ lead)
+                        uint32_t *__restrict__ lead, const uint8_t *__restrict__ owner, int me)
 {
     const int lane = threadIdx.x & 31;
     const int64_t c0 = prev->c1;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (owner && owner[r] != me) continue;                 // another rank's row
     uint32_t res = NONE16;
     if (rowpiv[r] == GBLA_NONE && c0 < nN) {
         const int64_t wmax = nN - c0 < PW ? nN - c0 : PW;
@@ -147,9 +166,7 @@ __device__ void unit_upper_inverse(const uint32_t (*U)[33], uint32_t (*W)[33], u
     }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field F, const uint16_t *__restrict__ D,
-                                                   int64_t ldD, uint32_t *__restrict__ rowpiv,
-                                                   const uint32_t *__restrict__ lead,
+__global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc src, uint32_t *__restrict__ rowpiv,
                                                    const P2State *__restrict__ prev, P2State *__restrict__ cur,
                                                    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,
                                                    const uint16_t *__restrict__ invtab,
@@ -176,6 +193,11 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
     const uint32_t p = F.p;
     const uint32_t m32 = 0xffffffffu / p;
     const int64_t c0 = prev->c1;
+    const int64_t mN = src.nrows;
+    const uint32_t *__restrict__ lead = src.lead;
+    const uint16_t *__restrict__ D = src.D;
+    const int64_t ldD = src.ldD;
+    const int64_t coff = src.gathered ? 0 : c0;           // column of window column 0 in D
     // optional trace (GBLA_PANEL_TRACE): cycles per phase, accumulated over panels by thread 0
     long long t_mark = trace ? clock64() : 0;
 #define P2_LAP(k_)                                                                        \
@@ -195,11 +217,13 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
     for (int64_t r = tid; r < mN; r += NT) {
         const uint32_t l = lead[r];
         if (l < (uint64_t)wmax) {
-            atomicAdd(&hist[l], 1u);
+            if (!src.ghist) atomicAdd(&hist[l], 1u);
             const uint32_t q = atomicAdd(&s_u[5], 1u);
             if (q < (uint32_t)CLMAX) clist[q] = (uint32_t)r;
         }
     }
+    if (src.ghist)
+        for (int k = tid; k < wmax; k += NT) hist[k] = src.ghist[k];
     __syncthreads();
     {   // exclusive prefix over hist[0..PW] (threads 0..PW-1 own one entry each; PW <= NT)
         const uint32_t v = tid < PW ? hist[tid] : 0;
@@ -323,19 +347,19 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
         P2_LAP(1);
         // (a) load the chunk: values D[r, c0 + k], coefficients = unit vector at the physical row
         {
-            const bool vec = ((c0 & 7) == 0) && ((ldD & 7) == 0);
+            const bool vec = ((coff & 7) == 0) && ((ldD & 7) == 0);
             const int gv = ldv / 8;                   // 8-column groups of values
             for (int idx = tid; idx < ncand * gv; idx += NT) {
                 const int ci = idx / gv, g = idx % gv;
                 const uint32_t q = freel[ci];
-                const uint16_t *src = D + (size_t)crow[q] * ldD + c0 + 8 * g;
+                const uint16_t *srow = D + (size_t)crow[q] * ldD + coff + 8 * g;
                 uint4 v;
                 if (vec && 8 * g + 8 <= width) {
-                    v = *reinterpret_cast<const uint4 *>(src);
+                    v = *reinterpret_cast<const uint4 *>(srow);
                 } else {
                     uint16_t t[8];
 #pragma unroll
-                    for (int u = 0; u < 8; u++) t[u] = (8 * g + u < width) ? src[u] : 0;
+                    for (int u = 0; u < 8; u++) t[u] = (8 * g + u < width) ? srow[u] : 0;
                     v = *reinterpret_cast<uint4 *>(t);
                 }
                 *reinterpret_cast<uint4 *>(X + q * LDX + 8 * g) = v;
@@ -708,10 +732,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
         Thi[o] = (uint8_t)(v >> 8);
     }
     if (tid < (int)nb) {
-        const uint32_t r = crow[bphys[tid]];
+        const uint32_t rr = crow[bphys[tid]];
+        const uint32_t r = src.rid ? src.rid[rr] : rr;
         cur->sel[tid] = r;
         cur->pc[tid] = (uint32_t)(c0 + bpc[tid]);
-        rowpiv[r] = (uint32_t)(c0 + bpc[tid]);          // marks S (pivot column >= c0)
+        if (!src.owner || src.owner[r] == src.me)
+            rowpiv[r] = (uint32_t)(c0 + bpc[tid]);      // marks S (pivot column >= c0)
     }
     P2_LAP(6);
     if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; }
@@ -729,7 +755,8 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t mN, int64_t nN, Field 
 // a nonzero coefficient (limb planes of the trailing GEMM's A tiles), rows[slot] = i.
 __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ldD,
                           const uint32_t *__restrict__ rowpiv, P2State *__restrict__ ps,
-                          uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows)
+                          uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
+                          const uint8_t *__restrict__ owner, int me)
 {
     constexpr int CPL = PK / 32;
     const int lane = threadIdx.x & 31;
@@ -737,6 +764,7 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     if (kp == 0) return;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mN;
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (owner && owner[i] != me) continue;                     // another rank's row
     const uint32_t rp = rowpiv[i];
     if (rp != GBLA_NONE && rp >= (uint64_t)ps->c0) continue;   // selected now: becomes Rn
     const uint16_t *drow = D + (size_t)i * ldD;
@@ -796,12 +824,13 @@ __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t
 // D[S_b, c0 + x] = Rn[b][x]; op counts (block 0, thread 0)
 // part 0: all columns; 1: the next panel's window [c1, c1 + PW); 2: the other columns (+ op counts)
 __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, const P2State *__restrict__ ps,
-                          const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops, int part)
+                          const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops, int part,
+                          const uint8_t *__restrict__ owner = nullptr, int me = 0)
 {
     const uint32_t b = blockIdx.y;
     const uint32_t kp = ps->kp;
     const int64_t c0 = ps->c0;
-    if (part != 1 && b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
+    if (ops && part != 1 && b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
         const unsigned long long w = (unsigned long long)(nN - c0);
         ops[0] += (unsigned long long)ps->nrows * kp * w;                     // trailing update
         ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
@@ -819,6 +848,7 @@ __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, con
     for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < (int64_t)kp * ng;
          it += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t bb = (uint32_t)(it / ng);
+        if (owner && owner[ps->sel[bb]] != me) continue;           // another rank's pivot row
         const int64_t x0 = xlo + (it % ng) * 8;
         uint16_t *dst = D + (size_t)ps->sel[bb] * ldD + c0;
         const uint16_t *src = Rn + (size_t)bb * ldR;
@@ -843,6 +873,176 @@ __global__ void k_p2_init(P2State *ps)
     ps[1].c0 = ps[1].c1 = 0;
     ps[0].kp = ps[1].kp = 0;
     ps[0].nrows = ps[1].nrows = 0;
+}
+
+// ---- distributed echelon (row-sharded D) ----------------------------
+// owner[r] = rank of D row r: target tiles (128 rows in lead order) dealt cyclically
+__global__ void k_owner(int64_t mN, const uint32_t *__restrict__ order, int G, uint8_t *__restrict__ owner)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < mN) owner[order[i]] = (uint8_t)((i / 128) % G);
+}
+
+// counts of this rank's active rows by leading column in the window (lead < wmax)
+__global__ void k_hist_local(int64_t mN, int64_t nN, const uint32_t *__restrict__ lead,
+                             const uint8_t *__restrict__ owner, int me, const P2State *__restrict__ prev,
+                             uint32_t *__restrict__ hist)
+{
+    const int64_t c0 = prev->c1;
+    const int64_t wmax = nN - c0 < PW ? nN - c0 : PW;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < mN; r += (int64_t)gridDim.x * blockDim.x) {
+        if (owner[r] != me) continue;
+        const uint32_t l = lead[r];
+        if (l < (uint64_t)wmax) atomicAdd(&hist[l], 1u);
+    }
+}
+
+__global__ void k_sum_u32(int64_t n, int G, const uint32_t *__restrict__ in, int64_t stride, uint32_t *__restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0;
+        for (int g = 0; g < G; g++) s += in[(size_t)g * stride + i];
+        out[i] = s;
+    }
+}
+
+// the panel width from the global lead counts (the same rule as k_panel2, serially):
+// w[0] = width, w[1] = dense flag, w[2] = 1 once c0 >= nN
+__global__ void k_width(int64_t nN, const uint32_t *__restrict__ cnt, const P2State *__restrict__ prev,
+                        uint32_t *__restrict__ w)
+{
+    const int64_t c0 = prev->c1;
+    int64_t wmax = nN - c0;
+    if (wmax > PW) wmax = PW;
+    if (wmax <= 0) { w[0] = 0; w[1] = 0; w[2] = 1; return; }
+    const int64_t w128 = wmax < 128 ? wmax : 128;
+    uint32_t cum = 0, width = (uint32_t)w128;
+    uint32_t c128 = 0;
+    for (int64_t c = 0; c < w128; c++) c128 += cnt[c];
+    const bool dense = c128 > (uint32_t)PK;
+    if (!dense) {
+        for (int64_t c = 0; c <= wmax; c++) {        // cum = #rows leading before c
+            if (c >= w128 && cum <= (uint32_t)PK && (c == wmax || (c & 31) == 0)) width = (uint32_t)c;
+            if (c < wmax) cum += cnt[c];
+        }
+    }
+    w[0] = width;
+    w[1] = dense;
+    w[2] = 0;
+}
+
+// this rank's candidates (lead < width): lead, D row id and window values (ld = ldc)
+__global__ void k_cand_pack(int64_t mN, const uint16_t *__restrict__ D, int64_t ldD, const uint32_t *__restrict__ lead,
+                            const uint8_t *__restrict__ owner, int me, const P2State *__restrict__ prev,
+                            const uint32_t *__restrict__ w, int64_t ldc, uint32_t *__restrict__ cnt,
+                            uint32_t *__restrict__ olead, uint32_t *__restrict__ orid, uint16_t *__restrict__ oval)
+{
+    const int64_t c0 = prev->c1;
+    const uint32_t width = w[0];
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (owner[r] != me || lead[r] >= width) continue;
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(cnt, 1u);
+        slot = __shfl_sync(FULL, slot, 0);
+        if (lane == 0) { olead[slot] = lead[r]; orid[slot] = (uint32_t)r; }
+        for (int64_t k = lane; k < ldc; k += 32)
+            oval[(size_t)slot * ldc + k] = k < (int64_t)width ? D[(size_t)r * ldD + c0 + k] : 0;
+    }
+}
+
+// pad the candidate block of one rank to `maxcnt` slots (lead NONE = not a candidate)
+__global__ void k_cand_pad(uint32_t cnt, uint32_t maxcnt, uint32_t *__restrict__ olead)
+{
+    const uint32_t i = cnt + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < maxcnt) olead[i] = NONE16;
+}
+
+// this rank's rows of S (u32, zero elsewhere): summed over ranks they give D[S, c0:]
+__global__ void k_srow_pack(int64_t nN, const uint16_t *__restrict__ D, int64_t ldD, const P2State *__restrict__ ps,
+                            const uint8_t *__restrict__ owner, int me, uint32_t *__restrict__ buf, int64_t ldb)
+{
+    const uint32_t kp = ps->kp;
+    const int64_t c0 = ps->c0;
+    if (c0 >= nN) return;
+    const int64_t width = nN - c0;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < (int64_t)kp * width;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(it / width);
+        const int64_t x = it % width;
+        const uint32_t r = ps->sel[b];
+        buf[(size_t)b * ldb + x] = owner[r] == me ? D[(size_t)r * ldD + c0 + x] : 0u;
+    }
+}
+
+// transposed limb planes of the summed S rows (as k_gather_st2, from the u32 buffer)
+__global__ void k_gather_st32(int64_t nN, const P2State *__restrict__ ps, const uint32_t *__restrict__ buf,
+                              int64_t ldb, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi)
+{
+    const uint32_t kp = ps->kp;
+    if (kp == 0) return;
+    const int64_t c0 = ps->c0;
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c0 + x >= nN) return;
+    const uint32_t s = blockIdx.y * 16;
+    uint8_t lo[16], hi[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+        const uint32_t v = (s + u < kp) ? buf[(size_t)(s + u) * ldb + x] : 0;
+        lo[u] = (uint8_t)(v & 0xff);
+        hi[u] = (uint8_t)(v >> 8);
+    }
+    const size_t o = (size_t)(x / 64) * (64 * PK) + tc::toff64((uint32_t)(x % 64), s);
+    *reinterpret_cast<uint4 *>(Blo + o) = *reinterpret_cast<uint4 *>(lo);
+    *reinterpret_cast<uint4 *>(Bhi + o) = *reinterpret_cast<uint4 *>(hi);
+}
+
+__global__ void k_colflag2(int64_t nN, const uint32_t *__restrict__ colrow, uint32_t *__restrict__ flag)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nN) flag[c] = colrow[c] != GBLA_NONE;
+    else if (c == nN) flag[c] = 0;
+}
+
+// R assembly: pivot columns of one rank's rows -> flags; that rank's R rows -> R
+__global__ void k_own_pivots(int64_t mN, const uint32_t *__restrict__ rowpiv, const uint8_t *__restrict__ owner,
+                             int me, uint32_t *__restrict__ colrow)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < mN && owner[i] == me && rowpiv[i] != GBLA_NONE) colrow[rowpiv[i]] = (uint32_t)i;
+}
+__global__ void k_flag_list(uint32_t n, const uint32_t *__restrict__ pcs, uint32_t *__restrict__ flag)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[pcs[i]] = 1;
+}
+// rows of the staging block (pivot columns pcs[0..n)) into R at cidx[pc]
+__global__ void k_scatter_rows(int64_t nN, uint32_t n, const uint32_t *__restrict__ pcs,
+                               const uint16_t *__restrict__ stg, int64_t ldS, const uint32_t *__restrict__ cidx,
+                               uint16_t *__restrict__ R, int64_t ldR, uint32_t *__restrict__ pivcol)
+{
+    const uint32_t j = blockIdx.y;
+    if (j >= n) return;
+    const uint32_t c = pcs[j], k = cidx[c];
+    if (blockIdx.x == 0 && threadIdx.x == 0) pivcol[k] = c;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nN; x += (int64_t)gridDim.x * blockDim.x)
+        R[(size_t)k * ldR + x] = stg[(size_t)j * ldS + x];
+}
+// one rank's pivot rows, in pivot-column order, into the staging block + their pivot columns
+__global__ void k_gather_own(int64_t nN, const uint32_t *__restrict__ colrow, const uint32_t *__restrict__ oidx,
+                             const uint16_t *__restrict__ D, int64_t ldD, uint16_t *__restrict__ stg, int64_t ldS,
+                             uint32_t *__restrict__ pcs, int64_t cbase)
+{
+    const int64_t c = cbase + blockIdx.y;
+    if (c >= nN) return;
+    const uint32_t r = colrow[c];
+    if (r == GBLA_NONE) return;
+    const uint32_t j = oidx[c];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && pcs) pcs[j] = (uint32_t)c;
+    if (!stg) return;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nN; x += (int64_t)gridDim.x * blockDim.x)
+        stg[(size_t)j * ldS + x] = D[(size_t)r * ldD + x];
 }
 
 }  // namespace
@@ -905,12 +1105,13 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
                                                                                 : 4u * h->ctx->sm_count;
-        k_lead2<<<rgrid, 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead);
+        k_lead2<<<rgrid, 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead, nullptr, 0);
         kt_mark_on(h, KT_PANEL, s);
-        k_panel2<<<1, NT, P2_SMEM, s>>>(mN, nN, h->F, h->D, ldD, rowpiv, lead, prev, cur, Tlo, Thi, invtab, trace);
+        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0};
+        k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, trace);
         kt_mark_on(h, KT_PANEL, s);
-        k_gather2<<<rgrid, 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
-                                                          rows[k & 1]);
+        k_gather2<<<rgrid, 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1], rows[k & 1], nullptr,
+                                        0);
         note_launch(3);
     };
     if (lookahead) {
@@ -1052,4 +1253,304 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
     }
     return status;
+}
+
+// ---- distributed echelon --------------------------------------------------------------
+gbla_status dist_allreduce_u32(gbla_mat h, uint32_t *buf, size_t n);
+gbla_status dist_allreduce_u64(gbla_mat h, unsigned long long *buf, size_t n);
+gbla_status dist_allgather(gbla_mat h, const void *send, void *recv, size_t bytes);
+gbla_status dist_bcast(gbla_mat h, void *buf, size_t bytes, int root);
+template <class T>
+static gbla_status exclusive_scan_u32(gbla_mat h, const T *in, T *out, int64_t count);
+
+// Echelon of a row-sharded D: rank g owns the rows of the target tiles
+// T = g, g+G, ... (owner[]); nothing but the exchanges below crosses ranks.  Per panel:
+//   leads + lead counts of own rows -> C3a all-reduce of the counts -> the panel width
+//   (same rule as k_panel2) -> C3b all-gather of every rank's candidate slices -> every
+//   rank runs the same panel factorization on the same gathered candidates (identical
+//   T, S, pivot columns) -> C4 all-reduce of the S rows (each row from its owner, zeros
+//   elsewhere) -> Rn = T D[S, c0:] on every rank -> K11 on own rows -> own S rows = Rn.
+// R: pivot-column lists all-gathered, then every rank's pivot rows broadcast (C6) and
+// placed in pivot-column order.  `real` = NCCL; otherwise the G ranks are emulated in
+// this process (one shared D whose rows are disjoint between ranks) and the exchanges
+// are device copies / sums - the same kernels and the same data movement.
+gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab, int G,
+                        int me, bool real)
+{
+    cudaStream_t st = h->stream;
+    modgemm_set_sms(h->ctx->sm_count);
+    const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
+    const int64_t npad = (nN + 63) / 64 * 64 + 64;
+    const int nloc = real ? 1 : G;                     // ranks handled by this process
+    auto rank_of = [&](int j) { return real ? me : j; };
+    uint8_t *owner;
+    uint32_t *rows, *lead, *hbuf, *ghist, *wdev, *cnt, *buf32, *bsum;
+    uint16_t *Rn;
+    uint8_t *Flo, *Fhi, *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
+    P2State *ps;
+    GBLA_TRY(dalloc_t(h, mN + 1, &owner));
+    k_owner<<<grid_for(mN, 256), 256, 0, st>>>(mN, h->order, G, owner);
+    note_launch();
+    GBLA_TRY(dalloc_t(h, mN + 1, &rows));
+    GBLA_TRY(dalloc_t(h, mN + 1, &lead));
+    GBLA_CUDA_TRY(cudaMemsetAsync(lead, 0xff, (mN + 1) * 4, st));
+    GBLA_TRY(dalloc_t(h, (size_t)nloc * PW, &hbuf));
+    GBLA_TRY(dalloc_t(h, PW, &ghist));
+    GBLA_TRY(dalloc_t(h, 4, &wdev));
+    GBLA_TRY(dalloc_t(h, (size_t)G + 1, &cnt));
+    const int64_t ldb = nN > 0 ? nN : 1;
+    GBLA_TRY(dalloc_t(h, (size_t)nloc * PK * ldb, &buf32));
+    bsum = buf32;
+    if (!real && G > 1) GBLA_TRY(dalloc_t(h, (size_t)PK * ldb, &bsum));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Flo));
+    GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Fhi));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rtlo));
+    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rthi));
+    GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
+    GBLA_TRY(dalloc(h, 2 * sizeof(P2State), (void **)&ps));
+    // candidate blocks: per local rank (send) and gathered (G blocks of maxcnt slots)
+    const int64_t cap = mN > 0 ? mN : 1;
+    uint32_t *sl, *sr, *gl, *gr;
+    uint16_t *sv, *gv;
+    GBLA_TRY(dalloc_t(h, (size_t)nloc * cap, &sl));
+    GBLA_TRY(dalloc_t(h, (size_t)nloc * cap, &sr));
+    GBLA_TRY(dalloc_t(h, (size_t)nloc * cap * PW, &sv));
+    int64_t gcap = 0;
+    gl = gr = nullptr;
+    gv = nullptr;
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+        attr = true;
+    }
+    uint32_t *hpin = nullptr;                          // [0..3) width info, [4..4+G) candidate counts
+    GBLA_CUDA_TRY(cudaMallocHost(&hpin, (8 + (size_t)G) * 4));
+    gbla_status status = GBLA_OK;
+    const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                            : 4u * h->ctx->sm_count;
+    k_p2_init<<<1, 1, 0, st>>>(ps);
+    note_launch();
+    for (int64_t k = 0; status == GBLA_OK; k++) {
+        P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
+        // C3a: lead counts of own rows, summed over ranks
+        if (cudaMemsetAsync(hbuf, 0, (size_t)nloc * PW * 4, st) != cudaSuccess) { status = GBLA_E_CUDA; break; }
+        for (int j = 0; j < nloc; j++) {
+            k_lead2<<<rgrid, 256, 0, st>>>(mN, nN, h->D, ldD, rowpiv, prev, lead, owner, rank_of(j));
+            k_hist_local<<<grid_for(mN, 256), 256, 0, st>>>(mN, nN, lead, owner, rank_of(j), prev,
+                                                            hbuf + (size_t)j * PW);
+            note_launch(2);
+        }
+        if (real) {
+            if ((status = dist_allreduce_u32(h, hbuf, PW)) != GBLA_OK) break;
+            GBLA_CUDA_TRY(cudaMemcpyAsync(ghist, hbuf, PW * 4, cudaMemcpyDeviceToDevice, st));
+        } else {
+            k_sum_u32<<<2, 256, 0, st>>>(PW, G, hbuf, PW, ghist);
+            note_launch();
+        }
+        k_width<<<1, 1, 0, st>>>(nN, ghist, prev, wdev);
+        GBLA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (G + 1) * 4, st));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(hpin, wdev, 12, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (hpin[2]) break;                                           // c0 >= nN: done
+        const int64_t width = hpin[0], ldc = (width + 31) / 32 * 32;
+        // C3b: every rank's candidates (lead < width)
+        for (int j = 0; j < nloc; j++) {
+            k_cand_pack<<<rgrid, 256, 0, st>>>(mN, h->D, ldD, lead, owner, rank_of(j), prev, wdev, ldc, cnt + j,
+                                                sl + (size_t)j * cap, sr + (size_t)j * cap, sv + (size_t)j * cap * PW);
+            note_launch();
+        }
+        if (real) {
+            GBLA_CUDA_TRY(cudaMemcpyAsync(cnt + G, cnt, 4, cudaMemcpyDeviceToDevice, st));
+            if ((status = dist_allgather(h, cnt + G, cnt, 4)) != GBLA_OK) break;
+        }
+        GBLA_CUDA_TRY(cudaMemcpyAsync(hpin + 4, cnt, (size_t)G * 4, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        uint32_t maxcnt = 0;
+        for (int g = 0; g < G; g++) maxcnt = hpin[4 + g] > maxcnt ? hpin[4 + g] : maxcnt;
+        if (maxcnt == 0) maxcnt = 1;
+        if ((int64_t)G * maxcnt > gcap) {
+            gcap = (int64_t)G * maxcnt;
+            GBLA_TRY(dalloc_t(h, (size_t)gcap, &gl));
+            GBLA_TRY(dalloc_t(h, (size_t)gcap, &gr));
+            GBLA_TRY(dalloc_t(h, (size_t)gcap * PW, &gv));
+        }
+        for (int j = 0; j < nloc; j++) {
+            const uint32_t cj = hpin[4 + rank_of(j)];
+            if (cj < maxcnt) k_cand_pad<<<grid_for(maxcnt - cj, 256), 256, 0, st>>>(cj, maxcnt, sl + (size_t)j * cap);
+        }
+        if (real) {
+            if ((status = dist_allgather(h, sl, gl, (size_t)maxcnt * 4)) != GBLA_OK) break;
+            if ((status = dist_allgather(h, sr, gr, (size_t)maxcnt * 4)) != GBLA_OK) break;
+            if ((status = dist_allgather(h, sv, gv, (size_t)maxcnt * ldc * 2)) != GBLA_OK) break;
+        } else {
+            for (int g = 0; g < G; g++) {
+                GBLA_CUDA_TRY(cudaMemcpyAsync(gl + (size_t)g * maxcnt, sl + (size_t)g * cap, maxcnt * 4,
+                                              cudaMemcpyDeviceToDevice, st));
+                GBLA_CUDA_TRY(cudaMemcpyAsync(gr + (size_t)g * maxcnt, sr + (size_t)g * cap, maxcnt * 4,
+                                              cudaMemcpyDeviceToDevice, st));
+                GBLA_CUDA_TRY(cudaMemcpyAsync(gv + (size_t)g * maxcnt * ldc, sv + (size_t)g * cap * PW,
+                                              (size_t)maxcnt * ldc * 2, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        // the same panel factorization on every rank
+        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1};
+        kt_mark(h, KT_PANEL);
+        k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr);
+        kt_mark(h, KT_PANEL);
+        note_launch();
+        // C4: the S rows from their owners
+        for (int j = 0; j < nloc; j++) {
+            k_srow_pack<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, owner, rank_of(j),
+                                                               buf32 + (size_t)j * PK * ldb, ldb);
+            note_launch();
+        }
+        if (real) {
+            if ((status = dist_allreduce_u32(h, buf32, (size_t)PK * ldb)) != GBLA_OK) break;
+        } else if (G > 1) {
+            k_sum_u32<<<4 * h->ctx->sm_count, 256, 0, st>>>((int64_t)PK * ldb, G, buf32, (int64_t)PK * ldb, bsum);
+            note_launch();
+        }
+        k_gather_st32<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, cur, bsum, ldb, Blo, Bhi);
+        note_launch();
+        kt_mark(h, KT_RN);
+        if ((status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp)) !=
+            GBLA_OK)
+            break;
+        kt_mark(h, KT_RN);
+        // K11 on own rows (emulated: every rank's rows in one list), own S rows = Rn
+        for (int j = 0; j < nloc; j++) {
+            k_gather2<<<rgrid, 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows, owner, rank_of(j));
+            note_launch();
+        }
+        kt_mark(h, KT_TRAIL);
+        if ((status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo, Fhi, Rtlo, Rthi, rows, h->D, ldD,
+                                     &cur->c0, nullptr, 0, 0, 0)) != GBLA_OK)
+            break;
+        kt_mark(h, KT_TRAIL);
+        for (int j = 0; j < nloc; j++) {
+            k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, j == 0 ? dops : nullptr, 0,
+                                                            owner, rank_of(j));
+            note_launch();
+        }
+        if (cudaGetLastError() != cudaSuccess) { set_error("distributed echelon: launch failed"); status = GBLA_E_CUDA; }
+    }
+    cudaFreeHost(hpin);
+    if (status != GBLA_OK) return status;
+    // op counts: the trailing updates were split over the ranks
+    if (real) GBLA_TRY(dist_allreduce_u64(h, dops, 1));
+    // ---- R: pivot-column lists of every rank, then every rank's pivot rows in pivot order
+    uint32_t *colrow, *oflag, *oidx, *gflag, *gidx, *pcs;
+    GBLA_TRY(dalloc_t(h, nN + 1, &colrow));
+    GBLA_TRY(dalloc_t(h, nN + 1, &oflag));
+    GBLA_TRY(dalloc_t(h, nN + 1, &oidx));
+    GBLA_TRY(dalloc_t(h, nN + 1, &gflag));
+    GBLA_TRY(dalloc_t(h, nN + 1, &gidx));
+    std::vector<uint32_t> counts(G, 0);
+    auto own_lists = [&](int g) -> gbla_status {     // colrow / oidx / count of rank g's pivot rows
+        GBLA_CUDA_TRY(cudaMemsetAsync(colrow, 0xff, (nN + 1) * 4, st));
+        k_own_pivots<<<grid_for(mN, 256), 256, 0, st>>>(mN, rowpiv, owner, g, colrow);
+        k_colflag2<<<grid_for(nN + 1, 256), 256, 0, st>>>(nN, colrow, oflag);
+        note_launch(2);
+        GBLA_TRY(exclusive_scan_u32<uint32_t>(h, oflag, oidx, nN + 1));
+        return GBLA_OK;
+    };
+    // pass 1: counts and pivot columns of every rank (pcs: G blocks of up to maxc entries)
+    uint32_t mycnt = 0;
+    std::vector<uint32_t> hc(G + 1, 0);
+    if (real) {
+        GBLA_TRY(own_lists(me));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(cnt + G, oidx + nN, 4, cudaMemcpyDeviceToDevice, st));
+        GBLA_TRY(dist_allgather(h, cnt + G, cnt, 4));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt, (size_t)G * 4, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        for (int g = 0; g < G; g++) counts[g] = hc[g];
+        mycnt = counts[me];
+    } else {
+        for (int g = 0; g < G; g++) {
+            GBLA_TRY(own_lists(g));
+            GBLA_CUDA_TRY(cudaMemcpyAsync(&hc[g], oidx + nN, 4, cudaMemcpyDeviceToHost, st));
+            GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+            counts[g] = hc[g];
+        }
+    }
+    uint32_t maxc = 1;
+    for (int g = 0; g < G; g++) maxc = counts[g] > maxc ? counts[g] : maxc;
+    GBLA_TRY(dalloc_t(h, (size_t)G * maxc, &pcs));
+    const unsigned gx = grid_for(nN, 256) < 8 ? grid_for(nN, 256) : 8;
+    auto own_pcs = [&](uint32_t *dst, uint16_t *stg, int64_t ldS) -> gbla_status {   // after own_lists
+        for (int64_t cb = 0; cb < nN; cb += 65535) {
+            const int64_t n = nN - cb < 65535 ? nN - cb : 65535;
+            k_gather_own<<<dim3(stg ? gx : 1, (unsigned)n), stg ? 256 : 32, 0, st>>>(nN, colrow, oidx, h->D, ldD, stg,
+                                                                                    ldS, dst, cb);
+            note_launch();
+        }
+        GBLA_CUDA_TRY(cudaGetLastError());
+        return GBLA_OK;
+    };
+    if (real) {
+        uint32_t *mine;
+        GBLA_TRY(dalloc_t(h, maxc, &mine));
+        GBLA_TRY(own_pcs(mine, nullptr, 0));
+        GBLA_TRY(dist_allgather(h, mine, pcs, (size_t)maxc * 4));
+    } else {
+        for (int g = 0; g < G; g++) {
+            GBLA_TRY(own_lists(g));
+            GBLA_TRY(own_pcs(pcs + (size_t)g * maxc, nullptr, 0));
+        }
+    }
+    GBLA_CUDA_TRY(cudaMemsetAsync(gflag, 0, (nN + 1) * 4, st));
+    for (int g = 0; g < G; g++)
+        if (counts[g]) {
+            k_flag_list<<<grid_for(counts[g], 256), 256, 0, st>>>(counts[g], pcs + (size_t)g * maxc, gflag);
+            note_launch();
+        }
+    GBLA_TRY(exclusive_scan_u32<uint32_t>(h, gflag, gidx, nN + 1));
+    uint32_t rk = 0;
+    unsigned long long dv[3] = {0, 0, 0};
+    GBLA_CUDA_TRY(cudaMemcpyAsync(&rk, gidx + nN, 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 24, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    h->rank = rk;
+    h->dense_ops = dv[0] + dv[1];
+    h->kwork[KT_TRAIL] = dv[0];
+    h->kwork[KT_RN] = dv[1];
+    h->kwork[KT_PANEL] = dv[2];
+    h->ldR = ldR;
+    GBLA_TRY(dalloc_t(h, (size_t)(rk > 0 ? rk : 1) * h->ldR, &h->R));
+    GBLA_TRY(dalloc_t(h, rk + 1, &h->pivcol));
+    // pass 2 (C6): rank g's pivot rows -> every rank -> R rows cidx[pivot column]
+    uint16_t *stg;
+    GBLA_TRY(dalloc_t(h, (size_t)maxc * ldR, &stg));
+    for (int g = 0; g < G; g++) {
+        if (!counts[g]) continue;
+        if (!real || g == me) {
+            GBLA_TRY(own_lists(g));
+            GBLA_TRY(own_pcs(nullptr, stg, ldR));
+        }
+        if (real) GBLA_TRY(dist_bcast(h, stg, (size_t)counts[g] * ldR * 2, g));
+        for (uint32_t j0 = 0; j0 < counts[g]; j0 += 65535) {
+            const uint32_t n = counts[g] - j0 < 65535 ? counts[g] - j0 : 65535;
+            k_scatter_rows<<<dim3(gx, n), 256, 0, st>>>(nN, n, pcs + (size_t)g * maxc + j0, stg + (size_t)j0 * ldR,
+                                                         ldR, gidx, h->R, h->ldR, h->pivcol);
+            note_launch();
+        }
+    }
+    GBLA_CUDA_TRY(cudaGetLastError());
+    (void)mycnt;
+    return GBLA_OK;
+}
+
+template <class T>
+static gbla_status exclusive_scan_u32(gbla_mat h, const T *in, T *out, int64_t count)
+{
+    size_t tmp = 0;
+    GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)count, h->stream));
+    void *t = nullptr;
+    GBLA_TRY(dalloc(h, tmp + 16, &t));
+    GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int)count, h->stream));
+    return GBLA_OK;
 }
