@@ -20,6 +20,7 @@ Multi-GPU (torchrun, N > 1): see DESIGN.md §"Multi-GPU"; one process per GPU.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -245,6 +246,10 @@ def main():
         h = gb.gbla_reduce(ctx, M.m, M.n, rp, col, val, M.p, flags=args.flags, stream=stream)
         return h
 
+    # libgbla allocates device memory through torch (a Python callback per buffer): keep the Python
+    # garbage collector from running inside those callbacks in the middle of a reduction
+    gc.collect()
+    gc.disable()
     for _ in range(max(args.warmup, 0)):
         step().free()
     torch.cuda.synchronize()
@@ -253,6 +258,7 @@ def main():
     phases = []
     kms = {k: [0.0, 0] for k in gb.Mat.KERNELS}
     kwork = {k: 0 for k in gb.Mat.KERNELS}
+    kms_steps = []
     ops = dense_ops = 0
     rank_d = None
     clocks = ClockSampler(dev)
@@ -266,9 +272,12 @@ def main():
         h = step()
         ev[i][1].record(stream)
         phases.append(h.phase_ms())
+        step_k = {}
         for k, (ms_k, n_k) in h.kernel_ms().items():
             kms[k][0] += ms_k
             kms[k][1] += n_k
+            step_k[k] = round(ms_k, 2)
+        kms_steps.append(step_k)
         for k, w in h.kernel_work().items():
             kwork[k] += w
         ops, dense_ops = h.opcount()
@@ -276,6 +285,7 @@ def main():
         h.free()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    gc.enable()
     launches = gb.kernel_launches() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
@@ -337,6 +347,8 @@ def main():
             "rank_D": rank_d[1], "npiv": rank_d[0][0],
             "phase_ms": ph, "step_ms": [round(x, 3) for x in step_ms],
             "kernel_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kms.items()},
+            "phase_ms_steps": [{k: round(v, 2) for k, v in p.items() if v} for p in phases],
+            "kernel_ms_steps": kms_steps,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "gpu_launches_per_step": round(launches / max(args.steps, 1), 1),
             "clocks": clk, "peaks_source": peak_src,

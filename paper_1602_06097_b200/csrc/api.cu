@@ -154,10 +154,49 @@ extern "C" gbla_status gbla_ctx_set_comm(gbla_ctx ctx, const void *nccl_unique_i
     return dist_set_comm(ctx, nccl_unique_id, rank, world);
 }
 
+cudaStream_t ctx_side_stream(gbla_ctx c)
+{
+    if (!c->side) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi) != cudaSuccess) {
+            cudaGetLastError();
+            c->side = nullptr;
+        }
+    }
+    return c->side;
+}
+
+cudaEvent_t ctx_event(gbla_ctx c, int i)
+{
+    if (!c->ev[i] && cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        c->ev[i] = nullptr;
+    }
+    return c->ev[i];
+}
+
+void *ctx_pinned(gbla_ctx c, size_t bytes)
+{
+    if (c->pinned_bytes < bytes) {
+        if (c->pinned) cudaFreeHost(c->pinned);
+        c->pinned = nullptr;
+        c->pinned_bytes = 0;
+        if (cudaMallocHost(&c->pinned, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        c->pinned_bytes = bytes;
+    }
+    return c->pinned;
+}
+
 extern "C" void gbla_ctx_destroy(gbla_ctx ctx)
 {
     if (!ctx) return;
     dist_destroy(ctx);
+    cudaSetDevice(ctx->device);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    for (cudaEvent_t e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
 }
 
@@ -174,20 +213,21 @@ struct PhaseTimer {
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
     explicit PhaseTimer(cudaStream_t st) : s(st) {
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
-        cudaEventRecord(a, s);
+        a = kt_event_get();
+        b = kt_event_get();
+        if (a) cudaEventRecord(a, s);
     }
     float stop() {
         float ms = 0;
+        if (!a || !b) return 0;
         cudaEventRecord(b, s);
         cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b);
         return ms;
     }
     ~PhaseTimer() {
-        if (a) cudaEventDestroy(a);
-        if (b) cudaEventDestroy(b);
+        if (a) kt_event_put(a);
+        if (b) kt_event_put(b);
     }
 };
 

@@ -45,7 +45,8 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev);
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev);
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
+                             int64_t win_w, int ctsel);
 
 namespace {
 

@@ -83,7 +83,16 @@ struct gbla_ctx_s {
     void *user = nullptr;
     void *nccl_comm = nullptr;   // ncclComm_t
     int rank = 0, world = 1;
+    // per-context resources reused across calls (creating them per call costs host time that
+    // stalls the pipelined panel loop): the echelon's side stream, sync events, pinned scratch
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void *pinned = nullptr;
+    size_t pinned_bytes = 0;
 };
+cudaStream_t ctx_side_stream(gbla_ctx c);      // high priority, non-blocking; NULL on failure
+cudaEvent_t ctx_event(gbla_ctx c, int i);      // i < 4, timing disabled
+void *ctx_pinned(gbla_ctx c, size_t bytes);    // pinned host scratch (grows), NULL on failure
 
 struct Alloc {
     void *ptr;

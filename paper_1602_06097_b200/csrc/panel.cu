@@ -33,6 +33,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <functional>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -46,7 +47,8 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
                            const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap);
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev);
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
+                             int64_t win_w, int ctsel);
 void modgemm_set_sms(int sms);
 
 namespace {
@@ -84,7 +86,17 @@ struct PanelSrc {
     const uint8_t *owner;       // [mN] rank of each D row (NULL: every row is local)
     int me;
     int gathered;
+    int cap;                    // wide panels: at most cap (<= PK) rows lead inside the window
 };
+
+// candidates per wide panel (GBLA_PANEL_CAP, default PK): fewer pivots per panel shorten the
+// panel factorization (quadratic in them) but add panels
+static int panel_cap()
+{
+    const char *e = getenv("GBLA_PANEL_CAP");
+    const int c = e ? atoi(e) : PK;
+    return c >= 16 && c <= PK ? c : PK;
+}
 
 __device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
 {
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         // widest w with <= PK candidates; a multiple of 32 (c0 stays 64-byte aligned for the
         // GEMM epilogue's vector path) unless the panel reaches the last column
         for (int64_t c = w128 + tid; c <= wmax; c += NT)
-            if (hist[c] <= (uint32_t)PK && (c == wmax || (c & 31) == 0)) atomicMax(&s_u[0], (uint32_t)c);
+            if (hist[c] <= (uint32_t)src.cap && (c == wmax || (c & 31) == 0)) atomicMax(&s_u[0], (uint32_t)c);
     }
     __syncthreads();
     const int width = (int)s_u[0];
@@ -909,7 +921,7 @@ __global__ void k_sum_u32(int64_t n, int G, const uint32_t *__restrict__ in, int
 // the panel width from the global lead counts (the same rule as k_panel2, serially):
 // w[0] = width, w[1] = dense flag, w[2] = 1 once c0 >= nN
 __global__ void k_width(int64_t nN, const uint32_t *__restrict__ cnt, const P2State *__restrict__ prev,
-                        uint32_t *__restrict__ w)
+                        uint32_t *__restrict__ w, int cap)
 {
     const int64_t c0 = prev->c1;
     int64_t wmax = nN - c0;
@@ -922,7 +934,7 @@ __global__ void k_width(int64_t nN, const uint32_t *__restrict__ cnt, const P2St
     const bool dense = c128 > (uint32_t)PK;
     if (!dense) {
         for (int64_t c = 0; c <= wmax; c++) {        // cum = #rows leading before c
-            if (c >= w128 && cum <= (uint32_t)PK && (c == wmax || (c & 31) == 0)) width = (uint32_t)c;
+            if (c >= w128 && cum <= (uint32_t)cap && (c == wmax || (c & 31) == 0)) width = (uint32_t)c;
             if (c < wmax) cum += cnt[c];
         }
     }
@@ -1064,7 +1076,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     const int64_t npad = (nN + 63) / 64 * 64 + 64;
     uint32_t *rows[2], *lead;
     uint16_t *Rn;
-    uint8_t *Flo[2], *Fhi[2], *Tlo, *Thi, *Blo, *Bhi, *Rtlo, *Rthi;
+    uint8_t *Flo[2], *Fhi[2], *Tlo2[2], *Thi2[2], *Blo, *Bhi, *Rtlo, *Rthi;
     P2State *ps;
     for (int q = 0; q < 2; q++) {
         GBLA_TRY(dalloc_t(h, mN + 1, &rows[q]));
@@ -1072,8 +1084,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_TRY(dalloc_t(h, (size_t)(mN + 128) * PK, &Fhi[q]));
     }
     GBLA_TRY(dalloc_t(h, mN + 1, &lead));
-    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo));
-    GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi));
+    for (int q = 0; q < 2; q++) {            // T of panel k+1 is written while the rest of panel k reads T
+        GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo2[q]));
+        GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi2[q]));
+    }
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rtlo));
@@ -1091,6 +1105,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 16 * 8, st));
     }
     const bool lookahead = getenv("GBLA_NO_LOOKAHEAD") == nullptr;
+    const int cap = panel_cap();
     cudaStream_t side = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr;
     int64_t *c1_host = nullptr;
@@ -1101,28 +1116,42 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     };
     const int gemm_grid = lookahead ? h->ctx->sm_count - 1 : h->ctx->sm_count;   // one SM for the next panel
     // the panel factorization of panel k on stream s (prev = panel k-1's state)
-    auto factor = [&](cudaStream_t s, int64_t k) {
-        P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
-        const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
-                                                                                : 4u * h->ctx->sm_count;
+    // panel k: leads of the window (all SMs), the factorization (one SM), F of the other rows (all SMs).
+    // With look-ahead the middle step runs on the side stream, the two wide ones on the main stream
+    // where they do not compete with the rest of the previous update.
+    const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                            : 4u * h->ctx->sm_count;
+    auto p_lead = [&](cudaStream_t s, int64_t k) {
+        P2State *prev = ps + ((k + 1) & 1);
         k_lead2<<<rgrid, 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead, nullptr, 0);
+        note_launch();
+    };
+    auto p_factor = [&](cudaStream_t s, int64_t k) {
+        P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         kt_mark_on(h, KT_PANEL, s);
-        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0};
-        k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, trace);
+        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap};
+        k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace);
         kt_mark_on(h, KT_PANEL, s);
+        note_launch();
+    };
+    auto p_gather = [&](cudaStream_t s, int64_t k) {
+        P2State *cur = ps + (k & 1);
         k_gather2<<<rgrid, 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1], rows[k & 1], nullptr,
                                         0);
-        note_launch(3);
+        note_launch();
     };
-    if (lookahead) {
-        int lo_pri = 0, hi_pri = 0;        // the next panel is the critical path: schedule it first
-        cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
-        if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_pri) != cudaSuccess ||
-            cudaEventCreateWithFlags(&evA, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&evB, cudaEventDisableTiming) != cudaSuccess)
-            fail("stream/event creation");
+    auto factor = [&](cudaStream_t s, int64_t k) {
+        p_lead(s, k);
+        p_factor(s, k);
+        p_gather(s, k);
+    };
+    if (lookahead) {                      // the next panel is the critical path: high-priority side stream
+        side = ctx_side_stream(h->ctx);
+        evA = ctx_event(h->ctx, 0);
+        evB = ctx_event(h->ctx, 1);
+        if (!side || !evA || !evB) fail("stream/event creation");
     }
-    if (status == GBLA_OK && cudaMallocHost(&c1_host, 2 * sizeof(int64_t)) != cudaSuccess) fail("cudaMallocHost");
+    if (status == GBLA_OK && !(c1_host = (int64_t *)ctx_pinned(h->ctx, 2 * sizeof(int64_t)))) fail("cudaMallocHost");
     if (status == GBLA_OK) {
         k_p2_init<<<1, 1, 0, st>>>(ps);
         note_launch();
@@ -1145,9 +1174,9 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     cudaEvent_t bev[2] = {nullptr, nullptr};
     int64_t bk[2] = {0, 0};
     int nb_done = 0;
-    if (status == GBLA_OK && (cudaEventCreateWithFlags(&bev[0], cudaEventDisableTiming) != cudaSuccess ||
-                              cudaEventCreateWithFlags(&bev[1], cudaEventDisableTiming) != cudaSuccess))
-        fail("event");
+    bev[0] = ctx_event(h->ctx, 2);
+    bev[1] = ctx_event(h->ctx, 3);
+    if (status == GBLA_OK && (!bev[0] || !bev[1])) fail("event");
     while (status == GBLA_OK) {
         for (int q = 0; q < batch && status == GBLA_OK; q++, k++) {
             P2State *cur = ps + (k & 1);
@@ -1156,7 +1185,9 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             k_gather_st2<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, h->D, ldD, cur, Blo, Bhi);
             note_launch();
             kt_mark(h, KT_RN);
-            status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp);
+            // look-ahead: only the window part of Rn is on the chain to the next panel
+            status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0,
+                                      &cur->kp, &cur->c1, PW, lookahead ? 1 : 0);
             kt_mark(h, KT_RN);
             if (status != GBLA_OK) break;
             if (!lookahead) {
@@ -1176,15 +1207,21 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 if (status != GBLA_OK) break;
                 k_commit2<<<h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 1);
                 note_launch();
+                p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
                     break;
                 }
                 tmark(k, side);
-                factor(side, k + 1);
+                p_factor(side, k + 1);
                 tmark(k, side);
                 if (cudaEventRecord(evB, side) != cudaSuccess) { fail("event"); break; }
                 tmark(k, st);
+                kt_mark(h, KT_RN);
+                status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0,
+                                          &cur->kp, &cur->c1, PW, 2);
+                kt_mark(h, KT_RN);
+                if (status != GBLA_OK) break;
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid);
                 kt_mark(h, KT_TRAIL);
@@ -1193,6 +1230,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 note_launch();
                 tmark(k, st);
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
+                p_gather(st, k + 1);
+                tmark(k, st);
             }
             if (cudaGetLastError() != cudaSuccess) { fail("launch"); break; }
         }
@@ -1220,27 +1259,20 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         }
     }
     if (status == GBLA_OK && cudaStreamSynchronize(st) != cudaSuccess) fail("sync");
-    for (int q = 0; q < 2; q++)
-        if (bev[q]) cudaEventDestroy(bev[q]);
-    if (side) {
-        cudaStreamSynchronize(side);
-        cudaStreamDestroy(side);
-    }
+
+    if (side) cudaStreamSynchronize(side);
     if (!tl.empty()) {
         cudaDeviceSynchronize();
-        // per iteration: [start(main), side start, side end, rest start(main), rest end(main)]
-        for (size_t i = 0; i + 5 <= tl.size(); i += 5) {
-            float a[5];
-            for (int j = 0; j < 5; j++) cudaEventElapsedTime(&a[j], tl[0], tl[i + j]);
-            fprintf(stderr, "[gbla timeline] it %zu: start %.1f  side %.1f..%.1f (%.1f us)  rest %.1f..%.1f (%.1f us)\n",
-                    i / 5, a[0] * 1e3, a[1] * 1e3, a[2] * 1e3, (a[2] - a[1]) * 1e3, a[3] * 1e3, a[4] * 1e3,
-                    (a[4] - a[3]) * 1e3);
+        // per iteration (us from its start): side panel start, end; main rest start, end; gather end
+        for (size_t i = 0; i + 6 <= tl.size(); i += 6) {
+            float a[6];
+            for (int j = 0; j < 6; j++) cudaEventElapsedTime(&a[j], tl[i], tl[i + j]);
+            fprintf(stderr, "[gbla timeline] it %zu: panel %.1f..%.1f (%.1f) | rest %.1f..%.1f | gather done %.1f\n",
+                    i / 6, a[1] * 1e3, a[2] * 1e3, (a[2] - a[1]) * 1e3, a[3] * 1e3, a[4] * 1e3, a[5] * 1e3);
         }
         for (cudaEvent_t e : tl) cudaEventDestroy(e);
     }
-    if (evA) cudaEventDestroy(evA);
-    if (evB) cudaEventDestroy(evB);
-    if (c1_host) cudaFreeHost(c1_host);
+
     if (trace && status == GBLA_OK) {   // diagnostics: mean cycles per phase over the panels that ran
         unsigned long long tr[16];
         GBLA_CUDA_TRY(cudaMemcpy(tr, trace, sizeof tr, cudaMemcpyDeviceToHost));
@@ -1282,6 +1314,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
     const int64_t npad = (nN + 63) / 64 * 64 + 64;
     const int nloc = real ? 1 : G;                     // ranks handled by this process
+    const int pcap = panel_cap();
     auto rank_of = [&](int j) { return real ? me : j; };
     uint8_t *owner;
     uint32_t *rows, *lead, *hbuf, *ghist, *wdev, *cnt, *buf32, *bsum;
@@ -1327,8 +1360,8 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
         attr = true;
     }
-    uint32_t *hpin = nullptr;                          // [0..3) width info, [4..4+G) candidate counts
-    GBLA_CUDA_TRY(cudaMallocHost(&hpin, (8 + (size_t)G) * 4));
+    uint32_t *hpin = (uint32_t *)ctx_pinned(h->ctx, (8 + (size_t)G) * 4);   // width info, candidate counts
+    if (!hpin) { set_error("pinned host scratch"); return GBLA_E_CUDA; }
     gbla_status status = GBLA_OK;
     const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
                                                                             : 4u * h->ctx->sm_count;
@@ -1351,7 +1384,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
             k_sum_u32<<<2, 256, 0, st>>>(PW, G, hbuf, PW, ghist);
             note_launch();
         }
-        k_width<<<1, 1, 0, st>>>(nN, ghist, prev, wdev);
+        k_width<<<1, 1, 0, st>>>(nN, ghist, prev, wdev, pcap);
         GBLA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (G + 1) * 4, st));
         GBLA_CUDA_TRY(cudaMemcpyAsync(hpin, wdev, 12, cudaMemcpyDeviceToHost, st));
         GBLA_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1397,7 +1430,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
             }
         }
         // the same panel factorization on every rank
-        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1};
+        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap};
         kt_mark(h, KT_PANEL);
         k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr);
         kt_mark(h, KT_PANEL);
@@ -1417,8 +1450,8 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         k_gather_st32<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, cur, bsum, ldb, Blo, Bhi);
         note_launch();
         kt_mark(h, KT_RN);
-        if ((status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp)) !=
-            GBLA_OK)
+        if ((status = modgemm_tc_store(st, nN, h->F, Tlo, Thi, Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0, &cur->kp,
+                                       nullptr, 0, 0)) != GBLA_OK)
             break;
         kt_mark(h, KT_RN);
         // K11 on own rows (emulated: every rank's rows in one list), own S rows = Rn
@@ -1438,7 +1471,6 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         }
         if (cudaGetLastError() != cudaSuccess) { set_error("distributed echelon: launch failed"); status = GBLA_E_CUDA; }
     }
-    cudaFreeHost(hpin);
     if (status != GBLA_OK) return status;
     // op counts: the trailing updates were split over the ranks
     if (real) GBLA_TRY(dist_allreduce_u64(h, dops, 1));

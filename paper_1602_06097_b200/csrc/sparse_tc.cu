@@ -322,70 +322,97 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
         const uint32_t nI = l1 - lb;
+        // this thread's row of C_J, loaded now (off the chain): the epilogue needs it when S is ready
+        const uint8_t *ct = Xrow + (size_t)J * TB;
+        uint4 cpl[8], cph[8];
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const uint32_t o = tc::toff(tid, c * 16);
+            cpl[c] = *reinterpret_cast<const uint4 *>(ct + o);
+            cph[c] = *reinterpret_cast<const uint4 *>(ct + PB + o);
+        }
+        // exactness: one TMEM accumulation covers at most ACC_PAIRS tile pairs (K = 128 each):
+        // limb sums <= 2 * K * 255^2 < 2^31 for K <= 16,512; longer lists (unbanded A) are folded
+        // into the C_J row (mod p) every ACC_PAIRS pairs
+        constexpr uint32_t ACC_PAIRS = 128;
+        auto fold = [&](bool to_ys) {
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                uint64_t S[16];
+                read_S(lane_addr, c * 16, S);
+                uint8_t *cl = reinterpret_cast<uint8_t *>(&cpl[c]), *ch = reinterpret_cast<uint8_t *>(&cph[c]);
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t cv = cl[j] | (ch[j] << 8);
+                    const uint32_t sv = fmod64(S[j], a.F);
+                    const uint32_t y = cv >= sv ? cv - sv : cv + p - sv;
+                    cl[j] = (uint8_t)(y & 0xff);
+                    ch[j] = (uint8_t)(y >> 8);
+                }
+                if (to_ys) {
+                    const uint32_t o = tc::toff(tid, c * 16);
+                    *reinterpret_cast<uint4 *>(Ys + o) = cpl[c];
+                    *reinterpret_cast<uint4 *>(Ys + PB + o) = cph[c];
+                }
+            }
+        };
+        auto load = [&](uint32_t it) {                 // thread 0 only
+            const uint32_t I = a.jl_idx[lb + it];
+            const int s = it % NSTAGE;
+            tc::mbar_expect_tx(&full[s], 2 * TB);
+            tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
+            // X_I[T] is produced by task (li, I): wait until it is published
+            if (ld_acquire(fl + I) == 0) {
+                while (ld_acquire(fl + I) == 0) __nanosleep(64);
+            }
+            fence_proxy_async_global();
+            tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
+        };
         if (tid == 0) {
             tc::mbar_expect_tx(&invbar, TB);
             tc::bulk_g2s(INV, a.invT + (size_t)J * TB, TB, &invbar);
-            auto load = [&](uint32_t it) {
-                const uint32_t I = a.jl_idx[lb + it];
-                const int s = it % NSTAGE;
-                tc::mbar_expect_tx(&full[s], 2 * TB);
-                tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
-                // X_I[T] is produced by task (li, I): wait until it is published
-                if (ld_acquire(fl + I) == 0) {
-                    while (ld_acquire(fl + I) == 0) __nanosleep(64);
-                }
-                fence_proxy_async_global();
-                tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
-            };
             for (uint32_t it = 0; it < nI && it < (uint32_t)NSTAGE; it++) load(it);
-            for (uint32_t it = 0; it < nI; it++) {
-                const int s = it % NSTAGE;
-                tc::mbar_wait(&full[s], ph_full[s]);
-                ph_full[s] ^= 1;
-                tc::fence_after();
-                issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > 0);
-                if (it + NSTAGE < nI) tc::commit(&mdone[s]);     // stage s is reloaded for it + NSTAGE
-                // refill the stage of the previous iteration once its MMAs are done
-                if (it >= 1 && it - 1 + NSTAGE < nI) {
-                    const int sp = (it - 1) % NSTAGE;
-                    tc::mbar_wait(&mdone[sp], ph_md[sp]);
-                    ph_md[sp] ^= 1;
-                    load(it - 1 + NSTAGE);
-                }
-            }
-            if (nI > 0) tc::commit(&accbar);
         }
-        if (nI > 0) {
+        for (uint32_t c0 = 0; c0 < nI; c0 += ACC_PAIRS) {
+            const uint32_t c1 = c0 + ACC_PAIRS < nI ? c0 + ACC_PAIRS : nI;
+            if (tid == 0) {
+                for (uint32_t it = c0; it < c1; it++) {
+                    const int s = it % NSTAGE;
+                    tc::mbar_wait(&full[s], ph_full[s]);
+                    ph_full[s] ^= 1;
+                    tc::fence_after();
+                    issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > c0);
+                    if (it + NSTAGE < nI) tc::commit(&mdone[s]);     // stage s is reloaded for it + NSTAGE
+                    // refill the stage of the previous iteration once its MMAs are done
+                    if (it >= 1 && it - 1 + NSTAGE < nI) {
+                        const int sp = (it - 1) % NSTAGE;
+                        tc::mbar_wait(&mdone[sp], ph_md[sp]);
+                        ph_md[sp] ^= 1;
+                        load(it - 1 + NSTAGE);
+                    }
+                }
+                tc::commit(&accbar);
+            }
             tc::mbar_wait(&accbar, ph_acc);
             ph_acc ^= 1;
             tc::fence_after();
+            if (c1 < nI) {                       // fold this chunk into the C_J row, free the accumulator
+                fold(false);
+                tc::fence_before();
+                __syncthreads();
+                tc::fence_after();
+            }
         }
-        // epilogue 1: Y = C_J - S -> shared memory (A operand of stage 2); C_J row from the tile itself
-        const uint8_t *ct = Xrow + (size_t)J * TB;
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 16) {
-            uint64_t S[16];
-            if (nI > 0) {
-                read_S(lane_addr, c, S);
-            } else {
+        // epilogue 1: Y = C_J - S -> shared memory (A operand of stage 2)
+        if (nI > 0) {
+            fold(true);
+        } else {
 #pragma unroll
-                for (int j = 0; j < 16; j++) S[j] = 0;
+            for (int c = 0; c < 8; c++) {
+                const uint32_t o = tc::toff(tid, c * 16);
+                *reinterpret_cast<uint4 *>(Ys + o) = cpl[c];
+                *reinterpret_cast<uint4 *>(Ys + PB + o) = cph[c];
             }
-            const uint32_t o = tc::toff(tid, c);
-            uint4 clo = *reinterpret_cast<const uint4 *>(ct + o);
-            uint4 chi = *reinterpret_cast<const uint4 *>(ct + PB + o);
-            const uint8_t *cl = reinterpret_cast<const uint8_t *>(&clo), *ch = reinterpret_cast<const uint8_t *>(&chi);
-            uint8_t lo8[16], hi8[16];
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint32_t cv = cl[j] | (ch[j] << 8);
-                const uint32_t sv = fmod64(S[j], a.F);
-                const uint32_t y = cv >= sv ? cv - sv : cv + p - sv;
-                lo8[j] = (uint8_t)(y & 0xff);
-                hi8[j] = (uint8_t)(y >> 8);
-            }
-            *reinterpret_cast<uint4 *>(Ys + o) = *reinterpret_cast<uint4 *>(lo8);
-            *reinterpret_cast<uint4 *>(Ys + PB + o) = *reinterpret_cast<uint4 *>(hi8);
         }
         tc::fence_async_smem();
         tc::fence_before();
@@ -494,57 +521,68 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     const uint32_t tbase = tmem_s;
     const uint32_t sStg = tc::smem_u32(smem);
     const uint8_t *Xrow = a.Xt + (size_t)blockIdx.y * a.NB * TB;
+    uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0}, ph_acc = 0;   // thread 0 / all
+    auto load = [&](uint32_t it) {                     // thread 0 only
+        const uint32_t I = a.kl_idx[lb + it];
+        const int s = it & 1;
+        tc::mbar_expect_tx(&full[s], 2 * TB);
+        tc::bulk_g2s(smem + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
+        tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + (a.offB[I] + (uint64_t)(K - a.bmin[I])) * TB, TB, &full[s]);
+    };
     if (tid == 0) {
-        uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0};
-        auto load = [&](uint32_t it) {
-            const uint32_t I = a.kl_idx[lb + it];
-            const int s = it & 1;
-            tc::mbar_expect_tx(&full[s], 2 * TB);
-            tc::bulk_g2s(smem + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
-            tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + (a.offB[I] + (uint64_t)(K - a.bmin[I])) * TB, TB,
-                         &full[s]);
-        };
         load(0);
         if (nI > 1) load(1);
-        for (uint32_t it = 0; it < nI; it++) {
-            const int s = it & 1;
-            tc::mbar_wait(&full[s], ph_full[s]);
-            ph_full[s] ^= 1;
-            tc::fence_after();
-            issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > 0);
-            if (it + 2 < nI) {
-                tc::commit(&mdone[s]);
-                tc::mbar_wait(&mdone[s], ph_md[s]);
-                ph_md[s] ^= 1;
-                load(it + 2);
-            }
-        }
-        tc::commit(&accbar);
     }
-    tc::mbar_wait(&accbar, 0);
-    tc::fence_after();
     const int64_t slot = first + tid;
     const bool live = slot < a.mN;
     uint16_t *drow = live ? a.D + (size_t)a.order[slot] * a.ldD + K * 128 : nullptr;
     const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
     const uint32_t p = a.F.p;
-#pragma unroll 1
-    for (int c = 0; c < 128; c += 16) {
-        uint64_t S[16];
-        read_S(lane_addr, c, S);
-        if (!live) continue;
-        uint4 v[2];
-        v[0] = *reinterpret_cast<const uint4 *>(drow + c);
-        v[1] = *reinterpret_cast<const uint4 *>(drow + c + 8);
-        uint16_t *d = reinterpret_cast<uint16_t *>(v);
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const uint32_t s = fmod64(S[j], a.F);
-            const uint32_t x = d[j];
-            d[j] = (uint16_t)(x >= s ? x - s : x + p - s);
+    // one TMEM accumulation covers at most 128 tile pairs (K <= 16,384: exact s32 limb sums);
+    // longer lists (unbanded B) subtract each chunk from D
+    constexpr uint32_t ACC_PAIRS = 128;
+    for (uint32_t c0 = 0; c0 < nI; c0 += ACC_PAIRS) {
+        const uint32_t c1 = c0 + ACC_PAIRS < nI ? c0 + ACC_PAIRS : nI;
+        if (tid == 0) {
+            for (uint32_t it = c0; it < c1; it++) {
+                const int s = it & 1;
+                tc::mbar_wait(&full[s], ph_full[s]);
+                ph_full[s] ^= 1;
+                tc::fence_after();
+                issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > c0);
+                if (it + 2 < nI) {
+                    tc::commit(&mdone[s]);
+                    tc::mbar_wait(&mdone[s], ph_md[s]);
+                    ph_md[s] ^= 1;
+                    load(it + 2);
+                }
+            }
+            tc::commit(&accbar);
         }
-        *reinterpret_cast<uint4 *>(drow + c) = v[0];
-        *reinterpret_cast<uint4 *>(drow + c + 8) = v[1];
+        tc::mbar_wait(&accbar, ph_acc);
+        ph_acc ^= 1;
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 16) {
+            uint64_t S[16];
+            read_S(lane_addr, c, S);
+            if (!live) continue;
+            uint4 v[2];
+            v[0] = *reinterpret_cast<const uint4 *>(drow + c);
+            v[1] = *reinterpret_cast<const uint4 *>(drow + c + 8);
+            uint16_t *d = reinterpret_cast<uint16_t *>(v);
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t s = fmod64(S[j], a.F);
+                const uint32_t x = d[j];
+                d[j] = (uint16_t)(x >= s ? x - s : x + p - s);
+            }
+            *reinterpret_cast<uint4 *>(drow + c) = v[0];
+            *reinterpret_cast<uint4 *>(drow + c + 8) = v[1];
+        }
+        tc::fence_before();
+        __syncthreads();                               // accumulator free for the next chunk
+        tc::fence_after();
     }
     tc::fence_before();
     __syncthreads();
@@ -654,6 +692,7 @@ static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
     const int64_t per_tile = h->bt->NB * (int64_t)TB;
     const char *e = getenv("GBLA_XT_BATCH");          // tests: force small batches
     if (e && atoll(e) > 0) return atoll(e) < nl ? atoll(e) : nl;
+    if (nl * per_tile <= ((int64_t)8 << 30)) return nl;   // small: no need to ask the driver
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
     const int64_t reserve = (int64_t)4 << 30;

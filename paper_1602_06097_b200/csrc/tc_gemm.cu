@@ -29,6 +29,8 @@
 //   MODE_SUB    C[rowidx[i], x] = C - S   mod p     (trailing update)
 //   MODE_STORE  O[i, x] = S mod p, plus O's limb planes as B tiles
 //               (the B operand of a following MODE_SUB GEMM)
+#include <stdlib.h>
+
 #include "internal.cuh"
 #include "tc.cuh"
 
@@ -71,9 +73,8 @@ struct MMArgs {
 };
 
 constexpr int NSB = 4;                               // B stages
-constexpr int EPI_WARPS = 16;                        // 4 per TMEM lane quarter, 16 columns each
-constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
-constexpr int WS_THREADS = 64 + 32 * EPI_WARPS;      // producer, MMA, epilogue warps
+// epilogue warps: 8 (2 per TMEM lane quarter, 32 columns each) or 16 (4 per quarter, 16 columns)
+constexpr int ws_threads(int epiw) { return 64 + 32 * epiw; }   // producer, MMA, epilogue warps
 constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB: one CTA per SM)
 
 // Warp-specialized persistent K11: warp 0 stages operands (A tile once per row
@@ -83,9 +84,10 @@ constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB:
 // the 64 columns each), so loads, MMAs and the epilogue of consecutive tiles
 // overlap.  Each CTA owns a contiguous range of output tiles in row-tile-major
 // order (A reuse).
-template <int MODE>
-__global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
+template <int MODE, int EPI_WARPS>
+__global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs g)
 {
+    constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t afull[2], aempty[2], bfull[NSB], bempty[NSB], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
@@ -213,30 +215,44 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_modgemm_ws(MMArgs g)
         const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && (g.ldc % 8 == 0);
         uint32_t tph[2] = {0, 0};
         int ab = 0;
-        for (int64_t tile = t_begin; tile < t_end; tile++) {
+        // C row segments are fetched one tile ahead (two tiles of loads in flight per warp)
+        uint32_t dn[EPI_COLS / 2];
+        uint16_t *crow_n = nullptr;
+        bool fast_n = false, live_n = false;
+        int64_t x0_n = 0, slot_n = 0;
+        auto fetch = [&](int64_t tile) {
             const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
-            const int64_t row0 = rt * BM, x0 = ct * BN + part * EPI_COLS;
-            const int64_t slot = row0 + quarter * 32 + lane;
-            const bool live = slot < nr;
-            uint16_t *crow = nullptr;
-            if (live) crow = C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot] : slot) * g.ldc + x0;
-            const bool fast = live && vec && x0 + EPI_COLS <= cols;
-            uint32_t dv[EPI_COLS / 2];
+            x0_n = ct * BN + part * EPI_COLS;
+            slot_n = rt * BM + quarter * 32 + lane;
+            live_n = slot_n < nr;
+            crow_n = nullptr;
+            if (live_n) crow_n = C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc + x0_n;
+            fast_n = live_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
-            for (int w = 0; w < EPI_COLS / 2; w++) dv[w] = 0;
-            if (MODE == MODE_SUB && live) {          // prefetch the C row segment before waiting
-                if (fast) {
+            for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
+            if (MODE == MODE_SUB && live_n) {
+                if (fast_n) {
 #pragma unroll
                     for (int u = 0; u < EPI_COLS / 8; u++) {
-                        const uint4 q = reinterpret_cast<const uint4 *>(crow)[u];
-                        dv[4 * u] = q.x; dv[4 * u + 1] = q.y; dv[4 * u + 2] = q.z; dv[4 * u + 3] = q.w;
+                        const uint4 q = reinterpret_cast<const uint4 *>(crow_n)[u];
+                        dn[4 * u] = q.x; dn[4 * u + 1] = q.y; dn[4 * u + 2] = q.z; dn[4 * u + 3] = q.w;
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < EPI_COLS; j++)
-                        if (x0 + j < cols) dv[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
+                        if (x0_n + j < cols) dn[j / 2] |= (uint32_t)crow_n[j] << (16 * (j & 1));
                 }
             }
+        };
+        fetch(t_begin);
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            uint32_t dv[EPI_COLS / 2];
+#pragma unroll
+            for (int w = 0; w < EPI_COLS / 2; w++) dv[w] = dn[w];
+            uint16_t *crow = crow_n;
+            const bool fast = fast_n, live = live_n;
+            const int64_t x0 = x0_n, slot = slot_n;
+            if (tile + 1 < t_end) fetch(tile + 1);
             tc::mbar_wait(&tfull[ab], tph[ab]);
             tph[ab] ^= 1;
             tc::fence_after();
@@ -333,13 +349,37 @@ __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, const ui
     hi[o] = (uint8_t)(v >> 8);
 }
 
-template <int MODE>
+template <int MODE, int EPIW>
 gbla_status set_attr()
 {
     static bool attr = false;
     if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           WS_SMEM));
         attr = true;
+    }
+    return GBLA_OK;
+}
+
+static int epi_warps()
+{
+    static int w = -1;
+    if (w < 0) {
+        const char *e = getenv("GBLA_EPI_WARPS");
+        w = (e && atoi(e) == 16) ? 16 : 8;
+    }
+    return w;
+}
+
+template <int MODE>
+static gbla_status launch_ws(const MMArgs &a, int64_t grid, cudaStream_t st)
+{
+    if (epi_warps() == 16) {
+        GBLA_TRY((set_attr<MODE, 16>()));
+        k_modgemm_ws<MODE, 16><<<(unsigned)grid, ws_threads(16), WS_SMEM, st>>>(a);
+    } else {
+        GBLA_TRY((set_attr<MODE, 8>()));
+        k_modgemm_ws<MODE, 8><<<(unsigned)grid, ws_threads(8), WS_SMEM, st>>>(a);
     }
     return GBLA_OK;
 }
@@ -356,14 +396,13 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
                            const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap)
 {
-    GBLA_TRY(set_attr<MODE_SUB>());
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
     const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
     int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
              c0_dev, nullptr, win_dev, win_w, ctsel};
-    k_modgemm_ws<MODE_SUB><<<(unsigned)grid, WS_THREADS, WS_SMEM, st>>>(a);
+    GBLA_TRY(launch_ws<MODE_SUB>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -371,15 +410,15 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
 
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev)
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
+                             int64_t win_w, int ctsel)
 {
-    GBLA_TRY(set_attr<MODE_STORE>());
     if (cols <= 0) return GBLA_OK;
     const int64_t tiles = (cols + BN - 1) / BN;
     int64_t grid = (tiles + 1) / 2;                       // two column tiles per CTA (TMEM double buffer)
     if (grid > g_sms) grid = g_sms;
-    MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev, nullptr, 0, CT_ALL};
-    k_modgemm_ws<MODE_STORE><<<(unsigned)grid, WS_THREADS, WS_SMEM, st>>>(a);
+    MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
+    GBLA_TRY(launch_ws<MODE_STORE>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;

@@ -201,6 +201,28 @@ def test_xt_batches(gb, ctx, monkeypatch):
     h.free()
 
 
+def test_long_accumulations_are_chunked(gb, ctx):
+    """Unbanded A|B with more than 128 blocks of 128 pivots: a target's block sweep and the D update
+    accumulate more than 128 tile pairs, which must be split into exact s32 chunks (K <= 16,384).
+    Sampled D_new rows (leftmost leads: the longest lists) against the oracle's Alg 2."""
+    import torch
+    cfg = gbla_gen.scaled(gbla_gen.CONFIGS["c3"], 0.42)
+    M = gbla_gen.f4_matrix(cfg)
+    S = oracle.splice(M)
+    assert (S.npiv + 127) // 128 > 129
+    rp, c, v = to_dev(M)
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+    gb.gbla_reduce_C(h, fused=True)
+    D = h.D()
+    ld = S.lead[S.nonpivot_row]
+    lead_sig = np.where(ld < M.n, S.sigma[np.minimum(ld, M.n - 1)], M.n)
+    t = np.sort(np.argsort(lead_sig, kind="stable")[:8])
+    dn, _, _ = oracle.dnew_rows(M, S, targets=t)
+    got = D.view(torch.int16)[torch.from_numpy(t).cuda().long()].cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, dn)
+    h.free()
+
+
 def test_echelon_without_lookahead(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     """The echelon's look-ahead (next panel on a side stream beside the rest of
     the trailing update) and the serial schedule give the same R."""
