@@ -20,15 +20,19 @@
 // conditional subtraction gives the canonical residue.
 struct Field {
     uint32_t p;
-    uint32_t pad;
+    uint32_t c16;      // 2^16 mod p (< 2^15 for every p < 2^16: p > 2^15 gives 2^16 - p, else < p)
     uint64_t m64;
+    uint32_t m32;      // floor((2^32 - 1) / p)
+    uint32_t pad;
 };
 
 static inline Field make_field(uint32_t p) {
     Field F;
     F.p = p;
-    F.pad = 0;
+    F.c16 = (uint32_t)(65536u % p);
     F.m64 = ~0ull / p;
+    F.m32 = 0xffffffffu / p;
+    F.pad = 0;
     return F;
 }
 
@@ -36,6 +40,22 @@ __device__ __forceinline__ uint32_t fmod64(uint64_t x, const Field &F) {
     uint64_t q = __umul64hi(x, F.m64);
     uint64_t r = x - q * (uint64_t)F.p;
     return (uint32_t)(r >= F.p ? r - F.p : r);
+}
+// v < 2^32 -> v mod p (32-bit Barrett: the quotient estimate is short by at most 1)
+__device__ __forceinline__ uint32_t fmod32(uint32_t v, const Field &F) {
+    const uint32_t r = v - __umulhi(v, F.m32) * F.p;
+    return r >= F.p ? r - F.p : r;
+}
+// S = 2^16 hh + 2^8 xx + ll mod p from the three u8-limb accumulators of a tensor-core product
+// (each < 2^31): with a, b, c = hh, xx, ll mod p, t = a c16 + 256 b + c < 2^31 + 2^24 + 2^16 < 2^32
+// (a c16 < p 2^15 for p > 2^15, < p^2 < 2^30 otherwise), then t mod p.  32-bit arithmetic only.
+__device__ __forceinline__ uint32_t fmod_limbs(uint32_t hh, uint32_t xx, uint32_t ll, const Field &F) {
+    const uint32_t t = fmod32(hh, F) * F.c16 + (fmod32(xx, F) << 8) + fmod32(ll, F);
+    return fmod32(t, F);
+}
+// d - s mod p for two residues packed in 16-bit halves
+__device__ __forceinline__ uint32_t fsub2(uint32_t d, uint32_t s, uint32_t p2) {
+    return __vadd2(__vsub2(d, s), __vcmpltu2(d, s) & p2);
 }
 __device__ __forceinline__ uint32_t fmul(uint32_t a, uint32_t b, const Field &F) {
     return fmod64((uint64_t)a * b, F);

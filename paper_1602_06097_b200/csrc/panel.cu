@@ -1136,8 +1136,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     };
     auto p_gather = [&](cudaStream_t s, int64_t k) {
         P2State *cur = ps + (k & 1);
-        k_gather2<<<rgrid, 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1], rows[k & 1], nullptr,
-                                        0);
+        // one warp per row, blocks in row order: the row list (and the D rows of each 128-row tile
+        // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
+        k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
+                                                         rows[k & 1], nullptr, 0);
         note_launch();
     };
     auto factor = [&](cudaStream_t s, int64_t k) {
@@ -1456,7 +1458,8 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         kt_mark(h, KT_RN);
         // K11 on own rows (emulated: every rank's rows in one list), own S rows = Rn
         for (int j = 0; j < nloc; j++) {
-            k_gather2<<<rgrid, 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows, owner, rank_of(j));
+            k_gather2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows, owner,
+                                                              rank_of(j));
             note_launch();
         }
         kt_mark(h, KT_TRAIL);

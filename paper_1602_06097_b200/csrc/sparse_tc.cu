@@ -158,6 +158,19 @@ __device__ __forceinline__ void issue_mmas(uint32_t tbase, uint32_t sA, uint32_t
     }
 }
 
+// the accumulators of 16 columns reduced mod p (32-bit arithmetic, fmod_limbs)
+__device__ __forceinline__ void read_R(uint32_t lane_addr, int c, uint32_t (&R)[16], const Field &F)
+{
+    uint32_t hh[16], xx[16], ll[16];
+    __syncwarp();
+    tc::tmem_ld16(lane_addr + c, hh);
+    tc::tmem_ld16(lane_addr + 128 + c, xx);
+    tc::tmem_ld16(lane_addr + 256 + c, ll);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; j++) R[j] = fmod_limbs(hh[j], xx[j], ll[j], F);
+}
+
 __device__ __forceinline__ void read_S(uint32_t lane_addr, int c, uint64_t (&S)[16])
 {
     uint32_t hh[16], xx[16], ll[16];
@@ -338,13 +351,13 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         auto fold = [&](bool to_ys) {
 #pragma unroll
             for (int c = 0; c < 8; c++) {
-                uint64_t S[16];
-                read_S(lane_addr, c * 16, S);
+                uint32_t Rv[16];
+                read_R(lane_addr, c * 16, Rv, a.F);
                 uint8_t *cl = reinterpret_cast<uint8_t *>(&cpl[c]), *ch = reinterpret_cast<uint8_t *>(&cph[c]);
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
                     const uint32_t cv = cl[j] | (ch[j] << 8);
-                    const uint32_t sv = fmod64(S[j], a.F);
+                    const uint32_t sv = Rv[j];
                     const uint32_t y = cv >= sv ? cv - sv : cv + p - sv;
                     cl[j] = (uint8_t)(y & 0xff);
                     ch[j] = (uint8_t)(y >> 8);
@@ -433,13 +446,13 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 16) {
-            uint64_t S[16];
-            read_S(lane_addr, c, S);
+            uint32_t Rv[16];
+            read_R(lane_addr, c, Rv, a.F);
             uint8_t lo8[16], hi8[16];
             uint16_t xs[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                const uint32_t x = fmod64(S[j], a.F);
+                const uint32_t x = Rv[j];
                 lo8[j] = (uint8_t)(x & 0xff);
                 hi8[j] = (uint8_t)(x >> 8);
                 xs[j] = (uint16_t)x;
@@ -564,8 +577,8 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
         tc::fence_after();
 #pragma unroll 1
         for (int c = 0; c < 128; c += 16) {
-            uint64_t S[16];
-            read_S(lane_addr, c, S);
+            uint32_t Rv[16];
+            read_R(lane_addr, c, Rv, a.F);
             if (!live) continue;
             uint4 v[2];
             v[0] = *reinterpret_cast<const uint4 *>(drow + c);
@@ -573,7 +586,7 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
             uint16_t *d = reinterpret_cast<uint16_t *>(v);
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                const uint32_t s = fmod64(S[j], a.F);
+                const uint32_t s = Rv[j];
                 const uint32_t x = d[j];
                 d[j] = (uint16_t)(x >= s ? x - s : x + p - s);
             }

@@ -84,7 +84,7 @@ constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB:
 // the 64 columns each), so loads, MMAs and the epilogue of consecutive tiles
 // overlap.  Each CTA owns a contiguous range of output tiles in row-tile-major
 // order (A reuse).
-template <int MODE, int EPI_WARPS>
+template <int MODE, int EPI_WARPS, bool PF2>
 __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs g)
 {
     constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
@@ -220,13 +220,19 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
         uint16_t *crow_n = nullptr;
         bool fast_n = false, live_n = false;
         int64_t x0_n = 0, slot_n = 0;
+        int64_t rt_c = -1;                   // row tile whose C row this thread holds (row index cached:
+        uint16_t *rowbase = nullptr;         // a CTA's tiles are row-tile-major, so rt changes rarely)
         auto fetch = [&](int64_t tile) {
             const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
             x0_n = ct * BN + part * EPI_COLS;
             slot_n = rt * BM + quarter * 32 + lane;
             live_n = slot_n < nr;
-            crow_n = nullptr;
-            if (live_n) crow_n = C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc + x0_n;
+            if (rt != rt_c) {
+                rt_c = rt;
+                rowbase = live_n ? C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc
+                                 : nullptr;
+            }
+            crow_n = live_n ? rowbase + x0_n : nullptr;
             fast_n = live_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
             for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
@@ -252,7 +258,9 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             uint16_t *crow = crow_n;
             const bool fast = fast_n, live = live_n;
             const int64_t x0 = x0_n, slot = slot_n;
-            if (tile + 1 < t_end) fetch(tile + 1);
+            if (PF2) {
+                if (tile + 1 < t_end) fetch(tile + 1);
+            }
             tc::mbar_wait(&tfull[ab], tph[ab]);
             tph[ab] ^= 1;
             tc::fence_after();
@@ -266,14 +274,11 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
                 tc::tmem_wait_ld();
 #pragma unroll
                 for (int j = 0; j < 16; j += 2) {
-                    const uint32_t s0 = fmod64(((uint64_t)hh[j] << 16) + ((uint64_t)xx[j] << 8) + ll[j], g.F);
-                    const uint32_t s1 = fmod64(((uint64_t)hh[j + 1] << 16) + ((uint64_t)xx[j + 1] << 8) + ll[j + 1], g.F);
+                    const uint32_t s0 = fmod_limbs(hh[j], xx[j], ll[j], g.F);
+                    const uint32_t s1 = fmod_limbs(hh[j + 1], xx[j + 1], ll[j + 1], g.F);
                     const int w = (c + j) / 2;
                     if (MODE == MODE_SUB) {
-                        uint32_t lo = dv[w] & 0xffffu, hi = dv[w] >> 16;
-                        lo = lo >= s0 ? lo - s0 : lo + g.F.p - s0;
-                        hi = hi >= s1 ? hi - s1 : hi + g.F.p - s1;
-                        dv[w] = lo | (hi << 16);
+                        dv[w] = fsub2(dv[w], s0 | (s1 << 16), g.F.p | (g.F.p << 16));
                     } else {
                         dv[w] = s0 | (s1 << 16);
                         if (live) {
@@ -299,6 +304,9 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
 #pragma unroll
                 for (int j = 0; j < EPI_COLS; j++)
                     if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
+            }
+            if (!PF2) {
+                if (tile + 1 < t_end) fetch(tile + 1);
             }
         }
     }
@@ -349,13 +357,13 @@ __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, const ui
     hi[o] = (uint8_t)(v >> 8);
 }
 
-template <int MODE, int EPIW>
+template <int MODE, int EPIW, bool PF2>
 gbla_status set_attr()
 {
     static bool attr = false;
     if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           WS_SMEM));
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW, PF2>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
         attr = true;
     }
     return GBLA_OK;
@@ -371,17 +379,26 @@ static int epi_warps()
     return w;
 }
 
+static bool epi_pf2()
+{
+    static int v = -1;
+    if (v < 0) v = getenv("GBLA_EPI_PF1") ? 0 : 1;
+    return v == 1;
+}
+
+template <int MODE, int EPIW, bool PF2>
+static gbla_status launch_ws1(const MMArgs &a, int64_t grid, cudaStream_t st)
+{
+    GBLA_TRY((set_attr<MODE, EPIW, PF2>()));
+    k_modgemm_ws<MODE, EPIW, PF2><<<(unsigned)grid, ws_threads(EPIW), WS_SMEM, st>>>(a);
+    return GBLA_OK;
+}
+
 template <int MODE>
 static gbla_status launch_ws(const MMArgs &a, int64_t grid, cudaStream_t st)
 {
-    if (epi_warps() == 16) {
-        GBLA_TRY((set_attr<MODE, 16>()));
-        k_modgemm_ws<MODE, 16><<<(unsigned)grid, ws_threads(16), WS_SMEM, st>>>(a);
-    } else {
-        GBLA_TRY((set_attr<MODE, 8>()));
-        k_modgemm_ws<MODE, 8><<<(unsigned)grid, ws_threads(8), WS_SMEM, st>>>(a);
-    }
-    return GBLA_OK;
+    if (epi_warps() == 16) return epi_pf2() ? launch_ws1<MODE, 16, true>(a, grid, st) : launch_ws1<MODE, 16, false>(a, grid, st);
+    return epi_pf2() ? launch_ws1<MODE, 8, true>(a, grid, st) : launch_ws1<MODE, 8, false>(a, grid, st);
 }
 
 int g_sms = 148;
