@@ -266,25 +266,26 @@ __global__ void k_cfill(int64_t mN, int64_t NB, int64_t prank, int64_t pworld, i
 }
 
 constexpr int NSTAGE = 3;
-constexpr int SWEEP_SMEM = NSTAGE * 65536 + TB;   // 3 operand stages + inv(A_JJ); Y reuses stage 0
+constexpr int PART_LD = 128;                       // running partial of long lists: u16 [128][PART_LD]
+constexpr int SWEEP_SMEM = NSTAGE * 65536 + 128 * PART_LD * 2;   // 3 operand stages + the partial
 
-// K5': persistent, dependency-driven block forward substitution.  Every CTA
-// claims tasks (i, J) in J-major order from a global counter; a task
-// accumulates S = sum_I X_I[T] A_IJ over the band list of block J, waiting
-// for each X_I[T] to be published (flag) just before its operands are
-// staged, then X_J = (C_J - S) inv(A_JJ) is stored and published.  A task
-// only waits on tasks with smaller numbers, which were claimed earlier by
-// co-resident CTAs (cooperative launch), so the schedule cannot deadlock;
-// the chain of one tile costs one tile-pair GEMM + two epilogues per block
-// while the rest of each task's GEMMs run off the critical path, and the
-// A_IJ tiles of one J are shared in L2 by all tiles working on J.
+// K5': persistent, dependency-driven block forward substitution.  With the band
+// tiles pre-multiplied (k_ahat: Â_IJ = -A_IJ inv(A_JJ) mod p) the block step is
+//   X_J = C_J inv(A_JJ) + sum_I X_I Â_IJ      (mod p)
+// one accumulation of nI + 1 tile pairs and ONE epilogue.  Every CTA claims tasks
+// (i, J) in J-major order from a global counter; the pair (C_J, inv(A_JJ)) comes
+// first, then the X_I in ascending I, each waited for by its flag just before its
+// operands are staged.  A task only waits on tasks with smaller numbers, which were
+// claimed earlier by co-resident CTAs (cooperative launch), so the schedule cannot
+// deadlock.  Per 128-pivot block the chain of one target tile costs the last tile
+// pair + one epilogue + the flag hand-off; the A tiles of one J are shared in L2 by
+// all tiles working on J.
 __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stg = smem;
-    uint8_t *Ys = smem;                        // stage 0's X half, free once the accumulation is done
-    uint8_t *INV = smem + NSTAGE * 65536;
-    __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar, invbar;
+    uint16_t *prow = reinterpret_cast<uint16_t *>(smem + NSTAGE * 65536) + threadIdx.x * PART_LD;
+    __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar;
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t s_np[128], s_w[128];
     __shared__ uint32_t s_task;
@@ -293,18 +294,18 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&mdone[s], 1); }
         tc::mbar_init(&accbar, 1);
-        tc::mbar_init(&invbar, 1);
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_s;
     const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-    uint32_t ph_acc = 0, ph_inv = 0;
+    uint32_t ph_acc = 0;
     uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
     unsigned long long opsA = 0, opsB = 0;
-    const uint32_t sStg = tc::smem_u32(stg), sY = tc::smem_u32(Ys), sINV = tc::smem_u32(INV);
+    const uint32_t sStg = tc::smem_u32(stg);
     const uint32_t p = a.F.p;
+    uint32_t gpair = 0;                        // stage ring position, continuous across tasks (thread 0)
 
     for (;;) {
         if (tid == 0) s_task = atomicAdd(a.next, 1u);
@@ -334,74 +335,49 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
-        const uint32_t nI = l1 - lb;
-        // this thread's row of C_J, loaded now (off the chain): the epilogue needs it when S is ready
-        const uint8_t *ct = Xrow + (size_t)J * TB;
-        uint4 cpl[8], cph[8];
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            const uint32_t o = tc::toff(tid, c * 16);
-            cpl[c] = *reinterpret_cast<const uint4 *>(ct + o);
-            cph[c] = *reinterpret_cast<const uint4 *>(ct + PB + o);
-        }
-        // exactness: one TMEM accumulation covers at most ACC_PAIRS tile pairs (K = 128 each):
-        // limb sums <= 2 * K * 255^2 < 2^31 for K <= 16,512; longer lists (unbanded A) are folded
-        // into the C_J row (mod p) every ACC_PAIRS pairs
-        constexpr uint32_t ACC_PAIRS = 128;
-        auto fold = [&](bool to_ys) {
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                uint32_t Rv[16];
-                read_R(lane_addr, c * 16, Rv, a.F);
-                uint8_t *cl = reinterpret_cast<uint8_t *>(&cpl[c]), *ch = reinterpret_cast<uint8_t *>(&cph[c]);
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const uint32_t cv = cl[j] | (ch[j] << 8);
-                    const uint32_t sv = Rv[j];
-                    const uint32_t y = cv >= sv ? cv - sv : cv + p - sv;
-                    cl[j] = (uint8_t)(y & 0xff);
-                    ch[j] = (uint8_t)(y >> 8);
-                }
-                if (to_ys) {
-                    const uint32_t o = tc::toff(tid, c * 16);
-                    *reinterpret_cast<uint4 *>(Ys + o) = cpl[c];
-                    *reinterpret_cast<uint4 *>(Ys + PB + o) = cph[c];
-                }
-            }
-        };
-        auto load = [&](uint32_t it) {                 // thread 0 only
-            const uint32_t I = a.jl_idx[lb + it];
-            const int s = it % NSTAGE;
+        const uint32_t npair = l1 - lb + 1;            // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
+        // pair q into stage (gpair + q) % NSTAGE (thread 0 only)
+        auto load = [&](uint32_t q) {
+            const int s = (gpair + q) % NSTAGE;
+            uint8_t *sa = stg + s * 65536, *sb = sa + TB;
             tc::mbar_expect_tx(&full[s], 2 * TB);
-            tc::bulk_g2s(stg + s * 65536 + TB, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);
+            if (q == 0) {
+                tc::bulk_g2s(sb, a.invT + (size_t)J * TB, TB, &full[s]);
+                tc::bulk_g2s(sa, Xrow + (size_t)J * TB, TB, &full[s]);          // C_J (not yet overwritten)
+                return;
+            }
+            const uint32_t I = a.jl_idx[lb + q - 1];
+            tc::bulk_g2s(sb, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);   // Â_IJ
             // X_I[T] is produced by task (li, I): wait until it is published
             if (ld_acquire(fl + I) == 0) {
-                while (ld_acquire(fl + I) == 0) __nanosleep(64);
+                while (ld_acquire(fl + I) == 0) __nanosleep(32);
             }
             fence_proxy_async_global();
-            tc::bulk_g2s(stg + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
+            tc::bulk_g2s(sa, Xrow + (size_t)I * TB, TB, &full[s]);
         };
-        if (tid == 0) {
-            tc::mbar_expect_tx(&invbar, TB);
-            tc::bulk_g2s(INV, a.invT + (size_t)J * TB, TB, &invbar);
-            for (uint32_t it = 0; it < nI && it < (uint32_t)NSTAGE; it++) load(it);
-        }
-        for (uint32_t c0 = 0; c0 < nI; c0 += ACC_PAIRS) {
-            const uint32_t c1 = c0 + ACC_PAIRS < nI ? c0 + ACC_PAIRS : nI;
+        // exactness: one TMEM accumulation covers at most ACC_PAIRS tile pairs (K = 128 each):
+        // limb sums <= 2 K 255^2 < 2^31 for K <= 16,512; longer lists (unbanded A) are folded
+        // into a running partial (mod p) every ACC_PAIRS pairs
+        constexpr uint32_t ACC_PAIRS = 128;
+        bool have_partial = false;                     // running partial of this thread's row in prow
+        if (tid == 0)
+            for (uint32_t q = 0; q < npair && q < (uint32_t)NSTAGE; q++) load(q);
+        for (uint32_t c0 = 0; c0 < npair; c0 += ACC_PAIRS) {
+            const uint32_t c1 = c0 + ACC_PAIRS < npair ? c0 + ACC_PAIRS : npair;
             if (tid == 0) {
-                for (uint32_t it = c0; it < c1; it++) {
-                    const int s = it % NSTAGE;
+                for (uint32_t q = c0; q < c1; q++) {
+                    const int s = (gpair + q) % NSTAGE;
                     tc::mbar_wait(&full[s], ph_full[s]);
                     ph_full[s] ^= 1;
                     tc::fence_after();
-                    issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > c0);
-                    if (it + NSTAGE < nI) tc::commit(&mdone[s]);     // stage s is reloaded for it + NSTAGE
-                    // refill the stage of the previous iteration once its MMAs are done
-                    if (it >= 1 && it - 1 + NSTAGE < nI) {
-                        const int sp = (it - 1) % NSTAGE;
+                    issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, q > c0);
+                    if (q + NSTAGE < npair) tc::commit(&mdone[s]);     // stage s is reloaded for q + NSTAGE
+                    // refill the stage of the previous pair once its MMAs are done
+                    if (q >= 1 && q - 1 + NSTAGE < npair) {
+                        const int sp = (gpair + q - 1) % NSTAGE;
                         tc::mbar_wait(&mdone[sp], ph_md[sp]);
                         ph_md[sp] ^= 1;
-                        load(it - 1 + NSTAGE);
+                        load(q - 1 + NSTAGE);
                     }
                 }
                 tc::commit(&accbar);
@@ -409,65 +385,59 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
             tc::mbar_wait(&accbar, ph_acc);
             ph_acc ^= 1;
             tc::fence_after();
-            if (c1 < nI) {                       // fold this chunk into the C_J row, free the accumulator
-                fold(false);
+            if (c1 < npair) {                          // fold this chunk into the partial, free TMEM
+#pragma unroll 1
+                for (int c = 0; c < 128; c += 16) {
+                    uint32_t Rv[16];
+                    read_R(lane_addr, c, Rv, a.F);
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        uint32_t v = Rv[j];
+                        if (have_partial) {
+                            v += prow[c + j];
+                            v = v >= p ? v - p : v;
+                        }
+                        prow[c + j] = (uint16_t)v;
+                    }
+                }
+                have_partial = true;
                 tc::fence_before();
                 __syncthreads();
                 tc::fence_after();
             }
         }
-        // epilogue 1: Y = C_J - S -> shared memory (A operand of stage 2)
-        if (nI > 0) {
-            fold(true);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const uint32_t o = tc::toff(tid, c * 16);
-                *reinterpret_cast<uint4 *>(Ys + o) = cpl[c];
-                *reinterpret_cast<uint4 *>(Ys + PB + o) = cph[c];
-            }
-        }
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        // stage 2: X_J = Y inv(A_JJ)
-        if (tid == 0) {
-            tc::mbar_wait(&invbar, ph_inv);
-            tc::fence_after();
-            issue_mmas(tbase, sY, sINV, false);
-            tc::commit(&accbar);
-        }
-        ph_inv ^= 1;
-        tc::mbar_wait(&accbar, ph_acc);
-        ph_acc ^= 1;
-        tc::fence_after();
-        // epilogue 2: X_J -> limb-plane tile (global) [+ C' u16], op counts (Alg 2 count)
+        if (tid == 0) gpair = (gpair + npair) % NSTAGE;
+        // epilogue: X_J = S (+ partial) mod p -> limb-plane tile (global) [+ C' u16], op counts (Alg 2)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 16) {
+        for (int c8 = 0; c8 < 128; c8 += 16) {
+            const int c = c8 / 16;
             uint32_t Rv[16];
-            read_R(lane_addr, c, Rv, a.F);
+            read_R(lane_addr, c8, Rv, a.F);
             uint8_t lo8[16], hi8[16];
             uint16_t xs[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                const uint32_t x = Rv[j];
+                uint32_t x = Rv[j];
+                if (have_partial) {
+                    x += prow[c8 + j];
+                    x = x >= p ? x - p : x;
+                }
                 lo8[j] = (uint8_t)(x & 0xff);
                 hi8[j] = (uint8_t)(x >> 8);
                 xs[j] = (uint16_t)x;
                 if (x && live) {
-                    opsA += s_np[c + j] - 1;
-                    opsB += s_w[c + j] - s_np[c + j];
+                    opsA += s_np[c * 16 + j] - 1;
+                    opsB += s_w[c * 16 + j] - s_np[c * 16 + j];
                 }
             }
-            const uint32_t o = tc::toff(tid, c);
+            const uint32_t o = tc::toff(tid, c * 16);
             *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo8);
             *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi8);
             if (a.X16 && live) {
 #pragma unroll
                 for (int j = 0; j < 16; j++)
-                    if (jbase + c + j < (uint64_t)a.npiv) a.X16[(size_t)t * a.ldX + jbase + c + j] = xs[j];
+                    if (jbase + c * 16 + j < (uint64_t)a.npiv) a.X16[(size_t)t * a.ldX + jbase + c * 16 + j] = xs[j];
             }
         }
         fence_proxy_async_global();     // X_J is read by later tasks through the async proxy
@@ -489,6 +459,78 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     }
     tc::fence_before();
     __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+// Â_IJ = -A_IJ inv(A_JJ) mod p for every off-diagonal band tile, in place (same layout:
+// element (i, j) at toff(j, i)).  As a tcgen05 product D[j][i] = sum_k W[k][j] A_IJ[i][k]:
+// the stored inv(A_JJ) tile is the A operand as is (toff(j, k) holds W[k][j]); A_IJ is
+// transposed in shared memory into the B operand (toff(i, k) must hold A_IJ[i][k]).  The
+// epilogue thread j writes its 128 values at toff(j, i), negated.  One CTA per tile.
+__global__ void __launch_bounds__(128, 1) k_ahat(Field F, int64_t NB, const uint64_t *__restrict__ offA,
+                                                 const uint32_t *__restrict__ amax, const uint64_t *__restrict__ tile_I,
+                                                 int64_t ntile, uint8_t *__restrict__ tilesA,
+                                                 const uint8_t *__restrict__ invT)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *sW = smem, *sA = smem + TB, *sB = smem + 2 * TB;   // W (A operand), A_IJ raw, A_IJ^T (B operand)
+    __shared__ uint64_t bar, accbar;
+    __shared__ uint32_t tmem_s;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::mbar_init(&accbar, 1); }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tmem_s, lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
+    uint32_t ph = 0, pha = 0;
+    for (int64_t q = blockIdx.x; q < ntile; q += gridDim.x) {
+        const uint64_t code = tile_I[q];
+        const uint32_t I = (uint32_t)(code >> 32), J = (uint32_t)code;
+        uint8_t *tA = tilesA + (offA[I] + (uint64_t)(J - I)) * TB;
+        if (tid == 0) {
+            tc::mbar_expect_tx(&bar, 2 * TB);
+            tc::bulk_g2s(sW, invT + (size_t)J * TB, TB, &bar);
+            tc::bulk_g2s(sA, tA, TB, &bar);
+        }
+        tc::mbar_wait(&bar, ph);
+        ph ^= 1;
+        // transpose both limb planes: sB[toff(i, k)] = sA[toff(k, i)]
+        for (int pl = 0; pl < 2; pl++)
+            for (int e = tid; e < 128 * 128; e += 128) {
+                const uint32_t i = e >> 7, k = e & 127;
+                sB[pl * PB + tc::toff(i, k)] = sA[pl * PB + tc::toff(k, i)];
+            }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid == 0) {
+            issue_mmas(tbase, tc::smem_u32(sW), tc::smem_u32(sB), false);
+            tc::commit(&accbar);
+        }
+        tc::mbar_wait(&accbar, pha);
+        pha ^= 1;
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 16) {
+            uint32_t Rv[16];
+            read_R(lane_addr, c, Rv, F);
+            uint8_t lo8[16], hi8[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t v = Rv[j] ? F.p - Rv[j] : 0;
+                lo8[j] = (uint8_t)(v & 0xff);
+                hi8[j] = (uint8_t)(v >> 8);
+            }
+            const uint32_t o = tc::toff(tid, c);          // thread = j, columns c.. = i
+            *reinterpret_cast<uint4 *>(tA + o) = *reinterpret_cast<uint4 *>(lo8);
+            *reinterpret_cast<uint4 *>(tA + PB + o) = *reinterpret_cast<uint4 *>(hi8);
+        }
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
@@ -688,6 +730,29 @@ static gbla_status band_build(gbla_mat h)
     k_diag_inv<<<(unsigned)NB, 128, DIAG_SMEM, st>>>(h->F, bt->offA, bt->tilesA, bt->invT);
     note_launch(3);
     GBLA_CUDA_TRY(cudaGetLastError());
+    // Â_IJ = -A_IJ inv(A_JJ) for every off-diagonal band tile (the sweep's B operands)
+    {
+        std::vector<uint64_t> tl;
+        for (int64_t I = 0; I < NB; I++)
+            for (uint32_t J = (uint32_t)I + 1; J <= amax[I]; J++) tl.push_back(((uint64_t)I << 32) | J);
+        if (!tl.empty()) {
+            uint64_t *dtl;
+            GBLA_TRY(dalloc_t(h, tl.size(), &dtl));
+            GBLA_CUDA_TRY(cudaMemcpyAsync(dtl, tl.data(), tl.size() * 8, cudaMemcpyHostToDevice, st));
+            static bool attr2 = false;
+            if (!attr2) {
+                GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TB));
+                attr2 = true;
+            }
+            const int64_t nt = (int64_t)tl.size();
+            const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
+            k_ahat<<<(unsigned)grid, 128, 3 * TB, st>>>(h->F, NB, bt->offA, bt->amax, dtl, nt, bt->tilesA, bt->invT);
+            note_launch();
+            GBLA_CUDA_TRY(cudaGetLastError());
+            // the host list must outlive the async copy
+            GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+    }
     return GBLA_OK;
 }
 
