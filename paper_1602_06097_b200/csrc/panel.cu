@@ -34,6 +34,7 @@
 #include <stdlib.h>
 
 #include <functional>
+#include <utility>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -52,6 +53,24 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
 void modgemm_set_sms(int sms);
 
 namespace {
+
+// launch with programmatic dependent launch (the kernel calls pdl_trigger / pdl_wait): its launch
+// overlaps the tail of the previous kernel of the stream
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PK = 128;                 // pivots per panel = K of the trailing GEMM
@@ -122,6 +141,8 @@ __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, 
                         const uint32_t *__restrict__ rowpiv, const P2State *__restrict__ prev,
                         uint32_t *__restrict__ lead, const uint8_t *__restrict__ owner, int me)
 {
+    tc::pdl_trigger();
+    tc::pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t c0 = prev->c1;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
@@ -770,6 +791,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
                           const uint8_t *__restrict__ owner, int me)
 {
+    tc::pdl_trigger();
+    tc::pdl_wait();
     constexpr int CPL = PK / 32;
     const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
@@ -809,6 +832,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
 __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
                              const P2State *__restrict__ ps, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi)
 {
+    tc::pdl_trigger();
+    tc::pdl_wait();
     const uint32_t kp = ps->kp;
     if (kp == 0) return;
     const int64_t c0 = ps->c0;
@@ -839,6 +864,8 @@ __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, con
                           const uint16_t *__restrict__ Rn, int64_t ldR, unsigned long long *__restrict__ ops, int part,
                           const uint8_t *__restrict__ owner = nullptr, int me = 0)
 {
+    tc::pdl_trigger();
+    tc::pdl_wait();
     const uint32_t b = blockIdx.y;
     const uint32_t kp = ps->kp;
     const int64_t c0 = ps->c0;
@@ -1123,7 +1150,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                                                             : 4u * h->ctx->sm_count;
     auto p_lead = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1);
-        k_lead2<<<rgrid, 256, 0, s>>>(mN, nN, h->D, ldD, rowpiv, prev, lead, nullptr, 0);
+        launch_pdl(k_lead2, dim3(rgrid), dim3(256), 0, s, mN, nN, (const uint16_t *)h->D, ldD,
+                   (const uint32_t *)rowpiv, (const P2State *)prev, lead, (const uint8_t *)nullptr, 0);
         note_launch();
     };
     auto p_factor = [&](cudaStream_t s, int64_t k) {
@@ -1184,7 +1212,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             P2State *cur = ps + (k & 1);
             const int f = (int)(k & 1);
             tmark(k, st);
-            k_gather_st2<<<dim3(grid_for(nN, 128), PK / 16), 128, 0, st>>>(nN, h->D, ldD, cur, Blo, Bhi);
+            launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN, (const uint16_t *)h->D,
+                       ldD, (const P2State *)cur, Blo, Bhi);
             note_launch();
             kt_mark(h, KT_RN);
             // look-ahead: only the window part of Rn is on the chain to the next panel
@@ -1207,7 +1236,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid);
                 if (status != GBLA_OK) break;
-                k_commit2<<<h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 1);
+                launch_pdl(k_commit2, dim3(h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD, (const P2State *)cur,
+                           (const uint16_t *)Rn, ldR, dops, 1, (const uint8_t *)nullptr, 0);
                 note_launch();
                 p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
@@ -1228,7 +1258,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
-                k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 2);
+                launch_pdl(k_commit2, dim3(2 * h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD,
+                           (const P2State *)cur, (const uint16_t *)Rn, ldR, dops, 2, (const uint8_t *)nullptr, 0);
                 note_launch();
                 tmark(k, st);
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }

@@ -122,6 +122,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
+// programmatic dependent launch: let the next kernel of the stream start launching, and wait
+// for the previous kernel's completion (and memory) before touching its results.  No-ops when
+// the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // order generic-proxy writes before later async-proxy (bulk copy / tensor core) reads
 __device__ __forceinline__ void fence_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 

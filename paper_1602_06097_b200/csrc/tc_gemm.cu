@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t afull[2], aempty[2], bfull[NSB], bempty[NSB], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
+    tc::pdl_trigger();
+    tc::pdl_wait();
     if (g.skip_dev && *g.skip_dev == 0) return;
     int64_t cols = g.cols, c0 = 0;
     uint16_t *C = g.C;
@@ -390,7 +392,18 @@ template <int MODE, int EPIW, bool PF2>
 static gbla_status launch_ws1(const MMArgs &a, int64_t grid, cudaStream_t st)
 {
     GBLA_TRY((set_attr<MODE, EPIW, PF2>()));
-    k_modgemm_ws<MODE, EPIW, PF2><<<(unsigned)grid, ws_threads(EPIW), WS_SMEM, st>>>(a);
+    // programmatic dependent launch: the GEMM's launch overlaps the tail of the previous kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(ws_threads(EPIW));
+    cfg.dynamicSmemBytes = WS_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    GBLA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_modgemm_ws<MODE, EPIW, PF2>, a));
     return GBLA_OK;
 }
 
