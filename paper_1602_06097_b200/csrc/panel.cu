@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                     else coll = 1;                              // eliminated next round
                 }
             }
-            coll = __syncthreads_or(coll);
+            coll = __syncthreads_count(coll);               // rows that lost their column this round
             for (int ci = warp; ci < ncand; ci += 32) {
                 const uint32_t q = freel[ci];
                 if (cstat[q] != 4) continue;
@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // sum over the list of W[b][row] * value.
             constexpr int LMAX = 8;
             uint32_t *lcnt = clead;                               // per physical column (clead is dead)
+            uint16_t *lrow = &FS[0][0], *lval = &FS[0][0] + LMAX * PK;   // [LMAX][PK] each (U is dead)
             for (int k = tid; k < PK; k += NT) lcnt[k] = 0;
             __syncthreads();
             for (int b2 = warp; b2 < (int)nb; b2 += 32) {        // warp per head row: contiguous E row
@@ -623,10 +624,9 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                     const uint32_t e = X[q2 * LDX + PW + sc];
                     if (!e) continue;
                     const uint32_t j = atomicAdd(&lcnt[sc], 1u);
-                    if (j < (uint32_t)LMAX) {
-                        uint16_t *lst = X + sc * LDX + 2 * PK;   // [0, LMAX) rows, [LMAX, 2 LMAX) values
-                        lst[j] = (uint16_t)b2;
-                        lst[LMAX + j] = (uint16_t)mod32(e * hv, p, m32);
+                    if (j < (uint32_t)LMAX) {                     // transposed lists: lanes read
+                        lrow[j * PK + sc] = (uint16_t)b2;         // different columns, not one bank
+                        lval[j * PK + sc] = (uint16_t)mod32(e * hv, p, m32);
                     }
                 }
             }
@@ -636,13 +636,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 uint32_t v = 0;
                 if (b < (int)nb && ls < (int)nb) {
                     const uint32_t sc = bphys[ls];
-                    const uint16_t *lst = X + sc * LDX + 2 * PK;
                     const uint32_t cnt = lcnt[sc];
                     uint64_t acc = 0;
                     if (cnt <= (uint32_t)LMAX) {
                         for (uint32_t j = 0; j < cnt; j++) {
-                            const uint32_t b2 = lst[j];
-                            if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lst[LMAX + j];
+                            const uint32_t b2 = lrow[j * PK + sc];
+                            if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lval[j * PK + sc];
                         }
                     } else {                                      // dense column: every head row
                         for (int b2 = b; b2 < (int)nb; b2++) {
