@@ -303,17 +303,23 @@ def main():
         (npiv, mN, nN), rk = rank_d
         h2d = M.row_ptr.nbytes + M.col.nbytes + M.val.nbytes
         d2h = rk * nN * 2 + rk * 4
+        # results land in pinned host buffers (allocated once, outside the timed region)
+        out_pc = torch.empty(max(rk, 1), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        out_R = torch.empty((max(rk, 1), max(nN, 1)), dtype=torch.int16).pin_memory().numpy().view(np.uint16)
         e_ms = []
+        gc.collect()
+        gc.disable()
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             h = gb.gbla_reduce(ctx, M.m, M.n, hn[0], hn[1], hn[2], M.p, flags=args.flags, stream=stream)
-            r, pc_h, R_h = h.rref_to_host(stream=stream)
+            r, pc_h, R_h = h.rref_to_host(stream=stream, out=(out_pc, out_R))
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) * 1e3
             h.free()
             if i > 0:
                 e_ms.append(dt)
+        gc.enable()
         em = statistics.mean(e_ms)
         if world > 1:
             t = torch.tensor([em], device="cuda", dtype=torch.float64)

@@ -268,14 +268,20 @@ class Mat:
         r = rk.value
         return r, _view(pc.value, (r,), "<u4").clone(), _view(R.value, (r, nN), "<u2", ld.value, 2).clone()
 
-    def rref_to_host(self, stream=None):
-        """(rank, pivcol, R) copied to host numpy arrays by the library."""
+    def rref_to_host(self, stream=None, out=None):
+        """(rank, pivcol, R) copied to host numpy arrays by the library.  `out` = (pivcol, R)
+        host arrays to fill (e.g. views of pinned buffers), at least rank and rank x nN."""
         npiv, mN, nN = self.dims()
         rk = ctypes.c_int64()
         _check(_lib.gbla_get_rref(self._h, ctypes.byref(rk), None, None, None))
         r = rk.value
-        pc = np.zeros(max(r, 1), np.uint32)
-        R = np.zeros((max(r, 1), max(nN, 1)), np.uint16)
+        if out is not None:
+            pc, R = out
+            if pc.size < r or R.shape[0] < r or R.shape[1] != max(nN, 1) or not R.flags.c_contiguous:
+                raise ValueError("rref_to_host: output buffers too small or not contiguous rank x nN")
+        else:
+            pc = np.zeros(max(r, 1), np.uint32)
+            R = np.zeros((max(r, 1), max(nN, 1)), np.uint16)
         _check(_lib.gbla_copy_rref_to_host(self._h, pc.ctypes.data_as(ctypes.c_void_p),
                                            R.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
         return r, pc[:r], R[:r, :nN]

@@ -11,8 +11,8 @@ import subprocess
 import sys
 
 FAMILIES = [("k_sweep", "sweep"), ("k_update_tc", "update"), ("k_panel", "panel"),
-            ("k_modgemm_tc<0>", "trailing"), ("k_modgemm_tc<1>", "rnew"), ("k_trail", "trailing"),
-            ("k_rnew_tc", "rnew")]
+            ("k_modgemm_tc<0>", "trailing"), ("k_modgemm_tc<1>", "rnew"), ("k_modgemm_ws<0", "trailing"),
+            ("k_modgemm_ws<1", "rnew")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 TSCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
 
@@ -24,8 +24,40 @@ def family(name):
     return None
 
 
+def from_launch_list(path, out):
+    """A launch list (--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv):
+    per family, the mean DRAM bytes and duration per launch over every captured launch."""
+    lines = [ln for ln in open(path) if ln.startswith('"')]
+    recs = {}
+    for r in csv.DictReader(lines):
+        rec = recs.setdefault(r["ID"], {"name": r["Kernel Name"]})
+        unit = r["Metric Unit"]
+        v = float(r["Metric Value"].replace(",", ""))
+        if r["Metric Name"].startswith("dram__bytes"):
+            v *= SCALE.get(unit, 1)
+        elif r["Metric Name"] == "gpu__time_duration.sum":
+            v *= TSCALE.get(unit, 1e-6)
+        rec[r["Metric Name"]] = v
+    acc = {}
+    for rec in recs.values():
+        fam = family(rec["name"])
+        if fam is None or "dram__bytes_read.sum" not in rec:
+            continue
+        a = acc.setdefault(fam, {"kernel": rec["name"].split("(")[0], "bytes": 0.0, "ms": 0.0, "n": 0})
+        a["bytes"] += rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
+        a["ms"] += rec.get("gpu__time_duration.sum", 0.0)
+        a["n"] += 1
+    res = {fam: {"kernel": a["kernel"], "dram_bytes_per_launch": round(a["bytes"] / a["n"]),
+                 "duration_ms_per_launch": round(a["ms"] / a["n"], 4), "launches_captured": a["n"],
+                 "source": path.split("/")[-1]} for fam, a in acc.items()}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 def main():
     rep, out = sys.argv[1], sys.argv[2]
+    if rep.endswith(".csv"):
+        return from_launch_list(rep, out)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
