@@ -85,16 +85,17 @@ __global__ void k_band_fill(int64_t npiv, const uint64_t *__restrict__ ab_ptr, c
         const uint32_t c = ab_col[q];
         const uint16_t v = ab_val[q];
         uint8_t *tile;
-        uint32_t r;
+        uint32_t o;
         if (c < (uint64_t)npiv) {
+            // A tiles are written row-major (element (i, c) at toff(i, c)): the B operand of k_ahat,
+            // which rewrites the off-diagonal ones as Â in the column layout toff(c, i)
             tile = tilesA + (offA[I] + (c / 128u - I)) * (uint64_t)TB;
-            r = c % 128u;
+            o = tc::toff(k, c % 128u);
         } else {
             const uint32_t nc = c - (uint32_t)npiv;
             tile = tilesB + (offB[I] + (nc / 128u - bmin[I])) * (uint64_t)TB;
-            r = nc % 128u;
+            o = tc::toff(nc % 128u, k);
         }
-        const uint32_t o = tc::toff(r, k);
         tile[o] = (uint8_t)(v & 0xff);
         tile[PB + o] = (uint8_t)(v >> 8);
     }
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(128) k_diag_inv(Field F, const uint64_t *__res
     const uint32_t J = blockIdx.x, j = threadIdx.x;
     const uint8_t *t = tilesA + offA[J] * (uint64_t)TB;     // tile (J, J) is first in row block J
     for (uint32_t idx = j; idx < 128 * 128; idx += 128) {
-        const uint32_t r = idx / 128, kk = idx % 128;       // element A[kk][r]
-        const uint32_t o = tc::toff(r, kk);
+        const uint32_t r = idx / 128, kk = idx % 128;       // element A[kk][r] (row-major A tiles)
+        const uint32_t o = tc::toff(kk, r);
         U[kk][r] = (uint16_t)(t[o] | (t[PB + o] << 8));
     }
     __syncthreads();
@@ -462,18 +463,19 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
-// Â_IJ = -A_IJ inv(A_JJ) mod p for every off-diagonal band tile, in place (same layout:
-// element (i, j) at toff(j, i)).  As a tcgen05 product D[j][i] = sum_k W[k][j] A_IJ[i][k]:
-// the stored inv(A_JJ) tile is the A operand as is (toff(j, k) holds W[k][j]); A_IJ is
-// transposed in shared memory into the B operand (toff(i, k) must hold A_IJ[i][k]).  The
-// epilogue thread j writes its 128 values at toff(j, i), negated.  One CTA per tile.
+// Â_IJ = -A_IJ inv(A_JJ) mod p for every off-diagonal band tile, in place: A_IJ arrives
+// row-major (element (i, k) at toff(i, k), k_band_fill) and leaves as Â in the layout the sweep
+// uses (element (i, j) at toff(j, i)).  As a tcgen05 product D[j][i] = sum_k W[k][j] A_IJ[i][k]:
+// the stored inv(A_JJ) tile is the A operand as is (toff(j, k) holds W[k][j]) and the row-major
+// A_IJ tile is the B operand as is (toff(i, k) holds A_IJ[i][k]).  The epilogue thread j writes
+// its 128 values at toff(j, i), negated.  One CTA per tile.
 __global__ void __launch_bounds__(128, 1) k_ahat(Field F, int64_t NB, const uint64_t *__restrict__ offA,
                                                  const uint32_t *__restrict__ amax, const uint64_t *__restrict__ tile_I,
                                                  int64_t ntile, uint8_t *__restrict__ tilesA,
                                                  const uint8_t *__restrict__ invT)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sW = smem, *sA = smem + TB, *sB = smem + 2 * TB;   // W (A operand), A_IJ raw, A_IJ^T (B operand)
+    uint8_t *sW = smem, *sB = smem + TB;                // W (A operand), A_IJ (B operand)
     __shared__ uint64_t bar, accbar;
     __shared__ uint32_t tmem_s;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -491,19 +493,10 @@ __global__ void __launch_bounds__(128, 1) k_ahat(Field F, int64_t NB, const uint
         if (tid == 0) {
             tc::mbar_expect_tx(&bar, 2 * TB);
             tc::bulk_g2s(sW, invT + (size_t)J * TB, TB, &bar);
-            tc::bulk_g2s(sA, tA, TB, &bar);
+            tc::bulk_g2s(sB, tA, TB, &bar);
         }
         tc::mbar_wait(&bar, ph);
         ph ^= 1;
-        // transpose both limb planes: sB[toff(i, k)] = sA[toff(k, i)]
-        for (int pl = 0; pl < 2; pl++)
-            for (int e = tid; e < 128 * 128; e += 128) {
-                const uint32_t i = e >> 7, k = e & 127;
-                sB[pl * PB + tc::toff(i, k)] = sA[pl * PB + tc::toff(k, i)];
-            }
-        tc::fence_async_smem();
-        tc::fence_before();
-        __syncthreads();
         tc::fence_after();
         if (tid == 0) {
             issue_mmas(tbase, tc::smem_u32(sW), tc::smem_u32(sB), false);
@@ -741,12 +734,12 @@ static gbla_status band_build(gbla_mat h)
             GBLA_CUDA_TRY(cudaMemcpyAsync(dtl, tl.data(), tl.size() * 8, cudaMemcpyHostToDevice, st));
             static bool attr2 = false;
             if (!attr2) {
-                GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TB));
+                GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB));
                 attr2 = true;
             }
             const int64_t nt = (int64_t)tl.size();
             const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
-            k_ahat<<<(unsigned)grid, 128, 3 * TB, st>>>(h->F, NB, bt->offA, bt->amax, dtl, nt, bt->tilesA, bt->invT);
+            k_ahat<<<(unsigned)grid, 128, 2 * TB, st>>>(h->F, NB, bt->offA, bt->amax, dtl, nt, bt->tilesA, bt->invT);
             note_launch();
             GBLA_CUDA_TRY(cudaGetLastError());
             // the host list must outlive the async copy
