@@ -47,10 +47,11 @@ __device__ __forceinline__ uint32_t fmod32(uint32_t v, const Field &F) {
     return r >= F.p ? r - F.p : r;
 }
 // S = 2^16 hh + 2^8 xx + ll mod p from the three u8-limb accumulators of a tensor-core product
-// (each < 2^31): with a, b, c = hh, xx, ll mod p, t = a c16 + 256 b + c < 2^31 + 2^24 + 2^16 < 2^32
-// (a c16 < p 2^15 for p > 2^15, < p^2 < 2^30 otherwise), then t mod p.  32-bit arithmetic only.
+// (each < 2^31): with a, b = hh, xx mod p, t = a c16 + 256 b + ll < 2^30 + 2^24 + 2^31 < 2^32
+// (a c16 <= p (2^16 - p) <= 2^30 for p > 2^15, < p^2 < 2^30 otherwise; ll needs no reduction),
+// then t mod p.  32-bit arithmetic only.
 __device__ __forceinline__ uint32_t fmod_limbs(uint32_t hh, uint32_t xx, uint32_t ll, const Field &F) {
-    const uint32_t t = fmod32(hh, F) * F.c16 + (fmod32(xx, F) << 8) + fmod32(ll, F);
+    const uint32_t t = fmod32(hh, F) * F.c16 + (fmod32(xx, F) << 8) + ll;
     return fmod32(t, F);
 }
 // d - s mod p for two residues packed in 16-bit halves

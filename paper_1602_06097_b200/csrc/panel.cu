@@ -45,7 +45,13 @@
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
-                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap);
+                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap,
+                           const int64_t *cend_dev = nullptr);
+gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                              const uint8_t *Alo, const uint8_t *Ahi, int64_t a_rt_stride, int nkb,
+                              const uint8_t *Blo, const uint8_t *Bhi, int64_t b_kb_stride, const int64_t *kb_c0,
+                              const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap);
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
@@ -106,7 +112,18 @@ struct PanelSrc {
     int me;
     int gathered;
     int cap;                    // wide panels: at most cap (<= PK) rows lead inside the window
+    int walign;                 // panel widths a multiple of this (32 if 0; 64 with deferred updates)
 };
+
+// panels per super-panel of deferred trailing updates (GBLA_SP = 1..4).  Default: 4 when D is
+// large (the trailing updates are HBM / epilogue bound: c2, c3, c4), else 1 (c1: the panel chain
+// is the critical path and the per-panel update is hidden behind it; fix-ups would lengthen it).
+static int sp_panels(int64_t mN, int64_t nN)
+{
+    const char *e = getenv("GBLA_SP");
+    const int g = e ? atoi(e) : ((double)mN * (double)nN >= 4e8 ? 4 : 1);
+    return g < 1 ? 1 : g > 4 ? 4 : g;
+}
 
 // candidates per wide panel (GBLA_PANEL_CAP, default PK): fewer pivots per panel shorten the
 // panel factorization (quadratic in them) but add panels
@@ -151,13 +168,23 @@ __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, 
     uint32_t res = NONE16;
     if (rowpiv[r] == GBLA_NONE && c0 < nN) {
         const int64_t wmax = nN - c0 < PW ? nN - c0 : PW;
-        const uint16_t *row = D + (size_t)r * ldD + c0;     // c0 is a multiple of 8? not in general
+        const uint16_t *row = D + (size_t)r * ldD + c0;
+        const bool vec = (((size_t)r * ldD + c0) & 7) == 0;  // c0 is a multiple of 32 but at the last panel
         for (int64_t base = 0; base < wmax && res == NONE16; base += 256) {
             const int64_t k0 = base + lane * 8;
             uint32_t first = NONE16;
-            for (int u = 0; u < 8; u++) {
-                const int64_t k = k0 + u;
-                if (k < wmax && row[k] != 0) { first = (uint32_t)k; break; }
+            if (vec && k0 + 8 <= wmax) {
+                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(row + k0));
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                uint32_t m = 0;
+#pragma unroll
+                for (int j = 0; j < 4; j++) m |= ((w[j] & 0xffffu) ? 1u : 0u) << (2 * j) | ((w[j] >> 16) ? 2u : 0u) << (2 * j);
+                if (m) first = (uint32_t)k0 + __ffs(m) - 1;
+            } else {
+                for (int u = 0; u < 8; u++) {
+                    const int64_t k = k0 + u;
+                    if (k < wmax && row[k] != 0) { first = (uint32_t)k; break; }
+                }
             }
             const unsigned m = __ballot_sync(FULL, first != NONE16);
             if (m) res = __shfl_sync(FULL, first, __ffs(m) - 1);
@@ -291,9 +318,11 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     const bool dense = hist[w128] > (uint32_t)PK;
     if (!dense) {
         // widest w with <= PK candidates; a multiple of 32 (c0 stays 64-byte aligned for the
-        // GEMM epilogue's vector path) unless the panel reaches the last column
+        // GEMM epilogue's vector path; 64 with deferred updates: column tiles of every panel
+        // line up) unless the panel reaches the last column
+        const int64_t wa = src.walign > 0 ? src.walign - 1 : 31;
         for (int64_t c = w128 + tid; c <= wmax; c += NT)
-            if (hist[c] <= (uint32_t)src.cap && (c == wmax || (c & 31) == 0)) atomicMax(&s_u[0], (uint32_t)c);
+            if (hist[c] <= (uint32_t)src.cap && (c == wmax || (c & wa) == 0)) atomicMax(&s_u[0], (uint32_t)c);
     }
     __syncthreads();
     const int width = (int)s_u[0];
@@ -560,8 +589,8 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // zero entries of E' skipped (E' is nearly diagonal on a staircase).  The value rows
             // are dead now: W and Q live in their first 512 bytes.
             uint16_t(*U)[PK] = FS;
-            for (int idx = tid; idx < PK * PK; idx += NT) {
-                const int b = idx / PK, b2 = idx % PK;
+            for (int idx = tid; idx < (int)nb * PK; idx += NT) {   // rows >= nb and columns >= nb are never read
+                const int b = idx >> 7, b2 = idx & (PK - 1);
                 uint32_t v = (b == b2) ? 1u : 0u;
                 if (b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
                 U[b][b2] = (uint16_t)v;
@@ -572,38 +601,69 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 #define WM(i_, j_) X[(i_) * LDX + (j_)]
 #define QM(i_, j_) X[(i_) * LDX + PK + (j_)]
             // the E rows (coefficients at offset PW) of every physical row stay untouched
-            for (int idx = tid; idx < PK * PK; idx += NT) WM(idx / PK, idx % PK) = (idx / PK == idx % PK) ? 1 : 0;
+            for (int idx = tid; idx < (int)nb * (PK / 8); idx += NT) {   // rows < nb of the identity, 8 columns a store
+                const int i = idx >> 4, c8 = (idx & 15) * 8;
+                uint4 z = make_uint4(0, 0, 0, 0);
+                if ((i & ~7) == c8) reinterpret_cast<uint16_t *>(&z)[i & 7] = 1;
+                *reinterpret_cast<uint4 *>(&WM(i, c8)) = z;
+            }
             __syncthreads();
-            for (int s = 1; s < PK; s <<= 1) {
-                const int ne = (PK / 2) * s;       // (PK / 2s) pairs x s^2 entries
-                // entries in rows or columns >= nb stay identity / zero (U is the identity there)
-                if (s >= (int)nb) break;
-                for (int e = tid; e < ne; e += NT) {
-                    const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
-                    if (base + r >= (int)nb || base + s + c >= (int)nb) continue;
-                    uint64_t a0 = 0, a1 = 0;        // (B C^-1)[r][c]
-                    int k = 0;
-                    for (; k + 1 <= c; k += 2) {
-                        a0 += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
-                        a1 += (uint64_t)U[base + r][base + s + k + 1] * WM(base + s + k + 1, base + s + c);
+            P2_LAP(13);
+            // levels s = 1, 2, .., 64: every aligned 2s-block [[A, B], [0, C]] with A^-1, C^-1 known
+            // gets Q = B C^-1, then -A^-1 Q.  One item = one row r and 4 consecutive columns (s >= 4):
+            // the U / W element of a step is shared by the 4 products.  W and Q are upper triangular
+            // with zeros beyond nb, so the sums need no per-column bounds.
+            for (int s = 1, ls = 0; s < PK && s < (int)nb; s <<= 1, ls++) {
+                const int cw = s >= 4 ? 4 : s, lcw = s >= 4 ? 2 : ls;   // columns per item, log2
+                const int lg = ls - lcw;                                 // log2(column groups per row)
+                const int npair = ((int)nb + 2 * s - 1) >> (ls + 1);     // pairs with base < nb
+                const int items = npair << (ls + lg);
+                for (int it = tid; it < items; it += NT) {
+                    const int q = it >> (ls + lg), r = (it >> lg) & (s - 1), c0 = (it & ((1 << lg) - 1)) << lcw;
+                    const int base = q << (ls + 1);
+                    if (base + r >= (int)nb || base + s + c0 >= (int)nb) continue;
+                    int kend = c0 + cw;                                  // W[s+k][s+c] = 0 for k > c
+                    if (kend > (int)nb - base - s) kend = (int)nb - base - s;
+                    uint64_t acc[4] = {0, 0, 0, 0};
+                    const uint16_t *urow = &U[base + r][base + s];
+                    if (cw == 4) {
+#pragma unroll 4
+                        for (int k = 0; k < kend; k++) {
+                            const uint64_t u = urow[k];
+                            const uint2 w = *reinterpret_cast<const uint2 *>(&WM(base + s + k, base + s + c0));
+                            acc[0] += u * (w.x & 0xffffu); acc[1] += u * (w.x >> 16);
+                            acc[2] += u * (w.y & 0xffffu); acc[3] += u * (w.y >> 16);
+                        }
+                    } else {
+                        for (int k = 0; k < kend; k++)
+                            for (int j = 0; j < cw; j++) acc[j] += (uint64_t)urow[k] * WM(base + s + k, base + s + c0 + j);
                     }
-                    if (k <= c) a0 += (uint64_t)U[base + r][base + s + k] * WM(base + s + k, base + s + c);
-                    QM(base + r, base + s + c) = (uint16_t)fmod64(a0 + a1, F);
+                    for (int j = 0; j < cw; j++) QM(base + r, base + s + c0 + j) = (uint16_t)fmod64(acc[j], F);
                 }
                 __syncthreads();
-                for (int e = tid; e < ne; e += NT) {
-                    const int q = e / (s * s), r = (e / s) % s, c = e % s, base = q * 2 * s;
-                    if (base + r >= (int)nb || base + s + c >= (int)nb) continue;
-                    uint64_t a0 = 0, a1 = 0;        // (A^-1 (B C^-1))[r][c]
+                for (int it = tid; it < items; it += NT) {
+                    const int q = it >> (ls + lg), r = (it >> lg) & (s - 1), c0 = (it & ((1 << lg) - 1)) << lcw;
+                    const int base = q << (ls + 1);
+                    if (base + r >= (int)nb || base + s + c0 >= (int)nb) continue;
                     const int kmax = (base + s <= (int)nb) ? s : (int)nb - base;
-                    int k = r;
-                    for (; k + 1 < kmax; k += 2) {
-                        a0 += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
-                        a1 += (uint64_t)WM(base + r, base + k + 1) * QM(base + k + 1, base + s + c);
+                    uint64_t acc[4] = {0, 0, 0, 0};
+                    const uint16_t *wrow = &WM(base + r, base);
+                    if (cw == 4) {
+#pragma unroll 4
+                        for (int k = r; k < kmax; k++) {
+                            const uint64_t w = wrow[k];
+                            const uint2 qv = *reinterpret_cast<const uint2 *>(&QM(base + k, base + s + c0));
+                            acc[0] += w * (qv.x & 0xffffu); acc[1] += w * (qv.x >> 16);
+                            acc[2] += w * (qv.y & 0xffffu); acc[3] += w * (qv.y >> 16);
+                        }
+                    } else {
+                        for (int k = r; k < kmax; k++)
+                            for (int j = 0; j < cw; j++) acc[j] += (uint64_t)wrow[k] * QM(base + k, base + s + c0 + j);
                     }
-                    if (k < kmax) a0 += (uint64_t)WM(base + r, base + k) * QM(base + k, base + s + c);
-                    const uint32_t z = fmod64(a0 + a1, F);
-                    WM(base + r, base + s + c) = (uint16_t)(z ? p - z : 0);
+                    for (int j = 0; j < cw; j++) {
+                        const uint32_t z = fmod64(acc[j], F);
+                        WM(base + r, base + s + c0 + j) = (uint16_t)(z ? p - z : 0);
+                    }
                 }
                 __syncthreads();
             }
@@ -631,29 +691,35 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 }
             }
             __syncthreads();
-            for (int idx = tid; idx < PK * PK; idx += NT) {
-                const int b = idx >> 7, ls = idx & (PK - 1);
-                uint32_t v = 0;
-                if (b < (int)nb && ls < (int)nb) {
-                    const uint32_t sc = bphys[ls];
-                    const uint32_t cnt = lcnt[sc];
-                    uint64_t acc = 0;
-                    if (cnt <= (uint32_t)LMAX) {
-                        for (uint32_t j = 0; j < cnt; j++) {
-                            const uint32_t b2 = lrow[j * PK + sc];
-                            if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lval[j * PK + sc];
+            for (int idx = tid; idx < PK * PK / 4; idx += NT) {   // 4 consecutive K entries: one 4-byte store per plane
+                const int b = idx >> 5, l0 = (idx & 31) * 4;
+                uint32_t lo = 0, hi = 0;
+                for (int u = 0; u < 4; u++) {
+                    const int ls = l0 + u;
+                    uint32_t v = 0;
+                    if (b < (int)nb && ls < (int)nb) {
+                        const uint32_t sc = bphys[ls];
+                        const uint32_t cnt = lcnt[sc];
+                        uint64_t acc = 0;
+                        if (cnt <= (uint32_t)LMAX) {
+                            for (uint32_t j = 0; j < cnt; j++) {
+                                const uint32_t b2 = lrow[j * PK + sc];
+                                if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lval[j * PK + sc];
+                            }
+                        } else {                                  // dense column: every head row
+                            for (int b2 = b; b2 < (int)nb; b2++) {
+                                const uint32_t e = X[bphys[b2] * LDX + PW + sc];
+                                if (e) acc += (uint64_t)WM(b, b2) * mod32(e * hinv[bphys[b2]], p, m32);
+                            }
                         }
-                    } else {                                      // dense column: every head row
-                        for (int b2 = b; b2 < (int)nb; b2++) {
-                            const uint32_t e = X[bphys[b2] * LDX + PW + sc];
-                            if (e) acc += (uint64_t)WM(b, b2) * mod32(e * hinv[bphys[b2]], p, m32);
-                        }
+                        v = fmod64(acc, F);
                     }
-                    v = fmod64(acc, F);
+                    lo |= (v & 0xffu) << (8 * u);
+                    hi |= (v >> 8) << (8 * u);
                 }
-                const uint32_t o = tc::toff((uint32_t)b, (uint32_t)ls);
-                Tlo[o] = (uint8_t)(v & 0xff);
-                Thi[o] = (uint8_t)(v >> 8);
+                const uint32_t o = tc::toff((uint32_t)b, (uint32_t)l0);
+                *reinterpret_cast<uint32_t *>(Tlo + o) = lo;
+                *reinterpret_cast<uint32_t *>(Thi + o) = hi;
             }
 #undef WM
 #undef QM
@@ -785,16 +851,20 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 
 // F[slot] = D[i, pivot columns] for every row i not selected in this panel with
 // a nonzero coefficient (limb planes of the trailing GEMM's A tiles), rows[slot] = i.
+// Deferred updates (Fd != NULL): F also goes to K-block j of the row-indexed A tiles
+// Fd[(i / 128) * G + j] (D row i), and kb_c0[j] = c0.
 __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ldD,
                           const uint32_t *__restrict__ rowpiv, P2State *__restrict__ ps,
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
-                          const uint8_t *__restrict__ owner, int me)
+                          const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
+                          uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
     constexpr int CPL = PK / 32;
     const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
+    if (kb_c0 && blockIdx.x == 0 && threadIdx.x == 0) kb_c0[j] = ps->c0;
     if (kp == 0) return;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mN;
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -824,7 +894,40 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     const size_t o = (size_t)(slot / 128) * (PK * 128) + tc::toff(slot % 128, lane * CPL);
     *reinterpret_cast<uint32_t *>(Flo + o) = lo;
     *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
+    if (Fdlo) {
+        const size_t od = (size_t)((i / 128) * G + j) * (PK * 128) + tc::toff((uint32_t)(i % 128), lane * CPL);
+        *reinterpret_cast<uint32_t *>(Fdlo + od) = lo;
+        *reinterpret_cast<uint32_t *>(Fdhi + od) = hi;
     }
+    }
+}
+
+// Deferred updates: the factors of this panel's selected rows S_b in the earlier K-blocks
+// i < nk of the super-panel, moved from the row-indexed tiles Fd into the A tile Af
+// (row b, K-block i) and cleared in Fd: after the fix-up GEMM brings D[S] up to date in the
+// deferred columns, S_b becomes a pivot row and the flush must not subtract them again.
+// Block (b, i), 32 threads x 4 K entries.
+__global__ void k_fix_gather(const P2State *__restrict__ ps, int G, uint8_t *__restrict__ Fdlo,
+                             uint8_t *__restrict__ Fdhi, uint8_t *__restrict__ Aflo, uint8_t *__restrict__ Afhi)
+{
+    const uint32_t b = blockIdx.x, i = blockIdx.y;
+    if (b >= ps->kp) return;
+    const uint32_t r = ps->sel[b];
+    const uint32_t k = threadIdx.x * 4;
+    const size_t os = (size_t)((r / 128) * G + i) * (PK * 128) + tc::toff(r % 128, k);
+    const size_t od = (size_t)i * (PK * 128) + tc::toff(b, k);
+    uint32_t *sl = reinterpret_cast<uint32_t *>(Fdlo + os), *sh = reinterpret_cast<uint32_t *>(Fdhi + os);
+    *reinterpret_cast<uint32_t *>(Aflo + od) = *sl;
+    *reinterpret_cast<uint32_t *>(Afhi + od) = *sh;
+    *sl = 0;
+    *sh = 0;
+}
+
+// start of a super-panel: deferred columns from Cd = min(nN, c1 + G * PW) on
+__global__ void k_sp_begin(const P2State *__restrict__ ps, int64_t nN, int G, int64_t *__restrict__ Cd)
+{
+    const int64_t c = (ps ? ps->c1 : 0) + (int64_t)G * PW;
+    *Cd = c < nN ? c : nN;
 }
 
 // transposed limb planes of D[S, c0:]: B operand tiles (64 columns x K = 128) of the Rn GEMM
@@ -1114,10 +1217,27 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Tlo2[q]));
         GBLA_TRY(dalloc_t(h, (size_t)PK * PK, &Thi2[q]));
     }
+    const bool lookahead = getenv("GBLA_NO_LOOKAHEAD") == nullptr;
+    // Deferred trailing updates (super-panels of G panels): each panel updates D eagerly only
+    // left of the column Cd; the columns from Cd on take one K = G * 128 update per super-panel
+    // (K11 multi-K: a quarter of the HBM passes and epilogue reductions of per-panel updates).
+    const int G = lookahead ? sp_panels(mN, nN) : 1;
+    const size_t rd_stride = (size_t)npad * PK;          // bytes per plane per K-block
+    const int64_t ntrD = (mN + 127) / 128;
+    uint8_t *Fdlo = nullptr, *Fdhi = nullptr, *Aflo = nullptr, *Afhi = nullptr;
+    int64_t *spc0 = nullptr, *spCd = nullptr;
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rtlo));
-    GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Rthi));
+    GBLA_TRY(dalloc_t(h, rd_stride * G, &Rtlo));
+    GBLA_TRY(dalloc_t(h, rd_stride * G, &Rthi));
+    if (G > 1) {
+        GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdlo));
+        GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdhi));
+        GBLA_TRY(dalloc_t(h, (size_t)G * PK * 128, &Aflo));
+        GBLA_TRY(dalloc_t(h, (size_t)G * PK * 128, &Afhi));
+        GBLA_TRY(dalloc_t(h, (size_t)G, &spc0));
+        GBLA_TRY(dalloc_t(h, 1, &spCd));
+    }
     GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
     GBLA_TRY(dalloc(h, 2 * sizeof(P2State), (void **)&ps));
     static bool attr = false;
@@ -1130,7 +1250,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_TRY(dalloc_t(h, 16, &trace));
         GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 16 * 8, st));
     }
-    const bool lookahead = getenv("GBLA_NO_LOOKAHEAD") == nullptr;
     const int cap = panel_cap();
     cudaStream_t side = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr;
@@ -1156,7 +1275,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     auto p_factor = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         kt_mark_on(h, KT_PANEL, s);
-        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap};
+        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32};
         k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace);
         kt_mark_on(h, KT_PANEL, s);
         note_launch();
@@ -1166,8 +1285,25 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         // one warp per row, blocks in row order: the row list (and the D rows of each 128-row tile
         // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
-                                                         rows[k & 1], nullptr, 0);
+                                                         rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0);
         note_launch();
+    };
+    // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
+    auto sp_begin = [&](const P2State *last) {
+        k_sp_begin<<<1, 1, 0, st>>>(last, nN, G, spCd);
+        note_launch();
+        if (cudaMemsetAsync(Fdlo, 0, (size_t)ntrD * G * PK * 128, st) != cudaSuccess ||
+            cudaMemsetAsync(Fdhi, 0, (size_t)ntrD * G * PK * 128, st) != cudaSuccess)
+            return GBLA_E_CUDA;
+        return GBLA_OK;
+    };
+    auto sp_flush = [&](const P2State *cur, int ctsel) {
+        kt_mark(h, KT_TRAIL);
+        const gbla_status r = modgemm_tc_sub_mk(st, mN, nullptr, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
+                                                (int64_t)rd_stride, spc0, nullptr, h->D, ldD, spCd, &cur->c1, PW,
+                                                ctsel, gemm_grid);
+        kt_mark(h, KT_TRAIL);
+        return r;
     };
     auto factor = [&](cudaStream_t s, int64_t k) {
         p_lead(s, k);
@@ -1184,6 +1320,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     if (status == GBLA_OK) {
         k_p2_init<<<1, 1, 0, st>>>(ps);
         note_launch();
+        if (G > 1) status = sp_begin(nullptr);
         factor(st, 0);                                  // panel 0 on the main stream
     }
     // optional timeline (GBLA_ECH_TIMELINE=n): device times of the first n look-ahead iterations
@@ -1210,13 +1347,25 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         for (int q = 0; q < batch && status == GBLA_OK; q++, k++) {
             P2State *cur = ps + (k & 1);
             const int f = (int)(k & 1);
+            const int j = (int)(k % G);                  // position in the super-panel
+            uint8_t *Rtl = Rtlo + j * rd_stride, *Rth = Rthi + j * rd_stride;
             tmark(k, st);
+            if (j > 0) {                                 // S up to date in the deferred columns
+                k_fix_gather<<<dim3(PK, j), 32, 0, st>>>(cur, G, Fdlo, Fdhi, Aflo, Afhi);
+                note_launch();
+                kt_mark(h, KT_TRAIL);
+                status = modgemm_tc_sub_mk(st, PK, &cur->kp, nN, h->F, Aflo, Afhi, G, j, Rtlo, Rthi,
+                                           (int64_t)rd_stride, spc0, cur->sel, h->D, ldD, spCd, nullptr, 0, 0,
+                                           gemm_grid);
+                kt_mark(h, KT_TRAIL);
+                if (status != GBLA_OK) break;
+            }
             launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN, (const uint16_t *)h->D,
                        ldD, (const P2State *)cur, Blo, Bhi);
             note_launch();
             kt_mark(h, KT_RN);
             // look-ahead: only the window part of Rn is on the chain to the next panel
-            status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0,
+            status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth, &cur->c0,
                                       &cur->kp, &cur->c1, PW, lookahead ? 1 : 0);
             kt_mark(h, KT_RN);
             if (status != GBLA_OK) break;
@@ -1232,12 +1381,13 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             } else {
                 // the next panel's window first, then the next panel beside the rest of the update
                 kt_mark(h, KT_TRAIL);
-                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
-                                        ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 if (status != GBLA_OK) break;
                 launch_pdl(k_commit2, dim3(h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD, (const P2State *)cur,
                            (const uint16_t *)Rn, ldR, dops, 1, (const uint8_t *)nullptr, 0);
                 note_launch();
+                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1)) != GBLA_OK) break;   // next window
                 p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
@@ -1249,17 +1399,20 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 if (cudaEventRecord(evB, side) != cudaSuccess) { fail("event"); break; }
                 tmark(k, st);
                 kt_mark(h, KT_RN);
-                status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtlo, Rthi, &cur->c0,
+                status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth, &cur->c0,
                                           &cur->kp, &cur->c1, PW, 2);
                 kt_mark(h, KT_RN);
                 if (status != GBLA_OK) break;
-                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtlo, Rthi, rows[f], h->D,
-                                        ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
                 launch_pdl(k_commit2, dim3(2 * h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD,
                            (const P2State *)cur, (const uint16_t *)Rn, ldR, dops, 2, (const uint8_t *)nullptr, 0);
                 note_launch();
+                if (G > 1 && j == G - 1) {              // end of the super-panel: the deferred columns
+                    if ((status = sp_flush(cur, 2)) != GBLA_OK || (status = sp_begin(cur)) != GBLA_OK) break;
+                }
                 tmark(k, st);
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
                 p_gather(st, k + 1);
@@ -1290,6 +1443,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             batch = 8;
         }
     }
+    if (status == GBLA_OK && G > 1 && (k % G) != 0) {      // the last, partial super-panel
+        P2State *last = ps + ((k - 1) & 1);
+        status = sp_flush(last, 0);
+    }
     if (status == GBLA_OK && cudaStreamSynchronize(st) != cudaSuccess) fail("sync");
 
     if (side) cudaStreamSynchronize(side);
@@ -1311,9 +1468,9 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         const double n = tr[9] ? (double)tr[9] : 1.0;
         fprintf(stderr,
                 "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f rounds(c1) %.0f "
-                "rounds(c2) %.0f dense-backsub %.0f output %.0f; wide: inverse %.0f T %.0f; rounds/panel %.2f "
+                "rounds(c2) %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f inverse %.0f T %.0f; rounds/panel %.2f "
                 "candidates %.1f pivots %.1f width %.1f\n",
-                tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[14] / n,
+                tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[13] / n, tr[14] / n,
                 tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
     }
     return status;

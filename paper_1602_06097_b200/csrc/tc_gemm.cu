@@ -70,12 +70,22 @@ struct MMArgs {
     const int64_t *win_dev;
     int64_t win_w;
     int ctsel;
+    // multi-K (MK kernels): K = nkb blocks of KP.  A tile (rt, i) at (rt * a_rt_stride + i) * A_PLANE;
+    // B tile of K-block i for output column tile ct at b_kb_stride * i + (ct + (c0 - kb_c0[i]) / BN) * B_PLANE
+    // (each K-block's B tiles are laid out from its own column origin kb_c0[i])
+    int nkb;
+    int64_t a_rt_stride;
+    int64_t b_kb_stride;
+    const int64_t *kb_c0;
+    const int64_t *cend_dev;          // optional end column (min(cols, *cend_dev))
 };
 
 constexpr int NSB = 4;                               // B stages
 // epilogue warps: 8 (2 per TMEM lane quarter, 32 columns each) or 16 (4 per quarter, 16 columns)
 constexpr int ws_threads(int epiw) { return 64 + 32 * epiw; }   // producer, MMA, epilogue warps
 constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB: one CTA per SM)
+constexpr int MK_MAX = 4;                            // K-blocks of a multi-K GEMM (K <= 512)
+constexpr int ws_smem(bool mk) { return mk ? MK_MAX * A_BYTES + NSB * B_BYTES : WS_SMEM; }   // 192 KB / 128 KB
 
 // Warp-specialized persistent K11: warp 0 stages operands (A tile once per row
 // tile, double-buffered; B tiles through a 4-stage ring), warp 1 issues the
@@ -84,7 +94,11 @@ constexpr int WS_SMEM = 2 * A_BYTES + NSB * B_BYTES; // 64 KB + 64 KB (> 114 KB:
 // the 64 columns each), so loads, MMAs and the epilogue of consecutive tiles
 // overlap.  Each CTA owns a contiguous range of output tiles in row-tile-major
 // order (A reuse).
-template <int MODE, int EPI_WARPS, bool PF2>
+//
+// MK (multi-K, MODE_SUB only): K = nkb <= 4 blocks of 128 (exact: every limb sum <= 512 * 255^2 * 2
+// < 2^31).  The A tiles of all K-blocks of a row tile stay resident (one buffer, 128 KB); the B
+// tiles stream through the ring, nkb per output tile.
+template <int MODE, int EPI_WARPS, bool PF2, bool MK = false>
 __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs g)
 {
     constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
@@ -95,6 +109,7 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     tc::pdl_wait();
     if (g.skip_dev && *g.skip_dev == 0) return;
     int64_t cols = g.cols, c0 = 0;
+    if (g.cend_dev && *g.cend_dev < cols) cols = *g.cend_dev;
     uint16_t *C = g.C;
     if (g.c0_dev) {
         c0 = *g.c0_dev;
@@ -106,11 +121,12 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     const int64_t ntr = (nr + BM - 1) / BM, ntc_all = (cols + BN - 1) / BN;
     int64_t w0 = 0, w1 = 0;
     if (g.ctsel != CT_ALL) {
-        const int64_t rel = *g.win_dev - c0;
-        w0 = rel / BN;
-        w1 = (rel + g.win_w + BN - 1) / BN;
+        const int64_t rel = *g.win_dev - c0;           // < 0: the window starts left of this GEMM
+        w0 = rel > 0 ? rel / BN : 0;
+        w1 = rel + g.win_w > 0 ? (rel + g.win_w + BN - 1) / BN : 0;
         if (w0 > ntc_all) w0 = ntc_all;
         if (w1 > ntc_all) w1 = ntc_all;
+        if (w1 < w0) w1 = w0;
     }
     const int64_t ntc = g.ctsel == CT_ALL ? ntc_all : g.ctsel == CT_WINDOW ? w1 - w0 : ntc_all - (w1 - w0);
     const int64_t ntiles = ntr * ntc;
@@ -141,10 +157,47 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_base;
-    uint8_t *Abuf = smem, *Bbuf = smem + 2 * A_BYTES;
+    uint8_t *Abuf = smem, *Bbuf = smem + (MK ? MK_MAX : 2) * A_BYTES;
 
     if (warp == 0) {
-        if (lane == 0) {                       // ---- producer
+        if (MK && lane == 0) {                 // ---- producer (multi-K)
+            int64_t cur_rt = -1;
+            uint32_t aph = 1, bph[NSB] = {1, 1, 1, 1};
+            int s = 0;
+            const int nkb = g.nkb;
+            int64_t boff[MK_MAX];
+            for (int i = 0; i < MK_MAX; i++) {
+                boff[i] = 0;
+                if (i < nkb && g.kb_c0) {
+                    const int64_t d = (c0 - g.kb_c0[i]) / BN;   // < 0 only for an empty K-block (zero A)
+                    boff[i] = d > 0 ? d : 0;
+                }
+            }
+            for (int64_t tile = t_begin; tile < t_end; tile++) {
+                const int64_t rt = tile / ntc, ct = ct_of(tile % ntc);
+                if (rt != cur_rt) {
+                    tc::mbar_wait(&aempty[0], aph);
+                    aph ^= 1;
+                    tc::mbar_expect_tx(&afull[0], nkb * A_BYTES);
+                    for (int i = 0; i < nkb; i++) {
+                        const int64_t at = rt * g.a_rt_stride + i;
+                        tc::bulk_g2s(Abuf + i * A_BYTES, g.Ahi + at * A_PLANE, A_PLANE, &afull[0]);
+                        tc::bulk_g2s(Abuf + i * A_BYTES + A_PLANE, g.Alo + at * A_PLANE, A_PLANE, &afull[0]);
+                    }
+                    cur_rt = rt;
+                }
+                for (int i = 0; i < nkb; i++) {
+                    tc::mbar_wait(&bempty[s], bph[s]);
+                    bph[s] ^= 1;
+                    uint8_t *bb = Bbuf + s * B_BYTES;
+                    const int64_t bo = g.b_kb_stride * i + (ct + boff[i]) * B_PLANE;
+                    tc::mbar_expect_tx(&bfull[s], B_BYTES);
+                    tc::bulk_g2s(bb, g.Bhi + bo, B_PLANE, &bfull[s]);
+                    tc::bulk_g2s(bb + B_PLANE, g.Blo + bo, B_PLANE, &bfull[s]);
+                    s = (s + 1) % NSB;
+                }
+            }
+        } else if (!MK && lane == 0) {         // ---- producer
             int64_t cur_rt = -1;
             int aslot = 1;
             uint32_t aph[2] = {1, 1}, bph[NSB] = {1, 1, 1, 1};
@@ -171,7 +224,49 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {                       // ---- MMA issuer
+        if (MK && lane == 0) {                 // ---- MMA issuer (multi-K)
+            int64_t cur_rt = -1;
+            uint32_t aph = 0, bph[NSB] = {0, 0, 0, 0}, tph[2] = {1, 1};
+            int s = 0, ab = 0;
+            const int nkb = g.nkb;
+            const uint32_t idesc = tc::idesc_u8(BM, BN);
+            for (int64_t tile = t_begin; tile < t_end; tile++) {
+                const int64_t rt = tile / ntc;
+                if (rt != cur_rt) {
+                    if (cur_rt >= 0) tc::commit(&aempty[0]);   // A free once the old row tile's MMAs finish
+                    tc::mbar_wait(&afull[0], aph);
+                    aph ^= 1;
+                    cur_rt = rt;
+                }
+                tc::mbar_wait(&tempty[ab], tph[ab]);
+                tph[ab] ^= 1;
+                const uint32_t d = tbase + ab * 3 * BN;
+                for (int i = 0; i < nkb; i++) {
+                    tc::mbar_wait(&bfull[s], bph[s]);
+                    bph[s] ^= 1;
+                    tc::fence_after();
+                    const uint32_t aH = tc::smem_u32(Abuf + i * A_BYTES), aL = aH + A_PLANE;
+                    const uint32_t bH = tc::smem_u32(Bbuf + s * B_BYTES), bL = bH + B_PLANE;
+#pragma unroll
+                    for (int k = 0; k < KP / 32; k++) {
+                        const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
+                        const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
+                        const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
+                        const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
+                        const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
+                        const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                        tc::mma_i8(d + 0, dAh, dBh, idesc, acc);          // HH
+                        tc::mma_i8(d + BN, dAh, dBl, idesc, acc);         // X
+                        tc::mma_i8(d + BN, dAl, dBh, idesc, 1);           // X
+                        tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, acc);     // LL
+                    }
+                    tc::commit(&bempty[s]);
+                    s = (s + 1) % NSB;
+                }
+                tc::commit(&tfull[ab]);
+                ab ^= 1;
+            }
+        } else if (!MK && lane == 0) {         // ---- MMA issuer
             int64_t cur_rt = -1;
             int aslot = 1;
             uint32_t aph[2] = {0, 0}, bph[NSB] = {0, 0, 0, 0}, tph[2] = {1, 1};
@@ -359,13 +454,13 @@ __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, const ui
     hi[o] = (uint8_t)(v >> 8);
 }
 
-template <int MODE, int EPIW, bool PF2>
+template <int MODE, int EPIW, bool PF2, bool MK = false>
 gbla_status set_attr()
 {
     static bool attr = false;
     if (!attr) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW, PF2>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW, PF2, MK>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem(MK)));
         attr = true;
     }
     return GBLA_OK;
@@ -388,22 +483,22 @@ static bool epi_pf2()
     return v == 1;
 }
 
-template <int MODE, int EPIW, bool PF2>
+template <int MODE, int EPIW, bool PF2, bool MK = false>
 static gbla_status launch_ws1(const MMArgs &a, int64_t grid, cudaStream_t st)
 {
-    GBLA_TRY((set_attr<MODE, EPIW, PF2>()));
+    GBLA_TRY((set_attr<MODE, EPIW, PF2, MK>()));
     // programmatic dependent launch: the GEMM's launch overlaps the tail of the previous kernel
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(ws_threads(EPIW));
-    cfg.dynamicSmemBytes = WS_SMEM;
+    cfg.dynamicSmemBytes = ws_smem(MK);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    GBLA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_modgemm_ws<MODE, EPIW, PF2>, a));
+    GBLA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_modgemm_ws<MODE, EPIW, PF2, MK>, a));
     return GBLA_OK;
 }
 
@@ -424,14 +519,14 @@ int g_sms = 148;
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
                            const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
                            const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
-                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap)
+                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap, const int64_t *cend_dev)
 {
     if (max_rows <= 0 || cols <= 0) return GBLA_OK;
     const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
     int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
-             c0_dev, nullptr, win_dev, win_w, ctsel};
+             c0_dev, nullptr, win_dev, win_w, ctsel, 1, 1, 0, nullptr, cend_dev};
     GBLA_TRY(launch_ws<MODE_SUB>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
@@ -449,6 +544,26 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
     if (grid > g_sms) grid = g_sms;
     MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
     GBLA_TRY(launch_ws<MODE_STORE>(a, grid, st));
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}
+
+// C[rowidx[i], c0:cols] -= sum over nkb K-blocks of A_i B_i (multi-K, K <= 512; see MMArgs)
+gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                              const uint8_t *Alo, const uint8_t *Ahi, int64_t a_rt_stride, int nkb,
+                              const uint8_t *Blo, const uint8_t *Bhi, int64_t b_kb_stride, const int64_t *kb_c0,
+                              const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap)
+{
+    if (max_rows <= 0 || cols <= 0 || nkb <= 0) return GBLA_OK;
+    if (nkb > MK_MAX) { set_error("modgemm_tc_sub_mk: K > %d", MK_MAX * KP); return GBLA_E_INVAL; }
+    const int64_t tiles = ((max_rows + BM - 1) / BM) * ((cols + BN - 1) / BN);
+    int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
+    if (grid > tiles) grid = tiles;
+    MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
+             c0_dev, nullptr, win_dev, win_w, ctsel, nkb, a_rt_stride, b_kb_stride, kb_c0, nullptr};
+    GBLA_TRY((launch_ws1<MODE_SUB, 8, true, true>(a, grid, st)));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -488,7 +603,7 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
     k_split_cols<<<grid_for(cp * KP, 256), 256, 0, st>>>(cols, cp, K, B, ldb, Blo, Bhi);
     note_launch(2);
     gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
-                                   CT_ALL, 0);
+                                   CT_ALL, 0, nullptr);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
