@@ -55,7 +55,7 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel);
+                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr);
 void modgemm_set_sms(int sms);
 
 namespace {
@@ -113,6 +113,7 @@ struct PanelSrc {
     int gathered;
     int cap;                    // wide panels: at most cap (<= PK) rows lead inside the window
     int walign;                 // panel widths a multiple of this (32 if 0; 64 with deferred updates)
+    int lumode;                 // chunk echelon: 0 rounds, 1 pivot steps, 2 pivot steps in dense mode
 };
 
 // panels per super-panel of deferred trailing updates (GBLA_SP = 1..4).  Default: 4 when D is
@@ -133,6 +134,15 @@ static int panel_cap()
     const int c = e ? atoi(e) : PK;
     return c >= 16 && c <= PK ? c : PK;
 }
+
+// GBLA_PANEL_LU: how k_panel2 puts a chunk of candidates in echelon form (see step (c))
+static int panel_lumode()
+{
+    const char *e = getenv("GBLA_PANEL_LU");
+    const int v = e ? atoi(e) : 2;
+    return v < 0 || v > 2 ? 2 : v;
+}
+__device__ __forceinline__ bool use_lu(bool dense, int mode) { return mode == 1 || (mode == 2 && dense); }
 
 __device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
 {
@@ -245,8 +255,8 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     __shared__ uint32_t Ub[32][33], Rb[32][33], Qb[32][33];
     constexpr int CLMAX = 1024;
     __shared__ uint32_t clist[CLMAX];        // rows leading inside the window (wide-mode candidates)
-    __shared__ uint32_t hmap[PW];            // column -> established head of this chunk
     __shared__ uint32_t hinv[PK];            // inverse of each head's leading value (wide mode)
+    __shared__ uint32_t hmap[PW];            // rounds: column -> established head of this chunk
     __shared__ uint32_t s_u[8];
     __shared__ long long s_pos;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -466,83 +476,174 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             __syncthreads();
         }
         P2_LAP(3);
-        // (c) rounds: leading columns, one head per column, eliminate collisions
-        for (int k = tid; k < width; k += NT) hmap[k] = NONE16;
-        __syncthreads();
-        for (;;) {
-            if (trace && tid == 0) trace[8] += 1;
-            // (c1) every remaining candidate (warp per row): leading column; while an established
-            //      head owns it, eliminate it (heads are fixed, so this chain needs no block sync)
-            for (int ci = warp; ci < ncand; ci += 32) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] != 1) continue;
-                uint16_t *xr = X + q * LDX;
-                int base = 0;
+        // (c) echelon form of the chunk: parallel rounds (staircase panels: many distinct leads)
+        //     or pivot steps (dense panels: the rounds would elect one head per round)
+        if (!use_lu(dense, src.lumode)) {
+            for (int k = tid; k < width; k += NT) hmap[k] = NONE16;
+            __syncthreads();
+            for (;;) {
+                if (trace && tid == 0) trace[8] += 1;
+                // (c1) every remaining candidate (warp per row): leading column; while an established
+                //      head owns it, eliminate it (heads are fixed, so this chain needs no block sync)
+                for (int ci = warp; ci < ncand; ci += 32) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] != 1) continue;
+                    uint16_t *xr = X + q * LDX;
+                    int base = 0;
+                    for (;;) {
+                        uint32_t ld = NONE16;
+                        for (; base < ldv; base += 32) {
+                            const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
+                            if (m) { ld = base + __ffs(m) - 1; break; }
+                        }
+                        if (ld == NONE16) {                       // dependent: zero on the panel
+                            if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
+                            break;
+                        }
+                        const uint32_t hq = hmap[ld];
+                        if (hq == NONE16) {
+                            if (lane == 0) clead[q] = ld;
+                            break;
+                        }
+                        const uint16_t *hr = X + hq * LDX;
+                        // dense mode: heads are normalized; wide mode: scale by the head's inverse
+                        const uint32_t gl = dense ? xr[ld] : mod32(xr[ld] * hinv[hq], p, m32);
+                        const uint32_t ng = gl ? p - gl : 0;
+                        __syncwarp();
+                        for (int k = base + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(xr[k] + ng * hr[k], p, m32);
+                        for (int k = lane; k < PK; k += 32)
+                            xr[PW + k] = (uint16_t)mod32(xr[PW + k] + ng * hr[PW + k], p, m32);
+                        __syncwarp();
+                    }
+                }
+                for (int k = tid; k < width; k += NT) hist[k] = NONE16;
+                __syncthreads();
+                P2_LAP(3);
+                // (c2) one new head per leading column among the remaining candidates
+                for (int ci = tid; ci < ncand; ci += NT) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] == 1) atomicMin(&hist[clead[q]], q);
+                }
+                __syncthreads();
+                int coll = 0;
+                for (int ci = tid; ci < ncand; ci += NT) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] == 1) {
+                        if (hist[clead[q]] == q) cstat[q] = 4;     // new head: normalize below
+                        else coll = 1;                              // eliminated next round
+                    }
+                }
+                coll = __syncthreads_count(coll);               // rows that lost their column this round
+                for (int ci = warp; ci < ncand; ci += 32) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] != 4) continue;
+                    uint16_t *xr = X + q * LDX;
+                    const uint32_t iv = invtab[xr[clead[q]]];
+                    if (!dense) {                       // wide mode: keep the row, remember 1 / lead value
+                        if (lane == 0) hinv[q] = iv;
+                        continue;
+                    }
+                    __syncwarp();
+                    for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
+                    for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
+                }
+                __syncthreads();
+                for (int ci = tid; ci < ncand; ci += NT) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] == 4) { cstat[q] = 2; hmap[clead[q]] = q; }
+                }
+                __syncthreads();
+                P2_LAP(4);
+                if (!coll) break;
+            }
+        } else {
+            // (c) echelon form of the chunk by pivot steps, ONE block barrier per pivot.  Every
+            //     candidate (warp-owned, <= 4 per warp) finds its leading column (from a cursor: leads
+            //     only move right); the smallest (lead, physical row) key becomes the next head, and
+            //     every other candidate with a nonzero f at that column is cross-eliminated,
+            //         row <- v_h * row - f * head           (v_h = the head's leading value),
+            //     i.e. replaced by a nonzero multiple of its reduced form: no inverse on the chain,
+            //     and E (the coefficients) follows the row, so row = E * candidates still holds.  A
+            //     head is never written again, so reading it needs no barrier beyond the one that
+            //     elected it.  Keys rotate over three slots (a slot is reset two steps after use).
+            {
+                __shared__ uint32_t skey[3];
+                if (tid < 3) skey[tid] = NONE16;
+                for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
+                __syncthreads();
+                int slot = 0, nsteps = 0;
                 for (;;) {
-                    uint32_t ld = NONE16;
-                    for (; base < ldv; base += 32) {
-                        const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
-                        if (m) { ld = base + __ffs(m) - 1; break; }
+                    nsteps++;
+                    uint32_t best = NONE16;
+                    for (int ci = warp; ci < ncand; ci += 32) {
+                        const uint32_t q = freel[ci];
+                        if (cstat[q] != 1) continue;
+                        const uint16_t *xr = X + q * LDX;
+                        uint32_t ld = NONE16;
+                        for (int base = (int)(clead[q] & ~31u); base < ldv; base += 32) {
+                            const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
+                            if (m) { ld = base + __ffs(m) - 1; break; }
+                        }
+                        __syncwarp();
+                        if (ld == NONE16) {                       // dependent: zero on the panel
+                            if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
+                        } else {
+                            if (lane == 0) clead[q] = ld;
+                            const uint32_t key = (ld << 7) | q;
+                            best = key < best ? key : best;
+                        }
+                        __syncwarp();
                     }
-                    if (ld == NONE16) {                       // dependent: zero on the panel
-                        if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
-                        break;
-                    }
-                    const uint32_t hq = hmap[ld];
-                    if (hq == NONE16) {
-                        if (lane == 0) clead[q] = ld;
-                        break;
-                    }
+                    if (lane == 0 && best != NONE16) atomicMin(&skey[slot], best);
+                    if (tid == 0) skey[slot == 0 ? 2 : slot - 1] = NONE16;
+                    __syncthreads();
+                    const uint32_t key = skey[slot];
+                    slot = slot == 2 ? 0 : slot + 1;
+                    if (key == NONE16) break;
+                    const uint32_t c = key >> 7, hq = key & 127u;
                     const uint16_t *hr = X + hq * LDX;
-                    // dense mode: heads are normalized; wide mode: scale by the head's inverse
-                    const uint32_t gl = dense ? xr[ld] : mod32(xr[ld] * hinv[hq], p, m32);
-                    const uint32_t ng = gl ? p - gl : 0;
+                    const uint32_t vh = hr[c];
+                    for (int ci = warp; ci < ncand; ci += 32) {
+                        const uint32_t q = freel[ci];
+                        if (cstat[q] != 1) continue;
+                        if (q == hq) {                            // the new head (owned by this warp)
+                            __syncwarp();
+                            if (lane == 0) cstat[q] = 2;
+                            __syncwarp();
+                            continue;
+                        }
+                        uint16_t *xr = X + q * LDX;
+                        const uint32_t f = xr[c];
+                        __syncwarp();
+                        if (!f) continue;
+                        const uint32_t nf = p - f;
+                        for (int k = (int)(c & ~31u) + lane; k < ldv; k += 32)
+                            xr[k] = (uint16_t)mod32(mod32(vh * xr[k], p, m32) + nf * hr[k], p, m32);
+                        for (int k = lane; k < PK; k += 32)
+                            xr[PW + k] = (uint16_t)mod32(mod32(vh * xr[PW + k], p, m32) + nf * hr[PW + k], p, m32);
+                        __syncwarp();
+                    }
+                }
+                if (trace && tid == 0) trace[8] += nsteps;
+                P2_LAP(3);
+                // heads: 1 / leading value (wide mode keeps the row), or normalized rows (dense mode)
+                for (int ci = warp; ci < ncand; ci += 32) {
+                    const uint32_t q = freel[ci];
+                    if (cstat[q] != 2) continue;
+                    uint16_t *xr = X + q * LDX;
+                    const uint32_t iv = invtab[xr[clead[q]]];
                     __syncwarp();
-                    for (int k = base + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(xr[k] + ng * hr[k], p, m32);
-                    for (int k = lane; k < PK; k += 32)
-                        xr[PW + k] = (uint16_t)mod32(xr[PW + k] + ng * hr[PW + k], p, m32);
+                    if (!dense) {
+                        if (lane == 0) hinv[q] = iv;
+                        continue;
+                    }
+                    for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
+                    for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
                     __syncwarp();
                 }
+                __syncthreads();
+                P2_LAP(4);
             }
-            for (int k = tid; k < width; k += NT) hist[k] = NONE16;
-            __syncthreads();
-            P2_LAP(3);
-            // (c2) one new head per leading column among the remaining candidates
-            for (int ci = tid; ci < ncand; ci += NT) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] == 1) atomicMin(&hist[clead[q]], q);
-            }
-            __syncthreads();
-            int coll = 0;
-            for (int ci = tid; ci < ncand; ci += NT) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] == 1) {
-                    if (hist[clead[q]] == q) cstat[q] = 4;     // new head: normalize below
-                    else coll = 1;                              // eliminated next round
-                }
-            }
-            coll = __syncthreads_count(coll);               // rows that lost their column this round
-            for (int ci = warp; ci < ncand; ci += 32) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] != 4) continue;
-                uint16_t *xr = X + q * LDX;
-                const uint32_t iv = invtab[xr[clead[q]]];
-                if (!dense) {                       // wide mode: keep the row, remember 1 / lead value
-                    if (lane == 0) hinv[q] = iv;
-                    continue;
-                }
-                __syncwarp();
-                for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
-                for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
-            }
-            __syncthreads();
-            for (int ci = tid; ci < ncand; ci += NT) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] == 4) { cstat[q] = 2; hmap[clead[q]] = q; }
-            }
-            __syncthreads();
-            P2_LAP(4);
-            if (!coll) break;
         }
         // (d) the chunk's heads, sorted by leading column, become basis slots nb .. nb+h-1
         if (tid < ncand) {
@@ -609,11 +710,39 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             }
             __syncthreads();
             P2_LAP(13);
-            // levels s = 1, 2, .., 64: every aligned 2s-block [[A, B], [0, C]] with A^-1, C^-1 known
+            // the 32 x 32 diagonal blocks of W, one warp each (warp d: rows / columns 32d ..): lane j
+            // holds column j in registers and the rows are back-substituted from the bottom,
+            // W[i][j] = -sum_{i<k<=j} U[i][k] W[k][j]  (u64 sums of < 32 products < 2^37)
+            if (warp < 4 && 32 * warp < (int)nb) {
+                const int base = 32 * warp;
+                const int bs = (int)nb - base < 32 ? (int)nb - base : 32;
+                uint32_t w[32];
+#pragma unroll
+                for (int i = 31; i >= 0; i--) {
+                    uint32_t v = (i == lane) ? 1u : 0u;
+                    if (i < bs && i < lane) {
+                        uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+                        for (int k = i + 1; k < 32; k++) {
+                            const uint64_t t = (uint64_t)U[base + i][base + k] * w[k];
+                            if (k & 1) a1 += t; else a0 += t;
+                        }
+                        const uint32_t z = fmod64(a0 + a1, F);
+                        v = z ? p - z : 0;
+                    }
+                    w[i] = v;
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                    if (i < bs) WM(base + i, base + lane) = (uint16_t)w[i];
+            }
+            __syncthreads();
+            P2_LAP(14);
+            // levels s = 32, 64: every aligned 2s-block [[A, B], [0, C]] with A^-1, C^-1 known
             // gets Q = B C^-1, then -A^-1 Q.  One item = one row r and 4 consecutive columns (s >= 4):
             // the U / W element of a step is shared by the 4 products.  W and Q are upper triangular
             // with zeros beyond nb, so the sums need no per-column bounds.
-            for (int s = 1, ls = 0; s < PK && s < (int)nb; s <<= 1, ls++) {
+            for (int s = 32, ls = 5; s < PK && s < (int)nb; s <<= 1, ls++) {
                 const int cw = s >= 4 ? 4 : s, lcw = s >= 4 ? 2 : ls;   // columns per item, log2
                 const int lg = ls - lcw;                                 // log2(column groups per row)
                 const int npair = ((int)nb + 2 * s - 1) >> (ls + 1);     // pairs with base < nb
@@ -931,11 +1060,19 @@ __global__ void k_sp_begin(const P2State *__restrict__ ps, int64_t nN, int G, in
 }
 
 // transposed limb planes of D[S, c0:]: B operand tiles (64 columns x K = 128) of the Rn GEMM
+// ops != NULL (look-ahead path, where the Rn GEMM commits D[S] itself): this panel's op counts
 __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
-                             const P2State *__restrict__ ps, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi)
+                             const P2State *__restrict__ ps, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi,
+                             unsigned long long *__restrict__ ops)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
+    if (ops && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && ps->c0 < nN) {
+        const unsigned long long w = (unsigned long long)(nN - ps->c0);
+        ops[0] += (unsigned long long)ps->nrows * ps->kp * w;                 // trailing update
+        ops[1] += (unsigned long long)ps->kp * ps->kp * w;                     // new pivot rows
+        ops[2] += (unsigned long long)ps->ncand * ps->kp * (unsigned long long)(ps->c1 - ps->c0);   // panel RREF
+    }
     const uint32_t kp = ps->kp;
     if (kp == 0) return;
     const int64_t c0 = ps->c0;
@@ -1275,7 +1412,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     auto p_factor = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         kt_mark_on(h, KT_PANEL, s);
-        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32};
+        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32, panel_lumode()};
         k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace);
         kt_mark_on(h, KT_PANEL, s);
         note_launch();
@@ -1361,12 +1498,15 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 if (status != GBLA_OK) break;
             }
             launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN, (const uint16_t *)h->D,
-                       ldD, (const P2State *)cur, Blo, Bhi);
+                       ldD, (const P2State *)cur, Blo, Bhi, lookahead ? dops : (unsigned long long *)nullptr);
             note_launch();
             kt_mark(h, KT_RN);
-            // look-ahead: only the window part of Rn is on the chain to the next panel
-            status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth, &cur->c0,
-                                      &cur->kp, &cur->c1, PW, lookahead ? 1 : 0);
+            // look-ahead: only the window part of Rn is on the chain to the next panel, and the Rn
+            // GEMM writes D[S, c0:] = Rn itself (no commit kernel on the chain)
+            status = lookahead ? modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth,
+                                                  &cur->c0, &cur->kp, &cur->c1, PW, 1, cur->sel)
+                               : modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth,
+                                                  &cur->c0, &cur->kp, &cur->c1, PW, 0);
             kt_mark(h, KT_RN);
             if (status != GBLA_OK) break;
             if (!lookahead) {
@@ -1384,9 +1524,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 if (status != GBLA_OK) break;
-                launch_pdl(k_commit2, dim3(h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD, (const P2State *)cur,
-                           (const uint16_t *)Rn, ldR, dops, 1, (const uint8_t *)nullptr, 0);
-                note_launch();
                 if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1)) != GBLA_OK) break;   // next window
                 p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
@@ -1399,17 +1536,14 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 if (cudaEventRecord(evB, side) != cudaSuccess) { fail("event"); break; }
                 tmark(k, st);
                 kt_mark(h, KT_RN);
-                status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth, &cur->c0,
-                                          &cur->kp, &cur->c1, PW, 2);
+                status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
+                                          &cur->kp, &cur->c1, PW, 2, cur->sel);
                 kt_mark(h, KT_RN);
                 if (status != GBLA_OK) break;
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
-                launch_pdl(k_commit2, dim3(2 * h->ctx->sm_count), dim3(256), 0, st, nN, h->D, ldD,
-                           (const P2State *)cur, (const uint16_t *)Rn, ldR, dops, 2, (const uint8_t *)nullptr, 0);
-                note_launch();
                 if (G > 1 && j == G - 1) {              // end of the super-panel: the deferred columns
                     if ((status = sp_flush(cur, 2)) != GBLA_OK || (status = sp_begin(cur)) != GBLA_OK) break;
                 }
@@ -1467,8 +1601,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_CUDA_TRY(cudaMemcpy(tr, trace, sizeof tr, cudaMemcpyDeviceToHost));
         const double n = tr[9] ? (double)tr[9] : 1.0;
         fprintf(stderr,
-                "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f rounds(c1) %.0f "
-                "rounds(c2) %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f inverse %.0f T %.0f; rounds/panel %.2f "
+                "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f reduce+LU %.0f "
+                "heads %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f inverse %.0f T %.0f; LU steps/panel %.2f "
                 "candidates %.1f pivots %.1f width %.1f\n",
                 tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[13] / n, tr[14] / n,
                 tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
@@ -1619,7 +1753,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
             }
         }
         // the same panel factorization on every rank
-        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap};
+        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap, 0, panel_lumode()};
         kt_mark(h, KT_PANEL);
         k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr);
         kt_mark(h, KT_PANEL);

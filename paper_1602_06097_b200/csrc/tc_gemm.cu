@@ -114,8 +114,11 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     if (g.c0_dev) {
         c0 = *g.c0_dev;
         cols -= c0;
-        if (MODE == MODE_SUB) C += c0;
+        if (MODE == MODE_SUB || g.rowidx) C += c0;
     }
+    // MODE_STORE with rowidx: row slot of the result goes straight to C[rowidx[slot], c0 + x] for
+    // slot < *skip_dev (the echelon's commit D[S, c0:] = Rn fused into the Rn GEMM)
+    const int64_t nwr = (MODE == MODE_STORE && g.rowidx) ? (int64_t)*g.skip_dev : INT64_MAX;
     if (cols <= 0) return;
     const int64_t nr = g.nrows_dev ? (int64_t)*g.nrows_dev : g.nrows;
     const int64_t ntr = (nr + BM - 1) / BM, ntc_all = (cols + BN - 1) / BN;
@@ -326,11 +329,11 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             live_n = slot_n < nr;
             if (rt != rt_c) {
                 rt_c = rt;
-                rowbase = live_n ? C + (size_t)(MODE == MODE_SUB && g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc
-                                 : nullptr;
+                rowbase = live_n && slot_n < nwr ? C + (size_t)(g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc
+                                                 : nullptr;
             }
-            crow_n = live_n ? rowbase + x0_n : nullptr;
-            fast_n = live_n && vec && x0_n + EPI_COLS <= cols;
+            crow_n = live_n && slot_n < nwr ? rowbase + x0_n : nullptr;
+            fast_n = crow_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
             for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
             if (MODE == MODE_SUB && live_n) {
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
 #pragma unroll
                 for (int u = 0; u < EPI_COLS / 8; u++)
                     reinterpret_cast<uint4 *>(crow)[u] = make_uint4(dv[4 * u], dv[4 * u + 1], dv[4 * u + 2], dv[4 * u + 3]);
-            } else if (live) {
+            } else if (crow) {
 #pragma unroll
                 for (int j = 0; j < EPI_COLS; j++)
                     if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
@@ -536,13 +539,14 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel)
+                             int64_t win_w, int ctsel, const uint32_t *orows)
 {
+    if (orows && (!skip_dev || !c0_dev)) { set_error("modgemm_tc_store: row map needs the pivot count"); return GBLA_E_INVAL; }
     if (cols <= 0) return GBLA_OK;
     const int64_t tiles = (cols + BN - 1) / BN;
     int64_t grid = (tiles + 1) / 2;                       // two column tiles per CTA (TMEM double buffer)
     if (grid > g_sms) grid = g_sms;
-    MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, nullptr, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
+    MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, orows, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
     GBLA_TRY(launch_ws<MODE_STORE>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
