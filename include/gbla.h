@@ -58,7 +58,11 @@ typedef enum {
 #define GBLA_SPARSE_INT      0x10u  /* sparse phase: per-target multiline AXPY (INT pipe)  */
 #define GBLA_DENSE_INT       0x20u  /* echelon trailing update on the INT pipe             */
 #define GBLA_DENSE_TC        0x40u  /* echelon trailing update on tcgen05 (u8-limb IMMA)   */
-#define GBLA_FLAGS_ALL       0x7Fu
+#define GBLA_ECHELON_REF     0x80u  /* echelon_D: row echelon form only, no elimination
+                                       above the pivots (rank / reduction-of-D use case of
+                                       the F5 runs; Alg 3's non-reduced echelon,
+                                       P:715-740)                          */
+#define GBLA_FLAGS_ALL       0xFFu
 
 /* ---- input ------------------------------------------------------------ */
 /* Sparse matrix M (m x n) over GF(p) in CSR: row i holds the entries
@@ -131,6 +135,11 @@ gbla_status gbla_update_D(gbla_mat h, void *stream);
  * zero rows dropped.  *rank = rows(R); rank(M) = n_piv + rank.
  * Echelons the CURRENT D (callable after any of the above).  flags select
  * the trailing-update engine (GBLA_DENSE_TC default, GBLA_DENSE_INT).
+ * GBLA_ECHELON_REF: skip the back elimination (rows are never reduced by
+ * later pivots): R is then a row echelon form of D -- rows sorted by pivot
+ * column, leading 1, zero below every pivot, the same pivot columns and rank
+ * as the RREF, RREF(R) = the fully reduced result -- but not canonical (the
+ * entries above later pivots depend on the panel boundaries).
  * Synchronizes `stream`. */
 gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *rank);
 

@@ -28,6 +28,7 @@ GBLA_KEEP_CPRIME = 0x08
 GBLA_SPARSE_INT = 0x10
 GBLA_DENSE_INT = 0x20
 GBLA_DENSE_TC = 0x40
+GBLA_ECHELON_REF = 0x80     # echelon_D: row echelon form only
 
 _STATUS = {0: "GBLA_OK", 1: "GBLA_E_INVAL", 2: "GBLA_E_DOMAIN", 3: "GBLA_E_ORDER", 4: "GBLA_E_NOMEM",
            5: "GBLA_E_CUDA", 6: "GBLA_E_NCCL", 7: "GBLA_E_INTERNAL"}

@@ -358,7 +358,7 @@ extern "C" gbla_status gbla_update_D(gbla_mat h, void *stream)
 extern "C" gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *rank)
 {
     GBLA_TRY(check_mat(h, stream));
-    if (flags & ~(uint32_t)(GBLA_DENSE_INT | GBLA_DENSE_TC)) {
+    if (flags & ~(uint32_t)(GBLA_DENSE_INT | GBLA_DENSE_TC | GBLA_ECHELON_REF)) {
         set_error("gbla_echelon_D: unsupported flags 0x%x", flags);
         return GBLA_E_INVAL;
     }
@@ -393,7 +393,8 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     } else {
         s = gbla_reduce_C(h, GBLA_FUSE_D | (flags & (GBLA_KEEP_CPRIME | GBLA_SPARSE_INT)), stream);
     }
-    if (s == GBLA_OK) s = gbla_echelon_D(h, flags & (GBLA_DENSE_INT | GBLA_DENSE_TC), stream, nullptr);
+    if (s == GBLA_OK)
+        s = gbla_echelon_D(h, flags & (GBLA_DENSE_INT | GBLA_DENSE_TC | GBLA_ECHELON_REF), stream, nullptr);
     if (s != GBLA_OK) { gbla_mat_free(h); return s; }
     *out = h;
     return GBLA_OK;

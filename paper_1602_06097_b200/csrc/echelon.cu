@@ -419,7 +419,7 @@ template <int PK, bool TC>
 __global__ void k_gather(int64_t mN, int64_t c0, const uint16_t *__restrict__ D, int64_t ldD,
                          const uint32_t *__restrict__ rowpiv, PanelState<PK> *__restrict__ ps,
                          uint16_t *__restrict__ Fc, uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi,
-                         uint32_t *__restrict__ rows)
+                         uint32_t *__restrict__ rows, int ref)
 {
     // one warp per row; lane l holds coefficients b = l*CPL .. l*CPL+CPL-1
     constexpr int CPL = PK / 32;
@@ -428,7 +428,7 @@ __global__ void k_gather(int64_t mN, int64_t c0, const uint16_t *__restrict__ D,
     const uint32_t kp = ps->kp;
     if (i >= mN || kp == 0) return;
     const uint32_t rp = rowpiv[i];
-    if (rp != GBLA_NONE && rp >= (uint64_t)c0) return;   // selected now: becomes Rn
+    if (rp != GBLA_NONE && (rp >= (uint64_t)c0 || ref)) return;   // selected now: becomes Rn (REF: any pivot row)
     const uint16_t *drow = D + (size_t)i * ldD;
     uint16_t v[CPL];
     bool nz = false;
@@ -640,7 +640,7 @@ gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                                         invtab, cflag, nullptr);
         note_launch();
         k_gather<PK, false><<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, c0, h->D, ldD, rowpiv, ps, Fc, nullptr, nullptr,
-                                                              rows);
+                                                              rows, h->ref_only ? 1 : 0);
         k_rnew<PK><<<dim3(grid_for(width, 256), PK), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps, Rn, ldR);
         k_trailing_int<<<dim3(grid_for(width, 256), grid_for(mN, 32)), 256, 0, st>>>(nN, c0, h->F, h->D, ldD, ps,
                                                                                       Fc, rows, Rn, ldR);
@@ -657,6 +657,7 @@ gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
 gbla_status echelon_impl(gbla_mat h, uint32_t flags)
 {
     cudaStream_t st = h->stream;
+    h->ref_only = (flags & GBLA_ECHELON_REF) != 0;
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD;
     uint32_t *rowpiv, *colrow, *cflag, *cidx;
     uint16_t *invtab;

@@ -181,6 +181,7 @@ struct gbla_mat_s {
     // call-order state
     bool did_reduce_B = false, did_cprime = false, did_update = false, did_fused = false;
     bool have_xt = false;              // C' held as tensor-core tiles (sparse_tc.cu)
+    bool ref_only = false;             // GBLA_ECHELON_REF: no back elimination in the echelon
     bool dist_rows = false;            // D is row-sharded over the ranks (dist_sparse_phase)
     float phase_ms[5] = {0, 0, 0, 0, 0};
 

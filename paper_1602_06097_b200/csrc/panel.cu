@@ -986,7 +986,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           const uint32_t *__restrict__ rowpiv, P2State *__restrict__ ps,
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
                           const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
-                          uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr)
+                          uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr,
+                          int ref = 0)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -999,7 +1000,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     if (owner && owner[i] != me) continue;                     // another rank's row
     const uint32_t rp = rowpiv[i];
-    if (rp != GBLA_NONE && rp >= (uint64_t)ps->c0) continue;   // selected now: becomes Rn
+    if (rp != GBLA_NONE && (rp >= (uint64_t)ps->c0 || ref)) continue;   // selected now: becomes Rn;
+                                                                         // REF: no back elimination
     const uint16_t *drow = D + (size_t)i * ldD;
     uint16_t v[CPL];
     bool nz = false;
@@ -1422,7 +1424,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         // one warp per row, blocks in row order: the row list (and the D rows of each 128-row tile
         // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
-                                                         rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0);
+                                                         rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0,
+                                                         h->ref_only ? 1 : 0);
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
@@ -1500,6 +1503,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN, (const uint16_t *)h->D,
                        ldD, (const P2State *)cur, Blo, Bhi, lookahead ? dops : (unsigned long long *)nullptr);
             note_launch();
+            if (lookahead) tmark(k, st);
             kt_mark(h, KT_RN);
             // look-ahead: only the window part of Rn is on the chain to the next panel, and the Rn
             // GEMM writes D[S, c0:] = Rn itself (no commit kernel on the chain)
@@ -1508,6 +1512,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                : modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth,
                                                   &cur->c0, &cur->kp, &cur->c1, PW, 0);
             kt_mark(h, KT_RN);
+            if (lookahead) tmark(k, st);
             if (status != GBLA_OK) break;
             if (!lookahead) {
                 kt_mark(h, KT_TRAIL);
@@ -1524,6 +1529,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 if (status != GBLA_OK) break;
+                tmark(k, st);
                 if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1)) != GBLA_OK) break;   // next window
                 p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
@@ -1587,11 +1593,14 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     if (!tl.empty()) {
         cudaDeviceSynchronize();
         // per iteration (us from its start): side panel start, end; main rest start, end; gather end
-        for (size_t i = 0; i + 6 <= tl.size(); i += 6) {
-            float a[6];
-            for (int j = 0; j < 6; j++) cudaEventElapsedTime(&a[j], tl[i], tl[i + j]);
-            fprintf(stderr, "[gbla timeline] it %zu: panel %.1f..%.1f (%.1f) | rest %.1f..%.1f | gather done %.1f\n",
-                    i / 6, a[1] * 1e3, a[2] * 1e3, (a[2] - a[1]) * 1e3, a[3] * 1e3, a[4] * 1e3, a[5] * 1e3);
+        // per iteration (us from its start): B tiles, Rn window, window update done (main stream);
+        // side panel start, end; main rest start, end; gather done
+        for (size_t i = 0; i + 9 <= tl.size(); i += 9) {
+            float a[9];
+            for (int j = 0; j < 9; j++) cudaEventElapsedTime(&a[j], tl[i], tl[i + j]);
+            fprintf(stderr, "[gbla timeline] it %zu: Btiles %.1f Rn-win %.1f upd-win %.1f | panel %.1f..%.1f (%.1f) | "
+                    "rest %.1f..%.1f | gather done %.1f\n", i / 9, a[1] * 1e3, a[2] * 1e3, a[3] * 1e3, a[4] * 1e3,
+                    a[5] * 1e3, (a[5] - a[4]) * 1e3, a[6] * 1e3, a[7] * 1e3, a[8] * 1e3);
         }
         for (cudaEvent_t e : tl) cudaEventDestroy(e);
     }
@@ -1780,7 +1789,8 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         // K11 on own rows (emulated: every rank's rows in one list), own S rows = Rn
         for (int j = 0; j < nloc; j++) {
             k_gather2<<<grid_for(mN * 32, 256), 256, 0, st>>>(mN, h->D, ldD, rowpiv, cur, Flo, Fhi, rows, owner,
-                                                              rank_of(j));
+                                                              rank_of(j), nullptr, nullptr, 1, 0, nullptr,
+                                                              h->ref_only ? 1 : 0);
             note_launch();
         }
         kt_mark(h, KT_TRAIL);

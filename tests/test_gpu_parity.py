@@ -368,6 +368,52 @@ def test_echelon_engines_agree_c0_and_dense(gb, ctx, c0_matrix, c0_oracle):
             check_full(gb, ctx, M, res, flags=f)
 
 
+def check_ref(gb, h, res, p):
+    """GBLA_ECHELON_REF output against the oracle: same rank and pivot columns, leading 1s, zeros
+    left of every pivot and below it, and RREF(R_ref) (computed by the oracle) = the oracle's R."""
+    r, pc, R = h.rref()
+    R, pc = np_(R), np_(pc)
+    assert r == res.rank and np.array_equal(pc, res.pivcol)
+    if r:
+        rows = np.arange(r)
+        assert np.all(R[rows, pc] == 1)
+        cols = np.arange(R.shape[1])
+        assert not np.any(R[cols[None, :] < pc[:, None]])              # zero left of the pivot
+        below = R[:, pc]                                                  # column pc[i] of row j
+        assert not np.any(np.tril(below, -1))                             # zero below every pivot
+    r2, R2, pc2 = oracle.rref(R, p)
+    assert r2 == res.rank and np.array_equal(pc2, res.pivcol) and np.array_equal(R2, res.R)
+    return R
+
+
+def test_echelon_ref_mode(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """the row echelon form without back elimination (GBLA_ECHELON_REF), on both
+    trailing-update engines, with look-ahead and super-panels, and with emulated ranks.  On a
+    multi-panel D it must really skip the back elimination (R_ref != R somewhere)."""
+    cases = [(c0_matrix, c0_oracle)]
+    for name, sc in (("c1", 0.05), ("c3", 0.03)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        cases.append((M, oracle.reduce(M)))
+    for i, (M, res) in enumerate(cases):
+        for f in (gb.GBLA_DENSE_TC, gb.GBLA_DENSE_INT):
+            h = gpu_reduce(gb, ctx, M, flags=f | gb.GBLA_ECHELON_REF)
+            R = check_ref(gb, h, res, M.p)
+            if i == 1:
+                assert not np.array_equal(R, res.R), "REF mode did a full reduction"
+            h.free()
+    M, res = cases[2]
+    monkeypatch.setenv("GBLA_SP", "4")                                    # deferred updates
+    h = gpu_reduce(gb, ctx, M, flags=gb.GBLA_ECHELON_REF)
+    check_ref(gb, h, res, M.p)
+    h.free()
+    monkeypatch.delenv("GBLA_SP")
+    monkeypatch.setenv("GBLA_DIST_EMULATE", "3")
+    h = gpu_reduce(gb, ctx, M, flags=gb.GBLA_ECHELON_REF)
+    check_ref(gb, h, res, M.p)
+    h.free()
+    monkeypatch.delenv("GBLA_DIST_EMULATE")
+
+
 def test_sharded_sparse_phase_emulated_ranks(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     """Multi-GPU row sharding (dist.cu), with G ranks emulated on one GPU
     (GBLA_DIST_EMULATE): each shard sweeps only its cyclic target tiles, the
