@@ -479,30 +479,42 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         // (c) echelon form of the chunk: parallel rounds (staircase panels: many distinct leads)
         //     or pivot steps (dense panels: the rounds would elect one head per round)
         if (!use_lu(dense, src.lumode)) {
-            for (int k = tid; k < width; k += NT) hmap[k] = NONE16;
+            // Two block barriers per round: (c1) every remaining candidate (warp per row) finds
+            // its leading column from a cursor (leads only move right) and, while an established
+            // head owns it, eliminates it (heads are fixed: no block sync); then it bids for its
+            // column (atomicMin of its physical row in this round's election buffer) and prefetches
+            // 1 / its leading value.  (c2) the winner of every column becomes a head; the other
+            // buffer is cleared for the next round.
+            uint32_t *elect[2] = {hist, clist};      // clist is dead once the candidates are loaded
+            for (int k = tid; k < width; k += NT) { hmap[k] = NONE16; hist[k] = NONE16; clist[k] = NONE16; }
+            for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
             __syncthreads();
-            for (;;) {
+            for (int round = 0;; round++) {
                 if (trace && tid == 0) trace[8] += 1;
-                // (c1) every remaining candidate (warp per row): leading column; while an established
-                //      head owns it, eliminate it (heads are fixed, so this chain needs no block sync)
+                uint32_t *hb = elect[round & 1];
                 for (int ci = warp; ci < ncand; ci += 32) {
                     const uint32_t q = freel[ci];
                     if (cstat[q] != 1) continue;
                     uint16_t *xr = X + q * LDX;
-                    int base = 0;
+                    int base = (int)(clead[q] & ~31u);
                     for (;;) {
                         uint32_t ld = NONE16;
                         for (; base < ldv; base += 32) {
                             const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
                             if (m) { ld = base + __ffs(m) - 1; break; }
                         }
+                        __syncwarp();
                         if (ld == NONE16) {                       // dependent: zero on the panel
                             if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
                             break;
                         }
                         const uint32_t hq = hmap[ld];
                         if (hq == NONE16) {
-                            if (lane == 0) clead[q] = ld;
+                            if (lane == 0) {
+                                clead[q] = ld;
+                                atomicMin(&hb[ld], q);
+                                hinv[q] = invtab[xr[ld]];
+                            }
                             break;
                         }
                         const uint16_t *hr = X + hq * LDX;
@@ -515,44 +527,28 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                             xr[PW + k] = (uint16_t)mod32(xr[PW + k] + ng * hr[PW + k], p, m32);
                         __syncwarp();
                     }
+                    __syncwarp();
                 }
-                for (int k = tid; k < width; k += NT) hist[k] = NONE16;
                 __syncthreads();
                 P2_LAP(3);
-                // (c2) one new head per leading column among the remaining candidates
-                for (int ci = tid; ci < ncand; ci += NT) {
-                    const uint32_t q = freel[ci];
-                    if (cstat[q] == 1) atomicMin(&hist[clead[q]], q);
-                }
-                __syncthreads();
                 int coll = 0;
-                for (int ci = tid; ci < ncand; ci += NT) {
-                    const uint32_t q = freel[ci];
-                    if (cstat[q] == 1) {
-                        if (hist[clead[q]] == q) cstat[q] = 4;     // new head: normalize below
-                        else coll = 1;                              // eliminated next round
-                    }
-                }
-                coll = __syncthreads_count(coll);               // rows that lost their column this round
                 for (int ci = warp; ci < ncand; ci += 32) {
                     const uint32_t q = freel[ci];
-                    if (cstat[q] != 4) continue;
-                    uint16_t *xr = X + q * LDX;
-                    const uint32_t iv = invtab[xr[clead[q]]];
-                    if (!dense) {                       // wide mode: keep the row, remember 1 / lead value
-                        if (lane == 0) hinv[q] = iv;
-                        continue;
+                    if (cstat[q] != 1) continue;
+                    if (hb[clead[q]] != q) { coll = 1; continue; }     // eliminated next round
+                    __syncwarp();
+                    if (lane == 0) { cstat[q] = 2; hmap[clead[q]] = q; }
+                    if (dense) {                                          // normalized heads
+                        uint16_t *xr = X + q * LDX;
+                        const uint32_t iv = hinv[q];
+                        for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
+                        for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
                     }
                     __syncwarp();
-                    for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
-                    for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
                 }
-                __syncthreads();
-                for (int ci = tid; ci < ncand; ci += NT) {
-                    const uint32_t q = freel[ci];
-                    if (cstat[q] == 4) { cstat[q] = 2; hmap[clead[q]] = q; }
-                }
-                __syncthreads();
+                uint32_t *ob = elect[(round + 1) & 1];
+                for (int k = tid; k < width; k += NT) ob[k] = NONE16;
+                coll = __syncthreads_count(coll);
                 P2_LAP(4);
                 if (!coll) break;
             }
@@ -689,6 +685,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // W by doubling block sizes (128 x 128, entries beyond nb: identity), then T with the
             // zero entries of E' skipped (E' is nearly diagonal on a staircase).  The value rows
             // are dead now: W and Q live in their first 512 bytes.
+            // T = U^-1 E' by a blocked back substitution over 32-slot row blocks, bottom up:
+            //     T_I = W_II (E'_I - U_{I,>I} T_{>I}),   W_II = (U_II)^-1 (one warp per block),
+            // warp w <-> row 32 I + w of the block, lane l <-> columns 4l .. 4l+3 of T, so the U
+            // element of a step is warp-uniform and the T row segment one 8-byte shared load.
+            // u64 sums (< 128 products < 2^32 each); the value rows are dead now: T lives in
+            // columns [0, 128) of store rows 0..127, the residual in [128, 256), W_II in [256, 288).
             uint16_t(*U)[PK] = FS;
             for (int idx = tid; idx < (int)nb * PK; idx += NT) {   // rows >= nb and columns >= nb are never read
                 const int b = idx >> 7, b2 = idx & (PK - 1);
@@ -697,22 +699,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 U[b][b2] = (uint16_t)v;
             }
             __syncthreads();
-            // bphys is a permutation of the physical rows 0..nb-1 only if the chunk filled them;
-            // W / Q rows are indexed by logical slot b in 0..127 (all rows of the store exist)
-#define WM(i_, j_) X[(i_) * LDX + (j_)]
-#define QM(i_, j_) X[(i_) * LDX + PK + (j_)]
-            // the E rows (coefficients at offset PW) of every physical row stay untouched
-            for (int idx = tid; idx < (int)nb * (PK / 8); idx += NT) {   // rows < nb of the identity, 8 columns a store
-                const int i = idx >> 4, c8 = (idx & 15) * 8;
-                uint4 z = make_uint4(0, 0, 0, 0);
-                if ((i & ~7) == c8) reinterpret_cast<uint16_t *>(&z)[i & 7] = 1;
-                *reinterpret_cast<uint4 *>(&WM(i, c8)) = z;
-            }
-            __syncthreads();
+#define TM(i_, j_) X[(i_) * LDX + (j_)]
+#define RM(i_, j_) X[(i_) * LDX + PK + (j_)]
+#define WD(i_, j_) X[(i_) * LDX + 2 * PK + (j_)]
             P2_LAP(13);
-            // the 32 x 32 diagonal blocks of W, one warp each (warp d: rows / columns 32d ..): lane j
-            // holds column j in registers and the rows are back-substituted from the bottom,
-            // W[i][j] = -sum_{i<k<=j} U[i][k] W[k][j]  (u64 sums of < 32 products < 2^37)
+            // W_II: warp I inverts diagonal block I (lane j holds column j; rows from the bottom,
+            // W[i][j] = -sum_{i<k<=j} U[i][k] W[k][j]); rows >= nb are the identity
             if (warp < 4 && 32 * warp < (int)nb) {
                 const int base = 32 * warp;
                 const int bs = (int)nb - base < 32 ? (int)nb - base : 32;
@@ -733,125 +725,77 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                     w[i] = v;
                 }
 #pragma unroll
-                for (int i = 0; i < 32; i++)
-                    if (i < bs) WM(base + i, base + lane) = (uint16_t)w[i];
+                for (int i = 0; i < 32; i++) WD(base + i, lane) = (uint16_t)w[i];
             }
             __syncthreads();
             P2_LAP(14);
-            // levels s = 32, 64: every aligned 2s-block [[A, B], [0, C]] with A^-1, C^-1 known
-            // gets Q = B C^-1, then -A^-1 Q.  One item = one row r and 4 consecutive columns (s >= 4):
-            // the U / W element of a step is shared by the 4 products.  W and Q are upper triangular
-            // with zeros beyond nb, so the sums need no per-column bounds.
-            for (int s = 32, ls = 5; s < PK && s < (int)nb; s <<= 1, ls++) {
-                const int cw = s >= 4 ? 4 : s, lcw = s >= 4 ? 2 : ls;   // columns per item, log2
-                const int lg = ls - lcw;                                 // log2(column groups per row)
-                const int npair = ((int)nb + 2 * s - 1) >> (ls + 1);     // pairs with base < nb
-                const int items = npair << (ls + lg);
-                for (int it = tid; it < items; it += NT) {
-                    const int q = it >> (ls + lg), r = (it >> lg) & (s - 1), c0 = (it & ((1 << lg) - 1)) << lcw;
-                    const int base = q << (ls + 1);
-                    if (base + r >= (int)nb || base + s + c0 >= (int)nb) continue;
-                    int kend = c0 + cw;                                  // W[s+k][s+c] = 0 for k > c
-                    if (kend > (int)nb - base - s) kend = (int)nb - base - s;
+            const int nblk = ((int)nb + 31) >> 5;
+            for (int I = nblk - 1; I >= 0; I--) {
+                const int b = 32 * I + warp;                 // this warp's row of block I
+                const int c4 = 4 * lane;                     // this lane's 4 columns (slots)
+                if (b < (int)nb) {
+                    // E'[b][s] = E[phys b][phys s] / h_b[pc_b]
+                    const uint32_t qb = bphys[b], hv = hinv[qb];
+                    uint32_t e[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        e[u] = (c4 + u < (int)nb) ? mod32(X[qb * LDX + PW + bphys[c4 + u]] * hv, p, m32) : 0u;
                     uint64_t acc[4] = {0, 0, 0, 0};
-                    const uint16_t *urow = &U[base + r][base + s];
-                    if (cw == 4) {
+                    const uint16_t *urow = &U[b][0];
 #pragma unroll 4
-                        for (int k = 0; k < kend; k++) {
-                            const uint64_t u = urow[k];
-                            const uint2 w = *reinterpret_cast<const uint2 *>(&WM(base + s + k, base + s + c0));
-                            acc[0] += u * (w.x & 0xffffu); acc[1] += u * (w.x >> 16);
-                            acc[2] += u * (w.y & 0xffffu); acc[3] += u * (w.y >> 16);
-                        }
-                    } else {
-                        for (int k = 0; k < kend; k++)
-                            for (int j = 0; j < cw; j++) acc[j] += (uint64_t)urow[k] * WM(base + s + k, base + s + c0 + j);
+                    for (int k = 32 * (I + 1); k < (int)nb; k++) {
+                        const uint64_t uk = urow[k];
+                        const uint2 t = *reinterpret_cast<const uint2 *>(&TM(k, c4));
+                        acc[0] += uk * (t.x & 0xffffu); acc[1] += uk * (t.x >> 16);
+                        acc[2] += uk * (t.y & 0xffffu); acc[3] += uk * (t.y >> 16);
                     }
-                    for (int j = 0; j < cw; j++) QM(base + r, base + s + c0 + j) = (uint16_t)fmod64(acc[j], F);
+                    uint32_t r[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t z = fmod64(acc[u], F);
+                        r[u] = e[u] >= z ? e[u] - z : e[u] + p - z;
+                    }
+                    *reinterpret_cast<uint2 *>(&RM(b, c4)) = make_uint2(r[0] | (r[1] << 16), r[2] | (r[3] << 16));
                 }
                 __syncthreads();
-                for (int it = tid; it < items; it += NT) {
-                    const int q = it >> (ls + lg), r = (it >> lg) & (s - 1), c0 = (it & ((1 << lg) - 1)) << lcw;
-                    const int base = q << (ls + 1);
-                    if (base + r >= (int)nb || base + s + c0 >= (int)nb) continue;
-                    const int kmax = (base + s <= (int)nb) ? s : (int)nb - base;
+                if (b < (int)nb) {
+                    const int kend = (int)nb - 32 * I < 32 ? (int)nb - 32 * I : 32;
                     uint64_t acc[4] = {0, 0, 0, 0};
-                    const uint16_t *wrow = &WM(base + r, base);
-                    if (cw == 4) {
 #pragma unroll 4
-                        for (int k = r; k < kmax; k++) {
-                            const uint64_t w = wrow[k];
-                            const uint2 qv = *reinterpret_cast<const uint2 *>(&QM(base + k, base + s + c0));
-                            acc[0] += w * (qv.x & 0xffffu); acc[1] += w * (qv.x >> 16);
-                            acc[2] += w * (qv.y & 0xffffu); acc[3] += w * (qv.y >> 16);
-                        }
-                    } else {
-                        for (int k = r; k < kmax; k++)
-                            for (int j = 0; j < cw; j++) acc[j] += (uint64_t)wrow[k] * QM(base + k, base + s + c0 + j);
+                    for (int k = warp; k < kend; k++) {
+                        const uint64_t wk = WD(32 * I + warp, k);
+                        const uint2 t = *reinterpret_cast<const uint2 *>(&RM(32 * I + k, c4));
+                        acc[0] += wk * (t.x & 0xffffu); acc[1] += wk * (t.x >> 16);
+                        acc[2] += wk * (t.y & 0xffffu); acc[3] += wk * (t.y >> 16);
                     }
-                    for (int j = 0; j < cw; j++) {
-                        const uint32_t z = fmod64(acc[j], F);
-                        WM(base + r, base + s + c0 + j) = (uint16_t)(z ? p - z : 0);
-                    }
+                    uint32_t r[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) r[u] = fmod64(acc[u], F);
+                    *reinterpret_cast<uint2 *>(&TM(b, c4)) = make_uint2(r[0] | (r[1] << 16), r[2] | (r[3] << 16));
                 }
                 __syncthreads();
             }
-            P2_LAP(14);
-            // T = W E' -> the T tile (K index = logical slot).  Column s of E' (s = physical row of
-            // a head) has few nonzeros (1 on a staircase: the head itself): list them per column,
-            // (row, value) pairs in the dead value area of store row s, then T[b][ls] =
-            // sum over the list of W[b][row] * value.
-            constexpr int LMAX = 8;
-            uint32_t *lcnt = clead;                               // per physical column (clead is dead)
-            uint16_t *lrow = &FS[0][0], *lval = &FS[0][0] + LMAX * PK;   // [LMAX][PK] each (U is dead)
-            for (int k = tid; k < PK; k += NT) lcnt[k] = 0;
-            __syncthreads();
-            for (int b2 = warp; b2 < (int)nb; b2 += 32) {        // warp per head row: contiguous E row
-                const uint32_t q2 = bphys[b2];
-                const uint32_t hv = hinv[q2];
-                for (int sc = lane; sc < PK; sc += 32) {
-                    const uint32_t e = X[q2 * LDX + PW + sc];
-                    if (!e) continue;
-                    const uint32_t j = atomicAdd(&lcnt[sc], 1u);
-                    if (j < (uint32_t)LMAX) {                     // transposed lists: lanes read
-                        lrow[j * PK + sc] = (uint16_t)b2;         // different columns, not one bank
-                        lval[j * PK + sc] = (uint16_t)mod32(e * hv, p, m32);
-                    }
-                }
-            }
-            __syncthreads();
-            for (int idx = tid; idx < PK * PK / 4; idx += NT) {   // 4 consecutive K entries: one 4-byte store per plane
-                const int b = idx >> 5, l0 = (idx & 31) * 4;
+            // the T tile (limb planes, K index = slot): 4 consecutive K entries per 4-byte store
+            for (int idx = tid; idx < PK * PK / 4; idx += NT) {
+                const int bb = idx >> 5, l0 = (idx & 31) * 4;
                 uint32_t lo = 0, hi = 0;
-                for (int u = 0; u < 4; u++) {
-                    const int ls = l0 + u;
-                    uint32_t v = 0;
-                    if (b < (int)nb && ls < (int)nb) {
-                        const uint32_t sc = bphys[ls];
-                        const uint32_t cnt = lcnt[sc];
-                        uint64_t acc = 0;
-                        if (cnt <= (uint32_t)LMAX) {
-                            for (uint32_t j = 0; j < cnt; j++) {
-                                const uint32_t b2 = lrow[j * PK + sc];
-                                if ((int)b2 >= b) acc += (uint64_t)WM(b, b2) * lval[j * PK + sc];
-                            }
-                        } else {                                  // dense column: every head row
-                            for (int b2 = b; b2 < (int)nb; b2++) {
-                                const uint32_t e = X[bphys[b2] * LDX + PW + sc];
-                                if (e) acc += (uint64_t)WM(b, b2) * mod32(e * hinv[bphys[b2]], p, m32);
-                            }
-                        }
-                        v = fmod64(acc, F);
+                if (bb < (int)nb) {
+                    const uint2 t = *reinterpret_cast<const uint2 *>(&TM(bb, l0));
+                    const uint32_t v[4] = {t.x & 0xffffu, t.x >> 16, t.y & 0xffffu, t.y >> 16};
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t x = (l0 + u < (int)nb) ? v[u] : 0u;
+                        lo |= (x & 0xffu) << (8 * u);
+                        hi |= (x >> 8) << (8 * u);
                     }
-                    lo |= (v & 0xffu) << (8 * u);
-                    hi |= (v >> 8) << (8 * u);
                 }
-                const uint32_t o = tc::toff((uint32_t)b, (uint32_t)l0);
+                const uint32_t o = tc::toff((uint32_t)bb, (uint32_t)l0);
                 *reinterpret_cast<uint32_t *>(Tlo + o) = lo;
                 *reinterpret_cast<uint32_t *>(Thi + o) = hi;
             }
-#undef WM
-#undef QM
+#undef TM
+#undef RM
+#undef WD
             P2_LAP(15);
             break;
         }
