@@ -1009,7 +1009,7 @@ __global__ void k_sp_begin(const P2State *__restrict__ ps, int64_t nN, int G, in
 // ops != NULL (look-ahead path, where the Rn GEMM commits D[S] itself): this panel's op counts
 __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
                              const P2State *__restrict__ ps, uint8_t *__restrict__ Blo, uint8_t *__restrict__ Bhi,
-                             unsigned long long *__restrict__ ops)
+                             unsigned long long *__restrict__ ops, int part)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -1022,8 +1022,12 @@ __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t
     const uint32_t kp = ps->kp;
     if (kp == 0) return;
     const int64_t c0 = ps->c0;
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // part 1: the 64-column tiles of the next panel's window [c1, c1 + PW) (the Rn GEMM's
+    // CT_WINDOW tiles: on the look-ahead chain); part 2: the others; 0: all
+    const int64_t w0 = (ps->c1 - c0) / 64 * 64, w1 = (ps->c1 - c0 + PW + 63) / 64 * 64;
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (part == 1 ? w0 : 0);
     if (c0 + x >= nN) return;
+    if ((part == 1 && x >= w1) || (part == 2 && x >= w0 && x < w1)) return;
     const uint32_t s = blockIdx.y * 16;
     if (s >= kp) {      // zero K rows beyond kp (the tile is reused panel to panel)
         const size_t o = (size_t)(x / 64) * (64 * PK) + tc::toff64((uint32_t)(x % 64), s);
@@ -1444,8 +1448,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
             }
-            launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN, (const uint16_t *)h->D,
-                       ldD, (const P2State *)cur, Blo, Bhi, lookahead ? dops : (unsigned long long *)nullptr);
+            // look-ahead: only the B tiles of the next window are on the chain (the rest: below)
+            launch_pdl(k_gather_st2, dim3(lookahead ? grid_for(PW + 64, 128) : grid_for(nN, 128), PK / 16), dim3(128),
+                       0, st, nN, (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
+                       lookahead ? dops : (unsigned long long *)nullptr, lookahead ? 1 : 0);
             note_launch();
             if (lookahead) tmark(k, st);
             kt_mark(h, KT_RN);
@@ -1485,6 +1491,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 tmark(k, side);
                 if (cudaEventRecord(evB, side) != cudaSuccess) { fail("event"); break; }
                 tmark(k, st);
+                launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, st, nN,
+                           (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
+                           (unsigned long long *)nullptr, 2);
+                note_launch();
                 kt_mark(h, KT_RN);
                 status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
                                           &cur->kp, &cur->c1, PW, 2, cur->sel);
