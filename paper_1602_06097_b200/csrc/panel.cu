@@ -204,6 +204,52 @@ __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, 
     }
 }
 
+// ---- warp-level tensor-core helpers (mma.sync m16n8k32, u8 x u8 -> s32) for the panel's small
+// modular products: u16 residues are split into limbs (lo, hi bytes) and a product is
+// 2^16 HH + 2^8 (HL + LH) + LL.  Fragment layouts: PTX ISA, mma.m16n8k32 (.u8).
+namespace tcs {
+__device__ __forceinline__ void mma_u8(uint32_t (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2])
+{
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void split4(uint2 v, uint32_t &lo, uint32_t &hi)
+{
+    lo = __byte_perm(v.x, v.y, 0x6420);
+    hi = __byte_perm(v.x, v.y, 0x7531);
+}
+// A (16 x 32, row-major u16 M with row stride ld): rows r0 + g (+8), columns k0 + 4 t (+16)
+__device__ __forceinline__ void frag_a(const uint16_t *M, int ld, int r0, int k0, uint32_t (&lo)[4], uint32_t (&hi)[4])
+{
+    const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+    const uint16_t *p0 = M + (size_t)(r0 + g) * ld + k0 + 4 * t, *p1 = p0 + 8 * (size_t)ld;
+    split4(*reinterpret_cast<const uint2 *>(p0), lo[0], hi[0]);
+    split4(*reinterpret_cast<const uint2 *>(p1), lo[1], hi[1]);
+    split4(*reinterpret_cast<const uint2 *>(p0 + 16), lo[2], hi[2]);
+    split4(*reinterpret_cast<const uint2 *>(p1 + 16), lo[3], hi[3]);
+}
+// B (32 x 8, given transposed: BT row n holds column n, K contiguous): column n0 + g, K k0 + 4 t (+16)
+__device__ __forceinline__ void frag_b(const uint16_t *BT, int ld, int n0, int k0, uint32_t (&lo)[2], uint32_t (&hi)[2])
+{
+    const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+    const uint16_t *q = BT + (size_t)(n0 + g) * ld + k0 + 4 * t;
+    split4(*reinterpret_cast<const uint2 *>(q), lo[0], hi[0]);
+    split4(*reinterpret_cast<const uint2 *>(q + 16), lo[1], hi[1]);
+}
+// as frag_b on the panel's rotated T^t (row c of BT at X + c * ld, K entry k at (k + 8 (c & 15)) mod 128)
+__device__ __forceinline__ void frag_b_rot(const uint16_t *X, int ld, int n0, int k0, uint32_t (&lo)[2], uint32_t (&hi)[2])
+{
+    const int g = (threadIdx.x & 31) >> 2, t = threadIdx.x & 3;
+    const int c = n0 + g;
+    const uint16_t *row = X + (size_t)c * ld;
+    const int rot = 8 * (c & 15);
+    split4(*reinterpret_cast<const uint2 *>(row + ((k0 + 4 * t + rot) & 127)), lo[0], hi[0]);
+    split4(*reinterpret_cast<const uint2 *>(row + ((k0 + 16 + 4 * t + rot) & 127)), lo[1], hi[1]);
+}
+}  // namespace tcs
+
 // Inverse W of a unit upper triangular 32 x 32 matrix U (entries beyond bs: identity),
 // by doubling block sizes: with the diagonal blocks of size s already inverted,
 // each aligned 2s-block [[A, B], [0, C]] gets its off-diagonal block -A^-1 B C^-1.
@@ -284,12 +330,21 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     for (int k = tid; k <= PW; k += NT) hist[k] = 0;
     if (tid == 0) s_u[5] = 0;
     __syncthreads();
-    for (int64_t r = tid; r < mN; r += NT) {
-        const uint32_t l = lead[r];
-        if (l < (uint64_t)wmax) {
-            if (!src.ghist) atomicAdd(&hist[l], 1u);
-            const uint32_t q = atomicAdd(&s_u[5], 1u);
-            if (q < (uint32_t)CLMAX) clist[q] = (uint32_t)r;
+    for (int64_t r0 = 0; r0 < mN; r0 += 8 * NT) {           // 8 loads in flight per thread
+        uint32_t l8[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int64_t r = r0 + u * NT + tid;
+            l8[u] = r < mN ? __ldcg(lead + r) : NONE16;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const uint32_t l = l8[u];
+            if (l < (uint64_t)wmax) {
+                if (!src.ghist) atomicAdd(&hist[l], 1u);
+                const uint32_t q = atomicAdd(&s_u[5], 1u);
+                if (q < (uint32_t)CLMAX) clist[q] = (uint32_t)(r0 + u * NT + tid);
+            }
         }
     }
     if (src.ghist)
@@ -380,14 +435,13 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             if (ok) clead[wsum[warp] + __popc(msk & ((1u << lane) - 1u))] = clist[t];   // clead: scratch
             __syncthreads();
             ncand = (int)s_u[3];
+            if (tid < ncand) hinv[tid] = lead[clead[tid]];   // leads of the candidates (hinv: scratch)
+            __syncthreads();
             if (tid < ncand) {                       // order by (lead, row): physical ~ pivot order
                 const uint32_t r = clead[tid];
-                const uint64_t kr = ((uint64_t)lead[r] << 32) | r;
+                const uint64_t kr = ((uint64_t)hinv[tid] << 32) | r;
                 int rk = 0;
-                for (int j = 0; j < ncand; j++) {
-                    const uint32_t r2 = clead[j];
-                    rk += (((uint64_t)lead[r2] << 32) | r2) < kr;
-                }
+                for (int j = 0; j < ncand; j++) rk += (((uint64_t)hinv[j] << 32) | clead[j]) < kr;
                 crow[freel[rk]] = r;
                 cstat[freel[rk]] = 1;
             }
@@ -436,10 +490,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 }
                 *reinterpret_cast<uint4 *>(X + q * LDX + 8 * g) = v;
             }
-            for (int idx = tid; idx < ncand * PK; idx += NT) {
-                const int ci = idx / PK, k = idx % PK;
+            for (int idx = tid; idx < ncand * (PK / 8); idx += NT) {    // E = unit vectors, 8 per store
+                const int ci = idx / (PK / 8), k8 = (idx % (PK / 8)) * 8;
                 const uint32_t q = freel[ci];
-                X[q * LDX + PW + k] = (k == (int)q) ? 1 : 0;
+                uint4 z = make_uint4(0, 0, 0, 0);
+                if ((int)(q & ~7u) == k8) reinterpret_cast<uint16_t *>(&z)[q & 7] = 1;
+                *reinterpret_cast<uint4 *>(&X[q * LDX + PW + k8]) = z;
             }
         }
         __syncthreads();
@@ -686,116 +742,130 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // zero entries of E' skipped (E' is nearly diagonal on a staircase).  The value rows
             // are dead now: W and Q live in their first 512 bytes.
             // T = U^-1 E' by a blocked back substitution over 32-slot row blocks, bottom up:
-            //     T_I = W_II (E'_I - U_{I,>I} T_{>I}),   W_II = (U_II)^-1 (one warp per block),
-            // warp w <-> row 32 I + w of the block, lane l <-> columns 4l .. 4l+3 of T, so the U
-            // element of a step is warp-uniform and the T row segment one 8-byte shared load.
-            // u64 sums (< 128 products < 2^32 each); the value rows are dead now: T lives in
-            // columns [0, 128) of store rows 0..127, the residual in [128, 256), W_II in [256, 288).
+            //     T_I = W_II (E'_I - U_{I,>I} T_{>I}),   W_II = (U_II)^-1,
+            // the two products of every block on the warp-level tensor cores (mma.sync m16n8k32
+            // u8 -> s32 on the limbs of the u16 residues: HH, HL + LH, LL, each <= 128 * 255^2 * 2
+            // < 2^31; S = 2^16 HH + 2^8 X + LL < 2^40 reduced once), one m16n8 output tile per
+            // warp.  W_II by doubling inside the four diagonal blocks.  T and the residual are
+            // kept transposed (slot-major, so the B fragments are 8-byte loads); the value rows
+            // are dead now and hold them.
             uint16_t(*U)[PK] = FS;
-            for (int idx = tid; idx < (int)nb * PK; idx += NT) {   // rows >= nb and columns >= nb are never read
+            for (int idx = tid; idx < PK * PK; idx += NT) {
                 const int b = idx >> 7, b2 = idx & (PK - 1);
                 uint32_t v = (b == b2) ? 1u : 0u;
-                if (b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
+                if (b < (int)nb && b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
                 U[b][b2] = (uint16_t)v;
             }
             __syncthreads();
-#define TM(i_, j_) X[(i_) * LDX + (j_)]
-#define RM(i_, j_) X[(i_) * LDX + PK + (j_)]
-#define WD(i_, j_) X[(i_) * LDX + 2 * PK + (j_)]
-            P2_LAP(13);
-            // W_II: warp I inverts diagonal block I (lane j holds column j; rows from the bottom,
-            // W[i][j] = -sum_{i<k<=j} U[i][k] W[k][j]); rows >= nb are the identity
-            if (warp < 4 && 32 * warp < (int)nb) {
-                const int base = 32 * warp;
-                const int bs = (int)nb - base < 32 ? (int)nb - base : 32;
-                uint32_t w[32];
-#pragma unroll
-                for (int i = 31; i >= 0; i--) {
-                    uint32_t v = (i == lane) ? 1u : 0u;
-                    if (i < bs && i < lane) {
-                        uint64_t a0 = 0, a1 = 0;
-#pragma unroll
-                        for (int k = i + 1; k < 32; k++) {
-                            const uint64_t t = (uint64_t)U[base + i][base + k] * w[k];
-                            if (k & 1) a1 += t; else a0 += t;
-                        }
-                        const uint32_t z = fmod64(a0 + a1, F);
-                        v = z ? p - z : 0;
-                    }
-                    w[i] = v;
-                }
-#pragma unroll
-                for (int i = 0; i < 32; i++) WD(base + i, lane) = (uint16_t)w[i];
+#define TT(c_, k_) X[(c_) * LDX + (((k_) + 8 * ((c_) & 15)) & (PK - 1))]   // T^t: slot c, row k (rows rotated: no bank conflicts)
+#define RT(c_, k_) X[(c_) * LDX + PK + (k_)]          // residual of the block, transposed (k < 32)
+#define WD(i_, j_) X[(i_) * LDX + PK + 32 + (j_)]     // W_II: row 32 I + i, column j < 32
+#define QD(i_, j_) X[(i_) * LDX + PK + 64 + (j_)]     // doubling scratch
+            for (int idx = tid; idx < PK * (PK / 8); idx += NT) {   // T^t = 0 (K padding beyond nb)
+                const int c = idx >> 4, k8 = (idx & 15) * 8;
+                *reinterpret_cast<uint4 *>(&TT(c, k8)) = make_uint4(0, 0, 0, 0);
+            }
+            for (int idx = tid; idx < PK * 32; idx += NT) {
+                const int i = idx >> 5, j = idx & 31;
+                WD(i, j) = (uint16_t)((i & 31) == j ? 1 : 0);
             }
             __syncthreads();
-            P2_LAP(14);
-            const int nblk = ((int)nb + 31) >> 5;
-            for (int I = nblk - 1; I >= 0; I--) {
-                const int b = 32 * I + warp;                 // this warp's row of block I
-                const int c4 = 4 * lane;                     // this lane's 4 columns (slots)
-                if (b < (int)nb) {
-                    // E'[b][s] = E[phys b][phys s] / h_b[pc_b]
-                    const uint32_t qb = bphys[b], hv = hinv[qb];
-                    uint32_t e[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++)
-                        e[u] = (c4 + u < (int)nb) ? mod32(X[qb * LDX + PW + bphys[c4 + u]] * hv, p, m32) : 0u;
-                    uint64_t acc[4] = {0, 0, 0, 0};
-                    const uint16_t *urow = &U[b][0];
-#pragma unroll 4
-                    for (int k = 32 * (I + 1); k < (int)nb; k++) {
-                        const uint64_t uk = urow[k];
-                        const uint2 t = *reinterpret_cast<const uint2 *>(&TM(k, c4));
-                        acc[0] += uk * (t.x & 0xffffu); acc[1] += uk * (t.x >> 16);
-                        acc[2] += uk * (t.y & 0xffffu); acc[3] += uk * (t.y >> 16);
-                    }
-                    uint32_t r[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const uint32_t z = fmod64(acc[u], F);
-                        r[u] = e[u] >= z ? e[u] - z : e[u] + p - z;
-                    }
-                    *reinterpret_cast<uint2 *>(&RM(b, c4)) = make_uint2(r[0] | (r[1] << 16), r[2] | (r[3] << 16));
+            P2_LAP(13);
+            // W_II: levels s = 1 .. 16; every aligned 2s-block [[A, B], [0, C]] of a diagonal block
+            // gets Q = B C^-1, then -A^-1 Q (64 s items per step, one per thread at s = 16)
+            for (int sl = 0; sl < 5; sl++) {
+                const int sz = 1 << sl;
+                const int items = 64 * sz;
+                for (int it = tid; it < items; it += NT) {
+                    const int c = it & (sz - 1), r = (it >> sl) & (sz - 1), q = it >> (2 * sl);   // q: pair over 128 rows
+                    const int base = q * 2 * sz, lb = base & 31;
+                    uint64_t acc = 0;
+                    for (int k = 0; k <= c; k++)
+                        acc += (uint64_t)U[base + r][base + sz + k] * WD(base + sz + k, lb + sz + c);
+                    QD(base + r, lb + sz + c) = (uint16_t)fmod64(acc, F);
                 }
                 __syncthreads();
-                if (b < (int)nb) {
-                    const int kend = (int)nb - 32 * I < 32 ? (int)nb - 32 * I : 32;
-                    uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll 4
-                    for (int k = warp; k < kend; k++) {
-                        const uint64_t wk = WD(32 * I + warp, k);
-                        const uint2 t = *reinterpret_cast<const uint2 *>(&RM(32 * I + k, c4));
-                        acc[0] += wk * (t.x & 0xffffu); acc[1] += wk * (t.x >> 16);
-                        acc[2] += wk * (t.y & 0xffffu); acc[3] += wk * (t.y >> 16);
-                    }
-                    uint32_t r[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) r[u] = fmod64(acc[u], F);
-                    *reinterpret_cast<uint2 *>(&TM(b, c4)) = make_uint2(r[0] | (r[1] << 16), r[2] | (r[3] << 16));
+                for (int it = tid; it < items; it += NT) {
+                    const int c = it & (sz - 1), r = (it >> sl) & (sz - 1), q = it >> (2 * sl);
+                    const int base = q * 2 * sz, lb = base & 31;
+                    uint64_t acc = 0;
+                    for (int k = r; k < sz; k++) acc += (uint64_t)WD(base + r, lb + k) * QD(base + k, lb + sz + c);
+                    const uint32_t z = fmod64(acc, F);
+                    WD(base + r, lb + sz + c) = (uint16_t)(z ? p - z : 0);
                 }
                 __syncthreads();
             }
-            // the T tile (limb planes, K index = slot): 4 consecutive K entries per 4-byte store
-            for (int idx = tid; idx < PK * PK / 4; idx += NT) {
-                const int bb = idx >> 5, l0 = (idx & 31) * 4;
-                uint32_t lo = 0, hi = 0;
-                if (bb < (int)nb) {
-                    const uint2 t = *reinterpret_cast<const uint2 *>(&TM(bb, l0));
-                    const uint32_t v[4] = {t.x & 0xffffu, t.x >> 16, t.y & 0xffffu, t.y >> 16};
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const uint32_t x = (l0 + u < (int)nb) ? v[u] : 0u;
-                        lo |= (x & 0xffu) << (8 * u);
-                        hi |= (x >> 8) << (8 * u);
+            P2_LAP(14);
+            {
+                const int g = lane >> 2, t4 = lane & 3;
+                const int mt = warp >> 4, n0 = (warp & 15) * 8;      // this warp's m16n8 tile of the block
+                const int nblk = ((int)nb + 31) >> 5;
+                for (int I = nblk - 1; I >= 0; I--) {
+                    const int r0 = 32 * I + 16 * mt;
+                    // R_I = E'_I - U_{I,>I} T_{>I}
+                    uint32_t hh[4] = {0, 0, 0, 0}, xx[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+                    for (int k0 = 32 * (I + 1); k0 < (int)nb; k0 += 32) {
+                        uint32_t alo[4], ahi[4], blo[2], bhi[2];
+                        tcs::frag_a(&U[0][0], PK, r0, k0, alo, ahi);
+                        tcs::frag_b_rot(X, LDX, n0, k0, blo, bhi);
+                        tcs::mma_u8(hh, ahi, bhi);
+                        tcs::mma_u8(xx, ahi, blo);
+                        tcs::mma_u8(xx, alo, bhi);
+                        tcs::mma_u8(ll, alo, blo);
                     }
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int row = r0 + g + ((e >> 1) << 3), col = n0 + 2 * t4 + (e & 1);
+                        const uint32_t z = fmod64(((uint64_t)hh[e] << 16) + ((uint64_t)xx[e] << 8) + ll[e], F);
+                        uint32_t ev = 0;
+                        if (row < (int)nb && col < (int)nb) {
+                            const uint32_t qb = bphys[row];
+                            ev = mod32(X[qb * LDX + PW + bphys[col]] * hinv[qb], p, m32);
+                        }
+                        RT(col, row - 32 * I) = (uint16_t)(ev >= z ? ev - z : ev + p - z);
+                    }
+                    __syncthreads();
+                    // T_I = W_II R_I
+#pragma unroll
+                    for (int e = 0; e < 4; e++) { hh[e] = 0; xx[e] = 0; ll[e] = 0; }
+                    {
+                        uint32_t alo[4], ahi[4], blo[2], bhi[2];
+                        tcs::frag_a(&WD(0, 0), LDX, r0, 0, alo, ahi);
+                        tcs::frag_b(&RT(0, 0), LDX, n0, 0, blo, bhi);
+                        tcs::mma_u8(hh, ahi, bhi);
+                        tcs::mma_u8(xx, ahi, blo);
+                        tcs::mma_u8(xx, alo, bhi);
+                        tcs::mma_u8(ll, alo, blo);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int row = r0 + g + ((e >> 1) << 3), col = n0 + 2 * t4 + (e & 1);
+                        const uint32_t z = fmod64(((uint64_t)hh[e] << 16) + ((uint64_t)xx[e] << 8) + ll[e], F);
+                        TT(col, row) = (uint16_t)(row < (int)nb ? z : 0u);
+                    }
+                    __syncthreads();
+                }
+            }
+            P2_LAP(16);
+            // the T tile (limb planes, K index = slot): 4 consecutive K entries per 4-byte store;
+            // consecutive lanes take consecutive rows bb (one row of T^t: conflict-free)
+            for (int idx = tid; idx < PK * PK / 4; idx += NT) {
+                const int bb = idx & (PK - 1), l0 = (idx >> 7) * 4;
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t x = (bb < (int)nb && l0 + u < (int)nb) ? TT(l0 + u, bb) : 0u;
+                    lo |= (x & 0xffu) << (8 * u);
+                    hi |= (x >> 8) << (8 * u);
                 }
                 const uint32_t o = tc::toff((uint32_t)bb, (uint32_t)l0);
                 *reinterpret_cast<uint32_t *>(Tlo + o) = lo;
                 *reinterpret_cast<uint32_t *>(Thi + o) = hi;
             }
-#undef TM
-#undef RM
+#undef TT
+#undef RT
 #undef WD
+#undef QD
             P2_LAP(15);
             break;
         }
@@ -1334,8 +1404,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     }
     unsigned long long *trace = nullptr;
     if (getenv("GBLA_PANEL_TRACE")) {
-        GBLA_TRY(dalloc_t(h, 16, &trace));
-        GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 16 * 8, st));
+        GBLA_TRY(dalloc_t(h, 20, &trace));
+        GBLA_CUDA_TRY(cudaMemsetAsync(trace, 0, 20 * 8, st));
     }
     const int cap = panel_cap();
     cudaStream_t side = nullptr;
@@ -1560,15 +1630,15 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     }
 
     if (trace && status == GBLA_OK) {   // diagnostics: mean cycles per phase over the panels that ran
-        unsigned long long tr[16];
+        unsigned long long tr[20];
         GBLA_CUDA_TRY(cudaMemcpy(tr, trace, sizeof tr, cudaMemcpyDeviceToHost));
         const double n = tr[9] ? (double)tr[9] : 1.0;
         fprintf(stderr,
                 "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f reduce+LU %.0f "
-                "heads %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f inverse %.0f T %.0f; LU steps/panel %.2f "
+                "heads %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f W_II %.0f T solve %.0f T tile %.0f; LU steps/panel %.2f "
                 "candidates %.1f pivots %.1f width %.1f\n",
                 tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[13] / n, tr[14] / n,
-                tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
+                tr[16] / n, tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
     }
     return status;
 }
