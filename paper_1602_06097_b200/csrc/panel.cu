@@ -81,7 +81,9 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PK = 128;                 // pivots per panel = K of the trailing GEMM
 constexpr int PW = 512;                 // widest panel (columns)
-constexpr int LDX = PW + PK;            // row of the store: values [0, PW) | coefficients [PW, PW+PK)
+constexpr int LDX = PW + PK + 8;        // row of the store: values [0, PW) | coefficients [PW, PW+PK) | pad
+                                        // (1296-byte rows: consecutive rows start 4 banks apart)
+constexpr int FSLD = PK + 8;            // row stride of the factor snapshot / U (same reason)
 constexpr int NT = 1024;                // threads of k_panel2
 constexpr uint32_t NONE16 = 0xffffffffu;
 
@@ -95,7 +97,7 @@ struct P2State {
     uint32_t pc[PK];                    // absolute pivot columns
 };
 
-constexpr int P2_SMEM = PK * LDX * 2 + PK * PK * 2;   // row store + factor snapshot (192 KB)
+constexpr int P2_SMEM = PK * LDX * 2 + PK * FSLD * 2;   // row store + factor snapshot (196 KB)
 
 // Where the panel reads its rows.  Single GPU: all rows of D, window at column c0.
 // Distributed echelon: the candidates gathered from every rank (their window slices,
@@ -113,7 +115,8 @@ struct PanelSrc {
     int gathered;
     int cap;                    // wide panels: at most cap (<= PK) rows lead inside the window
     int walign;                 // panel widths a multiple of this (32 if 0; 64 with deferred updates)
-    int lumode;                 // chunk echelon: 0 rounds, 1 pivot steps, 2 pivot steps in dense mode
+    int lumode;                 // chunk echelon: 0 rounds, 1 pivot steps, 2 pivot steps in dense mode,
+                                //   3 blocked LU in dense mode (default)
 };
 
 // panels per super-panel of deferred trailing updates (GBLA_SP = 1..4).  Default: 4 when D is
@@ -139,10 +142,10 @@ static int panel_cap()
 static int panel_lumode()
 {
     const char *e = getenv("GBLA_PANEL_LU");
-    const int v = e ? atoi(e) : 2;
-    return v < 0 || v > 2 ? 2 : v;
+    const int v = e ? atoi(e) : 3;
+    return v < 0 || v > 3 ? 3 : v;
 }
-__device__ __forceinline__ bool use_lu(bool dense, int mode) { return mode == 1 || (mode == 2 && dense); }
+__device__ __forceinline__ bool use_lu(bool dense, int mode) { return mode == 1 || (mode >= 2 && dense); }
 
 __device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
 {
@@ -250,6 +253,127 @@ __device__ __forceinline__ void frag_b_rot(const uint16_t *X, int ld, int n0, in
 }
 }  // namespace tcs
 
+// Dense chunk echelon form by a blocked LU (GBLA_PANEL_LU=3): column blocks of 32 inside the
+// window (ldv <= 128).  Phase F: pivot steps (one barrier each, smallest (lead, row) key) on a
+// copy V of the block's columns of the candidate rows, cross-multiplied (row <- v_h row - f head)
+// and tracked against the block-start rows Y:  row_r = sigma_r Y_r + sum_j L[r][j] Y_{p_j}.
+// Phase U: the columns right of the block and the coefficients get that update at once,
+//     X[r][x] = sigma_r Y[r][x] + (L Y_p)[r][x]   (mma.sync m16n8k32 u8 limbs, K = 32),
+// the block's columns are V.  Heads are never written again in the chunk (LU: no elimination
+// above pivots here; the chunk's back substitution follows).  Returns the pivot steps taken.
+// Scratch (dense mode: the value columns >= 128 are unused): V at 128, L at 160, the snapshot
+// Y_p^t at 192 (virtual column n -> row n & 127, offset 32 (n >> 7)) of every store row.
+__device__ int blocked_lu(uint16_t *X, int ncand, const uint32_t *freel, uint32_t *cstat, uint32_t *clead,
+                          uint32_t *skey, uint32_t p, uint32_t m32, const Field &F, int ldv)
+{
+    __shared__ uint32_t sig[PK];
+    __shared__ uint32_t prow[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#define BV(q_, j_) X[(q_) * LDX + 128 + (j_)]
+#define BL(q_, j_) X[(q_) * LDX + 160 + (j_)]
+    int slot = 0, nsteps = 0;
+    for (int cb = 0; cb < ldv; cb += 32) {
+        for (int idx = tid; idx < PK * 32; idx += NT) {
+            const int q = idx >> 5, j = idx & 31;
+            BV(q, j) = X[q * LDX + cb + j];
+            BL(q, j) = 0;
+        }
+        for (int q = tid; q < PK; q += NT) sig[q] = 1;
+        __syncthreads();
+        int kj = 0;
+        for (;;) {                                                             // phase F
+            nsteps++;
+            uint32_t best = NONE16;
+            for (int ci = warp; ci < ncand; ci += 32) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] != 1) continue;
+                const unsigned m = __ballot_sync(FULL, BV(q, lane) != 0);
+                if (m) {
+                    const uint32_t key = ((uint32_t)(__ffs(m) - 1) << 7) | q;
+                    best = key < best ? key : best;
+                }
+            }
+            if (lane == 0 && best != NONE16) atomicMin(&skey[slot], best);
+            if (tid == 0) skey[slot == 0 ? 2 : slot - 1] = NONE16;
+            __syncthreads();
+            const uint32_t key = skey[slot];
+            slot = slot == 2 ? 0 : slot + 1;
+            if (key == NONE16) break;
+            const int c = (int)(key >> 7);
+            const uint32_t hq = key & 127u;
+            const uint32_t vh = BV(hq, c), sh = sig[hq];
+            for (int ci = warp; ci < ncand; ci += 32) {
+                const uint32_t q = freel[ci];
+                if (cstat[q] != 1) continue;
+                if (q == hq) {
+                    __syncwarp();
+                    if (lane == 0) { cstat[q] = 2; clead[q] = (uint32_t)(cb + c); }
+                    __syncwarp();
+                    continue;
+                }
+                const uint32_t f = BV(q, c);
+                __syncwarp();
+                if (!f) continue;
+                const uint32_t nf = p - f;
+                BV(q, lane) = (uint16_t)mod32(mod32(vh * BV(q, lane), p, m32) + nf * BV(hq, lane), p, m32);
+                uint32_t l = 0;
+                if (lane < kj) l = mod32(mod32(vh * BL(q, lane), p, m32) + nf * BL(hq, lane), p, m32);
+                else if (lane == kj) l = mod32(nf * sh, p, m32);
+                if (lane <= kj) BL(q, lane) = (uint16_t)l;
+                if (lane == 0) sig[q] = mod32(vh * sig[q], p, m32);
+                __syncwarp();
+            }
+            if (tid == 0) prow[kj] = hq;
+            kj++;
+            if (kj == 32) {                         // the block is full: every column has a pivot
+                __syncthreads();
+                break;
+            }
+        }
+        // phase U: block columns = V; the rest of the window and the coefficients by one K = 32 product
+        if (kj > 0) {
+            const int nv = ldv - cb - 32, nvc = nv + PK;
+            for (int idx = tid; idx < PK * 32; idx += NT) {
+                const int q = idx >> 5, j = idx & 31;
+                if (cstat[q] != 0) X[q * LDX + cb + j] = BV(q, j);
+            }
+            for (int idx = tid; idx < nvc * 32; idx += NT) {       // snapshot Y_p^t (zero beyond kj)
+                const int n = idx >> 5, k = idx & 31;
+                const int col = n < nv ? cb + 32 + n : PW + (n - nv);
+                X[(n & 127) * LDX + 192 + 32 * (n >> 7) + k] = k < kj ? X[prow[k] * LDX + col] : (uint16_t)0;
+            }
+            __syncthreads();
+            const int g = lane >> 2, t4 = lane & 3;
+            const int ntile = 8 * (nvc / 8);
+            for (int tile = warp; tile < ntile; tile += 32) {
+                const int mt = tile & 7, n0 = (tile >> 3) * 8;
+                const int r0 = 16 * mt;
+                uint32_t hh[4] = {0, 0, 0, 0}, xx[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+                uint32_t alo[4], ahi[4], blo[2], bhi[2];
+                tcs::frag_a(&BL(0, 0), LDX, r0, 0, alo, ahi);
+                tcs::frag_b(X + 192 + 32 * (n0 >> 7), LDX, n0 & 127, 0, blo, bhi);
+                tcs::mma_u8(hh, ahi, bhi);
+                tcs::mma_u8(xx, ahi, blo);
+                tcs::mma_u8(xx, alo, bhi);
+                tcs::mma_u8(ll, alo, blo);
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const int r = r0 + g + ((e >> 1) << 3), n = n0 + 2 * t4 + (e & 1);
+                    if (cstat[r] == 0) continue;
+                    const int col = n < nv ? cb + 32 + n : PW + (n - nv);
+                    const uint32_t z = fmod_limbs(hh[e], xx[e], ll[e], F);
+                    uint16_t *y = &X[r * LDX + col];
+                    *y = (uint16_t)mod32(mod32(sig[r] * *y, p, m32) + z, p, m32);
+                }
+            }
+            __syncthreads();
+        }
+    }
+#undef BV
+#undef BL
+    return nsteps;
+}
+
 // Inverse W of a unit upper triangular 32 x 32 matrix U (entries beyond bs: identity),
 // by doubling block sizes: with the diagonal blocks of size s already inverted,
 // each aligned 2s-block [[A, B], [0, C]] gets its off-diagonal block -A^-1 B C^-1.
@@ -289,7 +413,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                                                    unsigned long long *__restrict__ trace)
 {
     extern __shared__ __align__(16) uint16_t X[];          // [PK][LDX] row store
-    uint16_t(*FS)[PK] = reinterpret_cast<uint16_t(*)[PK]>(X + PK * LDX);   // factor snapshot
+    uint16_t(*FS)[FSLD] = reinterpret_cast<uint16_t(*)[FSLD]>(X + PK * LDX);   // factor snapshot
     __shared__ uint32_t hist[PW + 1];       // lead histogram -> prefix; reused as column -> head key
     __shared__ uint32_t crow[PK];           // D row of each physical row of the store
     __shared__ uint32_t clead[PK];          // leading column of each physical row (chunk rounds)
@@ -624,7 +748,10 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
                 __syncthreads();
                 int slot = 0, nsteps = 0;
-                for (;;) {
+                const bool blocked = dense && src.lumode == 3 && ldv <= 128;
+                if (blocked) {
+                    nsteps = blocked_lu(X, ncand, freel, cstat, clead, skey, p, m32, F, ldv);
+                } else for (;;) {
                     nsteps++;
                     uint32_t best = NONE16;
                     for (int ci = warp; ci < ncand; ci += 32) {
@@ -749,7 +876,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // warp.  W_II by doubling inside the four diagonal blocks.  T and the residual are
             // kept transposed (slot-major, so the B fragments are 8-byte loads); the value rows
             // are dead now and hold them.
-            uint16_t(*U)[PK] = FS;
+            uint16_t(*U)[FSLD] = FS;
             for (int idx = tid; idx < PK * PK; idx += NT) {
                 const int b = idx >> 7, b2 = idx & (PK - 1);
                 uint32_t v = (b == b2) ? 1u : 0u;
@@ -761,6 +888,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 #define RT(c_, k_) X[(c_) * LDX + PK + (k_)]          // residual of the block, transposed (k < 32)
 #define WD(i_, j_) X[(i_) * LDX + PK + 32 + (j_)]     // W_II: row 32 I + i, column j < 32
 #define QD(i_, j_) X[(i_) * LDX + PK + 64 + (j_)]     // doubling scratch
+#define EP(b_, c_) X[(b_) * LDX + PK + 96 + (((c_) + 8 * ((b_) & 15)) & (PK - 1))]   // E' (rotated rows)
             for (int idx = tid; idx < PK * (PK / 8); idx += NT) {   // T^t = 0 (K padding beyond nb)
                 const int c = idx >> 4, k8 = (idx & 15) * 8;
                 *reinterpret_cast<uint4 *>(&TT(c, k8)) = make_uint4(0, 0, 0, 0);
@@ -768,6 +896,15 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             for (int idx = tid; idx < PK * 32; idx += NT) {
                 const int i = idx >> 5, j = idx & 31;
                 WD(i, j) = (uint16_t)((i & 31) == j ? 1 : 0);
+            }
+            for (int idx = tid; idx < PK * PK; idx += NT) {    // E'[b][c] = E[phys b][phys c] / h_b[pc_b]
+                const int b = idx >> 7, c = idx & (PK - 1);
+                uint32_t v = 0;
+                if (b < (int)nb && c < (int)nb) {
+                    const uint32_t qb = bphys[b];
+                    v = mod32(X[qb * LDX + PW + bphys[c]] * hinv[qb], p, m32);
+                }
+                EP(b, c) = (uint16_t)v;
             }
             __syncthreads();
             P2_LAP(13);
@@ -806,7 +943,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                     uint32_t hh[4] = {0, 0, 0, 0}, xx[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
                     for (int k0 = 32 * (I + 1); k0 < (int)nb; k0 += 32) {
                         uint32_t alo[4], ahi[4], blo[2], bhi[2];
-                        tcs::frag_a(&U[0][0], PK, r0, k0, alo, ahi);
+                        tcs::frag_a(&U[0][0], FSLD, r0, k0, alo, ahi);
                         tcs::frag_b_rot(X, LDX, n0, k0, blo, bhi);
                         tcs::mma_u8(hh, ahi, bhi);
                         tcs::mma_u8(xx, ahi, blo);
@@ -816,12 +953,8 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
                         const int row = r0 + g + ((e >> 1) << 3), col = n0 + 2 * t4 + (e & 1);
-                        const uint32_t z = fmod64(((uint64_t)hh[e] << 16) + ((uint64_t)xx[e] << 8) + ll[e], F);
-                        uint32_t ev = 0;
-                        if (row < (int)nb && col < (int)nb) {
-                            const uint32_t qb = bphys[row];
-                            ev = mod32(X[qb * LDX + PW + bphys[col]] * hinv[qb], p, m32);
-                        }
+                        const uint32_t z = fmod_limbs(hh[e], xx[e], ll[e], F);
+                        const uint32_t ev = EP(row, col);
                         RT(col, row - 32 * I) = (uint16_t)(ev >= z ? ev - z : ev + p - z);
                     }
                     __syncthreads();
@@ -840,7 +973,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
                         const int row = r0 + g + ((e >> 1) << 3), col = n0 + 2 * t4 + (e & 1);
-                        const uint32_t z = fmod64(((uint64_t)hh[e] << 16) + ((uint64_t)xx[e] << 8) + ll[e], F);
+                        const uint32_t z = fmod_limbs(hh[e], xx[e], ll[e], F);
                         TT(col, row) = (uint16_t)(row < (int)nb ? z : 0u);
                     }
                     __syncthreads();
@@ -866,6 +999,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
 #undef RT
 #undef WD
 #undef QD
+#undef EP
             P2_LAP(15);
             break;
         }
@@ -981,7 +1115,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             rowpiv[r] = (uint32_t)(c0 + bpc[tid]);      // marks S (pivot column >= c0)
     }
     P2_LAP(6);
-    if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; }
+    if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; trace[17] += dense ? 1 : 0; }
 #undef P2_LAP
     if (tid == 0) {
         cur->c0 = c0;
@@ -1636,9 +1770,9 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         fprintf(stderr,
                 "[gbla panel2 trace] %llu panels, mean cycles: width %.0f collect %.0f load %.0f reduce+LU %.0f "
                 "heads %.0f dense-backsub %.0f output %.0f; wide: U/W init %.0f W_II %.0f T solve %.0f T tile %.0f; LU steps/panel %.2f "
-                "candidates %.1f pivots %.1f width %.1f\n",
+                "candidates %.1f pivots %.1f width %.1f dense panels %llu\n",
                 tr[9], tr[0] / n, tr[1] / n, tr[2] / n, tr[3] / n, tr[4] / n, tr[5] / n, tr[6] / n, tr[13] / n, tr[14] / n,
-                tr[16] / n, tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n);
+                tr[16] / n, tr[15] / n, tr[8] / n, tr[10] / n, tr[11] / n, tr[12] / n, tr[17]);
     }
     return status;
 }
