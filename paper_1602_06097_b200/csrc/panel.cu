@@ -268,6 +268,7 @@ __device__ int blocked_lu(uint16_t *X, int ncand, const uint32_t *freel, uint32_
 {
     __shared__ uint32_t sig[PK];
     __shared__ uint32_t prow[32];
+    __shared__ uint32_t wbest[2][32];      // per-warp bids, double-buffered by step parity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #define BV(q_, j_) X[(q_) * LDX + 128 + (j_)]
 #define BL(q_, j_) X[(q_) * LDX + 160 + (j_)]
@@ -293,11 +294,10 @@ __device__ int blocked_lu(uint16_t *X, int ncand, const uint32_t *freel, uint32_
                     best = key < best ? key : best;
                 }
             }
-            if (lane == 0 && best != NONE16) atomicMin(&skey[slot], best);
-            if (tid == 0) skey[slot == 0 ? 2 : slot - 1] = NONE16;
+            if (lane == 0) wbest[slot][warp] = best;              // one slot per warp: no atomics
             __syncthreads();
-            const uint32_t key = skey[slot];
-            slot = slot == 2 ? 0 : slot + 1;
+            const uint32_t key = __reduce_min_sync(FULL, wbest[slot][lane]);
+            slot ^= 1;
             if (key == NONE16) break;
             const int c = (int)(key >> 7);
             const uint32_t hq = key & 127u;
@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             //     elected it.  Keys rotate over three slots (a slot is reset two steps after use).
             {
                 __shared__ uint32_t skey[3];
+                __shared__ uint32_t skey2[2][32];
                 if (tid < 3) skey[tid] = NONE16;
                 for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
                 __syncthreads();
@@ -773,11 +774,10 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                         }
                         __syncwarp();
                     }
-                    if (lane == 0 && best != NONE16) atomicMin(&skey[slot], best);
-                    if (tid == 0) skey[slot == 0 ? 2 : slot - 1] = NONE16;
+                    if (lane == 0) skey2[slot][warp] = best;              // one slot per warp: no atomics
                     __syncthreads();
-                    const uint32_t key = skey[slot];
-                    slot = slot == 2 ? 0 : slot + 1;
+                    const uint32_t key = __reduce_min_sync(FULL, skey2[slot][lane]);
+                    slot ^= 1;
                     if (key == NONE16) break;
                     const uint32_t c = key >> 7, hq = key & 127u;
                     const uint16_t *hr = X + hq * LDX;
