@@ -165,7 +165,21 @@ def roofline(kms, kwork, peaks, peak_src, sm_count):
         traffic_db = {}
     tr = traffic_db.get(dom)
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    if dom == "panel":
+    if dom == "trailing" and kwork.get("trailing_elems"):
+        # K11 trailing update: K = 128 (multi-K 512) products into u16 D read-modify-written once per
+        # launch: 128 modMACs x 8 u8 ops per 4 bytes = 256 ops/B < the int8 ridge (3342 TOPS / 6.5 TB/s
+        # ~ 510 ops/B), so HBM bounds it.  Algorithmic bytes = 4 per D entry of the update (u16 read +
+        # write; the A/B operand tiles are L2-resident and not counted).
+        byts = 4.0 * kwork["trailing_elems"]
+        peak = float(peaks["hbm_gbs"])
+        ach = byts / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        tens = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        out = {"bound": "hbm", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
+               "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+               "algorithmic_bytes": int(byts), "algorithmic_bytes_per_launch": int(byts / max(n, 1)),
+               "tensor_TOPS": round(tens, 2), "tensor_frac": round(tens / (2.0 * float(peaks["bf16_tflops"])), 5),
+               "intensity_ops_per_byte": round(work * 8 / byts, 1) if byts else None}
+    elif dom == "panel":
         peak = sm_count * 64 * sm_mhz * 1e6 / 1e12
         ach = work / (ms / 1e3) / 1e12 if ms > 0 else 0.0
         out = {"bound": "alu", "achieved": round(ach, 5), "peak": round(peak, 3), "unit": "Tmodmac/s",
@@ -257,7 +271,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phases = []
     kms = {k: [0.0, 0] for k in gb.Mat.KERNELS}
-    kwork = {k: 0 for k in gb.Mat.KERNELS}
+    kwork = {k: 0 for k in list(gb.Mat.KERNELS) + ["trailing_elems"]}
     kms_steps = []
     ops = dense_ops = 0
     rank_d = None

@@ -209,7 +209,9 @@ gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int64_t *launch
 /* Algorithmic modMACs of the same kernel family on this handle (this rank):
  * 0 = Alg 2 A-part count (sum over nonzero lambda_j of nnz(A_j) - 1),
  * 1 = Alg 2 B-part count, 2 = sum over panels of candidates * kp * 128,
- * 3 = sum over panels of nrows * kp * width, 4 = sum of kp * kp * width. */
+ * 3 = sum over panels of nrows * kp * width, 4 = sum of kp * kp * width;
+ * 5 = not modMACs: sum over panels of nrows * width, the D entries the
+ * trailing updates read and write (the HBM roofline of K11). */
 gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *modmac);
 /* Number of libgbla kernels launched by this process so far (diagnostics). */
 uint64_t gbla_kernel_launches(void);

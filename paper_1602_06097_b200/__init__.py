@@ -311,6 +311,9 @@ class Mat:
             w = ctypes.c_uint64()
             _check(_lib.gbla_get_kernel_work(self._h, i, ctypes.byref(w)))
             out[name] = w.value
+        w = ctypes.c_uint64()
+        _check(_lib.gbla_get_kernel_work(self._h, len(self.KERNELS), ctypes.byref(w)))
+        out["trailing_elems"] = w.value                 # D entries read + written by the trailing updates
         return out
 
     def phase_ms(self):

@@ -167,6 +167,19 @@ cudaStream_t ctx_side_stream(gbla_ctx c)
     return c->side;
 }
 
+cudaStream_t ctx_rest_stream(gbla_ctx c)
+{
+    if (!c->rest) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&c->rest, cudaStreamNonBlocking, lo) != cudaSuccess) {
+            cudaGetLastError();
+            c->rest = nullptr;
+        }
+    }
+    return c->rest;
+}
+
 cudaEvent_t ctx_event(gbla_ctx c, int i)
 {
     if (!c->ev[i] && cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -194,6 +207,7 @@ extern "C" void gbla_ctx_destroy(gbla_ctx ctx)
     dist_destroy(ctx);
     cudaSetDevice(ctx->device);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->rest) cudaStreamDestroy(ctx->rest);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -522,8 +536,8 @@ extern "C" gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int6
 
 extern "C" gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *modmac)
 {
-    if (!h || which < 0 || which >= KT_N || !modmac) { set_error("gbla_get_kernel_work: bad argument"); return GBLA_E_INVAL; }
-    *modmac = h->kwork[which];
+    if (!h || which < 0 || which > KT_N || !modmac) { set_error("gbla_get_kernel_work: bad argument"); return GBLA_E_INVAL; }
+    *modmac = which == KT_N ? h->trail_elems : h->kwork[which];
     return GBLA_OK;
 }
 

@@ -43,7 +43,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr);
+                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr, int grid_cap = 0);
 
 namespace {
 
@@ -579,6 +579,7 @@ __global__ void k_count(int64_t width, const PanelState<PK> *__restrict__ ps, un
     ops[0] += nr * kp * (unsigned long long)width;
     ops[1] += kp * kp * (unsigned long long)width;
     ops[2] += (unsigned long long)ps->ncand * kp * PK;   // panel RREF: each pivot eliminated from every candidate
+    ops[3] += nr * (unsigned long long)width;              // D entries of the trailing update
 }
 
 // K13: R rows sorted by pivot column.
@@ -663,10 +664,10 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     uint16_t *invtab;
     unsigned long long *dops;
     GBLA_TRY(dalloc_t(h, mN + 1, &rowpiv));
-    GBLA_TRY(dalloc_t(h, 3, &dops));
+    GBLA_TRY(dalloc_t(h, 4, &dops));
     GBLA_TRY(dalloc_t(h, 65536, &invtab));
     GBLA_CUDA_TRY(cudaMemsetAsync(rowpiv, 0xff, (mN + 1) * 4, st));
-    GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 24, st));
+    GBLA_CUDA_TRY(cudaMemsetAsync(dops, 0, 32, st));
     k_invtab<<<grid_for(h->p, 256), 256, 0, st>>>(h->F, invtab);
     note_launch();
     // row-sharded D (multi-GPU, or emulated ranks): the distributed echelon assembles R itself
@@ -695,15 +696,16 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
         GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t, tb, cflag, cidx, (int)(nN + 1), st));
     }
     uint32_t rk = 0;
-    unsigned long long dv[3] = {0, 0, 0};
+    unsigned long long dv[4] = {0, 0, 0, 0};
     GBLA_CUDA_TRY(cudaMemcpyAsync(&rk, cidx + nN, 4, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 24, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 32, cudaMemcpyDeviceToHost, st));
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
     h->rank = rk;
     h->dense_ops = dv[0] + dv[1];
     h->kwork[KT_TRAIL] = dv[0];
     h->kwork[KT_RN] = dv[1];
     h->kwork[KT_PANEL] = dv[2];
+    h->trail_elems = dv[3];
     h->ldR = ldD;
     GBLA_TRY(dalloc_t(h, (size_t)(rk > 0 ? rk : 1) * h->ldR, &h->R));
     GBLA_TRY(dalloc_t(h, rk + 1, &h->pivcol));

@@ -107,11 +107,13 @@ struct gbla_ctx_s {
     // per-context resources reused across calls (creating them per call costs host time that
     // stalls the pipelined panel loop): the echelon's side stream, sync events, pinned scratch
     cudaStream_t side = nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t rest = nullptr;         // low priority: the off-chain part of the echelon's trailing updates
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
 };
 cudaStream_t ctx_side_stream(gbla_ctx c);      // high priority, non-blocking; NULL on failure
+cudaStream_t ctx_rest_stream(gbla_ctx c);      // low priority, non-blocking; NULL on failure
 cudaEvent_t ctx_event(gbla_ctx c, int i);      // i < 4, timing disabled
 void *ctx_pinned(gbla_ctx c, size_t bytes);    // pinned host scratch (grows), NULL on failure
 
@@ -177,6 +179,7 @@ struct gbla_mat_s {
     uint64_t *opcount = nullptr;       // [mN] per-target sparse modMACs
     uint64_t sparse_ops = 0, dense_ops = 0;
     uint64_t kwork[KT_N] = {0, 0, 0, 0, 0};   // algorithmic modMACs per kernel family (this rank)
+    uint64_t trail_elems = 0;                  // D entries the echelon's trailing updates read + write
 
     // call-order state
     bool did_reduce_B = false, did_cprime = false, did_update = false, did_fused = false;

@@ -55,7 +55,7 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr);
+                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr, int grid_cap = 0);
 void modgemm_set_sms(int sms);
 
 namespace {
@@ -272,64 +272,81 @@ __device__ int blocked_lu(uint16_t *X, int ncand, const uint32_t *freel, uint32_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #define BV(q_, j_) X[(q_) * LDX + 128 + (j_)]
 #define BL(q_, j_) X[(q_) * LDX + 160 + (j_)]
+    // phase F layout: thread = (store row r = tid / 8, lane group gl = tid % 8); it holds the row's
+    // block columns 4 gl .. 4 gl + 3 (v) and transform columns 4 gl .. (l) in registers, and
+    // publishes them to BV / BL after every change (the next pivot row is read from there)
+    const int r = tid >> 3, gl = tid & 7, c4 = 4 * gl;
+    const unsigned gmask = 0xffu << (lane & 24);
     int slot = 0, nsteps = 0;
     for (int cb = 0; cb < ldv; cb += 32) {
-        for (int idx = tid; idx < PK * 32; idx += NT) {
-            const int q = idx >> 5, j = idx & 31;
-            BV(q, j) = X[q * LDX + cb + j];
-            BL(q, j) = 0;
+        const bool loaded = cstat[r] != 0;
+        bool fr = cstat[r] == 1;                               // free candidate row
+        uint32_t v[4], l[4] = {0, 0, 0, 0}, sg = 1;
+        {
+            const uint2 q = *reinterpret_cast<const uint2 *>(&X[r * LDX + cb + c4]);
+            v[0] = q.x & 0xffffu; v[1] = q.x >> 16; v[2] = q.y & 0xffffu; v[3] = q.y >> 16;
+            *reinterpret_cast<uint2 *>(&BV(r, c4)) = q;
+            *reinterpret_cast<uint2 *>(&BL(r, c4)) = make_uint2(0, 0);
+            if (gl == 0) sig[r] = 1;
         }
-        for (int q = tid; q < PK; q += NT) sig[q] = 1;
         __syncthreads();
         int kj = 0;
         for (;;) {                                                             // phase F
             nsteps++;
-            uint32_t best = NONE16;
-            for (int ci = warp; ci < ncand; ci += 32) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] != 1) continue;
-                const unsigned m = __ballot_sync(FULL, BV(q, lane) != 0);
-                if (m) {
-                    const uint32_t key = ((uint32_t)(__ffs(m) - 1) << 7) | q;
-                    best = key < best ? key : best;
-                }
+            uint32_t ld = NONE16;                                  // the row's lead in the block (group min)
+            if (fr) {
+#pragma unroll
+                for (int i = 3; i >= 0; i--) if (v[i]) ld = (uint32_t)(c4 + i);
             }
-            if (lane == 0) wbest[slot][warp] = best;              // one slot per warp: no atomics
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {                      // all lanes: no divergent shuffles
+                const uint32_t y = __shfl_xor_sync(FULL, ld, o);
+                ld = y < ld ? y : ld;
+            }
+            uint32_t key = ld != NONE16 ? ((ld << 7) | (uint32_t)r) : NONE16;
+            key = __reduce_min_sync(FULL, key);
+            if (lane == 0) wbest[slot][warp] = key;              // one slot per warp: no atomics
             __syncthreads();
-            const uint32_t key = __reduce_min_sync(FULL, wbest[slot][lane]);
+            key = __reduce_min_sync(FULL, wbest[slot][lane]);
             slot ^= 1;
             if (key == NONE16) break;
             const int c = (int)(key >> 7);
-            const uint32_t hq = key & 127u;
-            const uint32_t vh = BV(hq, c), sh = sig[hq];
-            for (int ci = warp; ci < ncand; ci += 32) {
-                const uint32_t q = freel[ci];
-                if (cstat[q] != 1) continue;
-                if (q == hq) {
-                    __syncwarp();
-                    if (lane == 0) { cstat[q] = 2; clead[q] = (uint32_t)(cb + c); }
-                    __syncwarp();
-                    continue;
+            const int hq = (int)(key & 127u);
+            if (r == hq) {
+                fr = false;
+                if (gl == 0) { cstat[r] = 2; clead[r] = (uint32_t)(cb + c); }
+            } else if (fr) {
+                const uint32_t src = (uint32_t)((lane & 24) | (c >> 2)), ci = (uint32_t)(c & 3);
+                const uint32_t mine = ci == 0 ? v[0] : ci == 1 ? v[1] : ci == 2 ? v[2] : v[3];
+                const uint32_t f = __shfl_sync(gmask, mine, src, 32);
+                if (f) {
+                    const uint32_t vh = BV(hq, c), nf = p - f;
+                    const uint2 pv = *reinterpret_cast<const uint2 *>(&BV(hq, c4));
+                    const uint2 pl = *reinterpret_cast<const uint2 *>(&BL(hq, c4));
+                    const uint32_t pvv[4] = {pv.x & 0xffffu, pv.x >> 16, pv.y & 0xffffu, pv.y >> 16};
+                    const uint32_t plv[4] = {pl.x & 0xffffu, pl.x >> 16, pl.y & 0xffffu, pl.y >> 16};
+                    const uint32_t sh = sig[hq];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        v[i] = mod32(mod32(vh * v[i], p, m32) + nf * pvv[i], p, m32);
+                        const int j = c4 + i;
+                        if (j < kj) l[i] = mod32(mod32(vh * l[i], p, m32) + nf * plv[i], p, m32);
+                        else if (j == kj) l[i] = mod32(nf * sh, p, m32);
+                    }
+                    sg = mod32(vh * sg, p, m32);
+                    *reinterpret_cast<uint2 *>(&BV(r, c4)) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+                    *reinterpret_cast<uint2 *>(&BL(r, c4)) = make_uint2(l[0] | (l[1] << 16), l[2] | (l[3] << 16));
+                    if (gl == 0) sig[r] = sg;
                 }
-                const uint32_t f = BV(q, c);
-                __syncwarp();
-                if (!f) continue;
-                const uint32_t nf = p - f;
-                BV(q, lane) = (uint16_t)mod32(mod32(vh * BV(q, lane), p, m32) + nf * BV(hq, lane), p, m32);
-                uint32_t l = 0;
-                if (lane < kj) l = mod32(mod32(vh * BL(q, lane), p, m32) + nf * BL(hq, lane), p, m32);
-                else if (lane == kj) l = mod32(nf * sh, p, m32);
-                if (lane <= kj) BL(q, lane) = (uint16_t)l;
-                if (lane == 0) sig[q] = mod32(vh * sig[q], p, m32);
-                __syncwarp();
             }
-            if (tid == 0) prow[kj] = hq;
+            if (tid == 0) prow[kj] = (uint32_t)hq;
             kj++;
             if (kj == 32) {                         // the block is full: every column has a pivot
                 __syncthreads();
                 break;
             }
         }
+        (void)loaded;
         // phase U: block columns = V; the rest of the window and the coefficients by one K = 32 product
         if (kj > 0) {
             const int nv = ldv - cb - 32, nvc = nv + PK;
@@ -1222,6 +1239,7 @@ __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t
         ops[0] += (unsigned long long)ps->nrows * ps->kp * w;                 // trailing update
         ops[1] += (unsigned long long)ps->kp * ps->kp * w;                     // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * ps->kp * (unsigned long long)(ps->c1 - ps->c0);   // panel RREF
+        ops[3] += (unsigned long long)ps->nrows * w;                          // D entries of the update
     }
     const uint32_t kp = ps->kp;
     if (kp == 0) return;
@@ -1267,6 +1285,7 @@ __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, con
         ops[0] += (unsigned long long)ps->nrows * kp * w;                     // trailing update
         ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * kp * (unsigned long long)(ps->c1 - c0);   // panel RREF
+        ops[3] += (unsigned long long)ps->nrows * w;                                       // D entries of the update
     }
     // grid-stride over (row b, 8-column group); a few hundred blocks, so the next panel's
     // CTA is not queued behind thousands of tiny ones
@@ -1581,20 +1600,20 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
-    auto sp_begin = [&](const P2State *last) {
-        k_sp_begin<<<1, 1, 0, st>>>(last, nN, G, spCd);
+    auto sp_begin = [&](const P2State *last, cudaStream_t s) {
+        k_sp_begin<<<1, 1, 0, s>>>(last, nN, G, spCd);
         note_launch();
-        if (cudaMemsetAsync(Fdlo, 0, (size_t)ntrD * G * PK * 128, st) != cudaSuccess ||
-            cudaMemsetAsync(Fdhi, 0, (size_t)ntrD * G * PK * 128, st) != cudaSuccess)
+        if (cudaMemsetAsync(Fdlo, 0, (size_t)ntrD * G * PK * 128, s) != cudaSuccess ||
+            cudaMemsetAsync(Fdhi, 0, (size_t)ntrD * G * PK * 128, s) != cudaSuccess)
             return GBLA_E_CUDA;
         return GBLA_OK;
     };
-    auto sp_flush = [&](const P2State *cur, int ctsel) {
-        kt_mark(h, KT_TRAIL);
-        const gbla_status r = modgemm_tc_sub_mk(st, mN, nullptr, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
+    auto sp_flush = [&](const P2State *cur, int ctsel, cudaStream_t s) {
+        kt_mark_on(h, KT_TRAIL, s);
+        const gbla_status r = modgemm_tc_sub_mk(s, mN, nullptr, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
                                                 (int64_t)rd_stride, spc0, nullptr, h->D, ldD, spCd, &cur->c1, PW,
                                                 ctsel, gemm_grid);
-        kt_mark(h, KT_TRAIL);
+        kt_mark_on(h, KT_TRAIL, s);
         return r;
     };
     auto factor = [&](cudaStream_t s, int64_t k) {
@@ -1602,6 +1621,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         p_factor(s, k);
         p_gather(s, k);
     };
+    cudaStream_t rest = nullptr;          // GBLA_LA_SIDE: the older schedule (panel on the side stream)
+    if (lookahead && !getenv("GBLA_LA_SIDE")) rest = ctx_rest_stream(h->ctx);
     if (lookahead) {                      // the next panel is the critical path: high-priority side stream
         side = ctx_side_stream(h->ctx);
         evA = ctx_event(h->ctx, 0);
@@ -1612,7 +1633,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     if (status == GBLA_OK) {
         k_p2_init<<<1, 1, 0, st>>>(ps);
         note_launch();
-        if (G > 1) status = sp_begin(nullptr);
+        if (G > 1) status = sp_begin(nullptr, st);
         factor(st, 0);                                  // panel 0 on the main stream
     }
     // optional timeline (GBLA_ECH_TIMELINE=n): device times of the first n look-ahead iterations
@@ -1677,6 +1698,53 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 0);
                 note_launch();
                 factor(st, k + 1);
+            } else if (rest) {
+                // critical chain on the main stream (launches back to back, PDL): window update ->
+                // leads -> panel -> F gather of the next panel; the rest of the update of this panel
+                // on the low-priority stream beside it.  Hazards: the rest writes D outside the next
+                // window, reads F / rows / T / P2State of parity k (the next panel writes parity k+1)
+                // and the B and Rn tiles, which the next iteration rewrites only after waiting evR.
+                kt_mark(h, KT_TRAIL);
+                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
+                kt_mark(h, KT_TRAIL);
+                if (status != GBLA_OK) break;
+                tmark(k, st);
+                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
+                if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(rest, evA, 0) != cudaSuccess) {
+                    fail("event");
+                    break;
+                }
+                tmark(k, rest);
+                launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, rest, nN,
+                           (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
+                           (unsigned long long *)nullptr, 2);
+                note_launch();
+                kt_mark_on(h, KT_RN, rest);
+                status = modgemm_tc_store(rest, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
+                                          &cur->kp, &cur->c1, PW, 2, cur->sel, gemm_grid);   // an SM for the panel
+                kt_mark_on(h, KT_RN, rest);
+                if (status != GBLA_OK) break;
+                kt_mark_on(h, KT_TRAIL, rest);
+                status = modgemm_tc_sub(rest, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
+                                        ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
+                kt_mark_on(h, KT_TRAIL, rest);
+                if (status != GBLA_OK) break;
+                if (G > 1 && j == G - 1) {              // end of the super-panel: the deferred columns
+                    if ((status = sp_flush(cur, 2, rest)) != GBLA_OK || (status = sp_begin(cur, rest)) != GBLA_OK)
+                        break;
+                }
+                tmark(k, rest);
+                if (cudaEventRecord(evB, rest) != cudaSuccess) { fail("event"); break; }
+                p_lead(st, k + 1);
+                tmark(k, st);
+                p_factor(st, k + 1);
+                tmark(k, st);
+                // sp_begin cleared the deferred factor tiles that the gather writes
+                if (G > 1 && j == G - 1 && cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
+                p_gather(st, k + 1);
+                tmark(k, st);
+                if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
             } else {
                 // the next panel's window first, then the next panel beside the rest of the update
                 kt_mark(h, KT_TRAIL);
@@ -1684,7 +1752,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 if (status != GBLA_OK) break;
                 tmark(k, st);
-                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1)) != GBLA_OK) break;   // next window
+                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
                 p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
@@ -1709,7 +1777,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
                 if (G > 1 && j == G - 1) {              // end of the super-panel: the deferred columns
-                    if ((status = sp_flush(cur, 2)) != GBLA_OK || (status = sp_begin(cur)) != GBLA_OK) break;
+                    if ((status = sp_flush(cur, 2, st)) != GBLA_OK || (status = sp_begin(cur, st)) != GBLA_OK) break;
                 }
                 tmark(k, st);
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
@@ -1743,11 +1811,12 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     }
     if (status == GBLA_OK && G > 1 && (k % G) != 0) {      // the last, partial super-panel
         P2State *last = ps + ((k - 1) & 1);
-        status = sp_flush(last, 0);
+        status = sp_flush(last, 0, st);
     }
     if (status == GBLA_OK && cudaStreamSynchronize(st) != cudaSuccess) fail("sync");
 
     if (side) cudaStreamSynchronize(side);
+    if (rest) cudaStreamSynchronize(rest);
     if (!tl.empty()) {
         cudaDeviceSynchronize();
         // per iteration (us from its start): side panel start, end; main rest start, end; gather end
@@ -2034,15 +2103,16 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         }
     GBLA_TRY(exclusive_scan_u32<uint32_t>(h, gflag, gidx, nN + 1));
     uint32_t rk = 0;
-    unsigned long long dv[3] = {0, 0, 0};
+    unsigned long long dv[4] = {0, 0, 0, 0};
     GBLA_CUDA_TRY(cudaMemcpyAsync(&rk, gidx + nN, 4, cudaMemcpyDeviceToHost, st));
-    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 24, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(dv, dops, 32, cudaMemcpyDeviceToHost, st));
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
     h->rank = rk;
     h->dense_ops = dv[0] + dv[1];
     h->kwork[KT_TRAIL] = dv[0];
     h->kwork[KT_RN] = dv[1];
     h->kwork[KT_PANEL] = dv[2];
+    h->trail_elems = dv[3];
     h->ldR = ldR;
     GBLA_TRY(dalloc_t(h, (size_t)(rk > 0 ? rk : 1) * h->ldR, &h->R));
     GBLA_TRY(dalloc_t(h, rk + 1, &h->pivcol));

@@ -269,6 +269,7 @@ __global__ void k_cfill(int64_t mN, int64_t NB, int64_t prank, int64_t pworld, i
 constexpr int NSTAGE = 3;
 constexpr int PART_LD = 128;                       // running partial of long lists: u16 [128][PART_LD]
 constexpr int SWEEP_SMEM = NSTAGE * 65536 + 128 * PART_LD * 2;   // 3 operand stages + the partial
+constexpr int SWEEP_THREADS = 256;                 // 8 warps: two per TMEM lane quarter in the epilogue
 
 // K5': persistent, dependency-driven block forward substitution.  With the band
 // tiles pre-multiplied (k_ahat: Â_IJ = -A_IJ inv(A_JJ) mod p) the block step is
@@ -281,11 +282,13 @@ constexpr int SWEEP_SMEM = NSTAGE * 65536 + 128 * PART_LD * 2;   // 3 operand st
 // deadlock.  Per 128-pivot block the chain of one target tile costs the last tile
 // pair + one epilogue + the flag hand-off; the A tiles of one J are shared in L2 by
 // all tiles working on J.
-__global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
+__global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stg = smem;
-    uint16_t *prow = reinterpret_cast<uint16_t *>(smem + NSTAGE * 65536) + threadIdx.x * PART_LD;
+    // 8 warps: warp w drains TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns 64 (w / 4) .. +63
+    const int row = threadIdx.x & 127, half = threadIdx.x >> 7, cbeg = 64 * half;
+    uint16_t *prow = reinterpret_cast<uint16_t *>(smem + NSTAGE * 65536) + row * PART_LD;
     __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar;
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t s_np[128], s_w[128];
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_s;
-    const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t ph_acc = 0;
     uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
     unsigned long long opsA = 0, opsB = 0;
@@ -322,17 +325,18 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         const int64_t J = lo, li = task - a.toff[lo];
         const int64_t T = a.prank + a.pworld * (a.i0 + li), first = T * 128;
         const int64_t Jmin = a.jmin[li];
-        const int64_t slot = first + tid;
+        const int64_t slot = first + row;
         const bool live = slot < a.mN;
         const uint32_t t = live ? a.order[slot] : 0;
         uint8_t *Xrow = a.Xt + (size_t)li * a.NB * TB;
         const uint32_t *fl = a.flags + (size_t)li * a.NB;
         const uint32_t jbase = (uint32_t)J * 128;
-        {
+        if (tid < 128) {
             const uint32_t jg = jbase + tid;
             s_np[tid] = jg < (uint64_t)a.npiv ? a.ab_np[jg] : 1;
             s_w[tid] = jg < (uint64_t)a.npiv ? a.ab_w[jg] : 1;
         }
+        __syncthreads();                               // s_np / s_w are read by other threads in the epilogue
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
             tc::fence_after();
             if (c1 < npair) {                          // fold this chunk into the partial, free TMEM
 #pragma unroll 1
-                for (int c = 0; c < 128; c += 16) {
+                for (int c = cbeg; c < cbeg + 64; c += 16) {
                     uint32_t Rv[16];
                     read_R(lane_addr, c, Rv, a.F);
 #pragma unroll
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
         // epilogue: X_J = S (+ partial) mod p -> limb-plane tile (global) [+ C' u16], op counts (Alg 2)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
-        for (int c8 = 0; c8 < 128; c8 += 16) {
+        for (int c8 = cbeg; c8 < cbeg + 64; c8 += 16) {
             const int c = c8 / 16;
             uint32_t Rv[16];
             read_R(lane_addr, c8, Rv, a.F);
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(128, 1) k_sweep(SweepArgs a)
                     opsB += s_w[c * 16 + j] - s_np[c * 16 + j];
                 }
             }
-            const uint32_t o = tc::toff(tid, c * 16);
+            const uint32_t o = tc::toff(row, c * 16);
             *reinterpret_cast<uint4 *>(xt + o) = *reinterpret_cast<uint4 *>(lo8);
             *reinterpret_cast<uint4 *>(xt + PB + o) = *reinterpret_cast<uint4 *>(hi8);
             if (a.X16 && live) {
@@ -784,7 +788,7 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
     static int occ = -1;
     if (occ < 0) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
-        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, 128, SWEEP_SMEM));
+        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, SWEEP_THREADS, SWEEP_SMEM));
         if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     }
     // task schedule: first block of every local tile -> J-major task offsets
@@ -834,7 +838,7 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
     void *kargs[] = {&a};
     kt_mark(h, KT_SWEEP);
-    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(128), kargs,
+    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(SWEEP_THREADS), kargs,
                                               (size_t)SWEEP_SMEM, st));
     kt_mark(h, KT_SWEEP);
     note_launch();

@@ -539,13 +539,14 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows)
+                             int64_t win_w, int ctsel, const uint32_t *orows, int grid_cap)
 {
     if (orows && (!skip_dev || !c0_dev)) { set_error("modgemm_tc_store: row map needs the pivot count"); return GBLA_E_INVAL; }
     if (cols <= 0) return GBLA_OK;
     const int64_t tiles = (cols + BN - 1) / BN;
     int64_t grid = (tiles + 1) / 2;                       // two column tiles per CTA (TMEM double buffer)
     if (grid > g_sms) grid = g_sms;
+    if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
     MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, orows, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
     GBLA_TRY(launch_ws<MODE_STORE>(a, grid, st));
     note_launch();
