@@ -177,6 +177,7 @@ def roofline(kms, kwork, peaks, peak_src, sm_count):
         out = {"bound": "hbm", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
                "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                "algorithmic_bytes": int(byts), "algorithmic_bytes_per_launch": int(byts / max(n, 1)),
+               "launch_note": "launches = timed K11 trailing launches (window and rest parts of every panel, flushes)",
                "tensor_TOPS": round(tens, 2), "tensor_frac": round(tens / (2.0 * float(peaks["bf16_tflops"])), 5),
                "intensity_ops_per_byte": round(work * 8 / byts, 1) if byts else None}
     elif dom == "panel":

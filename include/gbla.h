@@ -90,6 +90,12 @@ gbla_status gbla_ctx_create(int device, gbla_ctx *out);
 /* Route every device allocation through (alloc, free); NULL restores the
  * default (cudaMallocAsync / cudaFreeAsync on the call's stream). */
 gbla_status gbla_ctx_set_allocator(gbla_ctx ctx, gbla_alloc_fn alloc, gbla_free_fn free_fn, void *user);
+/* Optional: bytes the context's allocator can still provide (the driver's free memory plus what
+ * a caching allocator holds unused).  The sparse phase sizes its batches of X tiles from it
+ * (without it: cudaMemGetInfo, which does not see a caching allocator's free blocks).  fn is
+ * called on the host thread that calls the library; NULL restores the default. */
+typedef size_t (*gbla_memq_fn)(void *user);
+gbla_status gbla_ctx_set_mem_query(gbla_ctx ctx, gbla_memq_fn fn, void *user);
 /* Multi-GPU: join an NCCL communicator built from a 128-byte ncclUniqueId
  * shared by the caller (e.g. through torch.distributed), as `rank` of
  * `world`.  Collective: every rank must call it.  world == 1 detaches. */

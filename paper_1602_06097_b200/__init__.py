@@ -47,6 +47,7 @@ class _CSR(ctypes.Structure):
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+_MEMQ_FN = ctypes.CFUNCTYPE(ctypes.c_size_t, ctypes.c_void_p)
 
 _lib = None
 
@@ -65,6 +66,7 @@ def load_library(path: str = LIB_PATH):
     sig = {
         "gbla_ctx_create": ([ctypes.c_int, P(vp)], st),
         "gbla_ctx_set_allocator": ([vp, _ALLOC_FN, _FREE_FN, vp], st),
+        "gbla_ctx_set_mem_query": ([vp, _MEMQ_FN, vp], st),
         "gbla_ctx_set_comm": ([vp, vp, ctypes.c_int, ctypes.c_int], st),
         "gbla_ctx_destroy": ([vp], None),
         "gbla_splice": ([vp, P(_CSR), u32, u32, vp, P(vp)], st),
@@ -104,7 +106,8 @@ def load_library(path: str = LIB_PATH):
 
 def exported_symbols():
     """Names the binding expects the library to export (tests check them)."""
-    return ["gbla_ctx_create", "gbla_ctx_set_allocator", "gbla_ctx_set_comm", "gbla_ctx_destroy",
+    return ["gbla_ctx_create", "gbla_ctx_set_allocator", "gbla_ctx_set_mem_query", "gbla_ctx_set_comm",
+            "gbla_ctx_destroy",
             "gbla_splice", "gbla_reduce_B", "gbla_reduce_C", "gbla_update_D", "gbla_echelon_D", "gbla_reduce",
             "gbla_get_dims", "gbla_get_maps", "gbla_get_D", "gbla_get_Cprime", "gbla_get_Bprime",
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
@@ -171,6 +174,14 @@ class Context:
             self._alloc_cb = _ALLOC_FN(_alloc)
             self._free_cb = _FREE_FN(_free)
             _check(L.gbla_ctx_set_allocator(self._h, self._alloc_cb, self._free_cb, None))
+
+            def _memq(user):
+                # driver free memory + blocks torch's caching allocator holds unused
+                free = torch.cuda.mem_get_info(dev)[0]
+                return int(free + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev))
+
+            self._memq_cb = _MEMQ_FN(_memq)
+            _check(L.gbla_ctx_set_mem_query(self._h, self._memq_cb, None))
 
     def set_comm(self, unique_id: bytes, rank: int, world: int):
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)

@@ -141,6 +141,14 @@ extern "C" gbla_status gbla_ctx_set_allocator(gbla_ctx ctx, gbla_alloc_fn alloc,
     return GBLA_OK;
 }
 
+extern "C" gbla_status gbla_ctx_set_mem_query(gbla_ctx ctx, gbla_memq_fn fn, void *user)
+{
+    if (!ctx) { set_error("NULL context"); return GBLA_E_INVAL; }
+    ctx->memq = fn;
+    ctx->memq_user = user;
+    return GBLA_OK;
+}
+
 gbla_status dist_set_comm(gbla_ctx ctx, const void *id, int rank, int world);
 void dist_destroy(gbla_ctx ctx);
 

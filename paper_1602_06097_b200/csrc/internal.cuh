@@ -106,6 +106,8 @@ struct gbla_ctx_s {
     int rank = 0, world = 1;
     // per-context resources reused across calls (creating them per call costs host time that
     // stalls the pipelined panel loop): the echelon's side stream, sync events, pinned scratch
+    size_t (*memq)(void *) = nullptr;    // gbla_ctx_set_mem_query
+    void *memq_user = nullptr;
     cudaStream_t side = nullptr;
     cudaStream_t rest = nullptr;         // low priority: the off-chain part of the echelon's trailing updates
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};

@@ -1752,6 +1752,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
+                kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
                 tmark(k, st);
                 if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
@@ -1774,6 +1775,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                           &cur->kp, &cur->c1, PW, 2, cur->sel);
                 kt_mark(h, KT_RN);
                 if (status != GBLA_OK) break;
+                kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);

@@ -270,6 +270,12 @@ constexpr int NSTAGE = 3;
 constexpr int PART_LD = 128;                       // running partial of long lists: u16 [128][PART_LD]
 constexpr int SWEEP_SMEM = NSTAGE * 65536 + 128 * PART_LD * 2;   // 3 operand stages + the partial
 constexpr int SWEEP_THREADS = 256;                 // 8 warps: two per TMEM lane quarter in the epilogue
+// GBLA_SWEEP_THREADS = 128: one warp per lane quarter (each drains all 128 columns)
+static int sweep_threads()
+{
+    const char *e = getenv("GBLA_SWEEP_THREADS");
+    return e && atoi(e) == 128 ? 128 : SWEEP_THREADS;
+}
 
 // K5': persistent, dependency-driven block forward substitution.  With the band
 // tiles pre-multiplied (k_ahat: Â_IJ = -A_IJ inv(A_JJ) mod p) the block step is
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *stg = smem;
     // 8 warps: warp w drains TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns 64 (w / 4) .. +63
-    const int row = threadIdx.x & 127, half = threadIdx.x >> 7, cbeg = 64 * half;
+    const int row = threadIdx.x & 127, ncol = 128 / (int)(blockDim.x >> 7), cbeg = ncol * (int)(threadIdx.x >> 7);
     uint16_t *prow = reinterpret_cast<uint16_t *>(smem + NSTAGE * 65536) + row * PART_LD;
     __shared__ uint64_t full[NSTAGE], mdone[NSTAGE], accbar;
     __shared__ uint32_t tmem_s;
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
             tc::fence_after();
             if (c1 < npair) {                          // fold this chunk into the partial, free TMEM
 #pragma unroll 1
-                for (int c = cbeg; c < cbeg + 64; c += 16) {
+                for (int c = cbeg; c < cbeg + ncol; c += 16) {
                     uint32_t Rv[16];
                     read_R(lane_addr, c, Rv, a.F);
 #pragma unroll
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         // epilogue: X_J = S (+ partial) mod p -> limb-plane tile (global) [+ C' u16], op counts (Alg 2)
         uint8_t *xt = Xrow + (size_t)J * TB;
 #pragma unroll 1
-        for (int c8 = cbeg; c8 < cbeg + 64; c8 += 16) {
+        for (int c8 = cbeg; c8 < cbeg + ncol; c8 += 16) {
             const int c = c8 / 16;
             uint32_t Rv[16];
             read_R(lane_addr, c8, Rv, a.F);
@@ -769,7 +775,8 @@ static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
     if (e && atoll(e) > 0) return atoll(e) < nl ? atoll(e) : nl;
     if (nl * per_tile <= ((int64_t)8 << 30)) return nl;   // small: no need to ask the driver
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
+    if (h->ctx->memq) fr = h->ctx->memq(h->ctx->memq_user);      // the caller's allocator (torch: + cached)
+    else if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
     const int64_t reserve = (int64_t)4 << 30;
     int64_t budget = (int64_t)fr - reserve;
     if (budget < per_tile) budget = per_tile;
@@ -788,7 +795,7 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
     static int occ = -1;
     if (occ < 0) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
-        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, SWEEP_THREADS, SWEEP_SMEM));
+        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, sweep_threads(), SWEEP_SMEM));
         if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     }
     // task schedule: first block of every local tile -> J-major task offsets
@@ -838,7 +845,7 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
     void *kargs[] = {&a};
     kt_mark(h, KT_SWEEP);
-    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(SWEEP_THREADS), kargs,
+    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(sweep_threads()), kargs,
                                               (size_t)SWEEP_SMEM, st));
     kt_mark(h, KT_SWEEP);
     note_launch();

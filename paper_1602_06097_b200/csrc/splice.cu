@@ -145,7 +145,7 @@ __global__ void k_fill_rows(int64_t nrows, int64_t npiv, const uint32_t *__restr
             if (take) {
                 uint32_t pos = base + __popc(msk & lt);
                 ocol[o + pos] = sc;
-                oval[o + pos] = (uint16_t)fmul(val[q], il, F);
+                oval[o + pos] = (uint16_t)fmod32((uint32_t)val[q] * il, F);   // < 2^32: 32-bit Barrett
             }
             base += __popc(msk);
         }

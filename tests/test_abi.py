@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "gbla.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(gbla_[A-Za-z_0-9]+)\s*\(", src)) - {"gbla_alloc_fn", "gbla_free_fn"})
+    return sorted(set(re.findall(r"\b(gbla_[A-Za-z_0-9]+)\s*\(", src)) - {"gbla_alloc_fn", "gbla_free_fn", "gbla_memq_fn"})
 
 
 @pytest.fixture(scope="module")
