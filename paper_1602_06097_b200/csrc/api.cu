@@ -1,3 +1,4 @@
+#include <algorithm>
 // api.cu -- the C ABI of include/gbla.h: argument checks, call-order state
 // machine, allocation through the context allocator, phase timing.
 #include <stdarg.h>
@@ -563,7 +564,10 @@ extern "C" void gbla_mat_free(gbla_mat h)
     dfree_all(h);
     cudaStreamSynchronize(h->stream);
     band_free(h);
-    for (auto &v : h->kt.ev)
-        for (cudaEvent_t e : v) kt_event_put(e);
+    std::vector<cudaEvent_t> all;                 // an event shared by two timer pairs goes back once
+    for (auto &v : h->kt.ev) all.insert(all.end(), v.begin(), v.end());
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    for (cudaEvent_t e : all) kt_event_put(e);
     delete h;
 }

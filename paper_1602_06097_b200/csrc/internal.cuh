@@ -236,6 +236,18 @@ static inline void kt_mark_on(gbla_mat h, int which, cudaStream_t s)
     h->kt.ev[which].push_back(e);
 }
 static inline void kt_mark(gbla_mat h, int which) { kt_mark_on(h, which, h->stream); }
+// one event closing a pair of family a and opening a pair of family b (adjacent launches: a second
+// record between them would cut the programmatic-dependent-launch overlap)
+static inline void kt_mark2(gbla_mat h, int a, int b, cudaStream_t s)
+{
+    if (!h->kt.on) return;
+    if (s != h->stream && getenv("GBLA_KT_MAIN_ONLY")) return;
+    cudaEvent_t e = kt_event_get();
+    if (!e) return;
+    cudaEventRecord(e, s);
+    h->kt.ev[a].push_back(e);
+    h->kt.ev[b].push_back(e);
+}
 // multi-GPU (dist.cu)
 gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out);
 gbla_status dist_sparse_phase(gbla_mat h);

@@ -1688,7 +1688,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                                                   &cur->c0, &cur->kp, &cur->c1, PW, 1, cur->sel)
                                : modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth,
                                                   &cur->c0, &cur->kp, &cur->c1, PW, 0);
-            kt_mark(h, KT_RN);
+            if (lookahead) kt_mark2(h, KT_RN, KT_TRAIL, st);    // closes Rn window, opens the window update
+            else kt_mark(h, KT_RN);
             if (lookahead) tmark(k, st);
             if (status != GBLA_OK) break;
             if (!lookahead) {
@@ -1706,7 +1707,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 // on the low-priority stream beside it.  Hazards: the rest writes D outside the next
                 // window, reads F / rows / T / P2State of parity k (the next panel writes parity k+1)
                 // and the B and Rn tiles, which the next iteration rewrites only after waiting evR.
-                kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);
@@ -1749,14 +1749,18 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
             } else {
                 // the next panel's window first, then the next panel beside the rest of the update
-                kt_mark(h, KT_TRAIL);
+                // timer pair of the window update closed after the next panel's lead scan: a mark
+                // between the two would cut the programmatic-dependent-launch overlap on the chain
+                // (the window part of the trailing time includes k_lead2: a small overestimate)
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
-                kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
                 tmark(k, st);
-                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
+                const bool wflush = G > 1 && j == G - 1;
+                if (wflush) kt_mark(h, KT_TRAIL);                 // (the flush has its own pair)
+                if (wflush && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
                 p_lead(st, k + 1);
+                if (!wflush) kt_mark(h, KT_TRAIL);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
                     break;
@@ -1773,9 +1777,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_RN);
                 status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
                                           &cur->kp, &cur->c1, PW, 2, cur->sel);
-                kt_mark(h, KT_RN);
+                kt_mark2(h, KT_RN, KT_TRAIL, st);
                 if (status != GBLA_OK) break;
-                kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
                                         ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);
