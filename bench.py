@@ -149,7 +149,7 @@ KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1, tcgen05)", "update": "k_upd
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
-def roofline(kms, kwork, peaks, peak_src, sm_count):
+def roofline(kms, kwork, peaks, peak_src, sm_count, deferred=False):
     """Roofline of the dominant kernel family (largest CUDA-event time over
     the timed steps).  Tensor-core kernels: achieved = algorithmic modMACs x
     4 u8 MACs (limb split) x 2 ops / kernel time, against the int8 dense peak
@@ -165,7 +165,18 @@ def roofline(kms, kwork, peaks, peak_src, sm_count):
         traffic_db = {}
     tr = traffic_db.get(dom)
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    if dom == "trailing" and kwork.get("trailing_elems"):
+    if dom == "trailing" and deferred:
+        # super-panels (D >= 4e8 entries: c2-c4): the columns right of the next windows take one
+        # K = 512 update per four panels (1024 u8 ops per byte of D moved, above the int8 ridge
+        # of ~510): the tensor rate bounds it
+        peak = 2.0 * float(peaks["bf16_tflops"])
+        ach = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        out = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 1), "unit": "TOPS",
+               "peak_source": f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TF/s "
+                              f"(MEASURED_PEAKS.json; nominal int8:bf16 = 2)",
+               "modmac_per_s_T": round(work / (ms / 1e3) / 1e12, 3) if ms > 0 else 0.0,
+               "note": "K11 with deferred (K = 512) updates of the columns beyond the next windows"}
+    elif dom == "trailing" and kwork.get("trailing_elems"):
         # K11 trailing update: K = 128 (multi-K 512) products into u16 D read-modify-written once per
         # launch: 128 modMACs x 8 u8 ops per 4 bytes = 256 ops/B < the int8 ridge (3342 TOPS / 6.5 TB/s
         # ~ 510 ops/B), so HBM bounds it.  Algorithmic bytes = 4 per D entry of the update (u16 read +
@@ -353,7 +364,9 @@ def main():
     if rank == 0:
         peaks, peak_src = _peaks()
         ph = {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]}
-        roof = roofline(kms, kwork, peaks, peak_src, sm_count=torch.cuda.get_device_properties(dev).multi_processor_count)
+        dims = rank_d[0] if rank_d else (0, 0, 0)
+        roof = roofline(kms, kwork, peaks, peak_src, sm_count=torch.cuda.get_device_properties(dev).multi_processor_count,
+                        deferred=float(dims[1]) * float(dims[2]) >= 4e8)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(cfg.name, M, args.cpu_targets)
