@@ -163,7 +163,11 @@ class Context:
             dev = torch.device("cuda", device)
 
             def _alloc(nbytes, stream, user):
-                t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                # an exception must not cross the C boundary: out of memory -> NULL -> GBLA_E_NOMEM
+                try:
+                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                except Exception:
+                    return None
                 ptr = t.data_ptr()
                 self._live[ptr] = t
                 return ptr
@@ -176,9 +180,14 @@ class Context:
             _check(L.gbla_ctx_set_allocator(self._h, self._alloc_cb, self._free_cb, None))
 
             def _memq(user):
-                # driver free memory + blocks torch's caching allocator holds unused
-                free = torch.cuda.mem_get_info(dev)[0]
-                return int(free + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev))
+                # what torch can still hand out in one piece: its unused cached blocks go back to the
+                # driver first (they may be fragmented), then the driver's free memory.  Called once
+                # per large reduction (sizing of the X-tile batches), never on a hot path.
+                try:
+                    torch.cuda.empty_cache()
+                    return int(torch.cuda.mem_get_info(dev)[0])
+                except Exception:
+                    return 0
 
             self._memq_cb = _MEMQ_FN(_memq)
             _check(L.gbla_ctx_set_mem_query(self._h, self._memq_cb, None))

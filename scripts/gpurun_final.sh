@@ -12,4 +12,4 @@ timeout 400 python bench.py --config c3 --steps 2 --warmup 1 --e2e-steps 0 --no-
 timeout 600 python bench.py --config c2 --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/f_bench_c2.log 2>&1
 timeout 900 python bench.py --config c4 --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/f_bench_c4.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 2000 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/f_ncu.log 2>&1; echo "ncu rc=$?" >> gpurun_out/f_ncu.log
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:"modgemm_ws<0" -s 41 -c 1 -o gpurun_out/f_trailing python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/f_ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/f_ncu_full.log
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_modgemm_ws -s 43 -c 1 -o gpurun_out/f_trailing python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/f_ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/f_ncu_full.log
