@@ -415,6 +415,255 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
+// ---- the echelon's window step in ONE launch (look-ahead path, GBLA_WIN_FUSED) ---------------
+// Tiles q = 0 .. nW-1: Rn window column tile ct = w0 + q (MODE_STORE: A = T, B = the gathered B
+// tiles of D[S, c0:]; writes D[S, c0:] = Rn and the Rn limb tiles, then publishes flag[q] = epoch);
+// tiles q >= nW: the window update D[rows, c0:] -= F Rn for row tile (q - nW) / nW and column tile
+// w0 + (q - nW) % nW (MODE_SUB), whose B operand (the Rn tile) is waited for by its flag.  CTA b
+// takes tiles b, b + grid, ...: a CTA's first tile is its only Rn tile, so every wait is on a tile
+// another CTA reaches first; all CTAs are co-resident (one per SM, grid <= SMs), so no cycle.
+struct WinArgs {
+    Field F;
+    const uint8_t *Tlo, *Thi;              // A operand of the Rn tiles (one 128 x 128 tile)
+    const uint8_t *Bglo, *Bghi;            // gathered B tiles of D[S, c0:] (column tiles from c0)
+    uint8_t *Rlo, *Rhi;                    // Rn limb tiles (written here, B operand of the update)
+    const uint8_t *Flo, *Fhi;              // A operand of the update (row tiles of the F list)
+    const uint32_t *rows;                  // D rows of the update (slot -> row)
+    const uint32_t *sel;                   // D rows of the pivot rows (slot -> row)
+    const uint32_t *nrows_dev, *kp_dev;
+    const int64_t *c0_dev, *win_dev;
+    int64_t win_w, cols;
+    uint16_t *D;
+    int64_t ldD;
+    uint32_t *flags;
+    uint32_t epoch;
+};
+
+__device__ __forceinline__ uint32_t ld_acq(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
+{
+    constexpr int EPI_WARPS = 8, EPI_COLS = BN / (EPI_WARPS / 4);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t afull[2], aempty[2], bfull[NSB], bempty[NSB], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base;
+    tc::pdl_trigger();
+    tc::pdl_wait();
+    const uint32_t kp = *g.kp_dev;
+    if (kp == 0) return;
+    const int64_t c0 = *g.c0_dev;
+    const int64_t cols = g.cols - c0;
+    if (cols <= 0) return;
+    uint16_t *C = g.D + c0;
+    const int64_t nr = (int64_t)*g.nrows_dev;
+    const int64_t ntr = (nr + BM - 1) / BM, ntc_all = (cols + BN - 1) / BN;
+    const int64_t rel = *g.win_dev - c0;
+    int64_t w0 = rel > 0 ? rel / BN : 0, w1 = rel + g.win_w > 0 ? (rel + g.win_w + BN - 1) / BN : 0;
+    if (w0 > ntc_all) w0 = ntc_all;
+    if (w1 > ntc_all) w1 = ntc_all;
+    if (w1 < w0) w1 = w0;
+    const int64_t nW = w1 - w0;
+    if (nW == 0) return;
+    const int64_t ntiles = nW + ntr * nW;
+    const int64_t cnt = (int64_t)blockIdx.x < ntiles ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    if (cnt == 0) return;
+    auto tile_q = [&](int64_t i) -> int64_t { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+    // -1: the T tile (Rn), else the row tile of the update; column tile
+    auto rt_of = [&](int64_t q) -> int64_t { return q < nW ? -1 : (q - nW) / nW; };
+    auto ct_of = [&](int64_t q) -> int64_t { return w0 + (q < nW ? q : (q - nW) % nW); };
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&afull[i], 1);
+            tc::mbar_init(&aempty[i], 1);
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], EPI_WARPS);
+        }
+        for (int i = 0; i < NSB; i++) {
+            tc::mbar_init(&bfull[i], 1);
+            tc::mbar_init(&bempty[i], 1);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tmem_base;
+    uint8_t *Abuf = smem, *Bbuf = smem + 2 * A_BYTES;
+    if (warp == 0) {
+        if (lane == 0) {                       // ---- producer
+            int64_t cur_rt = -2;
+            int aslot = 1;
+            uint32_t aph[2] = {1, 1}, bph[NSB] = {1, 1, 1, 1};
+            int s = 0;
+            for (int64_t i = 0; i < cnt; i++) {
+                const int64_t q = tile_q(i), rt = rt_of(q), ct = ct_of(q);
+                if (rt != cur_rt) {
+                    aslot ^= 1;
+                    tc::mbar_wait(&aempty[aslot], aph[aslot]);
+                    aph[aslot] ^= 1;
+                    uint8_t *ab = Abuf + aslot * A_BYTES;
+                    tc::mbar_expect_tx(&afull[aslot], A_BYTES);
+                    if (rt < 0) {
+                        tc::bulk_g2s(ab, g.Thi, A_PLANE, &afull[aslot]);
+                        tc::bulk_g2s(ab + A_PLANE, g.Tlo, A_PLANE, &afull[aslot]);
+                    } else {
+                        tc::bulk_g2s(ab, g.Fhi + rt * A_PLANE, A_PLANE, &afull[aslot]);
+                        tc::bulk_g2s(ab + A_PLANE, g.Flo + rt * A_PLANE, A_PLANE, &afull[aslot]);
+                    }
+                    cur_rt = rt;
+                }
+                tc::mbar_wait(&bempty[s], bph[s]);
+                bph[s] ^= 1;
+                uint8_t *bb = Bbuf + s * B_BYTES;
+                if (rt >= 0) {                 // the Rn tile: published by the CTA that computed it
+                    const uint32_t *fl = g.flags + (ct - w0);
+                    for (uint32_t it = 0; ld_acq(fl) != g.epoch; it++) {
+                        __nanosleep(64);
+                        if (it > (1u << 24)) break;          // never hang the GPU (a test would fail)
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                tc::mbar_expect_tx(&bfull[s], B_BYTES);
+                const uint8_t *bh = rt < 0 ? g.Bghi : g.Rhi, *bl = rt < 0 ? g.Bglo : g.Rlo;
+                tc::bulk_g2s(bb, bh + ct * B_PLANE, B_PLANE, &bfull[s]);
+                tc::bulk_g2s(bb + B_PLANE, bl + ct * B_PLANE, B_PLANE, &bfull[s]);
+                s = (s + 1) % NSB;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                       // ---- MMA issuer
+            int64_t cur_rt = -2;
+            int aslot = 1;
+            uint32_t aph[2] = {0, 0}, bph[NSB] = {0, 0, 0, 0}, tph[2] = {1, 1};
+            int s = 0, ab = 0;
+            const uint32_t idesc = tc::idesc_u8(BM, BN);
+            for (int64_t i = 0; i < cnt; i++) {
+                const int64_t rt = rt_of(tile_q(i));
+                if (rt != cur_rt) {
+                    if (cur_rt != -2) tc::commit(&aempty[aslot]);
+                    aslot ^= 1;
+                    tc::mbar_wait(&afull[aslot], aph[aslot]);
+                    aph[aslot] ^= 1;
+                    cur_rt = rt;
+                }
+                tc::mbar_wait(&bfull[s], bph[s]);
+                bph[s] ^= 1;
+                tc::mbar_wait(&tempty[ab], tph[ab]);
+                tph[ab] ^= 1;
+                tc::fence_after();
+                const uint32_t aH = tc::smem_u32(Abuf + aslot * A_BYTES), aL = aH + A_PLANE;
+                const uint32_t bH = tc::smem_u32(Bbuf + s * B_BYTES), bL = bH + B_PLANE;
+                const uint32_t d = tbase + ab * 3 * BN;
+#pragma unroll
+                for (int k = 0; k < KP / 32; k++) {
+                    const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
+                    const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
+                    const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
+                    const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
+                    const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
+                    tc::mma_i8(d + 0, dAh, dBh, idesc, k > 0);
+                    tc::mma_i8(d + BN, dAh, dBl, idesc, k > 0);
+                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);
+                    tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, k > 0);
+                }
+                tc::commit(&bempty[s]);
+                tc::commit(&tfull[ab]);
+                s = (s + 1) % NSB;
+                ab ^= 1;
+            }
+        }
+    } else {                                   // ---- epilogue warps 2..9
+        const int e = warp - 2, quarter = warp & 3, part = e >> 2;
+        uint32_t tph[2] = {0, 0};
+        int ab = 0;
+        for (int64_t i = 0; i < cnt; i++) {
+            const int64_t q = tile_q(i), rt = rt_of(q), ct = ct_of(q);
+            const bool rn = rt < 0;
+            const int64_t x0 = ct * BN + part * EPI_COLS;
+            const int64_t slot = (rn ? 0 : rt * BM) + quarter * 32 + lane;
+            const bool live = rn ? slot < BM : slot < nr;            // rows of the accumulator
+            uint16_t *crow = nullptr;
+            if (rn ? slot < (int64_t)kp : live) crow = C + (size_t)(rn ? g.sel[slot] : g.rows[slot]) * g.ldD + x0;
+            const bool fast = crow && x0 + EPI_COLS <= cols && (g.ldD % 8 == 0) &&
+                              ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+            uint32_t dv[EPI_COLS / 2];
+#pragma unroll
+            for (int w = 0; w < EPI_COLS / 2; w++) dv[w] = 0;
+            if (!rn && crow) {                 // the D row segment to update
+                if (fast) {
+#pragma unroll
+                    for (int u = 0; u < EPI_COLS / 8; u++) {
+                        const uint4 v = reinterpret_cast<const uint4 *>(crow)[u];
+                        dv[4 * u] = v.x; dv[4 * u + 1] = v.y; dv[4 * u + 2] = v.z; dv[4 * u + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < EPI_COLS; j++)
+                        if (x0 + j < cols) dv[j / 2] |= (uint32_t)crow[j] << (16 * (j & 1));
+                }
+            }
+            tc::mbar_wait(&tfull[ab], tph[ab]);
+            tph[ab] ^= 1;
+            tc::fence_after();
+            const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 3 * BN + part * EPI_COLS;
+#pragma unroll
+            for (int c = 0; c < EPI_COLS; c += 16) {
+                uint32_t hh[16], xx[16], ll[16];
+                tc::tmem_ld16(la + c, hh);
+                tc::tmem_ld16(la + BN + c, xx);
+                tc::tmem_ld16(la + 2 * BN + c, ll);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const uint32_t s0 = fmod_limbs(hh[j], xx[j], ll[j], g.F);
+                    const uint32_t s1 = fmod_limbs(hh[j + 1], xx[j + 1], ll[j + 1], g.F);
+                    const int w = (c + j) / 2;
+                    if (!rn) {
+                        dv[w] = fsub2(dv[w], s0 | (s1 << 16), g.F.p | (g.F.p << 16));
+                    } else {
+                        dv[w] = s0 | (s1 << 16);
+                        const uint32_t x = (uint32_t)(x0 + c + j);
+                        const size_t o = (size_t)(x / BN) * B_PLANE + toff64(x % BN, (uint32_t)slot);
+                        g.Rlo[o] = (uint8_t)(s0 & 0xff);
+                        g.Rhi[o] = (uint8_t)(s0 >> 8);
+                        g.Rlo[o + 16] = (uint8_t)(s1 & 0xff);
+                        g.Rhi[o + 16] = (uint8_t)(s1 >> 8);
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+            ab ^= 1;
+            if (fast) {
+#pragma unroll
+                for (int u = 0; u < EPI_COLS / 8; u++)
+                    reinterpret_cast<uint4 *>(crow)[u] = make_uint4(dv[4 * u], dv[4 * u + 1], dv[4 * u + 2], dv[4 * u + 3]);
+            } else if (crow) {
+#pragma unroll
+                for (int j = 0; j < EPI_COLS; j++)
+                    if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
+            }
+            if (rn) {                          // publish the Rn tile: every epilogue thread's stores, then the flag
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+                if (warp == 2 && lane == 0)
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + (ct - w0)), "r"(g.epoch) : "memory");
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
 // INT-pipe reference engine for the same op (tests / GBLA_DENSE_INT).
 __global__ void k_modgemm_int(int64_t rows, int64_t cols, int64_t K, Field F, const uint16_t *__restrict__ A,
                               int64_t lda, const uint16_t *__restrict__ B, int64_t ldb,
@@ -571,6 +820,36 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
     GBLA_TRY((launch_ws1<MODE_SUB, 8, true, true>(a, grid, st)));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}
+
+// the echelon's window step in one launch (see k_modgemm_win)
+gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t *Tlo, const uint8_t *Thi,
+                           const uint8_t *Bglo, const uint8_t *Bghi, uint8_t *Rlo, uint8_t *Rhi,
+                           const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
+                           const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
+                           const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
+                           uint32_t epoch, int grid)
+{
+    static bool attr = false;
+    if (!attr) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_win, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
+        attr = true;
+    }
+    WinArgs a{F, Tlo, Thi, Bglo, Bghi, Rlo, Rhi, Flo, Fhi, rows, sel, nrows_dev, kp_dev, c0_dev, win_dev, win_w, cols,
+              D, ldD, flags, epoch};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(ws_threads(8));
+    cfg.dynamicSmemBytes = WS_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    GBLA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_modgemm_win, a));
+    note_launch();
     return GBLA_OK;
 }
 
