@@ -62,7 +62,7 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
                            const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
                            const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
-                           uint32_t epoch, int grid);
+                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN);
 
 namespace {
 
@@ -1635,6 +1635,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // flags; c1: 14.4 -> 14.1 ms); single super-panel panels only (G == 1), side-stream schedule;
     // GBLA_WIN_FUSED=0: two launches
     const bool winfused = lookahead && !rest && G == 1 && !(getenv("GBLA_WIN_FUSED") && atoi(getenv("GBLA_WIN_FUSED")) == 0);
+    // GBLA_WIN_LEAD=1: the window step also scans the next window's leads after a grid barrier (no
+    // k_lead2 launch).  Measured slower on c1 (14.2 vs 14.0 ms: 1,470 warps scanning ~5 rows each
+    // after the barrier vs a separate 4,700-warp launch), so off by default
+    const bool winlead = winfused && getenv("GBLA_WIN_LEAD") && atoi(getenv("GBLA_WIN_LEAD")) == 1;
     uint32_t *wflags = nullptr;
     if (winfused) {
         GBLA_TRY(dalloc_t(h, 64, &wflags));
@@ -1701,7 +1705,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_win(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rtl, Rth, Flo[f], Fhi[f], rows[f],
                                         cur->sel, &cur->nrows, &cur->kp, &cur->c0, &cur->c1, PW, h->D, ldD, wflags,
-                                        (uint32_t)(k + 1), gemm_grid);
+                                        (uint32_t)(k + 1), gemm_grid, winlead ? lead : nullptr, rowpiv, mN);
             } else {
                 kt_mark(h, KT_RN);
                 // look-ahead: only the window part of Rn is on the chain to the next panel, and the Rn
@@ -1783,7 +1787,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 const bool wflush = G > 1 && j == G - 1;
                 if (wflush) kt_mark(h, KT_TRAIL);                 // (the flush has its own pair)
                 if (wflush && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
-                p_lead(st, k + 1);
+                if (!(winfused && winlead)) p_lead(st, k + 1);   // else the window step scanned the leads
                 if (!wflush) kt_mark(h, KT_TRAIL);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");

@@ -223,6 +223,15 @@ def test_long_accumulations_are_chunked(gb, ctx):
     h.free()
 
 
+def test_window_step_with_lead_scan(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """GBLA_WIN_LEAD=1: the fused window step also computes the next window's leading columns after a
+    grid barrier (instead of k_lead2)."""
+    monkeypatch.setenv("GBLA_WIN_LEAD", "1")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.05))
+    check_full(gb, ctx, M, oracle.reduce(M))
+
+
 def test_window_step_in_two_launches(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     """GBLA_WIN_FUSED=0: the Rn window and the window update as two launches (the default fuses
     them into one persistent kernel with column-tile flags); both must give the oracle's R."""
