@@ -1628,13 +1628,14 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         p_gather(s, k);
     };
     // GBLA_LA_MAIN: the chain on the main stream and the rest of the update on a low-priority stream
-    // (measured slower on c1: 14.8 vs 14.4 ms); default: the next panel on the high-priority side stream
+    // (measured slower on c1: 14.3 vs 14.0 ms with the fused window step); default: the next panel on
+    // the high-priority side stream
     cudaStream_t rest = nullptr;
     if (lookahead && getenv("GBLA_LA_MAIN")) rest = ctx_rest_stream(h->ctx);
     // the Rn window and the window update in one persistent launch (k_modgemm_win, column-tile
     // flags; c1: 14.4 -> 14.1 ms); single super-panel panels only (G == 1), side-stream schedule;
     // GBLA_WIN_FUSED=0: two launches
-    const bool winfused = lookahead && !rest && G == 1 && !(getenv("GBLA_WIN_FUSED") && atoi(getenv("GBLA_WIN_FUSED")) == 0);
+    const bool winfused = lookahead && G == 1 && !(getenv("GBLA_WIN_FUSED") && atoi(getenv("GBLA_WIN_FUSED")) == 0);
     // GBLA_WIN_LEAD=1: the window step also scans the next window's leads after a grid barrier (no
     // k_lead2 launch).  Measured slower on c1 (14.2 vs 14.0 ms: 1,470 warps scanning ~5 rows each
     // after the barrier vs a separate 4,700-warp launch), so off by default
@@ -1734,12 +1735,15 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 // on the low-priority stream beside it.  Hazards: the rest writes D outside the next
                 // window, reads F / rows / T / P2State of parity k (the next panel writes parity k+1)
                 // and the B and Rn tiles, which the next iteration rewrites only after waiting evR.
-                status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
-                                        ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
+                if (!winfused)
+                    status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
+                                            ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
                 tmark(k, st);
                 if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
+                // the leads of the next window before the rest starts (they would compete for the SMs)
+                if (!winlead) p_lead(st, k + 1);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(rest, evA, 0) != cudaSuccess) {
                     fail("event");
                     break;
@@ -1765,7 +1769,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 }
                 tmark(k, rest);
                 if (cudaEventRecord(evB, rest) != cudaSuccess) { fail("event"); break; }
-                p_lead(st, k + 1);
                 tmark(k, st);
                 p_factor(st, k + 1);
                 tmark(k, st);
