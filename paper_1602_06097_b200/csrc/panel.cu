@@ -98,7 +98,7 @@ struct P2State {
     uint32_t kp;                        // pivots
     uint32_t nrows;                     // rows listed for the trailing update
     uint32_t ncand;                     // candidates integrated
-    uint32_t pad;
+    uint32_t ready;                     // epoch: sel / pc / kp / c0 / c1 / rowpiv marks are published
     uint32_t sel[PK];                   // selected rows (D row ids), pivot order of T
     uint32_t pc[PK];                    // absolute pivot columns
 };
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                                                    const P2State *__restrict__ prev, P2State *__restrict__ cur,
                                                    uint8_t *__restrict__ Tlo, uint8_t *__restrict__ Thi,
                                                    const uint16_t *__restrict__ invtab,
-                                                   unsigned long long *__restrict__ trace)
+                                                   unsigned long long *__restrict__ trace, uint32_t epoch)
 {
     extern __shared__ __align__(16) uint16_t X[];          // [PK][LDX] row store
     uint16_t(*FS)[FSLD] = reinterpret_cast<uint16_t(*)[FSLD]>(X + PK * LDX);   // factor snapshot
@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     const uint16_t *__restrict__ D = src.D;
     const int64_t ldD = src.ldD;
     const int64_t coff = src.gathered ? 0 : c0;           // column of window column 0 in D
+    bool published = false;                                // S / pivots published early (wide mode)
     // optional trace (GBLA_PANEL_TRACE): cycles per phase, accumulated over panels by thread 0
     long long t_mark = trace ? clock64() : 0;
 #define P2_LAP(k_)                                                                        \
@@ -470,7 +471,13 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     int64_t wmax = nN - c0;
     if (wmax > PW) wmax = PW;
     if (wmax <= 0) {
-        if (tid == 0) { cur->c0 = c0; cur->c1 = c0; cur->kp = 0; cur->nrows = 0; cur->ncand = 0; }
+        if (tid == 0) {
+            cur->c0 = c0; cur->c1 = c0; cur->kp = 0; cur->nrows = 0; cur->ncand = 0;
+            if (epoch) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&cur->ready), "r"(epoch) : "memory");
+            }
+        }
         return;
     }
     // ---- 1. width from the lead histogram
@@ -885,6 +892,30 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         //     basis); wide mode (one chunk) only needs the coefficients: T = U^-1 E.
         P2_LAP(4);
         if (!dense) {
+            if (epoch) {
+                // the pivots are final: publish S, the pivot columns and the window so that the F
+                // gather of the next step (k_gather2, waiting on `ready`) overlaps the T solve
+                if (tid < (int)nb) {
+                    const uint32_t rr = crow[bphys[tid]];
+                    const uint32_t r = src.rid ? src.rid[rr] : rr;
+                    cur->sel[tid] = r;
+                    cur->pc[tid] = (uint32_t)(c0 + bpc[tid]);
+                    if (!src.owner || src.owner[r] == src.me) rowpiv[r] = (uint32_t)(c0 + bpc[tid]);
+                }
+                if (tid == 0) {
+                    cur->c0 = c0;
+                    cur->c1 = c0 + width;
+                    cur->kp = nb;
+                    cur->nrows = 0;
+                    cur->ncand = ncand_tot;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&cur->ready), "r"(epoch) : "memory");
+                }
+                published = true;
+            }
             // Wide mode (one chunk, nb0 = 0): heads h_b (pivot order, not normalized) with
             // coefficients E_b.  U[b][b'] = h_b[pc_b'] / h_b[pc_b] is unit upper triangular and the
             // RREF basis is W (h_b / h_b[pc_b]) with W = U^-1, so T = W E', E'_b = E_b / h_b[pc_b].
@@ -1129,7 +1160,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         Tlo[o] = (uint8_t)(v & 0xff);
         Thi[o] = (uint8_t)(v >> 8);
     }
-    if (tid < (int)nb) {
+    if (!published && tid < (int)nb) {
         const uint32_t rr = crow[bphys[tid]];
         const uint32_t r = src.rid ? src.rid[rr] : rr;
         cur->sel[tid] = r;
@@ -1140,12 +1171,19 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     P2_LAP(6);
     if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; trace[17] += dense ? 1 : 0; }
 #undef P2_LAP
-    if (tid == 0) {
+    if (!published && tid == 0) {
         cur->c0 = c0;
         cur->c1 = c0 + width;
         cur->kp = nb;
         cur->nrows = 0;
         cur->ncand = ncand_tot;
+    }
+    if (epoch && !published) {
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&cur->ready), "r"(epoch) : "memory");
+        }
     }
 }
 
@@ -1158,10 +1196,21 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
                           const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
                           uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr,
-                          int ref = 0)
+                          int ref = 0, uint32_t epoch = 0)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
+    if (epoch) {                                  // the panel publishes S and its pivots before its T solve
+        if (threadIdx.x == 0) {
+            for (uint32_t it = 0;; it++) {
+                uint32_t v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&ps->ready) : "memory");
+                if (v == epoch || it > (1u << 24)) break;          // bounded: never hang the GPU
+                __nanosleep(128);
+            }
+        }
+        __syncthreads();
+    }
     constexpr int CPL = PK / 32;
     const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
@@ -1330,6 +1379,7 @@ __global__ void k_p2_init(P2State *ps)
     ps[1].c0 = ps[1].c1 = 0;
     ps[0].kp = ps[1].kp = 0;
     ps[0].nrows = ps[1].nrows = 0;
+    ps[0].ready = ps[1].ready = 0;
 }
 
 // ---- distributed echelon (row-sharded D) ----------------------------
@@ -1592,7 +1642,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         kt_mark_on(h, KT_PANEL, s);
         PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32, panel_lumode()};
-        k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace);
+        k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace,
+                                        (uint32_t)(k + 1));
         kt_mark_on(h, KT_PANEL, s);
         note_launch();
     };
@@ -1602,7 +1653,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
                                                          rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0,
-                                                         h->ref_only ? 1 : 0);
+                                                         h->ref_only ? 1 : 0, (uint32_t)(k + 1));
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
@@ -1640,6 +1691,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // k_lead2 launch).  Measured slower on c1 (14.2 vs 14.0 ms: 1,470 warps scanning ~5 rows each
     // after the barrier vs a separate 4,700-warp launch), so off by default
     const bool winlead = winfused && getenv("GBLA_WIN_LEAD") && atoi(getenv("GBLA_WIN_LEAD")) == 1;
+    // GBLA_EARLY_GATHER=0: the next panel's F gather waits for the whole panel (default: for its flag)
+    const bool early_gather = !(getenv("GBLA_EARLY_GATHER") && atoi(getenv("GBLA_EARLY_GATHER")) == 0);
     uint32_t *wflags = nullptr;
     if (winfused) {
         GBLA_TRY(dalloc_t(h, 64, &wflags));
@@ -1818,8 +1871,15 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                     if ((status = sp_flush(cur, 2, st)) != GBLA_OK || (status = sp_begin(cur, st)) != GBLA_OK) break;
                 }
                 tmark(k, st);
-                if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
-                p_gather(st, k + 1);
+                if (early_gather) {
+                    // the F gather waits on the panel's `ready` flag (S and pivots, published before
+                    // its T solve) instead of its completion, so it overlaps the T solve
+                    p_gather(st, k + 1);
+                    if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
+                } else {
+                    if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
+                    p_gather(st, k + 1);
+                }
                 tmark(k, st);
             }
             if (cudaGetLastError() != cudaSuccess) { fail("launch"); break; }
@@ -2029,7 +2089,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
         // the same panel factorization on every rank
         PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap, 0, panel_lumode()};
         kt_mark(h, KT_PANEL);
-        k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr);
+        k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr, 0u);
         kt_mark(h, KT_PANEL);
         note_launch();
         // C4: the S rows from their owners
