@@ -232,6 +232,15 @@ def test_window_step_with_lead_scan(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     check_full(gb, ctx, M, oracle.reduce(M))
 
 
+def test_gather_after_the_whole_panel(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """GBLA_EARLY_GATHER=0: the next step's F gather waits for the whole panel (the default waits on
+    the panel's flag, set before its T solve)."""
+    monkeypatch.setenv("GBLA_EARLY_GATHER", "0")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.05))
+    check_full(gb, ctx, M, oracle.reduce(M))
+
+
 def test_window_step_in_two_launches(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     """GBLA_WIN_FUSED=0: the Rn window and the window update as two launches (the default fuses
     them into one persistent kernel with column-tile flags); both must give the oracle's R."""
