@@ -1693,6 +1693,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     const bool winlead = winfused && getenv("GBLA_WIN_LEAD") && atoi(getenv("GBLA_WIN_LEAD")) == 1;
     // GBLA_EARLY_GATHER=0: the next panel's F gather waits for the whole panel (default: for its flag)
     const bool early_gather = !(getenv("GBLA_EARLY_GATHER") && atoi(getenv("GBLA_EARLY_GATHER")) == 0);
+    bool btiles_ready = false;               // the B tiles of the next window were gathered early
     uint32_t *wflags = nullptr;
     if (winfused) {
         GBLA_TRY(dalloc_t(h, 64, &wflags));
@@ -1748,11 +1749,15 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
             }
-            // look-ahead: only the B tiles of the next window are on the chain (the rest: below)
-            launch_pdl(k_gather_st2, dim3(lookahead ? grid_for(PW + 64, 128) : grid_for(nN, 128), PK / 16), dim3(128),
-                       0, st, nN, (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
-                       lookahead ? dops : (unsigned long long *)nullptr, lookahead ? 1 : 0);
-            note_launch();
+            // look-ahead: only the B tiles of the next window are on the chain (the rest: below); with
+            // the early gather they were gathered already, right after the F gather of this panel
+            if (!btiles_ready) {
+                launch_pdl(k_gather_st2, dim3(lookahead ? grid_for(PW + 64, 128) : grid_for(nN, 128), PK / 16),
+                           dim3(128), 0, st, nN, (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
+                           lookahead ? dops : (unsigned long long *)nullptr, lookahead ? 1 : 0);
+                note_launch();
+            }
+            btiles_ready = false;
             if (lookahead) tmark(k, st);
             if (winfused) {
                 // Rn window + window update in one launch (k_modgemm_win): timed as the trailing family
@@ -1873,8 +1878,16 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 tmark(k, st);
                 if (early_gather) {
                     // the F gather waits on the panel's `ready` flag (S and pivots, published before
-                    // its T solve) instead of its completion, so it overlaps the T solve
+                    // its T solve) instead of its completion, so it overlaps the T solve; so does the
+                    // gather of the next window's B tiles (D[S] there is final once the rest is done)
                     p_gather(st, k + 1);
+                    if (G == 1) {
+                        P2State *nxt = ps + ((k + 1) & 1);
+                        launch_pdl(k_gather_st2, dim3(grid_for(PW + 64, 128), PK / 16), dim3(128), 0, st, nN,
+                                   (const uint16_t *)h->D, ldD, (const P2State *)nxt, Blo, Bhi, dops, 1);
+                        note_launch();
+                        btiles_ready = true;
+                    }
                     if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
                 } else {
                     if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
