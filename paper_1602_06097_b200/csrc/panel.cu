@@ -269,8 +269,8 @@ __device__ __forceinline__ void frag_b_rot(const uint16_t *X, int ld, int n0, in
 // above pivots here; the chunk's back substitution follows).  Returns the pivot steps taken.
 // Scratch (dense mode: the value columns >= 128 are unused): V at 128, L at 160, the snapshot
 // Y_p^t at 192 (virtual column n -> row n & 127, offset 32 (n >> 7)) of every store row.
-__device__ int blocked_lu(uint16_t *X, int ncand, const uint32_t *freel, uint32_t *cstat, uint32_t *clead,
-                          uint32_t *skey, uint32_t p, uint32_t m32, const Field &F, int ldv)
+__device__ int blocked_lu(uint16_t *X, uint32_t *cstat, uint32_t *clead, uint32_t p, uint32_t m32, const Field &F,
+                          int ldv)
 {
     __shared__ uint32_t sig[PK];
     __shared__ uint32_t prow[32];
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 int slot = 0, nsteps = 0;
                 const bool blocked = dense && src.lumode == 3 && ldv <= 128;
                 if (blocked) {
-                    nsteps = blocked_lu(X, ncand, freel, cstat, clead, skey, p, m32, F, ldv);
+                    nsteps = blocked_lu(X, cstat, clead, p, m32, F, ldv);
                 } else for (;;) {
                     nsteps++;
                     uint32_t best = NONE16;
