@@ -130,9 +130,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gops, 4), "unit": "Gop/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64 accumulate, u16 residues", "data": "synthetic",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "p": cfg.p},
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "npiv": cfg.npiv, "p": cfg.p,
+                   "density": cfg.density, "band": cfg.band, "rank_planted": cfg.rank_planted,
+                   "flags": args.flags, "parallelism": f"CPU oracle on {threads} host threads (rank 0 only)"},
         "cpu_baseline": {"value": round(gops, 4), "unit": "Gop/s", "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(gops, 4), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
