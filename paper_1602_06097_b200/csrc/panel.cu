@@ -1630,8 +1630,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // panel k: leads of the window (all SMs), the factorization (one SM), F of the other rows (all SMs).
     // With look-ahead the middle step runs on the side stream, the two wide ones on the main stream
     // where they do not compete with the rest of the previous update.
-    const unsigned rgrid = grid_for(mN * 32, 256) < 4u * h->ctx->sm_count ? grid_for(mN * 32, 256)
-                                                                            : 4u * h->ctx->sm_count;
+    // lead scan: one warp per row in a single pass up to 8 blocks per SM (GBLA_LEAD_BPS overrides)
+    const unsigned lbps = getenv("GBLA_LEAD_BPS") ? (unsigned)atoi(getenv("GBLA_LEAD_BPS")) : 8u;
+    const unsigned rgrid = grid_for(mN * 32, 256) < lbps * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                            : lbps * h->ctx->sm_count;
     auto p_lead = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1);
         launch_pdl(k_lead2, dim3(rgrid), dim3(256), 0, s, mN, nN, (const uint16_t *)h->D, ldD,
