@@ -930,11 +930,12 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // warp.  W_II by doubling inside the four diagonal blocks.  T and the residual are
             // kept transposed (slot-major, so the B fragments are 8-byte loads); the value rows
             // are dead now and hold them.
+            // (rows >= nb of U, and rows / columns >= nb of E', only reach outputs that are dropped)
             uint16_t(*U)[FSLD] = FS;
-            for (int idx = tid; idx < PK * PK; idx += NT) {
+            for (int idx = tid; idx < (int)nb * PK; idx += NT) {
                 const int b = idx >> 7, b2 = idx & (PK - 1);
                 uint32_t v = (b == b2) ? 1u : 0u;
-                if (b < (int)nb && b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
+                if (b2 > b && b2 < (int)nb) v = mod32(X[bphys[b] * LDX + bpc[b2]] * hinv[bphys[b]], p, m32);
                 U[b][b2] = (uint16_t)v;
             }
             __syncthreads();
@@ -951,10 +952,10 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 const int i = idx >> 5, j = idx & 31;
                 WD(i, j) = (uint16_t)((i & 31) == j ? 1 : 0);
             }
-            for (int idx = tid; idx < PK * PK; idx += NT) {    // E'[b][c] = E[phys b][phys c] / h_b[pc_b]
+            for (int idx = tid; idx < (int)nb * PK; idx += NT) {   // E'[b][c] = E[phys b][phys c] / h_b[pc_b]
                 const int b = idx >> 7, c = idx & (PK - 1);
                 uint32_t v = 0;
-                if (b < (int)nb && c < (int)nb) {
+                if (c < (int)nb) {
                     const uint32_t qb = bphys[b];
                     v = mod32(X[qb * LDX + PW + bphys[c]] * hinv[qb], p, m32);
                 }
