@@ -159,11 +159,19 @@ gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t fl
  *   C[r_i, x] <- (C[r_i, x] - sum_{k<K} A[i, k] * B[k, x]) mod p,
  *   i < rows, x < cols, r_i = rowidx ? rowidx[i] : i.
  * A: rows x K (row stride lda), B: K x cols (stride ldb), C: stride ldc; all
- * device u16 residues < p; K <= 128.  engine 0 = tcgen05 (u8 limbs, exact:
- * 128 * 255^2 * 2 < 2^31 per s32 accumulator), 1 = INT pipe.  Synchronizes. */
+ * device u16 residues < p; K <= 512.  engine 0 = tcgen05 (u8 limbs; K <= 128:
+ * one K-block, else the multi-K kernel of the echelon's deferred updates;
+ * exact: every s32 limb sum <= 512 * 255^2 * 2 < 2^31), 1 = INT pipe.
+ * Synchronizes. */
 gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K,
                          const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
                          const uint32_t *rowidx, uint16_t *C, int64_t ldc, int engine, void *stream);
+/* K11 microbenchmark (roofline of the trailing update): device-generated
+ * pseudo-random operand tiles and C (rows x cols, K <= 512), one untimed launch, then
+ * `reps` launches timed by CUDA events on `stream`; *ms_per_launch = mean device time.
+ * Work per launch: rows * cols * ceil(K/128)*128 modMACs (4 u8 MACs each). */
+gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K, int reps,
+                               void *stream, float *ms_per_launch);
 
 /* ---- results (views valid until gbla_mat_free) ------------------------- */
 gbla_status gbla_get_dims(gbla_mat h, int64_t *npiv, int64_t *mN, int64_t *nN);

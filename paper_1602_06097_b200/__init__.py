@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH):
         "gbla_get_kernel_ms": ([vp, ctypes.c_int, P(ctypes.c_float), P(i64)], st),
         "gbla_get_multilines": ([vp, vp, P(i64), P(vp), P(vp), P(vp)], st),
         "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
+        "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -113,7 +114,7 @@ def exported_symbols():
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
-            "gbla_get_multilines", "gbla_get_kernel_work"]
+            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench"]
 
 
 def _check(status: int):
@@ -419,7 +420,7 @@ def gbla_reduce(ctx: Context, m, n, row_ptr, col, val, p, flags: int = 0, stream
 
 def gbla_modgemm(ctx: Context, p: int, A, B, C, rowidx=None, engine: int = 0, stream=None):
     """K11: C[rowidx[i]] -= A[i] @ B  (mod p), in place.  A: rows x K, B: K x cols,
-    C: torch uint16 CUDA tensors (2-D, unit column stride); K <= 128."""
+    C: torch uint16 CUDA tensors (2-D, unit column stride); K <= 512."""
     rows, K = A.shape
     K2, cols = B.shape
     assert K == K2 and C.shape[1] >= cols
@@ -427,6 +428,14 @@ def gbla_modgemm(ctx: Context, p: int, A, B, C, rowidx=None, engine: int = 0, st
     _check(_lib.gbla_modgemm(ctx._h, p, rows, cols, K, ctypes.c_void_p(A.data_ptr()), A.stride(0),
                              ctypes.c_void_p(B.data_ptr()), B.stride(0), ri, ctypes.c_void_p(C.data_ptr()),
                              C.stride(0), engine, _stream_ptr(stream)))
+
+
+def modgemm_bench(ctx: Context, p: int, rows: int, cols: int, K: int, reps: int = 10, stream=None) -> float:
+    """K11 microbenchmark (gbla_modgemm_bench): mean device ms per launch of
+    C -= A B mod p on device-generated operands (rows x cols, K <= 512)."""
+    ms = ctypes.c_float()
+    _check(_lib.gbla_modgemm_bench(ctx._h, p, rows, cols, K, reps, _stream_ptr(stream), ctypes.byref(ms)))
+    return ms.value
 
 
 def tile_shard(ntiles: int, rank: int, world: int):

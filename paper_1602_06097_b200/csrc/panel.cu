@@ -1197,7 +1197,7 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
                           const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
                           uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr,
-                          int ref = 0, uint32_t epoch = 0)
+                          int ref = 0, uint32_t epoch = 0, const uint32_t *__restrict__ spos = nullptr)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -1247,7 +1247,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     *reinterpret_cast<uint32_t *>(Flo + o) = lo;
     *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
     if (Fdlo) {
-        const size_t od = (size_t)((i / 128) * G + j) * (PK * 128) + tc::toff((uint32_t)(i % 128), lane * CPL);
+        const uint32_t q = spos ? spos[i] : (uint32_t)i;       // slot of row i in the flush's row order
+        const size_t od = (size_t)((q / 128) * G + j) * (PK * 128) + tc::toff(q % 128, lane * CPL);
         *reinterpret_cast<uint32_t *>(Fdlo + od) = lo;
         *reinterpret_cast<uint32_t *>(Fdhi + od) = hi;
     }
@@ -1260,11 +1261,12 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
 // deferred columns, S_b becomes a pivot row and the flush must not subtract them again.
 // Block (b, i), 32 threads x 4 K entries.
 __global__ void k_fix_gather(const P2State *__restrict__ ps, int G, uint8_t *__restrict__ Fdlo,
-                             uint8_t *__restrict__ Fdhi, uint8_t *__restrict__ Aflo, uint8_t *__restrict__ Afhi)
+                             uint8_t *__restrict__ Fdhi, uint8_t *__restrict__ Aflo, uint8_t *__restrict__ Afhi,
+                             const uint32_t *__restrict__ spos)
 {
     const uint32_t b = blockIdx.x, i = blockIdx.y;
     if (b >= ps->kp) return;
-    const uint32_t r = ps->sel[b];
+    const uint32_t r = spos[ps->sel[b]];
     const uint32_t k = threadIdx.x * 4;
     const size_t os = (size_t)((r / 128) * G + i) * (PK * 128) + tc::toff(r % 128, k);
     const size_t od = (size_t)i * (PK * 128) + tc::toff(b, k);
@@ -1280,6 +1282,61 @@ __global__ void k_sp_begin(const P2State *__restrict__ ps, int64_t nN, int G, in
 {
     const int64_t c = (ps ? ps->c1 : 0) + (int64_t)G * PW;
     *Cd = c < nN ? c : nN;
+}
+
+// Row order of the deferred flushes: D rows sorted by their leading column at the start of the
+// echelon (ilead).  A row whose leading column is >= c1 has zero coefficients at every pivot of
+// the panels up to column c1, so no update before then changes it: the flush of a super-panel
+// ending at column c1 only touches the slots [0, #{ilead < c1}) of this order (a staircase D_new
+// with uniform leads: a third of mN x width on average instead of all of it).
+// ilead[r] = first nonzero column of D row r (nN if none); one warp per row, 16 bytes per lane.
+__global__ void k_row_first_nz(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
+                               uint32_t *__restrict__ ilead, uint32_t *__restrict__ iota)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint16_t *row = D + (size_t)r * ldD;
+        uint32_t res = (uint32_t)nN;
+        for (int64_t base = 0; base < nN && res == (uint32_t)nN; base += 256) {
+            const int64_t k0 = base + lane * 8;
+            uint32_t first = 0xffffffffu;
+            if (k0 + 8 <= nN && (ldD % 8) == 0) {
+                const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(row + k0));
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                uint32_t m = 0;
+#pragma unroll
+                for (int j = 0; j < 4; j++) m |= ((w[j] & 0xffffu) ? 1u : 0u) << (2 * j) | ((w[j] >> 16) ? 2u : 0u) << (2 * j);
+                if (m) first = (uint32_t)k0 + __ffs(m) - 1;
+            } else {
+                for (int u = 0; u < 8; u++)
+                    if (k0 + u < nN && row[k0 + u] != 0) { first = (uint32_t)(k0 + u); break; }
+            }
+            const unsigned m = __ballot_sync(FULL, first != 0xffffffffu);
+            if (m) res = __shfl_sync(FULL, first, __ffs(m) - 1);
+        }
+        if (lane == 0) { ilead[r] = res; iota[r] = (uint32_t)r; }
+    }
+}
+__global__ void k_inv_perm(int64_t n, const uint32_t *__restrict__ srow, uint32_t *__restrict__ spos)
+{
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) spos[srow[s]] = (uint32_t)s;
+}
+// *cnt = #{s : skey[s] < c1} (skey sorted ascending): the rows a flush ending at column c1 touches
+__global__ void k_prefix_count(int64_t n, const uint32_t *__restrict__ skey, const int64_t *__restrict__ c1,
+                               uint32_t *__restrict__ cnt)
+{
+    tc::pdl_trigger();
+    tc::pdl_wait();
+    const int64_t c = *c1;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)skey[mid] < c) lo = mid + 1;
+        else hi = mid;
+    }
+    *cnt = (uint32_t)lo;
 }
 
 // transposed limb planes of D[S, c0:]: B operand tiles (64 columns x K = 128) of the Rn GEMM
@@ -1597,6 +1654,27 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
     GBLA_TRY(dalloc_t(h, rd_stride * G, &Rtlo));
     GBLA_TRY(dalloc_t(h, rd_stride * G, &Rthi));
+    uint32_t *srow = nullptr, *spos = nullptr, *skey = nullptr, *nflush = nullptr;
+    if (G > 1) {
+        uint32_t *ilead, *iota;
+        GBLA_TRY(dalloc_t(h, mN, &ilead));
+        GBLA_TRY(dalloc_t(h, mN, &iota));
+        GBLA_TRY(dalloc_t(h, mN, &skey));
+        GBLA_TRY(dalloc_t(h, mN, &srow));
+        GBLA_TRY(dalloc_t(h, mN, &spos));
+        GBLA_TRY(dalloc_t(h, 1, &nflush));
+        k_row_first_nz<<<grid_for(mN * 32, 256) < 16u * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                         : 16u * h->ctx->sm_count, 256, 0, st>>>(
+            mN, nN, h->D, ldD, ilead, iota);
+        note_launch();
+        size_t tb = 0;
+        GBLA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, ilead, skey, iota, srow, (int)mN, 0, 32, st));
+        void *tmp;
+        GBLA_TRY(dalloc(h, tb + 16, &tmp));
+        GBLA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, ilead, skey, iota, srow, (int)mN, 0, 32, st));
+        k_inv_perm<<<grid_for(mN, 256), 256, 0, st>>>(mN, srow, spos);
+        note_launch(3);
+    }
     if (G > 1) {
         GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdlo));
         GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdhi));
@@ -1656,7 +1734,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
                                                          rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0,
-                                                         h->ref_only ? 1 : 0, (uint32_t)(k + 1));
+                                                         h->ref_only ? 1 : 0, (uint32_t)(k + 1), spos);
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
@@ -1670,8 +1748,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     };
     auto sp_flush = [&](const P2State *cur, int ctsel, cudaStream_t s) {
         kt_mark_on(h, KT_TRAIL, s);
-        const gbla_status r = modgemm_tc_sub_mk(s, mN, nullptr, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
-                                                (int64_t)rd_stride, spc0, nullptr, h->D, ldD, spCd, &cur->c1, PW,
+        launch_pdl(k_prefix_count, dim3(1), dim3(1), 0, s, mN, (const uint32_t *)skey, &cur->c1, nflush);
+        note_launch();
+        const gbla_status r = modgemm_tc_sub_mk(s, mN, nflush, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
+                                                (int64_t)rd_stride, spc0, srow, h->D, ldD, spCd, &cur->c1, PW,
                                                 ctsel, gemm_grid);
         kt_mark_on(h, KT_TRAIL, s);
         return r;
@@ -1743,7 +1823,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             uint8_t *Rtl = Rtlo + j * rd_stride, *Rth = Rthi + j * rd_stride;
             tmark(k, st);
             if (j > 0) {                                 // S up to date in the deferred columns
-                k_fix_gather<<<dim3(PK, j), 32, 0, st>>>(cur, G, Fdlo, Fdhi, Aflo, Afhi);
+                k_fix_gather<<<dim3(PK, j), 32, 0, st>>>(cur, G, Fdlo, Fdhi, Aflo, Afhi, spos);
                 note_launch();
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub_mk(st, PK, &cur->kp, nN, h->F, Aflo, Afhi, G, j, Rtlo, Rthi,

@@ -78,6 +78,7 @@ struct MMArgs {
     int64_t b_kb_stride;
     const int64_t *kb_c0;
     const int64_t *cend_dev;          // optional end column (min(cols, *cend_dev))
+    int exp;                          // microbenchmark experiments (0 = normal)
 };
 
 constexpr int NSB = 4;                               // B stages
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             fast_n = crow_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
             for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
-            if (MODE == MODE_SUB && live_n) {
+            if (MODE == MODE_SUB && live_n && g.exp != 1) {
                 if (fast_n) {
 #pragma unroll
                     for (int u = 0; u < EPI_COLS / 8; u++) {
@@ -364,6 +365,13 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             tc::mbar_wait(&tfull[ab], tph[ab]);
             tph[ab] ^= 1;
             tc::fence_after();
+            if (g.exp == 2) {                      // experiment: MMA + operand staging only
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[ab]);
+                ab ^= 1;
+                continue;
+            }
             const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 3 * BN + part * EPI_COLS;
 #pragma unroll
             for (int c = 0; c < EPI_COLS; c += 16) {
@@ -396,7 +404,12 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[ab]);          // accumulator may be overwritten
             ab ^= 1;
-            if (fast) {
+            if (g.exp == 1) {                      // experiment: no D traffic (keep the result live)
+                uint32_t acc = 0;
+#pragma unroll
+                for (int w = 0; w < EPI_COLS / 2; w++) acc ^= dv[w];
+                if (acc == 0x9e3779b9u && crow) crow[0] = 1;
+            } else if (fast) {
 #pragma unroll
                 for (int u = 0; u < EPI_COLS / 8; u++)
                     reinterpret_cast<uint4 *>(crow)[u] = make_uint4(dv[4 * u], dv[4 * u + 1], dv[4 * u + 2], dv[4 * u + 3]);
@@ -733,30 +746,51 @@ __global__ void k_modgemm_int(int64_t rows, int64_t cols, int64_t K, Field F, co
     *c = (uint16_t)(d >= s ? d - s : d + F.p - s);
 }
 
-// rows x K (lda) u16 -> A tiles (limb planes), zero padded
-__global__ void k_split_rows(int64_t rows, int64_t rows_pad, int64_t K, const uint16_t *__restrict__ A, int64_t lda,
-                             uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
+// rows x K (lda) u16 -> A tiles (limb planes), zero padded; K-block i of row tile rt is tile
+// rt * nkb + i (nkb = 1: one 128 x 128 tile per row tile)
+__global__ void k_split_rows(int64_t rows, int64_t rows_pad, int64_t K, int nkb, const uint16_t *__restrict__ A,
+                             int64_t lda, uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows_pad * KP) return;
-    const int64_t i = idx / KP, k = idx % KP;
+    if (idx >= rows_pad * KP * nkb) return;
+    const int64_t i = idx / (KP * nkb), k = idx % (KP * nkb);
     const uint16_t v = (i < rows && k < K) ? A[i * lda + k] : 0;
-    const size_t o = (size_t)(i / BM) * A_PLANE + tc::toff((uint32_t)(i % BM), (uint32_t)k);
+    const size_t o = (size_t)((i / BM) * nkb + k / KP) * A_PLANE + tc::toff((uint32_t)(i % BM), (uint32_t)(k % KP));
     lo[o] = (uint8_t)(v & 0xff);
     hi[o] = (uint8_t)(v >> 8);
 }
 
-// K x cols (ldb) u16 -> B tiles (limb planes, K-major), zero padded
-__global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, const uint16_t *__restrict__ B, int64_t ldb,
-                             uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
+// K x cols (ldb) u16 -> B tiles (limb planes, K-major), zero padded; K-block i starts at
+// i * cols_pad * KP (the multi-K GEMM's b_kb_stride)
+__global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, int nkb, const uint16_t *__restrict__ B,
+                             int64_t ldb, uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= cols_pad * KP) return;
+    if (idx >= cols_pad * KP * nkb) return;
     const int64_t x = idx % cols_pad, k = idx / cols_pad;
     const uint16_t v = (x < cols && k < K) ? B[k * ldb + x] : 0;
-    const size_t o = (size_t)(x / BN) * B_PLANE + toff64((uint32_t)(x % BN), (uint32_t)k);
+    const size_t o = (size_t)(k / KP) * cols_pad * KP + (size_t)(x / BN) * B_PLANE +
+                     toff64((uint32_t)(x % BN), (uint32_t)(k % KP));
     lo[o] = (uint8_t)(v & 0xff);
     hi[o] = (uint8_t)(v >> 8);
+}
+
+// deterministic pseudo-random bytes / residues for the K11 microbenchmark
+__global__ void k_fill_hash(uint8_t *__restrict__ p, size_t n, uint32_t seed)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+        x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+        p[i] = (uint8_t)x;
+    }
+}
+__global__ void k_fill_res(uint16_t *__restrict__ p, size_t n, uint32_t prime, uint32_t seed)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+        x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+        p[i] = (uint16_t)(x % prime);
+    }
 }
 
 template <int MODE, int EPIW, bool PF2, bool MK = false>
@@ -815,6 +849,7 @@ static gbla_status launch_ws(const MMArgs &a, int64_t grid, cudaStream_t st)
 }
 
 int g_sms = 148;
+int g_k11_exp = 0;       // gbla_modgemm_bench experiments (GBLA_K11_EXP; 0 everywhere else)
 
 }  // namespace
 
@@ -831,7 +866,7 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
     int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
-             c0_dev, nullptr, win_dev, win_w, ctsel, 1, 1, 0, nullptr, cend_dev};
+             c0_dev, nullptr, win_dev, win_w, ctsel, 1, 1, 0, nullptr, cend_dev, g_k11_exp};
     GBLA_TRY(launch_ws<MODE_SUB>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
@@ -869,7 +904,7 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
     int64_t grid = grid_cap > 0 ? grid_cap : g_sms;
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
-             c0_dev, nullptr, win_dev, win_w, ctsel, nkb, a_rt_stride, b_kb_stride, kb_c0, nullptr};
+             c0_dev, nullptr, win_dev, win_w, ctsel, nkb, a_rt_stride, b_kb_stride, kb_c0, nullptr, g_k11_exp};
     GBLA_TRY((launch_ws1<MODE_SUB, 8, true, true>(a, grid, st)));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
@@ -909,13 +944,26 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
 void modgemm_set_sms(int sms) { g_sms = sms > 0 ? sms : 148; }
 
 // ---- C ABI: K11 as a standalone op -------------------------------------
+// K <= 128: one K-block (k_modgemm_ws); 128 < K <= 512: the multi-K kernel of the deferred
+// super-panel updates (exact: every limb sum <= 512 * 255^2 * 2 < 2^31).
+static gbla_status modgemm_tiles(cudaStream_t st, const Field &F, int64_t rows, int64_t cols, int nkb,
+                                 const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
+                                 int64_t cp, const uint32_t *rowidx, uint16_t *C, int64_t ldc)
+{
+    if (nkb == 1)
+        return modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
+                              CT_ALL, 0, nullptr);
+    return modgemm_tc_sub_mk(st, rows, nullptr, cols, F, Alo, Ahi, nkb, nkb, Blo, Bhi, cp * KP, nullptr, rowidx, C,
+                             ldc, nullptr, nullptr, 0, CT_ALL, 0);
+}
+
 extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K,
                                     const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
                                     const uint32_t *rowidx, uint16_t *C, int64_t ldc, int engine, void *stream)
 {
     if (!ctx || !A || !B || !C) { set_error("gbla_modgemm: NULL argument"); return GBLA_E_INVAL; }
-    if (rows < 0 || cols < 0 || K < 0 || K > KP || lda < K || ldb < cols || ldc < cols) {
-        set_error("gbla_modgemm: bad sizes (K must be <= %d)", KP);
+    if (rows < 0 || cols < 0 || K < 0 || K > MK_MAX * KP || lda < K || ldb < cols || ldc < cols) {
+        set_error("gbla_modgemm: bad sizes (K must be <= %d)", MK_MAX * KP);
         return GBLA_E_INVAL;
     }
     if (p <= 2 || p >= 65536) { set_error("gbla_modgemm: p out of range"); return GBLA_E_DOMAIN; }
@@ -931,18 +979,68 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
         GBLA_CUDA_TRY(cudaGetLastError());
         return GBLA_OK;
     }
+    const int nkb = K <= KP ? 1 : (int)((K + KP - 1) / KP);
     const int64_t rp = (rows + BM - 1) / BM * BM, cp = (cols + BN - 1) / BN * BN;
-    const size_t bytes = (size_t)(rp + cp) * KP * 2 + 256;
+    const size_t bytes = (size_t)(rp + cp) * KP * nkb * 2 + 256;
     uint8_t *ws = (uint8_t *)ctx_alloc(ctx, bytes, st);
     if (!ws) { set_error("gbla_modgemm: workspace allocation failed"); return GBLA_E_NOMEM; }
-    uint8_t *Alo = ws, *Ahi = Alo + rp * KP, *Blo = Ahi + rp * KP, *Bhi = Blo + cp * KP;
-    k_split_rows<<<grid_for(rp * KP, 256), 256, 0, st>>>(rows, rp, K, A, lda, Alo, Ahi);
-    k_split_cols<<<grid_for(cp * KP, 256), 256, 0, st>>>(cols, cp, K, B, ldb, Blo, Bhi);
+    uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
+    k_split_rows<<<grid_for(rp * KP * nkb, 256), 256, 0, st>>>(rows, rp, K, nkb, A, lda, Alo, Ahi);
+    k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, K, nkb, B, ldb, Blo, Bhi);
     note_launch(2);
-    gbla_status s = modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
-                                   CT_ALL, 0, nullptr);
+    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, rowidx, C, ldc);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    return s;
+}
+
+// K11 microbenchmark: random operand tiles and C (rows x cols, K = 128 * nkb) on the device,
+// one untimed launch, then `reps` launches timed with CUDA events on `stream`.
+extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K, int reps,
+                                          void *stream, float *ms_per_launch)
+{
+    if (!ctx || !ms_per_launch || rows <= 0 || cols <= 0 || K <= 0 || K > MK_MAX * KP || reps <= 0) {
+        set_error("gbla_modgemm_bench: bad arguments");
+        return GBLA_E_INVAL;
+    }
+    if (p <= 2 || p >= 65536) { set_error("gbla_modgemm_bench: p out of range"); return GBLA_E_DOMAIN; }
+    cudaStream_t st = (cudaStream_t)stream;
+    GBLA_CUDA_TRY(cudaSetDevice(ctx->device));
+    modgemm_set_sms(ctx->sm_count);
+    const Field F = make_field(p);
+    const int nkb = (int)((K + KP - 1) / KP);
+    const int64_t rp = (rows + BM - 1) / BM * BM, cp = (cols + BN - 1) / BN * BN, ldc = cp;
+    const size_t opb = (size_t)(rp + cp) * KP * nkb * 2, cb = (size_t)rows * ldc * 2;
+    uint8_t *ws = (uint8_t *)ctx_alloc(ctx, opb + cb + 256, st);
+    if (!ws) { set_error("gbla_modgemm_bench: allocation failed"); return GBLA_E_NOMEM; }
+    uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
+    uint16_t *C = reinterpret_cast<uint16_t *>(ws + (opb + 255) / 256 * 256);
+    k_fill_hash<<<4 * ctx->sm_count, 256, 0, st>>>(ws, opb, 12345u);
+    k_fill_res<<<4 * ctx->sm_count, 256, 0, st>>>(C, (size_t)rows * ldc, p, 777u);
+    note_launch(2);
+    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (s == GBLA_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)) {
+        set_error("gbla_modgemm_bench: event creation failed");
+        s = GBLA_E_CUDA;
+    }
+    if (s == GBLA_OK) {
+        g_k11_exp = getenv("GBLA_K11_EXP") ? atoi(getenv("GBLA_K11_EXP")) : 0;
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < reps && s == GBLA_OK; r++)
+            s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc);
+        cudaEventRecord(e1, st);
+        g_k11_exp = 0;
+        if (cudaEventSynchronize(e1) != cudaSuccess) { set_error("gbla_modgemm_bench: kernel failed"); s = GBLA_E_CUDA; }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *ms_per_launch = ms / reps;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaStreamSynchronize(st);
+    ctx_free(ctx, ws, st);
+    cudaGetLastError();
     return s;
 }

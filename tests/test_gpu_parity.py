@@ -354,7 +354,8 @@ def test_modgemm_tc_and_int_against_numpy(gb, ctx):
     import torch
     from pins import matmul_mod
     rng = np.random.default_rng(8)
-    shapes = [(1, 1, 1), (5, 7, 3), (128, 64, 128), (129, 65, 127), (300, 200, 128), (1000, 333, 77), (77, 1030, 128)]
+    shapes = [(1, 1, 1), (5, 7, 3), (128, 64, 128), (129, 65, 127), (300, 200, 128), (1000, 333, 77), (77, 1030, 128),
+              (130, 70, 129), (257, 300, 384), (200, 129, 512), (1, 64, 500)]
     for p in (3, 251, 32003, 65521):
         for rows, cols, K in shapes:
             A = rng.integers(0, p, (rows, K)); B = rng.integers(0, p, (K, cols))
@@ -368,13 +369,14 @@ def test_modgemm_tc_and_int_against_numpy(gb, ctx):
                 tC = torch.from_numpy(C0.astype(np.uint16)).cuda()
                 gb.gbla_modgemm(ctx, p, tA, tB, tC, rowidx=torch.from_numpy(perm).cuda(), engine=engine)
                 assert np.array_equal(tC.cpu().numpy().astype(np.int64), exp), (p, rows, cols, K, engine)
-    # worst case for the s32 limb accumulators: all entries p - 1, K = 128
+    # worst case for the s32 limb accumulators: all entries p - 1, K = 128 and K = 512 (multi-K)
     p = 65521
-    A = np.full((128, 128), p - 1); B = np.full((128, 64), p - 1); C0 = np.zeros((128, 64), np.int64)
-    tC = torch.from_numpy(C0.astype(np.uint16)).cuda()
-    gb.gbla_modgemm(ctx, p, torch.from_numpy(A.astype(np.uint16)).cuda(),
-                    torch.from_numpy(B.astype(np.uint16)).cuda(), tC)
-    assert np.array_equal(tC.cpu().numpy().astype(np.int64), (C0 - matmul_mod(A, B, p)) % p)
+    for K in (128, 512):
+        A = np.full((128, K), p - 1); B = np.full((K, 64), p - 1); C0 = np.zeros((128, 64), np.int64)
+        tC = torch.from_numpy(C0.astype(np.uint16)).cuda()
+        gb.gbla_modgemm(ctx, p, torch.from_numpy(A.astype(np.uint16)).cuda(),
+                        torch.from_numpy(B.astype(np.uint16)).cuda(), tC)
+        assert np.array_equal(tC.cpu().numpy().astype(np.int64), (C0 - matmul_mod(A, B, p)) % p), K
 
 
 def test_echelon_engines_agree_c0_and_dense(gb, ctx, c0_matrix, c0_oracle):
@@ -453,6 +455,23 @@ def test_echelon_ref_mode(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     check_ref(gb, h, res, M.p)
     h.free()
     monkeypatch.delenv("GBLA_DIST_EMULATE")
+
+
+def test_super_panels_rref_exact(gb, ctx, monkeypatch):
+    """The default echelon schedule of c2-c4 (GBLA_SP = 4 panels per super-panel: per-panel updates
+    left of the deferred columns, one K = 512 multi-K flush per super-panel over the rows whose
+    leading column is left of the super-panel's end, per-panel fix-ups of the selected rows, the
+    back elimination into earlier pivot rows), in full RREF mode and with look-ahead, bit-exact
+    against the oracle's R at scaled c2, c3 and c4 with several super-panels; also
+    2 panels per super-panel and a partial last super-panel."""
+    for name, sc in (("c2", 0.05), ("c3", 0.1), ("c4", 0.012)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        res = oracle.reduce(M)
+        assert res.rank > 2 * 4 * 128, (name, res.rank)             # several super-panels of 4 panels
+        for sp in ("4", "2", "3"):
+            monkeypatch.setenv("GBLA_SP", sp)
+            check_full(gb, ctx, M, res, check_dnew=(sp == "4"))
+    monkeypatch.delenv("GBLA_SP")
 
 
 def test_sharded_sparse_phase_emulated_ranks(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
