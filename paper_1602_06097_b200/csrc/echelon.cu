@@ -36,14 +36,9 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
-void modgemm_set_sms(int sms);
 gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab);
 gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, const uint16_t *invtab, int G,
                         int me, bool real);
-gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
-                             const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr, int grid_cap = 0);
 
 namespace {
 

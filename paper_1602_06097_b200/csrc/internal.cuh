@@ -254,6 +254,33 @@ gbla_status dist_sparse_phase(gbla_mat h);
 int dist_emulated_world();
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
 
+// K11 launchers (tc_gemm.cu); see the kernels there for the argument conventions
+gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                           const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
+                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap,
+                           const int64_t *cend_dev = nullptr);
+gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
+                              const uint8_t *Alo, const uint8_t *Ahi, int64_t a_rt_stride, int nkb,
+                              const uint8_t *Blo, const uint8_t *Bhi, int64_t b_kb_stride, const int64_t *kb_c0,
+                              const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
+                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap,
+                              const uint8_t *B2lo = nullptr, const uint8_t *B2hi = nullptr);
+gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
+                             const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
+                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
+                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr, int grid_cap = 0,
+                             uint8_t *Tlo2 = nullptr, uint8_t *Thi2 = nullptr);
+void modgemm_set_sms(int sms);
+gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t *Tlo, const uint8_t *Thi,
+                           const uint8_t *Bglo, const uint8_t *Bghi, uint8_t *Rlo, uint8_t *Rhi,
+                           const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
+                           const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
+                           const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
+                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
+                           uint8_t *Rlo2 = nullptr, uint8_t *Rhi2 = nullptr);
+
+
 static inline unsigned grid_for(int64_t work, int per_block) {
     int64_t g = (work + per_block - 1) / per_block;
     if (g < 1) g = 1;

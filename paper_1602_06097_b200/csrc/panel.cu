@@ -42,28 +42,6 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
-gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
-                           const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                           const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
-                           const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap,
-                           const int64_t *cend_dev = nullptr);
-gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,
-                              const uint8_t *Alo, const uint8_t *Ahi, int64_t a_rt_stride, int nkb,
-                              const uint8_t *Blo, const uint8_t *Bhi, int64_t b_kb_stride, const int64_t *kb_c0,
-                              const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
-                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap);
-gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
-                             const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
-                             uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows = nullptr, int grid_cap = 0);
-void modgemm_set_sms(int sms);
-gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t *Tlo, const uint8_t *Thi,
-                           const uint8_t *Bglo, const uint8_t *Bghi, uint8_t *Rlo, uint8_t *Rhi,
-                           const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
-                           const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
-                           const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
-                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN);
-
 namespace {
 
 // launch with programmatic dependent launch (the kernel calls pdl_trigger / pdl_wait): its launch
@@ -1626,7 +1604,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     cudaStream_t st = h->stream;
     modgemm_set_sms(h->ctx->sm_count);
     const int64_t mN = h->mN, nN = h->nN, ldD = h->ldD, ldR = h->ldD;
-    const int64_t npad = (nN + 63) / 64 * 64 + 64;
+    const int64_t npad = (nN + 63) / 64 * 64 + 128;      // + the 64-column tiles a 128-column pair tile reads
     uint32_t *rows[2], *lead;
     uint16_t *Rn;
     uint8_t *Flo[2], *Fhi[2], *Tlo2[2], *Thi2[2], *Blo, *Bhi, *Rtlo, *Rthi;
@@ -1647,13 +1625,18 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // (K11 multi-K: a quarter of the HBM passes and epilogue reductions of per-panel updates).
     const int G = lookahead ? sp_panels(mN, nN) : 1;
     const size_t rd_stride = (size_t)npad * PK;          // bytes per plane per K-block
-    const int64_t ntrD = (mN + 127) / 128;
+    const int64_t ntrD = (mN + 127) / 128, ntrD2 = (ntrD + 1) / 2 * 2;
     uint8_t *Fdlo = nullptr, *Fdhi = nullptr, *Aflo = nullptr, *Afhi = nullptr;
     int64_t *spc0 = nullptr, *spCd = nullptr;
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Blo));
     GBLA_TRY(dalloc_t(h, (size_t)npad * PK, &Bhi));
     GBLA_TRY(dalloc_t(h, rd_stride * G, &Rtlo));
     GBLA_TRY(dalloc_t(h, rd_stride * G, &Rthi));
+    uint8_t *Rplo = nullptr, *Rphi = nullptr;            // 2^8 Rn mod p: the second B operand of the pair flush
+    if (G > 1) {
+        GBLA_TRY(dalloc_t(h, rd_stride * G, &Rplo));
+        GBLA_TRY(dalloc_t(h, rd_stride * G, &Rphi));
+    }
     uint32_t *srow = nullptr, *spos = nullptr, *skey = nullptr, *nflush = nullptr;
     if (G > 1) {
         uint32_t *ilead, *iota;
@@ -1676,10 +1659,13 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         note_launch(3);
     }
     if (G > 1) {
-        GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdlo));
-        GBLA_TRY(dalloc_t(h, (size_t)ntrD * G * PK * 128, &Fdhi));
-        GBLA_TRY(dalloc_t(h, (size_t)G * PK * 128, &Aflo));
-        GBLA_TRY(dalloc_t(h, (size_t)G * PK * 128, &Afhi));
+        // an even number of row tiles (the CTA-pair GEMM reads row tiles in pairs; the extra one is zero)
+        GBLA_TRY(dalloc_t(h, (size_t)ntrD2 * G * PK * 128, &Fdlo));
+        GBLA_TRY(dalloc_t(h, (size_t)ntrD2 * G * PK * 128, &Fdhi));
+        GBLA_TRY(dalloc_t(h, (size_t)2 * G * PK * 128, &Aflo));
+        GBLA_TRY(dalloc_t(h, (size_t)2 * G * PK * 128, &Afhi));
+        GBLA_CUDA_TRY(cudaMemsetAsync(Aflo + (size_t)G * PK * 128, 0, (size_t)G * PK * 128, st));
+        GBLA_CUDA_TRY(cudaMemsetAsync(Afhi + (size_t)G * PK * 128, 0, (size_t)G * PK * 128, st));
         GBLA_TRY(dalloc_t(h, (size_t)G, &spc0));
         GBLA_TRY(dalloc_t(h, 1, &spCd));
     }
@@ -1741,8 +1727,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     auto sp_begin = [&](const P2State *last, cudaStream_t s) {
         k_sp_begin<<<1, 1, 0, s>>>(last, nN, G, spCd);
         note_launch();
-        if (cudaMemsetAsync(Fdlo, 0, (size_t)ntrD * G * PK * 128, s) != cudaSuccess ||
-            cudaMemsetAsync(Fdhi, 0, (size_t)ntrD * G * PK * 128, s) != cudaSuccess)
+        if (cudaMemsetAsync(Fdlo, 0, (size_t)ntrD2 * G * PK * 128, s) != cudaSuccess ||
+            cudaMemsetAsync(Fdhi, 0, (size_t)ntrD2 * G * PK * 128, s) != cudaSuccess)
             return GBLA_E_CUDA;
         return GBLA_OK;
     };
@@ -1752,7 +1738,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         note_launch();
         const gbla_status r = modgemm_tc_sub_mk(s, mN, nflush, nN, h->F, Fdlo, Fdhi, G, G, Rtlo, Rthi,
                                                 (int64_t)rd_stride, spc0, srow, h->D, ldD, spCd, &cur->c1, PW,
-                                                ctsel, gemm_grid);
+                                                ctsel, gemm_grid, Rplo, Rphi);
         kt_mark_on(h, KT_TRAIL, s);
         return r;
     };
@@ -1821,6 +1807,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             const int f = (int)(k & 1);
             const int j = (int)(k % G);                  // position in the super-panel
             uint8_t *Rtl = Rtlo + j * rd_stride, *Rth = Rthi + j * rd_stride;
+            uint8_t *Rpl = Rplo ? Rplo + j * rd_stride : nullptr, *Rph = Rphi ? Rphi + j * rd_stride : nullptr;
             tmark(k, st);
             if (j > 0) {                                 // S up to date in the deferred columns
                 k_fix_gather<<<dim3(PK, j), 32, 0, st>>>(cur, G, Fdlo, Fdhi, Aflo, Afhi, spos);
@@ -1828,7 +1815,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_sub_mk(st, PK, &cur->kp, nN, h->F, Aflo, Afhi, G, j, Rtlo, Rthi,
                                            (int64_t)rd_stride, spc0, cur->sel, h->D, ldD, spCd, nullptr, 0, 0,
-                                           gemm_grid);
+                                           gemm_grid, Rplo, Rphi);
                 kt_mark(h, KT_TRAIL);
                 if (status != GBLA_OK) break;
             }
@@ -1847,13 +1834,13 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_win(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rtl, Rth, Flo[f], Fhi[f], rows[f],
                                         cur->sel, &cur->nrows, &cur->kp, &cur->c0, &cur->c1, PW, h->D, ldD, wflags,
-                                        (uint32_t)(k + 1), gemm_grid, winlead ? lead : nullptr, rowpiv, mN);
+                                        (uint32_t)(k + 1), gemm_grid, winlead ? lead : nullptr, rowpiv, mN, Rpl, Rph);
             } else {
                 kt_mark(h, KT_RN);
                 // look-ahead: only the window part of Rn is on the chain to the next panel, and the Rn
                 // GEMM writes D[S, c0:] = Rn itself (no commit kernel on the chain)
                 status = lookahead ? modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth,
-                                                      &cur->c0, &cur->kp, &cur->c1, PW, 1, cur->sel)
+                                                      &cur->c0, &cur->kp, &cur->c1, PW, 1, cur->sel, 0, Rpl, Rph)
                                    : modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rn, ldR, Rtl, Rth,
                                                       &cur->c0, &cur->kp, &cur->c1, PW, 0);
                 if (lookahead) kt_mark2(h, KT_RN, KT_TRAIL, st);    // closes Rn window, opens the window update
@@ -1896,7 +1883,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 note_launch();
                 kt_mark_on(h, KT_RN, rest);
                 status = modgemm_tc_store(rest, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
-                                          &cur->kp, &cur->c1, PW, 2, cur->sel, gemm_grid);   // an SM for the panel
+                                          &cur->kp, &cur->c1, PW, 2, cur->sel, gemm_grid, Rpl, Rph);   // an SM for the panel
                 kt_mark_on(h, KT_RN, rest);
                 if (status != GBLA_OK) break;
                 kt_mark_on(h, KT_TRAIL, rest);
@@ -1948,7 +1935,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 note_launch();
                 kt_mark(h, KT_RN);
                 status = modgemm_tc_store(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
-                                          &cur->kp, &cur->c1, PW, 2, cur->sel);
+                                          &cur->kp, &cur->c1, PW, 2, cur->sel, 0, Rpl, Rph);
                 kt_mark2(h, KT_RN, KT_TRAIL, st);
                 if (status != GBLA_OK) break;
                 status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,

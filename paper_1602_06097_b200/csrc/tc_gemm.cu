@@ -79,6 +79,10 @@ struct MMArgs {
     const int64_t *kb_c0;
     const int64_t *cend_dev;          // optional end column (min(cols, *cend_dev))
     int exp;                          // microbenchmark experiments (0 = normal)
+    // the multi-K CTA-pair kernel's second B operand: limb planes of B' = 2^8 B mod p (same tile
+    // layout as Blo / Bhi); MODE_STORE writes them for its result when Tlo2 != NULL
+    const uint8_t *B2lo, *B2hi;
+    uint8_t *Tlo2, *Thi2;
 };
 
 constexpr int NSB = 4;                               // B stages
@@ -396,6 +400,13 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
                             g.Thi[o] = (uint8_t)(s0 >> 8);
                             g.Tlo[o + 16] = (uint8_t)(s1 & 0xff);
                             g.Thi[o + 16] = (uint8_t)(s1 >> 8);
+                            if (g.Tlo2) {                  // B' = 2^8 B mod p (multi-K pair kernel)
+                                const uint32_t t0 = fmod32(s0 << 8, g.F), t1 = fmod32(s1 << 8, g.F);
+                                g.Tlo2[o] = (uint8_t)(t0 & 0xff);
+                                g.Thi2[o] = (uint8_t)(t0 >> 8);
+                                g.Tlo2[o + 16] = (uint8_t)(t1 & 0xff);
+                                g.Thi2[o + 16] = (uint8_t)(t1 >> 8);
+                            }
                         }
                     }
                 }
@@ -428,6 +439,391 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
+// ---- K11 multi-K on a CTA pair (tcgen05 cta_group::2) -----------------------------------------
+// The deferred super-panel flush C[rowidx[i], c0 + x] -= sum_{j < nkb} A_j[i] B_j[:, x] (K <= 512):
+// the dominant kernel of c2-c4.  A single CTA issuing M = 128 MMAs re-reads its A operand from
+// shared memory for every N = 64 column block and reaches about half of the tensor rate
+// (measured 1.48 POPS without any epilogue); a CTA pair (cluster of 2 on one TPC) issues
+// M = 256 MMAs (tcgen05.mma.cta_group::2): each CTA holds the A tiles of its own 128 rows
+// (resident per row-tile pair, 128 KB) and HALF of every B tile (32 of the 64 columns), the
+// leader's single thread issues the MMAs for both, and each CTA's TMEM receives its own
+// 128 x 64 accumulators (HH | X | LL, double-buffered).  Barriers: the leader's afull / bfull
+// complete when its own bulk copies landed AND the peer's forwarder (which waits on the peer's
+// own barrier) arrived remotely; the MMA commits multicast to both CTAs' empty / tfull barriers;
+// both CTAs' epilogue warps arrive on the leader's tempty.  Exactness as k_modgemm_ws (MK).
+// Waits are bounded (~10 s, then trap: a launch failure instead of a hung GPU).
+namespace pair {
+__device__ __forceinline__ uint32_t cta_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void *p, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr)
+{
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t *bar, uint32_t phase)
+{
+    const long long t0 = clock64();
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(tc::smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > (1ll << 34)) __trap();          // ~9 s at 1.9 GHz: never hang the GPU
+    }
+}
+// CTA-scope wait (no L1 invalidation): for barriers whose data is this CTA's own (TMEM accumulators)
+__device__ __forceinline__ void wait_cta(uint64_t *bar, uint32_t phase)
+{
+    const long long t0 = clock64();
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(tc::smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+__device__ __forceinline__ void mma2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t *bar)
+{
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            tc::smem_u32(bar))
+        : "memory");
+}
+}  // namespace pair
+
+// Two accumulators instead of three (the limb products regrouped mod p): with a = 2^8 a_h + a_l and
+// B' = 2^8 B mod p (precomputed per B entry, limbs b'_h, b'_l),
+//   a b = 2^8 a_h b + a_l b  ==  a_h b' + a_l b  (mod p)  ==  2^8 (a_h b'_h + a_l b_h) + (a_h b'_l + a_l b_l),
+// so U = sum a_h b'_h + a_l b_h and V = sum a_h b'_l + a_l b_l (4 MMAs per K step as before) and
+// S == 2^8 U + V (mod p).  Exact: U, V <= 2 K 255^2 < 2^31 for K <= 16,512 (here K <= 512); the
+// epilogue forms (2^8 (U mod p) + V) < 2^24 + 2^31 in 32 bits.  A pair tile is 256 rows x 128
+// columns (M = 256, N = 128 MMAs: each CTA stages one whole 64-column B tile, B and B' planes), so
+// 2 x 128 TMEM columns per tile: two accumulator sets (double-buffered, 512 columns).
+constexpr int PR_NP = 128;                                     // columns of a pair tile
+constexpr int PR_NSB = 3;                                      // B stages
+constexpr uint32_t PR_BSTAGE = 4 * B_PLANE;                    // B_h, B_l, B'_h, B'_l of one 64-col tile
+constexpr int PR_SMEM = MK_MAX * A_BYTES + PR_NSB * PR_BSTAGE; // 128 KB + 96 KB
+
+__global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_mk2(MMArgs g)
+{
+    constexpr int NP = PR_NP, NSB = PR_NSB;
+    constexpr int EPI_WARPS = 8, EPI_COLS = NP / (EPI_WARPS / 4);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t afull, aempty, bfull[NSB], bempty[NSB], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base;
+    tc::pdl_trigger();
+    tc::pdl_wait();
+    const uint32_t rank = pair::cta_rank();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // the pair's work (identical in both CTAs); an empty launch still runs the cluster handshakes
+    int64_t cols = g.cols, c0 = 0;
+    uint16_t *C = g.C;
+    if (g.c0_dev) {
+        c0 = *g.c0_dev;
+        cols -= c0;
+        C += c0;
+    }
+    const int64_t nr = g.nrows_dev ? (int64_t)*g.nrows_dev : g.nrows;
+    const int64_t ntr2 = cols > 0 ? (nr + 2 * BM - 1) / (2 * BM) : 0, ntc_all = cols > 0 ? (cols + NP - 1) / NP : 0;
+    int64_t w0 = 0, w1 = 0;
+    if (g.ctsel != CT_ALL && cols > 0) {
+        const int64_t rel = *g.win_dev - c0;
+        w0 = rel > 0 ? rel / NP : 0;
+        w1 = rel + g.win_w > 0 ? (rel + g.win_w + NP - 1) / NP : 0;
+        if (w0 > ntc_all) w0 = ntc_all;
+        if (w1 > ntc_all) w1 = ntc_all;
+        if (w1 < w0) w1 = w0;
+    }
+    const int64_t ntc = g.ctsel == CT_ALL ? ntc_all : g.ctsel == CT_WINDOW ? w1 - w0 : ntc_all - (w1 - w0);
+    const int64_t ntiles = ntr2 * ntc;
+    const int64_t npairs = gridDim.x / 2, pid = blockIdx.x / 2;
+    const int64_t per = (ntiles + npairs - 1) / npairs;
+    const int64_t t_begin = pid * per;
+    const int64_t t_end = t_begin + per < ntiles ? t_begin + per : ntiles;
+    auto ct_of = [&](int64_t j) -> int64_t {
+        if (g.ctsel == CT_WINDOW) return w0 + j;
+        if (g.ctsel == CT_REST) return j < w0 ? j : j + (w1 - w0);
+        return j;
+    };
+    const int nkb = g.nkb;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::smem_u32(&tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        const uint32_t nfill = rank == 0 ? 2 : 1;        // leader: own copies + the peer's forwarder
+        tc::mbar_init(&afull, nfill);
+        tc::mbar_init(&aempty, 1);
+        for (int i = 0; i < NSB; i++) {
+            tc::mbar_init(&bfull[i], nfill);
+            tc::mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], 2 * EPI_WARPS);
+        }
+    }
+    tc::fence_before();
+    pair::cluster_sync();
+    tc::fence_after();
+    const uint32_t tbase = tmem_base;
+    uint8_t *Abuf = smem, *Bbuf = smem + MK_MAX * A_BYTES;
+    if (t_begin < t_end) {
+    if (warp == 0 && lane == 0) {                    // ---- producer (both CTAs): own A rows, own B tile
+        int64_t cur_rt = -1;
+        uint32_t aph = 1, bph = 0;                   // bph: bit s = phase of stage s
+        int s = 0;
+        int64_t boff[MK_MAX];
+#pragma unroll
+        for (int i = 0; i < MK_MAX; i++) {
+            boff[i] = 0;
+            if (i < nkb && g.kb_c0) {
+                const int64_t d = (c0 - g.kb_c0[i]) / BN;
+                boff[i] = d > 0 ? d : 0;
+            }
+        }
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            const int64_t rt2 = tile / ntc, ct = ct_of(tile % ntc);
+            if (rt2 != cur_rt) {
+                pair::wait(&aempty, aph);
+                aph ^= 1;
+                tc::mbar_expect_tx(&afull, nkb * A_BYTES);
+                const int64_t rt = 2 * rt2 + rank;
+                for (int i = 0; i < nkb; i++) {
+                    const int64_t at = rt * g.a_rt_stride + i;
+                    tc::bulk_g2s(Abuf + i * A_BYTES, g.Ahi + at * A_PLANE, A_PLANE, &afull);
+                    tc::bulk_g2s(Abuf + i * A_BYTES + A_PLANE, g.Alo + at * A_PLANE, A_PLANE, &afull);
+                }
+                cur_rt = rt2;
+            }
+#pragma unroll 1
+            for (int i = 0; i < nkb && g.exp != 3; i++) {
+                pair::wait(&bempty[s], ((bph >> s) & 1) ^ 1);
+                uint8_t *bb = Bbuf + s * PR_BSTAGE;
+                tc::mbar_expect_tx(&bfull[s], PR_BSTAGE);
+                // this CTA's 64 columns: the 64-column B tile 2 ct + rank (planes B_h, B_l, B'_h, B'_l)
+                const int64_t bo = g.b_kb_stride * i + (2 * ct + rank + boff[i]) * B_PLANE;
+                tc::bulk_g2s(bb, g.Bhi + bo, B_PLANE, &bfull[s]);
+                tc::bulk_g2s(bb + B_PLANE, g.Blo + bo, B_PLANE, &bfull[s]);
+                tc::bulk_g2s(bb + 2 * B_PLANE, g.B2hi + bo, B_PLANE, &bfull[s]);
+                tc::bulk_g2s(bb + 3 * B_PLANE, g.B2lo + bo, B_PLANE, &bfull[s]);
+                bph ^= 1u << s;
+                s = (s + 1) % NSB;
+            }
+        }
+    } else if (warp == 1 && lane == 0 && rank == 1) {   // ---- peer: forward own fills to the leader
+        int64_t cur_rt = -1;
+        uint32_t aph = 0, bph = 0;
+        int s = 0;
+        const uint32_t ra = pair::mapa(&afull, 0);
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            const int64_t rt2 = tile / ntc;
+            if (rt2 != cur_rt) {
+                pair::wait(&afull, aph);
+                aph ^= 1;
+                pair::arrive_remote(ra);
+                cur_rt = rt2;
+            }
+#pragma unroll 1
+            for (int i = 0; i < nkb && g.exp != 3; i++) {
+                pair::wait(&bfull[s], (bph >> s) & 1);
+                bph ^= 1u << s;
+                pair::arrive_remote(pair::mapa(&bfull[s], 0));
+                s = (s + 1) % NSB;
+            }
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {   // ---- MMA issuer (leader)
+        int64_t cur_rt = -1;
+        uint32_t aph = 0, bph = 0, tph[2] = {1, 1};
+        int s = 0, ab = 0;
+        const uint32_t idesc = tc::idesc_u8(2 * BM, NP);
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            const int64_t rt2 = tile / ntc;
+            if (rt2 != cur_rt) {
+                if (cur_rt >= 0) pair::commit2(&aempty);
+                pair::wait(&afull, aph);
+                aph ^= 1;
+                cur_rt = rt2;
+            }
+            pair::wait(&tempty[ab], tph[ab]);
+            tph[ab] ^= 1;
+            const uint32_t dU = tbase + ab * 2 * NP, dV = dU + NP;
+#pragma unroll 1
+            for (int i = 0; i < nkb; i++) {
+                if (g.exp != 3) {                        // experiment 3: tensor rate alone (no B traffic)
+                    pair::wait(&bfull[s], (bph >> s) & 1);
+                    bph ^= 1u << s;
+                }
+                tc::fence_after();
+                const uint32_t aH = tc::smem_u32(Abuf + i * A_BYTES), aL = aH + A_PLANE;
+                const uint32_t bH = tc::smem_u32(Bbuf + s * PR_BSTAGE), bL = bH + B_PLANE;
+                const uint32_t b2H = bH + 2 * B_PLANE, b2L = bH + 3 * B_PLANE;
+#pragma unroll
+                for (int k = 0; k < KP / 32; k++) {
+                    const uint32_t ao = k * 2 * (BM * 16), bo = k * 2 * (BN * 16);
+                    const uint64_t dAh = tc::desc_kmajor(aH + ao, BM * 16, 128);
+                    const uint64_t dAl = tc::desc_kmajor(aL + ao, BM * 16, 128);
+                    const uint64_t dBh = tc::desc_kmajor(bH + bo, BN * 16, 128);
+                    const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
+                    const uint64_t dB2h = tc::desc_kmajor(b2H + bo, BN * 16, 128);
+                    const uint64_t dB2l = tc::desc_kmajor(b2L + bo, BN * 16, 128);
+                    const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                    // alternate the accumulators: an MMA into the accumulator of the one just issued
+                    // waits for it (measured: U, U, V, V runs at half the rate of U, V, U, V)
+                    pair::mma2(dU, dAh, dB2h, idesc, acc);        // U += a_h b'_h
+                    pair::mma2(dV, dAh, dB2l, idesc, acc);        // V += a_h b'_l
+                    pair::mma2(dU, dAl, dBh, idesc, 1);           // U += a_l b_h
+                    pair::mma2(dV, dAl, dBl, idesc, 1);           // V += a_l b_l
+                }
+                if (g.exp != 3) pair::commit2(&bempty[s]);
+                s = (s + 1) % NSB;
+            }
+            pair::commit2(&tfull[ab]);
+            ab ^= 1;
+        }
+    } else if (warp >= 2) {                          // ---- epilogue warps 2..9 (both CTAs)
+        const int e = warp - 2, quarter = warp & 3, part = e >> 2;
+        // 32-byte vectors (LDG/STG.256) when every row segment is 32-byte aligned
+        const bool vec = ((reinterpret_cast<uintptr_t>(C) & 31) == 0) && (g.ldc % 16 == 0);
+        const uint32_t tempty_leader[2] = {pair::mapa(&tempty[0], 0), pair::mapa(&tempty[1], 0)};
+        uint32_t tph[2] = {0, 0};
+        int ab = 0;
+        uint32_t dn[EPI_COLS / 2];
+        uint16_t *crow_n = nullptr;
+        bool fast_n = false, live_n = false;
+        int64_t x0_n = 0;
+        int64_t rt_c = -1;
+        uint16_t *rowbase = nullptr;
+        auto fetch = [&](int64_t tile) {
+            const int64_t rt2 = tile / ntc, ct = ct_of(tile % ntc);
+            x0_n = ct * NP + part * EPI_COLS;
+            const int64_t slot = (2 * rt2 + rank) * BM + quarter * 32 + lane;
+            live_n = slot < nr;
+            if (rt2 != rt_c) {
+                rt_c = rt2;
+                rowbase = live_n ? C + (size_t)(g.rowidx ? g.rowidx[slot] : slot) * g.ldc : nullptr;
+            }
+            crow_n = live_n ? rowbase + x0_n : nullptr;
+            fast_n = crow_n && vec && x0_n + EPI_COLS <= cols;
+#pragma unroll
+            for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
+            if (live_n && g.exp != 1) {
+                if (fast_n) {
+#pragma unroll
+                    for (int u = 0; u < EPI_COLS / 16; u++)
+                        asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                     : "=r"(dn[8 * u]), "=r"(dn[8 * u + 1]), "=r"(dn[8 * u + 2]), "=r"(dn[8 * u + 3]),
+                                       "=r"(dn[8 * u + 4]), "=r"(dn[8 * u + 5]), "=r"(dn[8 * u + 6]), "=r"(dn[8 * u + 7])
+                                     : "l"(crow_n + 16 * u));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < EPI_COLS; j++)
+                        if (x0_n + j < cols) dn[j / 2] |= (uint32_t)crow_n[j] << (16 * (j & 1));
+                }
+            }
+        };
+        fetch(t_begin);
+        const uint32_t p2 = g.F.p | (g.F.p << 16);
+        for (int64_t tile = t_begin; tile < t_end; tile++) {
+            uint32_t dv[EPI_COLS / 2];
+#pragma unroll
+            for (int w = 0; w < EPI_COLS / 2; w++) dv[w] = dn[w];
+            uint16_t *crow = crow_n;
+            const bool fast = fast_n;
+            const int64_t x0 = x0_n;
+            if (tile + 1 < t_end) fetch(tile + 1);
+            pair::wait_cta(&tfull[ab], tph[ab]);
+            tph[ab] ^= 1;
+            tc::fence_after();
+            if (g.exp != 2) {
+                const uint32_t la = tbase + ((uint32_t)(quarter * 32) << 16) + ab * 2 * NP + part * EPI_COLS;
+#pragma unroll
+                for (int c = 0; c < EPI_COLS; c += 16) {
+                    uint32_t uu[16], vv[16];
+                    tc::tmem_ld16(la + c, uu);
+                    tc::tmem_ld16(la + NP + c, vv);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; j += 2) {
+                        const uint32_t s0 = fmod32((fmod32(uu[j], g.F) << 8) + vv[j], g.F);
+                        const uint32_t s1 = fmod32((fmod32(uu[j + 1], g.F) << 8) + vv[j + 1], g.F);
+                        const int w = (c + j) / 2;
+                        dv[w] = fsub2(dv[w], s0 | (s1 << 16), p2);
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) mbar_arrive(&tempty[ab]);
+                else pair::arrive_remote(tempty_leader[ab]);
+            }
+            ab ^= 1;
+            if (g.exp >= 1) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int w = 0; w < EPI_COLS / 2; w++) acc ^= dv[w];
+                if (acc == 0x9e3779b9u && crow) crow[0] = 1;
+            } else if (fast) {
+#pragma unroll
+                for (int u = 0; u < EPI_COLS / 16; u++)
+                    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + 16 * u), "r"(dv[8 * u]),
+                                 "r"(dv[8 * u + 1]), "r"(dv[8 * u + 2]), "r"(dv[8 * u + 3]), "r"(dv[8 * u + 4]),
+                                 "r"(dv[8 * u + 5]), "r"(dv[8 * u + 6]), "r"(dv[8 * u + 7])
+                                 : "memory");
+            } else if (crow) {
+#pragma unroll
+                for (int j = 0; j < EPI_COLS; j++)
+                    if (x0 + j < cols) crow[j] = (uint16_t)(dv[j / 2] >> (16 * (j & 1)));
+            }
+        }
+    }
+    }
+    tc::fence_before();
+    pair::cluster_sync();                            // the MMAs read both CTAs' shared memory
+    if (warp == 0) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    }
+}
+
 // ---- the echelon's window step in ONE launch (look-ahead path, GBLA_WIN_FUSED) ---------------
 // Tiles q = 0 .. nW-1: Rn window column tile ct = w0 + q (MODE_STORE: A = T, B = the gathered B
 // tiles of D[S, c0:]; writes D[S, c0:] = Rn and the Rn limb tiles, then publishes flag[q] = epoch);
@@ -440,6 +836,7 @@ struct WinArgs {
     const uint8_t *Tlo, *Thi;              // A operand of the Rn tiles (one 128 x 128 tile)
     const uint8_t *Bglo, *Bghi;            // gathered B tiles of D[S, c0:] (column tiles from c0)
     uint8_t *Rlo, *Rhi;                    // Rn limb tiles (written here, B operand of the update)
+    uint8_t *Rlo2, *Rhi2;                  // optional: limb tiles of 2^8 Rn mod p (multi-K pair kernel)
     const uint8_t *Flo, *Fhi;              // A operand of the update (row tiles of the F list)
     const uint32_t *rows;                  // D rows of the update (slot -> row)
     const uint32_t *sel;                   // D rows of the pivot rows (slot -> row)
@@ -653,6 +1050,13 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
                         g.Rhi[o] = (uint8_t)(s0 >> 8);
                         g.Rlo[o + 16] = (uint8_t)(s1 & 0xff);
                         g.Rhi[o + 16] = (uint8_t)(s1 >> 8);
+                        if (g.Rlo2) {
+                            const uint32_t t0 = fmod32(s0 << 8, g.F), t1 = fmod32(s1 << 8, g.F);
+                            g.Rlo2[o] = (uint8_t)(t0 & 0xff);
+                            g.Rhi2[o] = (uint8_t)(t0 >> 8);
+                            g.Rlo2[o + 16] = (uint8_t)(t1 & 0xff);
+                            g.Rhi2[o + 16] = (uint8_t)(t1 >> 8);
+                        }
                     }
                 }
             }
@@ -763,7 +1167,8 @@ __global__ void k_split_rows(int64_t rows, int64_t rows_pad, int64_t K, int nkb,
 // K x cols (ldb) u16 -> B tiles (limb planes, K-major), zero padded; K-block i starts at
 // i * cols_pad * KP (the multi-K GEMM's b_kb_stride)
 __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, int nkb, const uint16_t *__restrict__ B,
-                             int64_t ldb, uint8_t *__restrict__ lo, uint8_t *__restrict__ hi)
+                             int64_t ldb, uint8_t *__restrict__ lo, uint8_t *__restrict__ hi, Field F,
+                             uint8_t *__restrict__ lo2, uint8_t *__restrict__ hi2)
 {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= cols_pad * KP * nkb) return;
@@ -773,6 +1178,11 @@ __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, int nkb,
                      toff64((uint32_t)(x % BN), (uint32_t)(k % KP));
     lo[o] = (uint8_t)(v & 0xff);
     hi[o] = (uint8_t)(v >> 8);
+    if (lo2) {                                    // B' = 2^8 B mod p (multi-K pair kernel)
+        const uint32_t w = fmod32((uint32_t)v << 8, F);
+        lo2[o] = (uint8_t)(w & 0xff);
+        hi2[o] = (uint8_t)(w >> 8);
+    }
 }
 
 // deterministic pseudo-random bytes / residues for the K11 microbenchmark
@@ -849,6 +1259,45 @@ static gbla_status launch_ws(const MMArgs &a, int64_t grid, cudaStream_t st)
 }
 
 int g_sms = 148;
+// K11 multi-K on CTA pairs (k_modgemm_mk2, the default); GBLA_K11_PAIR=0 selects the single-CTA
+// kernel (k_modgemm_ws<MK>), which needs no B' planes
+static bool use_pair()
+{
+    static int v = -1;
+    if (v < 0) v = (getenv("GBLA_K11_PAIR") && atoi(getenv("GBLA_K11_PAIR")) == 0) ? 0 : 1;
+    return v == 1;
+}
+
+static gbla_status launch_pair(const MMArgs &a, int64_t max_rows, int64_t cols, int64_t grid, cudaStream_t st)
+{
+    static bool attr2 = false;
+    if (!attr2) {
+        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_mk2, cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM));
+        attr2 = true;
+    }
+    const int64_t ptiles = ((max_rows + 2 * BM - 1) / (2 * BM)) * ((cols + PR_NP - 1) / PR_NP);
+    int64_t pairs = grid / 2;
+    if (pairs > ptiles) pairs = ptiles;
+    if (pairs < 1) pairs = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(ws_threads(8));
+    cfg.dynamicSmemBytes = PR_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    GBLA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_modgemm_mk2, a));
+    note_launch();
+    return GBLA_OK;
+}
+
 int g_k11_exp = 0;       // gbla_modgemm_bench experiments (GBLA_K11_EXP; 0 everywhere else)
 
 }  // namespace
@@ -876,7 +1325,8 @@ gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nr
 gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8_t *Alo, const uint8_t *Ahi,
                              const uint8_t *Blo, const uint8_t *Bhi, uint16_t *O, int64_t ldo, uint8_t *Tlo,
                              uint8_t *Thi, const int64_t *c0_dev, const uint32_t *skip_dev, const int64_t *win_dev,
-                             int64_t win_w, int ctsel, const uint32_t *orows, int grid_cap)
+                             int64_t win_w, int ctsel, const uint32_t *orows, int grid_cap, uint8_t *Tlo2,
+                             uint8_t *Thi2)
 {
     if (orows && (!skip_dev || !c0_dev)) { set_error("modgemm_tc_store: row map needs the pivot count"); return GBLA_E_INVAL; }
     if (cols <= 0) return GBLA_OK;
@@ -885,6 +1335,8 @@ gbla_status modgemm_tc_store(cudaStream_t st, int64_t cols, Field F, const uint8
     if (grid > g_sms) grid = g_sms;
     if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
     MMArgs a{BM, nullptr, cols, F, Alo, Ahi, Blo, Bhi, orows, O, ldo, Tlo, Thi, c0_dev, skip_dev, win_dev, win_w, ctsel};
+    a.Tlo2 = Tlo2;
+    a.Thi2 = Thi2;
     GBLA_TRY(launch_ws<MODE_STORE>(a, grid, st));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
@@ -896,7 +1348,8 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
                               const uint8_t *Alo, const uint8_t *Ahi, int64_t a_rt_stride, int nkb,
                               const uint8_t *Blo, const uint8_t *Bhi, int64_t b_kb_stride, const int64_t *kb_c0,
                               const uint32_t *rowidx, uint16_t *C, int64_t ldc, const int64_t *c0_dev,
-                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap)
+                              const int64_t *win_dev, int64_t win_w, int ctsel, int grid_cap, const uint8_t *B2lo,
+                              const uint8_t *B2hi)
 {
     if (max_rows <= 0 || cols <= 0 || nkb <= 0) return GBLA_OK;
     if (nkb > MK_MAX) { set_error("modgemm_tc_sub_mk: K > %d", MK_MAX * KP); return GBLA_E_INVAL; }
@@ -905,6 +1358,14 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
              c0_dev, nullptr, win_dev, win_w, ctsel, nkb, a_rt_stride, b_kb_stride, kb_c0, nullptr, g_k11_exp};
+    if (use_pair() && B2lo && B2hi) {
+        // CTA pairs over row-tile pairs: the A tiles of row tile 2 * ceil(rows / 256) - 1 are read
+        // (zero rows: the caller's A buffer holds an even number of row tiles), and the B tiles of an
+        // even number of 64-column tiles (the callers' B buffers are padded)
+        a.B2lo = B2lo;
+        a.B2hi = B2hi;
+        return launch_pair(a, max_rows, cols, grid, st);
+    }
     GBLA_TRY((launch_ws1<MODE_SUB, 8, true, true>(a, grid, st)));
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
@@ -917,15 +1378,16 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
                            const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
                            const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
-                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN)
+                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
+                           uint8_t *Rlo2, uint8_t *Rhi2)
 {
     static bool attr = false;
     if (!attr) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_win, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
         attr = true;
     }
-    WinArgs a{F, Tlo, Thi, Bglo, Bghi, Rlo, Rhi, Flo, Fhi, rows, sel, nrows_dev, kp_dev, c0_dev, win_dev, win_w, cols,
-              D, ldD, flags, epoch, lead, rowpiv, mN};
+    WinArgs a{F, Tlo, Thi, Bglo, Bghi, Rlo, Rhi, Rlo2, Rhi2, Flo, Fhi, rows, sel, nrows_dev, kp_dev, c0_dev, win_dev,
+              win_w, cols, D, ldD, flags, epoch, lead, rowpiv, mN};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(ws_threads(8));
@@ -948,13 +1410,14 @@ void modgemm_set_sms(int sms) { g_sms = sms > 0 ? sms : 148; }
 // super-panel updates (exact: every limb sum <= 512 * 255^2 * 2 < 2^31).
 static gbla_status modgemm_tiles(cudaStream_t st, const Field &F, int64_t rows, int64_t cols, int nkb,
                                  const uint8_t *Alo, const uint8_t *Ahi, const uint8_t *Blo, const uint8_t *Bhi,
-                                 int64_t cp, const uint32_t *rowidx, uint16_t *C, int64_t ldc)
+                                 int64_t cp, const uint32_t *rowidx, uint16_t *C, int64_t ldc, const uint8_t *B2lo,
+                                 const uint8_t *B2hi)
 {
     if (nkb == 1)
         return modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
                               CT_ALL, 0, nullptr);
     return modgemm_tc_sub_mk(st, rows, nullptr, cols, F, Alo, Ahi, nkb, nkb, Blo, Bhi, cp * KP, nullptr, rowidx, C,
-                             ldc, nullptr, nullptr, 0, CT_ALL, 0);
+                             ldc, nullptr, nullptr, 0, CT_ALL, 0, B2lo, B2hi);
 }
 
 extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K,
@@ -980,15 +1443,17 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
         return GBLA_OK;
     }
     const int nkb = K <= KP ? 1 : (int)((K + KP - 1) / KP);
-    const int64_t rp = (rows + BM - 1) / BM * BM, cp = (cols + BN - 1) / BN * BN;
-    const size_t bytes = (size_t)(rp + cp) * KP * nkb * 2 + 256;
+    const int64_t rp = (rows + 2 * BM - 1) / (2 * BM) * (2 * BM), cp = (cols + 2 * BN - 1) / (2 * BN) * (2 * BN);
+    const size_t bytes = (size_t)(rp + 2 * cp) * KP * nkb * 2 + 256;
     uint8_t *ws = (uint8_t *)ctx_alloc(ctx, bytes, st);
     if (!ws) { set_error("gbla_modgemm: workspace allocation failed"); return GBLA_E_NOMEM; }
     uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
+    uint8_t *B2lo = Bhi + cp * KP * nkb, *B2hi = B2lo + cp * KP * nkb;
     k_split_rows<<<grid_for(rp * KP * nkb, 256), 256, 0, st>>>(rows, rp, K, nkb, A, lda, Alo, Ahi);
-    k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, K, nkb, B, ldb, Blo, Bhi);
+    k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, K, nkb, B, ldb, Blo, Bhi, F,
+                                                              nkb > 1 ? B2lo : nullptr, B2hi);
     note_launch(2);
-    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, rowidx, C, ldc);
+    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, rowidx, C, ldc, B2lo, B2hi);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1010,16 +1475,17 @@ extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows
     modgemm_set_sms(ctx->sm_count);
     const Field F = make_field(p);
     const int nkb = (int)((K + KP - 1) / KP);
-    const int64_t rp = (rows + BM - 1) / BM * BM, cp = (cols + BN - 1) / BN * BN, ldc = cp;
-    const size_t opb = (size_t)(rp + cp) * KP * nkb * 2, cb = (size_t)rows * ldc * 2;
+    const int64_t rp = (rows + 2 * BM - 1) / (2 * BM) * (2 * BM), cp = (cols + 2 * BN - 1) / (2 * BN) * (2 * BN), ldc = cp;
+    const size_t opb = (size_t)(rp + 2 * cp) * KP * nkb * 2, cb = (size_t)rows * ldc * 2;
     uint8_t *ws = (uint8_t *)ctx_alloc(ctx, opb + cb + 256, st);
     if (!ws) { set_error("gbla_modgemm_bench: allocation failed"); return GBLA_E_NOMEM; }
     uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
+    uint8_t *B2lo = Bhi + cp * KP * nkb, *B2hi = B2lo + cp * KP * nkb;
     uint16_t *C = reinterpret_cast<uint16_t *>(ws + (opb + 255) / 256 * 256);
     k_fill_hash<<<4 * ctx->sm_count, 256, 0, st>>>(ws, opb, 12345u);
     k_fill_res<<<4 * ctx->sm_count, 256, 0, st>>>(C, (size_t)rows * ldc, p, 777u);
     note_launch(2);
-    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc);
+    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc, B2lo, B2hi);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (s == GBLA_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)) {
         set_error("gbla_modgemm_bench: event creation failed");
@@ -1029,7 +1495,7 @@ extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows
         g_k11_exp = getenv("GBLA_K11_EXP") ? atoi(getenv("GBLA_K11_EXP")) : 0;
         cudaEventRecord(e0, st);
         for (int r = 0; r < reps && s == GBLA_OK; r++)
-            s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc);
+            s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc, B2lo, B2hi);
         cudaEventRecord(e1, st);
         g_k11_exp = 0;
         if (cudaEventSynchronize(e1) != cudaSuccess) { set_error("gbla_modgemm_bench: kernel failed"); s = GBLA_E_CUDA; }
