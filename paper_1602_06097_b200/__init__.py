@@ -163,10 +163,23 @@ class Context:
         if torch_allocator:
             dev = torch.device("cuda", device)
 
+            streams = {}
+
             def _alloc(nbytes, stream, user):
-                # an exception must not cross the C boundary: out of memory -> NULL -> GBLA_E_NOMEM
+                # an exception must not cross the C boundary: out of memory -> NULL -> GBLA_E_NOMEM.
+                # The block belongs to the library's stream (torch reuses a freed block only in that
+                # stream's order), not to torch's current stream.
                 try:
-                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                    sid = int(stream or 0)
+                    if sid == torch.cuda.current_stream(dev).cuda_stream:
+                        t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                    else:
+                        s = streams.get(sid)
+                        if s is None:
+                            s = torch.cuda.ExternalStream(sid, device=dev) if sid else torch.cuda.default_stream(dev)
+                            streams[sid] = s
+                        with torch.cuda.stream(s):
+                            t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
                 except Exception:
                     return None
                 ptr = t.data_ptr()
@@ -182,8 +195,9 @@ class Context:
 
             def _memq(user):
                 # what torch can still hand out in one piece: its unused cached blocks go back to the
-                # driver first (they may be fragmented), then the driver's free memory.  Called once
-                # per large reduction (sizing of the X-tile batches), never on a hot path.
+                # driver first (they may be fragmented), then the driver's free memory.  Called only
+                # when the driver's free memory alone is short of a whole sparse phase's X tiles (c4),
+                # never on a hot path: emptying the cache makes later allocations fresh cudaMallocs.
                 try:
                     torch.cuda.empty_cache()
                     return int(torch.cuda.mem_get_info(dev)[0])

@@ -403,7 +403,8 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     GBLA_TRY(gbla_splice(ctx, M, p, flags & GBLA_HOST_INPUT, stream, &h));
     gbla_status s;
     const bool dist = (ctx->world > 1 && ctx->nccl_comm) || dist_emulated_world() > 1;
-    if (dist && !(flags & (GBLA_ORDER_STANDARD | GBLA_SPARSE_INT | GBLA_KEEP_CPRIME))) {
+    // (the INT-pipe echelon is single-GPU only: with GBLA_DENSE_INT every rank reduces the whole D)
+    if (dist && !(flags & (GBLA_ORDER_STANDARD | GBLA_SPARSE_INT | GBLA_KEEP_CPRIME | GBLA_DENSE_INT))) {
         // multi-GPU (dist.cu): row-sharded tensor-core sparse phase + D_new all-gather
         PhaseTimer tm(h->stream);
         s = dist_sparse_phase(h);
@@ -561,8 +562,10 @@ extern "C" void gbla_mat_free(gbla_mat h)
 {
     if (!h) return;
     cudaSetDevice(h->ctx->device);
-    dfree_all(h);
+    // every kernel of this handle is done before its memory goes back to the allocator (the echelon
+    // joins its side streams before returning, so h->stream covers them)
     cudaStreamSynchronize(h->stream);
+    dfree_all(h);
     band_free(h);
     std::vector<cudaEvent_t> all;                 // an event shared by two timer pairs goes back once
     for (auto &v : h->kt.ev) all.insert(all.end(), v.begin(), v.end());

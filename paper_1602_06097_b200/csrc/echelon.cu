@@ -668,7 +668,13 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     // row-sharded D (multi-GPU, or emulated ranks): the distributed echelon assembles R itself
     const bool real = h->ctx->world > 1 && h->ctx->nccl_comm;
     const int G = real ? h->ctx->world : dist_emulated_world();
-    if (h->dist_rows && G > 1 && !(flags & GBLA_DENSE_INT)) {
+    if (h->dist_rows && G > 1) {
+        if (flags & GBLA_DENSE_INT) {
+            // a row-sharded D holds only this rank's updated rows: the single-GPU INT engine would
+            // echelon a partly updated D and give every rank a different (wrong) R
+            set_error("gbla_echelon_D: GBLA_DENSE_INT is single-GPU only (D is row-sharded)");
+            return GBLA_E_INVAL;
+        }
         if (mN > 0 && nN > 0) return panels_dist(h, rowpiv, dops, invtab, G, real ? h->ctx->rank : 0, real);
     }
     if (mN > 0 && nN > 0) {

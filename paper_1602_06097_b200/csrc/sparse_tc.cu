@@ -157,10 +157,12 @@ __device__ __forceinline__ void issue_mmas(uint32_t tbase, uint32_t sA, uint32_t
         const uint64_t dAl = tc::desc_kmajor(sA + off, 2048, 128), dAh = tc::desc_kmajor(sA + PB + off, 2048, 128);
         const uint64_t dBl = tc::desc_kmajor(sB + off, 2048, 128), dBh = tc::desc_kmajor(sB + PB + off, 2048, 128);
         const uint32_t acc = (acc_in || s > 0) ? 1u : 0u;
+        // the two X products are not issued back to back (an MMA into the accumulator of the one
+        // just issued waits for it)
         tc::mma_i8(tbase + 0, dAh, dBh, idesc, acc);
         tc::mma_i8(tbase + 128, dAh, dBl, idesc, acc);
-        tc::mma_i8(tbase + 128, dAl, dBh, idesc, 1u);
         tc::mma_i8(tbase + 256, dAl, dBl, idesc, acc);
+        tc::mma_i8(tbase + 128, dAl, dBh, idesc, 1u);
     }
 }
 
@@ -947,9 +949,10 @@ static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
     if (e && atoll(e) > 0) return atoll(e) < nl ? atoll(e) : nl;
     if (nl * per_tile <= ((int64_t)8 << 30)) return nl;   // small: no need to ask the driver
     size_t fr = 0, tot = 0;
-    if (h->ctx->memq) fr = h->ctx->memq(h->ctx->memq_user);      // the caller's allocator (torch: + cached)
-    else if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
     const int64_t reserve = (int64_t)4 << 30;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return nl; }
+    if ((int64_t)fr - reserve >= nl * per_tile) return nl;         // fits in what the driver has free
+    if (h->ctx->memq) fr = h->ctx->memq(h->ctx->memq_user);      // the caller's allocator (torch: + cached)
     int64_t budget = (int64_t)fr - reserve;
     if (budget < per_tile) budget = per_tile;
     const int64_t b = budget / per_tile;

@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
                         const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
                         tc::mma_i8(d + 0, dAh, dBh, idesc, acc);          // HH
                         tc::mma_i8(d + BN, dAh, dBl, idesc, acc);         // X
-                        tc::mma_i8(d + BN, dAl, dBh, idesc, 1);           // X
                         tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, acc);     // LL
+                        tc::mma_i8(d + BN, dAl, dBh, idesc, 1);           // X (not back to back)
                     }
                     tc::commit(&bempty[s]);
                     s = (s + 1) % NSB;
@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
                     const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
                     tc::mma_i8(d + 0, dAh, dBh, idesc, k > 0);          // HH
                     tc::mma_i8(d + BN, dAh, dBl, idesc, k > 0);         // X
-                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);             // X
                     tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, k > 0);     // LL
+                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);             // X (not back to back)
                 }
                 tc::commit(&bempty[s]);                                 // B stage free
                 tc::commit(&tfull[ab]);                                 // accumulator ready
@@ -985,8 +985,8 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
                     const uint64_t dBl = tc::desc_kmajor(bL + bo, BN * 16, 128);
                     tc::mma_i8(d + 0, dAh, dBh, idesc, k > 0);
                     tc::mma_i8(d + BN, dAh, dBl, idesc, k > 0);
-                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);
                     tc::mma_i8(d + 2 * BN, dAl, dBl, idesc, k > 0);
+                    tc::mma_i8(d + BN, dAl, dBh, idesc, 1);
                 }
                 tc::commit(&bempty[s]);
                 tc::commit(&tfull[ab]);
@@ -1183,6 +1183,18 @@ __global__ void k_split_cols(int64_t cols, int64_t cols_pad, int64_t K, int nkb,
         lo2[o] = (uint8_t)(w & 0xff);
         hi2[o] = (uint8_t)(w >> 8);
     }
+}
+
+// a permutation of [0, n) for the K11 microbenchmark: i -> (a i + b) mod n with gcd(a, n) = 1
+__global__ void k_bench_perm(int64_t n, uint32_t *__restrict__ perm)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t a = 2654435761ull % (uint64_t)n;
+    if (a == 0) a = 1;
+    auto g = [](uint64_t x, uint64_t y) { while (y) { const uint64_t t = x % y; x = y; y = t; } return x; };
+    while (g(a, (uint64_t)n) != 1) a++;
+    perm[i] = (uint32_t)((a * (uint64_t)i + 12345u) % (uint64_t)n);
 }
 
 // deterministic pseudo-random bytes / residues for the K11 microbenchmark
@@ -1482,10 +1494,18 @@ extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows
     uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
     uint8_t *B2lo = Bhi + cp * KP * nkb, *B2hi = B2lo + cp * KP * nkb;
     uint16_t *C = reinterpret_cast<uint16_t *>(ws + (opb + 255) / 256 * 256);
+    // GBLA_K11_BENCH_PERM=1: C rows gathered through a pseudo-random row index (the echelon's
+    // flushes address D rows in lead order, scattered in memory)
+    uint32_t *perm = nullptr;
+    if (getenv("GBLA_K11_BENCH_PERM") && atoi(getenv("GBLA_K11_BENCH_PERM")) == 1) {
+        perm = (uint32_t *)ctx_alloc(ctx, (size_t)rows * 4 + 16, st);
+        if (!perm) { ctx_free(ctx, ws, st); set_error("gbla_modgemm_bench: allocation failed"); return GBLA_E_NOMEM; }
+        k_bench_perm<<<grid_for(rows, 256), 256, 0, st>>>(rows, perm);
+    }
     k_fill_hash<<<4 * ctx->sm_count, 256, 0, st>>>(ws, opb, 12345u);
     k_fill_res<<<4 * ctx->sm_count, 256, 0, st>>>(C, (size_t)rows * ldc, p, 777u);
     note_launch(2);
-    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc, B2lo, B2hi);
+    gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, perm, C, ldc, B2lo, B2hi);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (s == GBLA_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)) {
         set_error("gbla_modgemm_bench: event creation failed");
@@ -1495,7 +1515,7 @@ extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows
         g_k11_exp = getenv("GBLA_K11_EXP") ? atoi(getenv("GBLA_K11_EXP")) : 0;
         cudaEventRecord(e0, st);
         for (int r = 0; r < reps && s == GBLA_OK; r++)
-            s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, nullptr, C, ldc, B2lo, B2hi);
+            s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, perm, C, ldc, B2lo, B2hi);
         cudaEventRecord(e1, st);
         g_k11_exp = 0;
         if (cudaEventSynchronize(e1) != cudaSuccess) { set_error("gbla_modgemm_bench: kernel failed"); s = GBLA_E_CUDA; }
@@ -1507,6 +1527,7 @@ extern "C" gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows
     if (e1) cudaEventDestroy(e1);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
+    if (perm) ctx_free(ctx, perm, st);
     cudaGetLastError();
     return s;
 }

@@ -1,0 +1,10 @@
+mkdir -p gpurun_out/r2c16
+timeout 2000 python -m pytest tests -q -x -m gpu > gpurun_out/r2c16/pytest_gpu.log 2>&1; tail -3 gpurun_out/r2c16/pytest_gpu.log
+for c in c1 c2; do timeout 600 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > gpurun_out/r2c16/bench_$c.log 2>&1; done
+python - <<'PY'
+import json
+for c in ('c1','c2'):
+    for l in open(f'gpurun_out/r2c16/bench_{c}.log'):
+        if l.startswith('{'):
+            d = json.loads(l); print(c, d['ms_per_step'], d['step_ms'], d['phase_ms'], d['kernel_ms_per_step'], d['clocks']['reasons'])
+PY
