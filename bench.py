@@ -1,10 +1,11 @@
 #!/usr/bin/env python
 """bench.py -- Faugere-Lachartre reduction (GBLA, arXiv 1602.06097) on B200.
 
-One STEP = one gbla_reduce over the bench workload (BASELINE.json configs[1]
-= c1, 45,000 x 55,000, p = 65521): splice -> sparse phase (Alg 2, fused
-reduce_C + update_D) -> fully reduced echelon of D, device-resident CSR in,
-device-resident R + rank out.
+One STEP = one gbla_reduce over the bench workload (default BASELINE.json
+configs[2] = c2, 200,000 x 250,000, p = 65521: the largest config that fits
+one GPU with room to spare; --config c1 for the Katsura-12-scale matrix):
+splice -> sparse phase (Alg 2, fused reduce_C + update_D) -> fully reduced
+echelon of D, device-resident CSR in, device-resident R + rank out.
 
 metric  nnz-AXPY Gop/s mod p: exact sparse-phase modMAC count (Alg 2 count,
         equal to the oracle's) / whole-step time.  ms_per_step is the F4
@@ -13,7 +14,7 @@ e2e     the same metric through the C ABI with HOST buffers: pinned-host CSR
         copied in by the library (GBLA_HOST_INPUT) and R + pivcol copied back
         to host, inside the timed region.
 --impl reference   the CPU oracle (oracle/, plain C) on the box's host cores,
-        each step a bounded sample of c1's targets (same metric, unit).
+        each step a bounded sample of the config's targets (same metric, unit).
 
 Multi-GPU (torchrun, N > 1): see DESIGN.md §"Multi-GPU"; one process per GPU.
 """
@@ -145,76 +146,75 @@ def run_reference(args):
 METRIC = "nnz-AXPY Gop/s mod p (F4 matrix reduction, gbla_reduce)"
 
 # kernel families timed by the library (gbla_get_kernel_ms) and how each is bounded
-KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1, tcgen05)", "update": "k_update_tc (K7', D -= C' B, tcgen05)",
-                "panel": "k_panel (K10, panel RREF, one CTA)", "trailing": "k_modgemm_tc<SUB> (K11 trailing update)",
-                "rnew": "k_modgemm_tc<STORE> (K11 new pivot rows)"}
+KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1 block forward substitution, tcgen05)",
+                "update": "k_update_tc (K7', D -= C' B, tcgen05)",
+                "panel": "k_panel2 (K10, panel echelon form, one CTA)",
+                "trailing": "K11 trailing update (k_modgemm_mk2 CTA-pair K = 512 flushes + k_modgemm_ws / "
+                            "k_modgemm_win K = 128 window updates)",
+                "rnew": "k_modgemm_ws<STORE> (K11 new pivot rows)"}
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+INT8_PEAK = os.path.join(ROOT, "profiles", "r02_int8_peak.json")      # scripts/peaks/int8_peak.py on a B200
+IMAD_PEAK = os.path.join(ROOT, "profiles", "r02_imad_peak.json")      # scripts/peaks/imad_peak.cu on a B200
 
 
-def roofline(kms, kwork, peaks, peak_src, sm_count, deferred=False):
-    """Roofline of the dominant kernel family (largest CUDA-event time over
-    the timed steps).  Tensor-core kernels: achieved = algorithmic modMACs x
-    4 u8 MACs (limb split) x 2 ops / kernel time, against the int8 dense peak
-    = 2 x the measured bf16 burst peak (B200 nominal int8:bf16 = 4.5:2.25).
-    The panel (one CTA, INT pipe): achieved = its modMACs / time against the
-    whole GPU's IMAD rate (148 SMs x 64 lanes x max clock)."""
+def _int8_peak(peaks, peak_src):
+    """Dense int8 tensor peak (TOPS): measured torch._int_mm 8192^3 (burst / sustained) if the
+    measurement is committed, else 2 x the measured bf16 peak (nominal int8:bf16 = 2)."""
+    try:
+        m = json.load(open(INT8_PEAK))
+        return float(m["int8_tops_burst"]), float(m["int8_tops_sustained"]), \
+            "measured torch._int_mm int8 8192^3 on a B200 (profiles/r02_int8_peak.json)"
+    except Exception:
+        return 2.0 * float(peaks["bf16_tflops"]), 2.0 * float(peaks["bf16_tflops_sustained"]), \
+            f"2 x {peak_src} bf16 (MEASURED_PEAKS.json; nominal int8:bf16 = 2; int8 not measured)"
+
+
+def _imad_peak(sm_count, sm_mhz):
+    try:
+        m = json.load(open(IMAD_PEAK))
+        return float(m["int_modmac_T_per_s"]), "measured acc += (u64)a*b microbenchmark (profiles/r02_imad_peak.json)"
+    except Exception:
+        return sm_count * 32 * sm_mhz * 1e6 / 1e12, f"derived: {sm_count} SMs x 32 IMAD.WIDE/clk x {sm_mhz:.0f} MHz"
+
+
+def roofline(kms, kwork, peaks, peak_src, sm_count, config):
+    """Roofline of the dominant kernel family (largest CUDA-event time over the timed steps), against
+    WHOLE-GPU peaks.  Tensor-core families: achieved = algorithmic modMACs (gbla_get_kernel_work,
+    DESIGN.md §6) x 4 u8 MACs (limb split) x 2 ops / family time, against the dense int8 peak
+    (the sustained figure: these kernels run inside a long step; burst beside it).  The panel K10
+    (one CTA, INT pipe + mma.sync): modMACs / time against the whole GPU's measured INT-pipe modMAC
+    rate.  traffic = ncu DRAM bytes per launch of that family in a launch list of the SAME config."""
     dom = max(kms, key=lambda k: kms[k][0])
     ms, n = kms[dom]
     work = kwork[dom]
     try:
-        traffic_db = json.load(open(TRAFFIC))
+        tr = json.load(open(TRAFFIC)).get(config, {}).get(dom)
     except Exception:
-        traffic_db = {}
-    tr = traffic_db.get(dom)
+        tr = None
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    if dom == "trailing" and deferred:
-        # super-panels (D >= 4e8 entries: c2-c4): the columns right of the next windows take one
-        # K = 512 update per four panels (1024 u8 ops per byte of D moved, above the int8 ridge
-        # of ~510): the tensor rate bounds it
-        peak = 2.0 * float(peaks["bf16_tflops"])
-        ach = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-        out = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 1), "unit": "TOPS",
-               "peak_source": f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TF/s "
-                              f"(MEASURED_PEAKS.json; nominal int8:bf16 = 2)",
-               "modmac_per_s_T": round(work / (ms / 1e3) / 1e12, 3) if ms > 0 else 0.0,
-               "note": "K11 with deferred (K = 512) updates of the columns beyond the next windows"}
-    elif dom == "trailing" and kwork.get("trailing_elems"):
-        # K11 trailing update: K = 128 (multi-K 512) products into u16 D read-modify-written once per
-        # launch: 128 modMACs x 8 u8 ops per 4 bytes = 256 ops/B < the int8 ridge (3342 TOPS / 6.5 TB/s
-        # ~ 510 ops/B), so HBM bounds it.  Algorithmic bytes = 4 per D entry of the update (u16 read +
-        # write; the A/B operand tiles are L2-resident and not counted).
-        byts = 4.0 * kwork["trailing_elems"]
-        peak = float(peaks["hbm_gbs"])
-        ach = byts / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-        tens = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-        out = {"bound": "hbm", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
-               "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-               "algorithmic_bytes": int(byts), "algorithmic_bytes_per_launch": int(byts / max(n, 1)),
-               "launch_note": "launches = timed K11 trailing launches (window and rest parts of every panel, flushes)",
-               "tensor_TOPS": round(tens, 2), "tensor_frac": round(tens / (2.0 * float(peaks["bf16_tflops"])), 5),
-               "intensity_ops_per_byte": round(work * 8 / byts, 1) if byts else None}
-    elif dom == "panel":
-        # K10 is ONE CTA by design (it runs on the SM the 147-CTA trailing GEMM leaves free, on the
-        # echelon's critical path): its resource is one SM.  peak = that SM's IMAD rate; the
-        # fraction of the whole GPU's rate is given beside it.  The kernel is latency/barrier bound
-        # (ncu: issue-active ~37 %), and part of its work runs on mma.sync (T solve, dense LU).
-        peak = 64 * sm_mhz * 1e6 / 1e12
-        ach = work / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-        out = {"bound": "alu", "achieved": round(ach, 5), "peak": round(peak, 4), "unit": "Tmodmac/s",
-               "peak_source": f"one SM: 64 IMAD/clk x {sm_mhz:.0f} MHz (derived; one modMAC = one IMAD); "
-                              f"the kernel is a single CTA by design",
-               "frac_of_whole_gpu": round(ach / (sm_count * peak), 5) if peak else 0.0}
+    sec = ms / 1e3 if ms > 0 else float("inf")
+    if dom == "panel":
+        peak, src = _imad_peak(sm_count, sm_mhz)
+        ach = work / sec / 1e12
+        out = {"bound": "alu", "achieved": round(ach, 5), "peak": round(peak, 3), "unit": "Tmodmac/s",
+               "peak_source": src + "; the kernel is ONE CTA by design (latency/barrier bound)"}
     else:
-        peak = 2.0 * float(peaks["bf16_tflops"])
-        ach = work * 4 * 2 / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-        out = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 1), "unit": "TOPS",
-               "peak_source": f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TF/s "
-                              f"(MEASURED_PEAKS.json; nominal int8:bf16 = 2)",
-               "modmac_per_s_T": round(work / (ms / 1e3) / 1e12, 3) if ms > 0 else 0.0}
+        burst, sustained, src = _int8_peak(peaks, peak_src)
+        ach = work * 4 * 2 / sec / 1e12
+        out = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(sustained, 1), "unit": "TOPS",
+               "peak_source": src + " (sustained; burst " + f"{burst:.0f})",
+               "frac_of_burst": round(ach / burst, 4) if burst else None,
+               "modmac_per_s_T": round(work / sec / 1e12, 3)}
+        if dom == "trailing" and kwork.get("trailing_elems"):
+            byts = 4.0 * kwork["trailing_elems"]          # u16 read + write per D entry of every update
+            out["hbm_algorithmic_GBs"] = round(byts / sec / 1e9, 1)
+            out["hbm_frac"] = round(byts / sec / 1e9 / float(peaks["hbm_gbs"]), 4)
     out.update({"kernel": KERNEL_NAMES[dom], "frac": round(out["achieved"] / out["peak"], 5) if out["peak"] else 0.0,
                 "kernel_ms_total": round(ms, 3), "launches": n, "algorithmic_modmac": int(work),
+                "algorithmic_modmac_per_launch": int(work / max(n, 1)),
                 "traffic": (tr["dram_bytes_per_launch"] if tr else None),
-                "traffic_source": (f"profiles/{tr['source']} (ncu dram__bytes_read+write per launch)" if tr else None)})
+                "traffic_source": (f"profiles/{tr['source']} ({config} launch list: ncu dram__bytes_read+write per "
+                                   f"launch of the family)" if tr else None)})
     return out
 
 
@@ -238,7 +238,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default="c2", help="BASELINE.json config (c2: the largest single-GPU headline)")
     ap.add_argument("--flags", type=int, default=0, help="gbla_reduce flags")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-targets", type=int, default=384)
@@ -367,8 +367,8 @@ def main():
         peaks, peak_src = _peaks()
         ph = {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]}
         dims = rank_d[0] if rank_d else (0, 0, 0)
-        roof = roofline(kms, kwork, peaks, peak_src, sm_count=torch.cuda.get_device_properties(dev).multi_processor_count,
-                        deferred=float(dims[1]) * float(dims[2]) >= 4e8)
+        roof = roofline(kms, kwork, peaks, peak_src, torch.cuda.get_device_properties(dev).multi_processor_count,
+                        cfg.name)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(cfg.name, M, args.cpu_targets)
@@ -376,8 +376,9 @@ def main():
             "metric": METRIC, "value": round(ops / (ms / 1e3) / 1e9, 4), "unit": "Gop/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8", "dtype_note": "u16 residues split into u8 limbs for tcgen05 kind::i8 (s32 accumulate); "
-                                         "u64 delayed-reduction accumulators on the INT pipe; exact mod p",
+            "dtype": "u16", "dtype_note": "exact arithmetic on u16 residues mod p (no rounding): tensor-core "
+                                          "products on u8 limbs with s32 accumulation, u64 delayed reduction on "
+                                          "the INT pipe",
             "data": "synthetic",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "npiv": cfg.npiv, "p": cfg.p,
                        "density": cfg.density, "band": cfg.band, "rank_planted": cfg.rank_planted,
@@ -385,6 +386,9 @@ def main():
                        "parallelism": (f"{world} GPUs: C1 broadcast of M, target tiles sharded (sparse phase), "
                                        f"row-sharded distributed echelon (NCCL all-reduce / all-gather per "
                                        f"panel, R assembled by broadcasts)") if world > 1 else "1 GPU"},
+            "value_note": "exact sparse-phase (Alg 2) modMAC count / WHOLE gbla_reduce time (splice + sparse phase "
+                          "+ echelon): conservative; SURVEY 8(d)'s sparse-phase-only rate is value_sparse_phase",
+            "value_sparse_phase": round(ops / (statistics.mean(p["reduce_C"] for p in phases) / 1e3) / 1e9, 2),
             "sparse_modmac_per_step": ops, "dense_modmac_per_step": dense_ops,
             "rank_D": rank_d[1], "npiv": rank_d[0][0],
             "phase_ms": ph, "step_ms": [round(x, 3) for x in step_ms],

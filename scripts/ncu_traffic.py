@@ -1,9 +1,11 @@
 #!/usr/bin/env python
-"""Per-kernel DRAM traffic from one `ncu --set full` capture, for bench.py's
-roofline "traffic" field.  Usage (here, no GPU needed):
-    python scripts/ncu_traffic.py gpurun_out/prof.ncu-rep profiles/ncu_traffic.json
-Writes {family: {kernel, dram_bytes_per_launch, duration_ms, tensor_pct,
-launches, source}} averaged over the captured launches of each family."""
+"""Per-kernel-family DRAM traffic for bench.py's roofline "traffic" field, from a
+launch list (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
+dram__bytes_write.sum --csv) or one `ncu --set full` capture of the SAME bench
+config.  Usage (here, no GPU needed):
+    python scripts/ncu_traffic.py <launches.csv | prof.ncu-rep> profiles/ncu_traffic.json <config>
+Merges {config: {family: {kernel, dram_bytes_per_launch, duration_ms_per_launch,
+launches_captured, source}}} into the JSON (other configs are kept)."""
 import csv
 import io
 import json
@@ -11,7 +13,7 @@ import subprocess
 import sys
 
 FAMILIES = [("k_sweep", "sweep"), ("k_update_tc", "update"), ("k_panel", "panel"),
-            ("k_modgemm_tc<0>", "trailing"), ("k_modgemm_tc<1>", "rnew"), ("k_modgemm_ws<0", "trailing"),
+            ("k_modgemm_ws<0", "trailing"), ("k_modgemm_mk2", "trailing"), ("k_modgemm_win", "trailing"),
             ("k_modgemm_ws<1", "rnew")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 TSCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
@@ -50,14 +52,24 @@ def from_launch_list(path, out):
     res = {fam: {"kernel": a["kernel"], "dram_bytes_per_launch": round(a["bytes"] / a["n"]),
                  "duration_ms_per_launch": round(a["ms"] / a["n"], 4), "launches_captured": a["n"],
                  "source": path.split("/")[-1]} for fam, a in acc.items()}
-    json.dump(res, open(out, "w"), indent=1)
-    print(json.dumps(res, indent=1))
+    return res
 
 
 def main():
-    rep, out = sys.argv[1], sys.argv[2]
-    if rep.endswith(".csv"):
-        return from_launch_list(rep, out)
+    rep, out, cfg = sys.argv[1], sys.argv[2], sys.argv[3]
+    res = from_launch_list(rep, out) if rep.endswith(".csv") else from_capture(rep)
+    try:
+        db = json.load(open(out))
+    except Exception:
+        db = {}
+    if db and not all(isinstance(v, dict) and "kernel" not in v for v in db.values()):
+        db = {}                                        # an old single-config file
+    db[cfg] = res
+    json.dump(db, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+def from_capture(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -85,8 +97,7 @@ def main():
                     "duration_ms_per_launch": round(a["ms"] / a["n"], 4),
                     "tensor_pipe_pct_of_active": round(sum(a["tensor"]) / len(a["tensor"]), 2) if a["tensor"] else None,
                     "launches_captured": a["n"], "source": rep.split("/")[-1]}
-    json.dump(res, open(out, "w"), indent=1)
-    print(json.dumps(res, indent=1))
+    return res
 
 
 if __name__ == "__main__":

@@ -259,4 +259,38 @@ def test_validate_rejects_bad_input():
     assert oracle.validate(bad) != 0
     assert oracle.validate(gbla_gen.CSR(2, 2, 8, M.row_ptr, M.col, M.val)) != 0   # 8 not prime
     badv = M.val.copy(); badv[0] = 7
-    assert oracle.validate(gbla_gen.CSR(2, 2, 7, M.row_ptr, M.col, badv)) != 0
+    assert oracle.validate(gbla_gen.CSR(2, 2, 7, M.row_ptr, M.col, badv)) == 4         # val >= p
+    zero = M.val.copy(); zero[1] = 0
+    assert oracle.validate(gbla_gen.CSR(2, 2, 7, M.row_ptr, M.col, zero)) == 4         # explicit zero
+    wide = M.col.copy(); wide[-1] = 2
+    assert oracle.validate(gbla_gen.CSR(2, 2, 7, M.row_ptr, wide, M.val)) == 3         # col >= n
+    assert oracle.validate(bad) == 3                                                    # unsorted columns
+    assert oracle.validate(gbla_gen.CSR(2, 2, 7, np.array([0, 2, 3], np.uint64), np.array([0, 0, 1], np.uint32),
+                                        np.array([1, 2, 3], np.uint16))) == 3       # duplicate column
+    assert oracle.validate(gbla_gen.CSR(2, 2, 7, np.array([0, 2, 1], np.uint64), M.col, M.val)) == 2   # row_ptr
+    with pytest.raises(ValueError):
+        oracle.splice(gbla_gen.CSR(2, 2, 7, M.row_ptr, M.col, zero))
+
+
+def test_modmac_count_hand_derived():
+    """The sparse-phase modMAC count (the numerator of the bench metric) on hand-worked Alg 2 runs
+    (reading R8/R9: lambda captured before use, subtract lambda * row_j, count
+    nnz(row_j) - 1 per nonzero lambda), not by re-typing the oracle's formula."""
+    # SPEC tie example [[1,2],[1,3]] mod 7: pivot row 0 (equal weights, lower id); the target
+    # [1,3] takes lambda = 1 once against a 2-entry row: 1 modMAC, D_new = [3 - 2] = [1]
+    R = oracle.reduce(csr_from_dense([[1, 2], [1, 3]], 7))
+    assert R.modmac == 1 and R.dnew.tolist() == [[1]]
+    # three pivots, p = 7, pivot rows r0 = [1,2,0,0,1], r1 = [0,1,3,0,0], r2 = [0,0,1,4,0]; target
+    # t = [1,1,1,1,1]: lambda_0 = 1 -> t = [0,6,1,1,0] (+2), lambda_1 = 6 -> [0,0,4,1,0] (+1),
+    # lambda_2 = 4 -> [0,0,0,6,0] (+1): 4 modMACs, D_new = [6, 0]
+    rows = [[1, 2, 0, 0, 1], [0, 1, 3, 0, 0], [0, 0, 1, 4, 0]]
+    R = oracle.reduce(csr_from_dense(rows + [[1, 1, 1, 1, 1]], 7))
+    assert R.splice.npiv == 3 and R.modmac == 4 and R.dnew.tolist() == [[6, 0]]
+    assert R.rank == 1 and R.R.tolist() == [[1, 0]] and R.rank_M == 4
+    # a zero lambda is skipped (no count): t = [1,2,6,0,1] -> [0,0,6,0,0] (+2), lambda_1 = 0,
+    # lambda_2 = 6 -> [0,0,0,4,0] (+1): 3 modMACs, D_new = [4, 0]
+    R = oracle.reduce(csr_from_dense(rows + [[1, 2, 6, 0, 1]], 7))
+    assert R.modmac == 3 and R.dnew.tolist() == [[4, 0]]
+    # both targets together: counts add, rows independent
+    R = oracle.reduce(csr_from_dense(rows + [[1, 1, 1, 1, 1], [1, 2, 6, 0, 1]], 7))
+    assert R.modmac == 7 and R.dnew.tolist() == [[6, 0], [4, 0]] and R.rank == 1
