@@ -98,7 +98,14 @@ typedef size_t (*gbla_memq_fn)(void *user);
 gbla_status gbla_ctx_set_mem_query(gbla_ctx ctx, gbla_memq_fn fn, void *user);
 /* Multi-GPU: join an NCCL communicator built from a 128-byte ncclUniqueId
  * shared by the caller (e.g. through torch.distributed), as `rank` of
- * `world`.  Collective: every rank must call it.  world == 1 detaches. */
+ * `world`.  Collective: every rank must call it.  nccl_unique_id == NULL
+ * (world 1) detaches; world == 1 WITH an id builds a one-rank communicator:
+ * the distributed code path (C1 broadcast, sharded sparse phase, distributed
+ * echelon) and every NCCL call in it then run on one GPU (tests).  Input
+ * errors found by rank 0 are returned by every rank (they travel with the
+ * C1 dims broadcast); asynchronous NCCL errors are polled
+ * (ncclCommGetAsyncError) at every host wait of a distributed phase, abort the
+ * communicator and return GBLA_E_NCCL. */
 gbla_status gbla_ctx_set_comm(gbla_ctx ctx, const void *nccl_unique_id, int rank, int world);
 /* Fill out128 with a fresh ncclUniqueId (call on one rank, broadcast it). */
 gbla_status gbla_nccl_get_unique_id(void *out128);

@@ -207,8 +207,9 @@ class Context:
             self._memq_cb = _MEMQ_FN(_memq)
             _check(L.gbla_ctx_set_mem_query(self._h, self._memq_cb, None))
 
-    def set_comm(self, unique_id: bytes, rank: int, world: int):
-        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    def set_comm(self, unique_id, rank: int, world: int):
+        """gbla_ctx_set_comm; unique_id None detaches (world 1)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128) if unique_id is not None else None
         _check(_lib.gbla_ctx_set_comm(self._h, buf, rank, world))
 
     def close(self):

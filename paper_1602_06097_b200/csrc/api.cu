@@ -15,18 +15,22 @@ static std::atomic<unsigned long long> g_launches{0};
 
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
+// timing events, pooled per device (an event belongs to the device that was current when it was created)
 static std::mutex g_ev_mu;
-static std::vector<cudaEvent_t> g_ev_pool;
+static std::vector<std::pair<int, cudaEvent_t>> g_ev_pool;
 
 cudaEvent_t kt_event_get()
 {
+    int dev = 0;
+    cudaGetDevice(&dev);
     {
         std::lock_guard<std::mutex> lk(g_ev_mu);
-        if (!g_ev_pool.empty()) {
-            cudaEvent_t e = g_ev_pool.back();
-            g_ev_pool.pop_back();
-            return e;
-        }
+        for (size_t i = g_ev_pool.size(); i-- > 0;)
+            if (g_ev_pool[i].first == dev) {
+                cudaEvent_t e = g_ev_pool[i].second;
+                g_ev_pool.erase(g_ev_pool.begin() + i);
+                return e;
+            }
     }
     cudaEvent_t e = nullptr;
     if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
@@ -35,8 +39,10 @@ cudaEvent_t kt_event_get()
 
 void kt_event_put(cudaEvent_t e)
 {
+    int dev = 0;
+    cudaGetDevice(&dev);                  // callers return events on the device they were taken on
     std::lock_guard<std::mutex> lk(g_ev_mu);
-    g_ev_pool.push_back(e);
+    g_ev_pool.push_back({dev, e});
 }
 
 extern "C" uint64_t gbla_kernel_launches(void) { return g_launches.load(); }
@@ -275,17 +281,20 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
         return GBLA_E_DOMAIN;
     }
     // with a communicator the splice is collective: rank 0's M is broadcast (C1)
-    const bool dist = ctx->world > 1 && ctx->nccl_comm;
+    const bool dist = ctx->nccl_comm != nullptr;
+    // rank 0's verdict on M travels with the dims broadcast, so every rank returns the same error
+    // instead of the other ranks waiting forever in the collective
+    gbla_status vs = GBLA_OK;
     if (!dist || ctx->rank == 0) {
         if (M->m < 0 || M->n < 0 || M->nnz < 0 || M->m >= (1ll << 31) || M->n >= (1ll << 31)) {
             set_error("gbla_splice: bad dimensions m=%lld n=%lld nnz=%lld", (long long)M->m, (long long)M->n,
                       (long long)M->nnz);
-            return GBLA_E_INVAL;
-        }
-        if (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))) {
+            vs = GBLA_E_INVAL;
+        } else if (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))) {
             set_error("gbla_splice: NULL CSR array");
-            return GBLA_E_INVAL;
+            vs = GBLA_E_INVAL;
         }
+        if (vs != GBLA_OK && !dist) return vs;
     }
     GBLA_CUDA_TRY(cudaSetDevice(ctx->device));
     gbla_mat h = new gbla_mat_s();
@@ -298,7 +307,7 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     gbla_status s;
     if (dist) {
         gbla_csr dm;
-        s = dist_bcast_input(h, M, (flags & GBLA_HOST_INPUT) != 0, &dm);
+        s = dist_bcast_input(h, M, (flags & GBLA_HOST_INPUT) != 0, &dm, vs);
         if (s == GBLA_OK) {
             h->m = dm.m; h->n = dm.n; h->nnz = dm.nnz;
             s = splice_impl(h, &dm, 0);
@@ -402,7 +411,7 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     gbla_mat h = nullptr;
     GBLA_TRY(gbla_splice(ctx, M, p, flags & GBLA_HOST_INPUT, stream, &h));
     gbla_status s;
-    const bool dist = (ctx->world > 1 && ctx->nccl_comm) || dist_emulated_world() > 1;
+    const bool dist = ctx->nccl_comm != nullptr || dist_emulated_world() > 1;
     // (the INT-pipe echelon is single-GPU only: with GBLA_DENSE_INT every rank reduces the whole D)
     if (dist && !(flags & (GBLA_ORDER_STANDARD | GBLA_SPARSE_INT | GBLA_KEEP_CPRIME | GBLA_DENSE_INT))) {
         // multi-GPU (dist.cu): row-sharded tensor-core sparse phase + D_new all-gather

@@ -40,6 +40,25 @@
 
 void band_release(gbla_mat h);
 gbla_status tc_shard(gbla_mat h, int prank, int pworld);
+
+// Asynchronous NCCL failures (a peer died, a network error) surface only through
+// ncclCommGetAsyncError: polled at every point where the host waits for a distributed phase.
+// On an error the communicator is aborted (every pending collective returns) and the call fails.
+gbla_status dist_check_async(gbla_ctx ctx)
+{
+    if (!ctx->nccl_comm) return GBLA_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError((ncclComm_t)ctx->nccl_comm, &ar);
+    if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+        set_error("NCCL asynchronous error: %s", ncclGetErrorString(r != ncclSuccess ? r : ar));
+        ncclCommAbort((ncclComm_t)ctx->nccl_comm);
+        ctx->nccl_comm = nullptr;
+        ctx->world = 1;
+        ctx->rank = 0;
+        return GBLA_E_NCCL;
+    }
+    return GBLA_OK;
+}
 gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2]);
 int64_t tc_ntiles(gbla_mat h);
 unsigned long long *tc_ops_dev(gbla_mat h);
@@ -57,7 +76,9 @@ void dist_destroy(gbla_ctx ctx)
 gbla_status dist_set_comm(gbla_ctx ctx, const void *id, int rank, int world)
 {
     dist_destroy(ctx);
-    if (world == 1) return GBLA_OK;
+    if (!id) return GBLA_OK;                  // detach
+    // world == 1 with an id: a one-rank communicator, so the distributed code path (row-sharded
+    // sparse phase, distributed echelon) and every NCCL call in it run on one GPU (tests)
     ncclUniqueId uid;
     static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
     memcpy(&uid, id, sizeof uid);
@@ -90,18 +111,25 @@ int dist_emulated_world()
 
 // C1: broadcast rank 0's CSR (device or host arrays) to every rank; returns a
 // device CSR view valid on this rank (owned by h).
-gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out)
+gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out, gbla_status root_ok)
 {
     gbla_ctx ctx = h->ctx;
     ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
     cudaStream_t st = h->stream;
     int64_t *ddims;
     GBLA_TRY(dalloc_t(h, 4, &ddims));
-    int64_t hd[4] = {M->m, M->n, M->nnz, 0};
+    // hd[3]: rank 0's validation status of M (every rank returns it)
+    int64_t hd[4] = {ctx->rank == 0 ? M->m : 0, ctx->rank == 0 ? M->n : 0, ctx->rank == 0 ? M->nnz : 0,
+                     ctx->rank == 0 ? (int64_t)root_ok : 0};
     GBLA_CUDA_TRY(cudaMemcpyAsync(ddims, hd, 32, cudaMemcpyHostToDevice, st));
     GBLA_NCCL_TRY(ncclBroadcast(ddims, ddims, 4, ncclInt64, 0, comm, st));
     GBLA_CUDA_TRY(cudaMemcpyAsync(hd, ddims, 32, cudaMemcpyDeviceToHost, st));
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    GBLA_TRY(dist_check_async(ctx));
+    if (hd[3] != GBLA_OK) {
+        if (ctx->rank != 0) set_error("gbla_splice: rank 0 rejected the input matrix (status %lld)", (long long)hd[3]);
+        return (gbla_status)hd[3];
+    }
     const int64_t m = hd[0], n = hd[1], nnz = hd[2];
     uint64_t *rp;
     uint32_t *col;
@@ -135,7 +163,7 @@ gbla_status dist_sparse_phase(gbla_mat h)
 {
     gbla_ctx ctx = h->ctx;
     cudaStream_t st = h->stream;
-    const bool real = ctx->world > 1 && ctx->nccl_comm;
+    const bool real = ctx->nccl_comm != nullptr;
     const int G = real ? ctx->world : dist_emulated_world();
     const int me = real ? ctx->rank : 0;
     if (h->mN == 0 || h->npiv == 0) return GBLA_OK;   // D_new = D on every rank
@@ -156,6 +184,8 @@ gbla_status dist_sparse_phase(gbla_mat h)
     }
     GBLA_TRY(tc_read_ops(h, ops));
     h->sparse_ops = ops[0] + ops[1];
+    GBLA_TRY(sweep_dev_err(st, "gbla_reduce (sharded sparse phase)"));
+    if (real) GBLA_TRY(dist_check_async(ctx));
     // D_new stays row-sharded: the echelon is distributed (panel.cu: panels_dist)
     return GBLA_OK;
 }

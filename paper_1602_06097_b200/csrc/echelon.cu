@@ -606,10 +606,10 @@ __global__ void k_compact(int64_t nN, int64_t cbase, const uint32_t *__restrict_
 template <int PK>
 gbla_status set_panel_smem()
 {
-    static bool done = false;
-    if (!done) {
+    static unsigned long long done = 0;   // devices done (dev_bit)
+    if (!(done & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<PK>()));
-        done = true;
+        done |= dev_bit();
     }
     return GBLA_OK;
 }
@@ -666,20 +666,28 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
     k_invtab<<<grid_for(h->p, 256), 256, 0, st>>>(h->F, invtab);
     note_launch();
     // row-sharded D (multi-GPU, or emulated ranks): the distributed echelon assembles R itself
-    const bool real = h->ctx->world > 1 && h->ctx->nccl_comm;
+    const bool real = h->ctx->nccl_comm != nullptr;
     const int G = real ? h->ctx->world : dist_emulated_world();
-    if (h->dist_rows && G > 1) {
+    if (h->dist_rows && (real || G > 1)) {
         if (flags & GBLA_DENSE_INT) {
             // a row-sharded D holds only this rank's updated rows: the single-GPU INT engine would
             // echelon a partly updated D and give every rank a different (wrong) R
             set_error("gbla_echelon_D: GBLA_DENSE_INT is single-GPU only (D is row-sharded)");
             return GBLA_E_INVAL;
         }
-        if (mN > 0 && nN > 0) return panels_dist(h, rowpiv, dops, invtab, G, real ? h->ctx->rank : 0, real);
+        if (mN > 0 && nN > 0) {
+            const gbla_status ds = panels_dist(h, rowpiv, dops, invtab, G, real ? h->ctx->rank : 0, real);
+            if (real) GBLA_TRY(dist_check_async(h->ctx));          // a peer's failure first
+            GBLA_TRY(ds);
+            GBLA_TRY(panel_dev_err(st, "gbla_echelon_D"));
+            return tcgemm_dev_err(st, "gbla_echelon_D");
+        }
     }
     if (mN > 0 && nN > 0) {
         if (flags & GBLA_DENSE_INT) GBLA_TRY(panels_int(h, rowpiv, dops, invtab));
         else GBLA_TRY(panels_tc2(h, rowpiv, dops, invtab));
+        GBLA_TRY(panel_dev_err(st, "gbla_echelon_D"));
+        GBLA_TRY(tcgemm_dev_err(st, "gbla_echelon_D"));
     }
     // K13: compaction
     GBLA_TRY(dalloc_t(h, nN + 1, &colrow));

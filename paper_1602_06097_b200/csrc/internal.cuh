@@ -73,6 +73,35 @@ __device__ __forceinline__ uint32_t finv(uint32_t a, const Field &F) {
 }
 __device__ __forceinline__ uint32_t fneg(uint32_t a, const Field &F) { return a ? F.p - a : 0; }
 
+// ------------------------------------------------------------------ device errors
+// Bounded spin-waits on inter-CTA flags (flags published by other CTAs of a persistent kernel, or
+// by a kernel on another stream) must never hang the GPU nor continue silently: on a timeout they
+// latch a code into the device error word of their translation unit and stop waiting; the host
+// reads and clears the word when the phase ends and fails the call with GBLA_E_INTERNAL (the
+// result is discarded).  GBLA_DEV_ERR_UNIT(fn) defines the word and the host check `fn`.
+enum { DEVERR_GATHER_WAIT = 1, DEVERR_WIN_FLAG = 2, DEVERR_WIN_BARRIER = 4, DEVERR_SWEEP_FLAG = 8 };
+#define GBLA_DEV_ERR_UNIT(fn)                                                                      \
+    static __device__ uint32_t g_dev_err = 0;                                                      \
+    static __device__ __forceinline__ void dev_err_latch(uint32_t code) { atomicOr(&g_dev_err, code); } \
+    gbla_status fn(cudaStream_t st, const char *where)                                             \
+    {                                                                                              \
+        uint32_t v = 0;                                                                            \
+        if (cudaMemcpyFromSymbolAsync(&v, g_dev_err, 4, 0, cudaMemcpyDeviceToHost, st) != cudaSuccess || \
+            cudaStreamSynchronize(st) != cudaSuccess) {                                            \
+            set_error("%s: reading the device error word: %s", where, cudaGetErrorString(cudaGetLastError())); \
+            return GBLA_E_CUDA;                                                                    \
+        }                                                                                          \
+        if (!v) return GBLA_OK;                                                                    \
+        const uint32_t z = 0;                                                                      \
+        cudaMemcpyToSymbolAsync(g_dev_err, &z, 4, 0, cudaMemcpyHostToDevice, st);                 \
+        cudaStreamSynchronize(st);                                                                 \
+        set_error("%s: an inter-CTA wait timed out on the device (code 0x%x); result discarded", where, v); \
+        return GBLA_E_INTERNAL;                                                                    \
+    }
+gbla_status panel_dev_err(cudaStream_t st, const char *where);
+gbla_status tcgemm_dev_err(cudaStream_t st, const char *where);
+gbla_status sweep_dev_err(cudaStream_t st, const char *where);
+
 // ------------------------------------------------------------------ launches
 // Host-side count of libgbla kernel launches (bench.py reports it).
 void note_launch(int n = 1);
@@ -249,8 +278,9 @@ static inline void kt_mark2(gbla_mat h, int a, int b, cudaStream_t s)
     h->kt.ev[b].push_back(e);
 }
 // multi-GPU (dist.cu)
-gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out);
+gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out, gbla_status root_ok);
 gbla_status dist_sparse_phase(gbla_mat h);
+gbla_status dist_check_async(gbla_ctx ctx);      // ncclCommGetAsyncError (aborts the comm on error)
 int dist_emulated_world();
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
 
@@ -280,6 +310,15 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
                            uint8_t *Rlo2 = nullptr, uint8_t *Rhi2 = nullptr);
 
+
+// one-time per-device setup (function attributes): a bit per device ordinal, so a second context on
+// another GPU of the same process sets them again
+static inline unsigned long long dev_bit()
+{
+    int d = 0;
+    cudaGetDevice(&d);
+    return 1ull << (d & 63);
+}
 
 static inline unsigned grid_for(int64_t work, int per_block) {
     int64_t g = (work + per_block - 1) / per_block;

@@ -42,6 +42,8 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
+GBLA_DEV_ERR_UNIT(panel_dev_err)
+
 namespace {
 
 // launch with programmatic dependent launch (the kernel calls pdl_trigger / pdl_wait): its launch
@@ -1184,7 +1186,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
             for (uint32_t it = 0;; it++) {
                 uint32_t v;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&ps->ready) : "memory");
-                if (v == epoch || it > (1u << 24)) break;          // bounded: never hang the GPU
+                if (v == epoch) break;
+                if (it > (1u << 24)) { dev_err_latch(DEVERR_GATHER_WAIT); break; }   // bounded: never hang
                 __nanosleep(128);
             }
         }
@@ -1695,10 +1698,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     }
     GBLA_TRY(dalloc_t(h, (size_t)PK * ldR, &Rn));
     GBLA_TRY(dalloc(h, 2 * sizeof(P2State), (void **)&ps));
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices done (dev_bit)
+    if (!(attr & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
-        attr = true;
+        attr |= dev_bit();
     }
     unsigned long long *trace = nullptr;
     if (getenv("GBLA_PANEL_TRACE")) {
@@ -2119,10 +2122,10 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
     int64_t gcap = 0;
     gl = gr = nullptr;
     gv = nullptr;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices done (dev_bit)
+    if (!(attr & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_panel2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
-        attr = true;
+        attr |= dev_bit();
     }
     uint32_t *hpin = (uint32_t *)ctx_pinned(h->ctx, (8 + (size_t)G) * 4);   // width info, candidate counts
     if (!hpin) { set_error("pinned host scratch"); return GBLA_E_CUDA; }
@@ -2239,7 +2242,10 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
     }
     if (status != GBLA_OK) return status;
     // op counts: the trailing updates were split over the ranks
-    if (real) GBLA_TRY(dist_allreduce_u64(h, dops, 1));
+    if (real) {                      // dops[1], dops[2] (Rn, panel) are identical on every rank
+        GBLA_TRY(dist_allreduce_u64(h, dops, 1));
+        GBLA_TRY(dist_allreduce_u64(h, dops + 3, 1));
+    }
     // ---- R: pivot-column lists of every rank, then every rank's pivot rows in pivot order
     uint32_t *colrow, *oflag, *oidx, *gflag, *gidx, *pcs;
     GBLA_TRY(dalloc_t(h, nN + 1, &colrow));

@@ -33,6 +33,8 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
+GBLA_DEV_ERR_UNIT(sweep_dev_err)
+
 struct BandTiles {
     int64_t NB = 0, NNB = 0, ntiles = 0;
     int64_t nA = 0, nB = 0;
@@ -384,7 +386,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
             tc::bulk_g2s(sb, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);   // Â_IJ
             // X_I[T] is produced by task (li, I): wait until it is published
             if (ld_acquire(fl + I) == 0) {
-                while (ld_acquire(fl + I) == 0) __nanosleep(32);
+                // every CTA is resident (cooperative launch) and tasks are claimed in dependency
+                // order, so X_I is on its way; bounded all the same (never hang the GPU)
+                for (uint32_t it = 0; ld_acquire(fl + I) == 0; it++) {
+                    __nanosleep(32);
+                    if (it > (1u << 26)) { dev_err_latch(DEVERR_SWEEP_FLAG); break; }
+                }
             }
             fence_proxy_async_global();
             tc::bulk_g2s(sa, Xrow + (size_t)I * TB, TB, &full[s]);
@@ -801,10 +808,10 @@ static gbla_status pair_tiles(gbla_mat h, const std::vector<uint32_t> &amax, con
     if (!ti.empty()) k_tile_t<<<(unsigned)(ti.size() / 2), 256, 0, st>>>(d + tp.size(), (int64_t)ti.size() / 2, bt->invT, invTT);
     note_launch(2);
     if (!tasks.empty()) {
-        static bool attr = false;
-        if (!attr) {
+        static unsigned long long attr = 0;   // devices done (dev_bit)
+        if (!(attr & dev_bit())) {
             GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB));
-            attr = true;
+            attr |= dev_bit();
         }
         const int64_t nt = (int64_t)tasks.size();
         const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
@@ -897,10 +904,10 @@ static gbla_status band_build(gbla_mat h)
                                                           bt->bmin, bt->tilesA, bt->tilesB);
     if (NB * 128 > npiv) k_band_pad<<<1, 128, 0, st>>>(npiv, NB, bt->offA, bt->tilesA);
     {
-        static bool attr = false;
-        if (!attr) {
+        static unsigned long long attr = 0;   // devices done (dev_bit)
+        if (!(attr & dev_bit())) {
             GBLA_CUDA_TRY(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, DIAG_SMEM));
-            attr = true;
+            attr |= dev_bit();
         }
     }
     k_diag_inv<<<(unsigned)NB, 128, DIAG_SMEM, st>>>(h->F, bt->offA, bt->tilesA, bt->invT);
@@ -915,10 +922,10 @@ static gbla_status band_build(gbla_mat h)
             uint64_t *dtl;
             GBLA_TRY(dalloc_t(h, tl.size(), &dtl));
             GBLA_CUDA_TRY(cudaMemcpyAsync(dtl, tl.data(), tl.size() * 8, cudaMemcpyHostToDevice, st));
-            static bool attr2 = false;
-            if (!attr2) {
+            static unsigned long long attr2 = 0;   // devices done (dev_bit)
+            if (!(attr2 & dev_bit())) {
                 GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB));
-                attr2 = true;
+                attr2 |= dev_bit();
             }
             const int64_t nt = (int64_t)tl.size();
             const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
@@ -1038,10 +1045,10 @@ static gbla_status tc_update_batch(gbla_mat h, int prank, int pworld, int64_t i0
     BandTiles *bt = h->bt;
     const int64_t nl = i1 - i0;
     if (bt->NB == 0 || bt->NNB == 0 || nl <= 0) return GBLA_OK;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices done (dev_bit)
+    if (!(attr & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM));
-        attr = true;
+        attr |= dev_bit();
     }
     UpdArgs a;
     a.mN = h->mN; a.npiv = h->npiv; a.nN = h->nN; a.NB = bt->NB; a.F = h->F;
@@ -1140,6 +1147,7 @@ gbla_status reduce_c_tc(gbla_mat h, bool want_x16, bool fused)
     if (fused) band_release(h);
     unsigned long long ops[2];
     GBLA_TRY(tc_read_ops(h, ops));
+    GBLA_TRY(sweep_dev_err(h->stream, "gbla_reduce_C"));
     h->sparse_ops += ops[0] + (fused ? ops[1] : 0);
     h->kwork[KT_SWEEP] = ops[0];
     if (fused) h->kwork[KT_UPDATE] = ops[1];

@@ -34,6 +34,8 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
+GBLA_DEV_ERR_UNIT(tcgemm_dev_err)
+
 namespace {
 
 constexpr int BM = 128, BN = 64, KP = 128;
@@ -941,7 +943,7 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
                     const uint32_t *fl = g.flags + (ct - w0);
                     for (uint32_t it = 0; ld_acq(fl) != g.epoch; it++) {
                         __nanosleep(64);
-                        if (it > (1u << 24)) break;          // never hang the GPU (a test would fail)
+                        if (it > (1u << 24)) { dev_err_latch(DEVERR_WIN_FLAG); break; }   // never hang the GPU
                     }
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
@@ -1098,7 +1100,7 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
         const uint32_t target = g.epoch * gridDim.x;
         for (uint32_t it = 0; ld_acq(g.flags + 63) < target; it++) {
             __nanosleep(64);
-            if (it > (1u << 24)) break;        // never hang the GPU (a test would fail)
+            if (it > (1u << 24)) { dev_err_latch(DEVERR_WIN_BARRIER); break; }   // never hang the GPU
         }
     }
     __syncthreads();
@@ -1218,11 +1220,11 @@ __global__ void k_fill_res(uint16_t *__restrict__ p, size_t n, uint32_t prime, u
 template <int MODE, int EPIW, bool PF2, bool MK = false>
 gbla_status set_attr()
 {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices done (dev_bit)
+    if (!(attr & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_ws<MODE, EPIW, PF2, MK>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem(MK)));
-        attr = true;
+        attr |= dev_bit();
     }
     return GBLA_OK;
 }
@@ -1282,10 +1284,10 @@ static bool use_pair()
 
 static gbla_status launch_pair(const MMArgs &a, int64_t max_rows, int64_t cols, int64_t grid, cudaStream_t st)
 {
-    static bool attr2 = false;
-    if (!attr2) {
+    static unsigned long long attr2 = 0;   // devices done (dev_bit)
+    if (!(attr2 & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_mk2, cudaFuncAttributeMaxDynamicSharedMemorySize, PR_SMEM));
-        attr2 = true;
+        attr2 |= dev_bit();
     }
     const int64_t ptiles = ((max_rows + 2 * BM - 1) / (2 * BM)) * ((cols + PR_NP - 1) / PR_NP);
     int64_t pairs = grid / 2;
@@ -1393,10 +1395,10 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
                            uint8_t *Rlo2, uint8_t *Rhi2)
 {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices done (dev_bit)
+    if (!(attr & dev_bit())) {
         GBLA_CUDA_TRY(cudaFuncSetAttribute(k_modgemm_win, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM));
-        attr = true;
+        attr |= dev_bit();
     }
     WinArgs a{F, Tlo, Thi, Bglo, Bghi, Rlo, Rhi, Rlo2, Rhi2, Flo, Fhi, rows, sel, nrows_dev, kp_dev, c0_dev, win_dev,
               win_w, cols, D, ldD, flags, epoch, lead, rowpiv, mN};

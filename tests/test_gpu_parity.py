@@ -457,6 +457,39 @@ def test_echelon_ref_mode(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     monkeypatch.delenv("GBLA_DIST_EMULATE")
 
 
+def test_one_rank_nccl_communicator(gb, monkeypatch):
+    """The real multi-GPU code path on one GPU (a one-rank NCCL communicator, gbla_ctx_set_comm with
+    world 1): C1 broadcast of M, the row-sharded sparse phase with the op-count all-reduce, the
+    distributed echelon (lead-count all-reduce, candidate all-gather, pivot-row all-reduce, R by
+    broadcasts) -- every ncclBroadcast / ncclAllGather / ncclAllReduce call site runs with its real
+    buffers, counts and types.  R, rank and op counts against the oracle; REF mode too; then
+    detach and reduce again on the single-GPU path."""
+    ctx1 = gb.Context(0)
+    ctx1.set_comm(gb.nccl_unique_id(), 0, 1)
+    cases = [gbla_gen.f4_matrix("c0")]
+    for name, sc in (("c1", 0.05), ("c3", 0.03), ("c2", 0.02)):
+        cases.append(gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc)))
+    for M in cases:
+        res = oracle.reduce(M)
+        h = gpu_reduce(gb, ctx1, M)
+        r, pc, R = h.rref()
+        assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R), M.name
+        assert h.opcount()[0] == res.modmac
+        h.free()
+    h = gpu_reduce(gb, ctx1, cases[1], flags=gb.GBLA_ECHELON_REF)
+    check_ref(gb, h, oracle.reduce(cases[1]), cases[1].p)
+    h.free()
+    # the INT-pipe echelon is single-GPU: with a communicator gbla_reduce keeps D whole on every rank
+    h = gpu_reduce(gb, ctx1, cases[0], flags=gb.GBLA_DENSE_INT)
+    r, pc, R = h.rref()
+    res0 = oracle.reduce(cases[0])
+    assert r == res0.rank and np.array_equal(np_(R), res0.R)
+    h.free()
+    ctx1.set_comm(None, 0, 1)
+    check_full(gb, ctx1, cases[0], oracle.reduce(cases[0], want_x=True))
+    ctx1.close()
+
+
 def test_super_panels_rref_exact(gb, ctx, monkeypatch):
     """The default echelon schedule of c2-c4 (GBLA_SP = 4 panels per super-panel: per-panel updates
     left of the deferred columns, one K = 512 multi-K flush per super-panel over the rows whose
