@@ -245,6 +245,35 @@ def reduce(M, want_x: bool = False, threads: int | None = None) -> Result:
     return Result(S, dn, rank, R, pc, int(ops.sum()), x)
 
 
+def full_rref(M, res: Result | None = None, threads: int | None = None):
+    """the fully reduced row echelon form of the WHOLE M in its original column
+    order, by the paper's route: Step 2 B' = A^-1 B (orc_trsm), the second
+    reduction of the pivot rows by R, B'' = B' - B'[:, pivcol(R)] R (orc_sub_mul), and
+    Step 5: the columns back in the original order, rows sorted by pivot column.  The
+    pivot rows become [1 at their pivot column | B''] and the R rows [0 | R].
+    Returns (rank(M), RREF(M) as a dense u16 array rank(M) x n, pivot columns u32[rank(M)]).
+    Small inputs only (dense quadrants).  Pinned by the textbook Gauss-Jordan RREF of M
+    (tests/pins.py brute_rref) -- the RREF is unique."""
+    if res is None:
+        res = reduce(M, threads=threads)
+    S = res.splice
+    p = M.p
+    A, B, _, _ = quadrants(M, S)
+    Bp = trsm(A, B, p)                                                     # Step 2
+    Bpp = sub_mul(Bp, Bp[:, res.pivcol.astype(np.int64)], res.R.astype(np.uint32), p) if res.rank else Bp
+    inv_sigma = np.empty(M.n, np.int64)                                   # sigma index -> original column
+    inv_sigma[S.sigma.astype(np.int64)] = np.arange(M.n)
+    pcol, ncol = inv_sigma[:S.npiv], inv_sigma[S.npiv:]
+    rank_M = S.npiv + res.rank
+    out = np.zeros((rank_M, M.n), np.uint16)
+    piv = np.concatenate([pcol, ncol[res.pivcol.astype(np.int64)]]).astype(np.int64)
+    out[np.arange(S.npiv), pcol] = 1                                       # Step 5: original columns
+    out[:S.npiv, ncol] = Bpp
+    out[S.npiv:, ncol] = res.R
+    order = np.argsort(piv, kind="stable")                                 # rows by pivot column
+    return rank_M, out[order], piv[order].astype(np.uint32)
+
+
 def rref_digest(rank: int, nN: int, pivcol: np.ndarray, R: np.ndarray) -> str:
     """SHA-256 of LE bytes (u32 rank, u32 nN, u32 pivcol[rank], u16 R row-major)."""
     h = hashlib.sha256()

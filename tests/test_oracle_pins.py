@@ -294,3 +294,23 @@ def test_modmac_count_hand_derived():
     # both targets together: counts add, rows independent
     R = oracle.reduce(csr_from_dense(rows + [[1, 1, 1, 1, 1], [1, 2, 6, 0, 1]], 7))
     assert R.modmac == 7 and R.dnew.tolist() == [[6, 0], [4, 0]] and R.rank == 1
+
+
+def test_full_rref_of_M_against_textbook_gauss_jordan(c0_matrix, c0_oracle):
+    """f2: the paper's route to RREF(M) in the original column order (B' = A^-1 B,
+    B'' = B' - B'[:, pivcol] R, Step 5 re-arrangement) equals the textbook Gauss-Jordan RREF of M
+    (unique) on the random suite, on matrices whose pivot rows are reduced by R, and on c0."""
+    from pins import brute_rref
+    cases = list(gbla_gen.random_suite(120, seed0=33))
+    cases.append(c0_matrix)
+    for M in cases:
+        dense = np.zeros((M.m, M.n), np.int64)
+        for i in range(M.m):
+            s, e = int(M.row_ptr[i]), int(M.row_ptr[i + 1])
+            dense[i, M.col[s:e].astype(np.int64)] = M.val[s:e]
+        r, R, piv = brute_rref(dense, M.p)
+        res = c0_oracle if M is c0_matrix else None
+        rk, RM, pc = oracle.full_rref(M, res)
+        assert rk == r, M.name
+        assert np.array_equal(RM.astype(np.int64), R), M.name
+        assert pc.tolist() == piv, M.name
