@@ -156,6 +156,21 @@ gbla_status gbla_update_D(gbla_mat h, void *stream);
  * Synchronizes `stream`. */
 gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, int64_t *rank);
 
+/* the fully reduced row echelon form of the WHOLE M, in M's original
+ * column order: after gbla_echelon_D (fully reduced), the pivot rows are
+ * reduced to [I | B''] with B' = A^-1 B (Step 2) and B'' = B' - B'[:, pivcol] R
+ * (the second reduction by the rows of R), and Step 5 puts the columns back in
+ * the original order.  The result is RREF(M): rank(M) = n_piv + rank rows,
+ * each with a leading 1, zero in every other pivot column, rows sorted by pivot column.
+ * B' is computed on the tensor cores by the sparse phase itself (targets e_k give
+ * -e_k A^-1 B); B'' by K11.  Stored in the handle as a device CSR (u64 row_ptr, u32
+ * original columns ascending per row, u16 values); *rank_M = rows.  GBLA_E_ORDER before
+ * gbla_echelon_D or after a GBLA_ECHELON_REF echelon; GBLA_E_INVAL on a row-sharded D.
+ * Synchronizes `stream`.  Memory: n_piv x nN u16 (dense -B') plus the CSR. */
+gbla_status gbla_rref_M(gbla_mat h, void *stream, int64_t *rank_M);
+/* Device CSR view of RREF(M) (m = rank(M) rows, n = M's columns), valid until gbla_mat_free. */
+gbla_status gbla_get_rref_M(gbla_mat h, gbla_csr *out);
+
 /* The whole pipeline: splice -> (new order: fused reduce_C | standard:
  * reduce_B + update_D) -> echelon_D.  Returns the handle holding every
  * result.  Synchronizes `stream`. */

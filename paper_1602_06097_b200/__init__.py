@@ -96,6 +96,8 @@ def load_library(path: str = LIB_PATH):
         "gbla_get_multilines": ([vp, vp, P(i64), P(vp), P(vp), P(vp)], st),
         "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
         "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
+        "gbla_rref_M": ([vp, vp, P(i64)], st),
+        "gbla_get_rref_M": ([vp, P(_CSR)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -114,7 +116,7 @@ def exported_symbols():
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
-            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench"]
+            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M"]
 
 
 def _check(status: int):
@@ -304,6 +306,17 @@ class Mat:
         _check(_lib.gbla_get_rref(self._h, ctypes.byref(rk), ctypes.byref(pc), ctypes.byref(R), ctypes.byref(ld)))
         r = rk.value
         return r, _view(pc.value, (r,), "<u4").clone(), _view(R.value, (r, nN), "<u2", ld.value, 2).clone()
+
+    def rref_M(self, stream=None):
+        """SURVEY 8(f) f2 (gbla_rref_M): RREF of the whole M in M's original column order, as
+        (rank(M), row_ptr, col, val) new torch tensors (a CSR; rows sorted by pivot column)."""
+        rk = ctypes.c_int64()
+        _check(_lib.gbla_rref_M(self._h, _stream_ptr(stream), ctypes.byref(rk)))
+        c = _CSR()
+        _check(_lib.gbla_get_rref_M(self._h, ctypes.byref(c)))
+        r, nnz = c.m, c.nnz
+        return (r, _view(c.row_ptr, (r + 1,), "<u8").clone(), _view(c.col, (nnz,), "<u4").clone(),
+                _view(c.val, (nnz,), "<u2").clone())
 
     def rref_to_host(self, stream=None, out=None):
         """(rank, pivcol, R) copied to host numpy arrays by the library.  `out` = (pivcol, R)

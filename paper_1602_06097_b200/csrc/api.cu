@@ -402,6 +402,30 @@ extern "C" gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, 
     return GBLA_OK;
 }
 
+extern "C" gbla_status gbla_rref_M(gbla_mat h, void *stream, int64_t *rank_M)
+{
+    GBLA_TRY(check_mat(h, stream));
+    if (h->rank < 0) { set_error("gbla_rref_M: needs gbla_echelon_D first"); return GBLA_E_ORDER; }
+    if (h->ref_only) { set_error("gbla_rref_M: needs the fully reduced R (not GBLA_ECHELON_REF)"); return GBLA_E_ORDER; }
+    if (h->dist_rows) { set_error("gbla_rref_M: single-GPU only (D was row-sharded)"); return GBLA_E_INVAL; }
+    if (h->rankM < 0) GBLA_TRY(full_rref_impl(h));
+    if (rank_M) *rank_M = h->rankM;
+    return GBLA_OK;
+}
+
+extern "C" gbla_status gbla_get_rref_M(gbla_mat h, gbla_csr *out)
+{
+    if (!h || !out) { set_error("gbla_get_rref_M: NULL argument"); return GBLA_E_INVAL; }
+    if (h->rankM < 0) { set_error("gbla_get_rref_M: call gbla_rref_M first"); return GBLA_E_ORDER; }
+    out->m = h->rankM;
+    out->n = h->n;
+    out->nnz = h->rm_nnz;
+    out->row_ptr = h->rm_ptr;
+    out->col = h->rm_col;
+    out->val = h->rm_val;
+    return GBLA_OK;
+}
+
 extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t flags, void *stream,
                                    gbla_mat *out)
 {

@@ -207,6 +207,14 @@ struct gbla_mat_s {
     uint32_t *pivcol = nullptr;
     int64_t rank = -1;
 
+    int64_t force_piv = 0;             // internal splices (f2): rows [0, force_piv) are the pivot rows
+
+    // f2: RREF of the whole M, original column order (gbla_rref_M): device CSR, rows by pivot column
+    int64_t rankM = -1, rm_nnz = 0;
+    uint64_t *rm_ptr = nullptr;
+    uint32_t *rm_col = nullptr;
+    uint16_t *rm_val = nullptr;
+
     uint64_t *opcount = nullptr;       // [mN] per-target sparse modMACs
     uint64_t sparse_ops = 0, dense_ops = 0;
     uint64_t kwork[KT_N] = {0, 0, 0, 0, 0};   // algorithmic modMACs per kernel family (this rank)
@@ -283,6 +291,9 @@ gbla_status dist_sparse_phase(gbla_mat h);
 gbla_status dist_check_async(gbla_ctx ctx);      // ncclCommGetAsyncError (aborts the comm on error)
 int dist_emulated_world();
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);
+gbla_status full_rref_impl(gbla_mat h);
+gbla_status modgemm_sub_chunked(gbla_ctx ctx, cudaStream_t st, const Field &F, int64_t rows, int64_t cols, int64_t K,
+                                const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb, uint16_t *C, int64_t ldc);
 
 // K11 launchers (tc_gemm.cu); see the kernels there for the argument conventions
 gbla_status modgemm_tc_sub(cudaStream_t st, int64_t max_rows, const uint32_t *nrows_dev, int64_t cols, Field F,

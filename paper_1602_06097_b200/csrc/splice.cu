@@ -17,10 +17,12 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 
 // K1: one warp per row.
+// nforce > 0 (internal splices only, f2): rows [0, nforce) win their pivot column whatever their
+// weight (key weight 0); the public splice passes 0 (reading R1).
 __global__ void k_scan_rows(int64_t m, int64_t n, int64_t nnz, const uint64_t *__restrict__ rp,
                             const uint32_t *__restrict__ col, const uint16_t *__restrict__ val, Field F,
                             uint32_t *__restrict__ lead, uint16_t *__restrict__ inv_lead,
-                            unsigned long long *__restrict__ key, uint32_t *__restrict__ err)
+                            unsigned long long *__restrict__ key, uint32_t *__restrict__ err, int64_t nforce)
 {
     int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
@@ -51,7 +53,7 @@ __global__ void k_scan_rows(int64_t m, int64_t n, int64_t nnz, const uint64_t *_
             uint32_t c = col[s];
             lead[r] = c;
             inv_lead[r] = (uint16_t)finv(val[s], F);
-            unsigned long long k = ((unsigned long long)(e - s) << 32) | (unsigned long long)r;
+            unsigned long long k = ((unsigned long long)(r < nforce ? 0 : e - s) << 32) | (unsigned long long)r;
             atomicMin(&key[c], k);
         }
     }
@@ -314,7 +316,7 @@ gbla_status splice_impl(gbla_mat h, const gbla_csr *M, uint32_t flags)
 
     if (m > 0)
         k_scan_rows<<<grid_for(m * 32, 256), 256, 0, st>>>(m, n, nnz, h->row_ptr, h->col, h->val, h->F, h->lead,
-                                                          h->inv_lead, key, err); note_launch();
+                                                          h->inv_lead, key, err, h->force_piv); note_launch();
     k_col_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(n, key, cflag); note_launch();
     GBLA_TRY(exclusive_scan<uint32_t>(h, cflag, pidx, n + 1));
     k_sigma<<<grid_for(n, 256), 256, 0, st>>>(n, key, pidx, h->sigma, h->pivot_row, h->pcol); note_launch();

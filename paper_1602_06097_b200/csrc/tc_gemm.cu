@@ -1427,7 +1427,7 @@ static gbla_status modgemm_tiles(cudaStream_t st, const Field &F, int64_t rows, 
                                  int64_t cp, const uint32_t *rowidx, uint16_t *C, int64_t ldc, const uint8_t *B2lo,
                                  const uint8_t *B2hi)
 {
-    if (nkb == 1)
+    if (nkb == 1 && !(getenv("GBLA_K11_K128_PAIR") && atoi(getenv("GBLA_K11_K128_PAIR")) == 1))
         return modgemm_tc_sub(st, rows, nullptr, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr, 0,
                               CT_ALL, 0, nullptr);
     return modgemm_tc_sub_mk(st, rows, nullptr, cols, F, Alo, Ahi, nkb, nkb, Blo, Bhi, cp * KP, nullptr, rowidx, C,
@@ -1464,13 +1464,41 @@ extern "C" gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int6
     uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
     uint8_t *B2lo = Bhi + cp * KP * nkb, *B2hi = B2lo + cp * KP * nkb;
     k_split_rows<<<grid_for(rp * KP * nkb, 256), 256, 0, st>>>(rows, rp, K, nkb, A, lda, Alo, Ahi);
-    k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, K, nkb, B, ldb, Blo, Bhi, F,
-                                                              nkb > 1 ? B2lo : nullptr, B2hi);
+    k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, K, nkb, B, ldb, Blo, Bhi, F, B2lo, B2hi);
     note_launch(2);
     gbla_status s = modgemm_tiles(st, F, rows, cols, nkb, Alo, Ahi, Blo, Bhi, cp, rowidx, C, ldc, B2lo, B2hi);
     cudaStreamSynchronize(st);
     ctx_free(ctx, ws, st);
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    return s;
+}
+
+// C[i, x] -= sum_{k < K} A[i, k] B[k, x] mod p for any K (f2's B'' = B' - B'[:, pivcol] R, K = rank):
+// chunks of 512 through the multi-K CTA-pair kernel, workspace from the context allocator.
+gbla_status modgemm_sub_chunked(gbla_ctx ctx, cudaStream_t st, const Field &F, int64_t rows, int64_t cols, int64_t K,
+                                const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb, uint16_t *C, int64_t ldc)
+{
+    if (rows <= 0 || cols <= 0 || K <= 0) return GBLA_OK;
+    modgemm_set_sms(ctx->sm_count);
+    const int nkb = MK_MAX;
+    const int64_t rp = (rows + 2 * BM - 1) / (2 * BM) * (2 * BM), cp = (cols + 2 * BN - 1) / (2 * BN) * (2 * BN);
+    const size_t bytes = (size_t)(rp + 2 * cp) * KP * nkb * 2 + 256;
+    uint8_t *ws = (uint8_t *)ctx_alloc(ctx, bytes, st);
+    if (!ws) { set_error("modgemm_sub_chunked: workspace allocation of %zu bytes failed", bytes); return GBLA_E_NOMEM; }
+    uint8_t *Alo = ws, *Ahi = Alo + rp * KP * nkb, *Blo = Ahi + rp * KP * nkb, *Bhi = Blo + cp * KP * nkb;
+    uint8_t *B2lo = Bhi + cp * KP * nkb, *B2hi = B2lo + cp * KP * nkb;
+    gbla_status s = GBLA_OK;
+    for (int64_t k0 = 0; k0 < K && s == GBLA_OK; k0 += (int64_t)nkb * KP) {
+        const int64_t kc = K - k0 < (int64_t)nkb * KP ? K - k0 : (int64_t)nkb * KP;
+        k_split_rows<<<grid_for(rp * KP * nkb, 256), 256, 0, st>>>(rows, rp, kc, nkb, A + k0, lda, Alo, Ahi);
+        k_split_cols<<<grid_for(cp * KP * nkb, 256), 256, 0, st>>>(cols, cp, kc, nkb, B + (size_t)k0 * ldb, ldb, Blo,
+                                                                  Bhi, F, B2lo, B2hi);
+        note_launch(2);
+        s = modgemm_tc_sub_mk(st, rows, nullptr, cols, F, Alo, Ahi, nkb, nkb, Blo, Bhi, cp * KP, nullptr, nullptr, C,
+                              ldc, nullptr, nullptr, 0, CT_ALL, 0, B2lo, B2hi);
+        if (s == GBLA_OK && cudaGetLastError() != cudaSuccess) { set_error("modgemm_sub_chunked: launch failed"); s = GBLA_E_CUDA; }
+    }
+    ctx_free(ctx, ws, st);
     return s;
 }
 

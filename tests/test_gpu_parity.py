@@ -457,6 +457,55 @@ def test_echelon_ref_mode(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     monkeypatch.delenv("GBLA_DIST_EMULATE")
 
 
+def _csr_dense(rp, col, val, rows, n):
+    import torch
+    rp = rp.view(torch.int64).cpu().numpy(); col = col.view(torch.int32).cpu().numpy().astype(np.int64)
+    val = val.view(torch.int16).cpu().numpy().view(np.uint16)
+    out = np.zeros((rows, n), np.uint16)
+    for i in range(rows):
+        s, e = rp[i], rp[i + 1]
+        c = col[s:e]
+        assert np.all(np.diff(c) > 0), "columns not ascending"
+        out[i, c] = val[s:e]
+    return out
+
+
+def test_full_rref_of_M(gb, ctx, c0_matrix, c0_oracle):
+    """SURVEY 8(f) f2 (gbla_rref_M): RREF of the whole M in the original column order (B' = A^-1 B
+    by the tensor-core sparse phase on the targets e_k, B'' = B' - B'[:, pivcol] R by K11, Step 5
+    re-arrangement) bit-exact against the oracle's route (itself pinned against textbook
+    Gauss-Jordan of M) on c0, a random suite (p in {3, 251, 32003, 65521}, zero rows, all-pivot and
+    no-pivot cases) and scaled c1 / c3 (several 128-pivot blocks, K = rank > 512 in chunks)."""
+    cases = [(c0_matrix, c0_oracle)]
+    cases += [(M, None) for M in gbla_gen.random_suite(40, seed0=71)]
+    for name, sc in (("c1", 0.05), ("c3", 0.05)):
+        cases.append((gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc)), None))
+    cases.append((csr_from_dense(np.eye(7, dtype=np.int64) * 3, 7), None))          # all pivots, no D
+    cases.append((csr_from_dense(np.zeros((4, 5), np.int64), 7), None))              # no pivots
+    for M, res in cases:
+        if res is None:
+            res = oracle.reduce(M)
+        rk, RM, pc = oracle.full_rref(M, res)
+        h = gpu_reduce(gb, ctx, M)
+        r, rp, col, val = h.rref_M()
+        assert r == rk == res.rank_M, M.name
+        got = _csr_dense(rp, col, val, r, M.n)
+        assert np.array_equal(got, RM), M.name
+        h.free()
+    # call order: before the echelon, and after a row-echelon-only echelon
+    rp_, c_, v_ = to_dev(c0_matrix)
+    h = gb.gbla_splice(ctx, c0_matrix.m, c0_matrix.n, rp_, c_, v_, c0_matrix.p)
+    with pytest.raises(gb.GblaError) as e:
+        h.rref_M()
+    assert e.value.status == 3
+    h.free()
+    h = gpu_reduce(gb, ctx, c0_matrix, flags=gb.GBLA_ECHELON_REF)
+    with pytest.raises(gb.GblaError) as e:
+        h.rref_M()
+    assert e.value.status == 3
+    h.free()
+
+
 def test_one_rank_nccl_communicator(gb, monkeypatch):
     """The real multi-GPU code path on one GPU (a one-rank NCCL communicator, gbla_ctx_set_comm with
     world 1): C1 broadcast of M, the row-sharded sparse phase with the op-count all-reduce, the
