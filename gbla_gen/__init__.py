@@ -182,3 +182,41 @@ def random_suite(count: int, seed0: int = 0, max_m: int = 100, max_n: int = 150,
         d = float(rng.choice([0.01, 0.03, 0.1, 0.2, 0.4]))
         p = int(primes[i % len(primes)])
         yield random_matrix(m, n, d, p, seed0 * 100003 + i)
+
+
+def gb_like_matrix(m: int, n: int, npoly: int, plen: int, p: int, seed: int, run: int = 4) -> CSR:
+    """Rows of the form m_i * f_j: npoly base polynomials f_j (plen monic coefficients on
+    a run-structured support), each row a random base polynomial shifted by a random column offset
+    (monomial multiplication moves the support, the coefficients stay), plus a few unique rows.
+    Exercises Format 2's polynomial deduplication and column-run compression; rows in random
+    order, some duplicates of a (shift, polynomial) pair allowed.  Input generation only."""
+    rng = np.random.default_rng(seed)
+    span = 4 * plen
+    bases = []
+    for _ in range(npoly):
+        offs = set()
+        while len(offs) < plen:
+            start = int(rng.integers(0, span - run))
+            for u in range(int(rng.integers(1, run + 1))):
+                offs.add(start + u)
+        offs = sorted(offs)[:plen]
+        offs = [o - offs[0] for o in offs]
+        vals = rng.integers(1, p, len(offs))
+        vals[0] = 1
+        bases.append((np.array(offs, np.int64), vals.astype(np.int64)))
+    rows = []
+    for i in range(m):
+        if i % 17 == 16:                                   # a unique row now and then
+            k = int(rng.integers(1, plen + 1))
+            c = np.sort(rng.choice(n, k, replace=False)).astype(np.int64)
+            v = rng.integers(1, p, k)
+            rows.append((c, v))
+            continue
+        offs, vals = bases[int(rng.integers(0, npoly))]
+        sh = int(rng.integers(0, max(1, n - int(offs[-1]))))
+        rows.append((offs + sh, vals))
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum([len(c) for c, _ in rows])
+    col = np.concatenate([c for c, _ in rows]).astype(np.uint32) if m else np.zeros(0, np.uint32)
+    val = np.concatenate([v for _, v in rows]).astype(np.uint16) if m else np.zeros(0, np.uint16)
+    return CSR(m=m, n=n, p=p, row_ptr=rp, col=col, val=val, name=f"gblike{m}x{n}s{seed}")
