@@ -195,6 +195,35 @@ gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, i
 gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K, int reps,
                                void *stream, float *ms_per_launch);
 
+/* ---- the paper's binary matrix formats -------- */
+/* Format 1 (Table `tab:bin_formats`): m, n, p (u32), nnz (u64), data (u16 x nnz),
+ * cols (u32 x nnz), rows (u32 x m, row lengths).  Format 2: b (u32: type code
+ * u | (v << 1) of the pdata elements in the low 3 bits, 8 * 2^v bits, unsigned/signed; format
+ * version in the top 8 bits, 0 or 1), m, n (u32), p, nnz (u64), rows (u32 x m), polmap (u32 x m),
+ * k (u64), colid (u64 x k: a run of s > 1 consecutive columns from f as the slot pair f, s; a
+ * single column f as f | 2^31), pnb (u32), pnnz (u64), prow (u32 x pnb), pdata.  Little-endian.
+ * Readings R20, R23-R26 of DESIGN.md: the paper's "f AND (1 << 31)" is read as OR; its type code
+ * example "011" for unsigned 16-bit is accepted beside 010. */
+typedef struct {
+    int32_t format;         /* 1 or 2 */
+    uint32_t typecode;      /* Format 2: b & 7 */
+    uint32_t version;       /* Format 2: b >> 24 */
+    uint32_t p;
+    int64_t m, n, nnz;
+    int64_t k, pnb, pnnz;   /* Format 2 section sizes */
+} gbla_file_info;
+/* Parse and check the header of a file image (host bytes, len = the whole file): sizes of every
+ * section must add up to len.  GBLA_E_INVAL on a malformed header, GBLA_E_DOMAIN for p >= 2^16. */
+gbla_status gbla_file_info_parse(const void *bytes, size_t len, int format, gbla_file_info *out);
+/* Decode a file image (host bytes) on the device into the caller's device CSR arrays:
+ * row_ptr (m + 1), col (nnz), val (nnz) -- sizes from gbla_file_info_parse -- ready for
+ * gbla_splice / gbla_reduce.  Format 2: column runs decoded by prefix sums over the colid slots
+ * and every row's values expanded from its polynomial (polmap, prow, pdata) on the GPU.
+ * GBLA_E_INVAL on content errors (counts, a run without its length, a polynomial length that
+ * is not the row's, values outside [1, p)).  Synchronizes `stream`. */
+gbla_status gbla_file_decode(gbla_ctx ctx, const void *bytes, size_t len, int format, uint64_t *row_ptr,
+                             uint32_t *col, uint16_t *val, void *stream);
+
 /* ---- results (views valid until gbla_mat_free) ------------------------- */
 gbla_status gbla_get_dims(gbla_mat h, int64_t *npiv, int64_t *mN, int64_t *nN);
 /* sigma[n]: column c -> sigma index; pivot_row[npiv]; nonpivot_row[mN]

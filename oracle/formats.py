@@ -101,7 +101,7 @@ def decode_colids(tokens, expected: int) -> list[int]:
 
 def write_format2(M, typecode: int = 0b010) -> bytes:
     """Table 2, Format 2 with polynomial deduplication (exact value sequences) and run-compressed
-    column ids; pdata as u16 (typecode 010 or 011)."""
+    column ids; pdata elements of 8 * 2^v bits for typecode = u | (v << 1) (010 / 011: 16-bit)."""
     if M.m >= 2 ** 31:
         raise ValueError("format 2: m >= 2^31")
     rows = _rows(M)
@@ -121,7 +121,7 @@ def write_format2(M, typecode: int = 0b010) -> bytes:
            np.array([len(c) for c, _ in rows], "<u4").tobytes(), np.array(polmap, "<u4").tobytes(),
            struct.pack("<Q", len(tokens)), np.array(tokens, "<u8").tobytes(),
            struct.pack("<IQ", len(plist), pnnz), np.array([len(q) for q in plist], "<u4").tobytes(),
-           np.array([v for q in plist for v in q], "<u2").tobytes()]
+           np.array([v for q in plist for v in q], {0: "<u1", 1: "<u2", 2: "<u4", 3: "<u8"}[(typecode >> 1) & 3]).tobytes()]
     return b"".join(out)
 
 
@@ -162,3 +162,33 @@ def read_format2(buf: bytes):
         cols += got
         vals += pdata[pstart[polmap[i]]:pstart[polmap[i]] + rows[i]].tolist()
     return m, n, p, rp, np.array(cols, np.uint32), np.array(vals, np.uint16)
+
+
+def write_format2_nodedup(M, typecode: int = 0b010) -> bytes:
+    """Format 2 without polynomial deduplication (polmap = identity, pdata = the values in row
+    order), column runs encoded vectorized -- the same byte layout, for large synthetic matrices
+    whose coefficients are i.i.d. (nothing to deduplicate) in benchmarks."""
+    rp = M.row_ptr.astype(np.int64)
+    col = M.col.astype(np.int64)
+    nnz = col.size
+    if nnz:
+        rowid = np.repeat(np.arange(M.m), np.diff(rp))
+        brk = np.ones(nnz, bool)
+        brk[1:] = (col[1:] != col[:-1] + 1) | (rowid[1:] != rowid[:-1])
+        starts = np.nonzero(brk)[0]
+        lens = np.diff(np.append(starts, nnz))
+        single = lens == 1
+        ntok = np.where(single, 1, 2)
+        off = np.concatenate([[0], np.cumsum(ntok)[:-1]])
+        tokens = np.zeros(int(ntok.sum()), np.uint64)
+        tokens[off[single]] = col[starts[single]].astype(np.uint64) | np.uint64(MASK)
+        tokens[off[~single]] = col[starts[~single]].astype(np.uint64)
+        tokens[off[~single] + 1] = lens[~single].astype(np.uint64)
+    else:
+        tokens = np.zeros(0, np.uint64)
+    rows = np.diff(rp).astype("<u4")
+    w = {0: "<u1", 1: "<u2", 2: "<u4", 3: "<u8"}[(typecode >> 1) & 3]
+    out = [struct.pack("<IIIQQ", (VERSION << 24) | typecode, M.m, M.n, M.p, nnz), rows.tobytes(),
+           np.arange(M.m, dtype="<u4").tobytes(), struct.pack("<Q", tokens.size), tokens.astype("<u8").tobytes(),
+           struct.pack("<IQ", M.m, nnz), rows.tobytes(), M.val.astype(w).tobytes()]
+    return b"".join(out)

@@ -45,6 +45,12 @@ class _CSR(ctypes.Structure):
                 ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p)]
 
 
+class _FileInfo(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("typecode", ctypes.c_uint32), ("version", ctypes.c_uint32),
+                ("p", ctypes.c_uint32), ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("k", ctypes.c_int64), ("pnb", ctypes.c_int64), ("pnnz", ctypes.c_int64)]
+
+
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 _MEMQ_FN = ctypes.CFUNCTYPE(ctypes.c_size_t, ctypes.c_void_p)
@@ -97,6 +103,8 @@ def load_library(path: str = LIB_PATH):
         "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
         "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
         "gbla_rref_M": ([vp, vp, P(i64)], st),
+        "gbla_file_info_parse": ([vp, ctypes.c_size_t, ctypes.c_int, P(_FileInfo)], st),
+        "gbla_file_decode": ([vp, vp, ctypes.c_size_t, ctypes.c_int, vp, vp, vp, vp], st),
         "gbla_get_rref_M": ([vp, P(_CSR)], st),
     }
     for name, (args, res) in sig.items():
@@ -116,7 +124,8 @@ def exported_symbols():
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
-            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M"]
+            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M",
+            "gbla_file_info_parse", "gbla_file_decode"]
 
 
 def _check(status: int):
@@ -464,6 +473,30 @@ def modgemm_bench(ctx: Context, p: int, rows: int, cols: int, K: int, reps: int 
     ms = ctypes.c_float()
     _check(_lib.gbla_modgemm_bench(ctx._h, p, rows, cols, K, reps, _stream_ptr(stream), ctypes.byref(ms)))
     return ms.value
+
+
+def file_info(data: bytes, fmt: int) -> dict:
+    """gbla_file_info_parse: the header of a Format 1 / Format 2 file image."""
+    fi = _FileInfo()
+    buf = ctypes.create_string_buffer(bytes(data), len(data))
+    _check(load_library().gbla_file_info_parse(buf, len(data), fmt, ctypes.byref(fi)))
+    return {k: getattr(fi, k) for k, _ in _FileInfo._fields_}
+
+
+def file_decode(ctx: Context, data: bytes, fmt: int, stream=None):
+    """gbla_file_decode: decode a file image on the device.  Returns (m, n, p, row_ptr, col, val)
+    with new torch CUDA tensors (uint64 / uint32 / uint16), ready for gbla_splice / gbla_reduce."""
+    import torch
+    info = file_info(data, fmt)
+    m, nnz = info["m"], info["nnz"]
+    rp = torch.empty(m + 1, dtype=torch.uint64, device="cuda")
+    col = torch.empty(max(nnz, 1), dtype=torch.uint32, device="cuda")
+    val = torch.empty(max(nnz, 1), dtype=torch.uint16, device="cuda")
+    buf = ctypes.create_string_buffer(bytes(data), len(data))
+    _check(_lib.gbla_file_decode(ctx._h, buf, len(data), fmt, ctypes.c_void_p(rp.data_ptr()),
+                                 ctypes.c_void_p(col.data_ptr()), ctypes.c_void_p(val.data_ptr()),
+                                 _stream_ptr(stream)))
+    return m, info["n"], info["p"], rp, col[:nnz], val[:nnz]
 
 
 def tile_shard(ntiles: int, rank: int, world: int):

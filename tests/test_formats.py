@@ -78,3 +78,8 @@ def test_format2_smaller_on_repeated_polynomials():
     f1, f2 = fm.write_format1(G), fm.write_format2(G)
     _eq(G, fm.read_format2(f2))
     assert len(f2) < len(f1) / 2
+
+
+def test_format2_without_dedup_reads_back():
+    for M in list(gbla_gen.random_suite(30, seed0=8)) + [gbla_gen.f4_matrix("c0")]:
+        _eq(M, fm.read_format2(fm.write_format2_nodedup(M)))
