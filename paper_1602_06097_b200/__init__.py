@@ -174,31 +174,23 @@ class Context:
         if torch_allocator:
             dev = torch.device("cuda", device)
 
-            streams = {}
+            raw_alloc = torch.cuda.caching_allocator_alloc
+            raw_free = torch.cuda.caching_allocator_delete
 
             def _alloc(nbytes, stream, user):
                 # an exception must not cross the C boundary: out of memory -> NULL -> GBLA_E_NOMEM.
-                # The block belongs to the library's stream (torch reuses a freed block only in that
-                # stream's order), not to torch's current stream.
+                # torch's caching allocator with the library's stream (a freed block is reused only in
+                # that stream's order), not torch's current stream
                 try:
-                    sid = int(stream or 0)
-                    if sid == torch.cuda.current_stream(dev).cuda_stream:
-                        t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
-                    else:
-                        s = streams.get(sid)
-                        if s is None:
-                            s = torch.cuda.ExternalStream(sid, device=dev) if sid else torch.cuda.default_stream(dev)
-                            streams[sid] = s
-                        with torch.cuda.stream(s):
-                            t = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+                    ptr = int(raw_alloc(int(nbytes), device, int(stream or 0)))
                 except Exception:
                     return None
-                ptr = t.data_ptr()
-                self._live[ptr] = t
+                self._live[ptr] = True
                 return ptr
 
             def _free(ptr, stream, user):
-                self._live.pop(int(ptr) if ptr else 0, None)
+                if ptr and self._live.pop(int(ptr), None):
+                    raw_free(int(ptr))
 
             self._alloc_cb = _ALLOC_FN(_alloc)
             self._free_cb = _FREE_FN(_free)
