@@ -182,19 +182,6 @@ cudaStream_t ctx_side_stream(gbla_ctx c)
     return c->side;
 }
 
-cudaStream_t ctx_rest_stream(gbla_ctx c)
-{
-    if (!c->rest) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&c->rest, cudaStreamNonBlocking, lo) != cudaSuccess) {
-            cudaGetLastError();
-            c->rest = nullptr;
-        }
-    }
-    return c->rest;
-}
-
 cudaEvent_t ctx_event(gbla_ctx c, int i)
 {
     if (!c->ev[i] && cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -222,7 +209,6 @@ extern "C" void gbla_ctx_destroy(gbla_ctx ctx)
     dist_destroy(ctx);
     cudaSetDevice(ctx->device);
     if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->rest) cudaStreamDestroy(ctx->rest);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);

@@ -79,7 +79,7 @@ __device__ __forceinline__ uint32_t fneg(uint32_t a, const Field &F) { return a 
 // latch a code into the device error word of their translation unit and stop waiting; the host
 // reads and clears the word when the phase ends and fails the call with GBLA_E_INTERNAL (the
 // result is discarded).  GBLA_DEV_ERR_UNIT(fn) defines the word and the host check `fn`.
-enum { DEVERR_GATHER_WAIT = 1, DEVERR_WIN_FLAG = 2, DEVERR_WIN_BARRIER = 4, DEVERR_SWEEP_FLAG = 8 };
+enum { DEVERR_GATHER_WAIT = 1, DEVERR_WIN_FLAG = 2, DEVERR_SWEEP_FLAG = 8 };
 #define GBLA_DEV_ERR_UNIT(fn)                                                                      \
     static __device__ uint32_t g_dev_err = 0;                                                      \
     static __device__ __forceinline__ void dev_err_latch(uint32_t code) { atomicOr(&g_dev_err, code); } \
@@ -138,13 +138,11 @@ struct gbla_ctx_s {
     size_t (*memq)(void *) = nullptr;    // gbla_ctx_set_mem_query
     void *memq_user = nullptr;
     cudaStream_t side = nullptr;
-    cudaStream_t rest = nullptr;         // low priority: the off-chain part of the echelon's trailing updates
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
 };
 cudaStream_t ctx_side_stream(gbla_ctx c);      // high priority, non-blocking; NULL on failure
-cudaStream_t ctx_rest_stream(gbla_ctx c);      // low priority, non-blocking; NULL on failure
 cudaEvent_t ctx_event(gbla_ctx c, int i);      // i < 4, timing disabled
 void *ctx_pinned(gbla_ctx c, size_t bytes);    // pinned host scratch (grows), NULL on failure
 
@@ -318,8 +316,7 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
                            const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
                            const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
-                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
-                           uint8_t *Rlo2 = nullptr, uint8_t *Rhi2 = nullptr);
+                           uint32_t epoch, int grid, uint8_t *Rlo2 = nullptr, uint8_t *Rhi2 = nullptr);
 
 
 // one-time per-device setup (function attributes): a bit per device ordinal, so a second context on

@@ -101,8 +101,6 @@ struct PanelSrc {
     int gathered;
     int cap;                    // wide panels: at most cap (<= PK) rows lead inside the window
     int walign;                 // panel widths a multiple of this (32 if 0; 64 with deferred updates)
-    int lumode;                 // chunk echelon: 0 rounds, 1 pivot steps, 2 pivot steps in dense mode,
-                                //   3 blocked LU in dense mode (default)
 };
 
 // panels per super-panel of deferred trailing updates (GBLA_SP = 1..4).  Default: 4 when D is
@@ -124,14 +122,6 @@ static int panel_cap()
     return c >= 16 && c <= PK ? c : PK;
 }
 
-// GBLA_PANEL_LU: how k_panel2 puts a chunk of candidates in echelon form (see step (c))
-static int panel_lumode()
-{
-    const char *e = getenv("GBLA_PANEL_LU");
-    const int v = e ? atoi(e) : 3;
-    return v < 0 || v > 3 ? 3 : v;
-}
-__device__ __forceinline__ bool use_lu(bool dense, int mode) { return mode == 1 || (mode >= 2 && dense); }
 
 __device__ __forceinline__ uint32_t mod32(uint32_t v, uint32_t p, uint32_t m32)
 {
@@ -239,7 +229,7 @@ __device__ __forceinline__ void frag_b_rot(const uint16_t *X, int ld, int n0, in
 }
 }  // namespace tcs
 
-// Dense chunk echelon form by a blocked LU (GBLA_PANEL_LU=3): column blocks of 32 inside the
+// Dense chunk echelon form by a blocked LU: column blocks of 32 inside the
 // window (ldv <= 128).  Phase F: pivot steps (one barrier each, smallest (lead, row) key) on a
 // copy V of the block's columns of the candidate rows, cross-multiplied (row <- v_h row - f head)
 // and tracked against the block-start rows Y:  row_r = sigma_r Y_r + sum_j L[r][j] Y_{p_j}.
@@ -668,7 +658,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         P2_LAP(3);
         // (c) echelon form of the chunk: parallel rounds (staircase panels: many distinct leads)
         //     or pivot steps (dense panels: the rounds would elect one head per round)
-        if (!use_lu(dense, src.lumode)) {
+        if (!dense) {
             // Two block barriers per round: (c1) every remaining candidate (warp per row) finds
             // its leading column from a cursor (leads only move right) and, while an established
             // head owns it, eliminates it (heads are fixed: no block sync); then it bids for its
@@ -759,7 +749,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
                 __syncthreads();
                 int slot = 0, nsteps = 0;
-                const bool blocked = dense && src.lumode == 3 && ldv <= 128;
+                const bool blocked = ldv <= 128;
                 if (blocked) {
                     nsteps = blocked_lu(X, cstat, clead, p, m32, F, ldv);
                 } else for (;;) {
@@ -1735,7 +1725,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     auto p_factor = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1), *cur = ps + (k & 1);
         kt_mark_on(h, KT_PANEL, s);
-        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32, panel_lumode()};
+        PanelSrc src{h->D, ldD, mN, lead, nullptr, nullptr, nullptr, 0, 0, cap, G > 1 ? 64 : 32};
         k_panel2<<<1, NT, P2_SMEM, s>>>(nN, h->F, src, rowpiv, prev, cur, Tlo2[k & 1], Thi2[k & 1], invtab, trace,
                                         (uint32_t)(k + 1));
         kt_mark_on(h, KT_PANEL, s);
@@ -1774,19 +1764,10 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         p_factor(s, k);
         p_gather(s, k);
     };
-    // GBLA_LA_MAIN: the chain on the main stream and the rest of the update on a low-priority stream
-    // (measured slower on c1: 14.3 vs 14.0 ms with the fused window step); default: the next panel on
-    // the high-priority side stream
-    cudaStream_t rest = nullptr;
-    if (lookahead && getenv("GBLA_LA_MAIN")) rest = ctx_rest_stream(h->ctx);
     // the Rn window and the window update in one persistent launch (k_modgemm_win, column-tile
     // flags; c1: 14.4 -> 14.1 ms); single super-panel panels only (G == 1), side-stream schedule;
     // GBLA_WIN_FUSED=0: two launches
     const bool winfused = lookahead && G == 1 && !(getenv("GBLA_WIN_FUSED") && atoi(getenv("GBLA_WIN_FUSED")) == 0);
-    // GBLA_WIN_LEAD=1: the window step also scans the next window's leads after a grid barrier (no
-    // k_lead2 launch).  Measured slower on c1 (14.2 vs 14.0 ms: 1,470 warps scanning ~5 rows each
-    // after the barrier vs a separate 4,700-warp launch), so off by default
-    const bool winlead = winfused && getenv("GBLA_WIN_LEAD") && atoi(getenv("GBLA_WIN_LEAD")) == 1;
     // GBLA_EARLY_GATHER=0: the next panel's F gather waits for the whole panel (default: for its flag)
     const bool early_gather = !(getenv("GBLA_EARLY_GATHER") && atoi(getenv("GBLA_EARLY_GATHER")) == 0);
     bool btiles_ready = false;               // the B tiles of the next window were gathered early
@@ -1861,7 +1842,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 kt_mark(h, KT_TRAIL);
                 status = modgemm_tc_win(st, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, Rtl, Rth, Flo[f], Fhi[f], rows[f],
                                         cur->sel, &cur->nrows, &cur->kp, &cur->c0, &cur->c1, PW, h->D, ldD, wflags,
-                                        (uint32_t)(k + 1), gemm_grid, winlead ? lead : nullptr, rowpiv, mN, Rpl, Rph);
+                                        (uint32_t)(k + 1), gemm_grid, Rpl, Rph);
             } else {
                 kt_mark(h, KT_RN);
                 // look-ahead: only the window part of Rn is on the chain to the next panel, and the Rn
@@ -1884,54 +1865,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 k_commit2<<<2 * h->ctx->sm_count, 256, 0, st>>>(nN, h->D, ldD, cur, Rn, ldR, dops, 0);
                 note_launch();
                 factor(st, k + 1);
-            } else if (rest) {
-                // critical chain on the main stream (launches back to back, PDL): window update ->
-                // leads -> panel -> F gather of the next panel; the rest of the update of this panel
-                // on the low-priority stream beside it.  Hazards: the rest writes D outside the next
-                // window, reads F / rows / T / P2State of parity k (the next panel writes parity k+1)
-                // and the B and Rn tiles, which the next iteration rewrites only after waiting evR.
-                if (!winfused)
-                    status = modgemm_tc_sub(st, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
-                                            ldD, &cur->c0, &cur->c1, PW, 1, gemm_grid, spCd);
-                kt_mark(h, KT_TRAIL);
-                if (status != GBLA_OK) break;
-                tmark(k, st);
-                if (G > 1 && j == G - 1 && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
-                // the leads of the next window before the rest starts (they would compete for the SMs)
-                if (!winlead) p_lead(st, k + 1);
-                if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(rest, evA, 0) != cudaSuccess) {
-                    fail("event");
-                    break;
-                }
-                tmark(k, rest);
-                launch_pdl(k_gather_st2, dim3(grid_for(nN, 128), PK / 16), dim3(128), 0, rest, nN,
-                           (const uint16_t *)h->D, ldD, (const P2State *)cur, Blo, Bhi,
-                           (unsigned long long *)nullptr, 2);
-                note_launch();
-                kt_mark_on(h, KT_RN, rest);
-                status = modgemm_tc_store(rest, nN, h->F, Tlo2[f], Thi2[f], Blo, Bhi, h->D, ldD, Rtl, Rth, &cur->c0,
-                                          &cur->kp, &cur->c1, PW, 2, cur->sel, gemm_grid, Rpl, Rph);   // an SM for the panel
-                kt_mark_on(h, KT_RN, rest);
-                if (status != GBLA_OK) break;
-                kt_mark_on(h, KT_TRAIL, rest);
-                status = modgemm_tc_sub(rest, mN, &cur->nrows, nN, h->F, Flo[f], Fhi[f], Rtl, Rth, rows[f], h->D,
-                                        ldD, &cur->c0, &cur->c1, PW, 2, gemm_grid, spCd);
-                kt_mark_on(h, KT_TRAIL, rest);
-                if (status != GBLA_OK) break;
-                if (G > 1 && j == G - 1) {              // end of the super-panel: the deferred columns
-                    if ((status = sp_flush(cur, 2, rest)) != GBLA_OK || (status = sp_begin(cur, rest)) != GBLA_OK)
-                        break;
-                }
-                tmark(k, rest);
-                if (cudaEventRecord(evB, rest) != cudaSuccess) { fail("event"); break; }
-                tmark(k, st);
-                p_factor(st, k + 1);
-                tmark(k, st);
-                // sp_begin cleared the deferred factor tiles that the gather writes
-                if (G > 1 && j == G - 1 && cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
-                p_gather(st, k + 1);
-                tmark(k, st);
-                if (cudaStreamWaitEvent(st, evB, 0) != cudaSuccess) { fail("event"); break; }
             } else {
                 // the next panel's window first, then the next panel beside the rest of the update
                 // timer pair of the window update closed after the next panel's lead scan: a mark
@@ -1945,7 +1878,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
                 const bool wflush = G > 1 && j == G - 1;
                 if (wflush) kt_mark(h, KT_TRAIL);                 // (the flush has its own pair)
                 if (wflush && (status = sp_flush(cur, 1, st)) != GBLA_OK) break;   // next window
-                if (!(winfused && winlead)) p_lead(st, k + 1);   // else the window step scanned the leads
+                p_lead(st, k + 1);
                 if (!wflush) kt_mark(h, KT_TRAIL);
                 if (cudaEventRecord(evA, st) != cudaSuccess || cudaStreamWaitEvent(side, evA, 0) != cudaSuccess) {
                     fail("event");
@@ -2024,7 +1957,6 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     if (status == GBLA_OK && cudaStreamSynchronize(st) != cudaSuccess) fail("sync");
 
     if (side) cudaStreamSynchronize(side);
-    if (rest) cudaStreamSynchronize(rest);
     if (!tl.empty()) {
         cudaDeviceSynchronize();
         // per iteration (us from its start): side panel start, end; main rest start, end; gather end
@@ -2197,7 +2129,7 @@ gbla_status panels_dist(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, 
             }
         }
         // the same panel factorization on every rank
-        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap, 0, panel_lumode()};
+        PanelSrc src{gv, ldc, (int64_t)G * maxcnt, gl, gr, ghist, real ? owner : nullptr, me, 1, pcap, 0};
         kt_mark(h, KT_PANEL);
         k_panel2<<<1, NT, P2_SMEM, st>>>(nN, h->F, src, rowpiv, prev, cur, Tlo, Thi, invtab, nullptr, 0u);
         kt_mark(h, KT_PANEL);

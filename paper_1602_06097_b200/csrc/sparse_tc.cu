@@ -39,11 +39,6 @@ struct BandTiles {
     int64_t NB = 0, NNB = 0, ntiles = 0;
     int64_t nA = 0, nB = 0;
     uint8_t *tilesA = nullptr, *tilesB = nullptr, *invT = nullptr, *Xt = nullptr;
-    // two-step look-ahead of the sweep (GBLA_SWEEP_PAIRS): odd blocks J from X_I, I <= J-2, with
-    // Â'_IJ = Â_IJ + Â_{I,J-1} Â_{J-1,J} (in place) and G_{J-1} = inv(A_{J-1,J-1}) Â_{J-1,J}; the
-    // C tiles of even blocks are kept (Ct) because X_{J-1} overwrites C_{J-1}
-    bool pairs = false;
-    uint8_t *Gt = nullptr, *Ct = nullptr;
     uint64_t *offA = nullptr, *offB = nullptr;
     uint32_t *amax = nullptr, *bmin = nullptr, *bmax = nullptr;
     uint32_t *jl_ptr = nullptr, *jl_idx = nullptr, *kl_ptr = nullptr, *kl_idx = nullptr;
@@ -215,9 +210,6 @@ struct SweepArgs {
     uint32_t *flags;               // [nl*NB] 1 once X_J of local tile i is stored
     unsigned int *next;            // task counter
     uint32_t ntasks;
-    const uint8_t *Gt;             // pairs: G_{J-1} tiles (index J-1), else NULL
-    const uint8_t *Ct;             // pairs: C tiles of even blocks, [local tile][J / 2]
-    int64_t NBh;                   // (NB + 1) / 2
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
@@ -256,8 +248,7 @@ __global__ void k_pos(int64_t mN, const uint32_t *__restrict__ order, uint32_t *
 __global__ void k_cfill(int64_t mN, int64_t NB, int64_t prank, int64_t pworld, int64_t i0, int64_t i1,
                         const uint32_t *__restrict__ pos, const uint64_t *__restrict__ cd_ptr,
                         const uint32_t *__restrict__ cd_col, const uint16_t *__restrict__ cd_val,
-                        const uint32_t *__restrict__ cd_np, uint8_t *__restrict__ Xt,
-                        uint8_t *__restrict__ Ct = nullptr, int64_t NBh = 0)
+                        const uint32_t *__restrict__ cd_np, uint8_t *__restrict__ Xt)
 {
     const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -276,11 +267,6 @@ __global__ void k_cfill(int64_t mN, int64_t NB, int64_t prank, int64_t pworld, i
         const uint32_t o = tc::toff((uint32_t)r, c % 128);
         tile[o] = (uint8_t)(v & 0xff);
         tile[PB + o] = (uint8_t)(v >> 8);
-        if (Ct && ((c / 128) & 1) == 0) {
-            uint8_t *ct = Ct + (T * NBh + (c / 128) / 2) * (uint64_t)TB;
-            ct[o] = (uint8_t)(v & 0xff);
-            ct[PB + o] = (uint8_t)(v >> 8);
-        }
     }
 }
 
@@ -364,9 +350,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
-        // odd J with pairs: (C_J, inv(A_JJ)), (C_{J-1}, G_{J-1}) if J-1 >= Jmin, then (X_I, Â'_IJ), I <= J-2
-        const uint32_t hasG = (a.Gt && (J & 1) && J - 1 >= Jmin) ? 1u : 0u;
-        const uint32_t npair = l1 - lb + 1 + hasG;     // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
+        const uint32_t npair = l1 - lb + 1;            // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
         // pair q into stage (gpair + q) % NSTAGE (thread 0 only)
         auto load = [&](uint32_t q) {
             const int s = (gpair + q) % NSTAGE;
@@ -377,12 +361,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
                 tc::bulk_g2s(sa, Xrow + (size_t)J * TB, TB, &full[s]);          // C_J (not yet overwritten)
                 return;
             }
-            if (hasG && q == 1) {
-                tc::bulk_g2s(sb, a.Gt + (size_t)(J - 1) * TB, TB, &full[s]);
-                tc::bulk_g2s(sa, a.Ct + ((size_t)li * a.NBh + (size_t)((J - 1) >> 1)) * TB, TB, &full[s]);
-                return;
-            }
-            const uint32_t I = a.jl_idx[lb + q - 1 - hasG];
+            const uint32_t I = a.jl_idx[lb + q - 1];
             tc::bulk_g2s(sb, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);   // Â_IJ
             // X_I[T] is produced by task (li, I): wait until it is published
             if (ld_acquire(fl + I) == 0) {
@@ -677,95 +656,6 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
-// dst tile = src tile transposed (both limb planes): dst element (a, b) at toff(a, b) = src element
-// (b, a) at toff(b, a).  Block per tile pair (src, dst byte offsets from the code list).
-__global__ void k_tile_t(const uint64_t *__restrict__ pairs, int64_t n, const uint8_t *__restrict__ srcbase,
-                         uint8_t *__restrict__ dstbase)
-{
-    const int64_t q = blockIdx.x;
-    if (q >= n) return;
-    const uint8_t *src = srcbase + pairs[2 * q];
-    uint8_t *dst = dstbase + pairs[2 * q + 1];
-    for (int e = threadIdx.x; e < 128 * 128; e += blockDim.x) {
-        const uint32_t a = (uint32_t)e >> 7, b = (uint32_t)e & 127u;
-        const uint32_t od = tc::toff(a, b), os = tc::toff(b, a);
-        dst[od] = src[os];
-        dst[PB + od] = src[PB + os];
-    }
-}
-
-// pairs of the sweep's look-ahead.  Task code (I, J, kind): D[j][i] = sum_k Â_{J-1,J}[k][j] B[i][k]
-// with the A operand the stored Â_{J-1,J} tile (element (k, j) at toff(j, k)) and B the transposed
-// copy of Â_{I,J-1} (kind 0: Â'_IJ = Â_IJ + D, in place) or of inv(A_{J-1,J-1}) (kind 1: G_{J-1} = D).
-// Outputs in the sweep's B layout (element (i, j) at toff(j, i)); thread = j.
-__global__ void __launch_bounds__(128, 1) k_ahat2(Field F, const uint64_t *__restrict__ offA,
-                                                  const uint64_t *__restrict__ tasks, int64_t ntask,
-                                                  uint8_t *__restrict__ tilesA, const uint8_t *__restrict__ tilesAT,
-                                                  const uint8_t *__restrict__ invTT, uint8_t *__restrict__ Gt)
-{
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sA = smem, *sB = smem + TB;
-    __shared__ uint64_t bar, accbar;
-    __shared__ uint32_t tmem_s;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
-    if (tid == 0) { tc::mbar_init(&bar, 1); tc::mbar_init(&accbar, 1); }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tbase = tmem_s, lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-    uint32_t ph = 0, pha = 0;
-    for (int64_t q = blockIdx.x; q < ntask; q += gridDim.x) {
-        const uint64_t code = tasks[q];
-        const uint32_t I = (uint32_t)(code >> 33), J = (uint32_t)(code >> 1) & 0xffffffffu, kind = (uint32_t)code & 1u;
-        const uint8_t *tAn = tilesA + (offA[J - 1] + 1) * TB;              // Â_{J-1,J}
-        const uint8_t *tB = kind ? invTT + (size_t)(J - 1) * TB : tilesAT + (offA[I] + (uint64_t)(J - 1 - I)) * TB;
-        uint8_t *out = kind ? Gt + (size_t)(J - 1) * TB : tilesA + (offA[I] + (uint64_t)(J - I)) * TB;
-        if (tid == 0) {
-            tc::mbar_expect_tx(&bar, 2 * TB);
-            tc::bulk_g2s(sA, tAn, TB, &bar);
-            tc::bulk_g2s(sB, tB, TB, &bar);
-        }
-        tc::mbar_wait(&bar, ph);
-        ph ^= 1;
-        tc::fence_after();
-        if (tid == 0) {
-            issue_mmas(tbase, tc::smem_u32(sA), tc::smem_u32(sB), false);
-            tc::commit(&accbar);
-        }
-        tc::mbar_wait(&accbar, pha);
-        pha ^= 1;
-        tc::fence_after();
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 16) {
-            uint32_t Rv[16];
-            read_R(lane_addr, c, Rv, F);
-            const uint32_t o = tc::toff(tid, c);          // thread = j, columns c.. = i
-            uint8_t lo8[16], hi8[16];
-            if (!kind) {
-                *reinterpret_cast<uint4 *>(lo8) = *reinterpret_cast<const uint4 *>(out + o);
-                *reinterpret_cast<uint4 *>(hi8) = *reinterpret_cast<const uint4 *>(out + PB + o);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                uint32_t v = Rv[j];
-                if (!kind) {
-                    v += (uint32_t)lo8[j] | ((uint32_t)hi8[j] << 8);
-                    v = v >= F.p ? v - F.p : v;
-                }
-                lo8[j] = (uint8_t)(v & 0xff);
-                hi8[j] = (uint8_t)(v >> 8);
-            }
-            *reinterpret_cast<uint4 *>(out + o) = *reinterpret_cast<uint4 *>(lo8);
-            *reinterpret_cast<uint4 *>(out + PB + o) = *reinterpret_cast<uint4 *>(hi8);
-        }
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-    }
-    if (warp == 0) tc::tmem_dealloc<512>(tbase);
-}
-
 }  // namespace
 
 void band_free(gbla_mat h)
@@ -774,57 +664,6 @@ void band_free(gbla_mat h)
     h->bt = nullptr;
 }
 
-// the look-ahead tiles of the sweep (BandTiles::pairs): transposed copies of the even-column band
-// tiles and of the even diagonal inverses, then Â'_IJ (in place) and G_{J-1} for every odd J
-static gbla_status pair_tiles(gbla_mat h, const std::vector<uint32_t> &amax, const std::vector<uint64_t> &offA)
-{
-    cudaStream_t st = h->stream;
-    BandTiles *bt = h->bt;
-    const int64_t NB = bt->NB;
-    uint8_t *tilesAT, *invTT;
-    GBLA_TRY(dalloc(h, bt->nA * TB + 16, (void **)&tilesAT));
-    GBLA_TRY(dalloc(h, NB * TB + 16, (void **)&invTT));
-    GBLA_TRY(dalloc(h, NB * TB + 16, (void **)&bt->Gt));
-    GBLA_CUDA_TRY(cudaMemsetAsync(bt->Gt, 0, NB * TB, st));
-    std::vector<uint64_t> tp, ti, tasks;
-    for (int64_t I = 0; I < NB; I++)
-        for (uint32_t J = (uint32_t)I + 1; J <= amax[I]; J++)
-            if ((J & 1) == 0) { tp.push_back((offA[I] + (J - I)) * TB); tp.push_back((offA[I] + (J - I)) * TB); }
-    for (int64_t J = 0; J < NB; J += 2) { ti.push_back((uint64_t)J * TB); ti.push_back((uint64_t)J * TB); }
-    for (int64_t J = 1; J < NB; J += 2) {
-        if (amax[J - 1] < (uint32_t)J) continue;                   // Â_{J-1,J} = 0: G = 0, Â' = Â
-        tasks.push_back(((uint64_t)J << 1) | 1u);                     // G_{J-1}
-        for (int64_t I = 0; I < J - 1; I++)
-            if (amax[I] >= (uint32_t)J) tasks.push_back(((uint64_t)I << 33) | ((uint64_t)J << 1));
-    }
-    uint64_t *d;
-    const size_t nall = tp.size() + ti.size() + tasks.size();
-    GBLA_TRY(dalloc_t(h, nall + 1, &d));
-    std::vector<uint64_t> all(tp);
-    all.insert(all.end(), ti.begin(), ti.end());
-    all.insert(all.end(), tasks.begin(), tasks.end());
-    GBLA_CUDA_TRY(cudaMemcpyAsync(d, all.data(), nall * 8, cudaMemcpyHostToDevice, st));
-    if (!tp.empty()) k_tile_t<<<(unsigned)(tp.size() / 2), 256, 0, st>>>(d, (int64_t)tp.size() / 2, bt->tilesA, tilesAT);
-    if (!ti.empty()) k_tile_t<<<(unsigned)(ti.size() / 2), 256, 0, st>>>(d + tp.size(), (int64_t)ti.size() / 2, bt->invT, invTT);
-    note_launch(2);
-    if (!tasks.empty()) {
-        static unsigned long long attr = 0;   // devices done (dev_bit)
-        if (!(attr & dev_bit())) {
-            GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB));
-            attr |= dev_bit();
-        }
-        const int64_t nt = (int64_t)tasks.size();
-        const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
-        k_ahat2<<<(unsigned)grid, 128, 2 * TB, st>>>(h->F, bt->offA, d + tp.size() + ti.size(), nt, bt->tilesA,
-                                                     tilesAT, invTT, bt->Gt);
-        note_launch();
-    }
-    GBLA_CUDA_TRY(cudaGetLastError());
-    GBLA_CUDA_TRY(cudaStreamSynchronize(st));      // the host lists must outlive the async copy
-    dfree(h, tilesAT);
-    dfree(h, invTT);
-    return GBLA_OK;
-}
 
 static gbla_status band_build(gbla_mat h)
 {
@@ -853,20 +692,12 @@ static gbla_status band_build(gbla_mat h)
     std::vector<uint64_t> offA(NB), offB(NB);
     std::vector<std::vector<uint32_t>> jl(NB), kl(NNB > 0 ? NNB : 1);
     uint64_t nA = 0, nB = 0;
-    {   // two-step look-ahead of the sweep: on by GBLA_SWEEP_PAIRS=1 when the extra tiles fit
-        const char *e = getenv("GBLA_SWEEP_PAIRS");
-        uint64_t n0 = 0;
-        for (int64_t I = 0; I < NB; I++) n0 += (amax[I] >= NB ? NB - 1 : amax[I]) - I + 1;
-        bt->pairs = e && atoi(e) == 1 && NB >= 3 && n0 * TB <= ((uint64_t)16 << 30);
-    }
     for (int64_t I = 0; I < NB; I++) {
         if (amax[I] >= NB) amax[I] = NB - 1;
-        // pairs: a row block whose last tile is in an even column J-1 > I also needs column J
-        if (bt->pairs && amax[I] > I && (amax[I] & 1) == 0 && amax[I] + 1 < NB) amax[I]++;
         offA[I] = nA;
         nA += amax[I] - I + 1;
         for (uint32_t J = I + 1; J <= amax[I]; J++)
-            if (!(bt->pairs && (J & 1) && I == J - 1)) jl[J].push_back((uint32_t)I);   // odd J: no X_{J-1}
+            jl[J].push_back((uint32_t)I);
         offB[I] = nB;
         if (bmin[I] <= bmax[I] && bmin[I] != 0xffffffffu) {
             nB += bmax[I] - bmin[I] + 1;
@@ -932,7 +763,6 @@ static gbla_status band_build(gbla_mat h)
             k_ahat<<<(unsigned)grid, 128, 2 * TB, st>>>(h->F, NB, bt->offA, bt->amax, dtl, nt, bt->tilesA, bt->invT);
             note_launch();
             GBLA_CUDA_TRY(cudaGetLastError());
-            if (bt->pairs) GBLA_TRY(pair_tiles(h, amax, offA));
             // the host list must outlive the async copy
             GBLA_CUDA_TRY(cudaStreamSynchronize(st));
         }
@@ -951,7 +781,7 @@ static inline int64_t local_tiles(int64_t ntiles, int prank, int pworld)
 // (1172 tiles x 6641 blocks x 32 KB would be 255 GB).
 static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
 {
-    const int64_t per_tile = (h->bt->NB + (h->bt->pairs ? (h->bt->NB + 1) / 2 : 0)) * (int64_t)TB;
+    const int64_t per_tile = h->bt->NB * (int64_t)TB;
     const char *e = getenv("GBLA_XT_BATCH");          // tests: force small batches
     if (e && atoll(e) > 0) return atoll(e) < nl ? atoll(e) : nl;
     if (nl * per_tile <= ((int64_t)8 << 30)) return nl;   // small: no need to ask the driver
@@ -1022,9 +852,6 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
     a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
     a.prank = prank; a.pworld = pworld; a.i0 = i0;
     a.toff = toff; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
-    a.Gt = bt->pairs ? bt->Gt : nullptr;
-    a.Ct = bt->pairs ? bt->Ct : nullptr;
-    a.NBh = (NB + 1) / 2;
     int64_t grid = (int64_t)h->ctx->sm_count * occ;
     if (grid > (int64_t)ntasks) grid = ntasks;
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
@@ -1093,11 +920,9 @@ static gbla_status tc_sparse(gbla_mat h, int prank, int pworld, bool want_x16, b
     const int64_t nl = local_tiles(bt->ntiles, prank, pworld);
     if (NB == 0 || nl == 0) return GBLA_OK;
     if (!bt->tilesA) { set_error("sparse phase: band tiles already released"); return GBLA_E_ORDER; }
-    const int64_t NBh = (NB + 1) / 2;
     if (!bt->Xt) {
         bt->xt_cap = update ? xt_batch_tiles(h, nl) : nl;
         GBLA_TRY(dalloc(h, (size_t)bt->xt_cap * NB * TB + 16, (void **)&bt->Xt));
-        if (bt->pairs) GBLA_TRY(dalloc(h, (size_t)bt->xt_cap * NBh * TB + 16, (void **)&bt->Ct));
     }
     const int64_t per = bt->xt_cap < nl ? bt->xt_cap : nl;
     if (!update && per < nl) { set_error("unfused reduce_C needs every C' tile resident"); return GBLA_E_NOMEM; }
@@ -1108,9 +933,8 @@ static gbla_status tc_sparse(gbla_mat h, int prank, int pworld, bool want_x16, b
     for (int64_t i0 = 0; i0 < nl; i0 += per) {
         const int64_t i1 = i0 + per < nl ? i0 + per : nl;
         GBLA_CUDA_TRY(cudaMemsetAsync(bt->Xt, 0, (size_t)(i1 - i0) * NB * TB, st));
-        if (bt->Ct) GBLA_CUDA_TRY(cudaMemsetAsync(bt->Ct, 0, (size_t)(i1 - i0) * NBh * TB, st));
         k_cfill<<<grid_for(h->mN * 32, 256), 256, 0, st>>>(h->mN, NB, prank, pworld, i0, i1, pos, h->cd_ptr,
-                                                           h->cd_col, h->cd_val, h->cd_np, bt->Xt, bt->Ct, NBh);
+                                                           h->cd_col, h->cd_val, h->cd_np, bt->Xt);
         note_launch();
         GBLA_CUDA_TRY(cudaGetLastError());
         GBLA_TRY(tc_sweep_batch(h, prank, pworld, i0, i1, want_x16));
@@ -1129,8 +953,6 @@ void band_release(gbla_mat h)
     dfree(h, bt->tilesB); bt->tilesB = nullptr;
     dfree(h, bt->invT); bt->invT = nullptr;
     dfree(h, bt->Xt); bt->Xt = nullptr;
-    dfree(h, bt->Ct); bt->Ct = nullptr;
-    dfree(h, bt->Gt); bt->Gt = nullptr;
     bt->xt_cap = 0;
 }
 

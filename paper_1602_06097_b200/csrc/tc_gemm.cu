@@ -849,11 +849,6 @@ struct WinArgs {
     int64_t ldD;
     uint32_t *flags;
     uint32_t epoch;
-    // optional (lead != NULL): after a grid barrier (counter flags[63], target epoch * gridDim.x),
-    // the leading column of every active row in the next window [*win_dev, + win_w), as k_lead2
-    uint32_t *lead;
-    const uint32_t *rowpiv;
-    int64_t mN;
 };
 
 __device__ __forceinline__ uint32_t ld_acq(const uint32_t *p)
@@ -1088,52 +1083,6 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
     } while (0);
-    if (!g.lead) return;
-    // grid barrier (every CTA is resident: one per SM, grid <= SMs), then the lead scan of the
-    // updated window: one warp per row, 8 columns (16 bytes) per lane per step, L2 loads (other
-    // CTAs wrote these rows; this SM's L1 may hold stale lines)
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        atomicAdd(g.flags + 63, 1u);
-        const uint32_t target = g.epoch * gridDim.x;
-        for (uint32_t it = 0; ld_acq(g.flags + 63) < target; it++) {
-            __nanosleep(64);
-            if (it > (1u << 24)) { dev_err_latch(DEVERR_WIN_BARRIER); break; }   // never hang the GPU
-        }
-    }
-    __syncthreads();
-    const int64_t wc0 = *g.win_dev;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; r < g.mN; r += nwarps) {
-        uint32_t res = 0xffffffffu;
-        if (g.rowpiv[r] == 0xffffffffu && wc0 < g.cols) {
-            const int64_t wmax = g.cols - wc0 < g.win_w ? g.cols - wc0 : g.win_w;
-            const uint16_t *row = g.D + (size_t)r * g.ldD + wc0;
-            const bool vec = (((size_t)r * g.ldD + wc0) & 7) == 0;
-            for (int64_t base = 0; base < wmax && res == 0xffffffffu; base += 256) {
-                const int64_t k0 = base + lane * 8;
-                uint32_t first = 0xffffffffu;
-                if (vec && k0 + 8 <= wmax) {
-                    const uint4 qv = __ldcg(reinterpret_cast<const uint4 *>(row + k0));
-                    const uint32_t w[4] = {qv.x, qv.y, qv.z, qv.w};
-                    uint32_t m = 0;
-#pragma unroll
-                    for (int j = 0; j < 4; j++) m |= ((w[j] & 0xffffu) ? 1u : 0u) << (2 * j) | ((w[j] >> 16) ? 2u : 0u) << (2 * j);
-                    if (m) first = (uint32_t)k0 + __ffs(m) - 1;
-                } else {
-                    for (int u = 0; u < 8; u++) {
-                        const int64_t kk = k0 + u;
-                        if (kk < wmax && __ldcg(row + kk) != 0) { first = (uint32_t)kk; break; }
-                    }
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, first != 0xffffffffu);
-                if (m) res = __shfl_sync(0xffffffffu, first, __ffs(m) - 1);
-            }
-        }
-        if (lane == 0) g.lead[r] = res;
-    }
 }
 
 // INT-pipe reference engine for the same op (tests / GBLA_DENSE_INT).
@@ -1392,8 +1341,7 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
                            const uint8_t *Flo, const uint8_t *Fhi, const uint32_t *rows, const uint32_t *sel,
                            const uint32_t *nrows_dev, const uint32_t *kp_dev, const int64_t *c0_dev,
                            const int64_t *win_dev, int64_t win_w, uint16_t *D, int64_t ldD, uint32_t *flags,
-                           uint32_t epoch, int grid, uint32_t *lead, const uint32_t *rowpiv, int64_t mN,
-                           uint8_t *Rlo2, uint8_t *Rhi2)
+                           uint32_t epoch, int grid, uint8_t *Rlo2, uint8_t *Rhi2)
 {
     static unsigned long long attr = 0;   // devices done (dev_bit)
     if (!(attr & dev_bit())) {
@@ -1401,7 +1349,7 @@ gbla_status modgemm_tc_win(cudaStream_t st, int64_t cols, Field F, const uint8_t
         attr |= dev_bit();
     }
     WinArgs a{F, Tlo, Thi, Bglo, Bghi, Rlo, Rhi, Rlo2, Rhi2, Flo, Fhi, rows, sel, nrows_dev, kp_dev, c0_dev, win_dev,
-              win_w, cols, D, ldD, flags, epoch, lead, rowpiv, mN};
+              win_w, cols, D, ldD, flags, epoch};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(ws_threads(8));

@@ -397,20 +397,6 @@ def test_echelon_engines_agree_c0_and_dense(gb, ctx, c0_matrix, c0_oracle):
             check_full(gb, ctx, M, res, flags=f)
 
 
-def test_sweep_two_step_lookahead(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
-    """GBLA_SWEEP_PAIRS=1: odd 128-pivot blocks computed from X_I, I <= J-2, with the modified band
-    tiles A'_IJ = A_IJ + A_{I,J-1} A_{J-1,J} and G_{J-1} = inv(A_{J-1,J-1}) A_{J-1,J} (same X = C A^-1,
-    so D_new, the op count and R are unchanged), also with forced small X-tile batches."""
-    monkeypatch.setenv("GBLA_SWEEP_PAIRS", "1")
-    check_full(gb, ctx, c0_matrix, c0_oracle)
-    for name, sc in (("c1", 0.05), ("c2", 0.02), ("c3", 0.03)):
-        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
-        check_full(gb, ctx, M, oracle.reduce(M))
-    monkeypatch.setenv("GBLA_XT_BATCH", "2")
-    M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.05))
-    check_full(gb, ctx, M, oracle.reduce(M))
-
-
 def check_ref(gb, h, res, p):
     """GBLA_ECHELON_REF output against the oracle: same rank and pivot columns, leading 1s, zeros
     left of every pivot and below it, and RREF(R_ref) (computed by the oracle) = the oracle's R."""
