@@ -249,6 +249,15 @@ gbla_status gbla_densify_quadrant(gbla_mat h, char which, uint16_t *out, int64_t
  * synchronized).  Device pointers, owned by h; *npairs = ceil(n_piv / 2). */
 gbla_status gbla_get_multilines(gbla_mat h, void *stream, int64_t *npairs, const uint64_t **ptr,
                                 const uint32_t **col, const uint32_t **val);
+/* Column runs of the multilines (north star "device sparse-row format with column runs"; the
+ * device analogue of Format 2's run compression (f, s)), built with them on first use:
+ * the slots of pair k are cut into maximal runs of consecutive columns (also cut where the pair's
+ * own diagonal-block columns end and where its N columns begin), runs [run_ptr[k], run_ptr[k+1]);
+ * run r covers columns run_col[r] .. run_col[r] + run_len[r] - 1 at the pair's slots
+ * run_slot[r] .. (relative to the pair's first slot; values in the multiline val array).  The
+ * INT-pipe engine (GBLA_SPARSE_INT) walks these runs.  Device pointers owned by h. */
+gbla_status gbla_get_multiline_runs(gbla_mat h, void *stream, int64_t *nruns, const uint64_t **run_ptr,
+                                    const uint32_t **run_col, const uint32_t **run_len, const uint32_t **run_slot);
 /* R (rank x nN, stride *ld) and pivcol[rank] after gbla_echelon_D. */
 gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol,
                           const uint16_t **R, int64_t *ld);

@@ -103,6 +103,7 @@ def load_library(path: str = LIB_PATH):
         "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
         "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
         "gbla_rref_M": ([vp, vp, P(i64)], st),
+        "gbla_get_multiline_runs": ([vp, vp, P(i64), P(vp), P(vp), P(vp), P(vp)], st),
         "gbla_file_info_parse": ([vp, ctypes.c_size_t, ctypes.c_int, P(_FileInfo)], st),
         "gbla_file_decode": ([vp, vp, ctypes.c_size_t, ctypes.c_int, vp, vp, vp, vp], st),
         "gbla_get_rref_M": ([vp, P(_CSR)], st),
@@ -125,7 +126,7 @@ def exported_symbols():
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
             "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M",
-            "gbla_file_info_parse", "gbla_file_decode"]
+            "gbla_file_info_parse", "gbla_file_decode", "gbla_get_multiline_runs"]
 
 
 def _check(status: int):
@@ -299,6 +300,18 @@ class Mat:
         P = _view(ptr.value, (npr.value + 1,), "<u8").clone()
         ns = int(P[-1].item()) if npr.value >= 0 else 0
         return P, _view(col.value, (ns,), "<u4").clone(), _view(val.value, (ns,), "<u4").clone()
+
+    def multiline_runs(self, stream=None):
+        """Column runs of the multilines (gbla_get_multiline_runs): (run_ptr[npairs+1], run_col,
+        run_len, run_slot) as new torch tensors."""
+        nr, ptr, col, ln, sl = (ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(),
+                                ctypes.c_void_p())
+        _check(_lib.gbla_get_multiline_runs(self._h, _stream_ptr(stream), ctypes.byref(nr), ctypes.byref(ptr),
+                                            ctypes.byref(col), ctypes.byref(ln), ctypes.byref(sl)))
+        npairs = (self.dims()[0] + 1) // 2
+        n = nr.value
+        return (_view(ptr.value, (npairs + 1,), "<u8").clone(), _view(col.value, (n,), "<u4").clone(),
+                _view(ln.value, (n,), "<u4").clone(), _view(sl.value, (n,), "<u4").clone())
 
     def rref(self):
         """(rank, pivcol[rank], R[rank x nN]) as new torch tensors."""

@@ -507,6 +507,21 @@ extern "C" gbla_status gbla_get_multilines(gbla_mat h, void *stream, int64_t *np
     return GBLA_OK;
 }
 
+extern "C" gbla_status gbla_get_multiline_runs(gbla_mat h, void *stream, int64_t *nruns, const uint64_t **run_ptr,
+                                               const uint32_t **run_col, const uint32_t **run_len,
+                                               const uint32_t **run_slot)
+{
+    GBLA_TRY(check_mat(h, stream));
+    GBLA_TRY(ensure_multilines(h));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (nruns) *nruns = h->nruns;
+    if (run_ptr) *run_ptr = h->mr_ptr;
+    if (run_col) *run_col = h->mr_col;
+    if (run_len) *run_len = h->mr_len;
+    if (run_slot) *run_slot = h->mr_rel;
+    return GBLA_OK;
+}
+
 extern "C" gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t **pivcol, const uint16_t **R,
                                      int64_t *ld)
 {

@@ -196,6 +196,12 @@ struct gbla_mat_s {
     uint16_t *ml_a01 = nullptr;        // [npairs] A[2k][2k+1]
     uint32_t *ab_w = nullptr;          // [npiv] nnz of pivot row
     int64_t nslots = 0;
+    // column runs of the multiline slots (splice.cu k_mlr_*): pair k has runs [mr_ptr[k], mr_ptr[k+1]);
+    // run r = columns mr_col[r] .. + mr_len[r] - 1 at slots ml_ptr[k] + mr_rel[r] ..; the first run of
+    // the N part / after the pair's own diagonal-block slots: mr_np[k] / mr_skip[k]
+    uint64_t *mr_ptr = nullptr, *mr_skip = nullptr, *mr_np = nullptr;
+    uint32_t *mr_col = nullptr, *mr_len = nullptr, *mr_rel = nullptr;
+    int64_t nruns = 0;
 
     // dense matrices
     uint16_t *D = nullptr; int64_t ldD = 0;     // mN x nN (current D)

@@ -34,7 +34,9 @@ __global__ void __launch_bounds__(256) k_reduce_targets(
     const uint32_t *__restrict__ ml_val, const uint32_t *__restrict__ ml_np, const uint32_t *__restrict__ ml_skip,
     const uint16_t *__restrict__ ml_a01, const uint32_t *__restrict__ ab_w, const uint32_t *__restrict__ ab_np,
     uint64_t *__restrict__ scratch, uint16_t *__restrict__ D, int64_t ldD, uint16_t *__restrict__ X, int64_t ldX,
-    uint64_t *__restrict__ opcount, unsigned int *__restrict__ next)
+    uint64_t *__restrict__ opcount, unsigned int *__restrict__ next, const uint64_t *__restrict__ mr_ptr,
+    const uint64_t *__restrict__ mr_skip, const uint64_t *__restrict__ mr_np, const uint32_t *__restrict__ mr_col,
+    const uint32_t *__restrict__ mr_len, const uint32_t *__restrict__ mr_rel)
 {
     uint64_t *acc = scratch + (size_t)blockIdx.x * n;
     __shared__ uint32_t s_t;
@@ -75,14 +77,37 @@ __global__ void __launch_bounds__(256) k_reduce_targets(
             }
             if ((l1 | l2) == 0) continue;   // uniform across the CTA (lightweight test)
             const uint64_t n1 = fneg(l1, F), n2 = fneg(l2, F);
-            uint64_t q0, q1;
-            if (MODE == MODE_FUSED) { q0 = ml_ptr[k] + ml_skip[k]; q1 = ml_ptr[k + 1]; }
-            else if (MODE == MODE_CPRIME) { q0 = ml_ptr[k] + ml_skip[k]; q1 = ml_ptr[k] + ml_np[k]; }
-            else { q0 = ml_ptr[k] + ml_np[k]; q1 = ml_ptr[k + 1]; }
-            for (uint64_t q = q0 + tid; q < q1; q += nth) {
-                const uint32_t c = ml_col[q];
-                const uint32_t v = ml_val[q];
-                acc[c] += n1 * (v & 0xffffu) + n2 * (v >> 16);
+            if (mr_ptr) {
+                // column runs (GBLA_INT_RUNS=1; a warp per run, lanes over its consecutive columns):
+                // one 12-byte descriptor per run instead of a 4-byte column id per slot.  Measured
+                // slower on c1 (1523 vs 273 ms; a thread per run: 3159 ms): the accumulator lives in
+                // global memory and the slot walk's 32 consecutive slots per warp access are the
+                // coalesced ones; runs of ~8 columns leave most lanes idle
+                uint64_t r0, r1;
+                if (MODE == MODE_FUSED) { r0 = mr_skip[k]; r1 = mr_ptr[k + 1]; }
+                else if (MODE == MODE_CPRIME) { r0 = mr_skip[k]; r1 = mr_np[k]; }
+                else { r0 = mr_np[k]; r1 = mr_ptr[k + 1]; }
+                const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
+                const uint32_t *vals = ml_val + ml_ptr[k];
+                for (uint64_t r = r0 + warp; r < r1; r += nw) {
+                    const uint32_t c0 = mr_col[r], len = mr_len[r];
+                    const uint32_t *vr = vals + mr_rel[r];
+                    uint64_t *ar = acc + c0;
+                    for (uint32_t u = lane; u < len; u += 32) {
+                        const uint32_t v = vr[u];
+                        ar[u] += n1 * (v & 0xffffu) + n2 * (v >> 16);
+                    }
+                }
+            } else {
+                uint64_t q0, q1;
+                if (MODE == MODE_FUSED) { q0 = ml_ptr[k] + ml_skip[k]; q1 = ml_ptr[k + 1]; }
+                else if (MODE == MODE_CPRIME) { q0 = ml_ptr[k] + ml_skip[k]; q1 = ml_ptr[k] + ml_np[k]; }
+                else { q0 = ml_ptr[k] + ml_np[k]; q1 = ml_ptr[k + 1]; }
+                for (uint64_t q = q0 + tid; q < q1; q += nth) {
+                    const uint32_t c = ml_col[q];
+                    const uint32_t v = ml_val[q];
+                    acc[c] += n1 * (v & 0xffffu) + n2 * (v >> 16);
+                }
             }
             if (tid == 0) {
                 if (MODE == MODE_FUSED) {
@@ -185,6 +210,9 @@ gbla_status launch_targets(gbla_mat h)
     cudaStream_t st = h->stream;
     if (h->mN == 0) return GBLA_OK;
     GBLA_TRY(ensure_multilines(h));
+    // GBLA_INT_RUNS=1: walk the column runs of the multilines instead of their column ids (slower, see
+    // k_reduce_targets)
+    const bool runs = getenv("GBLA_INT_RUNS") && atoi(getenv("GBLA_INT_RUNS")) == 1;
     int per_sm = 0;
     GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce_targets<MODE>, 256, 0));
     if (per_sm < 1) per_sm = 1;
@@ -198,7 +226,8 @@ gbla_status launch_targets(gbla_mat h)
     k_reduce_targets<MODE><<<(unsigned)grid, 256, 0, st>>>(
         h->mN, h->n, h->npiv, h->npairs, h->F, h->order, h->tlead, h->cd_ptr, h->cd_col, h->cd_val, h->ml_ptr,
         h->ml_col, h->ml_val, h->ml_np, h->ml_skip, h->ml_a01, h->ab_w, h->ab_np, scratch, h->D, h->ldD, h->X, h->ldX,
-        h->opcount, next); note_launch();
+        h->opcount, next, runs ? h->mr_ptr : nullptr, h->mr_skip, h->mr_np, h->mr_col, h->mr_len, h->mr_rel);
+    note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }

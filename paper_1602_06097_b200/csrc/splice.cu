@@ -213,6 +213,69 @@ __global__ void k_ml_fill(int64_t npairs, int64_t npiv, const uint64_t *__restri
     a01[k] = v01;
 }
 
+// Column runs of the multilines (north star "device sparse-row format with column runs"; the
+// device analogue of Format 2's run compression (f, s)): the slots of pair k are cut into
+// maximal runs of consecutive columns, also cut where the pair's own diagonal-block slots end
+// (ml_skip) and where its N part begins (ml_np), so every consumer's slot range is a run range.
+// Run r: start column mr_col[r], length mr_len[r], first slot ml_ptr[k] + mr_rel[r].  One warp per
+// pair; runs found by ballots over the slots (count pass, then fill pass).
+__device__ __forceinline__ bool ml_run_start(const uint32_t *col, uint64_t q, uint64_t q0, uint64_t qs, uint64_t qn)
+{
+    return q == q0 || q == qs || q == qn || col[q] != col[q - 1] + 1;
+}
+__global__ void k_mlr_count(int64_t npairs, const uint64_t *__restrict__ ml_ptr, const uint32_t *__restrict__ ml_col,
+                            const uint32_t *__restrict__ ml_skip, const uint32_t *__restrict__ ml_np,
+                            uint64_t *__restrict__ cnt)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (k > npairs) return;
+    if (k == npairs) { if (lane == 0) cnt[k] = 0; return; }
+    const uint64_t q0 = ml_ptr[k], q1 = ml_ptr[k + 1], qs = q0 + ml_skip[k], qn = q0 + ml_np[k];
+    uint32_t c = 0;
+    for (uint64_t q = q0 + lane; q < q1; q += 32) c += ml_run_start(ml_col, q, q0, qs, qn);
+    c = __reduce_add_sync(FULL, c);
+    if (lane == 0) cnt[k] = c;
+}
+__global__ void k_mlr_fill(int64_t npairs, const uint64_t *__restrict__ ml_ptr, const uint32_t *__restrict__ ml_col,
+                           const uint32_t *__restrict__ ml_skip, const uint32_t *__restrict__ ml_np,
+                           const uint64_t *__restrict__ mr_ptr, uint32_t *__restrict__ mr_col,
+                           uint32_t *__restrict__ mr_len, uint32_t *__restrict__ mr_rel,
+                           uint64_t *__restrict__ mr_skip, uint64_t *__restrict__ mr_np)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (k >= npairs) return;
+    const uint64_t q0 = ml_ptr[k], q1 = ml_ptr[k + 1], qs = q0 + ml_skip[k], qn = q0 + ml_np[k];
+    uint64_t r = mr_ptr[k];                           // next run index of this pair
+    if (lane == 0) { mr_skip[k] = mr_ptr[k + 1]; mr_np[k] = mr_ptr[k + 1]; }
+    __syncwarp();
+    for (uint64_t base = q0; base < q1; base += 32) {
+        const uint64_t q = base + lane;
+        const bool st = q < q1 && ml_run_start(ml_col, q, q0, qs, qn);
+        const unsigned m = __ballot_sync(FULL, st);
+        if (st) {
+            const uint64_t ri = r + __popc(m & ((1u << lane) - 1));
+            mr_col[ri] = ml_col[q];
+            mr_rel[ri] = (uint32_t)(q - q0);
+            if (q == qs) mr_skip[k] = ri;
+            if (q == qn) mr_np[k] = ri;
+        }
+        r += __popc(m);
+    }
+    __syncwarp();
+    // lengths: next run's first slot (or the pair's end) minus this run's
+    for (uint64_t ri = mr_ptr[k] + lane; ri < mr_ptr[k + 1]; ri += 32) {
+        const uint64_t e = ri + 1 < mr_ptr[k + 1] ? mr_rel[ri + 1] : q1 - q0;
+        mr_len[ri] = (uint32_t)(e - mr_rel[ri]);
+    }
+    // a boundary at the pair's end (no skip / N slots) is the end index, set above
+    if (lane == 0) {
+        if (qs >= q1) mr_skip[k] = mr_ptr[k + 1];
+        if (qn >= q1) mr_np[k] = mr_ptr[k + 1];
+    }
+}
+
 // w[i] = nnz of sigma-ordered pivot row i
 __global__ void k_row_w(int64_t npiv, const uint64_t *__restrict__ ab_ptr, uint32_t *__restrict__ w)
 {
@@ -431,6 +494,23 @@ gbla_status ensure_multilines(gbla_mat h)
     if (np2)
         k_ml_fill<<<grid_for(np2, 128), 128, 0, st>>>(np2, npiv, h->ab_ptr, h->ab_col, h->ab_val, h->ml_ptr,
                                                       h->ml_col, h->ml_val, h->ml_a01); note_launch();
+    // column runs over the multiline slots
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->mr_ptr));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->mr_skip));
+    GBLA_TRY(dalloc_t(h, np2 + 1, &h->mr_np));
+    k_mlr_count<<<grid_for((np2 + 1) * 32, 256), 256, 0, st>>>(np2, h->ml_ptr, h->ml_col, h->ml_skip, h->ml_np, cnt);
+    note_launch();
+    GBLA_TRY(exclusive_scan<uint64_t>(h, cnt, h->mr_ptr, np2 + 1));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(&tmp64, h->mr_ptr + np2, 8, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    h->nruns = (int64_t)tmp64;
+    GBLA_TRY(dalloc_t(h, h->nruns + 1, &h->mr_col));
+    GBLA_TRY(dalloc_t(h, h->nruns + 1, &h->mr_len));
+    GBLA_TRY(dalloc_t(h, h->nruns + 1, &h->mr_rel));
+    if (np2)
+        k_mlr_fill<<<grid_for(np2 * 32, 256), 256, 0, st>>>(np2, h->ml_ptr, h->ml_col, h->ml_skip, h->ml_np, h->mr_ptr,
+                                                            h->mr_col, h->mr_len, h->mr_rel, h->mr_skip, h->mr_np);
+    note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
 }

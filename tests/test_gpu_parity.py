@@ -115,9 +115,56 @@ def test_multilines_match_oracle_definition(gb, ctx):
         h.free()
 
 
+def test_multiline_column_runs(gb, ctx):
+    """a2: the column runs of the device multilines (gbla_get_multiline_runs) decode to exactly the
+    multiline columns, and are the maximal runs of the paper's run rule (the reference
+    codec's encode_colids) cut only at the pair's diagonal-block end and its first N column."""
+    from oracle import formats as fm
+    cases = list(gbla_gen.random_suite(30, seed0=37)) + [gbla_gen.f4_matrix("c0")]
+    cases.append(gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c3"], 0.02)))
+    for M in cases:
+        S = oracle.splice(M)
+        rp, c, v = to_dev(M)
+        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+        ptr, col, val = (np_(t) for t in h.multilines())
+        rptr, rcol, rlen, rslot = (np_(t).astype(np.int64) for t in h.multiline_runs())
+        for k in range((S.npiv + 1) // 2):
+            q0, q1 = int(ptr[k]), int(ptr[k + 1])
+            cols = col[q0:q1].astype(np.int64)
+            runs = list(range(int(rptr[k]), int(rptr[k + 1])))
+            dec = np.concatenate([np.arange(rcol[r], rcol[r] + rlen[r]) for r in runs]) if runs else np.zeros(0)
+            assert np.array_equal(dec, cols), k
+            assert all(np.array_equal(cols[rslot[r]:rslot[r] + rlen[r]], np.arange(rcol[r], rcol[r] + rlen[r]))
+                       for r in runs), k
+            # the run rule on the pieces between the cut points
+            cuts = sorted({0, int(np.searchsorted(cols, min(2 * k + 2, S.npiv))), int(np.searchsorted(cols, S.npiv)),
+                           cols.size})
+            exp = []
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                t = fm.encode_colids(cols[a:b])
+                i = 0
+                while i < len(t):
+                    if t[i] & fm.MASK:
+                        exp.append((t[i] & ~fm.MASK, 1)); i += 1
+                    else:
+                        exp.append((t[i], t[i + 1])); i += 2
+            assert [(int(rcol[r]), int(rlen[r])) for r in runs] == exp, k
+        h.free()
+
+
 def test_pipeline_random_suite_new_order(gb, ctx):
     for M in gbla_gen.random_suite(150, seed0=23):
         check_full(gb, ctx, M)
+
+
+def test_int_pipe_over_column_runs(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """The INT-pipe engine walking the multilines' column runs (GBLA_INT_RUNS=1) gives the same
+    D_new, op counts and R as the oracle (c0, a random suite, scaled c1)."""
+    monkeypatch.setenv("GBLA_INT_RUNS", "1")
+    check_full(gb, ctx, c0_matrix, c0_oracle, flags=gb.GBLA_SPARSE_INT)
+    for M in list(gbla_gen.random_suite(30, seed0=41)) + [gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.03))]:
+        check_full(gb, ctx, M, flags=gb.GBLA_SPARSE_INT)
+    monkeypatch.delenv("GBLA_INT_RUNS")
 
 
 def test_pipeline_random_suite_int_pipe(gb, ctx):
