@@ -76,7 +76,8 @@ constexpr uint32_t NONE16 = 0xffffffffu;
 struct P2State {
     int64_t c0, c1;                     // panel columns [c0, c1)
     uint32_t kp;                        // pivots
-    uint32_t nrows;                     // rows listed for the trailing update
+    uint32_t nrows;                     // rows (slots) of the trailing update
+    uint32_t ntouch;                    // of which rows with a nonzero coefficient (the op counts)
     uint32_t ncand;                     // candidates integrated
     uint32_t ready;                     // epoch: sel / pc / kp / c0 / c1 / rowpiv marks are published
     uint32_t sel[PK];                   // selected rows (D row ids), pivot order of T
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     if (wmax > PW) wmax = PW;
     if (wmax <= 0) {
         if (tid == 0) {
-            cur->c0 = c0; cur->c1 = c0; cur->kp = 0; cur->nrows = 0; cur->ncand = 0;
+            cur->c0 = c0; cur->c1 = c0; cur->kp = 0; cur->nrows = 0; cur->ntouch = 0; cur->ncand = 0;
             if (epoch) {
                 __threadfence();
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&cur->ready), "r"(epoch) : "memory");
@@ -877,6 +878,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                     cur->c1 = c0 + width;
                     cur->kp = nb;
                     cur->nrows = 0;
+                    cur->ntouch = 0;
                     cur->ncand = ncand_tot;
                 }
                 __syncthreads();
@@ -1147,6 +1149,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
         cur->c1 = c0 + width;
         cur->kp = nb;
         cur->nrows = 0;
+        cur->ntouch = 0;
         cur->ncand = ncand_tot;
     }
     if (epoch && !published) {
@@ -1167,7 +1170,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           uint8_t *__restrict__ Flo, uint8_t *__restrict__ Fhi, uint32_t *__restrict__ rows,
                           const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
                           uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr,
-                          int ref = 0, uint32_t epoch = 0, const uint32_t *__restrict__ spos = nullptr)
+                          int ref = 0, uint32_t epoch = 0, const uint32_t *__restrict__ spos = nullptr,
+                          const uint32_t *__restrict__ skey = nullptr)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -1187,27 +1191,53 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     const int lane = threadIdx.x & 31;
     const uint32_t kp = ps->kp;
     if (kb_c0 && blockIdx.x == 0 && threadIdx.x == 0) kb_c0[j] = ps->c0;
+    // prefix mode (skey != NULL: D's rows sorted by their initial leading column, skey the sorted
+    // leads): the rows that can have a nonzero coefficient are exactly [0, #{ilead < c1}), and row i
+    // takes slot i -- the trailing GEMM's 128-row tiles are consecutive rows of D (untouched rows
+    // and this panel's pivot rows get zero factors and the row index NONE: no D traffic)
+    int64_t nlim = mN;
+    if (skey) {
+        __shared__ uint32_t s_nt;
+        if (threadIdx.x == 0) {
+            const int64_t c = ps->c1;
+            int64_t lo = 0, hi = mN;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)skey[mid] < c) lo = mid + 1;
+                else hi = mid;
+            }
+            s_nt = kp ? (uint32_t)lo : 0u;
+            if (blockIdx.x == 0) ps->nrows = s_nt;
+        }
+        __syncthreads();
+        nlim = s_nt;
+    }
     if (kp == 0) return;
-    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mN;
+    uint32_t touched = 0;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlim;
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     if (owner && owner[i] != me) continue;                     // another rank's row
     const uint32_t rp = rowpiv[i];
-    if (rp != GBLA_NONE && (rp >= (uint64_t)ps->c0 || ref)) continue;   // selected now: becomes Rn;
-                                                                         // REF: no back elimination
+    const bool skip = rp != GBLA_NONE && (rp >= (uint64_t)ps->c0 || ref);   // selected now: becomes Rn;
+                                                                             // REF: no back elimination
     const uint16_t *drow = D + (size_t)i * ldD;
     uint16_t v[CPL];
     bool nz = false;
 #pragma unroll
     for (int u = 0; u < CPL; u++) {
         const uint32_t b = lane * CPL + u;
-        v[u] = b < kp ? drow[ps->pc[b]] : 0;
+        v[u] = (!skip && b < kp) ? drow[ps->pc[b]] : 0;
         nz |= v[u] != 0;
     }
-    if (!__any_sync(FULL, nz)) continue;
-    uint32_t slot = 0;
-    if (lane == 0) slot = atomicAdd(&ps->nrows, 1u);
-    slot = __shfl_sync(FULL, slot, 0);
-    if (lane == 0) rows[slot] = (uint32_t)i;
+    const bool any = __any_sync(FULL, nz);
+    if (!any && !skey) continue;
+    uint32_t slot = (uint32_t)i;
+    if (!skey) {
+        if (lane == 0) slot = atomicAdd(&ps->nrows, 1u);
+        slot = __shfl_sync(FULL, slot, 0);
+    }
+    if (lane == 0) rows[slot] = any ? (uint32_t)i : GBLA_NONE;
+    touched += any ? 1u : 0u;
     uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int u = 0; u < CPL; u++) {
@@ -1217,13 +1247,14 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
     const size_t o = (size_t)(slot / 128) * (PK * 128) + tc::toff(slot % 128, lane * CPL);
     *reinterpret_cast<uint32_t *>(Flo + o) = lo;
     *reinterpret_cast<uint32_t *>(Fhi + o) = hi;
-    if (Fdlo) {
+    if (Fdlo && any) {
         const uint32_t q = spos ? spos[i] : (uint32_t)i;       // slot of row i in the flush's row order
         const size_t od = (size_t)((q / 128) * G + j) * (PK * 128) + tc::toff(q % 128, lane * CPL);
         *reinterpret_cast<uint32_t *>(Fdlo + od) = lo;
         *reinterpret_cast<uint32_t *>(Fdhi + od) = hi;
     }
     }
+    if (lane == 0 && touched) atomicAdd(&ps->ntouch, touched);
 }
 
 // Deferred updates: the factors of this panel's selected rows S_b in the earlier K-blocks
@@ -1327,10 +1358,10 @@ __global__ void k_gather_st2(int64_t nN, const uint16_t *__restrict__ D, int64_t
     tc::pdl_wait();
     if (ops && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && ps->c0 < nN) {
         const unsigned long long w = (unsigned long long)(nN - ps->c0);
-        ops[0] += (unsigned long long)ps->nrows * ps->kp * w;                 // trailing update
+        ops[0] += (unsigned long long)ps->ntouch * ps->kp * w;                // trailing update
         ops[1] += (unsigned long long)ps->kp * ps->kp * w;                     // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * ps->kp * (unsigned long long)(ps->c1 - ps->c0);   // panel RREF
-        ops[3] += (unsigned long long)ps->nrows * w;                          // D entries of the update
+        ops[3] += (unsigned long long)ps->ntouch * w;                         // D entries of the update
     }
     const uint32_t kp = ps->kp;
     if (kp == 0) return;
@@ -1373,10 +1404,10 @@ __global__ void k_commit2(int64_t nN, uint16_t *__restrict__ D, int64_t ldD, con
     const int64_t c0 = ps->c0;
     if (ops && part != 1 && b == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c0 < nN) {
         const unsigned long long w = (unsigned long long)(nN - c0);
-        ops[0] += (unsigned long long)ps->nrows * kp * w;                     // trailing update
+        ops[0] += (unsigned long long)ps->ntouch * kp * w;                    // trailing update
         ops[1] += (unsigned long long)kp * kp * w;                             // new pivot rows
         ops[2] += (unsigned long long)ps->ncand * kp * (unsigned long long)(ps->c1 - c0);   // panel RREF
-        ops[3] += (unsigned long long)ps->nrows * w;                                       // D entries of the update
+        ops[3] += (unsigned long long)ps->ntouch * w;                                      // D entries of the update
     }
     // grid-stride over (row b, 8-column group); a few hundred blocks, so the next panel's
     // CTA is not queued behind thousands of tiny ones
@@ -1415,6 +1446,7 @@ __global__ void k_p2_init(P2State *ps)
     ps[1].c0 = ps[1].c1 = 0;
     ps[0].kp = ps[1].kp = 0;
     ps[0].nrows = ps[1].nrows = 0;
+    ps[0].ntouch = ps[1].ntouch = 0;
     ps[0].ready = ps[1].ready = 0;
 }
 
@@ -1638,6 +1670,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         GBLA_TRY(dalloc_t(h, rd_stride * G, &Rphi));
     }
     uint32_t *srow = nullptr, *spos = nullptr, *skey = nullptr, *nflush = nullptr;
+    bool sorted_rows = false;                 // D physically in lead order: per-panel rows in prefix mode
     if (G > 1) {                              // (c1-sized D: the panel chain is the critical path)
         uint32_t *ilead, *iota;
         GBLA_TRY(dalloc_t(h, mN, &ilead));
@@ -1671,6 +1704,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             h->D = D2;
             srow = nullptr;                   // identity from here on
             spos = nullptr;
+            sorted_rows = !getenv("GBLA_NO_PREFIX_SLOTS");
         } else {
             cudaGetLastError();
         }
@@ -1737,7 +1771,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         // of K11) comes out nearly sorted, which keeps K11's scattered row accesses TLB/DRAM friendly
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
                                                          rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0,
-                                                         h->ref_only ? 1 : 0, (uint32_t)(k + 1), spos);
+                                                         h->ref_only ? 1 : 0, (uint32_t)(k + 1), spos,
+                                                         sorted_rows ? (const uint32_t *)skey : nullptr);
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush

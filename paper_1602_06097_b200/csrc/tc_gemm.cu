@@ -336,14 +336,15 @@ __global__ void __launch_bounds__(ws_threads(EPI_WARPS), 1) k_modgemm_ws(MMArgs 
             live_n = slot_n < nr;
             if (rt != rt_c) {
                 rt_c = rt;
-                rowbase = live_n && slot_n < nwr ? C + (size_t)(g.rowidx ? g.rowidx[slot_n] : slot_n) * g.ldc
-                                                 : nullptr;
+                // a row index NONE (a slot of the echelon's prefix mode with zero factors): no D traffic
+                const uint32_t ri = live_n && slot_n < nwr ? (g.rowidx ? g.rowidx[slot_n] : (uint32_t)slot_n) : GBLA_NONE;
+                rowbase = ri != GBLA_NONE ? C + (size_t)ri * g.ldc : nullptr;
             }
-            crow_n = live_n && slot_n < nwr ? rowbase + x0_n : nullptr;
+            crow_n = rowbase ? rowbase + x0_n : nullptr;
             fast_n = crow_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
             for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
-            if (MODE == MODE_SUB && live_n && g.exp != 1) {
+            if (MODE == MODE_SUB && crow_n && g.exp != 1) {
                 if (fast_n) {
 #pragma unroll
                     for (int u = 0; u < EPI_COLS / 8; u++) {
@@ -740,13 +741,14 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_mk2(MMArgs g)
             live_n = slot < nr;
             if (rt2 != rt_c) {
                 rt_c = rt2;
-                rowbase = live_n ? C + (size_t)(g.rowidx ? g.rowidx[slot] : slot) * g.ldc : nullptr;
+                const uint32_t ri = live_n ? (g.rowidx ? g.rowidx[slot] : (uint32_t)slot) : GBLA_NONE;
+                rowbase = ri != GBLA_NONE ? C + (size_t)ri * g.ldc : nullptr;
             }
-            crow_n = live_n ? rowbase + x0_n : nullptr;
+            crow_n = rowbase ? rowbase + x0_n : nullptr;
             fast_n = crow_n && vec && x0_n + EPI_COLS <= cols;
 #pragma unroll
             for (int w = 0; w < EPI_COLS / 2; w++) dn[w] = 0;
-            if (live_n && g.exp != 1) {
+            if (crow_n && g.exp != 1) {
                 if (fast_n) {
 #pragma unroll
                     for (int u = 0; u < EPI_COLS / 16; u++)
@@ -1002,7 +1004,10 @@ __global__ void __launch_bounds__(ws_threads(8), 1) k_modgemm_win(WinArgs g)
             const int64_t slot = (rn ? 0 : rt * BM) + quarter * 32 + lane;
             const bool live = rn ? slot < BM : slot < nr;            // rows of the accumulator
             uint16_t *crow = nullptr;
-            if (rn ? slot < (int64_t)kp : live) crow = C + (size_t)(rn ? g.sel[slot] : g.rows[slot]) * g.ldD + x0;
+            if (rn ? slot < (int64_t)kp : live) {
+                const uint32_t ri = rn ? g.sel[slot] : g.rows[slot];
+                if (ri != GBLA_NONE) crow = C + (size_t)ri * g.ldD + x0;        // NONE: zero factors
+            }
             const bool fast = crow && x0 + EPI_COLS <= cols && (g.ldD % 8 == 0) &&
                               ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
             uint32_t dv[EPI_COLS / 2];
