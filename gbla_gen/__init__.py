@@ -220,3 +220,50 @@ def gb_like_matrix(m: int, n: int, npoly: int, plen: int, p: int, seed: int, run
     col = np.concatenate([c for c, _ in rows]).astype(np.uint32) if m else np.zeros(0, np.uint32)
     val = np.concatenate([v for _, v in rows]).astype(np.uint16) if m else np.zeros(0, np.uint16)
     return CSR(m=m, n=n, p=p, row_ptr=rp, col=col, val=val, name=f"gblike{m}x{n}s{seed}")
+
+
+# ---- residues below 2^31 (input generation only) --------------------------------
+@dataclass
+class WideCSR:
+    """Host CSR over GF(p), p < 2^31: row_ptr u64[m+1], col u32[nnz], val u32[nnz]."""
+    m: int
+    n: int
+    p: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    name: str = ""
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if self.m else 0
+
+    def dense(self) -> np.ndarray:
+        a = np.zeros((self.m, self.n), np.int64)
+        for i in range(self.m):
+            s, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+            a[i, self.col[s:e].astype(np.int64)] = self.val[s:e]
+        return a
+
+
+def random_wide(m: int, n: int, density: float, p: int, seed: int) -> WideCSR:
+    """Random sparse matrix with residues in [1, p) (input generation only; zero rows allowed)."""
+    rng = np.random.default_rng(seed)
+    rp, cols, vals = [0], [], []
+    for _ in range(m):
+        k = int(rng.binomial(n, density))
+        c = np.sort(rng.choice(n, k, replace=False)) if k else np.zeros(0, np.int64)
+        cols.append(c)
+        vals.append(rng.integers(1, p, c.size))
+        rp.append(rp[-1] + c.size)
+    col = np.concatenate(cols).astype(np.uint32) if cols else np.zeros(0, np.uint32)
+    val = np.concatenate(vals).astype(np.uint32) if vals else np.zeros(0, np.uint32)
+    return WideCSR(m, n, p, np.array(rp, np.uint64), col, val, f"wide{m}x{n}p{p}s{seed}")
+
+
+def widen(M, p: int, seed: int) -> WideCSR:
+    """An F4-shaped matrix's pattern (a gbla_gen CSR) with values redrawn in [1, p)."""
+    rng = np.random.default_rng(seed)
+    val = rng.integers(1, p, M.col.size).astype(np.uint32)
+    return WideCSR(M.m, M.n, p, M.row_ptr.astype(np.uint64), M.col.astype(np.uint32), val,
+                   f"{M.name}-p{p}")

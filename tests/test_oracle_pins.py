@@ -314,3 +314,30 @@ def test_full_rref_of_M_against_textbook_gauss_jordan(c0_matrix, c0_oracle):
         assert rk == r, M.name
         assert np.array_equal(RM.astype(np.int64), R), M.name
         assert pc.tolist() == piv, M.name
+
+
+def test_wide_field_oracle_pins(c0_matrix, c0_oracle):
+    """f4 oracle (oracle/wide.py, p < 2^31): against the brute-force Gauss-Jordan of the whole M*sigma
+    (the first n_piv columns are pivots, rank(M) = n_piv + rank(D_new), R = the bottom-right block)
+    for p up to 2^31 - 1, and equal to the C oracle (D_new, modMACs, R) for p < 2^16."""
+    from oracle import wide
+    from pins import brute_rref
+    for p in (3, 65521, 1048573, 8388593, 2147483647):
+        for s in range(12):
+            M = gbla_gen.random_wide(int(5 + 7 * s), int(8 + 9 * s), 0.15 + 0.02 * (s % 4), p, 1000 * s + p % 977)
+            W = wide.reduce(M)
+            dense = M.dense()
+            perm = np.argsort(W.sigma)                              # column of sigma index k
+            r, RR, piv = brute_rref(dense[:, perm], p)
+            assert r == W.rank_M
+            assert piv[:W.npiv] == list(range(W.npiv))
+            assert np.array_equal(RR[W.npiv:, W.npiv:], W.R)
+    # equal to the C oracle on 16-bit primes (c0 and a random suite)
+    W = wide.reduce(gbla_gen.WideCSR(c0_matrix.m, c0_matrix.n, c0_matrix.p, c0_matrix.row_ptr,
+                                     c0_matrix.col.astype(np.uint32), c0_matrix.val.astype(np.uint32)))
+    assert W.modmac == c0_oracle.modmac and np.array_equal(W.dnew, c0_oracle.dnew)
+    assert W.rank == c0_oracle.rank and np.array_equal(W.R, c0_oracle.R)
+    for M in gbla_gen.random_suite(20, seed0=17):
+        res = oracle.reduce(M)
+        W = wide.reduce(gbla_gen.WideCSR(M.m, M.n, M.p, M.row_ptr, M.col.astype(np.uint32), M.val.astype(np.uint32)))
+        assert W.modmac == res.modmac and np.array_equal(W.dnew, res.dnew) and np.array_equal(W.R, res.R)
