@@ -195,6 +195,29 @@ gbla_status gbla_modgemm(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, i
 gbla_status gbla_modgemm_bench(gbla_ctx ctx, uint32_t p, int64_t rows, int64_t cols, int64_t K, int reps,
                                void *stream, float *ms_per_launch);
 
+/* ---- wider prime fields --------------------- */
+/* M over GF(p) with residues below 2^31: as gbla_csr with u32 values (1 <= val < p). */
+typedef struct {
+    int64_t m, n, nnz;
+    const uint64_t *row_ptr;
+    const uint32_t *col;
+    const uint32_t *val;
+} gbla_csr32;
+/* The whole reduction for a prime 2 < p < 2^31 (the paper's float representation covers p < 2^23,
+ * its library 32-bit residues too): Step 1 with readings R1-R7, Alg 2 (new order, readings R8/R9)
+ * with u64 accumulators (delayed reduction when n_piv (p-1)^2 < 2^63, else reduced at every add),
+ * the canonical RREF of D_new (R13) by column-by-column Gauss-Jordan -- all on the INT pipe with
+ * u32 storage (the tensor-core pipeline is u16 / two u8 limbs).  flags: GBLA_HOST_INPUT only.
+ * Results through gbla_get_dims / gbla_get_maps / gbla_get_opcount and gbla_get_wide; the u16
+ * calls reject a wide handle (GBLA_E_ORDER).  GBLA_E_DOMAIN if p is not a prime in (2, 2^31),
+ * GBLA_E_INVAL for malformed input.  Synchronizes `stream`. */
+gbla_status gbla_reduce_wide(gbla_ctx ctx, const gbla_csr32 *M, uint32_t p, uint32_t flags, void *stream,
+                             gbla_mat *out);
+/* Results of gbla_reduce_wide (device pointers owned by h, row stride *ld): rank(D_new), pivcol[rank],
+ * R (rank x nN, u32), D_new (mN x nN, u32). */
+gbla_status gbla_get_wide(gbla_mat h, int64_t *rank, const uint32_t **pivcol, const uint32_t **R,
+                          const uint32_t **Dnew, int64_t *ld);
+
 /* ---- the paper's binary matrix formats -------- */
 /* Format 1 (Table `tab:bin_formats`): m, n, p (u32), nnz (u64), data (u16 x nnz),
  * cols (u32 x nnz), rows (u32 x m, row lengths).  Format 2: b (u32: type code

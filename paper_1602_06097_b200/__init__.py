@@ -104,6 +104,8 @@ def load_library(path: str = LIB_PATH):
         "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
         "gbla_rref_M": ([vp, vp, P(i64)], st),
         "gbla_get_multiline_runs": ([vp, vp, P(i64), P(vp), P(vp), P(vp), P(vp)], st),
+        "gbla_reduce_wide": ([vp, P(_CSR), u32, u32, vp, P(vp)], st),
+        "gbla_get_wide": ([vp, P(i64), P(vp), P(vp), P(vp), P(i64)], st),
         "gbla_file_info_parse": ([vp, ctypes.c_size_t, ctypes.c_int, P(_FileInfo)], st),
         "gbla_file_decode": ([vp, vp, ctypes.c_size_t, ctypes.c_int, vp, vp, vp, vp], st),
         "gbla_get_rref_M": ([vp, P(_CSR)], st),
@@ -126,7 +128,8 @@ def exported_symbols():
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
             "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M",
-            "gbla_file_info_parse", "gbla_file_decode", "gbla_get_multiline_runs"]
+            "gbla_file_info_parse", "gbla_file_decode", "gbla_get_multiline_runs", "gbla_reduce_wide",
+            "gbla_get_wide"]
 
 
 def _check(status: int):
@@ -301,6 +304,18 @@ class Mat:
         ns = int(P[-1].item()) if npr.value >= 0 else 0
         return P, _view(col.value, (ns,), "<u4").clone(), _view(val.value, (ns,), "<u4").clone()
 
+    def wide(self):
+        """gbla_reduce_wide results: (rank, pivcol[rank], R[rank x nN], D_new[mN x nN]) as new torch
+        tensors (uint32)."""
+        npiv, mN, nN = self.dims()
+        rk, pc, R, Dn, ld = (ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(),
+                             ctypes.c_int64())
+        _check(_lib.gbla_get_wide(self._h, ctypes.byref(rk), ctypes.byref(pc), ctypes.byref(R), ctypes.byref(Dn),
+                                  ctypes.byref(ld)))
+        r = rk.value
+        return (r, _view(pc.value, (r,), "<u4").clone(), _view(R.value, (r, nN), "<u4", ld.value, 4).clone(),
+                _view(Dn.value, (mN, nN), "<u4", ld.value, 4).clone())
+
     def multiline_runs(self, stream=None):
         """Column runs of the multilines (gbla_get_multiline_runs): (run_ptr[npairs+1], run_col,
         run_len, run_slot) as new torch tensors."""
@@ -470,6 +485,28 @@ def gbla_modgemm(ctx: Context, p: int, A, B, C, rowidx=None, engine: int = 0, st
     _check(_lib.gbla_modgemm(ctx._h, p, rows, cols, K, ctypes.c_void_p(A.data_ptr()), A.stride(0),
                              ctypes.c_void_p(B.data_ptr()), B.stride(0), ri, ctypes.c_void_p(C.data_ptr()),
                              C.stride(0), engine, _stream_ptr(stream)))
+
+
+def gbla_reduce_wide(ctx: Context, m, n, row_ptr, col, val, p, stream=None) -> Mat:
+    """the reduction over GF(p) for a prime 2 < p < 2^31 (gbla_reduce_wide).  CSR
+    arrays: numpy (host: row_ptr u64, col u32, val u32) or torch CUDA tensors (uint64/uint32/uint32).
+    Results: Mat.wide() -> (rank, pivcol, R, D_new); dims / maps / opcount as for gbla_reduce."""
+    host = isinstance(row_ptr, np.ndarray)
+    if host:
+        row_ptr = np.ascontiguousarray(row_ptr, np.uint64)
+        col = np.ascontiguousarray(col, np.uint32)
+        val = np.ascontiguousarray(val, np.uint32)
+        ptrs = [a.ctypes.data for a in (row_ptr, col, val)]
+        nnz = int(row_ptr[-1]) if row_ptr.size else 0
+    else:
+        ptrs = [t.data_ptr() for t in (row_ptr, col, val)]
+        nnz = int(col.numel())
+    keep = (row_ptr, col, val)
+    csr = _CSR(m, n, nnz, ptrs[0], ptrs[1], ptrs[2])       # same layout as gbla_csr32 (val: u32 pointer)
+    h = ctypes.c_void_p()
+    _check(_lib.gbla_reduce_wide(ctx._h, ctypes.byref(csr), p, GBLA_HOST_INPUT if host else 0,
+                                 _stream_ptr(stream), ctypes.byref(h)))
+    return Mat(ctx, h, p, keep)
 
 
 def modgemm_bench(ctx: Context, p: int, rows: int, cols: int, K: int, reps: int = 10, stream=None) -> float:

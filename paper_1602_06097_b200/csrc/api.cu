@@ -249,6 +249,7 @@ struct PhaseTimer {
 static gbla_status check_mat(gbla_mat h, void *stream)
 {
     if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
+    if (h->wide) { set_error("a gbla_reduce_wide handle: use gbla_get_wide"); return GBLA_E_ORDER; }
     h->stream = (cudaStream_t)stream;
     GBLA_CUDA_TRY(cudaSetDevice(h->ctx->device));
     return GBLA_OK;
@@ -526,7 +527,7 @@ extern "C" gbla_status gbla_get_rref(gbla_mat h, int64_t *rank, const uint32_t *
                                      int64_t *ld)
 {
     if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }
-    if (h->rank < 0) { set_error("gbla_get_rref: echelon_D not run"); return GBLA_E_ORDER; }
+    if (h->rank < 0 || h->wide) { set_error("gbla_get_rref: echelon_D not run (or a wide handle)"); return GBLA_E_ORDER; }
     if (rank) *rank = h->rank;
     if (pivcol) *pivcol = h->pivcol;
     if (R) *R = h->R;

@@ -212,6 +212,10 @@ struct gbla_mat_s {
     int64_t rank = -1;
 
     int64_t force_piv = 0;             // internal splices (f2): rows [0, force_piv) are the pivot rows
+    // f4 (gbla_reduce_wide): residues below 2^31, u32 storage
+    bool wide = false;
+    uint32_t *Dw = nullptr, *Rw = nullptr;
+    int64_t ldw = 0;
 
     // f2: RREF of the whole M, original column order (gbla_rref_M): device CSR, rows by pivot column
     int64_t rankM = -1, rm_nnz = 0;
