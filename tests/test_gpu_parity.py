@@ -342,6 +342,28 @@ def test_c1_full_size_against_golden(gb, ctx):
     h.free()
 
 
+def test_c3_full_size_against_golden(gb, ctx):
+    """c3 (dense-D-heavy, 60,000 x 80,000, p = 32003) at full size through the default path (super-
+    panels of 4: deferred K = 512 flushes on CTA pairs, lead-sorted rows, prefix slots, back
+    elimination): the modMAC count, the R digest and the D_new digest written by the oracle
+    (tests/golden/make_golden.py c3: 2.2 h on 8 cores), bit-exact."""
+    g = json.load(open(os.path.join(GOLD, "c3_oracle.json")))
+    M = gbla_gen.f4_matrix("c3")
+    h = gpu_reduce(gb, ctx, M)
+    npiv, mN, nN = h.dims()
+    assert (npiv, mN, nN) == (g["npiv"], g["mN"], g["nN"])
+    assert h.opcount()[0] == g["modmac_sparse"]
+    r, pc, R = h.rref()
+    assert r == g["rank_D"]
+    assert oracle.rref_digest(r, nN, np_(pc), np_(R)) == g["rref_sha256"]
+    h.free()
+    rp, c, v = to_dev(M)
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+    gb.gbla_reduce_C(h, fused=True)
+    assert oracle.array_digest(np_(h.D())) == g["dnew_sha256"]
+    h.free()
+
+
 def test_edge_cases(gb, ctx):
     cases = [
         np.eye(6, dtype=np.int64),                        # A = I, no C|D
