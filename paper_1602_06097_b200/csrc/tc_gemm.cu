@@ -1326,7 +1326,8 @@ gbla_status modgemm_tc_sub_mk(cudaStream_t st, int64_t max_rows, const uint32_t 
     if (grid > tiles) grid = tiles;
     MMArgs a{max_rows, nrows_dev, cols, F, Alo, Ahi, Blo, Bhi, rowidx, C, ldc, nullptr, nullptr,
              c0_dev, nullptr, win_dev, win_w, ctsel, nkb, a_rt_stride, b_kb_stride, kb_c0, nullptr, g_k11_exp};
-    if (use_pair() && B2lo && B2hi) {
+    // (up to 128 rows -- the super-panel fix-ups -- half of every pair would idle: one CTA per tile)
+    if (use_pair() && B2lo && B2hi && max_rows > BM) {
         // CTA pairs over row-tile pairs: the A tiles of row tile 2 * ceil(rows / 256) - 1 are read
         // (zero rows: the caller's A buffer holds an even number of row tiles), and the B tiles of an
         // even number of 64-column tiles (the callers' B buffers are padded)
