@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     __shared__ uint32_t hinv[PK];            // inverse of each head's leading value (wide mode)
     __shared__ uint32_t hmap[PW];            // rounds: column -> established head of this chunk
     __shared__ uint32_t s_u[8];
+    __shared__ uint32_t s_hbits[PW / 32];     // leading columns of the chunk's heads
     __shared__ long long s_pos;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t p = F.p;
@@ -434,10 +435,14 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
     const int64_t coff = src.gathered ? 0 : c0;           // column of window column 0 in D
     bool published = false;                                // S / pivots published early (wide mode)
     // optional trace (GBLA_PANEL_TRACE): cycles per phase, accumulated over panels by thread 0
+    // (laps kept in shared memory and flushed once at the end: a global read-modify-write per lap
+    // would add its own latency to the next lap)
+    __shared__ unsigned long long s_tr[18];
+    if (trace && tid < 18) s_tr[tid] = 0;
     long long t_mark = trace ? clock64() : 0;
 #define P2_LAP(k_)                                                                        \
     do {                                                                                  \
-        if (trace && tid == 0) { const long long t_ = clock64(); trace[k_] += t_ - t_mark; t_mark = t_; } \
+        if (trace && tid == 0) { const long long t_ = clock64(); s_tr[k_] += t_ - t_mark; t_mark = t_; } \
     } while (0)
     int64_t wmax = nN - c0;
     if (wmax > PW) wmax = PW;
@@ -547,28 +552,44 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // wide mode: the candidates (<= PK) are in the window list; take them in row order
             const int ncl = (int)s_u[5];
             const int t = tid;
-            const bool ok = t < ncl && lead[clist[t]] < (uint32_t)width;
+            const uint32_t lt = t < ncl ? lead[clist[t]] : NONE16;
+            const bool ok = lt < (uint32_t)width;
             const unsigned msk = __ballot_sync(FULL, ok);
             if (lane == 0) wsum[warp] = __popc(msk);
             __syncthreads();
-            if (tid == 0) {
-                uint32_t s = 0;
-                for (int w = 0; w < 32; w++) { const uint32_t c = wsum[w]; wsum[w] = s; s += c; }
-                s_u[3] = s;
+            if (warp == 0) {                         // exclusive scan of the warp counts
+                const uint32_t c = wsum[lane];
+                uint32_t x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= o) x += y;
+                }
+                wsum[lane] = x - c;
+                if (lane == 31) s_u[3] = x;
             }
             __syncthreads();
-            if (ok) clead[wsum[warp] + __popc(msk & ((1u << lane) - 1u))] = clist[t];   // clead: scratch
+            if (ok) {                                // clead: rows, hinv: their leads (scratch)
+                const uint32_t at = wsum[warp] + __popc(msk & ((1u << lane) - 1u));
+                clead[at] = clist[t];
+                hinv[at] = lt;
+            }
             __syncthreads();
             ncand = (int)s_u[3];
-            if (tid < ncand) hinv[tid] = lead[clead[tid]];   // leads of the candidates (hinv: scratch)
-            __syncthreads();
-            if (tid < ncand) {                       // order by (lead, row): physical ~ pivot order
-                const uint32_t r = clead[tid];
-                const uint64_t kr = ((uint64_t)hinv[tid] << 32) | r;
+            {   // order by (lead, row): physical ~ pivot order; rank counted by 8 threads per candidate
+                const int ct = tid >> 3, part = tid & 7;
+                const bool mine = ct < ncand;
+                const uint64_t kr = mine ? ((uint64_t)hinv[ct] << 32) | clead[ct] : 0;
                 int rk = 0;
-                for (int j = 0; j < ncand; j++) rk += (((uint64_t)hinv[j] << 32) | clead[j]) < kr;
-                crow[freel[rk]] = r;
-                cstat[freel[rk]] = 1;
+                if (mine)
+                    for (int j = part; j < ncand; j += 8) rk += (((uint64_t)hinv[j] << 32) | clead[j]) < kr;
+                rk += __shfl_xor_sync(FULL, rk, 1);
+                rk += __shfl_xor_sync(FULL, rk, 2);
+                rk += __shfl_xor_sync(FULL, rk, 4);
+                if (mine && part == 0) {
+                    crow[freel[rk]] = clead[ct];
+                    cstat[freel[rk]] = 1;
+                }
             }
             pos = mN;
             __syncthreads();
@@ -667,34 +688,58 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             // 1 / its leading value.  (c2) the winner of every column becomes a head; the other
             // buffer is cleared for the next round.
             uint32_t *elect[2] = {hist, clist};      // clist is dead once the candidates are loaded
+            // Each round walks a compact list of the still-open candidates (the losers of the last
+            // election), so the warps share them evenly.  An elimination updates value columns in
+            // pairs (32-bit words) and finds the row's next leading column on the way; coefficient
+            // columns are updated only in the 32-column chunks where the head's coefficients are
+            // nonzero (emask: E starts as unit vectors and a row's chunks grow by its heads').
+            __shared__ uint32_t alist[2][PK];
+            __shared__ uint32_t s_nact[2];
+            __shared__ uint8_t emask[PK];
             for (int k = tid; k < width; k += NT) { hmap[k] = NONE16; hist[k] = NONE16; clist[k] = NONE16; }
-            for (int ci = tid; ci < ncand; ci += NT) clead[freel[ci]] = 0;
+            for (int ci = tid; ci < ncand; ci += NT) {
+                const uint32_t q = freel[ci];
+                clead[q] = 0;
+                alist[0][ci] = q;
+                emask[q] = nb == 0 ? (uint8_t)(1u << (q >> 5)) : (uint8_t)0xf;
+            }
+            if (tid == 0) { s_nact[0] = (uint32_t)ncand; s_nact[1] = 0; }
             __syncthreads();
             for (int round = 0;; round++) {
-                if (trace && tid == 0) trace[8] += 1;
+                if (trace && tid == 0) s_tr[8] += 1;
                 uint32_t *hb = elect[round & 1];
-                for (int ci = warp; ci < ncand; ci += 32) {
-                    const uint32_t q = freel[ci];
-                    if (cstat[q] != 1) continue;
+                const uint32_t *al = alist[round & 1];
+                const int nact = (int)s_nact[round & 1];
+                // 1 / leading value of every bidder: loaded now, consumed by the election (the
+                // table read's latency is not waited for per candidate)
+                uint32_t pend[PK / 32];
+#pragma unroll
+                for (int j = 0; j < PK / 32; j++) {
+                    const int ci = warp + 32 * j;
+                    pend[j] = 0;
+                    if (ci >= nact) continue;
+                    const uint32_t q = al[ci];
                     uint16_t *xr = X + q * LDX;
-                    int base = (int)(clead[q] & ~31u);
+                    uint32_t ld = NONE16;
+                    for (int base = (int)(clead[q] & ~31u); base < ldv; base += 32) {
+                        const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
+                        if (m) { ld = base + __ffs(m) - 1; break; }
+                    }
+                    uint32_t em = emask[q];
                     for (;;) {
-                        uint32_t ld = NONE16;
-                        for (; base < ldv; base += 32) {
-                            const unsigned m = __ballot_sync(FULL, xr[base + lane] != 0);
-                            if (m) { ld = base + __ffs(m) - 1; break; }
-                        }
-                        __syncwarp();
                         if (ld == NONE16) {                       // dependent: zero on the panel
+                            __syncwarp();
                             if (lane == 0) { cstat[q] = 0; clead[q] = NONE16; }
                             break;
                         }
                         const uint32_t hq = hmap[ld];
                         if (hq == NONE16) {
+                            __syncwarp();
                             if (lane == 0) {
                                 clead[q] = ld;
+                                emask[q] = (uint8_t)em;
                                 atomicMin(&hb[ld], q);
-                                hinv[q] = invtab[xr[ld]];
+                                pend[j] = __ldg(invtab + xr[ld]);
                             }
                             break;
                         }
@@ -703,25 +748,56 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                         const uint32_t gl = dense ? xr[ld] : mod32(xr[ld] * hinv[hq], p, m32);
                         const uint32_t ng = gl ? p - gl : 0;
                         __syncwarp();
-                        for (int k = base + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(xr[k] + ng * hr[k], p, m32);
-                        for (int k = lane; k < PK; k += 32)
-                            xr[PW + k] = (uint16_t)mod32(xr[PW + k] + ng * hr[PW + k], p, m32);
+                        uint32_t nl = NONE16;
+                        for (int k0 = (int)(ld & ~31u); k0 < ldv; k0 += 64) {
+                            const int k = k0 + 2 * lane;
+                            uint32_t lo = 0, hi = 0;
+                            if (k < ldv) {
+                                const uint32_t xv = *reinterpret_cast<const uint32_t *>(xr + k);
+                                const uint32_t hv = *reinterpret_cast<const uint32_t *>(hr + k);
+                                lo = mod32((xv & 0xffffu) + ng * (hv & 0xffffu), p, m32);
+                                hi = mod32((xv >> 16) + ng * (hv >> 16), p, m32);
+                                *reinterpret_cast<uint32_t *>(xr + k) = lo | (hi << 16);
+                            }
+                            if (nl == NONE16) {
+                                const unsigned m = __ballot_sync(FULL, (lo | hi) != 0);
+                                if (m) {
+                                    const int j = __ffs(m) - 1;
+                                    nl = (uint32_t)(k0 + 2 * j) + __shfl_sync(FULL, lo == 0 ? 1u : 0u, j);
+                                }
+                            }
+                        }
+                        const uint32_t hm = emask[hq];
+#pragma unroll
+                        for (int c = 0; c < PK / 32; c++)
+                            if ((hm >> c) & 1u) {
+                                const int k = PW + 32 * c + lane;
+                                xr[k] = (uint16_t)mod32(xr[k] + ng * hr[k], p, m32);
+                            }
+                        em |= hm;
+                        ld = nl;
                         __syncwarp();
                     }
                     __syncwarp();
                 }
                 __syncthreads();
                 P2_LAP(3);
-                int coll = 0;
-                for (int ci = warp; ci < ncand; ci += 32) {
-                    const uint32_t q = freel[ci];
+                uint32_t *nl_ = alist[(round + 1) & 1];
+#pragma unroll
+                for (int j = 0; j < PK / 32; j++) {
+                    const int ci = warp + 32 * j;
+                    if (ci >= nact) continue;
+                    const uint32_t q = al[ci];
                     if (cstat[q] != 1) continue;
-                    if (hb[clead[q]] != q) { coll = 1; continue; }     // eliminated next round
+                    if (hb[clead[q]] != q) {                     // eliminated next round
+                        if (lane == 0) nl_[atomicAdd(&s_nact[(round + 1) & 1], 1u)] = q;
+                        continue;
+                    }
                     __syncwarp();
-                    if (lane == 0) { cstat[q] = 2; hmap[clead[q]] = q; }
+                    if (lane == 0) { cstat[q] = 2; hmap[clead[q]] = q; hinv[q] = pend[j]; }
                     if (dense) {                                          // normalized heads
                         uint16_t *xr = X + q * LDX;
-                        const uint32_t iv = hinv[q];
+                        const uint32_t iv = __shfl_sync(FULL, pend[j], 0);
                         for (int k = (clead[q] & ~31u) + lane; k < ldv; k += 32) xr[k] = (uint16_t)mod32(iv * xr[k], p, m32);
                         for (int k = lane; k < PK; k += 32) xr[PW + k] = (uint16_t)mod32(iv * xr[PW + k], p, m32);
                     }
@@ -729,9 +805,10 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                 }
                 uint32_t *ob = elect[(round + 1) & 1];
                 for (int k = tid; k < width; k += NT) ob[k] = NONE16;
-                coll = __syncthreads_count(coll);
+                if (tid == 0) s_nact[round & 1] = 0;
+                __syncthreads();
                 P2_LAP(4);
-                if (!coll) break;
+                if (s_nact[(round + 1) & 1] == 0) break;
             }
         } else {
             // (c) echelon form of the chunk by pivot steps, ONE block barrier per pivot.  Every
@@ -804,7 +881,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
                         __syncwarp();
                     }
                 }
-                if (trace && tid == 0) trace[8] += nsteps;
+                if (trace && tid == 0) s_tr[8] += nsteps;
                 P2_LAP(3);
                 // heads: 1 / leading value (wide mode keeps the row), or normalized rows (dense mode)
                 for (int ci = warp; ci < ncand; ci += 32) {
@@ -826,25 +903,21 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             }
         }
         // (d) the chunk's heads, sorted by leading column, become basis slots nb .. nb+h-1
-        if (tid < ncand) {
-            const uint32_t q = freel[tid];
-            if (cstat[q] == 2) {
-                uint32_t rk = 0;
-                for (int cj = 0; cj < ncand; cj++) {
-                    const uint32_t q2 = freel[cj];
-                    rk += cstat[q2] == 2 && clead[q2] < clead[q];
-                }
-                bphys[nb + rk] = q;
-                bpc[nb + rk] = clead[q];
-            }
-        }
-        if (tid == 0) {
-            uint32_t h = 0;
-            for (int cj = 0; cj < ncand; cj++) h += cstat[freel[cj]] == 2;
-            s_u[4] = h;
+        //     (heads have distinct leading columns: rank = heads left of it, from a column bitmap)
+        if (tid < PW / 32) s_hbits[tid] = 0;
+        __syncthreads();
+        const bool is_head = tid < ncand && cstat[freel[tid]] == 2;
+        const uint32_t hq_ = is_head ? freel[tid] : 0, hc_ = is_head ? clead[hq_] : 0;
+        if (is_head) atomicOr(&s_hbits[hc_ >> 5], 1u << (hc_ & 31));
+        const uint32_t h = (uint32_t)__syncthreads_count(is_head);
+        if (is_head) {
+            uint32_t rk = __popc(s_hbits[hc_ >> 5] & ((1u << (hc_ & 31)) - 1u));
+            for (uint32_t w = 0; w < (hc_ >> 5); w++) rk += __popc(s_hbits[w]);
+            bphys[nb + rk] = hq_;
+            bpc[nb + rk] = hc_;
         }
         __syncthreads();
-        const uint32_t nb0 = nb, h = s_u[4];
+        const uint32_t nb0 = nb;
         // dead rows are free again (their coefficient columns are zero in every head)
         for (int ci = tid; ci < ncand; ci += NT) {
             const uint32_t q = freel[ci];
@@ -1081,7 +1154,7 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             }
             __syncthreads();
             P2_LAP(15);
-            if (trace && tid == 0) trace[7] += s_u[7];
+            if (trace && tid == 0) s_tr[7] += s_u[7];
             // rows above: R <- R - sum_k g_k * block_k, two rows per item, nonzero groups only
             const int ngm = (int)s_u[7], nrp = (r0 + 1) / 2;
             for (int it = tid; it < nrp * ngm; it += NT) {
@@ -1142,7 +1215,10 @@ __global__ void __launch_bounds__(NT, 1) k_panel2(int64_t nN, Field F, PanelSrc 
             rowpiv[r] = (uint32_t)(c0 + bpc[tid]);      // marks S (pivot column >= c0)
     }
     P2_LAP(6);
-    if (trace && tid == 0) { trace[9] += 1; trace[10] += ncand_tot; trace[11] += nb; trace[12] += width; trace[17] += dense ? 1 : 0; }
+    if (trace && tid == 0) {
+        s_tr[9] += 1; s_tr[10] += ncand_tot; s_tr[11] += nb; s_tr[12] += width; s_tr[17] += dense ? 1 : 0;
+        for (int k = 0; k < 18; k++) trace[k] += s_tr[k];
+    }
 #undef P2_LAP
     if (!published && tid == 0) {
         cur->c0 = c0;

@@ -538,8 +538,11 @@ __device__ __forceinline__ void commit2(uint64_t *bar)
 // epilogue forms (2^8 (U mod p) + V) < 2^24 + 2^31 in 32 bits.  A pair tile is 256 rows x 128
 // columns (M = 256, N = 128 MMAs: each CTA stages one whole 64-column B tile, B and B' planes), so
 // 2 x 128 TMEM columns per tile: two accumulator sets (double-buffered, 512 columns).
+#ifndef PR_NSB_OVERRIDE
+#define PR_NSB_OVERRIDE 3
+#endif
 constexpr int PR_NP = 128;                                     // columns of a pair tile
-constexpr int PR_NSB = 3;                                      // B stages
+constexpr int PR_NSB = PR_NSB_OVERRIDE;                      // B stages
 constexpr uint32_t PR_BSTAGE = 4 * B_PLANE;                    // B_h, B_l, B'_h, B'_l of one 64-col tile
 constexpr int PR_SMEM = MK_MAX * A_BYTES + PR_NSB * PR_BSTAGE; // 128 KB + 96 KB
 

@@ -14,6 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     import torch
     import paper_1602_06097_b200 as gb
+    if os.environ.get("GBLA_LIB"):
+        gb.load_library(os.environ["GBLA_LIB"])   # a variant build (experiments)
     ctx = gb.Context(0)
     shapes = [(40000, 45056, 512), (40000, 45056, 128), (16384, 16384, 512), (8192, 90112, 512)]
     if len(sys.argv) > 1:
