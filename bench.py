@@ -151,7 +151,9 @@ KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1 block forward substitution, 
                 "panel": "k_panel2 (K10, panel echelon form, one CTA)",
                 "trailing": "K11 trailing update (k_modgemm_mk2 CTA-pair K = 512 flushes + k_modgemm_ws / "
                             "k_modgemm_win K = 128 window updates)",
-                "rnew": "k_modgemm_ws<STORE> (K11 new pivot rows)"}
+                "rnew": "k_modgemm_ws<STORE> (K11 new pivot rows)",
+                "backsub": "K14 back substitution RREF = U_sq^-1 U (k_sweep on the pivot block of the row echelon "
+                           "form; band / C-tile setup included)"}
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 INT8_PEAK = os.path.join(ROOT, "profiles", "r02_int8_peak.json")      # scripts/peaks/int8_peak.py on a B200
 IMAD_PEAK = os.path.join(ROOT, "profiles", "r02_imad_peak.json")      # scripts/peaks/imad_peak.cu on a B200
@@ -177,7 +179,7 @@ def _imad_peak(sm_count, sm_mhz):
         return sm_count * 32 * sm_mhz * 1e6 / 1e12, f"derived: {sm_count} SMs x 32 IMAD.WIDE/clk x {sm_mhz:.0f} MHz"
 
 
-def roofline(kms, kwork, peaks, peak_src, sm_count, config):
+def roofline(kms, kwork, peaks, peak_src, sm_count, config, kexec=None):
     """Roofline of the dominant kernel family (largest CUDA-event time over the timed steps), against
     WHOLE-GPU peaks.  Tensor-core families: achieved = algorithmic modMACs (gbla_get_kernel_work,
     DESIGN.md §6) x 4 u8 MACs (limb split) x 2 ops / family time, against the dense int8 peak
@@ -205,6 +207,12 @@ def roofline(kms, kwork, peaks, peak_src, sm_count, config):
                "peak_source": src + " (sustained; burst " + f"{burst:.0f})",
                "frac_of_burst": round(ach / burst, 4) if burst else None,
                "modmac_per_s_T": round(work / sec / 1e12, 3)}
+        if kexec and kexec.get(dom):
+            # the dense 128 x 128 band tiles the family executes (any density): executed int8 rate
+            ex = kexec[dom] * 2 / sec / 1e12
+            out["executed_TOPS"] = round(ex, 1)
+            out["executed_frac"] = round(ex / sustained, 4)
+            out["algorithmic_over_executed"] = round(work * 4 / kexec[dom], 4)
         if dom == "trailing" and kwork.get("trailing_elems"):
             byts = 4.0 * kwork["trailing_elems"]          # u16 read + write per D entry of every update
             out["hbm_algorithmic_GBs"] = round(byts / sec / 1e9, 1)
@@ -292,6 +300,7 @@ def main():
     phases = []
     kms = {k: [0.0, 0] for k in gb.Mat.KERNELS}
     kwork = {k: 0 for k in list(gb.Mat.KERNELS) + ["trailing_elems"]}
+    kexec = {k: 0 for k in gb.Mat.KERNELS}
     kms_steps = []
     ops = dense_ops = 0
     rank_d = None
@@ -314,6 +323,8 @@ def main():
         kms_steps.append(step_k)
         for k, w in h.kernel_work().items():
             kwork[k] += w
+        for k, w in h.kernel_exec().items():
+            kexec[k] += w
         ops, dense_ops = h.opcount()
         rank_d = h.dims(), h.rref()[0]
         h.free()
@@ -368,7 +379,7 @@ def main():
         ph = {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]}
         dims = rank_d[0] if rank_d else (0, 0, 0)
         roof = roofline(kms, kwork, peaks, peak_src, torch.cuda.get_device_properties(dev).multi_processor_count,
-                        cfg.name)
+                        cfg.name, kexec)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(cfg.name, M, args.cpu_targets)

@@ -300,16 +300,25 @@ const char *gbla_last_error(void);
  * variable GBLA_KERNEL_TIMERS is set when the handle is created).  which:
  * 0 = K5' sweep (C' = C A^-1 block forward substitution, tcgen05),
  * 1 = K7' update (D -= C' B, tcgen05), 2 = K10 panel factorization,
- * 3 = K11 trailing update of the echelon (tcgen05), 4 = K11 new pivot rows.
+ * 3 = K11 trailing update of the echelon (tcgen05), 4 = K11 new pivot rows,
+ * 5 = K14 back substitution of the row echelon form (RREF = U_sq^-1 U by the
+ * K5' sweep on the pivot block of U; its setup kernels included).
  * Synchronizes the handle's stream. */
 gbla_status gbla_get_kernel_ms(gbla_mat h, int which, float *ms, int64_t *launches);
 /* Algorithmic modMACs of the same kernel family on this handle (this rank):
  * 0 = Alg 2 A-part count (sum over nonzero lambda_j of nnz(A_j) - 1),
  * 1 = Alg 2 B-part count, 2 = sum over panels of candidates * kp * 128,
- * 3 = sum over panels of nrows * kp * width, 4 = sum of kp * kp * width;
- * 5 = not modMACs: sum over panels of nrows * width, the D entries the
+ * 3 = sum over panels of nrows * kp * width, 4 = sum of kp * kp * width,
+ * 5 = back substitution: sum over the non-pivot columns q of R of r_q (r_q + 1) / 2,
+ * r_q = pivots left of q (the modMACs of the triangular solve U_sq X = U_rest);
+ * 6 = not modMACs: sum over panels of nrows * width, the D entries the
  * trailing updates read and write (the HBM roofline of K11). */
 gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *modmac);
+/* u8 MACs the tensor cores executed for kernel family `which` (as in gbla_get_kernel_ms) on this
+ * handle: 0 (K5' sweep) and 5 (K14 back substitution) count 4 x 128^3 per 128 x 128 tile pair of
+ * the dense band tiles (limb products), whatever the tiles' density; the other families 0 (not
+ * counted).  Executed / (4 x algorithmic) is the dense-tile overhead of the family. */
+gbla_status gbla_get_kernel_exec(gbla_mat h, int which, uint64_t *u8macs);
 /* Number of libgbla kernels launched by this process so far (diagnostics). */
 uint64_t gbla_kernel_launches(void);
 /* Library build/version string. */

@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
         "gbla_get_kernel_ms": ([vp, ctypes.c_int, P(ctypes.c_float), P(i64)], st),
         "gbla_get_multilines": ([vp, vp, P(i64), P(vp), P(vp), P(vp)], st),
         "gbla_get_kernel_work": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
+        "gbla_get_kernel_exec": ([vp, ctypes.c_int, P(ctypes.c_uint64)], st),
         "gbla_modgemm_bench": ([vp, u32, i64, i64, i64, ctypes.c_int, vp, P(ctypes.c_float)], st),
         "gbla_rref_M": ([vp, vp, P(i64)], st),
         "gbla_get_multiline_runs": ([vp, vp, P(i64), P(vp), P(vp), P(vp), P(vp)], st),
@@ -127,7 +128,7 @@ def exported_symbols():
             "gbla_densify_quadrant", "gbla_get_rref", "gbla_copy_rref_to_host", "gbla_get_opcount",
             "gbla_get_phase_ms", "gbla_sync", "gbla_mat_free", "gbla_last_error", "gbla_version",
             "gbla_kernel_launches", "gbla_nccl_get_unique_id", "gbla_modgemm", "gbla_get_kernel_ms",
-            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M",
+            "gbla_get_multilines", "gbla_get_kernel_work", "gbla_get_kernel_exec", "gbla_modgemm_bench", "gbla_rref_M", "gbla_get_rref_M",
             "gbla_file_info_parse", "gbla_file_decode", "gbla_get_multiline_runs", "gbla_reduce_wide",
             "gbla_get_wide"]
 
@@ -370,7 +371,7 @@ class Mat:
         _check(_lib.gbla_get_opcount(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
-    KERNELS = ("sweep", "update", "panel", "trailing", "rnew")
+    KERNELS = ("sweep", "update", "panel", "trailing", "rnew", "backsub")
 
     def kernel_ms(self):
         """{family: (ms, launches)} from the library's CUDA-event timers
@@ -392,6 +393,15 @@ class Mat:
         w = ctypes.c_uint64()
         _check(_lib.gbla_get_kernel_work(self._h, len(self.KERNELS), ctypes.byref(w)))
         out["trailing_elems"] = w.value                 # D entries read + written by the trailing updates
+        return out
+
+    def kernel_exec(self):
+        """{family: u8 MACs the tensor cores executed} (gbla_get_kernel_exec; 0 = not counted)."""
+        out = {}
+        for i, name in enumerate(self.KERNELS):
+            w = ctypes.c_uint64()
+            _check(_lib.gbla_get_kernel_exec(self._h, i, ctypes.byref(w)))
+            out[name] = w.value
         return out
 
     def phase_ms(self):

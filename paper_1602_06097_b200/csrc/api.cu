@@ -586,6 +586,13 @@ extern "C" gbla_status gbla_get_kernel_work(gbla_mat h, int which, uint64_t *mod
     return GBLA_OK;
 }
 
+extern "C" gbla_status gbla_get_kernel_exec(gbla_mat h, int which, uint64_t *u8macs)
+{
+    if (!h || which < 0 || which >= KT_N || !u8macs) { set_error("gbla_get_kernel_exec: bad argument"); return GBLA_E_INVAL; }
+    *u8macs = h->kexec[which];
+    return GBLA_OK;
+}
+
 extern "C" gbla_status gbla_sync(gbla_mat h)
 {
     if (!h) { set_error("NULL gbla_mat"); return GBLA_E_INVAL; }

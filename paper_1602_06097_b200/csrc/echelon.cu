@@ -650,6 +650,67 @@ gbla_status panels_int(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
 
 }  // namespace
 
+gbla_status bsub_rref(gbla_mat h);   // sparse_tc.cu (K14)
+
+// distinct leading columns of D's rows (warp per row; flag[c] set once, cnt counts first setters)
+__global__ void k_lead_distinct(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
+                                uint32_t *__restrict__ flag, unsigned int *__restrict__ cnt)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint16_t *row = D + (size_t)r * ldD;
+        int64_t res = nN;
+        for (int64_t base = 0; base < nN && res == nN; base += 32 * 8) {
+            int64_t first = nN;
+            for (int u = 0; u < 8; u++) {
+                const int64_t k = base + lane * 8 + u;
+                if (k < nN && row[k] != 0) { first = k; break; }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, first < nN);
+            if (m) res = __shfl_sync(0xffffffffu, first, __ffs(m) - 1);
+        }
+        if (lane == 0 && res < nN && atomicExch(&flag[res], 1u) == 0u) atomicAdd(cnt, 1u);
+    }
+}
+
+// The fully reduced form through a row echelon form and one back substitution (K14, sparse_tc.cu)
+// instead of the Gauss-Jordan back elimination inside the panels (GBLA_BACKSUB=0/1 forces it).
+// The REF panels touch only rows leading inside each window, so on a staircase D_new (the F4
+// shape: c1, c2, c4) the echelon becomes the panel chain plus a triangular solve on the tensor
+// cores (c2: 48 ms REF + the solve against 260 ms of Gauss-Jordan).
+// Which one: a row echelon form is cheap when the rows of D mostly lead in columns of their own
+// (each panel then touches only the few rows colliding in its window); when most rows lead in the
+// same few columns (a dense D, c3) the REF does nearly the Gauss-Jordan trailing work and the
+// solve comes on top (c3: 153 vs 123 ms).  Rule: at least half the nonzero rows lead in distinct
+// columns (c1, c2, c4: ~0.8; c3: < 0.1).
+static gbla_status use_bsub(gbla_mat h, uint32_t flags, bool *out)
+{
+    *out = false;
+    if (flags & (GBLA_ECHELON_REF | GBLA_DENSE_INT)) return GBLA_OK;
+    const char *e = getenv("GBLA_BACKSUB");
+    if (e) { *out = atoi(e) != 0; return GBLA_OK; }
+    if (h->mN < 2 || h->nN < 2) return GBLA_OK;
+    cudaStream_t st = h->stream;
+    uint32_t *flag;
+    unsigned int *cnt;
+    GBLA_TRY(dalloc_t(h, h->nN + 1, &flag));
+    GBLA_TRY(dalloc_t(h, 1, &cnt));
+    GBLA_CUDA_TRY(cudaMemsetAsync(flag, 0, (h->nN + 1) * 4, st));
+    GBLA_CUDA_TRY(cudaMemsetAsync(cnt, 0, 4, st));
+    const unsigned g = grid_for(h->mN * 32, 256) < 16u * h->ctx->sm_count ? grid_for(h->mN * 32, 256)
+                                                                          : 16u * h->ctx->sm_count;
+    k_lead_distinct<<<g, 256, 0, st>>>(h->mN, h->nN, h->D, h->ldD, flag, cnt);
+    note_launch();
+    unsigned int hc = 0;
+    GBLA_CUDA_TRY(cudaMemcpyAsync(&hc, cnt, 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t lim = h->mN < h->nN ? h->mN : h->nN;
+    *out = 2 * (int64_t)hc >= lim;
+    dfree(h, flag);
+    return GBLA_OK;
+}
+
 gbla_status echelon_impl(gbla_mat h, uint32_t flags)
 {
     cudaStream_t st = h->stream;
@@ -683,6 +744,9 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
             return tcgemm_dev_err(st, "gbla_echelon_D");
         }
     }
+    bool bsub = false;
+    if (!(h->dist_rows && (real || G > 1))) GBLA_TRY(use_bsub(h, flags, &bsub));
+    if (bsub) h->ref_only = true;            // the panels stop at a row echelon form
     if (mN > 0 && nN > 0) {
         if (flags & GBLA_DENSE_INT) GBLA_TRY(panels_int(h, rowpiv, dops, invtab));
         else GBLA_TRY(panels_tc2(h, rowpiv, dops, invtab));
@@ -727,6 +791,11 @@ gbla_status echelon_impl(gbla_mat h, uint32_t flags)
             note_launch();
         }
         GBLA_CUDA_TRY(cudaGetLastError());
+    }
+    if (bsub) {
+        h->ref_only = false;
+        GBLA_TRY(bsub_rref(h));
+        h->dense_ops += h->kwork[KT_BSUB];
     }
     return GBLA_OK;
 }

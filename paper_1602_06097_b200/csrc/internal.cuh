@@ -152,7 +152,7 @@ struct Alloc {
 };
 
 // per-kernel-family CUDA-event timers (GBLA_KERNEL_TIMERS=1; gbla_get_kernel_ms)
-enum { KT_SWEEP = 0, KT_UPDATE = 1, KT_PANEL = 2, KT_TRAIL = 3, KT_RN = 4, KT_N = 5 };
+enum { KT_SWEEP = 0, KT_UPDATE = 1, KT_PANEL = 2, KT_TRAIL = 3, KT_RN = 4, KT_BSUB = 5, KT_N = 6 };
 struct KTimers {
     bool on = false;
     std::vector<cudaEvent_t> ev[KT_N];
@@ -225,7 +225,8 @@ struct gbla_mat_s {
 
     uint64_t *opcount = nullptr;       // [mN] per-target sparse modMACs
     uint64_t sparse_ops = 0, dense_ops = 0;
-    uint64_t kwork[KT_N] = {0, 0, 0, 0, 0};   // algorithmic modMACs per kernel family (this rank)
+    uint64_t kwork[KT_N] = {0, 0, 0, 0, 0, 0};   // algorithmic modMACs per kernel family (this rank)
+    uint64_t kexec[KT_N] = {0, 0, 0, 0, 0, 0};   // u8 MACs the tensor cores executed (dense tiles; 0 = not counted)
     uint64_t trail_elems = 0;                  // D entries the echelon's trailing updates read + write
 
     // call-order state

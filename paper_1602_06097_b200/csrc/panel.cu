@@ -107,10 +107,12 @@ struct PanelSrc {
 // panels per super-panel of deferred trailing updates (GBLA_SP = 1..4).  Default: 4 when D is
 // large (the trailing updates are HBM / epilogue bound: c2, c3, c4), else 1 (c1: the panel chain
 // is the critical path and the per-panel update is hidden behind it; fix-ups would lengthen it).
-static int sp_panels(int64_t mN, int64_t nN)
+static int sp_panels(int64_t mN, int64_t nN, bool ref)
 {
     const char *e = getenv("GBLA_SP");
-    const int g = e ? atoi(e) : ((double)mN * (double)nN >= 4e8 ? 4 : 1);
+    // a row echelon form (no back elimination) touches only the rows leading inside each window:
+    // the prefix rows of a super-panel flush would be zero-factor work (c2: 247 vs 48 ms)
+    const int g = e ? atoi(e) : (!ref && (double)mN * (double)nN >= 4e8 ? 4 : 1);
     return g < 1 ? 1 : g > 4 ? 4 : g;
 }
 
@@ -1731,7 +1733,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     // Deferred trailing updates (super-panels of G panels): each panel updates D eagerly only
     // left of the column Cd; the columns from Cd on take one K = G * 128 update per super-panel
     // (K11 multi-K: a quarter of the HBM passes and epilogue reductions of per-panel updates).
-    const int G = lookahead ? sp_panels(mN, nN) : 1;
+    const int G = lookahead ? sp_panels(mN, nN, h->ref_only) : 1;
     const size_t rd_stride = (size_t)npad * PK;          // bytes per plane per K-block
     const int64_t ntrD = (mN + 127) / 128, ntrD2 = (ntrD + 1) / 2 * 2;
     uint8_t *Fdlo = nullptr, *Fdhi = nullptr, *Aflo = nullptr, *Afhi = nullptr;

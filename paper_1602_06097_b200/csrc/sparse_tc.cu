@@ -30,6 +30,8 @@
 
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "internal.cuh"
 #include "tc.cuh"
 
@@ -42,7 +44,7 @@ struct BandTiles {
     uint64_t *offA = nullptr, *offB = nullptr;
     uint32_t *amax = nullptr, *bmin = nullptr, *bmax = nullptr;
     uint32_t *jl_ptr = nullptr, *jl_idx = nullptr, *kl_ptr = nullptr, *kl_idx = nullptr;
-    unsigned long long *ops = nullptr;   // [2] A-part, B-part modMACs (Alg 2 count)
+    unsigned long long *ops = nullptr;   // [3] A-part, B-part modMACs (Alg 2 count), tile pairs swept
     int64_t xt_cap = 0;                  // target tiles the X-tile buffer holds
     bool swept = false;
 };
@@ -50,6 +52,8 @@ struct BandTiles {
 namespace {
 
 constexpr uint32_t TB = 32768, PB = 16384;
+// u8 MACs the tensor cores execute per tile pair of the sweep: 4 limb products of 128 x 128 x 128
+constexpr unsigned long long EXEC_PER_PAIR = 4ull * 128 * 128 * 128;
 
 __global__ void k_band_ranges(int64_t npiv, const uint64_t *__restrict__ ab_ptr, const uint32_t *__restrict__ ab_col,
                               const uint32_t *__restrict__ ab_np, uint32_t *__restrict__ amax,
@@ -198,14 +202,19 @@ struct SweepArgs {
     uint8_t *Xt;                   // X tiles; tile (T, J) holds C_J[T] until task (T, J) overwrites it with X_J[T]
     uint16_t *X16;
     int64_t ldX;
-    const uint32_t *ab_w, *ab_np;
+    const uint32_t *ab_w, *ab_np;  // op counts (Alg 2); NULL: not counted
+    // back substitution (bsub_rref): X_J of target t also goes to Rout[(rrev - 1 - i) * ldR + rcol[t]]
+    // for every pivot index i of block J (the reversed pivot order of the triangular solve)
+    uint16_t *Rout;
+    int64_t ldR, rrev;
+    const uint32_t *rcol;
     unsigned long long *ops;
     int64_t prank, pworld;         // target tiles T = prank + pworld * (i0 + li) (multi-GPU row shards)
     int64_t i0;                    // first local tile of this batch; Xt / jmin / flags are batch-relative (li)
-    // dependency-driven schedule: task (i, J) computes X_J of local tile i.  Tasks are
-    // numbered J-major: those of column block J are [toff[J], toff[J+1]) = local tiles
-    // 0 .. toff[J+1]-toff[J]-1 (tiles are sorted by lead, so the active ones are a prefix).
-    const uint32_t *toff;          // [NB+1]
+    // dependency-driven schedule: task q computes X_J of local tile i, (J, i) = tasks[q] (low /
+    // high 32 bits).  Tasks are numbered group-major, then J-major inside a group of consecutive
+    // tiles (tile_group_order), so every task waits only on tasks with smaller numbers.
+    const uint64_t *tasks;         // [ntasks]
     const uint32_t *jmin;          // [nl] first block of local tile i
     uint32_t *flags;               // [nl*NB] 1 once X_J of local tile i is stored
     unsigned int *next;            // task counter
@@ -285,13 +294,14 @@ static int sweep_threads()
 // tiles pre-multiplied (k_ahat: Â_IJ = -A_IJ inv(A_JJ) mod p) the block step is
 //   X_J = C_J inv(A_JJ) + sum_I X_I Â_IJ      (mod p)
 // one accumulation of nI + 1 tile pairs and ONE epilogue.  Every CTA claims tasks
-// (i, J) in J-major order from a global counter; the pair (C_J, inv(A_JJ)) comes
-// first, then the X_I in ascending I, each waited for by its flag just before its
-// operands are staged.  A task only waits on tasks with smaller numbers, which were
-// claimed earlier by co-resident CTAs (cooperative launch), so the schedule cannot
-// deadlock.  Per 128-pivot block the chain of one target tile costs the last tile
-// pair + one epilogue + the flag hand-off; the A tiles of one J are shared in L2 by
-// all tiles working on J.
+// (i, J) from a global counter in the order of a.tasks (groups of consecutive target
+// tiles, J-major inside a group); the pair (C_J, inv(A_JJ)) comes first, then the X_I
+// in ascending I, each waited for by its flag just before its operands are staged.
+// A task only waits on tasks with smaller numbers, which were claimed earlier by
+// co-resident CTAs (cooperative launch), so the schedule cannot deadlock.  Per
+// 128-pivot block the chain of one target tile costs the last tile pair + one
+// epilogue + the flag hand-off.  L2 reuse: the Â tiles of one J are shared by the
+// tiles working on J (tile_group_size: J-major by default).
 __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
     const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t ph_acc = 0;
     uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
-    unsigned long long opsA = 0, opsB = 0;
+    unsigned long long opsA = 0, opsB = 0, pairs_done = 0;   // pairs_done: thread 0
     const uint32_t sStg = tc::smem_u32(stg);
     const uint32_t p = a.F.p;
     uint32_t gpair = 0;                        // stage ring position, continuous across tasks (thread 0)
@@ -326,13 +336,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         __syncthreads();
         const uint32_t task = s_task;
         if (task >= a.ntasks) break;
-        // decode: J = last block with toff[J] <= task
-        uint32_t lo = 0, hi = (uint32_t)a.NB;          // toff[lo] <= task < toff[hi]
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (a.toff[mid] <= task) lo = mid; else hi = mid;
-        }
-        const int64_t J = lo, li = task - a.toff[lo];
+        const uint64_t tv = a.tasks[task];
+        const int64_t J = (uint32_t)tv, li = (uint32_t)(tv >> 32);
         const int64_t T = a.prank + a.pworld * (a.i0 + li), first = T * 128;
         const int64_t Jmin = a.jmin[li];
         const int64_t slot = first + row;
@@ -343,14 +348,15 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         const uint32_t jbase = (uint32_t)J * 128;
         if (tid < 128) {
             const uint32_t jg = jbase + tid;
-            s_np[tid] = jg < (uint64_t)a.npiv ? a.ab_np[jg] : 1;
-            s_w[tid] = jg < (uint64_t)a.npiv ? a.ab_w[jg] : 1;
+            s_np[tid] = a.ab_np && jg < (uint64_t)a.npiv ? a.ab_np[jg] : 1;
+            s_w[tid] = a.ab_w && jg < (uint64_t)a.npiv ? a.ab_w[jg] : 1;
         }
         __syncthreads();                               // s_np / s_w are read by other threads in the epilogue
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = a.jl_ptr[J];
         while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
         const uint32_t npair = l1 - lb + 1;            // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
+        pairs_done += npair;
         // pair q into stage (gpair + q) % NSTAGE (thread 0 only)
         auto load = [&](uint32_t q) {
             const int s = (gpair + q) % NSTAGE;
@@ -459,6 +465,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
                 for (int j = 0; j < 16; j++)
                     if (jbase + c * 16 + j < (uint64_t)a.npiv) a.X16[(size_t)t * a.ldX + jbase + c * 16 + j] = xs[j];
             }
+            if (a.Rout && live) {
+                uint16_t *rc = a.Rout + a.rcol[t];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const int64_t i = (int64_t)jbase + c * 16 + j;
+                    if (i < a.npiv) rc[(size_t)(a.rrev - 1 - i) * a.ldR] = xs[j];
+                }
+            }
         }
         fence_proxy_async_global();     // X_J is read by later tasks through the async proxy
         tc::fence_before();
@@ -477,6 +491,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         atomicAdd(&a.ops[0], opsA);
         atomicAdd(&a.ops[1], opsB);
     }
+    if (tid == 0) atomicAdd(&a.ops[2], pairs_done);
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<512>(tbase);
@@ -676,8 +691,8 @@ static gbla_status band_build(gbla_mat h)
     bt->NNB = (nN + 127) / 128;
     bt->ntiles = (h->mN + 127) / 128;
     const int64_t NB = bt->NB, NNB = bt->NNB;
-    GBLA_TRY(dalloc_t(h, 2, &bt->ops));
-    GBLA_CUDA_TRY(cudaMemsetAsync(bt->ops, 0, 16, st));
+    GBLA_TRY(dalloc_t(h, 3, &bt->ops));
+    GBLA_CUDA_TRY(cudaMemsetAsync(bt->ops, 0, 24, st));
     if (NB == 0) return GBLA_OK;
     GBLA_TRY(dalloc_t(h, NB, &bt->amax));
     GBLA_TRY(dalloc_t(h, NB, &bt->bmin));
@@ -796,11 +811,53 @@ static int64_t xt_batch_tiles(gbla_mat h, int64_t nl)
     return b < nl ? (b > 0 ? b : 1) : nl;
 }
 
+// Target tiles per task group of the sweep (GBLA_SWEEP_GROUP / GBLA_BSUB_GROUP = n; default: one
+// group, i.e. plain J-major order).  Small groups keep a target tile's X_I in L2 between its
+// consecutive J (several J of one tile in flight) and large ones share each Â tile among many
+// tiles; measured on c2 (sparse sweep / back substitution): groups of 4 and 8 tiles are chain-bound
+// (368 / 190 ms against 107 ms J-major: a tile's chain advances one J per last pair + epilogue +
+// flag hand-off, slower than 18-37 CTAs consume its tasks), 32 and 64 equal to J-major.
+static int64_t tile_group_size(int64_t grid, double pairs, int64_t nl, const char *env)
+{
+    (void)grid;
+    (void)pairs;
+    const char *e = getenv(env);
+    int64_t g = e && atoll(e) > 0 ? atoll(e) : nl;
+    if (g < 1) g = 1;
+    return g < nl ? g : (nl > 0 ? nl : 1);
+}
+
+// What one sweep solves: x_t A = c_t for the targets t (A = the band tiles of bt, C in bt->Xt)
+struct SweepSrc {
+    BandTiles *bt;
+    int64_t mN, npiv;                        // targets, pivots (A is npiv x npiv)
+    const uint32_t *order, *tlead;           // targets sorted by lead; sigma(lead) per target
+    uint16_t *X16 = nullptr;                 // optional u16 copy of X (row t, ldX)
+    int64_t ldX = 0;
+    const uint32_t *ab_w = nullptr, *ab_np = nullptr;   // Alg 2 op counts (NULL: none)
+    uint16_t *Rout = nullptr;                // optional reversed transposed output (bsub_rref)
+    int64_t ldR = 0, rrev = 0;
+    const uint32_t *rcol = nullptr;
+    int kt = KT_SWEEP;                       // timer family (-1: none)
+    const char *group_env = "GBLA_SWEEP_GROUP";   // tile_group_size override
+};
+
+static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pworld, int64_t i0, int64_t i1);
+
 // K5' for the local target tiles [i0, i1) (T = prank + pworld * i)
 static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0, int64_t i1, bool want_x16)
 {
+    SweepSrc src;
+    src.bt = h->bt; src.mN = h->mN; src.npiv = h->npiv; src.order = h->order; src.tlead = h->tlead;
+    src.X16 = want_x16 ? h->X : nullptr; src.ldX = h->ldX;
+    src.ab_w = h->ab_w; src.ab_np = h->ab_np;
+    return sweep_run(h, src, prank, pworld, i0, i1);
+}
+
+static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pworld, int64_t i0, int64_t i1)
+{
     cudaStream_t st = h->stream;
-    BandTiles *bt = h->bt;
+    BandTiles *bt = src.bt;
     const int64_t nl = i1 - i0;
     const int64_t NB = bt->NB;
     if (NB == 0 || nl <= 0) return GBLA_OK;
@@ -810,56 +867,65 @@ static gbla_status tc_sweep_batch(gbla_mat h, int prank, int pworld, int64_t i0,
         GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, sweep_threads(), SWEEP_SMEM));
         if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     }
-    // task schedule: first block of every local tile -> J-major task offsets
-    uint32_t *jmin, *toff, *flags;
+    // task schedule: first block of every local tile -> grouped task list
+    uint32_t *jmin, *flags;
+    uint64_t *tasks;
     unsigned int *next;
     GBLA_TRY(dalloc_t(h, nl, &jmin));
-    GBLA_TRY(dalloc_t(h, NB + 1, &toff));
     GBLA_TRY(dalloc_t(h, (size_t)nl * NB, &flags));
     GBLA_TRY(dalloc_t(h, 1, &next));
-    k_tile_jmin<<<grid_for(nl, 256), 256, 0, st>>>(nl, h->mN, h->npiv, NB, prank, pworld, i0, h->order, h->tlead,
+    k_tile_jmin<<<grid_for(nl, 256), 256, 0, st>>>(nl, src.mN, src.npiv, NB, prank, pworld, i0, src.order, src.tlead,
                                                      jmin);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
-    std::vector<uint32_t> hj(nl), ho(NB + 1);
+    std::vector<uint32_t> hj(nl), hjl(NB + 1);
     GBLA_CUDA_TRY(cudaMemcpyAsync(hj.data(), jmin, nl * 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(hjl.data(), bt->jl_ptr, (NB + 1) * 4, cudaMemcpyDeviceToHost, st));
     GBLA_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)nl * NB * 4, st));
     GBLA_CUDA_TRY(cudaMemsetAsync(next, 0, 4, st));
     GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int64_t q = 1; q < nl; q++)
+        if (hj[q] < hj[q - 1]) { set_error("k_sweep: target tiles not sorted by lead"); return GBLA_E_INTERNAL; }
+    int64_t grid = (int64_t)h->ctx->sm_count * occ;
+    std::vector<uint64_t> ht;
     {
-        // tiles are sorted by lead, so jmin is nondecreasing in i: active tiles of J are a prefix
-        int64_t i = 0;
-        uint64_t tot = 0;
-        for (int64_t J = 0; J < NB; J++) {
-            while (i < nl && hj[i] <= (uint64_t)J) i++;
-            ho[J] = (uint32_t)tot;
-            tot += (uint64_t)i;
+        // mean tile pairs per task (band depth) over the active blocks
+        double pairs = 0.0, nact = 0.0;
+        for (int64_t J = (nl ? hj[0] : NB); J < NB; J++) { pairs += hjl[J + 1] - hjl[J] + 1.0; nact += 1.0; }
+        const int64_t GT = tile_group_size(grid, nact > 0 ? pairs / nact : 1.0, nl, src.group_env);
+        // group-major, then J-major over the group's tiles active at J (a prefix: sorted by lead)
+        for (int64_t g0 = 0; g0 < nl; g0 += GT) {
+            const int64_t g1 = g0 + GT < nl ? g0 + GT : nl;
+            int64_t i = g0;
+            for (int64_t J = hj[g0]; J < NB; J++) {
+                while (i < g1 && hj[i] <= (uint64_t)J) i++;
+                for (int64_t q = g0; q < i; q++) ht.push_back(((uint64_t)q << 32) | (uint64_t)J);
+            }
         }
-        ho[NB] = (uint32_t)tot;
-        if (tot >= 0xffffffffull) { set_error("k_sweep: too many tasks"); return GBLA_E_INTERNAL; }
-        for (int64_t q = 1; q < nl; q++)
-            if (hj[q] < hj[q - 1]) { set_error("k_sweep: target tiles not sorted by lead"); return GBLA_E_INTERNAL; }
+        if (ht.size() >= 0xffffffffull) { set_error("k_sweep: too many tasks"); return GBLA_E_INTERNAL; }
     }
-    GBLA_CUDA_TRY(cudaMemcpyAsync(toff, ho.data(), (NB + 1) * 4, cudaMemcpyHostToDevice, st));
-    const uint32_t ntasks = ho[NB];
+    const uint32_t ntasks = (uint32_t)ht.size();
     if (ntasks == 0) return GBLA_OK;
+    GBLA_TRY(dalloc_t(h, ht.size(), &tasks));
+    GBLA_CUDA_TRY(cudaMemcpyAsync(tasks, ht.data(), ht.size() * 8, cudaMemcpyHostToDevice, st));
+    // (pageable source: the copy is staged before cudaMemcpyAsync returns)
     SweepArgs a;
-    a.mN = h->mN; a.npiv = h->npiv; a.NB = NB; a.F = h->F;
-    a.order = h->order; a.tlead = h->tlead;
+    a.mN = src.mN; a.npiv = src.npiv; a.NB = NB; a.F = h->F;
+    a.order = src.order; a.tlead = src.tlead;
     a.tilesA = bt->tilesA; a.invT = bt->invT; a.offA = bt->offA;
     a.jl_ptr = bt->jl_ptr; a.jl_idx = bt->jl_idx;
-    a.Xt = bt->Xt; a.X16 = want_x16 ? h->X : nullptr; a.ldX = h->ldX;
-    a.ab_w = h->ab_w; a.ab_np = h->ab_np; a.ops = bt->ops;
+    a.Xt = bt->Xt; a.X16 = src.X16; a.ldX = src.ldX;
+    a.ab_w = src.ab_w; a.ab_np = src.ab_np; a.ops = bt->ops;
+    a.Rout = src.Rout; a.ldR = src.ldR; a.rrev = src.rrev; a.rcol = src.rcol;
     a.prank = prank; a.pworld = pworld; a.i0 = i0;
-    a.toff = toff; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
-    int64_t grid = (int64_t)h->ctx->sm_count * occ;
+    a.tasks = tasks; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
     if (grid > (int64_t)ntasks) grid = ntasks;
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
     void *kargs[] = {&a};
-    kt_mark(h, KT_SWEEP);
+    if (src.kt >= 0) kt_mark(h, src.kt);
     GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(sweep_threads()), kargs,
                                               (size_t)SWEEP_SMEM, st));
-    kt_mark(h, KT_SWEEP);
+    if (src.kt >= 0) kt_mark(h, src.kt);
     note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -902,8 +968,12 @@ gbla_status tc_read_ops(gbla_mat h, unsigned long long ops[2])
 {
     ops[0] = ops[1] = 0;
     if (!h->bt) return GBLA_OK;
-    GBLA_CUDA_TRY(cudaMemcpyAsync(ops, h->bt->ops, 16, cudaMemcpyDeviceToHost, h->stream));
+    unsigned long long o3[3];
+    GBLA_CUDA_TRY(cudaMemcpyAsync(o3, h->bt->ops, 24, cudaMemcpyDeviceToHost, h->stream));
     GBLA_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    ops[0] = o3[0];
+    ops[1] = o3[1];
+    h->kexec[KT_SWEEP] = o3[2] * EXEC_PER_PAIR;
     return GBLA_OK;
 }
 
@@ -999,3 +1069,267 @@ gbla_status tc_shard(gbla_mat h, int prank, int pworld)
 }
 int64_t tc_ntiles(gbla_mat h) { return h->bt ? h->bt->ntiles : (h->mN + 127) / 128; }
 unsigned long long *tc_ops_dev(gbla_mat h) { return h->bt ? h->bt->ops : nullptr; }
+
+// ---- K14: the fully reduced echelon from a row echelon form (back substitution) -------------
+//
+// R13 asks for RREF(D).  The echelon's panels can stop at a row echelon form U
+// (rows r x nN by pivot column, leading 1, zero below every pivot: GBLA_ECHELON_REF, which on a
+// staircase D_new touches only the rows leading inside each panel's window) and the reduced
+// form is then one triangular solve:
+//   RREF = U_sq^-1 U,  U_sq = U[:, pc] (unit upper triangular):  RREF[:, pc] = I and
+//   X = RREF[:, q] solves U_sq X = U[:, q] for the non-pivot columns q.
+// Column q only involves the r_q = #{pc < q} pivot rows above it (U[i][q] = 0 for pc[i] > q),
+// so the solve costs sum_q r_q (r_q - 1) / 2 modMACs, against the sum over pivot columns c of
+// #{rows above} x #{all columns right of c} that a Gauss-Jordan back elimination spends
+// (which also keeps the future pivot columns of earlier rows up to date).
+// The solve is the K5' sweep itself: transposed and with both pivot orders reversed
+// (a' = r - 1 - i), X^T U_sq^T = U[:, q]^T becomes x'_q A' = c'_q with
+//   A'[a'][b'] = U[r-1-b'][pc[r-1-a']]  (upper unitriangular, dense: every band tile I <= J),
+//   c'_q[a']   = U[r-1-a'][q],  lead of target q = r - r_q (targets: q descending),
+// and the sweep writes x'_q[a'] straight into R[r-1-a'][q] (R = U in place: every target column
+// is read into its C tiles before its batch is swept, the band tiles read pivot columns only).
+namespace {
+
+// A' band tiles, row-major A layout (element (a', b') at toff(a' % 128, b' % 128)) for k_diag_inv /
+// k_ahat; pivots r .. NB*128-1 are identity (padding)
+__global__ void k_bs_band(int64_t r, const uint64_t *__restrict__ tl, const uint64_t *__restrict__ offA,
+                          const uint16_t *__restrict__ U, int64_t ldU, const uint32_t *__restrict__ pc,
+                          uint8_t *__restrict__ tilesA)
+{
+    const uint64_t code = tl[blockIdx.x];
+    const uint32_t I = (uint32_t)(code >> 32), J = (uint32_t)code;
+    uint8_t *tile = tilesA + (offA[I] + (uint64_t)(J - I)) * TB;
+    for (int it = threadIdx.x; it < 128 * 8; it += blockDim.x) {
+        const uint32_t k = it & 127, c16 = (uint32_t)(it >> 7) * 16;
+        const int64_t a = (int64_t)I * 128 + k;
+        const uint32_t col = a < r ? pc[r - 1 - a] : 0;
+        uint8_t lo[16], hi[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int64_t b = (int64_t)J * 128 + c16 + j;
+            uint16_t x = 0;
+            if (a < r && b < r) {
+                if (a <= b) x = U[(size_t)(r - 1 - b) * ldU + col];
+            } else if (a == b) {
+                x = 1;
+            }
+            lo[j] = (uint8_t)(x & 0xff);
+            hi[j] = (uint8_t)(x >> 8);
+        }
+        const uint32_t o = tc::toff(k, c16);
+        *reinterpret_cast<uint4 *>(tile + o) = *reinterpret_cast<const uint4 *>(lo);
+        *reinterpret_cast<uint4 *>(tile + PB + o) = *reinterpret_cast<const uint4 *>(hi);
+    }
+}
+
+// isp[c] = 1 for pivot columns (isp has nN + 1 entries, zeroed)
+__global__ void k_bs_mark(int64_t r, const uint32_t *__restrict__ pc, uint32_t *__restrict__ isp)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < r) isp[pc[k]] = 1;
+}
+
+// targets t = non-pivot columns in ascending order: q[t], lead r - #{pc < q[t]}; slot s holds target
+// nq - 1 - s (leads ascending)
+__global__ void k_bs_targets(int64_t nN, int64_t r, const uint32_t *__restrict__ isp,
+                             const uint32_t *__restrict__ pscan, uint32_t *__restrict__ q,
+                             uint32_t *__restrict__ tlead, uint32_t *__restrict__ order)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nq = nN - r;
+    if (c < nN && !isp[c]) {
+        const int64_t t = c - pscan[c];
+        q[t] = (uint32_t)c;
+        tlead[t] = (uint32_t)(r - pscan[c]);
+        order[nq - 1 - t] = (uint32_t)t;
+    }
+}
+
+// C tiles of the local target tiles [i0, i0 + gridDim.y): tile T, block J >= the tile's first block
+__global__ void k_bs_cfill(int64_t nq, int64_t r, int64_t NB, int64_t i0, const uint32_t *__restrict__ order,
+                           const uint32_t *__restrict__ tlead, const uint32_t *__restrict__ q,
+                           const uint16_t *__restrict__ U, int64_t ldU, uint8_t *__restrict__ Xt)
+{
+    const int64_t J = blockIdx.x, li = blockIdx.y, T = i0 + li;
+    const int64_t s0 = T * 128;
+    if (s0 >= nq) return;
+    const uint32_t l0 = tlead[order[s0]];
+    if (l0 >= (uint64_t)r || J < (int64_t)(l0 / 128)) return;
+    uint8_t *tile = Xt + ((size_t)li * NB + J) * TB;
+    for (int it = threadIdx.x; it < 128 * 8; it += blockDim.x) {
+        const uint32_t row = it & 127, c16 = (uint32_t)(it >> 7) * 16;
+        const int64_t s = s0 + row;
+        const bool live = s < nq;
+        const uint32_t col = live ? q[order[s]] : 0;
+        uint8_t lo[16], hi[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int64_t a = J * 128 + c16 + j;
+            const uint16_t x = (live && a < r) ? U[(size_t)(r - 1 - a) * ldU + col] : 0;
+            lo[j] = (uint8_t)(x & 0xff);
+            hi[j] = (uint8_t)(x >> 8);
+        }
+        const uint32_t o = tc::toff(row, c16);
+        *reinterpret_cast<uint4 *>(tile + o) = *reinterpret_cast<const uint4 *>(lo);
+        *reinterpret_cast<uint4 *>(tile + PB + o) = *reinterpret_cast<const uint4 *>(hi);
+    }
+}
+
+// RREF[i][pc[k]] = 0 for k > i (row i's entries at later pivot columns); the diagonal is 1 already
+__global__ void k_bs_pivcols(int64_t r, const uint32_t *__restrict__ pc, uint16_t *__restrict__ R, int64_t ldR)
+{
+    const int64_t i = blockIdx.x;
+    uint16_t *row = R + (size_t)i * ldR;
+    for (int64_t k = i + 1 + threadIdx.x; k < r; k += blockDim.x) row[pc[k]] = 0;
+}
+
+}  // namespace
+
+// R (rank rows, h->R / h->pivcol) from a row echelon form to the fully reduced one, in place.
+gbla_status bsub_rref(gbla_mat h)
+{
+    cudaStream_t st = h->stream;
+    const int64_t r = h->rank, nN = h->nN, ldR = h->ldR;
+    if (r <= 1) return GBLA_OK;                      // nothing above any pivot
+    const int64_t nq = nN - r;
+    uint16_t *R = h->R;
+    const uint32_t *pc = h->pivcol;
+    kt_mark(h, KT_BSUB);
+    if (nq > 0) {
+        // targets
+        uint32_t *isp, *pscan, *q, *tlead, *order;
+        GBLA_TRY(dalloc_t(h, nN + 1, &isp));
+        GBLA_TRY(dalloc_t(h, nN + 1, &pscan));
+        GBLA_TRY(dalloc_t(h, nq, &q));
+        GBLA_TRY(dalloc_t(h, nq, &tlead));
+        GBLA_TRY(dalloc_t(h, nq, &order));
+        GBLA_CUDA_TRY(cudaMemsetAsync(isp, 0, (nN + 1) * 4, st));
+        k_bs_mark<<<grid_for(r, 256), 256, 0, st>>>(r, pc, isp);
+        {
+            size_t tb = 0;
+            GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, isp, pscan, (int)(nN + 1), st));
+            void *t;
+            GBLA_TRY(dalloc(h, tb + 16, &t));
+            GBLA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t, tb, isp, pscan, (int)(nN + 1), st));
+        }
+        k_bs_targets<<<grid_for(nN, 256), 256, 0, st>>>(nN, r, isp, pscan, q, tlead, order);
+        note_launch(2);
+        GBLA_CUDA_TRY(cudaGetLastError());
+        // algorithmic work: sum over targets of r_q (r_q - 1) / 2
+        {
+            std::vector<uint32_t> hl(nq);
+            GBLA_CUDA_TRY(cudaMemcpyAsync(hl.data(), tlead, nq * 4, cudaMemcpyDeviceToHost, st));
+            GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+            uint64_t w = 0;
+            for (int64_t t = 0; t < nq; t++) {
+                const uint64_t rq = (uint64_t)(r - hl[t]);
+                w += rq * (rq ? rq - 1 : 0) / 2;
+            }
+            h->kwork[KT_BSUB] = w;
+        }
+        // A' band: every tile I <= J of the NB x NB block triangle
+        BandTiles bt;
+        bt.NB = (r + 127) / 128;
+        const int64_t NB = bt.NB;
+        std::vector<uint64_t> offA(NB), tl;
+        std::vector<uint32_t> amax(NB, (uint32_t)(NB - 1)), jptr(NB + 1), jidx;
+        uint64_t nA = 0;
+        for (int64_t I = 0; I < NB; I++) { offA[I] = nA; nA += (uint64_t)(NB - I); }
+        for (int64_t J = 0; J < NB; J++) {
+            jptr[J] = (uint32_t)jidx.size();
+            for (int64_t I = 0; I < J; I++) jidx.push_back((uint32_t)I);
+        }
+        jptr[NB] = (uint32_t)jidx.size();
+        for (int64_t I = 0; I < NB; I++)
+            for (int64_t J = I; J < NB; J++) tl.push_back(((uint64_t)I << 32) | (uint64_t)J);
+        uint64_t *dtl;
+        GBLA_TRY(dalloc_t(h, tl.size(), &dtl));
+        GBLA_TRY(dalloc_t(h, NB, &bt.offA));
+        GBLA_TRY(dalloc_t(h, NB, &bt.amax));
+        GBLA_TRY(dalloc_t(h, NB + 1, &bt.jl_ptr));
+        GBLA_TRY(dalloc_t(h, jidx.size() + 1, &bt.jl_idx));
+        GBLA_TRY(dalloc_t(h, 3, &bt.ops));
+        GBLA_TRY(dalloc(h, nA * TB + 16, (void **)&bt.tilesA));
+        GBLA_TRY(dalloc(h, NB * TB + 16, (void **)&bt.invT));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(dtl, tl.data(), tl.size() * 8, cudaMemcpyHostToDevice, st));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(bt.offA, offA.data(), NB * 8, cudaMemcpyHostToDevice, st));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(bt.amax, amax.data(), NB * 4, cudaMemcpyHostToDevice, st));
+        GBLA_CUDA_TRY(cudaMemcpyAsync(bt.jl_ptr, jptr.data(), (NB + 1) * 4, cudaMemcpyHostToDevice, st));
+        if (!jidx.empty())
+            GBLA_CUDA_TRY(cudaMemcpyAsync(bt.jl_idx, jidx.data(), jidx.size() * 4, cudaMemcpyHostToDevice, st));
+        GBLA_CUDA_TRY(cudaMemsetAsync(bt.ops, 0, 24, st));
+        k_bs_band<<<(unsigned)tl.size(), 256, 0, st>>>(r, dtl, bt.offA, R, ldR, pc, bt.tilesA);
+        note_launch();
+        {
+            static unsigned long long attr = 0;   // devices done (dev_bit)
+            if (!(attr & dev_bit())) {
+                GBLA_CUDA_TRY(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, DIAG_SMEM));
+                GBLA_CUDA_TRY(cudaFuncSetAttribute(k_ahat, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB));
+                attr |= dev_bit();
+            }
+        }
+        k_diag_inv<<<(unsigned)NB, 128, DIAG_SMEM, st>>>(h->F, bt.offA, bt.tilesA, bt.invT);
+        note_launch();
+        {
+            // the off-diagonal tiles: the tail of each row block's list (diagonal tiles first)
+            std::vector<uint64_t> off;
+            for (int64_t I = 0; I < NB; I++)
+                for (int64_t J = I + 1; J < NB; J++) off.push_back(((uint64_t)I << 32) | (uint64_t)J);
+            if (!off.empty()) {
+                uint64_t *doff;
+                GBLA_TRY(dalloc_t(h, off.size(), &doff));
+                GBLA_CUDA_TRY(cudaMemcpyAsync(doff, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+                const int64_t nt = (int64_t)off.size();
+                const int64_t grid = nt < 2 * (int64_t)h->ctx->sm_count ? nt : 2 * (int64_t)h->ctx->sm_count;
+                k_ahat<<<(unsigned)grid, 128, 2 * TB, st>>>(h->F, NB, bt.offA, bt.amax, doff, nt, bt.tilesA, bt.invT);
+                note_launch();
+            }
+        }
+        GBLA_CUDA_TRY(cudaGetLastError());
+        // target tiles in batches of X tiles
+        const int64_t ntiles = (nq + 127) / 128;
+        const int64_t per_tile = NB * (int64_t)TB;
+        int64_t per = ntiles;
+        {
+            const char *e = getenv("GBLA_XT_BATCH");
+            if (e && atoll(e) > 0) per = atoll(e);
+            else if (ntiles * per_tile > ((int64_t)8 << 30)) {
+                size_t fr = 0, tot = 0;
+                if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError();
+                if (h->ctx->memq) fr = h->ctx->memq(h->ctx->memq_user);
+                const int64_t budget = (int64_t)fr - ((int64_t)4 << 30);
+                per = budget > per_tile ? budget / per_tile : 1;
+            }
+            if (per > ntiles) per = ntiles;
+            if (per > 65535) per = 65535;
+            if (per < 1) per = 1;
+        }
+        GBLA_TRY(dalloc(h, (size_t)per * per_tile + 16, (void **)&bt.Xt));
+        SweepSrc src;
+        src.bt = &bt; src.mN = nq; src.npiv = r; src.order = order; src.tlead = tlead;
+        src.Rout = R; src.ldR = ldR; src.rrev = r; src.rcol = q; src.kt = -1;   // timed as a whole
+        src.group_env = "GBLA_BSUB_GROUP";
+        for (int64_t i0 = 0; i0 < ntiles; i0 += per) {
+            const int64_t i1 = i0 + per < ntiles ? i0 + per : ntiles;
+            k_bs_cfill<<<dim3((unsigned)NB, (unsigned)(i1 - i0)), 256, 0, st>>>(nq, r, NB, i0, order, tlead, q, R, ldR,
+                                                                              bt.Xt);
+            note_launch();
+            GBLA_CUDA_TRY(cudaGetLastError());
+            GBLA_TRY(sweep_run(h, src, 0, 1, i0, i1));
+        }
+        GBLA_TRY(sweep_dev_err(st, "gbla_echelon_D (back substitution)"));
+        unsigned long long o3[3];
+        GBLA_CUDA_TRY(cudaMemcpyAsync(o3, bt.ops, 24, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        h->kexec[KT_BSUB] = o3[2] * EXEC_PER_PAIR;
+        dfree(h, bt.Xt);
+        dfree(h, bt.tilesA);
+        dfree(h, bt.invT);
+        bt.Xt = bt.tilesA = bt.invT = nullptr;
+    }
+    k_bs_pivcols<<<(unsigned)r, 256, 0, st>>>(r, pc, R, ldR);
+    note_launch();
+    kt_mark(h, KT_BSUB);
+    GBLA_CUDA_TRY(cudaGetLastError());
+    return GBLA_OK;
+}

@@ -48,7 +48,7 @@ def gpu_reduce(gb, ctx, M, flags=0):
     return h
 
 
-def check_full(gb, ctx, M, res=None, flags=0, check_dnew=True):
+def check_full(gb, ctx, M, res=None, flags=0, check_dnew=True, keep=False):
     if res is None:
         res = oracle.reduce(M, want_x=True)
     S = res.splice
@@ -73,6 +73,8 @@ def check_full(gb, ctx, M, res=None, flags=0, check_dnew=True):
     assert r == rank == res.rank
     assert np.array_equal(np_(pc), res.pivcol)
     assert np.array_equal(np_(R), res.R)
+    if keep:
+        return h
     h.free()
 
 
@@ -601,6 +603,7 @@ def test_super_panels_rref_exact(gb, ctx, monkeypatch):
     back elimination into earlier pivot rows), in full RREF mode and with look-ahead, bit-exact
     against the oracle's R at scaled c2, c3 and c4 with several super-panels; also
     2 panels per super-panel and a partial last super-panel."""
+    monkeypatch.setenv("GBLA_BACKSUB", "0")         # the Gauss-Jordan back elimination in the panels
     for name, sc in (("c2", 0.05), ("c3", 0.1), ("c4", 0.012)):
         M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
         res = oracle.reduce(M)
@@ -630,3 +633,63 @@ def test_sharded_sparse_phase_emulated_ranks(gb, ctx, c0_matrix, c0_oracle, monk
             assert h.opcount()[0] == res.modmac
             h.free()
     monkeypatch.delenv("GBLA_DIST_EMULATE")
+
+
+def test_backsub_rref_exact(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """K14: the RREF through a row echelon form and one triangular solve RREF = U_sq^-1 U (the K5'
+    sweep on the reversed, transposed pivot block; R13), forced on every config shape at
+    reduced scale (several 128-pivot blocks, long accumulations folded every 128 tile pairs on the
+    unbanded triangle), with forced 1- and 3-tile batches of target tiles, and on c0: R, rank and
+    pivot columns bit-exact against the oracle; the Gauss-Jordan path (GBLA_BACKSUB=0) agrees."""
+    monkeypatch.setenv("GBLA_BACKSUB", "1")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    for name, sc in (("c1", 0.05), ("c2", 0.03), ("c3", 0.06), ("c4", 0.01)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        res = oracle.reduce(M)
+        h = check_full(gb, ctx, M, res, check_dnew=False, keep=True)
+        assert h.kernel_work()["backsub"] > 0, name          # the solve ran (non-pivot columns exist)
+        h.free()
+        if name in ("c1", "c3"):
+            for b in ("1", "3"):
+                monkeypatch.setenv("GBLA_XT_BATCH", b)
+                check_full(gb, ctx, M, res, check_dnew=False)
+            monkeypatch.delenv("GBLA_XT_BATCH")
+    monkeypatch.setenv("GBLA_BACKSUB", "0")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+
+
+def test_backsub_edge_cases(gb, ctx, monkeypatch):
+    """K14 on the degenerate shapes: rank 0 and 1 (nothing above a pivot), a full-rank square D (no
+    non-pivot column: only the pivot columns are cleared), a single non-pivot column, dense random
+    D over small and large p, all bit-exact against the oracle."""
+    monkeypatch.setenv("GBLA_BACKSUB", "1")
+    from pins import matmul_mod
+    rng = np.random.default_rng(11)
+    npiv = 130
+    for p in (3, 251, 65521):
+        for (mn, nn, rk) in ((5, 7, 0), (6, 9, 1), (40, 40, 40), (40, 41, 40), (150, 260, 137), (300, 300, 150)):
+            a = np.zeros((npiv + mn, npiv + nn), dtype=np.int64)
+            a[:npiv, :npiv] = np.triu(rng.integers(0, p, (npiv, npiv)))
+            np.fill_diagonal(a[:npiv, :npiv], 1)
+            a[:npiv, npiv:] = rng.integers(0, p, (npiv, nn))
+            base = rng.integers(0, p, (max(rk, 1), npiv + nn))
+            comb = rng.integers(0, p, (mn, max(rk, 1))) if rk else np.zeros((mn, 1), np.int64)
+            a[npiv:, :] = matmul_mod(comb, base, p)
+            M = csr_from_dense(a, p)
+            res = oracle.reduce(M)
+            if p > 3:
+                assert res.rank == rk, (p, mn, nn, rk, res.rank)
+            check_full(gb, ctx, M, res)
+
+
+def test_backsub_choice(gb, ctx, monkeypatch):
+    """Default choice of the echelon route (echelon.cu use_bsub): a staircase D_new (rows leading in
+    distinct columns: the c1/c2/c4 shapes) takes the row echelon form + back substitution, a dense
+    D_new (rows leading in the same few columns: c3) the Gauss-Jordan panels."""
+    monkeypatch.delenv("GBLA_BACKSUB", raising=False)
+    for name, sc, want in (("c2", 0.03, True), ("c3", 0.06, False)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        res = oracle.reduce(M)
+        h = check_full(gb, ctx, M, res, check_dnew=False, keep=True)
+        assert (h.kernel_work()["backsub"] > 0) == want, name
+        h.free()
