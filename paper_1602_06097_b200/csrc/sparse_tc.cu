@@ -221,6 +221,18 @@ struct SweepArgs {
     uint32_t ntasks;
 };
 
+// first position in the ascending list v[lo, hi) with v >= key (hi if none)
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__ v, uint32_t lo, uint32_t hi,
+                                                    uint32_t key)
+{
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (v[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
 {
     uint32_t v;
@@ -353,8 +365,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
         }
         __syncthreads();                               // s_np / s_w are read by other threads in the epilogue
         const uint32_t l1 = a.jl_ptr[J + 1];
-        uint32_t lb = a.jl_ptr[J];
-        while (lb < l1 && a.jl_idx[lb] < Jmin) lb++;
+        uint32_t lb = lower_bound_u32(a.jl_idx, a.jl_ptr[J], l1, (uint32_t)Jmin);   // first I >= Jmin
         const uint32_t npair = l1 - lb + 1;            // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
         pairs_done += npair;
         // pair q into stage (gpair + q) % NSTAGE (thread 0 only)
@@ -574,12 +585,13 @@ struct UpdArgs {
     int64_t i0;                    // first local tile of the batch (Xt is batch-relative)
 };
 
-constexpr int UPD_SMEM = 2 * 65536;
+constexpr int UPD_NS = 3;                        // operand stages (one CTA per SM either way)
+constexpr int UPD_SMEM = UPD_NS * 65536;
 
 __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t full[2], mdone[2], accbar;
+    __shared__ uint64_t full[UPD_NS], mdone[UPD_NS], accbar;
     __shared__ uint32_t tmem_s;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t K = blockIdx.x, T = a.prank + a.pworld * (a.i0 + (int64_t)blockIdx.y), first = T * 128;
@@ -587,14 +599,12 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     if (lead0 >= (uint64_t)a.npiv) return;
     const int64_t Jmin = lead0 / 128;
     const uint32_t l1 = a.kl_ptr[K + 1];
-    uint32_t lb = a.kl_ptr[K];
-    while (lb < l1 && a.kl_idx[lb] < Jmin) lb++;
+    const uint32_t lb = lower_bound_u32(a.kl_idx, a.kl_ptr[K], l1, (uint32_t)Jmin);
     const uint32_t nI = l1 - lb;
     if (nI == 0) return;
     if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
     if (tid == 0) {
-        tc::mbar_init(&full[0], 1); tc::mbar_init(&full[1], 1);
-        tc::mbar_init(&mdone[0], 1); tc::mbar_init(&mdone[1], 1);
+        for (int q = 0; q < UPD_NS; q++) { tc::mbar_init(&full[q], 1); tc::mbar_init(&mdone[q], 1); }
         tc::mbar_init(&accbar, 1);
     }
     tc::fence_before();
@@ -603,18 +613,16 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     const uint32_t tbase = tmem_s;
     const uint32_t sStg = tc::smem_u32(smem);
     const uint8_t *Xrow = a.Xt + (size_t)blockIdx.y * a.NB * TB;
-    uint32_t ph_full[2] = {0, 0}, ph_md[2] = {0, 0}, ph_acc = 0;   // thread 0 / all
+    uint32_t ph_full[UPD_NS] = {}, ph_md[UPD_NS] = {}, ph_acc = 0;   // thread 0 / all
     auto load = [&](uint32_t it) {                     // thread 0 only
         const uint32_t I = a.kl_idx[lb + it];
-        const int s = it & 1;
+        const int s = it % UPD_NS;
         tc::mbar_expect_tx(&full[s], 2 * TB);
         tc::bulk_g2s(smem + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
         tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + (a.offB[I] + (uint64_t)(K - a.bmin[I])) * TB, TB, &full[s]);
     };
-    if (tid == 0) {
-        load(0);
-        if (nI > 1) load(1);
-    }
+    if (tid == 0)
+        for (uint32_t q = 0; q < nI && q < (uint32_t)UPD_NS; q++) load(q);
     const int64_t slot = first + tid;
     const bool live = slot < a.mN;
     uint16_t *drow = live ? a.D + (size_t)a.order[slot] * a.ldD + K * 128 : nullptr;
@@ -627,16 +635,19 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
         const uint32_t c1 = c0 + ACC_PAIRS < nI ? c0 + ACC_PAIRS : nI;
         if (tid == 0) {
             for (uint32_t it = c0; it < c1; it++) {
-                const int s = it & 1;
+                const int s = it % UPD_NS;
                 tc::mbar_wait(&full[s], ph_full[s]);
                 ph_full[s] ^= 1;
                 tc::fence_after();
                 issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > c0);
-                if (it + 2 < nI) {
-                    tc::commit(&mdone[s]);
-                    tc::mbar_wait(&mdone[s], ph_md[s]);
-                    ph_md[s] ^= 1;
-                    load(it + 2);
+                if (it + UPD_NS < nI) tc::commit(&mdone[s]);       // stage s is reloaded for it + UPD_NS
+                // refill the stage of the previous pair once its MMAs are done (this pair's MMAs
+                // are queued behind them: the tensor pipe never waits for the refill)
+                if (it >= 1 && it - 1 + UPD_NS < nI) {
+                    const int sp = (it - 1) % UPD_NS;
+                    tc::mbar_wait(&mdone[sp], ph_md[sp]);
+                    ph_md[sp] ^= 1;
+                    load(it - 1 + UPD_NS);
                 }
             }
             tc::commit(&accbar);
