@@ -394,7 +394,10 @@ extern "C" gbla_status gbla_rref_M(gbla_mat h, void *stream, int64_t *rank_M)
     GBLA_TRY(check_mat(h, stream));
     if (h->rank < 0) { set_error("gbla_rref_M: needs gbla_echelon_D first"); return GBLA_E_ORDER; }
     if (h->ref_only) { set_error("gbla_rref_M: needs the fully reduced R (not GBLA_ECHELON_REF)"); return GBLA_E_ORDER; }
-    if (h->dist_rows) { set_error("gbla_rref_M: single-GPU only (D was row-sharded)"); return GBLA_E_INVAL; }
+    if (h->dist_rows || h->dist_phase) {
+        set_error("gbla_rref_M: single-GPU only (the sparse phase ran sharded)");
+        return GBLA_E_INVAL;
+    }
     if (h->rankM < 0) GBLA_TRY(full_rref_impl(h));
     if (rank_M) *rank_M = h->rankM;
     return GBLA_OK;
@@ -428,9 +431,10 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
         // multi-GPU (dist.cu): row-sharded tensor-core sparse phase + D_new all-gather
         PhaseTimer tm(h->stream);
         s = dist_sparse_phase(h);
-        h->phase_ms[1] = tm.stop();
         h->did_fused = h->did_update = true;
-        h->dist_rows = true;
+        h->dist_rows = h->dist_phase = true;
+        if (s == GBLA_OK && dist_echelon_replicated()) s = dist_gather_dnew(h);   // C7
+        h->phase_ms[1] = tm.stop();
     } else if (flags & GBLA_ORDER_STANDARD) {
         s = gbla_reduce_B(h, stream);
         if (s == GBLA_OK) s = gbla_update_D(h, stream);

@@ -26,6 +26,7 @@
 // movement, a local transport.
 #include <nccl.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "internal.cuh"
 
@@ -187,6 +188,96 @@ gbla_status dist_sparse_phase(gbla_mat h)
     GBLA_TRY(sweep_dev_err(st, "gbla_reduce (sharded sparse phase)"));
     if (real) GBLA_TRY(dist_check_async(ctx));
     // D_new stays row-sharded: the echelon is distributed (panel.cu: panels_dist)
+    return GBLA_OK;
+}
+
+// ---- replicated echelon: D_new all-gathered, then the single-GPU echelon on every rank ----------
+// Echelon mode of a multi-GPU reduction (GBLA_DIST_ECHELON): "replicated" (default) gathers D_new
+// so that every rank holds all of it and runs the single-GPU echelon (the K14 / super-panel /
+// look-ahead routes, no per-panel collective or host synchronization; identical R on every rank
+// since every step is deterministic); "panels" keeps D row-sharded and runs the distributed panel
+// Gauss-Jordan (panel.cu: panels_dist; per panel an all-reduce, an all-gather and a host sync).
+bool dist_echelon_replicated()
+{
+    const char *e = getenv("GBLA_DIST_ECHELON");
+    return !(e && strcmp(e, "panels") == 0);
+}
+
+namespace {
+// Dp[slot] = D[order[slot]] for the slots of this rank's target tiles (T = me + G i); block = one slot
+__global__ void k_pack_own(int64_t mN, int64_t ldD, const uint16_t *__restrict__ D, const uint32_t *__restrict__ order,
+                           int me, int G, uint16_t *__restrict__ Dp)
+{
+    const int64_t l = blockIdx.x, T = me + (int64_t)G * (l / 128), slot = T * 128 + l % 128;
+    if (slot >= mN) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(D + (size_t)order[slot] * ldD);
+    uint4 *dst = reinterpret_cast<uint4 *>(Dp + (size_t)slot * ldD);
+    for (int64_t q = threadIdx.x; q < ldD / 8; q += blockDim.x) dst[q] = src[q];
+}
+// D[order[slot]] = Dp[slot] for every slot of the other ranks' tiles
+__global__ void k_unpack_others(int64_t mN, int64_t ldD, const uint16_t *__restrict__ Dp,
+                                const uint32_t *__restrict__ order, int me, int G, uint16_t *__restrict__ D)
+{
+    const int64_t slot = blockIdx.x;
+    if ((slot / 128) % G == me) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(Dp + (size_t)slot * ldD);
+    uint4 *dst = reinterpret_cast<uint4 *>(D + (size_t)order[slot] * ldD);
+    for (int64_t q = threadIdx.x; q < ldD / 8; q += blockDim.x) dst[q] = __ldcs(src + q);
+}
+}  // namespace
+
+// C7 (replicated echelon): every rank ends with all of D_new.  The target tiles (128 slots of the
+// lead order each) were dealt cyclically, so round k = tiles kG .. kG+G-1 is one contiguous block
+// of the slot-ordered buffer Dp in which rank g holds sub-block g: one in-place ncclAllGather per
+// round (grouped), between a pack of this rank's rows into slot order and an unpack of the others'
+// rows back into D's row order.  Extra memory: one D-sized buffer while the gather runs (c4:
+// 45 GB; the band tiles are released by then).  If a rank cannot allocate it, every rank learns
+// it (all-reduce of a flag) and D stays row-sharded (panels_dist).  Emulated ranks share one
+// fully updated D: nothing to move.
+gbla_status dist_gather_dnew(gbla_mat h)
+{
+    gbla_ctx ctx = h->ctx;
+    const bool real = ctx->nccl_comm != nullptr;
+    if (!real) { h->dist_rows = false; return GBLA_OK; }
+    if (h->mN == 0 || h->nN == 0 || h->npiv == 0) { h->dist_rows = false; return GBLA_OK; }
+    ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
+    cudaStream_t st = h->stream;
+    const int G = ctx->world, me = ctx->rank;
+    const int64_t mN = h->mN, ldD = h->ldD;
+    const int64_t ntile = (mN + 127) / 128, rounds = (ntile + G - 1) / G;
+    uint16_t *Dp = nullptr;
+    uint32_t *fail;
+    GBLA_TRY(dalloc_t(h, 1, &fail));
+    const gbla_status as = dalloc_t(h, (size_t)rounds * G * 128 * ldD, &Dp);
+    const uint32_t hf = as == GBLA_OK ? 0u : 1u;
+    GBLA_CUDA_TRY(cudaMemcpyAsync(fail, &hf, 4, cudaMemcpyHostToDevice, st));
+    GBLA_NCCL_TRY(ncclAllReduce(fail, fail, 1, ncclUint32, ncclSum, comm, st));
+    uint32_t nfail = 0;
+    GBLA_CUDA_TRY(cudaMemcpyAsync(&nfail, fail, 4, cudaMemcpyDeviceToHost, st));
+    GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+    GBLA_TRY(dist_check_async(ctx));
+    dfree(h, fail);
+    if (nfail) {                              // some rank is short of memory: keep D row-sharded
+        if (Dp) dfree(h, Dp);
+        return GBLA_OK;
+    }
+    const int64_t own = ((ntile - me + G - 1) / G) * 128;   // slots of this rank's tiles (padded)
+    if (own > 0) k_pack_own<<<(unsigned)own, 256, 0, st>>>(mN, ldD, h->D, h->order, me, G, Dp);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    const size_t blk = (size_t)128 * ldD;    // u16 per tile
+    GBLA_NCCL_TRY(ncclGroupStart());
+    for (int64_t k = 0; k < rounds; k++) {
+        uint16_t *round = Dp + (size_t)k * G * blk;
+        GBLA_NCCL_TRY(ncclAllGather(round + (size_t)me * blk, round, blk * 2, ncclUint8, comm, st));
+    }
+    GBLA_NCCL_TRY(ncclGroupEnd());
+    k_unpack_others<<<(unsigned)mN, 256, 0, st>>>(mN, ldD, Dp, h->order, me, G, h->D);
+    note_launch();
+    GBLA_CUDA_TRY(cudaGetLastError());
+    dfree(h, Dp);
+    GBLA_TRY(dist_check_async(ctx));
+    h->dist_rows = false;
     return GBLA_OK;
 }
 

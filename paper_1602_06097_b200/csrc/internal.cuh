@@ -234,6 +234,7 @@ struct gbla_mat_s {
     bool have_xt = false;              // C' held as tensor-core tiles (sparse_tc.cu)
     bool ref_only = false;             // GBLA_ECHELON_REF: no back elimination in the echelon
     bool dist_rows = false;            // D is row-sharded over the ranks (dist_sparse_phase)
+    bool dist_phase = false;           // the sparse phase ran sharded (no band / C' for gbla_rref_M)
     float phase_ms[5] = {0, 0, 0, 0, 0};
 
     // tensor-core sparse path: dense band tiles of A|B, X tiles (sparse_tc.cu)
@@ -297,6 +298,8 @@ static inline void kt_mark2(gbla_mat h, int a, int b, cudaStream_t s)
 // multi-GPU (dist.cu)
 gbla_status dist_bcast_input(gbla_mat h, const gbla_csr *M, bool host_input, gbla_csr *out, gbla_status root_ok);
 gbla_status dist_sparse_phase(gbla_mat h);
+gbla_status dist_gather_dnew(gbla_mat h);   // replicated echelon: all of D_new on every rank
+bool dist_echelon_replicated();             // GBLA_DIST_ECHELON != "panels"
 gbla_status dist_check_async(gbla_ctx ctx);      // ncclCommGetAsyncError (aborts the comm on error)
 int dist_emulated_world();
 gbla_status densify_impl(gbla_mat h, char which, uint16_t *out, int64_t ld);

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
     const uint32_t tbase = tmem_s;
     const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t ph_acc = 0;
-    uint32_t ph_full[NSTAGE] = {0, 0, 0}, ph_md[NSTAGE] = {0, 0, 0};   // used by thread 0
+    uint32_t ph_full = 0, ph_md = 0;           // phase bit of every stage (thread 0)
     unsigned long long opsA = 0, opsB = 0, pairs_done = 0;   // pairs_done: thread 0
     const uint32_t sStg = tc::smem_u32(stg);
     const uint32_t p = a.F.p;
@@ -404,16 +404,16 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
             if (tid == 0) {
                 for (uint32_t q = c0; q < c1; q++) {
                     const int s = (gpair + q) % NSTAGE;
-                    tc::mbar_wait(&full[s], ph_full[s]);
-                    ph_full[s] ^= 1;
+                    tc::mbar_wait(&full[s], (ph_full >> s) & 1u);
+                    ph_full ^= 1u << s;
                     tc::fence_after();
                     issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, q > c0);
                     if (q + NSTAGE < npair) tc::commit(&mdone[s]);     // stage s is reloaded for q + NSTAGE
                     // refill the stage of the previous pair once its MMAs are done
                     if (q >= 1 && q - 1 + NSTAGE < npair) {
                         const int sp = (gpair + q - 1) % NSTAGE;
-                        tc::mbar_wait(&mdone[sp], ph_md[sp]);
-                        ph_md[sp] ^= 1;
+                        tc::mbar_wait(&mdone[sp], (ph_md >> sp) & 1u);
+                        ph_md ^= 1u << sp;
                         load(q - 1 + NSTAGE);
                     }
                 }
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     const uint32_t tbase = tmem_s;
     const uint32_t sStg = tc::smem_u32(smem);
     const uint8_t *Xrow = a.Xt + (size_t)blockIdx.y * a.NB * TB;
-    uint32_t ph_full[UPD_NS] = {}, ph_md[UPD_NS] = {}, ph_acc = 0;   // thread 0 / all
+    uint32_t ph_full = 0, ph_md = 0, ph_acc = 0;       // phase bit of every stage (thread 0) / all
     auto load = [&](uint32_t it) {                     // thread 0 only
         const uint32_t I = a.kl_idx[lb + it];
         const int s = it % UPD_NS;
@@ -636,8 +636,8 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
         if (tid == 0) {
             for (uint32_t it = c0; it < c1; it++) {
                 const int s = it % UPD_NS;
-                tc::mbar_wait(&full[s], ph_full[s]);
-                ph_full[s] ^= 1;
+                tc::mbar_wait(&full[s], (ph_full >> s) & 1u);
+                ph_full ^= 1u << s;
                 tc::fence_after();
                 issue_mmas(tbase, sStg + s * 65536, sStg + s * 65536 + TB, it > c0);
                 if (it + UPD_NS < nI) tc::commit(&mdone[s]);       // stage s is reloaded for it + UPD_NS
@@ -645,8 +645,8 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
                 // are queued behind them: the tensor pipe never waits for the refill)
                 if (it >= 1 && it - 1 + UPD_NS < nI) {
                     const int sp = (it - 1) % UPD_NS;
-                    tc::mbar_wait(&mdone[sp], ph_md[sp]);
-                    ph_md[sp] ^= 1;
+                    tc::mbar_wait(&mdone[sp], (ph_md >> sp) & 1u);
+                    ph_md ^= 1u << sp;
                     load(it - 1 + UPD_NS);
                 }
             }
@@ -872,12 +872,11 @@ static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pwo
     const int64_t nl = i1 - i0;
     const int64_t NB = bt->NB;
     if (NB == 0 || nl <= 0) return GBLA_OK;
-    static int occ = -1;
-    if (occ < 0) {
-        GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
-        GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, sweep_threads(), SWEEP_SMEM));
-        if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
-    }
+    // set on the current device every time (one context per device; the call is cheap)
+    GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
+    int occ = 0;
+    GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, sweep_threads(), SWEEP_SMEM));
+    if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     // task schedule: first block of every local tile -> grouped task list
     uint32_t *jmin, *flags;
     uint64_t *tasks;

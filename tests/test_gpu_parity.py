@@ -508,9 +508,12 @@ def test_echelon_ref_mode(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     h.free()
     monkeypatch.delenv("GBLA_SP")
     monkeypatch.setenv("GBLA_DIST_EMULATE", "3")
-    h = gpu_reduce(gb, ctx, M, flags=gb.GBLA_ECHELON_REF)
-    check_ref(gb, h, res, M.p)
-    h.free()
+    for mode in ("panels", "replicated"):
+        monkeypatch.setenv("GBLA_DIST_ECHELON", mode)
+        h = gpu_reduce(gb, ctx, M, flags=gb.GBLA_ECHELON_REF)
+        check_ref(gb, h, res, M.p)
+        h.free()
+    monkeypatch.delenv("GBLA_DIST_ECHELON")
     monkeypatch.delenv("GBLA_DIST_EMULATE")
 
 
@@ -565,26 +568,32 @@ def test_full_rref_of_M(gb, ctx, c0_matrix, c0_oracle):
 
 def test_one_rank_nccl_communicator(gb, monkeypatch):
     """The real multi-GPU code path on one GPU (a one-rank NCCL communicator, gbla_ctx_set_comm with
-    world 1): C1 broadcast of M, the row-sharded sparse phase with the op-count all-reduce, the
-    distributed echelon (lead-count all-reduce, candidate all-gather, pivot-row all-reduce, R by
-    broadcasts) -- every ncclBroadcast / ncclAllGather / ncclAllReduce call site runs with its real
-    buffers, counts and types.  R, rank and op counts against the oracle; REF mode too; then
-    detach and reduce again on the single-GPU path."""
+    world 1): C1 broadcast of M, the row-sharded sparse phase with the op-count all-reduce, then
+    either echelon mode: "replicated" (C7: pack, grouped in-place all-gathers of the slot-ordered
+    D_new rounds, unpack; then the single-GPU echelon) or "panels" (the distributed echelon:
+    lead-count all-reduce, candidate all-gather, pivot-row all-reduce, R by broadcasts) -- every
+    ncclBroadcast / ncclAllGather / ncclAllReduce call site runs with its real buffers, counts and
+    types.  R, rank and op counts against the oracle; REF mode too; then detach and reduce again
+    on the single-GPU path."""
     ctx1 = gb.Context(0)
     ctx1.set_comm(gb.nccl_unique_id(), 0, 1)
     cases = [gbla_gen.f4_matrix("c0")]
     for name, sc in (("c1", 0.05), ("c3", 0.03), ("c2", 0.02)):
         cases.append(gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc)))
-    for M in cases:
-        res = oracle.reduce(M)
-        h = gpu_reduce(gb, ctx1, M)
-        r, pc, R = h.rref()
-        assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R), M.name
-        assert h.opcount()[0] == res.modmac
+    for mode in ("replicated", "panels"):
+        monkeypatch.setenv("GBLA_DIST_ECHELON", mode)
+        for M in cases:
+            res = oracle.reduce(M)
+            h = gpu_reduce(gb, ctx1, M)
+            r, pc, R = h.rref()
+            assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R), \
+                (mode, M.name)
+            assert h.opcount()[0] == res.modmac
+            h.free()
+        h = gpu_reduce(gb, ctx1, cases[1], flags=gb.GBLA_ECHELON_REF)
+        check_ref(gb, h, oracle.reduce(cases[1]), cases[1].p)
         h.free()
-    h = gpu_reduce(gb, ctx1, cases[1], flags=gb.GBLA_ECHELON_REF)
-    check_ref(gb, h, oracle.reduce(cases[1]), cases[1].p)
-    h.free()
+    monkeypatch.delenv("GBLA_DIST_ECHELON")
     # the INT-pipe echelon is single-GPU: with a communicator gbla_reduce keeps D whole on every rank
     h = gpu_reduce(gb, ctx1, cases[0], flags=gb.GBLA_DENSE_INT)
     r, pc, R = h.rref()
@@ -626,13 +635,16 @@ def test_sharded_sparse_phase_emulated_ranks(gb, ctx, c0_matrix, c0_oracle, monk
         cases.append((M, oracle.reduce(M)))
     for M, res in cases:
         for G in (2, 3, 8):
-            monkeypatch.setenv("GBLA_DIST_EMULATE", str(G))
-            h = gpu_reduce(gb, ctx, M)
-            r, pc, R = h.rref()
-            assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R)
-            assert h.opcount()[0] == res.modmac
-            h.free()
+            for mode in ("panels", "replicated"):
+                monkeypatch.setenv("GBLA_DIST_EMULATE", str(G))
+                monkeypatch.setenv("GBLA_DIST_ECHELON", mode)
+                h = gpu_reduce(gb, ctx, M)
+                r, pc, R = h.rref()
+                assert r == res.rank and np.array_equal(np_(pc), res.pivcol) and np.array_equal(np_(R), res.R)
+                assert h.opcount()[0] == res.modmac
+                h.free()
     monkeypatch.delenv("GBLA_DIST_EMULATE")
+    monkeypatch.delenv("GBLA_DIST_ECHELON")
 
 
 def test_backsub_rref_exact(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
