@@ -146,13 +146,13 @@ def run_reference(args):
 METRIC = "nnz-AXPY Gop/s mod p (F4 matrix reduction, gbla_reduce)"
 
 # kernel families timed by the library (gbla_get_kernel_ms) and how each is bounded
-KERNEL_NAMES = {"sweep": "k_sweep (K5', C' = C A^-1 block forward substitution, tcgen05)",
+KERNEL_NAMES = {"sweep": "k_sweep<0> (K5', C' = C A^-1 block forward substitution, tcgen05)",
                 "update": "k_update_tc (K7', D -= C' B, tcgen05)",
                 "panel": "k_panel2 (K10, panel echelon form, one CTA)",
                 "trailing": "K11 trailing update (k_modgemm_mk2 CTA-pair K = 512 flushes + k_modgemm_ws / "
                             "k_modgemm_win K = 128 window updates)",
                 "rnew": "k_modgemm_ws<STORE> (K11 new pivot rows)",
-                "backsub": "K14 back substitution RREF = U_sq^-1 U (k_sweep on the pivot block of the row echelon "
+                "backsub": "K14 back substitution RREF = U_sq^-1 U (k_sweep<1> on the pivot block of the row echelon "
                            "form; band / C-tile setup included)"}
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 INT8_PEAK = os.path.join(ROOT, "profiles", "r02_int8_peak.json")      # scripts/peaks/int8_peak.py on a B200

@@ -314,6 +314,9 @@ static int sweep_threads()
 // 128-pivot block the chain of one target tile costs the last tile pair + one
 // epilogue + the flag hand-off.  L2 reuse: the Â tiles of one J are shared by the
 // tiles working on J (tile_group_size: J-major by default).
+// ROLE: 0 = the sparse phase's sweep (K5'), 1 = the K14 back substitution (same code; the two
+// instantiations only keep the two uses apart in profiler launch lists)
+template <int ROLE>
 __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -873,9 +876,10 @@ static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pwo
     const int64_t NB = bt->NB;
     if (NB == 0 || nl <= 0) return GBLA_OK;
     // set on the current device every time (one context per device; the call is cheap)
-    GBLA_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
+    const void *kfn = src.Rout ? (const void *)k_sweep<1> : (const void *)k_sweep<0>;
+    GBLA_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SWEEP_SMEM));
     int occ = 0;
-    GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep, sweep_threads(), SWEEP_SMEM));
+    GBLA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, sweep_threads(), SWEEP_SMEM));
     if (occ < 1) { set_error("k_sweep does not fit on an SM"); return GBLA_E_INTERNAL; }
     // task schedule: first block of every local tile -> grouped task list
     uint32_t *jmin, *flags;
@@ -933,7 +937,7 @@ static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pwo
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
     void *kargs[] = {&a};
     if (src.kt >= 0) kt_mark(h, src.kt);
-    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_sweep, dim3((unsigned)grid), dim3(sweep_threads()), kargs,
+    GBLA_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3((unsigned)grid), dim3(sweep_threads()), kargs,
                                               (size_t)SWEEP_SMEM, st));
     if (src.kt >= 0) kt_mark(h, src.kt);
     note_launch();

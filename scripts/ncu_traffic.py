@@ -12,7 +12,7 @@ import json
 import subprocess
 import sys
 
-FAMILIES = [("k_sweep", "sweep"), ("k_update_tc", "update"), ("k_panel", "panel"),
+FAMILIES = [("k_sweep<1>", "backsub"), ("k_sweep", "sweep"), ("k_update_tc", "update"), ("k_panel", "panel"),
             ("k_modgemm_ws<0", "trailing"), ("k_modgemm_mk2", "trailing"), ("k_modgemm_win", "trailing"),
             ("k_modgemm_ws<1", "rnew")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
