@@ -210,6 +210,8 @@ struct SweepArgs {
     const uint32_t *rcol;
     unsigned long long *ops;
     int64_t prank, pworld;         // target tiles T = prank + pworld * (i0 + li) (multi-GPU row shards)
+    int exp;                       // diagnostics (GBLA_SWEEP_EXP=1): no operand copies after each CTA's
+                                   // first stages (the MMA loop alone; wrong results)
     int64_t i0;                    // first local tile of this batch; Xt / jmin / flags are batch-relative (li)
     // dependency-driven schedule: task q computes X_J of local tile i, (J, i) = tasks[q] (low /
     // high 32 bits).  Tasks are numbered group-major, then J-major inside a group of consecutive
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t s_np[128], s_w[128];
     __shared__ uint32_t s_task;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) tc::tmem_alloc<512>(&tmem_s);
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&mdone[s], 1); }
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
     const uint32_t sStg = tc::smem_u32(stg);
     const uint32_t p = a.F.p;
     uint32_t gpair = 0;                        // stage ring position, continuous across tasks (thread 0)
+    uint32_t nloads = 0;                       // diagnostics (a.exp)
 
     for (;;) {
         if (tid == 0) s_task = atomicAdd(a.next, 1u);
@@ -366,33 +369,80 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(SweepArgs a)
             s_np[tid] = a.ab_np && jg < (uint64_t)a.npiv ? a.ab_np[jg] : 1;
             s_w[tid] = a.ab_w && jg < (uint64_t)a.npiv ? a.ab_w[jg] : 1;
         }
-        __syncthreads();                               // s_np / s_w are read by other threads in the epilogue
         const uint32_t l1 = a.jl_ptr[J + 1];
         uint32_t lb = lower_bound_u32(a.jl_idx, a.jl_ptr[J], l1, (uint32_t)Jmin);   // first I >= Jmin
         const uint32_t npair = l1 - lb + 1;            // (C_J, inv(A_JJ)), then (X_I, Â_IJ)
         pairs_done += npair;
-        // pair q into stage (gpair + q) % NSTAGE (thread 0 only)
+        // the X_I already published: warp 0 reads the list's flags at once (relaxed, 32 per step) and
+        // thread 0 acquires them with ONE fence (+ one proxy fence) instead of an acquire load and a
+        // proxy fence per tile pair on its issue path (measured: those cost a third of the sweep)
+        uint32_t nready = 0;
+        if (warp == 0) {
+            const uint32_t nlist = npair - 1;
+            for (uint32_t b0 = 0; b0 < nlist; b0 += 32) {
+                const uint32_t q = b0 + (uint32_t)lane;
+                uint32_t v = 1;
+                if (q < nlist) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + a.jl_idx[lb + q]) : "memory");
+                const unsigned bad = __ballot_sync(0xffffffffu, v == 0);
+                if (bad) { nready = b0 + (uint32_t)__ffs(bad) - 1; break; }
+                nready = b0 + 32 < nlist ? b0 + 32 : nlist;
+            }
+            if (lane == 0 && nready) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                fence_proxy_async_global();
+            }
+        }
+        __syncthreads();                               // s_np / s_w are read by other threads in the epilogue
+        // thread 0: the list entries (I, tile of Â_IJ) are read ahead of their use, so the global loads
+        // are not on the issue path (entry e + 1's tile and entry e + 2's I while entry e is staged)
+        const uint32_t nlist = npair - 1;
+        uint32_t curI = 0, nxtI = 0;
+        uint64_t curT = 0;
+        if (tid == 0 && nlist > 0) {
+            curI = __ldg(a.jl_idx + lb);
+            if (nlist > 1) nxtI = __ldg(a.jl_idx + lb + 1);
+            curT = __ldg(a.offA + curI) + (uint64_t)(J - curI);
+        }
+        // pair q into stage (gpair + q) % NSTAGE (thread 0 only, q ascending)
         auto load = [&](uint32_t q) {
             const int s = (gpair + q) % NSTAGE;
             uint8_t *sa = stg + s * 65536, *sb = sa + TB;
-            tc::mbar_expect_tx(&full[s], 2 * TB);
-            if (q == 0) {
-                tc::bulk_g2s(sb, a.invT + (size_t)J * TB, TB, &full[s]);
-                tc::bulk_g2s(sa, Xrow + (size_t)J * TB, TB, &full[s]);          // C_J (not yet overwritten)
+            if (a.exp == 1 && nloads >= (uint32_t)NSTAGE) {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&full[s])) : "memory");
                 return;
             }
-            const uint32_t I = a.jl_idx[lb + q - 1];
-            tc::bulk_g2s(sb, a.tilesA + (a.offA[I] + (uint64_t)(J - I)) * TB, TB, &full[s]);   // Â_IJ
-            // X_I[T] is produced by task (li, I): wait until it is published
-            if (ld_acquire(fl + I) == 0) {
-                // every CTA is resident (cooperative launch) and tasks are claimed in dependency
-                // order, so X_I is on its way; bounded all the same (never hang the GPU)
-                for (uint32_t it = 0; ld_acquire(fl + I) == 0; it++) {
-                    __nanosleep(32);
-                    if (it > (1u << 26)) { dev_err_latch(DEVERR_SWEEP_FLAG); break; }
-                }
+            const bool warm = nloads >= (uint32_t)NSTAGE;
+            nloads++;
+            // diagnostics: 2 = skip the Â copies, 3 = skip the X copies (after the first stages)
+            const bool skipB = a.exp == 2 && warm, skipA = a.exp == 3 && warm;
+            tc::mbar_expect_tx(&full[s], (skipA || skipB) ? TB : 2 * TB);
+            if (q == 0) {
+                if (!skipB) tc::bulk_g2s(sb, a.invT + (size_t)J * TB, TB, &full[s]);
+                if (!skipA) tc::bulk_g2s(sa, Xrow + (size_t)J * TB, TB, &full[s]);          // C_J (not yet overwritten)
+                return;
             }
-            fence_proxy_async_global();
+            const uint32_t I = curI;
+            const uint64_t tileA = curT;
+            {
+                const uint32_t e = q - 1;                  // advance the read-ahead
+                curI = nxtI;
+                curT = e + 1 < nlist ? __ldg(a.offA + nxtI) + (uint64_t)(J - nxtI) : 0;
+                nxtI = e + 2 < nlist ? __ldg(a.jl_idx + lb + e + 2) : 0;
+            }
+            if (!skipB) tc::bulk_g2s(sb, a.tilesA + tileA * TB, TB, &full[s]);   // Â_IJ
+            if (skipA) return;
+            // X_I[T] is produced by task (li, I): wait until it is published (unless the scan saw it)
+            if (q - 1 >= nready) {
+                if (ld_acquire(fl + I) == 0) {
+                    // every CTA is resident (cooperative launch) and tasks are claimed in dependency
+                    // order, so X_I is on its way; bounded all the same (never hang the GPU)
+                    for (uint32_t it = 0; ld_acquire(fl + I) == 0; it++) {
+                        __nanosleep(32);
+                        if (it > (1u << 26)) { dev_err_latch(DEVERR_SWEEP_FLAG); break; }
+                    }
+                }
+                fence_proxy_async_global();
+            }
             tc::bulk_g2s(sa, Xrow + (size_t)I * TB, TB, &full[s]);
         };
         // exactness: one TMEM accumulation covers at most ACC_PAIRS tile pairs (K = 128 each):
@@ -617,12 +667,25 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
     const uint32_t sStg = tc::smem_u32(smem);
     const uint8_t *Xrow = a.Xt + (size_t)blockIdx.y * a.NB * TB;
     uint32_t ph_full = 0, ph_md = 0, ph_acc = 0;       // phase bit of every stage (thread 0) / all
-    auto load = [&](uint32_t it) {                     // thread 0 only
-        const uint32_t I = a.kl_idx[lb + it];
+    // thread 0: list entries read ahead of their use (entry it + 1's tile and entry it + 2's I while
+    // entry it is staged), so no dependent global load sits on the issue path
+    uint32_t curI = 0, nxtI = 0;
+    uint64_t curT = 0;
+    if (tid == 0) {
+        curI = __ldg(a.kl_idx + lb);
+        if (nI > 1) nxtI = __ldg(a.kl_idx + lb + 1);
+        curT = __ldg(a.offB + curI) + (uint64_t)(K - __ldg(a.bmin + curI));
+    }
+    auto load = [&](uint32_t it) {                     // thread 0 only, it ascending
+        const uint32_t I = curI;
+        const uint64_t tileB = curT;
+        curI = nxtI;
+        curT = it + 1 < nI ? __ldg(a.offB + nxtI) + (uint64_t)(K - __ldg(a.bmin + nxtI)) : 0;
+        nxtI = it + 2 < nI ? __ldg(a.kl_idx + lb + it + 2) : 0;
         const int s = it % UPD_NS;
         tc::mbar_expect_tx(&full[s], 2 * TB);
         tc::bulk_g2s(smem + s * 65536, Xrow + (size_t)I * TB, TB, &full[s]);
-        tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + (a.offB[I] + (uint64_t)(K - a.bmin[I])) * TB, TB, &full[s]);
+        tc::bulk_g2s(smem + s * 65536 + TB, a.tilesB + tileB * TB, TB, &full[s]);
     };
     if (tid == 0)
         for (uint32_t q = 0; q < nI && q < (uint32_t)UPD_NS; q++) load(q);
@@ -933,6 +996,7 @@ static gbla_status sweep_run(gbla_mat h, const SweepSrc &src, int prank, int pwo
     a.Rout = src.Rout; a.ldR = src.ldR; a.rrev = src.rrev; a.rcol = src.rcol;
     a.prank = prank; a.pworld = pworld; a.i0 = i0;
     a.tasks = tasks; a.jmin = jmin; a.flags = flags; a.next = next; a.ntasks = ntasks;
+    a.exp = getenv("GBLA_SWEEP_EXP") ? atoi(getenv("GBLA_SWEEP_EXP")) : 0;
     if (grid > (int64_t)ntasks) grid = ntasks;
     // co-residency of every CTA is what makes the flag waits safe: cooperative launch
     void *kargs[] = {&a};
