@@ -326,7 +326,7 @@ def main():
         for k, w in h.kernel_exec().items():
             kexec[k] += w
         ops, dense_ops = h.opcount()
-        rank_d = h.dims(), h.rref()[0]
+        rank_d = h.dims(), h.rank()
         h.free()
     torch.cuda.synchronize()
     clk = clocks.stop()

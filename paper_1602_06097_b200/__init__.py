@@ -329,6 +329,12 @@ class Mat:
         return (_view(ptr.value, (npairs + 1,), "<u8").clone(), _view(col.value, (n,), "<u4").clone(),
                 _view(ln.value, (n,), "<u4").clone(), _view(sl.value, (n,), "<u4").clone())
 
+    def rank(self):
+        """rank(D) (no copy of R)."""
+        rk = ctypes.c_int64()
+        _check(_lib.gbla_get_rref(self._h, ctypes.byref(rk), None, None, None))
+        return rk.value
+
     def rref(self):
         """(rank, pivcol[rank], R[rank x nN]) as new torch tensors."""
         npiv, mN, nN = self.dims()
