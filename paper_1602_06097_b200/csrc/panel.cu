@@ -146,16 +146,37 @@ __device__ __forceinline__ void st8(uint16_t *s, const uint32_t (&v)[8])
 
 // lead[r] = first nonzero column of active row r in [c0, c0 + PW) relative to c0, else NONE.
 // One warp per row, 8 columns (16 bytes) per lane per step.
+// Row echelon form (srow != NULL: rows sorted by their initial leading column skey, D in place):
+// a row's lead only moves right, so only the rows with skey < c0 + PW can lead in the window;
+// the others keep lead NONE (set once before the first panel) and are not read.
 __global__ void k_lead2(int64_t mN, int64_t nN, const uint16_t *__restrict__ D, int64_t ldD,
                         const uint32_t *__restrict__ rowpiv, const P2State *__restrict__ prev,
-                        uint32_t *__restrict__ lead, const uint8_t *__restrict__ owner, int me)
+                        uint32_t *__restrict__ lead, const uint8_t *__restrict__ owner, int me,
+                        const uint32_t *__restrict__ srow = nullptr, const uint32_t *__restrict__ skey = nullptr)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t c0 = prev->c1;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < mN;
-         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t nrow = mN;
+    if (srow) {
+        __shared__ uint32_t s_n;
+        if (threadIdx.x == 0) {
+            const int64_t c = c0 + PW;
+            int64_t lo = 0, hi = mN;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)skey[mid] < c) lo = mid + 1;
+                else hi = mid;
+            }
+            s_n = (uint32_t)lo;
+        }
+        __syncthreads();
+        nrow = s_n;
+    }
+    for (int64_t ri = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ri < nrow;
+         ri += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = srow ? (int64_t)srow[ri] : ri;
     if (owner && owner[r] != me) continue;                 // another rank's row
     uint32_t res = NONE16;
     if (rowpiv[r] == GBLA_NONE && c0 < nN) {
@@ -1249,7 +1270,8 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
                           const uint8_t *__restrict__ owner, int me, uint8_t *__restrict__ Fdlo = nullptr,
                           uint8_t *__restrict__ Fdhi = nullptr, int G = 1, int j = 0, int64_t *__restrict__ kb_c0 = nullptr,
                           int ref = 0, uint32_t epoch = 0, const uint32_t *__restrict__ spos = nullptr,
-                          const uint32_t *__restrict__ skey = nullptr)
+                          const uint32_t *__restrict__ skey = nullptr, const uint32_t *__restrict__ irow = nullptr,
+                          const uint32_t *__restrict__ ikey = nullptr)
 {
     tc::pdl_trigger();
     tc::pdl_wait();
@@ -1290,10 +1312,28 @@ __global__ void k_gather2(int64_t mN, const uint16_t *__restrict__ D, int64_t ld
         __syncthreads();
         nlim = s_nt;
     }
+    // row echelon form with rows indexed by their initial lead (irow / ikey, D in place, row slots
+    // by atomics): only the rows with ikey < c1 can have a nonzero coefficient at this panel's pivots
+    if (irow) {
+        __shared__ uint32_t s_ni;
+        if (threadIdx.x == 0) {
+            const int64_t c = ps->c1;
+            int64_t lo = 0, hi = mN;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)ikey[mid] < c) lo = mid + 1;
+                else hi = mid;
+            }
+            s_ni = (uint32_t)lo;
+        }
+        __syncthreads();
+        nlim = s_ni;
+    }
     if (kp == 0) return;
     uint32_t touched = 0;
-    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlim;
-         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ii < nlim;
+         ii += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t i = irow ? (int64_t)irow[ii] : ii;
     if (owner && owner[i] != me) continue;                     // another rank's row
     const uint32_t rp = rowpiv[i];
     const bool skip = rp != GBLA_NONE && (rp >= (uint64_t)ps->c0 || ref);   // selected now: becomes Rn;
@@ -1787,6 +1827,29 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
             cudaGetLastError();
         }
     }
+    // Row echelon form (K14 route, one GPU): every panel's lead scan and F gather read only the rows
+    // whose INITIAL leading column is left of the window's end / the panel's end (a row's lead only
+    // moves right, and an earlier pivot row is never updated), found through the rows sorted by
+    // that column (D stays in place; row slots by atomics).  On a staircase D this is a few hundred
+    // active rows per panel instead of all mN (c2: 40,000 rows x 1 KB per lead scan).
+    uint32_t *rrow = nullptr, *rkey = nullptr;
+    if (G == 1 && h->ref_only && !getenv("GBLA_REF_FULLSCAN")) {
+        uint32_t *ilead, *iota;
+        GBLA_TRY(dalloc_t(h, mN, &ilead));
+        GBLA_TRY(dalloc_t(h, mN, &iota));
+        GBLA_TRY(dalloc_t(h, mN, &rkey));
+        GBLA_TRY(dalloc_t(h, mN, &rrow));
+        k_row_first_nz<<<grid_for(mN * 32, 256) < 16u * h->ctx->sm_count ? grid_for(mN * 32, 256)
+                                                                         : 16u * h->ctx->sm_count, 256, 0, st>>>(
+            mN, nN, h->D, ldD, ilead, iota);
+        note_launch();
+        size_t tb = 0;
+        GBLA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, ilead, rkey, iota, rrow, (int)mN, 0, 32, st));
+        void *tmp;
+        GBLA_TRY(dalloc(h, tb + 16, &tmp));
+        GBLA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, ilead, rkey, iota, rrow, (int)mN, 0, 32, st));
+        GBLA_CUDA_TRY(cudaMemsetAsync(lead, 0xff, (mN + 1) * 4, st));   // NONE16: rows never scanned
+    }
     if (G > 1) {
         // an even number of row tiles (the CTA-pair GEMM reads row tiles in pairs; the extra one is zero)
         GBLA_TRY(dalloc_t(h, (size_t)ntrD2 * G * PK * 128, &Fdlo));
@@ -1831,7 +1894,8 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
     auto p_lead = [&](cudaStream_t s, int64_t k) {
         P2State *prev = ps + ((k + 1) & 1);
         launch_pdl(k_lead2, dim3(rgrid), dim3(256), 0, s, mN, nN, (const uint16_t *)h->D, ldD,
-                   (const uint32_t *)rowpiv, (const P2State *)prev, lead, (const uint8_t *)nullptr, 0);
+                   (const uint32_t *)rowpiv, (const P2State *)prev, lead, (const uint8_t *)nullptr, 0,
+                   (const uint32_t *)rrow, (const uint32_t *)rkey);
         note_launch();
     };
     auto p_factor = [&](cudaStream_t s, int64_t k) {
@@ -1850,7 +1914,7 @@ gbla_status panels_tc2(gbla_mat h, uint32_t *rowpiv, unsigned long long *dops, c
         k_gather2<<<grid_for(mN * 32, 256), 256, 0, s>>>(mN, h->D, ldD, rowpiv, cur, Flo[k & 1], Fhi[k & 1],
                                                          rows[k & 1], nullptr, 0, Fdlo, Fdhi, G, (int)(k % G), spc0,
                                                          h->ref_only ? 1 : 0, (uint32_t)(k + 1), spos,
-                                                         sorted_rows ? (const uint32_t *)skey : nullptr);
+                                                         sorted_rows ? (const uint32_t *)skey : nullptr, rrow, rkey);
         note_launch();
     };
     // deferred columns [Cd, nN): super-panel start (Cd, cleared factor tiles) and the K = G * 128 flush
