@@ -670,6 +670,18 @@ def test_backsub_rref_exact(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
     check_full(gb, ctx, c0_matrix, c0_oracle)
 
 
+def test_backsub_prefix_scans(gb, ctx, c0_matrix, c0_oracle, monkeypatch):
+    """Row echelon panels walking only the rows whose initial lead is left of the window / panel end
+    (the default for mN >= 65,536, forced here with GBLA_REF_PREFIX at reduced scale): R, rank and
+    pivot columns bit-exact against the oracle on c0 and scaled c1/c2/c4 shapes."""
+    monkeypatch.setenv("GBLA_BACKSUB", "1")
+    monkeypatch.setenv("GBLA_REF_PREFIX", "1")
+    check_full(gb, ctx, c0_matrix, c0_oracle)
+    for name, sc in (("c1", 0.05), ("c2", 0.03), ("c4", 0.01)):
+        M = gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS[name], sc))
+        check_full(gb, ctx, M, oracle.reduce(M), check_dnew=False)
+
+
 def test_backsub_edge_cases(gb, ctx, monkeypatch):
     """K14 on the degenerate shapes: rank 0 and 1 (nothing above a pivot), a full-rank square D (no
     non-pivot column: only the pivot columns are cleared), a single non-pivot column, dense random
