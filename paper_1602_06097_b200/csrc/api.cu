@@ -5,6 +5,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 #include <atomic>
@@ -224,10 +226,13 @@ static bool is_prime_u32(uint32_t p)
     return true;
 }
 
+// CUDA-event timer of one phase of the C ABI, also an NVTX range of the same name (host timeline;
+// free when no tool is attached: nvtx3 is header-only and resolves its hooks lazily)
 struct PhaseTimer {
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
-    explicit PhaseTimer(cudaStream_t st) : s(st) {
+    explicit PhaseTimer(cudaStream_t st, const char *name = "gbla") : s(st) {
+        nvtxRangePushA(name);
         a = kt_event_get();
         b = kt_event_get();
         if (a) cudaEventRecord(a, s);
@@ -243,6 +248,7 @@ struct PhaseTimer {
     ~PhaseTimer() {
         if (a) kt_event_put(a);
         if (b) kt_event_put(b);
+        nvtxRangePop();
     }
 };
 
@@ -290,7 +296,7 @@ extern "C" gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     h->p = p;
     h->F = make_field(p);
     h->kt.on = getenv("GBLA_KERNEL_TIMERS") != nullptr;
-    PhaseTimer tm(h->stream);
+    PhaseTimer tm(h->stream, "gbla_splice");
     gbla_status s;
     if (dist) {
         gbla_csr dm;
@@ -330,7 +336,7 @@ extern "C" gbla_status gbla_reduce_C(gbla_mat h, uint32_t flags, void *stream)
         set_error("gbla_reduce_C(FUSE_D) after reduce_B/update_D would reduce D twice");
         return GBLA_E_ORDER;
     }
-    PhaseTimer tm(h->stream);
+    PhaseTimer tm(h->stream, "gbla_reduce_C");
     const bool keep_x = (flags & GBLA_KEEP_CPRIME) != 0;
     if (flags & GBLA_SPARSE_INT) {
         GBLA_TRY(reduce_c_int(h, fused, keep_x));
@@ -348,7 +354,7 @@ extern "C" gbla_status gbla_reduce_B(gbla_mat h, void *stream)
 {
     GBLA_TRY(check_mat(h, stream));
     if (h->did_reduce_B) { set_error("gbla_reduce_B: already done"); return GBLA_E_ORDER; }
-    PhaseTimer tm(h->stream);
+    PhaseTimer tm(h->stream, "gbla_reduce_B");
     GBLA_TRY(reduce_b_int(h));
     h->phase_ms[2] = tm.stop();
     h->did_reduce_B = true;
@@ -365,7 +371,7 @@ extern "C" gbla_status gbla_update_D(gbla_mat h, void *stream)
                          : "gbla_update_D: needs reduce_B or an unfused reduce_C first");
         return GBLA_E_ORDER;
     }
-    PhaseTimer tm(h->stream);
+    PhaseTimer tm(h->stream, "gbla_update_D");
     if (have_x && h->have_xt) GBLA_TRY(update_d_tc(h));
     else if (have_x) GBLA_TRY(update_d_from_x_int(h));
     else GBLA_TRY(update_d_from_bp_int(h));
@@ -382,7 +388,7 @@ extern "C" gbla_status gbla_echelon_D(gbla_mat h, uint32_t flags, void *stream, 
         return GBLA_E_INVAL;
     }
     if (h->rank >= 0) { set_error("gbla_echelon_D: already echelonized"); return GBLA_E_ORDER; }
-    PhaseTimer tm(h->stream);
+    PhaseTimer tm(h->stream, "gbla_echelon_D");
     GBLA_TRY(echelon_impl(h, flags));
     h->phase_ms[4] = tm.stop();
     if (rank) *rank = h->rank;
@@ -429,7 +435,7 @@ extern "C" gbla_status gbla_reduce(gbla_ctx ctx, const gbla_csr *M, uint32_t p, 
     // (the INT-pipe echelon is single-GPU only: with GBLA_DENSE_INT every rank reduces the whole D)
     if (dist && !(flags & (GBLA_ORDER_STANDARD | GBLA_SPARSE_INT | GBLA_KEEP_CPRIME | GBLA_DENSE_INT))) {
         // multi-GPU (dist.cu): row-sharded tensor-core sparse phase + D_new all-gather
-        PhaseTimer tm(h->stream);
+        PhaseTimer tm(h->stream, "gbla_reduce:sharded_sparse_phase");
         s = dist_sparse_phase(h);
         h->did_fused = h->did_update = true;
         h->dist_rows = h->dist_phase = true;
