@@ -138,18 +138,28 @@ __global__ void k_fill_rows(int64_t nrows, int64_t npiv, const uint32_t *__restr
     unsigned lt = (1u << lane) - 1u;
     uint32_t base = 0;
     for (int pass = 0; pass < 2; pass++) {
-        for (uint64_t q0 = s; q0 < e; q0 += 32) {
-            uint64_t q = q0 + lane;
-            bool in = q < e;
-            uint32_t sc = in ? sigma[col[q]] : 0;
-            bool take = in && ((sc < (uint64_t)npiv) == (pass == 0));
-            unsigned msk = __ballot_sync(FULL, take);
-            if (take) {
-                uint32_t pos = base + __popc(msk & lt);
-                ocol[o + pos] = sc;
-                oval[o + pos] = (uint16_t)fmod32((uint32_t)val[q] * il, F);   // < 2^32: 32-bit Barrett
+        // four 32-slot chunks per step: their column and sigma loads are in flight together
+        for (uint64_t q0 = s; q0 < e; q0 += 128) {
+            uint32_t c[4], sc[4], v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint64_t q = q0 + 32 * u + lane;
+                c[u] = q < e ? col[q] : 0xffffffffu;
+                v[u] = q < e ? val[q] : 0u;
             }
-            base += __popc(msk);
+#pragma unroll
+            for (int u = 0; u < 4; u++) sc[u] = c[u] != 0xffffffffu ? sigma[c[u]] : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool take = sc[u] != 0xffffffffu && ((sc[u] < (uint64_t)npiv) == (pass == 0));
+                const unsigned msk = __ballot_sync(FULL, take);
+                if (take) {
+                    const uint32_t pos = base + __popc(msk & lt);
+                    ocol[o + pos] = sc[u];
+                    oval[o + pos] = (uint16_t)fmod32(v[u] * il, F);   // < 2^32: 32-bit Barrett
+                }
+                base += __popc(msk);
+            }
         }
         if (pass == 0 && lane == 0) onp[i] = base;
     }
