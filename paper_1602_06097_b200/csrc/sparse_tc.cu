@@ -718,17 +718,24 @@ __global__ void __launch_bounds__(128, 1) k_update_tc(UpdArgs a)
             }
             tc::commit(&accbar);
         }
+        // this thread's D row segment (256 B) read while the MMAs run: the epilogue's global loads
+        // are off the path after the accumulator is done
+        uint4 dv[16];
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < 16; j++) dv[j] = *reinterpret_cast<const uint4 *>(drow + 8 * j);
+        }
         tc::mbar_wait(&accbar, ph_acc);
         ph_acc ^= 1;
         tc::fence_after();
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < 128; c += 16) {
             uint32_t Rv[16];
             read_R(lane_addr, c, Rv, a.F);
             if (!live) continue;
             uint4 v[2];
-            v[0] = *reinterpret_cast<const uint4 *>(drow + c);
-            v[1] = *reinterpret_cast<const uint4 *>(drow + c + 8);
+            v[0] = dv[c / 8];
+            v[1] = dv[c / 8 + 1];
             uint16_t *d = reinterpret_cast<uint16_t *>(v);
 #pragma unroll
             for (int j = 0; j < 16; j++) {
