@@ -126,7 +126,13 @@ gbla_status gbla_splice(gbla_ctx ctx, const gbla_csr *M, uint32_t p, uint32_t fl
                         void *stream, gbla_mat *out);
 
 /* Step 2, TRSM: B <- A^-1 B (A unit upper triangular; "one only
- * reads A and writes to B").  Result kept as dense B' (n_piv x nN). */
+ * reads A and writes to B").  Result kept as dense B' (n_piv x nN, u16
+ * residues, row stride from gbla_get_Bprime), owned by h.  Default engine:
+ * the tensor-core sparse phase applied to the unit targets e_k (row k of
+ * -A^-1 B is the D_new row of the target e_k; exact), then negated;
+ * environment GBLA_TRSM_INT=1 selects the INT-pipe back substitution (one
+ * thread per column).  Synchronizes `stream`.  Errors: GBLA_E_ORDER if
+ * already done, GBLA_E_NOMEM, GBLA_E_CUDA, GBLA_E_INTERNAL. */
 gbla_status gbla_reduce_B(gbla_mat h, void *stream);
 
 /* C <- C A^-1 (new order): per non-pivot row, forward

@@ -355,7 +355,11 @@ extern "C" gbla_status gbla_reduce_B(gbla_mat h, void *stream)
     GBLA_TRY(check_mat(h, stream));
     if (h->did_reduce_B) { set_error("gbla_reduce_B: already done"); return GBLA_E_ORDER; }
     PhaseTimer tm(h->stream, "gbla_reduce_B");
-    GBLA_TRY(reduce_b_int(h));
+    // default: the tensor-core sparse phase on the targets e_k (fullrref.cu); GBLA_TRSM_INT=1: K8
+    const char *te = getenv("GBLA_TRSM_INT");
+    const bool trsm_int = te && atoi(te) != 0;
+    if (trsm_int) GBLA_TRY(reduce_b_int(h));
+    else GBLA_TRY(reduce_b_tc(h));
     h->phase_ms[2] = tm.stop();
     h->did_reduce_B = true;
     return GBLA_OK;

@@ -132,6 +132,98 @@ __global__ void k_rm_fill(int64_t npiv, int64_t rank, int64_t nN, Field F, const
 
 }  // namespace
 
+// -B' = -(A^-1 B) on the tensor cores (see the header): a new internal handle whose D (npiv x nN,
+// stride ldD) holds -B'.  The caller frees it with gbla_mat_free after the last kernel that reads it.
+// The Alg 2 op count of the e_k targets is added to h->sparse_ops.
+gbla_status neg_bprime_tc(gbla_mat h, const char *who, gbla_mat *out)
+{
+    cudaStream_t st = h->stream;
+    const int64_t npiv = h->npiv, n = h->n;
+    *out = nullptr;
+    gbla_mat h2 = new gbla_mat_s();
+    h2->ctx = h->ctx;
+    h2->stream = st;
+    h2->p = h->p;
+    h2->F = h->F;
+    h2->m = 2 * npiv;
+    h2->n = n;
+    h2->nnz = h->nnz_ab + npiv;
+    h2->force_piv = npiv;
+    uint64_t *rp = nullptr;
+    uint32_t *col = nullptr;
+    uint16_t *val = nullptr;
+    gbla_status s = dalloc_t(h2, 2 * npiv + 1, &rp);
+    if (s == GBLA_OK) s = dalloc_t(h2, (size_t)h2->nnz, &col);
+    if (s == GBLA_OK) s = dalloc_t(h2, (size_t)h2->nnz, &val);
+    if (s == GBLA_OK && h->nnz_ab) {
+        if (cudaMemcpyAsync(col, h->ab_col, h->nnz_ab * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(val, h->ab_val, h->nnz_ab * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+            set_error("%s: copy of the pivot rows failed", who);
+            s = GBLA_E_CUDA;
+        }
+    }
+    if (s == GBLA_OK) {
+        k_f2_rows<<<grid_for(2 * npiv + 1, 256), 256, 0, st>>>(npiv, h->ab_ptr, (uint64_t)h->nnz_ab, rp, col, val);
+        note_launch();
+        const gbla_csr Mf{2 * npiv, n, h2->nnz, rp, col, val};
+        s = splice_impl(h2, &Mf, 0);
+    }
+    if (s == GBLA_OK && (h2->npiv != npiv || h2->mN != npiv)) {
+        set_error("%s: internal splice gave %lld pivots / %lld targets (expected %lld)", who,
+                  (long long)h2->npiv, (long long)h2->mN, (long long)npiv);
+        s = GBLA_E_INTERNAL;
+    }
+    if (s == GBLA_OK) s = reduce_c_tc(h2, false, true);      // h2->D = -B'
+    if (s == GBLA_OK) h->sparse_ops += h2->sparse_ops;       // (the op count of this TRSM)
+    if (s != GBLA_OK) {
+        cudaStreamSynchronize(st);
+        gbla_mat_free(h2);
+        return s;
+    }
+    *out = h2;
+    return GBLA_OK;
+}
+
+namespace {
+
+// Bp[i][c] = -Bn[i][c] mod p
+__global__ void k_negate_rows(int64_t rows, int64_t cols, Field F, const uint16_t *__restrict__ Bn, int64_t ldn,
+                              uint16_t *__restrict__ Bp, int64_t ldp)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+        const uint32_t v = Bn[(size_t)i * ldn + c];
+        Bp[(size_t)i * ldp + c] = (uint16_t)(v ? F.p - v : 0);
+    }
+}
+
+}  // namespace
+
+// Step 2 on the tensor cores: B' = A^-1 B = -(-B'), dense in h->Bp (the layout of
+// reduce_b_int).  gbla_reduce_B's default; GBLA_TRSM_INT=1 keeps the INT-pipe K8.
+gbla_status reduce_b_tc(gbla_mat h)
+{
+    cudaStream_t st = h->stream;
+    h->ldB = (h->nN + 127) / 128 * 128;
+    if (h->ldB == 0) h->ldB = 128;
+    if (!h->Bp) GBLA_TRY(dalloc_t(h, (size_t)(h->npiv > 0 ? h->npiv : 1) * h->ldB, &h->Bp));
+    GBLA_CUDA_TRY(cudaMemsetAsync(h->Bp, 0, (size_t)(h->npiv > 0 ? h->npiv : 1) * h->ldB * sizeof(uint16_t), st));
+    if (h->npiv == 0 || h->nN == 0) return GBLA_OK;
+    gbla_mat h2 = nullptr;
+    GBLA_TRY(neg_bprime_tc(h, "gbla_reduce_B", &h2));
+    dim3 g(grid_for(h->nN, 256), (unsigned)(h->npiv < 1184 ? h->npiv : 1184));
+    k_negate_rows<<<g, 256, 0, st>>>(h->npiv, h->nN, h->F, h2->D, h2->ldD, h->Bp, h->ldB);
+    note_launch();
+    gbla_status s = GBLA_OK;
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("gbla_reduce_B: %s", cudaGetErrorString(cudaGetLastError()));
+        s = GBLA_E_CUDA;
+    }
+    gbla_mat_free(h2);
+    return s;
+}
+
 gbla_status full_rref_impl(gbla_mat h)
 {
     cudaStream_t st = h->stream;
@@ -143,44 +235,10 @@ gbla_status full_rref_impl(gbla_mat h)
     if (ldb == 0) ldb = 128;
     gbla_status s = GBLA_OK;
     if (npiv > 0) {
-        h2 = new gbla_mat_s();
-        h2->ctx = h->ctx;
-        h2->stream = st;
-        h2->p = h->p;
-        h2->F = h->F;
-        h2->m = 2 * npiv;
-        h2->n = n;
-        h2->nnz = h->nnz_ab + npiv;
-        h2->force_piv = npiv;
-        uint64_t *rp = nullptr;
-        uint32_t *col = nullptr;
-        uint16_t *val = nullptr;
-        s = dalloc_t(h2, 2 * npiv + 1, &rp);
-        if (s == GBLA_OK) s = dalloc_t(h2, (size_t)h2->nnz, &col);
-        if (s == GBLA_OK) s = dalloc_t(h2, (size_t)h2->nnz, &val);
-        if (s == GBLA_OK && h->nnz_ab) {
-            if (cudaMemcpyAsync(col, h->ab_col, h->nnz_ab * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-                cudaMemcpyAsync(val, h->ab_val, h->nnz_ab * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
-                set_error("gbla_rref_M: copy of the pivot rows failed");
-                s = GBLA_E_CUDA;
-            }
-        }
-        if (s == GBLA_OK) {
-            k_f2_rows<<<grid_for(2 * npiv + 1, 256), 256, 0, st>>>(npiv, h->ab_ptr, (uint64_t)h->nnz_ab, rp, col, val);
-            note_launch();
-            const gbla_csr Mf{2 * npiv, n, h2->nnz, rp, col, val};
-            s = splice_impl(h2, &Mf, 0);
-        }
-        if (s == GBLA_OK && (h2->npiv != npiv || h2->mN != npiv)) {
-            set_error("gbla_rref_M: internal splice gave %lld pivots / %lld targets (expected %lld)",
-                      (long long)h2->npiv, (long long)h2->mN, (long long)npiv);
-            s = GBLA_E_INTERNAL;
-        }
-        if (s == GBLA_OK) s = reduce_c_tc(h2, false, true);      // h2->D = -B'
+        s = neg_bprime_tc(h, "gbla_rref_M", &h2);
         if (s == GBLA_OK) {
             Bn = h2->D;
             ldb = h2->ldD;
-            h->sparse_ops += h2->sparse_ops;                    // (the op count of f2's TRSM)
         }
         // ---- -B'' = -B' - (-B'[:, pivcol]) R  (K11, K = rank)
         if (s == GBLA_OK && rank > 0 && nN > 0) {

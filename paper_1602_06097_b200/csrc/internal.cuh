@@ -261,6 +261,7 @@ gbla_status splice_impl(gbla_mat h, const gbla_csr *M, uint32_t flags);
 gbla_status reduce_c_int(gbla_mat h, bool fused, bool keep_x);
 gbla_status update_d_from_x_int(gbla_mat h);
 gbla_status reduce_b_int(gbla_mat h);
+gbla_status reduce_b_tc(gbla_mat h);      // fullrref.cu: B' by the tensor-core sparse phase
 gbla_status update_d_from_bp_int(gbla_mat h);
 gbla_status echelon_impl(gbla_mat h, uint32_t flags);
 gbla_status reduce_c_tc(gbla_mat h, bool want_x16, bool fused);

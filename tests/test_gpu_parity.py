@@ -179,8 +179,9 @@ def test_pipeline_random_suite_standard_order(gb, ctx):
         check_full(gb, ctx, M, flags=gb.GBLA_ORDER_STANDARD)
 
 
-def test_unfused_cprime_bprime(gb, ctx):
-    for M in list(gbla_gen.random_suite(40, seed0=27)) + [gbla_gen.f4_matrix("c0")]:
+def test_unfused_cprime_bprime(gb, ctx, monkeypatch):
+    for M in list(gbla_gen.random_suite(40, seed0=27)) + [gbla_gen.f4_matrix("c0"),
+                                                          gbla_gen.f4_matrix(gbla_gen.scaled(gbla_gen.CONFIGS["c1"], 0.03))]:
         S = oracle.splice(M)
         A, B, C, D = oracle.quadrants(M, S)
         dn, x, ops = oracle.dnew_rows(M, S, want_x=True)
@@ -192,13 +193,16 @@ def test_unfused_cprime_bprime(gb, ctx):
         assert np.array_equal(np_(h.D()), dn)
         assert h.opcount()[0] == int(ops.sum())
         h.free()
-        h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
-        gb.gbla_reduce_B(h)
-        if M.m <= 200:
-            assert np.array_equal(np_(h.bprime()).astype(np.uint32), oracle.trsm(A, B, M.p))
-        gb.gbla_update_D(h)
-        assert np.array_equal(np_(h.D()), dn)
-        h.free()
+        bp = oracle.trsm(A, B, M.p)
+        for trsm_int in ("0", "1"):               # tensor-core TRSM (default) and the INT-pipe K8
+            monkeypatch.setenv("GBLA_TRSM_INT", trsm_int)
+            h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+            gb.gbla_reduce_B(h)
+            assert np.array_equal(np_(h.bprime()).astype(np.uint32), bp)
+            gb.gbla_update_D(h)
+            assert np.array_equal(np_(h.D()), dn)
+            h.free()
+        monkeypatch.delenv("GBLA_TRSM_INT")
         for ip in (False, True):
             h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
             gb.gbla_reduce_C(h, fused=True, keep_cprime=True, int_pipe=ip)
