@@ -20,6 +20,8 @@
 //   thread per column of B ("one only reads A and writes to B"; columns of B
 //   are independent).
 // K7 k_update_from_bp: Step 3, D <- D - C B'.
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace {
@@ -302,7 +304,7 @@ gbla_status reduce_b_int(gbla_mat h)
     return GBLA_OK;
 }
 
-gbla_status update_d_from_bp_int(gbla_mat h)
+static gbla_status update_d_from_bp_rows(gbla_mat h)
 {
     cudaStream_t st = h->stream;
     if (h->mN == 0 || h->nN == 0) return GBLA_OK;
@@ -311,4 +313,55 @@ gbla_status update_d_from_bp_int(gbla_mat h)
                                             h->ldB, h->D, h->ldD); note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
+}
+
+namespace {
+
+// sum of a u32 array into one u64 (nnz(C) = sum of the rows' pivot-column entry counts)
+__global__ void k_sum_u32(int64_t n, const uint32_t *__restrict__ a, unsigned long long *__restrict__ out)
+{
+    unsigned long long s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) s += a[i];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+}  // namespace
+
+// Step 3 of the standard order: D -= C B'.  C is sparse, B' dense.  Two engines:
+// the sparse rows of C on the INT pipe (k_update_from_bp, nnz(C) nN modMACs), or C densified and one
+// K11 product on the tensor cores (mN npiv nN dense modMACs).  Measured rates: ~2.3 T modMAC/s
+// against ~200 T dense modMAC/s (K11 flush), so K11 wins from a C density of ~1/85; the rule is
+// nnz(C) >= mN npiv / 64 (c1 2.2 % and c3 5.3 % -> K11, c2 1.1 % -> INT).  GBLA_UPDATE_BP=int|tc
+// forces one.
+gbla_status update_d_from_bp_int(gbla_mat h)
+{
+    cudaStream_t st = h->stream;
+    if (h->mN == 0 || h->nN == 0 || h->npiv == 0) return GBLA_OK;
+    const char *e = getenv("GBLA_UPDATE_BP");
+    bool dense;
+    if (e && !strcmp(e, "int")) dense = false;
+    else if (e && !strcmp(e, "tc")) dense = true;
+    else {
+        unsigned long long *d = nullptr, nnzC = 0;
+        GBLA_TRY(dalloc_t(h, 1, &d));
+        GBLA_CUDA_TRY(cudaMemsetAsync(d, 0, 8, st));
+        k_sum_u32<<<128, 256, 0, st>>>(h->mN, h->cd_np, d); note_launch();
+        GBLA_CUDA_TRY(cudaMemcpyAsync(&nnzC, d, 8, cudaMemcpyDeviceToHost, st));
+        GBLA_CUDA_TRY(cudaStreamSynchronize(st));
+        dfree(h, d);
+        dense = (double)nnzC * 64.0 >= (double)h->mN * (double)h->npiv;
+    }
+    if (!dense) return update_d_from_bp_rows(h);
+    uint16_t *Cd = nullptr;
+    const int64_t lda = (h->npiv + 7) / 8 * 8;
+    GBLA_TRY(dalloc_t(h, (size_t)h->mN * lda, &Cd));
+    gbla_status s = densify_impl(h, 'C', Cd, lda);
+    if (s == GBLA_OK) s = modgemm_sub_chunked(h->ctx, st, h->F, h->mN, h->nN, h->npiv, Cd, lda, h->Bp, h->ldB, h->D, h->ldD);
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == GBLA_OK) {
+        set_error("gbla_update_D: %s", cudaGetErrorString(cudaGetLastError()));
+        s = GBLA_E_CUDA;
+    }
+    dfree(h, Cd);
+    return s;
 }

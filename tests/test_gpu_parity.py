@@ -194,14 +194,19 @@ def test_unfused_cprime_bprime(gb, ctx, monkeypatch):
         assert h.opcount()[0] == int(ops.sum())
         h.free()
         bp = oracle.trsm(A, B, M.p)
-        for trsm_int in ("0", "1"):               # tensor-core TRSM (default) and the INT-pipe K8
+        # TRSM on the tensor cores (default) and on the INT pipe (K8); D -= C B' by the sparse rows of
+        # C (INT pipe) and by K11 on the densified C
+        for trsm_int, upd in (("0", "tc"), ("1", "int"), ("0", "int"), ("0", None)):
             monkeypatch.setenv("GBLA_TRSM_INT", trsm_int)
+            if upd:
+                monkeypatch.setenv("GBLA_UPDATE_BP", upd)
             h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
             gb.gbla_reduce_B(h)
             assert np.array_equal(np_(h.bprime()).astype(np.uint32), bp)
             gb.gbla_update_D(h)
             assert np.array_equal(np_(h.D()), dn)
             h.free()
+            monkeypatch.delenv("GBLA_UPDATE_BP", raising=False)
         monkeypatch.delenv("GBLA_TRSM_INT")
         for ip in (False, True):
             h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
