@@ -353,6 +353,20 @@ def test_c1_full_size_against_golden(gb, ctx):
     h.free()
 
 
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_standard_order_full_size_against_golden(gb, ctx, name):
+    """The standard order (Step 2 TRSM on the tensor cores, Step 3 D - C B' by K11) at
+    full size: its D_new is the new order's (the oracle's golden digest), hundreds of tiles wide."""
+    g = json.load(open(os.path.join(GOLD, name + "_oracle.json")))
+    M = gbla_gen.f4_matrix(name)
+    rp, c, v = to_dev(M)
+    h = gb.gbla_splice(ctx, M.m, M.n, rp, c, v, M.p)
+    gb.gbla_reduce_B(h)
+    gb.gbla_update_D(h)
+    assert oracle.array_digest(np_(h.D())) == g["dnew_sha256"]
+    h.free()
+
+
 def test_c3_full_size_against_golden(gb, ctx):
     """c3 (dense-D-heavy, 60,000 x 80,000, p = 32003) at full size through the default path (super-
     panels of 4: deferred K = 512 flushes on CTA pairs, lead-sorted rows, prefix slots, back
