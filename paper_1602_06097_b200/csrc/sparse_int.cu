@@ -168,8 +168,12 @@ __global__ void __launch_bounds__(128) k_trsm_cols(int64_t npiv, int64_t nN, Fie
 }
 
 // Step 3 (standard order): D_t <- D_t - sum_{j in supp C_t} C_tj B'_j.
-// Grid (column chunks, targets); each thread owns 4 columns.
-__global__ void __launch_bounds__(256) k_update_from_bp(int64_t mN, int64_t nN, Field F,
+// Grid (targets, column chunks): the CTAs resident at one time work on consecutive targets and the
+// SAME column chunk, so the B' rows they read (the targets' supports, a band that moves slowly from
+// one target to the next) stay in L2 as a strip of 4 * blockDim.x columns.  Each thread owns 4
+// columns (one 8-byte load per reducer row); the row's (column, coefficient) pairs are staged in
+// shared memory 256 at a time; products are u32 x u32 + u64 (one IMAD.WIDE each).
+__global__ void __launch_bounds__(128) k_update_from_bp(int64_t mN, int64_t nN, Field F,
                                                         const uint64_t *__restrict__ cd_ptr,
                                                         const uint32_t *__restrict__ cd_col,
                                                         const uint16_t *__restrict__ cd_val,
@@ -177,23 +181,41 @@ __global__ void __launch_bounds__(256) k_update_from_bp(int64_t mN, int64_t nN, 
                                                         const uint16_t *__restrict__ Bp, int64_t ldB,
                                                         uint16_t *__restrict__ D, int64_t ldD)
 {
-    const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (c0 >= nN) return;
-    for (int64_t t = blockIdx.y; t < mN; t += gridDim.y) {
-    uint64_t acc[4];
+    __shared__ uint32_t s_col[256], s_a[256];
+    const int tid = threadIdx.x;
+    const int64_t c0 = ((int64_t)blockIdx.y * blockDim.x + tid) * 4;
+    const bool live = c0 < nN;
+    for (int64_t t = blockIdx.x; t < mN; t += gridDim.x) {
+        uint64_t acc[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) acc[u] = (c0 + u < nN) ? D[(size_t)t * ldD + c0 + u] : 0;
-    const uint64_t s = cd_ptr[t], e = s + cd_np[t];
-    for (uint64_t q = s; q < e; q++) {
-        const uint32_t j = cd_col[q];
-        const uint64_t a = fneg(cd_val[q], F);
-        const uint16_t *row = Bp + (size_t)j * ldB + c0;
+        for (int u = 0; u < 4; u++) acc[u] = (live && c0 + u < nN) ? D[(size_t)t * ldD + c0 + u] : 0;
+        const uint64_t s = cd_ptr[t], e = s + cd_np[t];
+        for (uint64_t q0 = s; q0 < e; q0 += 256) {
+            const int cnt = (int)(e - q0 < 256 ? e - q0 : 256);
+            __syncthreads();
+            for (int i = tid; i < cnt; i += blockDim.x) {
+                s_col[i] = cd_col[q0 + i];
+                s_a[i] = fneg(cd_val[q0 + i], F);
+            }
+            __syncthreads();
+            if (live) {
+#pragma unroll 4
+                for (int i = 0; i < cnt; i++) {
+                    const uint32_t a = s_a[i];
+                    // (ldB is a multiple of 128 and c0 of 4: 8-byte aligned, c0 + 3 < ldB)
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(Bp + (size_t)s_col[i] * ldB + c0));
+                    acc[0] += (uint64_t)a * (w.x & 0xffffu);
+                    acc[1] += (uint64_t)a * (w.x >> 16);
+                    acc[2] += (uint64_t)a * (w.y & 0xffffu);
+                    acc[3] += (uint64_t)a * (w.y >> 16);
+                }
+            }
+        }
+        if (live) {
 #pragma unroll
-        for (int u = 0; u < 4; u++) acc[u] += a * row[u];   // ldB padded: c0+u < ldB always
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-        if (c0 + u < nN) D[(size_t)t * ldD + c0 + u] = (uint16_t)fmod64(acc[u], F);
+            for (int u = 0; u < 4; u++)
+                if (c0 + u < nN) D[(size_t)t * ldD + c0 + u] = (uint16_t)fmod64(acc[u], F);
+        }
     }
 }
 
@@ -308,8 +330,8 @@ static gbla_status update_d_from_bp_rows(gbla_mat h)
 {
     cudaStream_t st = h->stream;
     if (h->mN == 0 || h->nN == 0) return GBLA_OK;
-    dim3 grid(grid_for((h->nN + 3) / 4, 256), (unsigned)(h->mN < 65535 ? h->mN : 65535));
-    k_update_from_bp<<<grid, 256, 0, st>>>(h->mN, h->nN, h->F, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np, h->Bp,
+    dim3 grid((unsigned)(h->mN < (1 << 30) ? h->mN : (1 << 30)), grid_for((h->nN + 3) / 4, 128));
+    k_update_from_bp<<<grid, 128, 0, st>>>(h->mN, h->nN, h->F, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np, h->Bp,
                                             h->ldB, h->D, h->ldD); note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
@@ -330,10 +352,10 @@ __global__ void k_sum_u32(int64_t n, const uint32_t *__restrict__ a, unsigned lo
 
 // Step 3 of the standard order: D -= C B'.  C is sparse, B' dense.  Two engines:
 // the sparse rows of C on the INT pipe (k_update_from_bp, nnz(C) nN modMACs), or C densified and one
-// K11 product on the tensor cores (mN npiv nN dense modMACs).  Measured rates: ~2.3 T modMAC/s
-// against ~200 T dense modMAC/s (K11 flush), so K11 wins from a C density of ~1/85; the rule is
-// nnz(C) >= mN npiv / 64 (c1 2.2 % and c3 5.3 % -> K11, c2 1.1 % -> INT).  GBLA_UPDATE_BP=int|tc
-// forces one.
+// K11 product on the tensor cores (mN npiv nN dense modMACs).  Measured rates on c1/c2/c3: ~5 T
+// modMAC/s (INT pipe, 2/3 of its measured peak) against 150-190 T dense modMAC/s (K11 flush), so K11
+// wins from a C density of ~1/34; the rule is nnz(C) >= mN npiv / 32 (c3 5.3 % -> K11; c1 2.2 % and
+// c2 1.1 % -> INT).  GBLA_UPDATE_BP=int|tc forces one.
 gbla_status update_d_from_bp_int(gbla_mat h)
 {
     cudaStream_t st = h->stream;
@@ -350,7 +372,7 @@ gbla_status update_d_from_bp_int(gbla_mat h)
         GBLA_CUDA_TRY(cudaMemcpyAsync(&nnzC, d, 8, cudaMemcpyDeviceToHost, st));
         GBLA_CUDA_TRY(cudaStreamSynchronize(st));
         dfree(h, d);
-        dense = (double)nnzC * 64.0 >= (double)h->mN * (double)h->npiv;
+        dense = (double)nnzC * 32.0 >= (double)h->mN * (double)h->npiv;
     }
     if (!dense) return update_d_from_bp_rows(h);
     uint16_t *Cd = nullptr;
