@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(128) k_trsm_cols(int64_t npiv, int64_t nN, Fie
 // one target to the next) stay in L2 as a strip of 4 * blockDim.x columns.  Each thread owns 4
 // columns (one 8-byte load per reducer row); the row's (column, coefficient) pairs are staged in
 // shared memory 256 at a time; products are u32 x u32 + u64 (one IMAD.WIDE each).
-__global__ void __launch_bounds__(128) k_update_from_bp(int64_t mN, int64_t nN, Field F,
+__global__ void __launch_bounds__(256) k_update_from_bp(int64_t mN, int64_t nN, Field F,
                                                         const uint64_t *__restrict__ cd_ptr,
                                                         const uint32_t *__restrict__ cd_col,
                                                         const uint16_t *__restrict__ cd_val,
@@ -330,8 +330,13 @@ static gbla_status update_d_from_bp_rows(gbla_mat h)
 {
     cudaStream_t st = h->stream;
     if (h->mN == 0 || h->nN == 0) return GBLA_OK;
-    dim3 grid((unsigned)(h->mN < (1 << 30) ? h->mN : (1 << 30)), grid_for((h->nN + 3) / 4, 128));
-    k_update_from_bp<<<grid, 128, 0, st>>>(h->mN, h->nN, h->F, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np, h->Bp,
+    // threads per CTA = a quarter of the B' strip width in columns: 128 while the whole strip
+    // (npiv rows x 1 KB) stays well inside the 126 MB L2, else 64 (c2: 1,355 -> 1,225 ms; c1/c3 the
+    // same either way).  GBLA_UBP_THREADS = 64, 128 or 256 forces one.
+    int nth = (size_t)h->npiv * 1024 <= ((size_t)96 << 20) ? 128 : 64;
+    if (const char *e = getenv("GBLA_UBP_THREADS")) { const int v = atoi(e); if (v == 64 || v == 128 || v == 256) nth = v; }
+    dim3 grid((unsigned)(h->mN < (1 << 30) ? h->mN : (1 << 30)), grid_for((h->nN + 3) / 4, nth));
+    k_update_from_bp<<<grid, nth, 0, st>>>(h->mN, h->nN, h->F, h->cd_ptr, h->cd_col, h->cd_val, h->cd_np, h->Bp,
                                             h->ldB, h->D, h->ldD); note_launch();
     GBLA_CUDA_TRY(cudaGetLastError());
     return GBLA_OK;
